@@ -1,0 +1,440 @@
+"""Float64 CPU oracle for the orthogonal-convolution hot path.
+
+TEST INFRASTRUCTURE ONLY.  Plain, slow, obviously-correct NumPy float64.  It is
+imported by ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU
+baseline leg, never by the product package ``paper_2601_13776_b200``, and it
+imports nothing from that package (no shared kernels, headers, helpers,
+constants or layouts).
+
+Citation convention: ``P:n`` = /root/reference/PAPER.md line n, ``S:n`` =
+SPEC.md line n (the SPEC binds a CPU program, we use it only for interfaces and
+examples).  Where the paper is silent we follow the readings numbered R1..R21 in
+DESIGN.md ("Readings of the paper"), which restate SURVEY.md §8(c).
+
+Every function below says what it computes and the passage it follows.  Pins
+that fix each function independently of itself live in ``tests/test_oracle_*.py``.
+Nothing here is "parity unpinned".
+
+Conventions (R11, R15):
+  * convolution = cross-correlation, NCHW arrays, kernels (c_out, c_in/g, k, k);
+  * default padding p_t = floor(d(k-1)/2), p_b = d(k-1) - p_t ("same");
+  * groups are group-major along the output-channel axis (PyTorch convention);
+  * parameters are ordered layer -> group -> [Q, U_1 .. U_2(k'-1), R].
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+__all__ = [
+    "Layer", "MatrixSpec", "layer_matrices", "layer_geometry",
+    "prescale_power", "prescale_frobenius", "bjorck", "ns_residual",
+    "orthogonalize",
+    "block_conv", "block_orth", "bcop", "rko", "layer_kernel",
+    "out_size", "conv2d", "conv_transpose2d",
+    "toeplitz", "fft_singular_values", "polyphase_singular_values",
+    "conv_singular_values",
+]
+
+
+# ---------------------------------------------------------------------------
+# O1/a1: layer description and unit derivation (R5-R8)
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class Layer:
+    """One orthogonal layer.  kind: 'conv' (AdaptiveOrthoConv2d),
+    'convT' (AdaptiveOrthoConvTranspose2d) or 'dense'
+    (OrthoLinear weight).  padding_mode: 'circular' | 'zeros'.
+    pad = (p_t, p_b, p_l, p_r) or None for the "same" rule (R11)."""
+    c_in: int
+    c_out: int
+    k: int = 3
+    s: int = 1
+    d: int = 1
+    g: int = 1
+    kind: str = "conv"
+    padding_mode: str = "circular"
+    pad: Optional[Tuple[int, int, int, int]] = None
+
+    def fwd_channels(self) -> Tuple[int, int]:
+        """(c_in, c_out) of the forward conv whose kernel is built.  A
+        transposed layer builds the kernel of its forward adjoint, with the
+        channel counts swapped (R13)."""
+        if self.kind == "convT":
+            return self.c_out, self.c_in
+        return self.c_in, self.c_out
+
+    def pads(self) -> Tuple[int, int, int, int]:
+        if self.pad is not None:
+            return tuple(self.pad)
+        ext = self.d * (self.k - 1)
+        pt = ext // 2
+        return (pt, ext - pt, pt, ext - pt)
+
+
+@dataclass(frozen=True)
+class MatrixSpec:
+    """One parameter matrix: role in {'Q','U','R','W'}; shape m x n."""
+    role: str
+    m: int
+    n: int
+
+
+def layer_geometry(L: Layer) -> dict:
+    """Per-group channel widths of the AOC construction.
+
+    P:323-330 define AOC = RKO (*) K_BCOP for k >= s; the internal widths are
+    not printed ("careful choice of internal channel dimensions").
+    Reading R7/R8: BCOP size k' = k - s + 1; c_mid = max(ci, floor(co/s^2)).
+    s == 1 -> BCOP only at width max(ci, co) (R5); k == s > 1 -> RKO only.
+    """
+    ci_f, co_f = L.fwd_channels()
+    ci, co = ci_f // L.g, co_f // L.g
+    if L.kind == "dense":
+        return dict(ci=ci, co=co, kind="dense", kp=0, c_b=0, c_mid=0)
+    if L.s == 1:
+        return dict(ci=ci, co=co, kind="bcop", kp=L.k, c_b=max(ci, co), c_mid=0)
+    if L.k == L.s:
+        return dict(ci=ci, co=co, kind="rko", kp=0, c_b=0, c_mid=ci)
+    c_mid = max(ci, co // (L.s * L.s))
+    return dict(ci=ci, co=co, kind="aoc", kp=L.k - L.s + 1, c_b=c_mid, c_mid=c_mid)
+
+
+def layer_matrices(L: Layer) -> List[MatrixSpec]:
+    """Matrices of ONE group, in packing order [Q, U_1..U_2(k'-1), R] (R15;
+    S:212-216: "BCOP: one square matrix plus 2(k-1) matrices; RKO: one matrix
+    of shape c_out x (c_in s^2 / g) per group")."""
+    geo = layer_geometry(L)
+    if geo["kind"] == "dense":
+        return [MatrixSpec("W", geo["co"], geo["ci"])]
+    out: List[MatrixSpec] = []
+    if geo["kind"] in ("bcop", "aoc"):
+        c = geo["c_b"]
+        out.append(MatrixSpec("Q", c, c))
+        for _ in range(2 * (geo["kp"] - 1)):
+            out.append(MatrixSpec("U", c, c // 2))          # rank floor(c/2), R5
+    if geo["kind"] in ("rko", "aoc"):
+        out.append(MatrixSpec("R", geo["co"], geo["c_mid"] * L.s * L.s))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# O2: pre-scaling ("spectral normalization via batched power
+# iteration"; P:313 cached vector; R2/R3)
+# ---------------------------------------------------------------------------
+def prescale_power(W: np.ndarray, P: int, v: np.ndarray):
+    """P power iterations from v: u = Wv/|Wv|; w = W^T u; sig = |w|; v = w/sig.
+    Returns (W/sig, sig, v_new).  Zero W is an error."""
+    W = np.asarray(W, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64).copy()
+    if W.size == 0:
+        return W.copy(), 0.0, v
+    if not np.any(W):
+        raise ZeroDivisionError("zero matrix (S:115)")
+    sig = 0.0
+    for _ in range(P):
+        wv = W @ v
+        nwv = math.sqrt(float(wv @ wv))
+        if nwv == 0.0:
+            raise ZeroDivisionError("power iteration hit W v = 0")
+        u = wv / nwv
+        w = W.T @ u
+        sig = math.sqrt(float(w @ w))
+        v = w / sig
+    return W / sig, sig, v
+
+
+def prescale_frobenius(W: np.ndarray):
+    """W / |W|_F (R3: |W|_F >= sigma_max, always a safe start)."""
+    W = np.asarray(W, dtype=np.float64)
+    if W.size == 0:
+        return W.copy(), 0.0
+    f = math.sqrt(float(np.sum(W * W)))
+    if f == 0.0:
+        raise ZeroDivisionError("zero matrix (S:115)")
+    return W / f, f
+
+
+# ---------------------------------------------------------------------------
+# O3: Bjorck-Bowie iteration (eq. P:308-312; R1, R4)
+# ---------------------------------------------------------------------------
+def bjorck(W0: np.ndarray, T: int, beta: float = 0.5) -> np.ndarray:
+    """T iterations of W <- (1+beta) W - beta W W^T W.  The Gram is
+    formed on the short side (associativity, R4): m >= n uses W (W^T W),
+    m < n uses (W W^T) W."""
+    W = np.asarray(W0, dtype=np.float64).copy()
+    if W.size == 0:
+        return W
+    m, n = W.shape
+    for _ in range(T):
+        if m >= n:
+            W = (1.0 + beta) * W - beta * (W @ (W.T @ W))
+        else:
+            W = (1.0 + beta) * W - beta * ((W @ W.T) @ W)
+    return W
+
+
+def ns_residual(X: np.ndarray) -> float:
+    """|I - X^T X|_F on the short side (the NS residual)."""
+    X = np.asarray(X, dtype=np.float64)
+    if X.size == 0:
+        return 0.0
+    m, n = X.shape
+    G = X.T @ X if m >= n else X @ X.T
+    return float(np.linalg.norm(np.eye(G.shape[0]) - G))
+
+
+def orthogonalize(mats: Sequence[np.ndarray], T: int = 12, beta: float = 0.5,
+                  prescale: str = "power", P: int = 3,
+                  v: Optional[Sequence[np.ndarray]] = None):
+    """a2+a3 for a list of matrices: pre-scale then Bjorck.  v: one start
+    vector per matrix (length n); None -> ones/sqrt(n) (R2).  Returns
+    (ortho_list, v_new_list)."""
+    outs, vs = [], []
+    for idx, W in enumerate(mats):
+        W = np.asarray(W, dtype=np.float64)
+        n = W.shape[1]
+        if W.size == 0:
+            outs.append(W.copy())
+            vs.append(np.zeros(n))
+            continue
+        if prescale == "power":
+            v0 = np.ones(n) / math.sqrt(n) if v is None else np.asarray(v[idx], np.float64)
+            W0, _, vn = prescale_power(W, P, v0)
+        else:
+            W0, _ = prescale_frobenius(W)
+            vn = np.zeros(n) if v is None else np.asarray(v[idx], np.float64)
+        outs.append(bjorck(W0, T, beta))
+        vs.append(vn)
+    return outs, vs
+
+
+# ---------------------------------------------------------------------------
+# O4-O7: block convolution and the AOC construction
+# ---------------------------------------------------------------------------
+def block_conv(K1: np.ndarray, K2: np.ndarray) -> np.ndarray:
+    """K1 (*) K2: the kernel of conv_{K1} o conv_{K2} (P:351 footnote).
+    K[:, :, a+c, b+e] += K1[:, :, a, b] @ K2[:, :, c, e]."""
+    A, B, h1, w1 = K1.shape
+    B2, C, h2, w2 = K2.shape
+    if B != B2:
+        raise ValueError("inner channel mismatch")
+    K = np.zeros((A, C, h1 + h2 - 1, w1 + w2 - 1))
+    for a in range(h1):
+        for b in range(w1):
+            for c in range(h2):
+                for e in range(w2):
+                    K[:, :, a + c, b + e] += K1[:, :, a, b] @ K2[:, :, c, e]
+    return K
+
+
+def block_orth(Pa: np.ndarray, Pb: np.ndarray) -> np.ndarray:
+    """2x2 BCOP block [[PaPb, Pa(I-Pb)], [(I-Pa)Pb, (I-Pa)(I-Pb)]] (R5; the
+    [P | I-P] elementary kernels of S:232 composed vertically then
+    horizontally; "composing elementary orthogonal building blocks")."""
+    c = Pa.shape[0]
+    I = np.eye(c)
+    K = np.zeros((c, c, 2, 2))
+    K[:, :, 0, 0] = Pa @ Pb
+    K[:, :, 0, 1] = Pa @ (I - Pb)
+    K[:, :, 1, 0] = (I - Pa) @ Pb
+    K[:, :, 1, 1] = (I - Pa) @ (I - Pb)
+    return K
+
+
+def bcop(Q: np.ndarray, Us: Sequence[np.ndarray], c_out: int, c_in: int) -> np.ndarray:
+    """BCOP kernel (R5/R6): P_j = U_j U_j^T;
+    K = Q (*) B_1 (*) ... (*) B_{k'-1}, B_j = block_orth(P_{2j-1}, P_{2j});
+    sliced to [:c_out, :c_in]."""
+    c = Q.shape[0]
+    K = np.asarray(Q, np.float64)[:, :, None, None]
+    Ps = [np.asarray(U, np.float64) @ np.asarray(U, np.float64).T if U.size else np.zeros((c, c))
+          for U in Us]
+    for j in range(len(Ps) // 2):
+        K = block_conv(K, block_orth(Ps[2 * j], Ps[2 * j + 1]))
+    return K[:c_out, :c_in]
+
+
+def rko(R: np.ndarray, c_out: int, c_mid: int, s: int) -> np.ndarray:
+    """RKO kernel: reshape of the semi-orthogonal R to (c_out, c_mid, s, s) in
+    C order (R7)."""
+    return np.asarray(R, np.float64).reshape(c_out, c_mid, s, s)
+
+
+def layer_kernel(L: Layer, group_mats: Sequence[Sequence[np.ndarray]]) -> np.ndarray:
+    """AOC kernel of one layer from its ORTHOGONALISED matrices, one list per
+    group in layer_matrices() order (R7, R8, R13, R15).
+    Returns the forward-conv kernel (co_f, ci_f/g, k, k); for 'dense' the
+    co x ci matrix."""
+    geo = layer_geometry(L)
+    ks = []
+    for mats in group_mats:
+        mats = [np.asarray(M, np.float64) for M in mats]
+        if geo["kind"] == "dense":
+            ks.append(mats[0])
+            continue
+        if geo["kind"] == "bcop":
+            ks.append(bcop(mats[0], mats[1:], geo["co"], geo["ci"]))
+        elif geo["kind"] == "rko":
+            ks.append(rko(mats[0], geo["co"], geo["ci"], L.s))
+        else:
+            Kb = bcop(mats[0], mats[1:-1], geo["c_mid"], geo["ci"])
+            Kr = rko(mats[-1], geo["co"], geo["c_mid"], L.s)
+            ks.append(block_conv(Kr, Kb))
+    return np.concatenate(ks, axis=0)
+
+
+# ---------------------------------------------------------------------------
+# O8/O9: convolution and its adjoint
+# ---------------------------------------------------------------------------
+def out_size(H: int, k: int, s: int, d: int, p0: int, p1: int) -> int:
+    """H_out = floor((H + p0 + p1 - d(k-1) - 1)/s) + 1."""
+    return (H + p0 + p1 - d * (k - 1) - 1) // s + 1
+
+
+def _tap_rows(H: int, Ho: int, s: int, d: int, a: int, p0: int, circular: bool):
+    r = s * np.arange(Ho) + d * a - p0
+    if circular:
+        return np.mod(r, H), np.ones(Ho, bool)
+    ok = (r >= 0) & (r < H)
+    return np.clip(r, 0, H - 1), ok
+
+
+def conv2d(x: np.ndarray, K: np.ndarray, s: int = 1, d: int = 1, g: int = 1,
+           pads=None, mode: str = "circular") -> np.ndarray:
+    """Strided/dilated/grouped cross-correlation (a6):
+    y[n,o,u,v] = sum_{i in grp(o)} sum_{a,b} K[o,i,a,b] x~[n, i, s u + d a - p_t, s v + d b - p_l],
+    x~ zero-extended or circular (index mod H).  Direct tap loops with a
+    channel matmul per tap."""
+    x = np.asarray(x, np.float64)
+    K = np.asarray(K, np.float64)
+    N, C, H, W = x.shape
+    Co, Cig, kh, kw = K.shape
+    if C != Cig * g or Co % g:
+        raise ValueError("channel/group mismatch")
+    if pads is None:
+        e = d * (kh - 1)
+        pads = (e // 2, e - e // 2, e // 2, e - e // 2)
+    pt, pb, pl, pr = pads
+    Ho, Wo = out_size(H, kh, s, d, pt, pb), out_size(W, kw, s, d, pl, pr)
+    circ = mode == "circular"
+    Cog = Co // g
+    y = np.zeros((N, Co, Ho, Wo))
+    for a in range(kh):
+        rows, rok = _tap_rows(H, Ho, s, d, a, pt, circ)
+        for b in range(kw):
+            cols, cok = _tap_rows(W, Wo, s, d, b, pl, circ)
+            patch = x[:, :, rows][:, :, :, cols] * (rok[:, None] & cok[None, :])
+            for gi in range(g):
+                xs = patch[:, gi * Cig:(gi + 1) * Cig]
+                Kt = K[gi * Cog:(gi + 1) * Cog, :, a, b]
+                y[:, gi * Cog:(gi + 1) * Cog] += np.einsum("oi,nihw->nohw", Kt, xs)
+    return y
+
+
+def conv_transpose2d(y: np.ndarray, K: np.ndarray, H: int, W: int, s: int = 1,
+                     d: int = 1, g: int = 1, pads=None, mode: str = "circular") -> np.ndarray:
+    """Exact adjoint of conv2d(., K, spec) on (H, W) inputs (a7, R13,
+    R14): scatter form x~[n, i, s u + d a - p_t, s v + d b - p_l] += K[o,i,a,b] y[n,o,u,v],
+    wrapped mod H (circular) or dropped when out of range (zeros)."""
+    y = np.asarray(y, np.float64)
+    K = np.asarray(K, np.float64)
+    N, Co, Ho, Wo = y.shape
+    _, Cig, kh, kw = K.shape
+    if pads is None:
+        e = d * (kh - 1)
+        pads = (e // 2, e - e // 2, e // 2, e - e // 2)
+    pt, pb, pl, pr = pads
+    if (Ho, Wo) != (out_size(H, kh, s, d, pt, pb), out_size(W, kw, s, d, pl, pr)):
+        raise ValueError("shape mismatch")
+    circ = mode == "circular"
+    Cog = Co // g
+    x = np.zeros((N, Cig * g, H, W))
+    for a in range(kh):
+        rows, rok = _tap_rows(H, Ho, s, d, a, pt, circ)
+        for b in range(kw):
+            cols, cok = _tap_rows(W, Wo, s, d, b, pl, circ)
+            mask = (rok[:, None] & cok[None, :])
+            for gi in range(g):
+                Kt = K[gi * Cog:(gi + 1) * Cog, :, a, b]
+                contrib = np.einsum("oi,nohw->nihw", Kt, y[:, gi * Cog:(gi + 1) * Cog]) * mask
+                # unbuffered scatter-add: repeated (wrapped) targets accumulate
+                np.add.at(x, (slice(None), slice(gi * Cig, (gi + 1) * Cig),
+                              rows[:, None], cols[None, :]), contrib)
+    return x
+
+
+# ---------------------------------------------------------------------------
+# O10: verifiers
+# ---------------------------------------------------------------------------
+def toeplitz(op, in_shape: Tuple[int, int, int]) -> np.ndarray:
+    """Matrix of a linear op by impulse responses ("Using the impulse
+    response approach, we construct the Toeplitz matrix"): column j =
+    flatten(op(e_j))."""
+    C, H, W = in_shape
+    n = C * H * W
+    E = np.eye(n).reshape(n, C, H, W)
+    Y = op(E)
+    return Y.reshape(n, -1).T
+
+
+def fft_singular_values(K: np.ndarray, H: int, W: int, d: int = 1) -> np.ndarray:
+    """Singular values of the circular stride-1 conv on H x W by per-frequency
+    SVD (P:433 FFT lineage).  Transfer matrix at (f1, f2):
+    M = sum_{a,b} K[:, :, a, b] exp(2 pi i (f1 d a / H + f2 d b / W))."""
+    Co, Ci, kh, kw = K.shape
+    out = []
+    for f1 in range(H):
+        for f2 in range(W):
+            M = np.zeros((Co, Ci), complex)
+            for a in range(kh):
+                for b in range(kw):
+                    M += K[:, :, a, b] * np.exp(2j * np.pi * (f1 * d * a / H + f2 * d * b / W))
+            out.append(np.linalg.svd(M, compute_uv=False))
+    return np.sort(np.concatenate(out))
+
+
+def polyphase_singular_values(K: np.ndarray, H: int, W: int, s: int, d: int = 1,
+                              pads=None) -> np.ndarray:
+    """Singular values of the circular stride-s conv (s | H, s | W) via the
+    polyphase reduction: with t = d a - p = s q + r,
+    x[s u + t] = x_r[u + q], so the strided conv is a stride-1 conv on the
+    s^2-phase input; per-frequency SVD of the c_out x (c_in s^2) symbol on the
+    (H/s) x (W/s) grid."""
+    Co, Ci, kh, kw = K.shape
+    if H % s or W % s:
+        raise ValueError("polyphase needs s | H and s | W")
+    if pads is None:
+        e = d * (kh - 1)
+        pads = (e // 2, e - e // 2, e // 2, e - e // 2)
+    pt, _, pl, _ = pads
+    Hs, Ws = H // s, W // s
+    out = []
+    for f1 in range(Hs):
+        for f2 in range(Ws):
+            M = np.zeros((Co, Ci, s, s), complex)
+            for a in range(kh):
+                qa, ra = divmod(d * a - pt, s)
+                for b in range(kw):
+                    qb, rb = divmod(d * b - pl, s)
+                    M[:, :, ra, rb] += K[:, :, a, b] * np.exp(2j * np.pi * (f1 * qa / Hs + f2 * qb / Ws))
+            out.append(np.linalg.svd(M.reshape(Co, Ci * s * s), compute_uv=False))
+    return np.sort(np.concatenate(out))
+
+
+def conv_singular_values(K: np.ndarray, L: Layer, H: int, W: int) -> np.ndarray:
+    """All singular values of a circular layer operator on H x W inputs,
+    group by group (block-diagonal), using FFT (s = 1) or polyphase."""
+    g = L.g
+    Cog = K.shape[0] // g
+    vals = []
+    for gi in range(g):
+        Kg = K[gi * Cog:(gi + 1) * Cog]
+        if L.s == 1:
+            vals.append(fft_singular_values(Kg, H, W, L.d))
+        else:
+            vals.append(polyphase_singular_values(Kg, H, W, L.s, L.d, L.pads()))
+    return np.sort(np.concatenate(vals))

@@ -1,0 +1,378 @@
+"""Pins of the float64 oracle against what the paper and mathematics fix
+(closed forms, library routines, brute force on tiny inputs, invariants,
+SPEC worked examples).  CPU only.  Each test names the oracle step it pins.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+import oracle as O
+from synth import configs, gen
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+rs = np.random.default_rng(1234)
+
+
+def t64(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float64))
+
+
+# --------------------------------------------------------------------- O2
+def test_prescale_special_cases():
+    W0, sig, _ = O.prescale_power(np.array(GOLD["power_identity"]["W"], float), 3, np.ones(3) / math.sqrt(3))
+    assert abs(sig - 1.0) < 1e-15 and np.allclose(W0, np.eye(3), atol=1e-15)
+    g = GOLD["power_diag21"]
+    W0, sig, _ = O.prescale_power(np.array(g["W"], float), 60, np.ones(2) / math.sqrt(2))
+    assert abs(sig - g["sigma"]) < 1e-12
+    assert np.allclose(W0, np.array(g["W0"]), atol=1e-12)
+
+
+def test_prescale_matches_lapack_sigma_max():
+    # 50 iterations -> sigma_max of the SVD (LAPACK) to 1e-6
+    for shape in [(8, 8), (12, 5), (5, 12)]:
+        W = rs.standard_normal(shape)
+        v = rs.standard_normal(shape[1]); v /= np.linalg.norm(v)
+        _, sig, vn = O.prescale_power(W, 50, v)
+        smax = np.linalg.svd(W, compute_uv=False)[0]
+        assert abs(sig - smax) / smax < 1e-6
+        assert abs(np.linalg.norm(vn) - 1) < 1e-12
+
+
+def test_prescale_zero_and_frobenius():
+    with pytest.raises(ZeroDivisionError):
+        O.prescale_power(np.zeros((3, 3)), 3, np.ones(3))
+    W = rs.standard_normal((7, 4))
+    W0, f = O.prescale_frobenius(W)
+    assert abs(f - np.sqrt((W ** 2).sum())) < 1e-12
+    assert np.linalg.svd(W0, compute_uv=False)[0] <= 1.0
+
+
+def test_power_iteration_one_step_by_hand():
+    # one step from v = e1 on W = [[3, 4], [0, 0]]: Wv = (3, 0) -> u = e1; w = W^T u = (3, 4); sig = 5
+    _, sig, v = O.prescale_power(np.array([[3.0, 4.0], [0.0, 0.0]]), 1, np.array([1.0, 0.0]))
+    assert abs(sig - 5.0) < 1e-15 and np.allclose(v, [0.6, 0.8])
+
+
+# --------------------------------------------------------------------- O3
+def _closed_form(W0, T, beta):
+    U, S, Vt = np.linalg.svd(W0, full_matrices=False)
+    for _ in range(T):
+        S = (1 + beta) * S - beta * S ** 3
+    return (U * S) @ Vt
+
+
+@pytest.mark.parametrize("shape", [(16, 16), (24, 9), (9, 24), (40, 40)])
+@pytest.mark.parametrize("beta", [0.5, 0.3])
+def test_bjorck_closed_form(shape, beta):
+    # NS_T(W0) = U f^T(Sigma) V^T with f(s) = (1+beta)s - beta s^3 (SURVEY §8(c) O3 pin)
+    W = rs.standard_normal(shape)
+    W0 = W / np.linalg.svd(W, compute_uv=False)[0] * 0.97
+    for T in (1, 2, 5, 12):
+        X = O.bjorck(W0, T, beta)
+        Y = _closed_form(W0, T, beta)
+        assert np.abs(X - Y).max() < 1e-12, (T, np.abs(X - Y).max())
+
+
+def test_bjorck_converges_to_polar_and_fixed_points():
+    W = rs.standard_normal((20, 12))
+    W0 = W / np.linalg.svd(W, compute_uv=False)[0]
+    U, _, Vt = np.linalg.svd(W0, full_matrices=False)
+    X = O.bjorck(W0, 60, 0.5)
+    assert np.abs(X - U @ Vt).max() < 1e-10              # S:129 polar factor
+    assert np.abs(O.bjorck(np.eye(6), 12) - np.eye(6)).max() == 0.0
+    Q, _ = np.linalg.qr(rs.standard_normal((9, 9)))
+    assert np.abs(O.bjorck(Q, 12) - Q).max() < 1e-14
+
+
+def test_bjorck_residual_monotone():
+    # |W_t^T W_t - I| non-increasing when |W0|_2 <= 1
+    W = rs.standard_normal((30, 30))
+    X = W / np.linalg.svd(W, compute_uv=False)[0]
+    prev = O.ns_residual(X)
+    for _ in range(25):
+        X = O.bjorck(X, 1)
+        r = O.ns_residual(X)
+        assert r <= prev + 1e-14
+        prev = r
+
+
+def test_orthogonalize_near_orthogonal_T12():
+    # R21: near-orthogonal parameters converge in 12 iterations ("12-25")
+    for (m, n) in [(64, 64), (128, 64), (64, 256)]:
+        W = gen.param_matrix(m, n, (9, m, n, 0, 1)).astype(np.float64)
+        (X,), _ = O.orthogonalize([W], T=12)
+        assert O.ns_residual(X) < 1e-10
+
+
+# --------------------------------------------------------------------- O4
+def test_block_conv_identity_and_matmul():
+    g = GOLD["blockconv_1x1"]
+    A = np.array(g["A"], float)[:, :, None, None]
+    B = np.array(g["B"], float)[:, :, None, None]
+    assert np.array_equal(O.block_conv(A, B)[:, :, 0, 0], np.array(g["AB"], float))
+    K = rs.standard_normal((3, 4, 3, 2))
+    delta_r = np.eye(4)[:, :, None, None]
+    delta_l = np.eye(3)[:, :, None, None]
+    assert np.array_equal(O.block_conv(K, delta_r), K)
+    assert np.array_equal(O.block_conv(delta_l, K), K)
+
+
+@pytest.mark.parametrize("k1,k2", [((2, 2), (2, 2)), ((3, 1), (2, 3)), ((1, 1), (3, 3))])
+def test_block_conv_is_composition_torch(k1, k2):
+    # conv_{K1}(conv_{K2}(x)) = conv_{K1 (*) K2}(x) (zero padding, summed pads);
+    # checked with torch-CPU f64 conv2d, an independent library routine
+    K1 = rs.standard_normal((3, 4, *k1))
+    K2 = rs.standard_normal((4, 2, *k2))
+    x = rs.standard_normal((2, 2, 9, 8))
+    seq = F.conv2d(F.conv2d(t64(x), t64(K2), padding=(k2[0] - 1, k2[1] - 1)), t64(K1),
+                   padding=(k1[0] - 1, k1[1] - 1))
+    K = O.block_conv(K1, K2)
+    fused = F.conv2d(t64(x), t64(K), padding=(k1[0] + k2[0] - 2, k1[1] + k2[1] - 2))
+    assert torch.allclose(seq, fused, atol=1e-10)
+
+
+def test_block_conv_circular_composition_and_stride():
+    # composition under circular padding with a strided outer conv (the AOC use)
+    K1 = rs.standard_normal((5, 3, 2, 2))   # outer, stride 2
+    K2 = rs.standard_normal((3, 3, 2, 2))   # inner, stride 1
+    x = rs.standard_normal((1, 3, 8, 8))
+    xt = t64(x)
+    inner = F.conv2d(F.pad(xt, (0, 1, 0, 1), mode="circular"), t64(K2))
+    outer = F.conv2d(F.pad(inner, (0, 1, 0, 1), mode="circular"), t64(K1), stride=2)
+    K = O.block_conv(K1, K2)
+    fused = F.conv2d(F.pad(xt, (0, 2, 0, 2), mode="circular"), t64(K), stride=2)
+    assert torch.allclose(outer, fused, atol=1e-10)
+
+
+def test_block_conv_associative():
+    A = rs.standard_normal((2, 3, 2, 1)); B = rs.standard_normal((3, 4, 1, 2)); C = rs.standard_normal((4, 2, 2, 2))
+    assert np.abs(O.block_conv(O.block_conv(A, B), C) - O.block_conv(A, O.block_conv(B, C))).max() < 1e-12
+
+
+# --------------------------------------------------------------------- O5
+def _proj(c, r):
+    U, _ = np.linalg.qr(rs.standard_normal((c, r)))
+    return U @ U.T, U
+
+
+def test_block_orth_unitary_symbol_and_factorisation():
+    Pa, _ = _proj(6, 3); Pb, _ = _proj(6, 3)
+    K = O.block_orth(Pa, Pb)
+    I = np.eye(6)
+    H = np.stack([Pa, I - Pa], -1)[:, :, :, None]      # 2x1 vertical [Pa; I-Pa]
+    W = np.stack([Pb, I - Pb], -1)[:, :, None, :]      # 1x2 horizontal [Pb | I-Pb]
+    assert np.abs(O.block_conv(H, W) - K).max() < 1e-14
+    for _ in range(5):
+        z1, z2 = np.exp(2j * np.pi * rs.random(2))
+        M = K[:, :, 0, 0] + K[:, :, 0, 1] * z2 + K[:, :, 1, 0] * z1 + K[:, :, 1, 1] * z1 * z2
+        assert np.abs(M.conj().T @ M - I).max() < 1e-13
+
+
+def test_bcop_degenerate_and_orthogonal():
+    Q, _ = np.linalg.qr(rs.standard_normal((4, 4)))
+    assert np.array_equal(O.bcop(Q, [], 4, 4)[:, :, 0, 0], Q)        # S:235 k'=1 -> Q
+    Us = [_proj(4, 2)[1] for _ in range(4)]
+    K = O.bcop(Q, Us, 4, 4)
+    assert K.shape == (4, 4, 3, 3)
+    T = O.toeplitz(lambda x: O.conv2d(x, K), (4, 8, 8))
+    sv = np.linalg.svd(T, compute_uv=False)
+    assert np.abs(sv - 1).max() < 1e-12
+
+
+# --------------------------------------------------------------------- O6
+def test_rko_equals_pixel_unshuffle_matmul():
+    # stride-s RKO conv == pixel_unshuffle + 1x1 conv with R (torch library)
+    co, cm, s = 6, 3, 2
+    R = rs.standard_normal((co, cm * s * s))
+    K = O.rko(R, co, cm, s)
+    x = rs.standard_normal((2, cm, 8, 8))
+    y = O.conv2d(x, K, s=s, mode="circular")
+    ref = F.conv2d(F.pixel_unshuffle(t64(x), s), t64(R)[:, :, None, None])
+    assert np.abs(y - ref.numpy()).max() < 1e-12
+
+
+# --------------------------------------------------------------------- O8/O9
+@pytest.mark.parametrize("s,d,g,k,mode", [(1, 1, 1, 3, "zeros"), (2, 1, 1, 3, "zeros"), (1, 2, 2, 3, "zeros"),
+                                          (2, 3, 1, 3, "circular"), (1, 1, 2, 2, "circular"),
+                                          (3, 1, 1, 4, "circular"), (2, 1, 1, 5, "circular")])
+def test_conv2d_matches_torch(s, d, g, k, mode):
+    x = rs.standard_normal((2, 4, 12, 11))
+    K = rs.standard_normal((6, 4 // g, k, k))
+    e = d * (k - 1); pads = (e // 2, e - e // 2, e // 2, e - e // 2)
+    y = O.conv2d(x, K, s=s, d=d, g=g, pads=pads, mode=mode)
+    xp = F.pad(t64(x), (pads[2], pads[3], pads[0], pads[1]), mode="circular" if mode == "circular" else "constant")
+    ref = F.conv2d(xp, t64(K), stride=s, dilation=d, groups=g)
+    assert y.shape == tuple(ref.shape)
+    assert np.abs(y - ref.numpy()).max() < 1e-12
+
+
+def test_conv2d_spec_examples():
+    for key in ("conv_identity_1x1", "conv_center_delta"):
+        g = GOLD[key]
+        x = rs.standard_normal((1, 1, g["H"], g["H"]))
+        y = O.conv2d(x, np.array(g["kernel"], float), s=g["s"], pads=tuple(g["pads"]), mode="zeros")
+        assert np.array_equal(y, x)
+    g = GOLD["conv_ones_stride2"]
+    y = O.conv2d(np.array(g["input"], float), np.array(g["kernel"], float), s=2, pads=(0, 0, 0, 0), mode="zeros")
+    assert np.array_equal(y, np.array(g["expect"], float))
+    g = GOLD["convT_ones_stride2"]
+    x = O.conv_transpose2d(np.array(g["input"], float), np.array(g["kernel"], float), 4, 4, s=2,
+                           pads=(0, 0, 0, 0), mode="zeros")
+    assert np.array_equal(x, np.array(g["expect"], float))
+
+
+@pytest.mark.parametrize("s,d,g,k,mode,H", [(1, 1, 1, 3, "circular", 8), (2, 1, 1, 3, "zeros", 9),
+                                            (2, 3, 2, 3, "circular", 12), (2, 1, 1, 4, "zeros", 8),
+                                            (1, 2, 1, 3, "zeros", 7), (3, 1, 1, 3, "circular", 9)])
+def test_conv_transpose_adjoint(s, d, g, k, mode, H):
+    K = rs.standard_normal((4, 6 // g, k, k))
+    x = rs.standard_normal((2, 6, H, H))
+    y = O.conv2d(x, K, s=s, d=d, g=g, mode=mode)
+    yr = rs.standard_normal(y.shape)
+    xt = O.conv_transpose2d(yr, K, H, H, s=s, d=d, g=g, mode=mode)
+    lhs, rhs = float((y * yr).sum()), float((x * xt).sum())
+    assert abs(lhs - rhs) < 1e-11 * max(1.0, abs(lhs))
+
+
+def test_conv_transpose_matches_torch_zero_padding():
+    K = rs.standard_normal((4, 3, 3, 3))
+    H = 9
+    y = rs.standard_normal((2, 4, 5, 5))          # conv of 9x9 with s=2 same-pad (1,1)
+    x = O.conv_transpose2d(y, K, H, H, s=2, pads=(1, 1, 1, 1), mode="zeros")
+    ref = F.conv_transpose2d(t64(y), t64(K), stride=2, padding=1, output_padding=0)
+    assert np.abs(x - ref.numpy()).max() < 1e-12
+
+
+# --------------------------------------------------------------------- O10
+def test_toeplitz_reproduces_conv_and_fft():
+    K = rs.standard_normal((3, 2, 3, 3))
+    T = O.toeplitz(lambda x: O.conv2d(x, K, d=2), (2, 8, 8))
+    x = rs.standard_normal((2, 8, 8))
+    assert np.abs(T @ x.ravel() - O.conv2d(x[None], K, d=2).ravel()).max() < 1e-12
+    sv_t = np.sort(np.linalg.svd(T, compute_uv=False))
+    sv_f = O.fft_singular_values(K, 8, 8, d=2)
+    sv_f = sv_f[-len(sv_t):]
+    assert np.abs(sv_t - sv_f).max() < 1e-10
+
+
+@pytest.mark.parametrize("co,ci,k,s,H", [(4, 8, 3, 2, 8), (3, 5, 4, 2, 8), (2, 6, 3, 3, 9), (4, 3, 5, 2, 10)])
+def test_polyphase_equals_toeplitz(co, ci, k, s, H):
+    K = rs.standard_normal((co, ci, k, k))
+    T = O.toeplitz(lambda x: O.conv2d(x, K, s=s), (ci, H, H))
+    sv_t = np.sort(np.linalg.svd(T, compute_uv=False))
+    sv_p = O.polyphase_singular_values(K, H, H, s)
+    sv_p = sv_p[-len(sv_t):]
+    assert np.abs(sv_t - sv_p).max() < 1e-10
+
+
+# --------------------------------------------------------------------- O7 + whole path
+def _exact_ortho_mats(L):
+    """Exactly (semi-)orthogonal matrices of the layer's shapes (QR), to pin the
+    composition independently of Bjorck."""
+    out = []
+    for _ in range(L.g):
+        ms = []
+        for M in O.layer_matrices(L):
+            if M.n == 0:
+                ms.append(np.zeros((M.m, 0)))
+                continue
+            A = rs.standard_normal((max(M.m, M.n), min(M.m, M.n)))
+            Q, _ = np.linalg.qr(A)
+            ms.append(Q if M.m >= M.n else Q.T)
+        out.append(ms)
+    return out
+
+
+AOC_GRID = [  # (c_in, c_out, k, s, d, g, kind)
+    (16, 16, 3, 1, 1, 1, "conv"), (4, 4, 3, 1, 1, 1, "conv"), (4, 8, 3, 1, 1, 1, "conv"), (8, 4, 3, 1, 1, 1, "conv"),
+    (4, 4, 2, 1, 1, 1, "conv"), (4, 4, 5, 1, 1, 1, "conv"), (4, 4, 4, 1, 1, 1, "conv"), (4, 8, 3, 2, 1, 1, "conv"),
+    (8, 4, 3, 2, 1, 1, "conv"), (4, 4, 3, 2, 1, 1, "conv"), (1, 8, 3, 2, 1, 1, "conv"), (2, 8, 3, 2, 1, 1, "conv"),
+    (4, 16, 3, 2, 1, 1, "conv"), (4, 32, 3, 2, 1, 1, "conv"), (8, 8, 4, 2, 1, 1, "conv"), (4, 4, 2, 2, 1, 1, "conv"),
+    (4, 16, 2, 2, 1, 1, "conv"), (1, 4, 2, 2, 1, 1, "conv"), (4, 4, 1, 1, 1, 1, "conv"), (1, 1, 3, 1, 1, 1, "conv"),
+    (8, 8, 3, 1, 1, 2, "conv"), (8, 16, 3, 2, 1, 2, "conv"), (4, 4, 3, 1, 2, 1, "conv"), (4, 8, 3, 2, 3, 1, "conv"),
+    (8, 8, 3, 1, 2, 2, "convT"), (8, 4, 3, 2, 1, 1, "convT"), (4, 8, 3, 2, 1, 2, "convT"), (4, 4, 3, 1, 1, 1, "convT"),
+]
+
+
+@pytest.mark.parametrize("ci,co,k,s,d,g,kind", AOC_GRID)
+def test_aoc_orthogonal_toeplitz(ci, co, k, s, d, g, kind):
+    # P:330 "rigorously proven orthogonal for any valid configuration (k >= s)";
+    # P:462 Toeplitz SVD on small images; all min(rows, cols) sigma = 1 (R9, R12)
+    L = O.Layer(ci, co, k, s, d, g, kind=kind)
+    K = O.layer_kernel(L, _exact_ortho_mats(L))
+    ci_f, co_f = L.fwd_channels()
+    assert K.shape == (co_f, ci_f // g, k, k)
+    H = 12 if s == 3 or d == 3 else 8
+    if kind == "conv":
+        op, shape = (lambda x: O.conv2d(x, K, s=s, d=d, g=g)), (ci_f, H, H)
+    else:
+        Hs = H // s
+        op, shape = (lambda y: O.conv_transpose2d(y, K, H, H, s=s, d=d, g=g)), (co_f, Hs, Hs)
+    T = O.toeplitz(op, shape)
+    sv = np.linalg.svd(T, compute_uv=False)
+    r = min(T.shape)
+    assert np.abs(sv[:r] - 1).max() < 1e-10, (sv.min(), sv.max())
+    if kind == "conv":   # scalable estimator agrees with the exact one
+        sv2 = O.conv_singular_values(K, L, H, H)
+        assert np.abs(sv2[-r:] - 1).max() < 1e-10
+
+
+def test_zero_padding_is_one_lipschitz_only():
+    # R12: zero padding -> sigma_max <= 1 (no lower bound); P:462 tests transposed with zero padding only
+    L = O.Layer(4, 4, 3, 1, padding_mode="zeros")
+    K = O.layer_kernel(L, _exact_ortho_mats(L))
+    T = O.toeplitz(lambda x: O.conv2d(x, K, mode="zeros"), (4, 8, 8))
+    sv = np.linalg.svd(T, compute_uv=False)
+    assert sv.max() <= 1 + 1e-12 and sv.min() < 0.5
+
+
+def test_gcd_stride_dilation_breaks_orthogonality():
+    # R10: gcd(s, d) != 1 loses orthogonality (why the boundary rejects it)
+    L = O.Layer(4, 8, 3, 2, 2)
+    K = O.layer_kernel(L, _exact_ortho_mats(L))
+    sv = O.conv_singular_values(K, L, 8, 8)
+    assert sv.max() > 1.2
+
+
+def test_cfg1_whole_path_norm_preservation():
+    # whole path on cfg1: params -> power/Bjorck -> BCOP -> conv; |y| = |x| per sample (isometry)
+    Ld = configs.cfg1()[0]
+    L = O.Layer(Ld["c_in"], Ld["c_out"], Ld["k"], Ld["s"], Ld["d"], Ld["g"])
+    specs = O.layer_matrices(L)
+    mats = [gen.param_matrix(M.m, M.n, (1, 0, 0, j, gen.ROLE_ID[M.role])).astype(np.float64)
+            for j, M in enumerate(specs)]
+    ortho, _ = O.orthogonalize(mats, T=12)
+    for X in ortho:
+        assert O.ns_residual(X) < 1e-12
+    K = O.layer_kernel(L, [ortho])
+    x = gen.activations((2, 16, 8, 8), (1, 0, 0, 0, gen.ROLE_ID["x"])).astype(np.float64)
+    y = O.conv2d(x, K)
+    nx = np.sqrt((x ** 2).sum(axis=(1, 2, 3)))
+    ny = np.sqrt((y ** 2).sum(axis=(1, 2, 3)))
+    assert np.abs(ny / nx - 1).max() < 1e-12
+
+
+# --------------------------------------------------------------------- a1 derivation
+def _count(cfg_layers):
+    n, flops = 0, 0.0
+    for Ld in cfg_layers:
+        L = O.Layer(Ld["c_in"], Ld["c_out"], Ld["k"], Ld["s"], Ld["d"], Ld["g"], kind=Ld["kind"])
+        for M in O.layer_matrices(L):
+            n += L.g
+            m_, n_ = max(M.m, M.n), min(M.m, M.n)
+            flops += L.g * 4.0 * m_ * n_ * n_ * 12
+    return n, flops
+
+
+def test_unit_derivation_counts_match_survey():
+    # SURVEY §8(d) totals: cfg2 57 matrices / 45.5 GF; cfg3 158 / 99.8 GF; cfg4 333 / 670 GF (T = 12)
+    n2, f2 = _count(configs.cfg2())
+    n3, f3 = _count(configs.cfg3())
+    n4, f4 = _count(configs.cfg4())
+    assert (n2, n3, n4) == (57, 158, 333)
+    assert abs(f2 / 1e9 - 45.5) < 0.1 and abs(f3 / 1e9 - 99.8) < 0.1 and abs(f4 / 1e9 - 670) < 1.0

@@ -1,0 +1,200 @@
+/*
+ * orth.h -- C ABI of the B200-native orthogonal-convolution hot path.
+ *
+ * The library turns free parameter matrices into exactly orthogonal conv
+ * kernels and applies them (arXiv 2601.13776 "Orthogonium", AOC layers):
+ *
+ *   orth_plan_create     host: validate layers, derive the matrices of every
+ *                        (layer, group) unit, packed layouts, workspace.
+ *   orth_orthogonalize   a2+a3: pre-scaling (batched power iteration, P:100-101,
+ *                        P:313, or Frobenius) then T Bjorck / Newton-Schulz
+ *                        iterations W <- (1+b)W - b W W^T W.
+ *   orth_compose_kernel  a4+a5: BCOP chain of projector blocks, RKO
+ *                        reshape and AOC = RKO (*) K_BCOP, emitted
+ *                        as FP32 PyTorch-layout and BF16 GEMM-layout kernels.
+ *   orth_conv_forward    a6: strided / dilated / grouped conv with that kernel
+ *                        ("a single call to torch.nn.Conv2d").
+ *   orth_conv_transpose  a7: its exact adjoint (P:334 transposed convolutions).
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, R<k> = reading k of
+ * DESIGN.md "Readings of the paper".  Everything computed here is defined by
+ * the float64 oracle in oracle/orth_oracle.py, which shares no code with it.
+ *
+ * Conventions
+ *  - Ownership: the caller owns every data buffer (params, ortho, power cache,
+ *    kernels, x, y, bias).  They are DEVICE pointers on the plan's device,
+ *    16-byte aligned (128 B preferred).  The plan owns its workspace (allocated
+ *    in orth_plan_create, freed in orth_plan_destroy) and a device status word.
+ *    No call allocates device memory after create.
+ *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *    default stream).  Compute calls are asynchronous: they validate
+ *    arguments synchronously (enqueuing nothing on failure), enqueue kernels on
+ *    `stream` and return.  None calls cudaDeviceSynchronize.
+ *  - Device-side conditions (zero matrix; non-finite NS residual,
+ *    S:125) set the plan's status word; orth_plan_check reports them.
+ *  - Determinism: results are bitwise reproducible for fixed inputs, device
+ *    type and (rank, world): no floating-point atomics, fixed reduction order.
+ *  - Threading: a plan serves one host thread at a time.  orth_last_error is
+ *    thread-local.
+ */
+#ifndef ORTH_H_
+#define ORTH_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct orth_plan* orth_plan_t;
+
+typedef enum {
+  ORTH_OK = 0,
+  ORTH_ERR_INVALID_ARGUMENT = 1,   /* null pointer, bad enum, dim < 1, g does not divide channels, beta not in (0, 1/2], T < 1 */
+  ORTH_ERR_UNSUPPORTED_CONFIG = 2, /* k < s, gcd(s, d) != 1 (R10), non-square k/s/d, dense forward */
+  ORTH_ERR_SHAPE_MISMATCH = 3,     /* N/H/W inconsistent with the layer, circular with s not dividing H or W (R11) */
+  ORTH_ERR_ZERO_NORM = 4,          /* device: a zero parameter matrix */
+  ORTH_ERR_NOT_CONVERGED = 5,      /* device: non-finite NS residual */
+  ORTH_ERR_CUDA = 6,               /* CUDA runtime error; detail in orth_last_error() */
+  ORTH_ERR_OUT_OF_MEMORY = 7,      /* workspace allocation failed */
+  ORTH_ERR_NO_DEVICE = 8           /* compute call on a host-only plan (device = -1) */
+} orth_status_t;
+
+typedef enum { ORTH_F32 = 0, ORTH_BF16 = 1 } orth_dtype_t;
+typedef enum { ORTH_PAD_ZEROS = 0, ORTH_PAD_CIRCULAR = 1 } orth_pad_t;
+typedef enum { ORTH_CONV2D = 0, ORTH_CONV_TRANSPOSE2D = 1, ORTH_DENSE = 2 } orth_kind_t;
+typedef enum { ORTH_PRESCALE_POWER = 0, ORTH_PRESCALE_FROBENIUS = 1 } orth_prescale_t;
+
+/* One orthogonal layer (S:35-40 ConvSpec + S:205-210 ConvLayerConfig).
+ *  kind ORTH_CONV2D: AdaptiveOrthoConv2d, c_in -> c_out.
+ *  kind ORTH_CONV_TRANSPOSE2D: AdaptiveOrthoConvTranspose2d, c_in (small
+ *    spatial) -> c_out (large spatial); its kernel is that of the forward
+ *    adjoint conv c_out -> c_in, PyTorch ConvTranspose2d weight layout
+ *    (c_in, c_out/g, k, k) (R13).
+ *  kind ORTH_DENSE: an OrthoLinear weight c_out x c_in; k = s = d = 1.
+ *  Square kernels/strides/dilations only (k_h == k_w, ...).  pad_* = -1 selects
+ *  the "same" rule p_t = floor(d(k-1)/2), p_b = d(k-1) - p_t (R11).  */
+typedef struct {
+  int32_t kind;          /* orth_kind_t */
+  int32_t c_in, c_out;
+  int32_t k_h, k_w;
+  int32_t stride_h, stride_w;
+  int32_t dil_h, dil_w;
+  int32_t groups;
+  int32_t pad_t, pad_b, pad_l, pad_r;
+  int32_t padding_mode;  /* orth_pad_t */
+} orth_layer_desc_t;
+
+/* OrthoParams, Bjorck only. */
+typedef struct {
+  int32_t ns_iters;      /* T >= 1, default 12 (R1) */
+  float beta;            /* in (0, 1/2], default 0.5 */
+  int32_t prescale;      /* orth_prescale_t, default power (R3) */
+  int32_t power_iters;   /* P >= 1, default 3 (R2) */
+  int32_t compute;       /* orth_dtype_t of the NS contractions: F32 (FP32-accurate) or BF16 tensor cores with FP32 master (R16) */
+  int32_t polish_iters;  /* BF16 only: trailing iterations run FP32-accurate, default 2 */
+  int32_t rank, world;   /* construction sharding by layer (R22); default 0, 1 */
+} orth_opts_t;
+
+/* Fill *opts with the defaults above. */
+void orth_opts_default(orth_opts_t* opts);
+
+/* Host-only validation of layer descriptors and options; needs no GPU.
+ * Returns the first failing status; detail in orth_last_error(). */
+orth_status_t orth_validate_desc(const orth_layer_desc_t* layers, int32_t n_layers, const orth_opts_t* opts);
+
+/* Create a plan for n_layers layers on CUDA device `device` (>= 0), or a
+ * host-only plan (device = -1) usable for orth_plan_query only.  Copies
+ * `layers` and `opts` (opts may be NULL = defaults).  On success *plan owns
+ * all workspace. */
+orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers, const orth_opts_t* opts,
+                               int32_t device, orth_plan_t* plan);
+orth_status_t orth_plan_destroy(orth_plan_t plan);
+
+/* Plan queries (int64 result in *out).  `index` is a layer index for the
+ * ORTH_Q_LAYER_* queries and a global matrix index for ORTH_Q_MATRIX_*. */
+typedef enum {
+  ORTH_Q_N_LAYERS = 0,
+  ORTH_Q_N_MATRICES = 1,          /* total parameter matrices over all layers and groups */
+  ORTH_Q_PARAMS_NUMEL = 2,        /* floats in the packed params / ortho buffers */
+  ORTH_Q_CACHE_NUMEL = 3,         /* floats in the packed power-iteration cache */
+  ORTH_Q_KERNELS_F32_NUMEL = 4,   /* floats in kernels_f32 (all ranks' segments) */
+  ORTH_Q_KERNELS_BF16_NUMEL = 5,  /* bf16 elements in kernels_bf16 */
+  ORTH_Q_WORKSPACE_BYTES = 6,
+  ORTH_Q_NS_FLOPS = 7,            /* algorithmic NS flops 4 m n^2 T (m >= n) of this rank's matrices */
+  ORTH_Q_KERNEL_SEGMENT_F32 = 8,  /* per-rank segment size (floats) of kernels_f32 */
+  ORTH_Q_KERNEL_SEGMENT_BF16 = 9,
+  ORTH_Q_LAYER_FIRST_MATRIX = 20, /* global index of the layer's first matrix */
+  ORTH_Q_LAYER_MATS_PER_GROUP = 21,
+  ORTH_Q_LAYER_KERNEL_OFF_F32 = 22,
+  ORTH_Q_LAYER_KERNEL_OFF_BF16 = 23,
+  ORTH_Q_LAYER_KERNEL_NUMEL = 24, /* elements of the layer kernel (same in both layouts) */
+  ORTH_Q_LAYER_OWNER = 25,        /* rank that constructs this layer */
+  ORTH_Q_LAYER_C_MID = 26,        /* derived internal width (R7); 0 if none */
+  ORTH_Q_LAYER_C_B = 27,          /* BCOP width; 0 if none */
+  ORTH_Q_LAYER_KP = 28,           /* BCOP size k' (R8); 0 if none */
+  ORTH_Q_MATRIX_ROWS = 40,
+  ORTH_Q_MATRIX_COLS = 41,
+  ORTH_Q_MATRIX_OFFSET = 42,      /* float offset in params / ortho */
+  ORTH_Q_MATRIX_CACHE_OFFSET = 43,/* float offset of its length-n vector in the power cache */
+  ORTH_Q_MATRIX_LAYER = 44,
+  ORTH_Q_MATRIX_GROUP = 45,
+  ORTH_Q_MATRIX_ROLE = 46         /* 0 Q, 1 U, 2 R, 3 W */
+} orth_query_t;
+orth_status_t orth_plan_query(orth_plan_t plan, int32_t what, int32_t index, int64_t* out);
+
+/* a2+a3.  params: packed FP32 matrices, layer -> group -> [Q, U_1..U_2(k'-1), R]
+ * (R15), each row-major at ORTH_Q_MATRIX_OFFSET (offsets 128 B aligned).
+ * ortho_out: same layout; receives the orthogonalised matrices of this rank's
+ * layers (others untouched).  power_cache: nullable in/out, one length-n
+ * vector per matrix at ORTH_Q_MATRIX_CACHE_OFFSET (P:313 cached vector); NULL
+ * starts every power iteration from ones/sqrt(n) (R2).  residual_out:
+ * nullable, one float per matrix: |I - X^T X|_F of the result on the short
+ * side.  Device-side zero matrices / non-finite residuals set the status word.
+ * params and ortho_out must not overlap. */
+orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* ortho_out, float* power_cache,
+                                 float* residual_out, void* stream);
+
+/* a4+a5.  ortho: the output of orth_orthogonalize.  kernels_f32: receives each
+ * layer owned by this rank at ORTH_Q_LAYER_KERNEL_OFF_F32 in PyTorch weight
+ * layout (Conv2d: (c_out, c_in/g, k, k); ConvTranspose2d: (c_in, c_out/g, k, k);
+ * dense: (c_out, c_in)).  kernels_bf16: nullable; receives the GEMM layout
+ * (C_o, k, k, C_i/g) of the forward conv, RNE-rounded, at
+ * ORTH_Q_LAYER_KERNEL_OFF_BF16.  Segments are rank-major (R22). */
+orth_status_t orth_compose_kernel(orth_plan_t plan, const float* ortho, float* kernels_f32, void* kernels_bf16,
+                                  void* stream);
+
+/* a6.  Applies the conv of layer `layer`'s kernel: input (N, H, W, C_i) NHWC
+ * -> output (N, H_out, W_out, C_o), H_out = floor((H + p_t + p_b - d(k-1) - 1)/s) + 1,
+ * where (C_i, C_o) = (c_in, c_out) for ORTH_CONV2D and (c_out, c_in) for
+ * ORTH_CONV_TRANSPOSE2D (whose forward adjoint this is).
+ * io = ORTH_F32: x, y float32 and `kernel` the layer's FP32 PyTorch-layout kernel;
+ * io = ORTH_BF16: x, y bfloat16 and `kernel` the layer's BF16 GEMM-layout kernel.
+ * bias: nullable FP32[C_o].  Accumulation FP32.  Circular padding requires
+ * s | H and s | W (R11).  Dense layers: ORTH_ERR_UNSUPPORTED_CONFIG. */
+orth_status_t orth_conv_forward(orth_plan_t plan, int32_t layer, const void* kernel, const float* bias,
+                                const void* x, void* y, int32_t N, int32_t H, int32_t W, int32_t io, void* stream);
+
+/* a7.  Exact adjoint of orth_conv_forward for the same layer and kernel:
+ * y_small (N, H_out, W_out, C_o) -> x_big (N, H_big, W_big, C_i).  For an
+ * ORTH_CONV_TRANSPOSE2D layer this is its forward (ConvTranspose2d); for an
+ * ORTH_CONV2D layer it is the data gradient.  The large size is explicit, so
+ * PyTorch's output_padding ambiguity does not arise.  bias: nullable FP32[C_i]. */
+orth_status_t orth_conv_transpose(orth_plan_t plan, int32_t layer, const void* kernel, const float* bias,
+                                  const void* y_small, void* x_big, int32_t N, int32_t H_big, int32_t W_big,
+                                  int32_t io, void* stream);
+
+/* Synchronises `stream`, reads and clears the device status word; returns the
+ * first device-side error since the last check (or a pending CUDA error). */
+orth_status_t orth_plan_check(orth_plan_t plan, void* stream);
+
+/* Number of kernel launches enqueued by this plan since creation (all calls). */
+int64_t orth_plan_launch_count(orth_plan_t plan);
+
+const char* orth_status_string(orth_status_t status);
+const char* orth_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ORTH_H_ */

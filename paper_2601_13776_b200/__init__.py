@@ -1,0 +1,270 @@
+"""Python binding of the C-ABI library ``liborth.so`` (include/orth.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  There is no CPU or PyTorch fallback: if the library is missing
+the import fails, and compute calls on a host-only plan raise.
+
+Module-level functions carry the ABI names (``orth_plan_create``,
+``orth_orthogonalize``, ``orth_compose_kernel``, ``orth_conv_forward``,
+``orth_conv_transpose``, ...); ``Plan`` wraps them for convenience.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, List, Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liborth.so")
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"{_LIB_PATH} is not built; run `python paper_2601_13776_b200/build.py` "
+                      "(or __graft_entry__.build()). There is no fallback path.")
+_lib = C.CDLL(_LIB_PATH)
+
+# ---------------------------------------------------------------- ABI types
+OK, INVALID_ARGUMENT, UNSUPPORTED_CONFIG, SHAPE_MISMATCH, ZERO_NORM, NOT_CONVERGED, CUDA_ERR, OOM, NO_DEVICE = range(9)
+F32, BF16 = 0, 1
+PAD_ZEROS, PAD_CIRCULAR = 0, 1
+CONV2D, CONV_TRANSPOSE2D, DENSE = 0, 1, 2
+PRESCALE_POWER, PRESCALE_FROBENIUS = 0, 1
+Q = dict(N_LAYERS=0, N_MATRICES=1, PARAMS_NUMEL=2, CACHE_NUMEL=3, KERNELS_F32_NUMEL=4, KERNELS_BF16_NUMEL=5,
+         WORKSPACE_BYTES=6, NS_FLOPS=7, KERNEL_SEGMENT_F32=8, KERNEL_SEGMENT_BF16=9,
+         LAYER_FIRST_MATRIX=20, LAYER_MATS_PER_GROUP=21, LAYER_KERNEL_OFF_F32=22, LAYER_KERNEL_OFF_BF16=23,
+         LAYER_KERNEL_NUMEL=24, LAYER_OWNER=25, LAYER_C_MID=26, LAYER_C_B=27, LAYER_KP=28,
+         MATRIX_ROWS=40, MATRIX_COLS=41, MATRIX_OFFSET=42, MATRIX_CACHE_OFFSET=43, MATRIX_LAYER=44,
+         MATRIX_GROUP=45, MATRIX_ROLE=46)
+ROLES = {0: "Q", 1: "U", 2: "R", 3: "W"}
+_KIND = {"conv": CONV2D, "convT": CONV_TRANSPOSE2D, "dense": DENSE}
+_MODE = {"zeros": PAD_ZEROS, "circular": PAD_CIRCULAR}
+
+
+class LayerDesc(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("kind", "c_in", "c_out", "k_h", "k_w", "stride_h", "stride_w", "dil_h",
+                                         "dil_w", "groups", "pad_t", "pad_b", "pad_l", "pad_r", "padding_mode")]
+
+
+class Opts(C.Structure):
+    _fields_ = [("ns_iters", C.c_int32), ("beta", C.c_float), ("prescale", C.c_int32), ("power_iters", C.c_int32),
+                ("compute", C.c_int32), ("polish_iters", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32)]
+
+
+_P = C.c_void_p
+_sig = {
+    "orth_opts_default": (None, [C.POINTER(Opts)]),
+    "orth_validate_desc": (C.c_int, [C.POINTER(LayerDesc), C.c_int32, C.POINTER(Opts)]),
+    "orth_plan_create": (C.c_int, [C.POINTER(LayerDesc), C.c_int32, C.POINTER(Opts), C.c_int32, C.POINTER(_P)]),
+    "orth_plan_destroy": (C.c_int, [_P]),
+    "orth_plan_query": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
+    "orth_orthogonalize": (C.c_int, [_P, _P, _P, _P, _P, _P]),
+    "orth_compose_kernel": (C.c_int, [_P, _P, _P, _P, _P]),
+    "orth_conv_forward": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
+    "orth_conv_transpose": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
+    "orth_plan_check": (C.c_int, [_P, _P]),
+    "orth_plan_launch_count": (C.c_int64, [_P]),
+    "orth_status_string": (C.c_char_p, [C.c_int]),
+    "orth_last_error": (C.c_char_p, []),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+EXPORTED = tuple(_sig)
+
+
+class OrthError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = _lib.orth_status_string(status).decode()
+        detail = (_lib.orth_last_error() or b"").decode()
+        super().__init__(f"{where}: {msg}: {detail}")
+
+
+def _check(st: int, where: str):
+    if st != OK:
+        raise OrthError(st, where)
+
+
+def layer_desc(d: Dict) -> LayerDesc:
+    """Marshal a synth.configs-style dict into orth_layer_desc_t."""
+    pads = d.get("pad") or (-1, -1, -1, -1)
+    k, s, dl = d.get("k", 3), d.get("s", 1), d.get("d", 1)
+    return LayerDesc(_KIND[d.get("kind", "conv")], d["c_in"], d["c_out"], k, k, s, s, dl, dl, d.get("g", 1),
+                     pads[0], pads[1], pads[2], pads[3], _MODE[d.get("padding_mode", "circular")])
+
+
+def make_opts(**kw) -> Opts:
+    o = Opts()
+    _lib.orth_opts_default(C.byref(o))
+    for k, v in kw.items():
+        if k == "compute" and isinstance(v, str):
+            v = {"f32": F32, "bf16": BF16}[v]
+        if k == "prescale" and isinstance(v, str):
+            v = {"power": PRESCALE_POWER, "frobenius": PRESCALE_FROBENIUS}[v]
+        setattr(o, k, v)
+    return o
+
+
+def orth_validate_desc(layers: Sequence[Dict], **opts) -> int:
+    arr = (LayerDesc * len(layers))(*[layer_desc(d) for d in layers])
+    o = make_opts(**opts)
+    return _lib.orth_validate_desc(arr, len(layers), C.byref(o))
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is not None:
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+def orth_plan_create(layers: Sequence[Dict], device: int = 0, **opts) -> int:
+    arr = (LayerDesc * len(layers))(*[layer_desc(d) for d in layers])
+    o = make_opts(**opts)
+    h = _P()
+    _check(_lib.orth_plan_create(arr, len(layers), C.byref(o), device, C.byref(h)), "orth_plan_create")
+    return h.value
+
+
+def orth_plan_destroy(h: int):
+    _check(_lib.orth_plan_destroy(h), "orth_plan_destroy")
+
+
+def orth_plan_query(h: int, what, index: int = 0) -> int:
+    out = C.c_int64()
+    w = Q[what] if isinstance(what, str) else what
+    _check(_lib.orth_plan_query(h, w, index, C.byref(out)), "orth_plan_query")
+    return out.value
+
+
+def orth_orthogonalize(h: int, params, ortho_out, power_cache=None, residual_out=None, stream=None):
+    _check(_lib.orth_orthogonalize(h, _ptr(params), _ptr(ortho_out), _ptr(power_cache), _ptr(residual_out),
+                                   _stream(stream)), "orth_orthogonalize")
+
+
+def orth_compose_kernel(h: int, ortho, kernels_f32, kernels_bf16=None, stream=None):
+    _check(_lib.orth_compose_kernel(h, _ptr(ortho), _ptr(kernels_f32), _ptr(kernels_bf16), _stream(stream)),
+           "orth_compose_kernel")
+
+
+def orth_conv_forward(h: int, layer: int, kernel, x, y, N: int, H: int, W: int, io: int, bias=None, stream=None):
+    _check(_lib.orth_conv_forward(h, layer, _ptr(kernel), _ptr(bias), _ptr(x), _ptr(y), N, H, W, io,
+                                  _stream(stream)), "orth_conv_forward")
+
+
+def orth_conv_transpose(h: int, layer: int, kernel, y_small, x_big, N: int, H_big: int, W_big: int, io: int,
+                        bias=None, stream=None):
+    _check(_lib.orth_conv_transpose(h, layer, _ptr(kernel), _ptr(bias), _ptr(y_small), _ptr(x_big), N, H_big, W_big,
+                                    io, _stream(stream)), "orth_conv_transpose")
+
+
+def orth_plan_check(h: int, stream=None):
+    _check(_lib.orth_plan_check(h, _stream(stream)), "orth_plan_check (device status)")
+
+
+def orth_plan_launch_count(h: int) -> int:
+    return _lib.orth_plan_launch_count(h)
+
+
+def out_size(H: int, k: int, s: int, d: int, p0: int, p1: int) -> int:
+    return (H + p0 + p1 - d * (k - 1) - 1) // s + 1
+
+
+class Plan:
+    """Owns an orth_plan_t.  ``layers``: synth.configs-style dicts."""
+
+    def __init__(self, layers: Sequence[Dict], device: int = 0, **opts):
+        self.layers = [dict(d) for d in layers]
+        self.device = device
+        self.h = orth_plan_create(self.layers, device, **opts)
+        q = lambda w, i=0: orth_plan_query(self.h, w, i)
+        self.n_layers = q("N_LAYERS")
+        self.n_matrices = q("N_MATRICES")
+        self.params_numel = q("PARAMS_NUMEL")
+        self.cache_numel = q("CACHE_NUMEL")
+        self.kf32_numel = q("KERNELS_F32_NUMEL")
+        self.kbf16_numel = q("KERNELS_BF16_NUMEL")
+        self.workspace_bytes = q("WORKSPACE_BYTES")
+        self.ns_flops = q("NS_FLOPS")
+        self.matrices = [dict(m=q("MATRIX_ROWS", i), n=q("MATRIX_COLS", i), off=q("MATRIX_OFFSET", i),
+                              cache_off=q("MATRIX_CACHE_OFFSET", i), layer=q("MATRIX_LAYER", i),
+                              group=q("MATRIX_GROUP", i), role=ROLES[q("MATRIX_ROLE", i)])
+                         for i in range(self.n_matrices)]
+        self.layer_info = [dict(first_matrix=q("LAYER_FIRST_MATRIX", l), mats_per_group=q("LAYER_MATS_PER_GROUP", l),
+                                kf32_off=q("LAYER_KERNEL_OFF_F32", l), kbf16_off=q("LAYER_KERNEL_OFF_BF16", l),
+                                numel=q("LAYER_KERNEL_NUMEL", l), owner=q("LAYER_OWNER", l),
+                                c_mid=q("LAYER_C_MID", l), c_b=q("LAYER_C_B", l), kp=q("LAYER_KP", l))
+                           for l in range(self.n_layers)]
+
+    # -- shapes ---------------------------------------------------------
+    def fwd_channels(self, l: int):
+        d = self.layers[l]
+        return (d["c_out"], d["c_in"]) if d.get("kind") == "convT" else (d["c_in"], d["c_out"])
+
+    def kernel_shape(self, l: int):
+        d = self.layers[l]
+        if d.get("kind") == "dense":
+            return (d["c_out"], d["c_in"])
+        ci, co = self.fwd_channels(l)
+        return (co, ci // d.get("g", 1), d.get("k", 3), d.get("k", 3))
+
+    def kernel_f32(self, kf32, l: int):
+        info = self.layer_info[l]
+        return kf32[info["kf32_off"]: info["kf32_off"] + info["numel"]].view(self.kernel_shape(l))
+
+    def kernel_bf16(self, kbf16, l: int):
+        info = self.layer_info[l]
+        sh = self.kernel_shape(l)
+        v = kbf16[info["kbf16_off"]: info["kbf16_off"] + info["numel"]]
+        return v.view(sh) if len(sh) == 2 else v.view(sh[0], sh[2], sh[3], sh[1])
+
+    def out_hw(self, l: int, H: int, W: int):
+        d = self.layers[l]
+        k, s, dl = d.get("k", 3), d.get("s", 1), d.get("d", 1)
+        pads = d.get("pad")
+        if pads is None:
+            e = dl * (k - 1)
+            pads = (e // 2, e - e // 2, e // 2, e - e // 2)
+        return out_size(H, k, s, dl, pads[0], pads[1]), out_size(W, k, s, dl, pads[2], pads[3])
+
+    # -- compute ----------------------------------------------------------
+    def orthogonalize(self, params, ortho_out, power_cache=None, residual_out=None, stream=None):
+        orth_orthogonalize(self.h, params, ortho_out, power_cache, residual_out, stream)
+
+    def compose(self, ortho, kernels_f32, kernels_bf16=None, stream=None):
+        orth_compose_kernel(self.h, ortho, kernels_f32, kernels_bf16, stream)
+
+    def conv_forward(self, l: int, kernel, x, y, bias=None, stream=None):
+        """x: NHWC (N, H, W, C_i) float32 or bfloat16 CUDA tensor; y preallocated."""
+        io = BF16 if str(x.dtype) == "torch.bfloat16" else F32
+        N, H, W, _ = x.shape
+        orth_conv_forward(self.h, l, kernel, x, y, N, H, W, io, bias, stream)
+
+    def conv_transpose(self, l: int, kernel, y_small, x_big, bias=None, stream=None):
+        io = BF16 if str(y_small.dtype) == "torch.bfloat16" else F32
+        N, H, W, _ = x_big.shape
+        orth_conv_transpose(self.h, l, kernel, y_small, x_big, N, H, W, io, bias, stream)
+
+    def check(self, stream=None):
+        orth_plan_check(self.h, stream)
+
+    @property
+    def launches(self) -> int:
+        return orth_plan_launch_count(self.h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            orth_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

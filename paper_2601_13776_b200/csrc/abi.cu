@@ -1,0 +1,156 @@
+// Compute entry points of the C ABI (include/orth.h).  Each validates
+// synchronously, then enqueues its kernels on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "orth_internal.h"
+
+using namespace orth;
+
+namespace {
+
+orth_status_t cuda_fail(int e, const char* where) {
+  if (e == 0) return ORTH_OK;
+  set_error("%s: %s", where, cudaGetErrorString((cudaError_t)e));
+  return ORTH_ERR_CUDA;
+}
+
+orth_status_t need_device(orth_plan_t plan) {
+  if (!plan) { set_error("NULL plan"); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (plan->p.device < 0) { set_error("host-only plan (device = -1) cannot compute"); return ORTH_ERR_NO_DEVICE; }
+  return ORTH_OK;
+}
+
+int out_dim(int H, int k, int s, int d, int p0, int p1) { return (H + p0 + p1 - d * (k - 1) - 1) / s + 1; }
+
+orth_status_t check_conv(Plan& P, int32_t layer, const void* kernel, const void* in, void* out, int N, int H, int W,
+                         int io, int& Ho, int& Wo) {
+  if (layer < 0 || layer >= (int)P.layers.size()) { set_error("layer %d out of range", layer); return ORTH_ERR_INVALID_ARGUMENT; }
+  const LayerInfo& L = P.layers[layer];
+  if (L.cons == CONS_DENSE) { set_error("dense layers have no conv forward (plain GEMM, out of scope)"); return ORTH_ERR_UNSUPPORTED_CONFIG; }
+  if (!kernel || !in || !out) { set_error("NULL kernel/input/output"); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (io != ORTH_F32 && io != ORTH_BF16) { set_error("bad io dtype %d", io); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (N < 1 || H < 1 || W < 1) { set_error("N, H, W must be >= 1"); return ORTH_ERR_SHAPE_MISMATCH; }
+  const int num = H + L.pt + L.pb - L.d * (L.k - 1) - 1, numw = W + L.pl + L.pr - L.d * (L.k - 1) - 1;
+  if (num < 0 || numw < 0) { set_error("input %dx%d smaller than the dilated kernel", H, W); return ORTH_ERR_SHAPE_MISMATCH; }
+  Ho = out_dim(H, L.k, L.s, L.d, L.pt, L.pb);
+  Wo = out_dim(W, L.k, L.s, L.d, L.pl, L.pr);
+  if (L.desc.padding_mode == ORTH_PAD_CIRCULAR && (H % L.s || W % L.s)) {
+    set_error("circular padding needs s | H and s | W (s=%d, H=%d, W=%d; reading R11)", L.s, H, W);
+    return ORTH_ERR_SHAPE_MISMATCH;
+  }
+  if (((uintptr_t)in | (uintptr_t)out | (uintptr_t)kernel) & 15) { set_error("buffers must be 16-byte aligned"); return ORTH_ERR_INVALID_ARGUMENT; }
+  return ORTH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* ortho_out, float* power_cache,
+                                 float* residual_out, void* stream) {
+  orth_status_t st = need_device(plan);
+  if (st != ORTH_OK) return st;
+  Plan& P = plan->p;
+  if (!params || !ortho_out) { set_error("NULL params or ortho_out"); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (params == ortho_out) { set_error("params and ortho_out must not overlap"); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (P.opts.compute != ORTH_F32) {
+    set_error("compute = BF16 tensor-core NS is not built into this library version");
+    return ORTH_ERR_UNSUPPORTED_CONFIG;
+  }
+  if (P.mat_items.empty()) return ORTH_OK;
+  const int T = P.opts.ns_iters;
+  float* bufs[BUF_COUNT] = {ortho_out, P.d_scratch, P.d_gram, P.d_comp};
+  // X0 goes where T swaps leave the result in ortho_out
+  int par = (T % 2 == 0) ? 0 : 1;      // 0: X lives in BUF_X
+  float* x0 = bufs[par == 0 ? BUF_X : BUF_Y];
+  const int frob = P.opts.prescale == ORTH_PRESCALE_FROBENIUS;
+  int e = 0;
+  if (frob) {
+    e = launch_power_partial(P, params, nullptr, 1, 1, stream);
+    if (!e) e = launch_power_finalize(P, nullptr, 1, 0, stream);
+  } else {
+    const int Pn = P.opts.power_iters;
+    for (int it = 0; it < Pn && !e; ++it) {
+      const float* vin = it == 0 ? power_cache : P.d_vbuf;
+      e = launch_power_partial(P, params, vin, (it == 0 && !power_cache) ? 1 : 0, 0, stream);
+      if (!e) e = launch_power_finalize(P, (it == Pn - 1) ? power_cache : nullptr, 0, 0, stream);
+    }
+  }
+  if (!e) e = launch_scale(P, params, x0, stream);
+  for (int t = 0; t < T && !e; ++t) {
+    e = launch_gemm_f32(P.gram[par], bufs, stream);
+    P.launches++;
+    if (!e) e = launch_gemm_f32(P.update[par], bufs, stream);
+    P.launches++;
+    par ^= 1;
+  }
+  if (!e && residual_out) {
+    e = launch_gemm_f32(P.gram[0], bufs, stream);
+    P.launches++;
+    if (!e) e = launch_residual(P, residual_out, stream);
+  }
+  return cuda_fail(e, "orth_orthogonalize");
+}
+
+orth_status_t orth_compose_kernel(orth_plan_t plan, const float* ortho, float* kernels_f32, void* kernels_bf16,
+                                  void* stream) {
+  orth_status_t st = need_device(plan);
+  if (st != ORTH_OK) return st;
+  Plan& P = plan->p;
+  if (!ortho || !kernels_f32) { set_error("NULL ortho or kernels_f32"); return ORTH_ERR_INVALID_ARGUMENT; }
+  float* bufs[BUF_COUNT] = {const_cast<float*>(ortho), nullptr, nullptr, P.d_comp};
+  int e = 0;
+  if (P.proj.total_tiles) { e = launch_gemm_f32(P.proj, bufs, stream); P.launches++; }
+  for (auto& ph : P.chain) {
+    if (e) break;
+    if (ph.total_tiles) { e = launch_gemm_f32(ph, bufs, stream); P.launches++; }
+  }
+  if (!e && P.aoc.total_tiles) { e = launch_gemm_f32(P.aoc, bufs, stream); P.launches++; }
+  if (!e) e = launch_emit(P, bufs, kernels_f32, (uint16_t*)kernels_bf16, stream);
+  return cuda_fail(e, "orth_compose_kernel");
+}
+
+orth_status_t orth_conv_forward(orth_plan_t plan, int32_t layer, const void* kernel, const float* bias, const void* x,
+                                void* y, int32_t N, int32_t H, int32_t W, int32_t io, void* stream) {
+  orth_status_t st = need_device(plan);
+  if (st != ORTH_OK) return st;
+  Plan& P = plan->p;
+  int Ho = 0, Wo = 0;
+  st = check_conv(P, layer, kernel, x, y, N, H, W, io, Ho, Wo);
+  if (st != ORTH_OK) return st;
+  const int e = launch_conv_fwd(P.layers[layer], kernel, bias, x, y, N, H, W, Ho, Wo, io, stream);
+  P.launches++;
+  return cuda_fail(e, "orth_conv_forward");
+}
+
+orth_status_t orth_conv_transpose(orth_plan_t plan, int32_t layer, const void* kernel, const float* bias,
+                                  const void* y_small, void* x_big, int32_t N, int32_t H_big, int32_t W_big, int32_t io,
+                                  void* stream) {
+  orth_status_t st = need_device(plan);
+  if (st != ORTH_OK) return st;
+  Plan& P = plan->p;
+  int Ho = 0, Wo = 0;
+  st = check_conv(P, layer, kernel, y_small, x_big, N, H_big, W_big, io, Ho, Wo);
+  if (st != ORTH_OK) return st;
+  const int e = launch_conv_bwd(P.layers[layer], kernel, bias, y_small, x_big, N, H_big, W_big, Ho, Wo, io, stream);
+  P.launches++;
+  return cuda_fail(e, "orth_conv_transpose");
+}
+
+orth_status_t orth_plan_check(orth_plan_t plan, void* stream) {
+  orth_status_t st = need_device(plan);
+  if (st != ORTH_OK) return st;
+  Plan& P = plan->p;
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail((int)e, "orth_plan_check");
+  int32_t h = 0;
+  e = cudaMemcpy(&h, P.d_status, sizeof(h), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(P.d_status, 0, sizeof(int32_t));
+  if (e != cudaSuccess) return cuda_fail((int)e, "orth_plan_check");
+  if (h != 0) set_error("device status %d", h);
+  return (orth_status_t)h;
+}
+
+}  // extern "C"

@@ -1,0 +1,242 @@
+// a6/a7 SIMT implicit-GEMM convolution (first CUDA path; FP32 accumulation).
+//
+// Forward:
+//   y[n,u,v,o] = sum_{a,b,c} K[o,c,a,b] x~[n, s u + d a - p_t, s v + d b - p_l, g*ci_g + c]
+// Adjoint / transposed (R13/R14), gather form:
+//   x[n,h,w,i] = sum_{a,b,o} K[o,i,a,b] y[n,u,v,o] over the (u,v) with
+//   s u + d a - p_t == h (mod H for circular, exactly for zero padding).
+// Activations are NHWC; bf16 I/O reads the BF16 GEMM-layout kernel
+// (C_o, k, k, C_i/g), f32 I/O the FP32 PyTorch-layout kernel (C_o, C_i/g, k, k).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "orth_internal.h"
+
+namespace orth {
+namespace {
+
+struct ConvArgs {
+  int N, H, W, Ci, Co, ci_g, co_g, k, s, d, pt, pl, Ho, Wo, circ;
+};
+
+template <typename T> __device__ __forceinline__ float ld(const T* p);
+template <> __device__ __forceinline__ float ld<float>(const float* p) { return *p; }
+template <> __device__ __forceinline__ float ld<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+template <typename T> __device__ __forceinline__ void st(T* p, float v);
+template <> __device__ __forceinline__ void st<float>(float* p, float v) { *p = v; }
+template <> __device__ __forceinline__ void st<__nv_bfloat16>(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+__device__ __forceinline__ int wrap(int x, int n) { x %= n; return x < 0 ? x + n : x; }
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+// T: activation type; W: kernel element type (bf16 -> GEMM layout, float -> canonical)
+template <typename T, typename Wt>
+__global__ void __launch_bounds__(256) conv_fwd_simt(const T* __restrict__ x, const Wt* __restrict__ wt,
+                                                     const float* __restrict__ bias, T* __restrict__ y, ConvArgs a) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  __shared__ int pn[BM], ph[BM], pw[BM];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int g = blockIdx.z;
+  const int64_t M = (int64_t)a.N * a.Ho * a.Wo;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+  if (tid < BM) {
+    const int64_t m = m0 + tid;
+    if (m < M) {
+      const int64_t hw = (int64_t)a.Ho * a.Wo;
+      const int n = (int)(m / hw), r = (int)(m % hw);
+      pn[tid] = n; ph[tid] = (r / a.Wo) * a.s - a.pt; pw[tid] = (r % a.Wo) * a.s - a.pl;
+    } else {
+      pn[tid] = -1; ph[tid] = 0; pw[tid] = 0;
+    }
+  }
+  __syncthreads();
+  float acc[4][4] = {};
+  const int kk2 = a.k * a.k;
+  for (int tap = 0; tap < kk2; ++tap) {
+    const int ta = tap / a.k, tb = tap % a.k;
+    for (int c0 = 0; c0 < a.ci_g; c0 += BK) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int e = tid + t * 256, kk = e % BK, i = e / BK;
+        float v = 0.f;
+        const int n = pn[i];
+        if (n >= 0 && c0 + kk < a.ci_g) {
+          int h = ph[i] + a.d * ta, w = pw[i] + a.d * tb;
+          bool ok = true;
+          if (a.circ) { h = wrap(h, a.H); w = wrap(w, a.W); }
+          else ok = h >= 0 && h < a.H && w >= 0 && w < a.W;
+          if (ok) v = ld(x + (((int64_t)n * a.H + h) * a.W + w) * a.Ci + g * a.ci_g + c0 + kk);
+        }
+        As[kk][i] = v;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int e = tid + t * 256, kk = e % BK, j = e / BK;
+        float v = 0.f;
+        const int oc = n0 + j, c = c0 + kk;
+        if (oc < a.co_g && c < a.ci_g) {
+          const int64_t o = (int64_t)g * a.co_g + oc;
+          if (sizeof(Wt) == 2) v = ld(wt + (o * kk2 + tap) * a.ci_g + c);
+          else v = ld(wt + (o * a.ci_g + c) * kk2 + tap);
+        }
+        Bs[kk][j] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        const float4 av = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+        const float4 bv = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+        const float aa[4] = {av.x, av.y, av.z, av.w}, bb[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(aa[i], bb[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int oc = n0 + tx * 4 + j;
+      if (oc >= a.co_g) continue;
+      const int o = g * a.co_g + oc;
+      float v = acc[i][j];
+      if (bias) v += bias[o];
+      st(y + m * a.Co + o, v);
+    }
+  }
+}
+
+// adjoint: output pixels over the big grid, reduction over (tap, o)
+template <typename T, typename Wt>
+__global__ void __launch_bounds__(256) conv_bwd_simt(const T* __restrict__ yv, const Wt* __restrict__ wt,
+                                                     const float* __restrict__ bias, T* __restrict__ x, ConvArgs a) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  __shared__ int pn[BM], ph[BM], pw[BM];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int g = blockIdx.z;
+  const int64_t M = (int64_t)a.N * a.H * a.W;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+  if (tid < BM) {
+    const int64_t m = m0 + tid;
+    if (m < M) {
+      const int64_t hw = (int64_t)a.H * a.W;
+      const int n = (int)(m / hw), r = (int)(m % hw);
+      pn[tid] = n; ph[tid] = r / a.W + a.pt; pw[tid] = r % a.W + a.pl;
+    } else {
+      pn[tid] = -1; ph[tid] = 0; pw[tid] = 0;
+    }
+  }
+  __syncthreads();
+  float acc[4][4] = {};
+  const int kk2 = a.k * a.k;
+  for (int tap = 0; tap < kk2; ++tap) {
+    const int ta = tap / a.k, tb = tap % a.k;
+    for (int c0 = 0; c0 < a.co_g; c0 += BK) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int e = tid + t * 256, kk = e % BK, i = e / BK;
+        float v = 0.f;
+        const int n = pn[i];
+        if (n >= 0 && c0 + kk < a.co_g) {
+          int th = ph[i] - a.d * ta, tw = pw[i] - a.d * tb;
+          if (a.circ) { th = wrap(th, a.H); tw = wrap(tw, a.W); }
+          bool ok = th >= 0 && tw >= 0 && (th % a.s) == 0 && (tw % a.s) == 0;
+          const int u = th / a.s, vv = tw / a.s;
+          ok = ok && u < a.Ho && vv < a.Wo;
+          if (ok) v = ld(yv + (((int64_t)n * a.Ho + u) * a.Wo + vv) * a.Co + g * a.co_g + c0 + kk);
+        }
+        As[kk][i] = v;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int e = tid + t * 256, j = e % BN, kk = e / BN;
+        float v = 0.f;
+        const int ic = n0 + j, oc = c0 + kk;
+        if (ic < a.ci_g && oc < a.co_g) {
+          const int64_t o = (int64_t)g * a.co_g + oc;
+          if (sizeof(Wt) == 2) v = ld(wt + (o * kk2 + tap) * a.ci_g + ic);
+          else v = ld(wt + (o * a.ci_g + ic) * kk2 + tap);
+        }
+        Bs[kk][j] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        const float4 av = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+        const float4 bv = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+        const float aa[4] = {av.x, av.y, av.z, av.w}, bb[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(aa[i], bb[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int ic = n0 + tx * 4 + j;
+      if (ic >= a.ci_g) continue;
+      const int c = g * a.ci_g + ic;
+      float v = acc[i][j];
+      if (bias) v += bias[c];
+      st(x + m * a.Ci + c, v);
+    }
+  }
+}
+
+ConvArgs make_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo) {
+  ConvArgs a;
+  a.N = N; a.H = H; a.W = W; a.Ci = L.ci_f; a.Co = L.co_f; a.ci_g = L.ci; a.co_g = L.co;
+  a.k = L.k; a.s = L.s; a.d = L.d; a.pt = L.pt; a.pl = L.pl; a.Ho = Ho; a.Wo = Wo;
+  a.circ = L.desc.padding_mode == ORTH_PAD_CIRCULAR;
+  return a;
+}
+
+}  // namespace
+
+int launch_conv_fwd(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N, int H,
+                    int W, int Ho, int Wo, int io, void* stream) {
+  const ConvArgs a = make_args(L, N, H, W, Ho, Wo);
+  const int64_t M = (int64_t)N * Ho * Wo;
+  dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((L.co + BN - 1) / BN), (unsigned)L.g);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (io == ORTH_BF16)
+    conv_fwd_simt<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, s>>>(
+        (const __nv_bfloat16*)x, (const __nv_bfloat16*)kernel, bias, (__nv_bfloat16*)y, a);
+  else
+    conv_fwd_simt<float, float><<<grid, 256, 0, s>>>((const float*)x, (const float*)kernel, bias, (float*)y, a);
+  return (int)cudaGetLastError();
+}
+
+int launch_conv_bwd(const LayerInfo& L, const void* kernel, const float* bias, const void* y, void* x, int N, int H,
+                    int W, int Ho, int Wo, int io, void* stream) {
+  const ConvArgs a = make_args(L, N, H, W, Ho, Wo);
+  const int64_t M = (int64_t)N * H * W;
+  dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((L.ci + BN - 1) / BN), (unsigned)L.g);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (io == ORTH_BF16)
+    conv_bwd_simt<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, s>>>(
+        (const __nv_bfloat16*)y, (const __nv_bfloat16*)kernel, bias, (__nv_bfloat16*)x, a);
+  else
+    conv_bwd_simt<float, float><<<grid, 256, 0, s>>>((const float*)y, (const float*)kernel, bias, (float*)x, a);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace orth

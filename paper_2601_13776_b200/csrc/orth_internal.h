@@ -1,0 +1,155 @@
+// Internal plan structures shared by the host planner (plan.cpp) and the CUDA
+// translation units.  Not part of the ABI (include/orth.h is).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/orth.h"
+
+namespace orth {
+
+enum Role : int32_t { ROLE_Q = 0, ROLE_U = 1, ROLE_R = 2, ROLE_W = 3 };
+enum Construct : int32_t { CONS_BCOP = 0, CONS_RKO = 1, CONS_AOC = 2, CONS_DENSE = 3 };
+enum BufId : int32_t { BUF_NONE = -1, BUF_X = 0, BUF_Y = 1, BUF_G = 2, BUF_W = 3, BUF_COUNT = 4 };
+
+constexpr int kPadF32 = 32;    // 128 B alignment of every packed float object
+constexpr int kPadBF16 = 64;   // 128 B alignment of every packed bf16 object
+
+inline int64_t pad_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct MatInfo {
+  int32_t layer, group, role;
+  int64_t m, n;
+  int64_t off;        // float offset in params / ortho / scratch
+  int64_t cache_off;  // float offset in power cache / v workspace
+  int64_t gram_off;   // float offset of its short-side Gram in the G workspace
+  int32_t owned;      // 1 if this rank orthogonalises it
+};
+
+struct LayerInfo {
+  orth_layer_desc_t desc;
+  int32_t cons;                 // Construct
+  int32_t ci_f, co_f;           // forward-conv channels (swapped for transposed, R13)
+  int32_t ci, co;               // per group
+  int32_t k, s, d, g;
+  int32_t pt, pb, pl, pr;
+  int32_t kp, c_b, c_mid;
+  int32_t first_mat, mats_per_group;
+  int32_t owner;
+  int64_t kf32_off, kbf16_off, kernel_numel;
+  double ns_flops, comp_flops;
+};
+
+// D[M x N] (+)= alpha * sum_seg opA(seg)[M x K] * opB(seg)[K x N] + beta * C.
+// Element (i,k) of A at bufs[a_buf][a_off + i*sa_m + k*sa_k] (minus the same
+// element of A2 when a2_off >= 0).  Offsets are relative to base pointers the
+// kernel receives, so descriptors are built once at plan creation.
+struct GemmSeg {
+  int64_t a_off, a2_off, b_off;
+};
+struct GemmDesc {
+  int32_t M, N, K;
+  int32_t a_buf, b_buf, c_buf, d_buf;
+  int64_t sa_m, sa_k, sb_k, sb_n;
+  int64_t c_off, ldc, d_off, ldd;
+  float alpha, beta;
+  int32_t seg_begin, seg_count;
+  int32_t tile_begin;   // first global tile of this problem
+  int32_t tiles_n;      // tiles along N
+};
+
+struct GemmPhase {        // one launch: a batch of independent problems
+  std::vector<GemmDesc> descs;
+  std::vector<GemmSeg> segs;
+  int32_t total_tiles = 0;
+  // device copies (inside the plan's descriptor arena)
+  GemmDesc* d_descs = nullptr;
+  GemmSeg* d_segs = nullptr;
+};
+
+struct PowerItem {        // one CTA of the pre-scaling kernels: rows [r0, r1) of matrix `mat`
+  int32_t mat, r0, r1, chunk;   // chunk: global partial slot
+  int32_t n, pad_;
+  int64_t off, cache_off;
+};
+
+struct MatItem {          // one owned, non-empty matrix (finalize / residual kernels)
+  int32_t mat, m, n, chunk0, nchunks, pad_;
+  int64_t off, cache_off, gram_off;
+};
+
+struct EmitItem {         // one (layer, group): copy the unit kernel into both layouts
+  int32_t layer, group;
+  int32_t src_buf;          // BUF_* base of the source
+  int64_t src_off;
+  int32_t mode;             // 0 tap-major (tap stride, ld), 1 RKO reshape
+  int64_t tap_stride, ld;
+  int32_t co, ci, k, s;
+  int64_t f32_off, bf16_off; // of the group's first output channel
+  int32_t ci_f_per_g;        // == ci
+};
+
+struct Plan {
+  std::vector<LayerInfo> layers;
+  std::vector<MatInfo> mats;
+  orth_opts_t opts;
+  int32_t device = -1;
+
+  int64_t params_numel = 0, cache_numel = 0, gram_numel = 0;
+  int64_t kf32_numel = 0, kbf16_numel = 0, seg_f32 = 0, seg_bf16 = 0;
+  int64_t comp_numel = 0;          // chain / projector / final workspace floats
+  int64_t partial_numel = 0;
+  int32_t n_chunks = 0;
+  double ns_flops = 0.0;
+
+  // NS phases (built once): gram and update per parity of the X buffer
+  GemmPhase gram[2], update[2];     // [0]: X in BUF_X -> out BUF_Y ; [1]: X in BUF_Y -> out BUF_X
+  std::vector<PowerItem> power_items;
+  std::vector<int32_t> owned_mats;  // indices of owned, non-empty matrices
+  std::vector<MatItem> mat_items;   // same order as owned_mats
+
+  // composition phases
+  GemmPhase proj;                   // P_j = U_j U_j^T
+  std::vector<GemmPhase> chain;     // 2(k'-1) substeps, batched over units
+  GemmPhase aoc;                    // RKO (*) BCOP
+  std::vector<EmitItem> emit;
+  int64_t comp_proj_off = 0, comp_ping_off = 0, comp_pong_off = 0, comp_final_off = 0;
+
+  // device allocations
+  void* d_arena = nullptr;          // one cudaMalloc for everything
+  size_t arena_bytes = 0;
+  float* d_scratch = nullptr;       // NS ping-pong partner (params_numel)
+  float* d_gram = nullptr;
+  float* d_vbuf = nullptr;
+  float* d_sigma = nullptr;
+  float* d_partial = nullptr;       // n_chunks * (max n + 1)
+  float* d_comp = nullptr;
+  int32_t* d_status = nullptr;
+  PowerItem* d_power_items = nullptr;
+  MatItem* d_mat_items = nullptr;
+  EmitItem* d_emit = nullptr;
+  int64_t partial_stride = 0;
+  int64_t launches = 0;
+};
+
+void set_error(const char* fmt, ...);
+
+// kernel launchers (CUDA translation units); return 0 or a cudaError_t value
+int launch_gemm_f32(const GemmPhase& ph, float* const bufs[BUF_COUNT], void* stream);
+int launch_power_partial(Plan& p, const float* W, const float* v_in, int use_const_v, int frob, void* stream);
+int launch_power_finalize(Plan& p, float* v_out, int frob, int write_sigma_only, void* stream);
+int launch_scale(Plan& p, const float* W, float* X0, void* stream);
+int launch_residual(Plan& p, float* residual_out, void* stream);
+int launch_emit(Plan& p, const float* const bufs[BUF_COUNT], float* kf32, uint16_t* kbf16, void* stream);
+int launch_conv_fwd(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N, int H,
+                    int W, int Ho, int Wo, int io, void* stream);
+int launch_conv_bwd(const LayerInfo& L, const void* kernel, const float* bias, const void* y, void* x, int N, int H,
+                    int W, int Ho, int Wo, int io, void* stream);
+
+}  // namespace orth
+
+struct orth_plan {
+  orth::Plan p;
+};

@@ -1,0 +1,622 @@
+// Host planner of the C ABI (include/orth.h): validation, unit derivation
+// (SURVEY §8(a) a1), packed layouts, construction sharding, GEMM/tile
+// descriptors of every phase, one-shot workspace allocation, queries.
+//
+// The derivation follows P:323-338 (AOC = RKO (*) K_BCOP, k >= s) with the
+// readings R5-R8 of DESIGN.md: s == 1 -> BCOP at width max(ci, co), k' = k;
+// k == s > 1 -> RKO only; k > s > 1 -> k' = k - s + 1,
+// c_mid = max(ci, floor(co / s^2)), BCOP at width c_mid.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+
+#include "orth_internal.h"
+
+namespace orth {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static int gcd_i(int a, int b) { return b == 0 ? a : gcd_i(b, a % b); }
+
+static orth_status_t validate_opts(const orth_opts_t& o) {
+  if (o.ns_iters < 1) { set_error("ns_iters must be >= 1 (got %d)", o.ns_iters); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (!(o.beta > 0.0f && o.beta <= 0.5f)) { set_error("beta must be in (0, 1/2] (P:311), got %g", o.beta); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (o.prescale != ORTH_PRESCALE_POWER && o.prescale != ORTH_PRESCALE_FROBENIUS) { set_error("bad prescale %d", o.prescale); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (o.prescale == ORTH_PRESCALE_POWER && o.power_iters < 1) { set_error("power_iters must be >= 1"); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (o.compute != ORTH_F32 && o.compute != ORTH_BF16) { set_error("bad compute dtype %d", o.compute); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (o.polish_iters < 0 || o.polish_iters > o.ns_iters) { set_error("polish_iters must be in [0, ns_iters]"); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (o.world < 1 || o.rank < 0 || o.rank >= o.world) { set_error("bad rank/world %d/%d", o.rank, o.world); return ORTH_ERR_INVALID_ARGUMENT; }
+  return ORTH_OK;
+}
+
+static orth_status_t validate_layer(const orth_layer_desc_t& L, int idx) {
+  if (L.kind < 0 || L.kind > 2) { set_error("layer %d: bad kind %d", idx, L.kind); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (L.c_in < 1 || L.c_out < 1 || L.k_h < 1 || L.k_w < 1 || L.stride_h < 1 || L.stride_w < 1 || L.dil_h < 1 ||
+      L.dil_w < 1 || L.groups < 1) {
+    set_error("layer %d: every dimension must be >= 1 (S:31)", idx);
+    return ORTH_ERR_INVALID_ARGUMENT;
+  }
+  if (L.c_in % L.groups || L.c_out % L.groups) {
+    set_error("layer %d: groups %d must divide c_in %d and c_out %d (S:38)", idx, L.groups, L.c_in, L.c_out);
+    return ORTH_ERR_INVALID_ARGUMENT;
+  }
+  if (L.padding_mode != ORTH_PAD_ZEROS && L.padding_mode != ORTH_PAD_CIRCULAR) {
+    set_error("layer %d: bad padding_mode %d", idx, L.padding_mode);
+    return ORTH_ERR_INVALID_ARGUMENT;
+  }
+  const bool all_def = L.pad_t == -1 && L.pad_b == -1 && L.pad_l == -1 && L.pad_r == -1;
+  const bool all_set = L.pad_t >= 0 && L.pad_b >= 0 && L.pad_l >= 0 && L.pad_r >= 0;
+  if (!all_def && !all_set) { set_error("layer %d: pads must be all -1 (same rule) or all >= 0", idx); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (L.kind == ORTH_DENSE) {
+    if (L.k_h != 1 || L.k_w != 1 || L.stride_h != 1 || L.stride_w != 1 || L.dil_h != 1 || L.dil_w != 1 || L.groups != 1) {
+      set_error("layer %d: dense layers need k = s = d = g = 1", idx);
+      return ORTH_ERR_INVALID_ARGUMENT;
+    }
+    return ORTH_OK;
+  }
+  if (L.k_h != L.k_w || L.stride_h != L.stride_w || L.dil_h != L.dil_w) {
+    set_error("layer %d: only square kernel/stride/dilation are supported", idx);
+    return ORTH_ERR_UNSUPPORTED_CONFIG;
+  }
+  if (L.k_h < L.stride_h) {
+    set_error("layer %d: k = %d < s = %d has no orthogonal AOC kernel (P:330)", idx, L.k_h, L.stride_h);
+    return ORTH_ERR_UNSUPPORTED_CONFIG;
+  }
+  if (gcd_i(L.stride_h, L.dil_h) != 1) {
+    set_error("layer %d: gcd(s=%d, d=%d) != 1 loses orthogonality (reading R10)", idx, L.stride_h, L.dil_h);
+    return ORTH_ERR_UNSUPPORTED_CONFIG;
+  }
+  return ORTH_OK;
+}
+
+static orth_status_t derive(Plan& P, const orth_layer_desc_t* layers, int n_layers) {
+  P.layers.clear();
+  P.mats.clear();
+  const int T = P.opts.ns_iters;
+  for (int l = 0; l < n_layers; ++l) {
+    LayerInfo L{};
+    L.desc = layers[l];
+    const auto& D = layers[l];
+    L.k = D.k_h; L.s = D.stride_h; L.d = D.dil_h; L.g = D.groups;
+    if (D.kind == ORTH_CONV_TRANSPOSE2D) { L.ci_f = D.c_out; L.co_f = D.c_in; }  // R13
+    else { L.ci_f = D.c_in; L.co_f = D.c_out; }
+    L.ci = L.ci_f / L.g; L.co = L.co_f / L.g;
+    if (D.pad_t == -1) {
+      const int e = L.d * (L.k - 1);
+      L.pt = L.pl = e / 2; L.pb = L.pr = e - e / 2;     // R11
+    } else { L.pt = D.pad_t; L.pb = D.pad_b; L.pl = D.pad_l; L.pr = D.pad_r; }
+    std::vector<std::pair<int, std::pair<int64_t, int64_t>>> ms;  // role, (m, n)
+    if (D.kind == ORTH_DENSE) {
+      L.cons = CONS_DENSE;
+      ms.push_back({ROLE_W, {L.co, L.ci}});
+    } else if (L.s == 1) {
+      L.cons = CONS_BCOP; L.kp = L.k; L.c_b = std::max(L.ci, L.co);
+    } else if (L.k == L.s) {
+      L.cons = CONS_RKO; L.c_mid = L.ci;
+    } else {
+      L.cons = CONS_AOC; L.kp = L.k - L.s + 1;
+      L.c_mid = std::max(L.ci, L.co / (L.s * L.s)); L.c_b = L.c_mid;
+    }
+    if (L.cons == CONS_BCOP || L.cons == CONS_AOC) {
+      ms.push_back({ROLE_Q, {L.c_b, L.c_b}});
+      for (int j = 0; j < 2 * (L.kp - 1); ++j) ms.push_back({ROLE_U, {L.c_b, L.c_b / 2}});
+    }
+    if (L.cons == CONS_RKO || L.cons == CONS_AOC) ms.push_back({ROLE_R, {L.co, (int64_t)L.c_mid * L.s * L.s}});
+    L.first_mat = (int)P.mats.size();
+    L.mats_per_group = (int)ms.size();
+    L.kernel_numel = (D.kind == ORTH_DENSE) ? (int64_t)L.co * L.ci : (int64_t)L.co_f * L.ci * L.k * L.k;
+    double fl = 0.0;
+    for (int gi = 0; gi < L.g; ++gi)
+      for (auto& e : ms) {
+        MatInfo M{};
+        M.layer = l; M.group = gi; M.role = e.first; M.m = e.second.first; M.n = e.second.second;
+        P.mats.push_back(M);
+        const double a = (double)std::max(M.m, M.n), b = (double)std::min(M.m, M.n);
+        fl += 4.0 * a * b * b * T;
+      }
+    L.ns_flops = fl;
+    // composition flops (structured chain, a4/a5; used only for load balance)
+    double cf = 0.0;
+    if (L.kp > 1) {
+      const double c = L.c_b;
+      cf += 2.0 * (L.kp - 1) * 2.0 * c * c * (c / 2);  // projectors
+      for (int j = 1; j < L.kp; ++j) cf += 2.0 * c * c * c * ((j + 1) * j + (j + 1) * (j + 1));
+    }
+    if (L.cons == CONS_AOC) cf += 2.0 * L.co * L.c_mid * L.ci * L.s * L.s * L.kp * L.kp;
+    L.comp_flops = cf * L.g;
+    P.layers.push_back(L);
+  }
+  return ORTH_OK;
+}
+
+// LPT greedy by cost over layers (R22): the largest unit to the least-loaded rank.
+static void assign_owners(Plan& P) {
+  const int R = P.opts.world;
+  std::vector<int> order(P.layers.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return P.layers[a].ns_flops + P.layers[a].comp_flops > P.layers[b].ns_flops + P.layers[b].comp_flops;
+  });
+  std::vector<double> load(R, 0.0);
+  for (int l : order) {
+    int best = 0;
+    for (int r = 1; r < R; ++r) if (load[r] < load[best]) best = r;
+    P.layers[l].owner = best;
+    load[best] += P.layers[l].ns_flops + P.layers[l].comp_flops + 1.0;
+  }
+}
+
+static void layout(Plan& P) {
+  int64_t off = 0, coff = 0, goff = 0;
+  P.ns_flops = 0.0;
+  for (auto& M : P.mats) {
+    M.off = off; off += pad_up(M.m * M.n, kPadF32);
+    M.cache_off = coff; coff += pad_up(M.n, kPadF32);
+    const int64_t s = std::min(M.m, M.n);
+    M.gram_off = goff; goff += pad_up(s * s, kPadF32);
+    M.owned = P.layers[M.layer].owner == P.opts.rank;
+    if (M.owned) {
+      const double a = (double)std::max(M.m, M.n), b = (double)s;
+      P.ns_flops += 4.0 * a * b * b * P.opts.ns_iters;
+    }
+  }
+  P.params_numel = std::max<int64_t>(off, kPadF32);
+  P.cache_numel = std::max<int64_t>(coff, kPadF32);
+  P.gram_numel = std::max<int64_t>(goff, kPadF32);
+  // rank-major kernel segments
+  const int R = P.opts.world;
+  std::vector<int64_t> s32(R, 0), s16(R, 0);
+  for (auto& L : P.layers) {
+    L.kf32_off = s32[L.owner]; s32[L.owner] += pad_up(L.kernel_numel, kPadF32);
+    L.kbf16_off = s16[L.owner]; s16[L.owner] += pad_up(L.kernel_numel, kPadBF16);
+  }
+  P.seg_f32 = std::max<int64_t>(*std::max_element(s32.begin(), s32.end()), kPadF32);
+  P.seg_bf16 = std::max<int64_t>(*std::max_element(s16.begin(), s16.end()), kPadBF16);
+  for (auto& L : P.layers) { L.kf32_off += L.owner * P.seg_f32; L.kbf16_off += L.owner * P.seg_bf16; }
+  P.kf32_numel = P.seg_f32 * R;
+  P.kbf16_numel = P.seg_bf16 * R;
+}
+
+static void finish_phase(GemmPhase& ph) {
+  int32_t t = 0;
+  for (auto& d : ph.descs) {
+    const int tm = (d.M + 63) / 64, tn = (d.N + 63) / 64;
+    d.tile_begin = t;
+    d.tiles_n = tn;
+    t += tm * tn;
+  }
+  ph.total_tiles = t;
+}
+
+static GemmDesc mk(int M, int N, int K) {
+  GemmDesc d{};
+  d.M = M; d.N = N; d.K = K;
+  d.a_buf = d.b_buf = d.c_buf = d.d_buf = BUF_NONE;
+  d.c_off = -1;
+  d.alpha = 1.0f; d.beta = 0.0f;
+  return d;
+}
+
+static void add_seg(GemmPhase& ph, GemmDesc& d, int64_t a_off, int64_t a2_off, int64_t b_off) {
+  if (d.seg_count == 0) d.seg_begin = (int32_t)ph.segs.size();
+  ph.segs.push_back(GemmSeg{a_off, a2_off, b_off});
+  d.seg_count++;
+}
+
+// NS phases: gram G = X^T X (m >= n) or X X^T, then X' = (1+b) X - b X G or (1+b) X - b G X.
+static void build_ns(Plan& P) {
+  const float b = P.opts.beta;
+  P.owned_mats.clear();
+  for (int i = 0; i < (int)P.mats.size(); ++i)
+    if (P.mats[i].owned && P.mats[i].m > 0 && P.mats[i].n > 0) P.owned_mats.push_back(i);
+  for (int par = 0; par < 2; ++par) {
+    const int xin = par == 0 ? BUF_X : BUF_Y, xout = par == 0 ? BUF_Y : BUF_X;
+    GemmPhase& g = P.gram[par];
+    GemmPhase& u = P.update[par];
+    g.descs.clear(); g.segs.clear(); u.descs.clear(); u.segs.clear();
+    for (int i : P.owned_mats) {
+      const MatInfo& M = P.mats[i];
+      const int m = (int)M.m, n = (int)M.n;
+      if (m >= n) {
+        GemmDesc d = mk(n, n, m);
+        d.a_buf = xin; d.b_buf = xin; d.d_buf = BUF_G;
+        d.sa_m = 1; d.sa_k = n; d.sb_k = n; d.sb_n = 1;
+        d.d_off = M.gram_off; d.ldd = n;
+        add_seg(g, d, M.off, -1, M.off);
+        g.descs.push_back(d);
+        GemmDesc e = mk(m, n, n);
+        e.a_buf = xin; e.b_buf = BUF_G; e.c_buf = xin; e.d_buf = xout;
+        e.sa_m = n; e.sa_k = 1; e.sb_k = n; e.sb_n = 1;
+        e.c_off = M.off; e.ldc = n; e.d_off = M.off; e.ldd = n;
+        e.alpha = -b; e.beta = 1.0f + b;
+        add_seg(u, e, M.off, -1, M.gram_off);
+        u.descs.push_back(e);
+      } else {
+        GemmDesc d = mk(m, m, n);
+        d.a_buf = xin; d.b_buf = xin; d.d_buf = BUF_G;
+        d.sa_m = n; d.sa_k = 1; d.sb_k = 1; d.sb_n = n;
+        d.d_off = M.gram_off; d.ldd = m;
+        add_seg(g, d, M.off, -1, M.off);
+        g.descs.push_back(d);
+        GemmDesc e = mk(m, n, m);
+        e.a_buf = BUF_G; e.b_buf = xin; e.c_buf = xin; e.d_buf = xout;
+        e.sa_m = m; e.sa_k = 1; e.sb_k = n; e.sb_n = 1;
+        e.c_off = M.off; e.ldc = n; e.d_off = M.off; e.ldd = n;
+        e.alpha = -b; e.beta = 1.0f + b;
+        add_seg(u, e, M.gram_off, -1, M.off);
+        u.descs.push_back(e);
+      }
+    }
+    finish_phase(g);
+    finish_phase(u);
+  }
+  // pre-scaling work items: ~4 CTAs per SM in total, split by rows
+  P.power_items.clear();
+  P.mat_items.clear();
+  double tot = 0.0;
+  int64_t maxn = 1;
+  for (int i : P.owned_mats) { tot += (double)P.mats[i].m * P.mats[i].n; maxn = std::max(maxn, P.mats[i].n); }
+  int chunk = 0;
+  for (int i : P.owned_mats) {
+    const MatInfo& M = P.mats[i];
+    const double frac = (double)M.m * M.n / std::max(tot, 1.0);
+    int64_t nc = (int64_t)std::llround(592.0 * frac);
+    nc = std::max<int64_t>(1, std::min<int64_t>(nc, M.m));
+    nc = std::max<int64_t>(nc, std::min<int64_t>(M.m, (M.m * M.n + 262143) / 262144));  // <= 256K elements per CTA
+    nc = std::max<int64_t>(nc, (M.m + 4095) / 4096);                                   // <= 4096 rows per CTA
+    const int64_t rpc = (M.m + nc - 1) / nc;
+    MatItem mi{};
+    mi.mat = i; mi.m = (int32_t)M.m; mi.n = (int32_t)M.n; mi.chunk0 = chunk;
+    mi.off = M.off; mi.cache_off = M.cache_off; mi.gram_off = M.gram_off;
+    for (int64_t r0 = 0; r0 < M.m; r0 += rpc) {
+      PowerItem it{};
+      it.mat = i; it.r0 = (int32_t)r0; it.r1 = (int32_t)std::min<int64_t>(M.m, r0 + rpc); it.chunk = chunk++;
+      it.n = (int32_t)M.n; it.off = M.off; it.cache_off = M.cache_off;
+      P.power_items.push_back(it);
+    }
+    mi.nchunks = chunk - mi.chunk0;
+    P.mat_items.push_back(mi);
+  }
+  P.n_chunks = chunk;
+  P.partial_stride = pad_up(maxn + 1, kPadF32);
+  P.partial_numel = std::max<int64_t>((int64_t)chunk * P.partial_stride, kPadF32);
+}
+
+// Composition phases (a4/a5).  Workspace (BUF_W): projectors, per-unit chain
+// ping/pong, per-unit AOC result.  Inputs come from the ortho buffer (BUF_X).
+static void build_compose(Plan& P) {
+  int64_t w = 0;
+  std::vector<int64_t> proj_off(P.mats.size(), -1);
+  P.proj = GemmPhase{};
+  P.chain.clear();
+  P.aoc = GemmPhase{};
+  P.emit.clear();
+  for (int i = 0; i < (int)P.mats.size(); ++i) {
+    const MatInfo& M = P.mats[i];
+    if (!M.owned || M.role != ROLE_U) continue;
+    proj_off[i] = w;
+    w += pad_up(M.m * M.m, kPadF32);
+    if (M.n == 0) continue;   // rank-0 projector: P = 0 (zero-filled at compose time)
+    GemmDesc d = mk((int)M.m, (int)M.m, (int)M.n);
+    d.a_buf = BUF_X; d.b_buf = BUF_X; d.d_buf = BUF_W;
+    d.sa_m = M.n; d.sa_k = 1; d.sb_k = 1; d.sb_n = M.n;
+    d.d_off = proj_off[i]; d.ldd = M.m;
+    add_seg(P.proj, d, M.off, -1, M.off);
+    P.proj.descs.push_back(d);
+  }
+  P.comp_proj_off = 0;
+  int max_sub = 0;
+  struct Unit { int layer, group; int64_t ping, pong, fin; int rows, c; };
+  std::vector<Unit> units;
+  for (int l = 0; l < (int)P.layers.size(); ++l) {
+    LayerInfo& L = P.layers[l];
+    if (L.owner != P.opts.rank) continue;
+    for (int gi = 0; gi < L.g; ++gi) {
+      Unit u{l, gi, -1, -1, -1, 0, 0};
+      if ((L.cons == CONS_BCOP || L.cons == CONS_AOC) && L.kp > 1) {
+        u.c = L.c_b;
+        u.rows = (L.cons == CONS_BCOP) ? std::min(L.co, L.c_b) : L.c_b;   // row subset (only [:co] is kept)
+        const int64_t sz = pad_up((int64_t)u.rows * u.c * L.kp * L.kp, kPadF32);
+        u.ping = w; w += sz;
+        u.pong = w; w += sz;
+        max_sub = std::max(max_sub, 2 * (L.kp - 1));
+      }
+      if (L.cons == CONS_AOC) { u.fin = w; w += pad_up((int64_t)L.co * L.ci * L.k * L.k, kPadF32); }
+      units.push_back(u);
+    }
+  }
+  P.chain.assign(max_sub, GemmPhase{});
+  for (auto& u : units) {
+    const LayerInfo& L = P.layers[u.layer];
+    if (u.ping < 0) continue;
+    const int base = L.first_mat + u.group * L.mats_per_group;
+    const MatInfo& Q = P.mats[base];
+    const int r = u.rows, c = u.c;
+    const int64_t tap = (int64_t)r * c;
+    int kh = 1, kw = 1;
+    int in_buf = BUF_X;
+    int64_t in_off = Q.off;
+    for (int t = 0; t < 2 * (L.kp - 1); ++t) {
+      const bool vert = (t % 2) == 0;
+      const int uidx = base + 1 + t;                 // U_{t+1}: P_{2j-1} vertical, P_{2j} horizontal
+      const int64_t poff = proj_off[uidx];
+      const int oh = vert ? kh + 1 : kh, ow = vert ? kw : kw + 1;
+      const int64_t out_off = (t % 2 == 0) ? u.ping : u.pong;
+      GemmPhase& ph = P.chain[t];
+      for (int p = 0; p < oh; ++p)
+        for (int q = 0; q < ow; ++q) {
+          // D[p,q] = (K[cur] - K[prev]) P + K[prev]; prev = tap shifted by one along the step axis
+          const int cp = p, cq = q;
+          const int pp = vert ? p - 1 : p, pq = vert ? q : q - 1;
+          const bool has_cur = vert ? (p < kh) : (q < kw);
+          const bool has_prev = vert ? (p >= 1) : (q >= 1);
+          const int64_t cur = in_off + (int64_t)(cp * kw + cq) * tap;
+          const int64_t prev = in_off + (int64_t)(pp * kw + pq) * tap;
+          GemmDesc d = mk(r, c, c);
+          d.a_buf = in_buf; d.b_buf = BUF_W; d.d_buf = BUF_W;
+          d.sa_m = c; d.sa_k = 1; d.sb_k = c; d.sb_n = 1;
+          d.d_off = out_off + (int64_t)(p * ow + q) * tap; d.ldd = c;
+          if (has_cur && has_prev) {
+            add_seg(ph, d, cur, prev, poff);
+            d.c_buf = in_buf; d.c_off = prev; d.ldc = c; d.beta = 1.0f;
+          } else if (has_cur) {
+            add_seg(ph, d, cur, -1, poff);
+          } else {  // last row/col: K[prev] (I - P)
+            add_seg(ph, d, prev, -1, poff);
+            d.alpha = -1.0f;
+            d.c_buf = in_buf; d.c_off = prev; d.ldc = c; d.beta = 1.0f;
+          }
+          ph.descs.push_back(d);
+        }
+      kh = oh; kw = ow;
+      in_buf = BUF_W;
+      in_off = out_off;
+    }
+  }
+  // AOC: K[p,q] = sum_{a,b} R_{ab} Kb[p-a, q-b]   (R_{ab}[o, j] = R[o, j s^2 + a s + b], R7)
+  for (auto& u : units) {
+    const LayerInfo& L = P.layers[u.layer];
+    if (L.cons != CONS_AOC) continue;
+    const int base = L.first_mat + u.group * L.mats_per_group;
+    const MatInfo& R = P.mats[base + L.mats_per_group - 1];
+    const int s = L.s, kp = L.kp, k = L.k, c = u.c;
+    const int64_t tap = (int64_t)u.rows * c;
+    for (int p = 0; p < k; ++p)
+      for (int q = 0; q < k; ++q) {
+        GemmDesc d = mk(L.co, L.ci, L.c_mid);
+        d.a_buf = BUF_X; d.b_buf = BUF_W; d.d_buf = BUF_W;
+        d.sa_m = (int64_t)L.c_mid * s * s; d.sa_k = (int64_t)s * s; d.sb_k = c; d.sb_n = 1;
+        d.d_off = u.fin + (int64_t)(p * k + q) * L.co * L.ci; d.ldd = L.ci;
+        for (int a = 0; a < s; ++a)
+          for (int b = 0; b < s; ++b) {
+            const int ta = p - a, tb = q - b;
+            if (ta < 0 || tb < 0 || ta >= kp || tb >= kp) continue;
+            add_seg(P.aoc, d, R.off + a * s + b, -1, u.pong + (int64_t)(ta * kp + tb) * tap);
+          }
+        P.aoc.descs.push_back(d);
+      }
+  }
+  for (auto* ph : {&P.proj, &P.aoc}) finish_phase(*ph);
+  for (auto& ph : P.chain) finish_phase(ph);
+  // emit items
+  for (auto& u : units) {
+    const LayerInfo& L = P.layers[u.layer];
+    const int base = L.first_mat + u.group * L.mats_per_group;
+    EmitItem e{};
+    e.layer = u.layer; e.group = u.group;
+    e.co = L.co; e.ci = L.ci; e.k = (L.cons == CONS_DENSE) ? 1 : L.k; e.s = L.s; e.ci_f_per_g = L.ci;
+    e.f32_off = L.kf32_off + (int64_t)u.group * L.co * L.ci * e.k * e.k;
+    e.bf16_off = L.kbf16_off + (int64_t)u.group * L.co * L.ci * e.k * e.k;
+    switch (L.cons) {
+      case CONS_DENSE:
+        e.src_buf = BUF_X; e.src_off = P.mats[base].off; e.mode = 0; e.tap_stride = 0; e.ld = L.ci; break;
+      case CONS_RKO:
+        e.src_buf = BUF_X; e.src_off = P.mats[base].off; e.mode = 1; e.tap_stride = 0; e.ld = 0; break;
+      case CONS_AOC:
+        e.src_buf = BUF_W; e.src_off = u.fin; e.mode = 0; e.tap_stride = (int64_t)L.co * L.ci; e.ld = L.ci; break;
+      default:  // BCOP
+        if (L.kp == 1) { e.src_buf = BUF_X; e.src_off = P.mats[base].off; e.mode = 0; e.tap_stride = 0; e.ld = L.c_b; }
+        else { e.src_buf = BUF_W; e.src_off = u.pong; e.mode = 0; e.tap_stride = (int64_t)u.rows * u.c; e.ld = u.c; }
+    }
+    P.emit.push_back(e);
+  }
+  P.comp_numel = std::max<int64_t>(w, kPadF32);
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static orth_status_t allocate(Plan& P) {
+  if (cudaSetDevice(P.device) != cudaSuccess) {
+    set_error("cudaSetDevice(%d) failed: %s", P.device, cudaGetErrorString(cudaGetLastError()));
+    return ORTH_ERR_CUDA;
+  }
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + std::max<size_t>(bytes, 1), 256); return o; };
+  const size_t o_scr = take(P.params_numel * 4), o_gram = take(P.gram_numel * 4), o_v = take(P.cache_numel * 4);
+  const size_t o_sig = take(std::max<size_t>(P.mats.size(), 1) * 4), o_part = take(P.partial_numel * 4);
+  const size_t o_comp = take(P.comp_numel * 4), o_stat = take(64);
+  const size_t o_pi = take(std::max<size_t>(P.power_items.size(), 1) * sizeof(PowerItem));
+  const size_t o_own = take(std::max<size_t>(P.mat_items.size(), 1) * sizeof(MatItem));
+  const size_t o_emit = take(std::max<size_t>(P.emit.size(), 1) * sizeof(EmitItem));
+  std::vector<GemmPhase*> phases = {&P.gram[0], &P.gram[1], &P.update[0], &P.update[1], &P.proj, &P.aoc};
+  for (auto& ph : P.chain) phases.push_back(&ph);
+  std::vector<std::pair<size_t, size_t>> ph_off;
+  for (auto* ph : phases)
+    ph_off.push_back({take(std::max<size_t>(ph->descs.size(), 1) * sizeof(GemmDesc)),
+                      take(std::max<size_t>(ph->segs.size(), 1) * sizeof(GemmSeg))});
+  P.arena_bytes = off;
+  if (cudaMalloc(&P.d_arena, off) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("workspace cudaMalloc(%zu bytes) failed", off);
+    return ORTH_ERR_OUT_OF_MEMORY;
+  }
+  char* base = (char*)P.d_arena;
+  P.d_scratch = (float*)(base + o_scr);
+  P.d_gram = (float*)(base + o_gram);
+  P.d_vbuf = (float*)(base + o_v);
+  P.d_sigma = (float*)(base + o_sig);
+  P.d_partial = (float*)(base + o_part);
+  P.d_comp = (float*)(base + o_comp);
+  P.d_status = (int32_t*)(base + o_stat);
+  P.d_power_items = (PowerItem*)(base + o_pi);
+  P.d_mat_items = (MatItem*)(base + o_own);
+  P.d_emit = (EmitItem*)(base + o_emit);
+  cudaError_t e = cudaMemset(P.d_arena, 0, off);
+  if (!P.power_items.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_power_items, P.power_items.data(), P.power_items.size() * sizeof(PowerItem), cudaMemcpyHostToDevice);
+  if (!P.mat_items.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_mat_items, P.mat_items.data(), P.mat_items.size() * sizeof(MatItem), cudaMemcpyHostToDevice);
+  if (!P.emit.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_emit, P.emit.data(), P.emit.size() * sizeof(EmitItem), cudaMemcpyHostToDevice);
+  for (size_t i = 0; i < phases.size() && e == cudaSuccess; ++i) {
+    GemmPhase* ph = phases[i];
+    ph->d_descs = (GemmDesc*)(base + ph_off[i].first);
+    ph->d_segs = (GemmSeg*)(base + ph_off[i].second);
+    if (!ph->descs.empty())
+      e = cudaMemcpy(ph->d_descs, ph->descs.data(), ph->descs.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice);
+    if (!ph->segs.empty() && e == cudaSuccess)
+      e = cudaMemcpy(ph->d_segs, ph->segs.data(), ph->segs.size() * sizeof(GemmSeg), cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    set_error("plan upload failed: %s", cudaGetErrorString(e));
+    cudaFree(P.d_arena);
+    P.d_arena = nullptr;
+    return ORTH_ERR_CUDA;
+  }
+  return ORTH_OK;
+}
+
+}  // namespace orth
+
+using namespace orth;
+
+extern "C" {
+
+void orth_opts_default(orth_opts_t* o) {
+  if (!o) return;
+  o->ns_iters = 12;
+  o->beta = 0.5f;
+  o->prescale = ORTH_PRESCALE_POWER;
+  o->power_iters = 3;
+  o->compute = ORTH_F32;
+  o->polish_iters = 2;
+  o->rank = 0;
+  o->world = 1;
+}
+
+orth_status_t orth_validate_desc(const orth_layer_desc_t* layers, int32_t n_layers, const orth_opts_t* opts) {
+  if (!layers || n_layers < 1) { set_error("layers is NULL or n_layers < 1"); return ORTH_ERR_INVALID_ARGUMENT; }
+  orth_opts_t o;
+  orth_opts_default(&o);
+  if (opts) o = *opts;
+  orth_status_t st = validate_opts(o);
+  if (st != ORTH_OK) return st;
+  for (int i = 0; i < n_layers; ++i) {
+    st = validate_layer(layers[i], i);
+    if (st != ORTH_OK) return st;
+  }
+  return ORTH_OK;
+}
+
+orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers, const orth_opts_t* opts,
+                               int32_t device, orth_plan_t* plan) {
+  if (!plan) { set_error("plan out-pointer is NULL"); return ORTH_ERR_INVALID_ARGUMENT; }
+  *plan = nullptr;
+  orth_status_t st = orth_validate_desc(layers, n_layers, opts);
+  if (st != ORTH_OK) return st;
+  if (device < -1) { set_error("device must be >= -1"); return ORTH_ERR_INVALID_ARGUMENT; }
+  auto* h = new orth_plan();
+  Plan& P = h->p;
+  orth_opts_default(&P.opts);
+  if (opts) P.opts = *opts;
+  P.device = device;
+  derive(P, layers, n_layers);
+  assign_owners(P);
+  layout(P);
+  build_ns(P);
+  build_compose(P);
+  if (device >= 0) {
+    st = allocate(P);
+    if (st != ORTH_OK) { delete h; return st; }
+  }
+  *plan = h;
+  return ORTH_OK;
+}
+
+orth_status_t orth_plan_destroy(orth_plan_t plan) {
+  if (!plan) return ORTH_OK;
+  if (plan->p.d_arena) cudaFree(plan->p.d_arena);
+  delete plan;
+  return ORTH_OK;
+}
+
+orth_status_t orth_plan_query(orth_plan_t plan, int32_t what, int32_t index, int64_t* out) {
+  if (!plan || !out) { set_error("NULL plan or out"); return ORTH_ERR_INVALID_ARGUMENT; }
+  const Plan& P = plan->p;
+  const bool lq = what >= 20 && what < 40, mq = what >= 40;
+  if (lq && (index < 0 || index >= (int)P.layers.size())) { set_error("layer index %d out of range", index); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (mq && (index < 0 || index >= (int)P.mats.size())) { set_error("matrix index %d out of range", index); return ORTH_ERR_INVALID_ARGUMENT; }
+  switch (what) {
+    case ORTH_Q_N_LAYERS: *out = (int64_t)P.layers.size(); break;
+    case ORTH_Q_N_MATRICES: *out = (int64_t)P.mats.size(); break;
+    case ORTH_Q_PARAMS_NUMEL: *out = P.params_numel; break;
+    case ORTH_Q_CACHE_NUMEL: *out = P.cache_numel; break;
+    case ORTH_Q_KERNELS_F32_NUMEL: *out = P.kf32_numel; break;
+    case ORTH_Q_KERNELS_BF16_NUMEL: *out = P.kbf16_numel; break;
+    case ORTH_Q_WORKSPACE_BYTES: *out = (int64_t)P.arena_bytes; break;
+    case ORTH_Q_NS_FLOPS: *out = (int64_t)P.ns_flops; break;
+    case ORTH_Q_KERNEL_SEGMENT_F32: *out = P.seg_f32; break;
+    case ORTH_Q_KERNEL_SEGMENT_BF16: *out = P.seg_bf16; break;
+    case ORTH_Q_LAYER_FIRST_MATRIX: *out = P.layers[index].first_mat; break;
+    case ORTH_Q_LAYER_MATS_PER_GROUP: *out = P.layers[index].mats_per_group; break;
+    case ORTH_Q_LAYER_KERNEL_OFF_F32: *out = P.layers[index].kf32_off; break;
+    case ORTH_Q_LAYER_KERNEL_OFF_BF16: *out = P.layers[index].kbf16_off; break;
+    case ORTH_Q_LAYER_KERNEL_NUMEL: *out = P.layers[index].kernel_numel; break;
+    case ORTH_Q_LAYER_OWNER: *out = P.layers[index].owner; break;
+    case ORTH_Q_LAYER_C_MID: *out = P.layers[index].c_mid; break;
+    case ORTH_Q_LAYER_C_B: *out = P.layers[index].c_b; break;
+    case ORTH_Q_LAYER_KP: *out = P.layers[index].kp; break;
+    case ORTH_Q_MATRIX_ROWS: *out = P.mats[index].m; break;
+    case ORTH_Q_MATRIX_COLS: *out = P.mats[index].n; break;
+    case ORTH_Q_MATRIX_OFFSET: *out = P.mats[index].off; break;
+    case ORTH_Q_MATRIX_CACHE_OFFSET: *out = P.mats[index].cache_off; break;
+    case ORTH_Q_MATRIX_LAYER: *out = P.mats[index].layer; break;
+    case ORTH_Q_MATRIX_GROUP: *out = P.mats[index].group; break;
+    case ORTH_Q_MATRIX_ROLE: *out = P.mats[index].role; break;
+    default: set_error("unknown query %d", what); return ORTH_ERR_INVALID_ARGUMENT;
+  }
+  return ORTH_OK;
+}
+
+int64_t orth_plan_launch_count(orth_plan_t plan) { return plan ? plan->p.launches : 0; }
+
+const char* orth_status_string(orth_status_t s) {
+  switch (s) {
+    case ORTH_OK: return "ORTH_OK";
+    case ORTH_ERR_INVALID_ARGUMENT: return "ORTH_ERR_INVALID_ARGUMENT";
+    case ORTH_ERR_UNSUPPORTED_CONFIG: return "ORTH_ERR_UNSUPPORTED_CONFIG";
+    case ORTH_ERR_SHAPE_MISMATCH: return "ORTH_ERR_SHAPE_MISMATCH";
+    case ORTH_ERR_ZERO_NORM: return "ORTH_ERR_ZERO_NORM";
+    case ORTH_ERR_NOT_CONVERGED: return "ORTH_ERR_NOT_CONVERGED";
+    case ORTH_ERR_CUDA: return "ORTH_ERR_CUDA";
+    case ORTH_ERR_OUT_OF_MEMORY: return "ORTH_ERR_OUT_OF_MEMORY";
+    case ORTH_ERR_NO_DEVICE: return "ORTH_ERR_NO_DEVICE";
+  }
+  return "ORTH_ERR_UNKNOWN";
+}
+
+const char* orth_last_error(void) { return orth::g_err; }
+
+}  // extern "C"

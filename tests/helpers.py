@@ -1,0 +1,68 @@
+"""Shared test helpers: seeded packing of parameters (synth) and the oracle
+construction of the same inputs.  The oracle never sees a value produced by
+the CUDA path; GPU outputs are only ever compared against it or checked by
+its verifiers."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle as O
+from synth import gen
+
+
+def oracle_layer(d) -> O.Layer:
+    return O.Layer(d["c_in"], d["c_out"], d.get("k", 3), d.get("s", 1), d.get("d", 1), d.get("g", 1),
+                   kind=d.get("kind", "conv"), padding_mode=d.get("padding_mode", "circular"),
+                   pad=d.get("pad"))
+
+
+def pack_params(plan, cfg_id: int, stress: bool = False):
+    """float32 flat params buffer in the plan's layout + the list of matrices."""
+    buf = np.zeros(plan.params_numel, np.float32)
+    mats = []
+    for i, m in enumerate(plan.matrices):
+        A = gen.param_matrix(m["m"], m["n"], (cfg_id, m["layer"], m["group"], i, gen.ROLE_ID[m["role"]]), stress)
+        buf[m["off"]: m["off"] + A.size] = A.ravel()
+        mats.append(A)
+    return buf, mats
+
+
+def pack_cache(plan, cfg_id: int):
+    buf = np.zeros(plan.cache_numel, np.float32)
+    vs = []
+    for i, m in enumerate(plan.matrices):
+        v = gen.unit_vector(m["n"], (cfg_id, m["layer"], m["group"], i, gen.ROLE_ID["v"]))
+        buf[m["cache_off"]: m["cache_off"] + v.size] = v
+        vs.append(v)
+    return buf, vs
+
+
+def oracle_construct(layers, mats, T=12, beta=0.5, prescale="power", P=3, v=None):
+    """Oracle a2..a5 on the float32 matrices (upcast to f64)."""
+    ortho, vnew = O.orthogonalize([A.astype(np.float64) for A in mats], T=T, beta=beta, prescale=prescale, P=P,
+                                  v=None if v is None else [x.astype(np.float64) for x in v])
+    kernels, idx = [], 0
+    for d in layers:
+        OL = oracle_layer(d)
+        nm = len(O.layer_matrices(OL))
+        groups = []
+        for _ in range(OL.g):
+            groups.append(ortho[idx: idx + nm])
+            idx += nm
+        kernels.append(O.layer_kernel(OL, groups))
+    return ortho, vnew, kernels
+
+
+def rel(a, b) -> float:
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+def nchw(x_nhwc):
+    return np.ascontiguousarray(np.transpose(x_nhwc, (0, 3, 1, 2)))
+
+
+def nhwc(x_nchw):
+    return np.ascontiguousarray(np.transpose(x_nchw, (0, 2, 3, 1)))

@@ -1,0 +1,155 @@
+"""Host-side tests of the C-ABI library (no GPU): symbol exports, validation
+and rejection rules, unit derivation against the oracle, packed layouts,
+construction sharding (LPT, rank-major segments) and the no-device contract."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2601_13776_b200 as orth
+from synth import configs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "orth.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(orth_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = _declared_symbols()
+    assert len(syms) >= 13
+    for s in syms:
+        assert hasattr(orth._lib, s), s
+    assert set(syms) == set(orth.EXPORTED)
+
+
+def L(**kw):
+    d = dict(kind="conv", c_in=8, c_out=8, k=3, s=1, d=1, g=1, padding_mode="circular")
+    d.update(kw)
+    return d
+
+
+@pytest.mark.parametrize("layer,status", [
+    (L(), orth.OK),
+    (L(g=3), orth.INVALID_ARGUMENT),                 # g must divide channels
+    (L(c_in=0), orth.INVALID_ARGUMENT),              # dims >= 1
+    (L(k=1, s=2), orth.UNSUPPORTED_CONFIG),          # k < s
+    (L(s=2, d=2), orth.UNSUPPORTED_CONFIG),          # gcd(s, d) != 1 (R10)
+    (L(s=2, d=4, k=3), orth.UNSUPPORTED_CONFIG),
+    (L(s=2, d=3), orth.OK),                          # gcd = 1 accepted
+    (L(c_in=1, c_out=8, s=2), orth.OK),              # c_out > c_in s^2 accepted (R9)
+    (L(kind="dense", k=1), orth.OK),
+    (L(kind="dense", k=3), orth.INVALID_ARGUMENT),
+    (L(pad=(1, 1, 1, -1)), orth.INVALID_ARGUMENT),
+    (L(kind="convT", padding_mode="circular", s=2), orth.OK),   # R14
+])
+def test_validation(layer, status):
+    assert orth.orth_validate_desc([layer]) == status
+
+
+@pytest.mark.parametrize("opts,status", [
+    (dict(beta=0.0), orth.INVALID_ARGUMENT), (dict(beta=0.6), orth.INVALID_ARGUMENT),
+    (dict(ns_iters=0), orth.INVALID_ARGUMENT), (dict(power_iters=0), orth.INVALID_ARGUMENT),
+    (dict(rank=2, world=2), orth.INVALID_ARGUMENT), (dict(beta=0.25, ns_iters=30), orth.OK),
+])
+def test_validation_opts(opts, status):
+    assert orth.orth_validate_desc([L()], **opts) == status
+
+
+def test_create_raises_with_detail():
+    with pytest.raises(orth.OrthError) as ei:
+        orth.Plan([L(k=1, s=2)], device=-1)
+    assert ei.value.status == orth.UNSUPPORTED_CONFIG
+    assert "P:330" in str(ei.value)
+
+
+def _oracle_layer(d):
+    return O.Layer(d["c_in"], d["c_out"], d["k"], d["s"], d["d"], d["g"], kind=d["kind"],
+                   padding_mode=d["padding_mode"])
+
+
+GRID = [L(c_in=ci, c_out=co, k=k, s=s, d=dd, g=g, kind=kind)
+        for (ci, co, k, s, dd, g, kind) in [
+            (16, 16, 3, 1, 1, 1, "conv"), (4, 8, 3, 2, 1, 1, "conv"), (8, 4, 3, 2, 1, 1, "conv"),
+            (1, 8, 3, 2, 1, 1, "conv"), (4, 16, 2, 2, 1, 1, "conv"), (8, 8, 4, 2, 1, 1, "conv"),
+            (1, 1, 3, 1, 1, 1, "conv"), (8, 16, 3, 2, 1, 2, "conv"), (8, 8, 3, 1, 2, 2, "convT"),
+            (4, 8, 3, 2, 1, 2, "convT"), (6, 9, 5, 3, 2, 3, "conv"), (3, 64, 4, 4, 1, 1, "conv")]]
+
+
+@pytest.mark.parametrize("cfg", [configs.cfg1(), configs.cfg2(), configs.cfg3(), configs.cfg4(), GRID,
+                                 configs.cfg5(512)[:4]])
+def test_derivation_matches_oracle(cfg):
+    p = orth.Plan(cfg, device=-1)
+    mats = p.matrices
+    idx = 0
+    for l, d in enumerate(cfg):
+        OL = _oracle_layer(d)
+        spec = O.layer_matrices(OL)
+        geo = O.layer_geometry(OL)
+        info = p.layer_info[l]
+        assert info["first_matrix"] == idx and info["mats_per_group"] == len(spec)
+        assert info["c_mid"] == geo["c_mid"] and info["c_b"] == geo["c_b"] and info["kp"] == geo["kp"]
+        for g in range(d["g"]):
+            for j, M in enumerate(spec):
+                m = mats[idx]
+                assert (m["m"], m["n"], m["role"], m["layer"], m["group"]) == (M.m, M.n, M.role, l, g)
+                idx += 1
+        assert info["numel"] == int(np.prod(p.kernel_shape(l)))
+    assert idx == p.n_matrices
+
+
+def test_layout_alignment_and_disjointness():
+    p = orth.Plan(configs.cfg2(), device=-1)
+    end = 0
+    for m in p.matrices:
+        assert m["off"] % 32 == 0 and m["cache_off"] % 32 == 0
+        assert m["off"] >= end
+        end = m["off"] + m["m"] * m["n"]
+    assert end <= p.params_numel
+    ends = 0
+    for l, info in enumerate(p.layer_info):
+        assert info["kf32_off"] % 32 == 0 and info["kbf16_off"] % 64 == 0
+        assert info["kf32_off"] >= ends
+        ends = info["kf32_off"] + info["numel"]
+    assert ends <= p.kf32_numel
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_lpt_sharding_rank_major_segments(world):
+    cfg = configs.cfg3()
+    plans = [orth.Plan(cfg, device=-1, rank=r, world=world) for r in range(world)]
+    owners = [info["owner"] for info in plans[0].layer_info]
+    for p in plans[1:]:   # every rank derives the same assignment and offsets
+        assert [i["owner"] for i in p.layer_info] == owners
+        assert [i["kf32_off"] for i in p.layer_info] == [i["kf32_off"] for i in plans[0].layer_info]
+    seg = orth.orth_plan_query(plans[0].h, "KERNEL_SEGMENT_F32")
+    for info in plans[0].layer_info:
+        r = info["owner"]
+        assert r * seg <= info["kf32_off"] and info["kf32_off"] + info["numel"] <= (r + 1) * seg
+    assert plans[0].kf32_numel == seg * world
+    # LPT balance: max load <= mean + largest unit
+    cost = {}
+    for l, d in enumerate(cfg):
+        OL = _oracle_layer(d)
+        cost[l] = sum(4.0 * max(M.m, M.n) * min(M.m, M.n) ** 2 for M in O.layer_matrices(OL)) * d["g"]
+    loads = [sum(c for l, c in cost.items() if owners[l] == r) for r in range(world)]
+    assert max(loads) <= sum(loads) / world + max(cost.values()) + 1
+    flops = [orth.orth_plan_query(p.h, "NS_FLOPS") for p in plans]
+    assert abs(sum(flops) - orth.orth_plan_query(orth.Plan(cfg, device=-1).h, "NS_FLOPS")) <= world
+
+
+def test_host_only_plan_cannot_compute():
+    p = orth.Plan(configs.cfg1(), device=-1)
+
+    class Fake:
+        def __init__(self, v): self.v = v
+        def data_ptr(self): return self.v
+
+    with pytest.raises(orth.OrthError) as ei:
+        orth.orth_orthogonalize(p.h, Fake(256), Fake(512), stream=0)
+    assert ei.value.status == orth.NO_DEVICE

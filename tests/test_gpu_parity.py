@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path through the C ABI against the float64 oracle on
+the same seeded inputs.  Tolerances (north star, reading R18): per tensor
+|gpu - oracle|_F / |oracle|_F <= 1e-5 for the FP32 path, <= 2e-2 for BF16;
+orthogonality max|sigma - 1| <= 1e-3 of the GPU's FP32 kernels."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import configs, gen
+from tests.helpers import nchw, nhwc, oracle_construct, oracle_layer, pack_cache, pack_params, rel
+
+pytestmark = pytest.mark.gpu
+
+TOL32, TOL16 = 1e-5, 2e-2
+
+
+def dev(a, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
+
+
+def gpu_construct(orth, layers, cfg_id, stress=False, with_cache=False, **opts):
+    plan = orth.Plan(layers, 0, **opts)
+    params, mats = pack_params(plan, cfg_id, stress)
+    p = dev(params)
+    ortho = torch.zeros_like(p)
+    res = torch.full((plan.n_matrices,), -1.0, device="cuda")
+    cache, vs = (None, None)
+    if with_cache:
+        cbuf, vs = pack_cache(plan, cfg_id)
+        cache = dev(cbuf)
+    plan.orthogonalize(p, ortho, cache, res)
+    kf = torch.zeros(plan.kf32_numel, device="cuda")
+    kb = torch.zeros(plan.kbf16_numel, device="cuda", dtype=torch.bfloat16)
+    plan.compose(ortho, kf, kb)
+    plan.check()
+    return plan, mats, vs, ortho, res, cache, kf, kb
+
+
+def unpack(plan, buf, i):
+    m = plan.matrices[i]
+    return buf[m["off"]: m["off"] + m["m"] * m["n"]].reshape(m["m"], m["n"])
+
+
+# ------------------------------------------------------------------ construction
+@pytest.mark.parametrize("cfg_id,layers", [(1, configs.cfg1()),
+                                           (11, [dict(kind=k, c_in=ci, c_out=co, k=kk, s=s, d=d, g=g,
+                                                      padding_mode="circular")
+                                                 for (ci, co, kk, s, d, g, k) in [
+                                                     (4, 8, 3, 2, 1, 1, "conv"), (8, 4, 3, 2, 1, 1, "conv"),
+                                                     (1, 8, 3, 2, 1, 1, "conv"), (4, 16, 2, 2, 1, 1, "conv"),
+                                                     (8, 8, 4, 2, 1, 1, "conv"), (1, 1, 3, 1, 1, 1, "conv"),
+                                                     (8, 16, 3, 2, 1, 2, "conv"), (8, 8, 3, 1, 2, 2, "convT"),
+                                                     (4, 8, 3, 2, 1, 2, "convT"), (6, 9, 5, 3, 2, 3, "conv"),
+                                                     (3, 64, 4, 4, 1, 1, "conv"), (96, 80, 3, 1, 1, 1, "conv"),
+                                                     (70, 70, 1, 1, 1, 1, "dense"), (33, 130, 1, 1, 1, 1, "dense")]])])
+@pytest.mark.parametrize("with_cache", [False, True])
+def test_construction_parity_fp32(cuda_lib, cfg_id, layers, with_cache):
+    plan, mats, vs, ortho, res, cache, kf, kb = gpu_construct(cuda_lib, layers, cfg_id, with_cache=with_cache)
+    o_ortho, o_v, o_k = oracle_construct(layers, mats, v=vs)
+    ortho_h, res_h, kf_h = ortho.cpu().numpy(), res.cpu().numpy(), kf.cpu().numpy()
+    kb_h = kb.float().cpu().numpy()
+    for i, X in enumerate(o_ortho):
+        if X.size == 0:
+            continue
+        assert rel(unpack(plan, ortho_h, i), X) < TOL32, (i, plan.matrices[i])
+        assert abs(res_h[i] - O.ns_residual(X)) < 1e-4
+        if with_cache:
+            m = plan.matrices[i]
+            vg = cache.cpu().numpy()[m["cache_off"]: m["cache_off"] + m["n"]]
+            assert rel(vg, o_v[i]) < 1e-4
+    for l, K in enumerate(o_k):
+        kg = plan.kernel_f32(torch.from_numpy(kf_h), l).numpy()
+        assert kg.shape == K.shape
+        assert rel(kg, K) < TOL32, l
+        kbg = plan.kernel_bf16(torch.from_numpy(kb_h), l).numpy()
+        if K.ndim == 4:
+            kbg = np.transpose(kbg, (0, 3, 1, 2))
+        assert np.array_equal(kbg, gen.bf16_round(kg.astype(np.float32)))   # emit is an RNE cast of the FP32 kernel
+
+
+def test_gpu_kernels_orthogonal_toeplitz(cuda_lib):
+    # P:462 explicit Toeplitz SVD on 8x8 inputs, applied to the GPU's FP32 kernels
+    layers = [dict(kind="conv", c_in=ci, c_out=co, k=k, s=s, d=1, g=g, padding_mode="circular")
+              for (ci, co, k, s, g) in [(16, 16, 3, 1, 1), (4, 8, 3, 2, 1), (8, 4, 3, 2, 1), (4, 32, 3, 2, 1),
+                                        (8, 8, 4, 2, 2), (4, 16, 2, 2, 1)]]
+    plan, mats, _, _, _, _, kf, _ = gpu_construct(cuda_lib, layers, 12)
+    kf_h = torch.from_numpy(kf.cpu().numpy())
+    for l, d in enumerate(layers):
+        K = plan.kernel_f32(kf_h, l).numpy().astype(np.float64)
+        OL = oracle_layer(d)
+        T = O.toeplitz(lambda x: O.conv2d(x, K, s=OL.s, d=OL.d, g=OL.g), (d["c_in"], 8, 8))
+        sv = np.linalg.svd(T, compute_uv=False)[: min(T.shape)]
+        assert np.abs(sv - 1).max() < 1e-3, (l, sv.min(), sv.max())
+
+
+def test_construction_cfg2_full(cuda_lib):
+    layers = configs.cfg2()
+    plan, mats, _, ortho, res, _, kf, _ = gpu_construct(cuda_lib, layers, 2)
+    o_ortho, _, o_k = oracle_construct(layers, mats)
+    ortho_h, kf_h = ortho.cpu().numpy(), torch.from_numpy(kf.cpu().numpy())
+    for i, X in enumerate(o_ortho):
+        assert rel(unpack(plan, ortho_h, i), X) < TOL32
+    for l, K in enumerate(o_k):
+        assert rel(plan.kernel_f32(kf_h, l).numpy(), K) < TOL32
+    assert float(res.max()) < 1e-3
+
+
+def test_frobenius_and_stress(cuda_lib):
+    layers = [dict(kind="conv", c_in=16, c_out=16, k=3, s=1, d=1, g=1, padding_mode="circular"),
+              dict(kind="dense", c_in=48, c_out=20, k=1, s=1, d=1, g=1, padding_mode="circular")]
+    plan, mats, _, ortho, res, _, kf, _ = gpu_construct(cuda_lib, layers, 13, stress=True, prescale="frobenius",
+                                                        ns_iters=40)
+    o_ortho, _, o_k = oracle_construct(layers, mats, T=40, prescale="frobenius")
+    ortho_h = ortho.cpu().numpy()
+    for i, X in enumerate(o_ortho):
+        assert rel(unpack(plan, ortho_h, i), X) < TOL32
+    assert float(res.max()) < 1e-4
+
+
+def test_determinism(cuda_lib):
+    layers = configs.cfg2()[:5]
+    a = gpu_construct(cuda_lib, layers, 2)
+    b = gpu_construct(cuda_lib, layers, 2)
+    assert torch.equal(a[3], b[3]) and torch.equal(a[6], b[6]) and torch.equal(a[7], b[7])
+
+
+def test_device_status_zero_and_nonconvergence(cuda_lib):
+    orth = cuda_lib
+    layers = [dict(kind="dense", c_in=2, c_out=2, k=1, s=1, d=1, g=1, padding_mode="circular")]
+    plan = orth.Plan(layers, 0, power_iters=1)
+    p = torch.zeros(plan.params_numel, device="cuda")
+    plan.orthogonalize(p, torch.zeros_like(p))
+    with pytest.raises(orth.OrthError) as ei:
+        plan.check()
+    assert ei.value.status == orth.ZERO_NORM
+    # sigma underestimated by a start vector orthogonal to the top singular vector -> divergence (R20)
+    p[0] = 100.0
+    p[3] = 1e-3
+    cache = torch.zeros(plan.cache_numel, device="cuda")
+    cache[1] = 1.0
+    res = torch.zeros(1, device="cuda")
+    plan.orthogonalize(p, torch.zeros_like(p), cache, res)
+    with pytest.raises(orth.OrthError) as ei:
+        plan.check()
+    assert ei.value.status == orth.NOT_CONVERGED
+    plan.check()                                              # cleared
+
+
+# ------------------------------------------------------------------ conv apply
+CONV_CASES = [  # (ci, co, k, s, d, g, mode, H, kind)
+    (16, 16, 3, 1, 1, 1, "circular", 8, "conv"), (3, 64, 3, 1, 1, 1, "circular", 32, "conv"),
+    (64, 128, 3, 2, 1, 1, "circular", 16, "conv"), (24, 40, 3, 2, 1, 1, "zeros", 9, "conv"),
+    (32, 32, 3, 1, 2, 4, "circular", 12, "conv"), (12, 18, 5, 3, 2, 3, "zeros", 11, "conv"),
+    (3, 64, 4, 4, 1, 1, "circular", 16, "conv"), (20, 20, 2, 1, 1, 1, "zeros", 7, "conv"),
+    (96, 80, 3, 2, 1, 1, "circular", 10, "convT"), (32, 32, 3, 1, 2, 8, "circular", 9, "convT"),
+    (17, 33, 3, 2, 1, 1, "zeros", 7, "convT"), (130, 70, 1, 1, 1, 1, "zeros", 5, "conv"),
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+@pytest.mark.parametrize("io", ["f32", "bf16"])
+def test_conv_forward_and_transpose(cuda_lib, case, io):
+    ci, co, k, s, d, g, mode, H, kind = case
+    layer = dict(kind=kind, c_in=ci, c_out=co, k=k, s=s, d=d, g=g, padding_mode=mode)
+    plan = cuda_lib.Plan([layer], 0)
+    OL = oracle_layer(layer)
+    ci_f, co_f = OL.fwd_channels()
+    rng = gen.rng(77, ci, co, k, s)
+    K = (rng.standard_normal((co_f, ci_f // g, k, k)) / np.sqrt(ci_f // g * k * k)).astype(np.float32)
+    N = 3
+    Hb = H * s if (kind == "convT" and mode == "circular") else H
+    x = gen.activations((N, Hb, Hb + 1 if mode == "zeros" else Hb, ci_f), (77, 1, ci, co, 6))
+    bias = gen.bias(co_f, (77, 2, ci, co, 7))
+    if io == "bf16":
+        K, x = gen.bf16_round(K), gen.bf16_round(x)
+        kdev = dev(np.transpose(K, (0, 2, 3, 1)), torch.bfloat16)
+        xdev, tdt, tol = dev(x, torch.bfloat16), torch.bfloat16, TOL16
+    else:
+        kdev, xdev, tdt, tol = dev(K), dev(x), torch.float32, TOL32
+    Hh, Ww = x.shape[1], x.shape[2]
+    Ho, Wo = plan.out_hw(0, Hh, Ww)
+    y = torch.zeros((N, Ho, Wo, co_f), device="cuda", dtype=tdt)
+    plan.conv_forward(0, kdev, xdev, y, bias=dev(bias))
+    ref = O.conv2d(nchw(x.astype(np.float64)), K.astype(np.float64), s=s, d=d, g=g, mode=mode) \
+        + bias[None, :, None, None]
+    assert rel(y.float().cpu().numpy(), nhwc(ref)) < tol
+    # adjoint
+    yr = gen.activations((N, Ho, Wo, co_f), (77, 3, ci, co, 6))
+    if io == "bf16":
+        yr = gen.bf16_round(yr)
+    xb = torch.zeros((N, Hh, Ww, ci_f), device="cuda", dtype=tdt)
+    plan.conv_transpose(0, kdev, dev(yr, tdt), xb)
+    refT = O.conv_transpose2d(nchw(yr.astype(np.float64)), K.astype(np.float64), Hh, Ww, s=s, d=d, g=g, mode=mode)
+    assert rel(xb.float().cpu().numpy(), nhwc(refT)) < tol
+    plan.check()
+
+
+def test_conv_rejections(cuda_lib):
+    orth = cuda_lib
+    plan = orth.Plan([dict(kind="conv", c_in=4, c_out=4, k=3, s=2, d=1, g=1, padding_mode="circular"),
+                      dict(kind="dense", c_in=4, c_out=4, k=1, s=1, d=1, g=1, padding_mode="circular")], 0)
+    K = torch.zeros(4 * 4 * 9, device="cuda")
+    x = torch.zeros((1, 9, 9, 4), device="cuda")
+    y = torch.zeros((1, 5, 5, 4), device="cuda")
+    with pytest.raises(orth.OrthError) as ei:
+        plan.conv_forward(0, K, x, y)
+    assert ei.value.status == orth.SHAPE_MISMATCH          # circular with s not dividing H (R11)
+    with pytest.raises(orth.OrthError) as ei:
+        plan.conv_forward(1, K, x, y)
+    assert ei.value.status == orth.UNSUPPORTED_CONFIG
+
+
+# ------------------------------------------------------------------ whole path, cfg1 and cfg2
+def test_whole_path_cfg1_norm_preserving(cuda_lib):
+    layers = configs.cfg1()
+    plan, mats, _, _, _, _, kf, kb = gpu_construct(cuda_lib, layers, 1)
+    _, _, o_k = oracle_construct(layers, mats)
+    x = gen.activations((2, 8, 8, 16), (1, 0, 0, 0, gen.ROLE_ID["x"]))
+    y = torch.zeros((2, 8, 8, 16), device="cuda")
+    plan.conv_forward(0, plan.kernel_f32(kf, 0), dev(x), y)
+    ref = nhwc(O.conv2d(nchw(x.astype(np.float64)), o_k[0]))
+    yh = y.cpu().numpy()
+    assert rel(yh, ref) < TOL32
+    nx = np.sqrt((x.astype(np.float64) ** 2).sum(axis=(1, 2, 3)))
+    ny = np.sqrt((yh.astype(np.float64) ** 2).sum(axis=(1, 2, 3)))
+    assert np.abs(ny / nx - 1).max() < 1e-5
+
+
+def test_whole_path_cfg2_bf16_chain_sampled(cuda_lib):
+    """Full-size cfg2 step as bench.py runs it (batch 256, bf16 chain); the
+    oracle chains its own kernels on a 2-image sample."""
+    layers = configs.cfg2()
+    plan, mats, _, _, _, _, kf, kb = gpu_construct(cuda_lib, layers, 2)
+    _, _, o_k = oracle_construct(layers, mats)
+    N = 256
+    x = gen.bf16_round(gen.activations((N, 32, 32, 3), (2, 0, 0, 0, gen.ROLE_ID["x"])))
+    cur = dev(x, torch.bfloat16)
+    H = 32
+    outs = []
+    for l, d in enumerate(layers):
+        Ho, _ = plan.out_hw(l, H, H)
+        y = torch.empty((N, Ho, Ho, d["c_out"]), device="cuda", dtype=torch.bfloat16)
+        plan.conv_forward(l, plan.kernel_bf16(kb, l), cur, y)
+        outs.append(y)
+        cur, H = y, Ho
+    plan.check()
+    sample = [0, 255]
+    ref = nchw(x[sample].astype(np.float64))
+    for l, d in enumerate(layers):
+        OL = oracle_layer(d)
+        ref = O.conv2d(ref, o_k[l], s=OL.s, d=OL.d, g=OL.g)
+        got = outs[l][sample].float().cpu().numpy()
+        assert rel(got, nhwc(ref)) < TOL16, l
+    # property at any size: circular isometries / co-isometries never increase the norm
+    xn = torch.linalg.vector_norm(dev(x).reshape(N, -1), dim=1)
+    yn = torch.linalg.vector_norm(outs[-1].float().reshape(N, -1), dim=1)
+    assert bool((yn <= xn * 1.02).all())

@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the orthogonal-conv hot path (BASELINE.json metric
+"orth-conv layers/s (orthogonalize+compose+fwd), NS TFLOP/s vs peak, HBM GB/s").
+
+One step = the whole hot path on one batch: orth_orthogonalize (power
+pre-scaling + T Bjorck/NS iterations of every parameter matrix), orth_compose_kernel
+(BCOP chain, RKO (*) BCOP, emit), then orth_conv_forward of every layer of the
+network, chained, on the step's batch.  Workload (N=1): BASELINE configs[1] =
+config 2 "CIFAR-AOC-12" (synth/configs.py), batch 256 at 32x32, bf16 NHWC
+activations, FP32 construction.
+
+value = layers/s = (#conv layers x ranks) / step time (weak scaling: every
+rank runs the forward on its own batch of 256; construction is sharded by
+layer across ranks and the BF16 kernels are NCCL-all-gathered).
+
+Usage: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "orth-conv layers/s (orthogonalize+compose+fwd), NS TFLOP/s vs peak, HBM GB/s"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "_fallback": True}
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        out = self.p.communicate()[0]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        load = [s for s in sm if mx and s > 0.3 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+def build_workload(orth, torch, cfg_layers, rank, world, device, compute, batch):
+    from synth import gen
+    plan = orth.Plan(cfg_layers, device, rank=rank, world=world, compute=compute)
+    params = np.zeros(plan.params_numel, np.float32)
+    for i, m in enumerate(plan.matrices):
+        A = gen.param_matrix(m["m"], m["n"], (2, m["layer"], m["group"], i, gen.ROLE_ID[m["role"]]))
+        params[m["off"]: m["off"] + A.size] = A.ravel()
+    cache = np.zeros(plan.cache_numel, np.float32)
+    for i, m in enumerate(plan.matrices):
+        v = gen.unit_vector(m["n"], (2, m["layer"], m["group"], i, gen.ROLE_ID["v"]))
+        cache[m["cache_off"]: m["cache_off"] + v.size] = v
+    H0 = cfg_layers[0]["H"]
+    x = gen.activations((batch, H0, H0, cfg_layers[0]["c_in"]), (2, rank, 0, 0, gen.ROLE_ID["x"]))
+    dev = torch.device("cuda", device)
+    W = dict(plan=plan, params_h=params, cache_h=cache, x_h=x)
+    W["params"] = torch.from_numpy(params).to(dev)
+    W["cache"] = torch.from_numpy(cache).to(dev)
+    W["ortho"] = torch.zeros_like(W["params"])
+    W["kf32"] = torch.zeros(plan.kf32_numel, device=dev)
+    W["kbf16"] = torch.zeros(plan.kbf16_numel, device=dev, dtype=torch.bfloat16)
+    W["x"] = torch.from_numpy(x).to(dev, torch.bfloat16)
+    acts, H = [], H0
+    shapes = []
+    for l, d in enumerate(cfg_layers):
+        Ho, _ = plan.out_hw(l, H, H)
+        acts.append(torch.empty((batch, Ho, Ho, d["c_out"]), device=dev, dtype=torch.bfloat16))
+        shapes.append((H, Ho, d))
+        H = Ho
+    W["acts"], W["shapes"] = acts, shapes
+    W["kviews"] = [plan.kernel_bf16(W["kbf16"], l) for l in range(len(cfg_layers))]
+    return W
+
+
+def conv_flops_bytes(shapes, batch):
+    fl, by = [], []
+    for (H, Ho, d) in shapes:
+        ci, co, k, g = d["c_in"], d["c_out"], d["k"], d["g"]
+        fl.append(2.0 * batch * Ho * Ho * co * (ci // g) * k * k)
+        by.append(2.0 * batch * (H * H * ci + Ho * Ho * co) + 2.0 * co * (ci // g) * k * k)
+    return fl, by
+
+
+def run_step(W, orth, torch, world, pg, ev=None):
+    """One step.  ev: optional dict of event lists to time the phases."""
+    plan = W["plan"]
+    rec = (lambda name: ev[name].append(torch.cuda.Event(enable_timing=True)) or ev[name][-1].record()) \
+        if ev is not None else (lambda name: None)
+    rec("orth0")
+    plan.orthogonalize(W["params"], W["ortho"], W["cache"])
+    rec("orth1")
+    plan.compose(W["ortho"], W["kf32"], W["kbf16"])
+    rec("comp1")
+    if world > 1:
+        import torch.distributed as dist
+        seg = orth.orth_plan_query(plan.h, "KERNEL_SEGMENT_BF16")
+        r = dist.get_rank()
+        dist.all_gather_into_tensor(W["kbf16"], W["kbf16"][r * seg:(r + 1) * seg].clone(), group=pg)
+    rec("gather1")
+    cur = W["x"]
+    for l, y in enumerate(W["acts"]):
+        rec(f"conv{l}_0")
+        plan.conv_forward(l, W["kviews"][l], cur, y)
+        rec(f"conv{l}_1")
+        cur = y
+    return cur
+
+
+def ours(args):
+    import torch
+    import paper_2601_13776_b200 as orth
+    from synth import configs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist.group.WORLD
+    cfg = configs.CONFIGS[args.config]()
+    batch = configs.BATCH[args.config]
+    W = build_workload(orth, torch, cfg, rank, world, local, args.compute, batch)
+    plan = W["plan"]
+    flush = torch.empty(int(2 * 126e6 // 4) + 1024, device="cuda", dtype=torch.float32)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        run_step(W, orth, torch, world, pg)
+    plan.check()
+    barrier()
+    clk = Clocks(local)
+    clk.start()
+    launches0 = plan.launches
+    names = ["orth0", "orth1", "comp1", "gather1"] + [f"conv{l}_{e}" for l in range(len(cfg)) for e in (0, 1)]
+    ev = {n: [] for n in names}
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()                                  # L2 flush outside the events
+        run_step(W, orth, torch, world, pg, ev)
+    barrier()
+    launches = plan.launches - launches0
+    clocks = clk.stop()
+    plan.check()
+    el = lambda a, b, i: ev[a][i].elapsed_time(ev[b][i])
+    step_ms = [el("orth0", f"conv{len(cfg) - 1}_1", i) for i in range(args.steps)]
+    t_step = sum(step_ms) / args.steps
+    t_orth = sum(el("orth0", "orth1", i) for i in range(args.steps)) / args.steps
+    t_comp = sum(el("orth1", "comp1", i) for i in range(args.steps)) / args.steps
+    t_gather = sum(el("comp1", "gather1", i) for i in range(args.steps)) / args.steps
+    t_conv = [sum(el(f"conv{l}_0", f"conv{l}_1", i) for i in range(args.steps)) / args.steps for l in range(len(cfg))]
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([t_step], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+    fl, by = conv_flops_bytes(W["shapes"], batch)
+    P = peaks()
+    ns_flops = orth.orth_plan_query(plan.h, "NS_FLOPS")
+    # dominant kernel class: conv forward (sum over layers) vs NS
+    conv_total = sum(t_conv)
+    if conv_total >= t_orth:
+        ach = sum(fl) / (conv_total * 1e-3) / 1e12
+        roof = {"kernel": "orth_conv_forward (12 launches, all layers)", "bound": "tensor", "achieved": ach,
+                "peak": P["bf16_tflops_sustained"], "unit": "TFLOP/s", "frac": ach / P["bf16_tflops_sustained"],
+                "traffic": None, "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                "per_launch_flops_avg": sum(fl) / len(fl), "avg_launch_ms": conv_total / len(fl),
+                "share_of_step": conv_total / t_step}
+    else:
+        ach = ns_flops / (t_orth * 1e-3) / 1e12
+        roof = {"kernel": "orth_orthogonalize (power + NS)", "bound": "tensor", "achieved": ach,
+                "peak": P["bf16_tflops_sustained"], "unit": "TFLOP/s", "frac": ach / P["bf16_tflops_sustained"],
+                "traffic": None, "share_of_step": t_orth / t_step}
+    # ---- e2e through the public API with host buffers
+    e2e = e2e_run(W, orth, torch, world, pg, args, barrier)
+    out = {
+        "metric": METRIC, "value": len(cfg) * world / (t_step * 1e-3), "unit": "layers/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if args.compute == "bf16" else "f32+bf16",
+        "data": "synthetic (seeded near-orthogonal params, N(0,1) activations; SURVEY §8(d))",
+        "config": {"workload": f"config {args.config}: CIFAR-AOC-12 (12 orthogonal 3x3 convs 64-512 ch, 3 stride-2)",
+                   "global_batch": batch * world, "per_rank_batch": batch, "image": 32, "ns_iters": 12,
+                   "construction": "FP32-accurate" if args.compute == "f32" else "BF16 tensor cores",
+                   "activations": "bf16 NHWC", "parallelism": f"dp{world} (construction sharded by layer + all-gather)",
+                   "l2": "flushed between timed steps (252 MB write)"},
+        "breakdown_ms": {"orthogonalize": t_orth, "compose": t_comp, "allgather": t_gather,
+                         "conv_forward": conv_total, "conv_per_layer": t_conv},
+        "ns_tflops": ns_flops / (t_orth * 1e-3) / 1e12,
+        "conv_tflops": sum(fl) / (conv_total * 1e-3) / 1e12,
+        "conv_gbs": sum(by) / (conv_total * 1e-3) / 1e9,
+        "roofline": roof,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def e2e_run(W, orth, torch, world, pg, args, barrier):
+    """Same step through the public API with HOST buffers: pinned H2D of the
+    step's inputs (params + x) and D2H of its result inside the timed region."""
+    ph = torch.from_numpy(W["params_h"]).pin_memory()
+    xh = torch.from_numpy(W["x_h"]).to(torch.bfloat16).pin_memory()
+    yh = torch.empty(W["acts"][-1].shape, dtype=torch.bfloat16).pin_memory()
+    s = torch.cuda.current_stream()
+    for _ in range(2):
+        W["params"].copy_(ph, non_blocking=True)
+        W["x"].copy_(xh, non_blocking=True)
+        run_step(W, orth, torch, world, pg)
+        yh.copy_(W["acts"][-1], non_blocking=True)
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(s)
+    n = max(1, args.steps)
+    for _ in range(n):
+        W["params"].copy_(ph, non_blocking=True)
+        W["x"].copy_(xh, non_blocking=True)
+        run_step(W, orth, torch, world, pg)
+        yh.copy_(W["acts"][-1], non_blocking=True)
+    t1.record(s)
+    barrier()
+    ms = t0.elapsed_time(t1) / n
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": len(W["acts"]) * world / (ms * 1e-3), "unit": "layers/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(ph.numel() * 4 + xh.numel() * 2), "d2h_bytes_per_step": int(yh.numel() * 2)}
+
+
+# ------------------------------------------------------------------ oracle (CPU) legs
+def _oracle_step(cfg, batch, n_img, seed_cfg=2):
+    """Oracle step on a bounded sample: full construction (all matrices) and the
+    forward of n_img images, extrapolated to the batch.  Returns (t_equiv_s, t_construct_s, t_img_s)."""
+    import oracle as O
+    from synth import gen
+    from tests.helpers import oracle_construct, oracle_layer
+    mats = []
+    i = 0
+    for l, d in enumerate(cfg):
+        OL = oracle_layer(d)
+        for g in range(OL.g):
+            for M in O.layer_matrices(OL):
+                mats.append(gen.param_matrix(M.m, M.n, (seed_cfg, l, g, i, gen.ROLE_ID[M.role])))
+                i += 1
+    t0 = time.perf_counter()
+    _, _, ks = oracle_construct(cfg, mats)
+    t1 = time.perf_counter()
+    x = gen.activations((n_img, cfg[0]["c_in"], cfg[0]["H"], cfg[0]["H"]), (seed_cfg, 0, 0, 0, 6)).astype(np.float64)
+    for l, d in enumerate(cfg):
+        OL = oracle_layer(d)
+        x = O.conv2d(x, ks[l], s=OL.s, d=OL.d, g=OL.g)
+    t2 = time.perf_counter()
+    t_img = (t2 - t1) / n_img
+    return (t1 - t0) + batch * t_img, t1 - t0, t_img
+
+
+def _threads():
+    n = len(os.sched_getaffinity(0))
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(n)
+    except Exception:
+        pass
+    return n
+
+
+def cpu_baseline(args, budget_s=30.0):
+    from synth import configs
+    cores = _threads()
+    cfg = configs.CONFIGS[args.config]()
+    batch = configs.BATCH[args.config]
+    t_eq, t_c, t_img = _oracle_step(cfg, batch, 1)
+    return {"value": len(cfg) / t_eq, "unit": "layers/s", "cores": cores, "kind": "oracle",
+            "sample": f"config {args.config}: full oracle construction ({t_c:.2f} s, all matrices, T=12, float64) + "
+                      f"forward of 1 image ({t_img:.2f} s) extrapolated to batch {batch}",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def reference(args):
+    """The oracle as the reference arm (tier framing: the CPU float64 oracle)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from synth import configs
+    cores = _threads()
+    cfg = configs.CONFIGS[args.config]()
+    batch = configs.BATCH[args.config]
+    for _ in range(min(args.warmup, 1)):
+        _oracle_step(cfg, batch, 1)
+    ts = []
+    for _ in range(args.steps):
+        t_eq, t_c, t_img = _oracle_step(cfg, batch, 1)
+        ts.append(t_eq)
+    t = sum(ts) / len(ts)
+    v = len(cfg) / t
+    out = {"metric": METRIC, "value": v, "unit": "layers/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": f"config {args.config}: CIFAR-AOC-12", "global_batch": batch},
+           "cpu_baseline": {"value": v, "unit": "layers/s", "cores": cores, "kind": "oracle",
+                            "sample": f"each step: full float64 oracle construction + forward of 1 image "
+                                      f"extrapolated to batch {batch}", "cpu": _cpu_model()},
+           "e2e": {"value": v, "unit": "layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--compute", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=30.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        reference(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "orth_internal.h"
 
@@ -213,6 +214,8 @@ ConvArgs make_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo) {
 
 int launch_conv_fwd(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N, int H,
                     int W, int Ho, int Wo, int io, void* stream) {
+  if (io == ORTH_BF16 && conv_fwd_tc_eligible(L) && !getenv("ORTH_FORCE_SIMT"))
+    return launch_conv_fwd_tc(L, kernel, bias, x, y, N, H, W, Ho, Wo, stream);
   const ConvArgs a = make_args(L, N, H, W, Ho, Wo);
   const int64_t M = (int64_t)N * Ho * Wo;
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((L.co + BN - 1) / BN), (unsigned)L.g);

@@ -145,6 +145,9 @@ int launch_residual(Plan& p, float* residual_out, void* stream);
 int launch_emit(Plan& p, const float* const bufs[BUF_COUNT], float* kf32, uint16_t* kbf16, void* stream);
 int launch_conv_fwd(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N, int H,
                     int W, int Ho, int Wo, int io, void* stream);
+bool conv_fwd_tc_eligible(const LayerInfo& L);
+int launch_conv_fwd_tc(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
+                       int H, int W, int Ho, int Wo, void* stream);
 int launch_conv_bwd(const LayerInfo& L, const void* kernel, const float* bias, const void* y, void* x, int N, int H,
                     int W, int Ho, int Wo, int io, void* stream);
 

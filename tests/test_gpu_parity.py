@@ -155,6 +155,12 @@ CONV_CASES = [  # (ci, co, k, s, d, g, mode, H, kind)
     (3, 64, 4, 4, 1, 1, "circular", 16, "conv"), (20, 20, 2, 1, 1, 1, "zeros", 7, "conv"),
     (96, 80, 3, 2, 1, 1, "circular", 10, "convT"), (32, 32, 3, 1, 2, 8, "circular", 9, "convT"),
     (17, 33, 3, 2, 1, 1, "zeros", 7, "convT"), (130, 70, 1, 1, 1, 1, "zeros", 5, "conv"),
+    # tcgen05-eligible shapes (co_g % 64 == 0, ci_g % 8 == 0) incl. ragged pixel tiles and channel tails
+    (64, 64, 3, 1, 1, 1, "circular", 10, "conv"), (64, 64, 3, 1, 1, 1, "zeros", 9, "conv"),
+    (128, 256, 3, 2, 1, 1, "circular", 8, "conv"), (256, 512, 3, 2, 1, 1, "zeros", 7, "conv"),
+    (64, 64, 3, 1, 2, 1, "circular", 12, "conv"), (128, 128, 3, 1, 1, 2, "circular", 8, "conv"),
+    (40, 64, 3, 1, 1, 1, "circular", 6, "conv"), (72, 128, 5, 2, 1, 1, "zeros", 9, "conv"),
+    (512, 512, 3, 1, 1, 1, "circular", 4, "conv"), (64, 128, 3, 2, 3, 1, "circular", 12, "conv"),
 ]
 
 

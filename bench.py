@@ -127,15 +127,22 @@ def conv_flops_bytes(shapes, batch):
     return fl, by
 
 
-def run_step(W, orth, torch, world, pg, ev=None):
-    """One step.  ev: optional dict of event lists to time the phases."""
+def run_step(W, orth, torch, world, pg, ev=None, graphs=None):
+    """One step.  ev: optional dict of event lists to time the phases.
+    graphs: optional CUDA graphs of the phases (captured from these same calls)."""
     plan = W["plan"]
     rec = (lambda name: ev[name].append(torch.cuda.Event(enable_timing=True)) or ev[name][-1].record()) \
         if ev is not None else (lambda name: None)
     rec("orth0")
-    plan.orthogonalize(W["params"], W["ortho"], W["cache"])
+    if graphs:
+        graphs["orth"].replay()
+    else:
+        plan.orthogonalize(W["params"], W["ortho"], W["cache"])
     rec("orth1")
-    plan.compose(W["ortho"], W["kf32"], W["kbf16"])
+    if graphs:
+        graphs["comp"].replay()
+    else:
+        plan.compose(W["ortho"], W["kf32"], W["kbf16"])
     rec("comp1")
     if world > 1:
         import torch.distributed as dist
@@ -146,10 +153,41 @@ def run_step(W, orth, torch, world, pg, ev=None):
     cur = W["x"]
     for l, y in enumerate(W["acts"]):
         rec(f"conv{l}_0")
-        plan.conv_forward(l, W["kviews"][l], cur, y)
+        if graphs:
+            graphs[f"conv{l}"].replay()
+        else:
+            plan.conv_forward(l, W["kviews"][l], cur, y)
         rec(f"conv{l}_1")
         cur = y
     return cur
+
+
+def capture_graphs(W, torch):
+    """One CUDA graph per phase (orthogonalize: ~31 launches, compose: ~7, one
+    per conv layer), captured from the library's own calls on the capture stream."""
+    plan = W["plan"]
+    graphs = {}
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            plan.orthogonalize(W["params"], W["ortho"], W["cache"])
+        graphs["orth"] = g
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            plan.compose(W["ortho"], W["kf32"], W["kbf16"])
+        graphs["comp"] = g
+        cur = W["x"]
+        for l, y in enumerate(W["acts"]):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                plan.conv_forward(l, W["kviews"][l], cur, y)
+            graphs[f"conv{l}"] = g
+            cur = y
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    return graphs
 
 
 def ours(args):
@@ -179,9 +217,16 @@ def ours(args):
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
+        l0 = plan.launches
         run_step(W, orth, torch, world, pg)
+        per_step_launches = plan.launches - l0
     plan.check()
     barrier()
+    graphs = capture_graphs(W, torch) if (world == 1 and not args.no_graph) else None
+    if graphs:
+        for _ in range(2):
+            run_step(W, orth, torch, world, pg, graphs=graphs)
+        barrier()
     clk = Clocks(local)
     clk.start()
     launches0 = plan.launches
@@ -190,9 +235,9 @@ def ours(args):
     barrier()
     for _ in range(args.steps):
         flush.zero_()                                  # L2 flush outside the events
-        run_step(W, orth, torch, world, pg, ev)
+        run_step(W, orth, torch, world, pg, ev, graphs)
     barrier()
-    launches = plan.launches - launches0
+    launches = plan.launches - launches0 if not graphs else per_step_launches * args.steps
     clocks = clk.stop()
     plan.check()
     el = lambda a, b, i: ev[a][i].elapsed_time(ev[b][i])
@@ -235,7 +280,8 @@ def ours(args):
                    "global_batch": batch * world, "per_rank_batch": batch, "image": 32, "ns_iters": 12,
                    "construction": "FP32-accurate" if args.compute == "f32" else "BF16 tensor cores",
                    "activations": "bf16 NHWC", "parallelism": f"dp{world} (construction sharded by layer + all-gather)",
-                   "l2": "flushed between timed steps (252 MB write)"},
+                   "l2": "flushed between timed steps (252 MB write)",
+                   "launch": "CUDA graphs per phase" if graphs else "eager"},
         "breakdown_ms": {"orthogonalize": t_orth, "compose": t_comp, "allgather": t_gather,
                          "conv_forward": conv_total, "conv_per_layer": t_conv},
         "ns_tflops": ns_flops / (t_orth * 1e-3) / 1e12,
@@ -384,8 +430,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--compute", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--compute", default="f32", choices=["f32", "bf16", "bf16x3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying CUDA graphs")
     ap.add_argument("--cpu-budget", type=float, default=30.0)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -60,7 +60,7 @@ typedef enum {
   ORTH_ERR_NO_DEVICE = 8           /* compute call on a host-only plan (device = -1) */
 } orth_status_t;
 
-typedef enum { ORTH_F32 = 0, ORTH_BF16 = 1 } orth_dtype_t;
+typedef enum { ORTH_F32 = 0, ORTH_BF16 = 1, ORTH_BF16X3 = 2 } orth_dtype_t;
 typedef enum { ORTH_PAD_ZEROS = 0, ORTH_PAD_CIRCULAR = 1 } orth_pad_t;
 typedef enum { ORTH_CONV2D = 0, ORTH_CONV_TRANSPOSE2D = 1, ORTH_DENSE = 2 } orth_kind_t;
 typedef enum { ORTH_PRESCALE_POWER = 0, ORTH_PRESCALE_FROBENIUS = 1 } orth_prescale_t;
@@ -91,7 +91,12 @@ typedef struct {
   float beta;            /* in (0, 1/2], default 0.5 */
   int32_t prescale;      /* orth_prescale_t, default power (R3) */
   int32_t power_iters;   /* P >= 1, default 3 (R2) */
-  int32_t compute;       /* orth_dtype_t of the NS contractions: F32 (FP32-accurate) or BF16 tensor cores with FP32 master (R16) */
+  int32_t compute;       /* NS / composition contractions (R16):
+                            ORTH_F32    FP32 FFMA (SIMT), FP32-accurate;
+                            ORTH_BF16   tensor cores, BF16 operands, FP32 master X in residual form
+                                        X <- X + b X (I - X^T X); the last polish_iters iterations and the
+                                        composition use the 3-pass hi/lo split (~2^-16 products);
+                            ORTH_BF16X3 tensor cores, 3-pass split everywhere (FP32-accurate to ~1e-5). */
   int32_t polish_iters;  /* BF16 only: trailing iterations run FP32-accurate, default 2 */
   int32_t rank, world;   /* construction sharding by layer (R22); default 0, 1 */
 } orth_opts_t;

@@ -24,7 +24,7 @@ _lib = C.CDLL(_LIB_PATH)
 
 # ---------------------------------------------------------------- ABI types
 OK, INVALID_ARGUMENT, UNSUPPORTED_CONFIG, SHAPE_MISMATCH, ZERO_NORM, NOT_CONVERGED, CUDA_ERR, OOM, NO_DEVICE = range(9)
-F32, BF16 = 0, 1
+F32, BF16, BF16X3 = 0, 1, 2
 PAD_ZEROS, PAD_CIRCULAR = 0, 1
 CONV2D, CONV_TRANSPOSE2D, DENSE = 0, 1, 2
 PRESCALE_POWER, PRESCALE_FROBENIUS = 0, 1
@@ -98,7 +98,7 @@ def make_opts(**kw) -> Opts:
     _lib.orth_opts_default(C.byref(o))
     for k, v in kw.items():
         if k == "compute" and isinstance(v, str):
-            v = {"f32": F32, "bf16": BF16}[v]
+            v = {"f32": F32, "bf16": BF16, "bf16x3": BF16X3}[v]
         if k == "prescale" and isinstance(v, str):
             v = {"power": PRESCALE_POWER, "frobenius": PRESCALE_FROBENIUS}[v]
         setattr(o, k, v)

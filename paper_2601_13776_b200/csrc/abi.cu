@@ -55,10 +55,6 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
   Plan& P = plan->p;
   if (!params || !ortho_out) { set_error("NULL params or ortho_out"); return ORTH_ERR_INVALID_ARGUMENT; }
   if (params == ortho_out) { set_error("params and ortho_out must not overlap"); return ORTH_ERR_INVALID_ARGUMENT; }
-  if (P.opts.compute != ORTH_F32) {
-    set_error("compute = BF16 tensor-core NS is not built into this library version");
-    return ORTH_ERR_UNSUPPORTED_CONFIG;
-  }
   if (P.mat_items.empty()) return ORTH_OK;
   const int T = P.opts.ns_iters;
   float* bufs[BUF_COUNT] = {ortho_out, P.d_scratch, P.d_gram, P.d_comp};
@@ -79,17 +75,28 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
     }
   }
   if (!e) e = launch_scale(P, params, x0, stream);
+  const int mode = P.opts.compute;
   for (int t = 0; t < T && !e; ++t) {
-    e = launch_gemm_f32(P.gram[par], bufs, stream);
-    P.launches++;
-    if (!e) e = launch_gemm_f32(P.update[par], bufs, stream);
-    P.launches++;
+    if (mode == ORTH_F32) {
+      e = launch_gemm_f32(P.gram[par], bufs, stream);
+      if (!e) e = launch_gemm_f32(P.update[par], bufs, stream);
+    } else {
+      const int np = (mode == ORTH_BF16X3 || t >= T - P.opts.polish_iters) ? 3 : 1;
+      e = launch_gemm_tc(P.gram_r[par], bufs, np, stream);
+      if (!e) e = launch_gemm_tc(P.update_r[par], bufs, np == 3 && mode == ORTH_BF16X3 ? 3 : 1, stream);
+    }
+    P.launches += 2;
     par ^= 1;
   }
   if (!e && residual_out) {
-    e = launch_gemm_f32(P.gram[0], bufs, stream);
+    if (mode == ORTH_F32) {
+      e = launch_gemm_f32(P.gram[0], bufs, stream);
+      if (!e) e = launch_residual(P, residual_out, stream);
+    } else {
+      e = launch_gemm_tc(P.gram_r[0], bufs, 3, stream);
+      if (!e) e = launch_residual_r(P, residual_out, stream);
+    }
     P.launches++;
-    if (!e) e = launch_residual(P, residual_out, stream);
   }
   return cuda_fail(e, "orth_orthogonalize");
 }
@@ -102,12 +109,15 @@ orth_status_t orth_compose_kernel(orth_plan_t plan, const float* ortho, float* k
   if (!ortho || !kernels_f32) { set_error("NULL ortho or kernels_f32"); return ORTH_ERR_INVALID_ARGUMENT; }
   float* bufs[BUF_COUNT] = {const_cast<float*>(ortho), nullptr, nullptr, P.d_comp};
   int e = 0;
-  if (P.proj.total_tiles) { e = launch_gemm_f32(P.proj, bufs, stream); P.launches++; }
-  for (auto& ph : P.chain) {
-    if (e) break;
-    if (ph.total_tiles) { e = launch_gemm_f32(ph, bufs, stream); P.launches++; }
-  }
-  if (!e && P.aoc.total_tiles) { e = launch_gemm_f32(P.aoc, bufs, stream); P.launches++; }
+  // composition stays FP32-accurate: SIMT FFMA, or the 3-pass split on tensor cores
+  auto gemm = [&](const GemmPhase& ph) {
+    if (!ph.total_tiles || e) return;
+    e = P.opts.compute == ORTH_F32 ? launch_gemm_f32(ph, bufs, stream) : launch_gemm_tc(ph, bufs, 3, stream);
+    P.launches++;
+  };
+  gemm(P.proj);
+  for (auto& ph : P.chain) gemm(ph);
+  gemm(P.aoc);
   if (!e) e = launch_emit(P, bufs, kernels_f32, (uint16_t*)kernels_bf16, stream);
   return cuda_fail(e, "orth_compose_kernel");
 }

@@ -202,6 +202,64 @@ __global__ void __launch_bounds__(256) conv_bwd_simt(const T* __restrict__ yv, c
   }
 }
 
+// Small reduction (ci_g * k^2 <= 64, e.g. the RGB stem): im2col of 128 pixels
+// into shared memory, the whole kernel slab in shared memory, FP32 FFMA; each
+// thread owns one pixel and writes 16-byte runs of 8 output channels.
+__global__ void __launch_bounds__(256) conv_fwd_smallk(const __nv_bfloat16* __restrict__ x,
+                                                       const __nv_bfloat16* __restrict__ wt,
+                                                       const float* __restrict__ bias, __nv_bfloat16* __restrict__ y,
+                                                       ConvArgs a) {
+  extern __shared__ float sm[];
+  const int KT = a.ci_g * a.k * a.k, ld = KT + 1;
+  float* patch = sm;                   // [128][KT + 1]
+  float* ws = sm + 128 * ld;           // [KT][co_g]
+  const int g = blockIdx.z, tid = threadIdx.x;
+  const int64_t M = (int64_t)a.N * a.Ho * a.Wo;
+  const int64_t m0 = (int64_t)blockIdx.x * 128;
+  for (int e = tid; e < KT * a.co_g; e += 256) {     // GEMM layout (co, k, k, ci_g): row o is K-contiguous
+    const int o = e / KT, kk = e % KT;
+    ws[kk * a.co_g + o] = __bfloat162float(wt[((int64_t)g * a.co_g + o) * KT + kk]);
+  }
+  for (int e = tid; e < 128 * KT; e += 256) {
+    const int p = e / KT, kk = e % KT;
+    const int tap = kk / a.ci_g, c = kk % a.ci_g;
+    const int64_t m = m0 + p;
+    float v = 0.f;
+    if (m < M) {
+      const int64_t hw = (int64_t)a.Ho * a.Wo;
+      const int n = (int)(m / hw), r = (int)(m % hw);
+      int h = (r / a.Wo) * a.s - a.pt + a.d * (tap / a.k), w = (r % a.Wo) * a.s - a.pl + a.d * (tap % a.k);
+      bool ok = true;
+      if (a.circ) { h = wrap(h, a.H); w = wrap(w, a.W); }
+      else ok = h >= 0 && h < a.H && w >= 0 && w < a.W;
+      if (ok) v = __bfloat162float(x[(((int64_t)n * a.H + h) * a.W + w) * a.Ci + g * a.ci_g + c]);
+    }
+    patch[p * ld + kk] = v;
+  }
+  __syncthreads();
+  const int p = tid & 127, half = tid >> 7;
+  const int64_t m = m0 + p;
+  if (m >= M) return;
+  const int cpt = a.co_g / 2;          // channels per thread (co_g % 16 == 0)
+  for (int c0 = half * cpt; c0 < (half + 1) * cpt; c0 += 8) {
+    float acc[8] = {};
+    for (int kk = 0; kk < KT; ++kk) {
+      const float av = patch[p * ld + kk];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = fmaf(av, ws[kk * a.co_g + c0 + j], acc[j]);
+    }
+    uint32_t pk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float v0 = acc[2 * j], v1 = acc[2 * j + 1];
+      if (bias) { v0 += bias[g * a.co_g + c0 + 2 * j]; v1 += bias[g * a.co_g + c0 + 2 * j + 1]; }
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
+      pk[j] = *reinterpret_cast<uint32_t*>(&b2);
+    }
+    *reinterpret_cast<uint4*>(y + m * a.Co + g * a.co_g + c0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+}
+
 ConvArgs make_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo) {
   ConvArgs a;
   a.N = N; a.H = H; a.W = W; a.Ci = L.ci_f; a.Co = L.co_f; a.ci_g = L.ci; a.co_g = L.co;
@@ -218,6 +276,21 @@ int launch_conv_fwd(const LayerInfo& L, const void* kernel, const float* bias, c
     return launch_conv_fwd_tc(L, kernel, bias, x, y, N, H, W, Ho, Wo, stream);
   const ConvArgs a = make_args(L, N, H, W, Ho, Wo);
   const int64_t M = (int64_t)N * Ho * Wo;
+  const int KT = L.ci * L.k * L.k;
+  if (io == ORTH_BF16 && KT <= 64 && L.co % 16 == 0 && L.co_f % 8 == 0 && !getenv("ORTH_FORCE_SIMT")) {
+    const size_t smem = (size_t)(128 * (KT + 1) + KT * L.co) * sizeof(float);
+    if (smem <= 200 * 1024) {
+      static size_t attr = 0;
+      if (smem > 48 * 1024 && smem > attr) {
+        cudaFuncSetAttribute(conv_fwd_smallk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+      }
+      dim3 g2((unsigned)((M + 127) / 128), 1, (unsigned)L.g);
+      conv_fwd_smallk<<<g2, 256, smem, (cudaStream_t)stream>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)kernel,
+                                                               bias, (__nv_bfloat16*)y, a);
+      return (int)cudaGetLastError();
+    }
+  }
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((L.co + BN - 1) / BN), (unsigned)L.g);
   cudaStream_t s = (cudaStream_t)stream;
   if (io == ORTH_BF16)

@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const GemmDesc* __restric
       if (gj >= d.N) continue;
       float v = d.alpha * acc[i][j];
       if (C) v = fmaf(d.beta, C[(int64_t)gi * d.ldc + gj], v);
+      if (gi == gj) v += d.diag;
       D[(int64_t)gi * d.ldd + gj] = v;
     }
   }
@@ -196,18 +197,15 @@ __global__ void __launch_bounds__(256) power_finalize_kernel(const MatItem* __re
     }
     return;
   }
-  float ss = 0.f;
-  if (threadIdx.x == 0)
-    for (int c = 0; c < M.nchunks; ++c) ss += partial[(int64_t)(M.chunk0 + c) * stride + n];
-  if (threadIdx.x == 0) red[0] = ss;
-  __syncthreads();
-  ss = red[0];
-  __syncthreads();
+  // |Wv|^2: one chunk per thread (nchunks <= 64), fixed-tree block sum
+  float ss = threadIdx.x < M.nchunks ? partial[(int64_t)(M.chunk0 + threadIdx.x) * stride + n] : 0.f;
+  ss = block_sum(ss, red);
   const bool bad = !(ss > 0.f) || !isfinite(ss);
   const float inv_wv = bad ? 0.f : rsqrtf(ss);
   float nw = 0.f;
   for (int j = threadIdx.x; j < n; j += 256) {
     float w = 0.f;
+#pragma unroll 8
     for (int c = 0; c < M.nchunks; ++c) w += partial[(int64_t)(M.chunk0 + c) * stride + j];
     w *= inv_wv;
     vbuf[M.cache_off + j] = w;
@@ -239,7 +237,8 @@ __global__ void __launch_bounds__(256) scale_kernel(const PowerItem* __restrict_
 
 // |I - G|_F per owned matrix from its Gram; non-finite -> NOT_CONVERGED
 __global__ void __launch_bounds__(256) residual_kernel(const MatItem* __restrict__ mats, const float* __restrict__ G,
-                                                       float* __restrict__ res, int32_t* __restrict__ status) {
+                                                       float* __restrict__ res, int32_t* __restrict__ status,
+                                                       int is_r) {
   __shared__ float red[9];
   const MatItem M = mats[blockIdx.x];
   const int s = M.m < M.n ? M.m : M.n;
@@ -247,7 +246,7 @@ __global__ void __launch_bounds__(256) residual_kernel(const MatItem* __restrict
   float a = 0.f;
   for (int64_t e = threadIdx.x; e < (int64_t)s * s; e += 256) {
     const int i = (int)(e / s), j = (int)(e % s);
-    const float r = (i == j ? 1.f : 0.f) - g[e];
+    const float r = is_r ? g[e] : (i == j ? 1.f : 0.f) - g[e];
     a = fmaf(r, r, a);
   }
   a = block_sum(a, red);
@@ -301,7 +300,15 @@ int launch_scale(Plan& p, const float* W, float* X0, void* stream) {
 int launch_residual(Plan& p, float* residual_out, void* stream) {
   if (p.mat_items.empty()) return 0;
   residual_kernel<<<(int)p.mat_items.size(), 256, 0, (cudaStream_t)stream>>>(p.d_mat_items, p.d_gram, residual_out,
-                                                                             p.d_status);
+                                                                             p.d_status, 0);
+  p.launches++;
+  return (int)cudaGetLastError();
+}
+
+int launch_residual_r(Plan& p, float* residual_out, void* stream) {
+  if (p.mat_items.empty()) return 0;
+  residual_kernel<<<(int)p.mat_items.size(), 256, 0, (cudaStream_t)stream>>>(p.d_mat_items, p.d_gram, residual_out,
+                                                                             p.d_status, 1);
   p.launches++;
   return (int)cudaGetLastError();
 }

@@ -55,15 +55,19 @@ struct GemmDesc {
   int64_t sa_m, sa_k, sb_k, sb_n;
   int64_t c_off, ldc, d_off, ldd;
   float alpha, beta;
+  float diag;           // added on the diagonal of D (residual-form Gram R = I - X^T X)
   int32_t seg_begin, seg_count;
-  int32_t tile_begin;   // first global tile of this problem
+  int32_t tile_begin;   // first global tile of this problem (SIMT 64x64 tiles)
   int32_t tiles_n;      // tiles along N
+  int32_t tc_tile_begin;  // same for the tensor-core kernel (128 x 128 tiles)
+  int32_t tc_tiles_n;
 };
 
 struct GemmPhase {        // one launch: a batch of independent problems
   std::vector<GemmDesc> descs;
   std::vector<GemmSeg> segs;
   int32_t total_tiles = 0;
+  int32_t tc_total_tiles = 0;
   // device copies (inside the plan's descriptor arena)
   GemmDesc* d_descs = nullptr;
   GemmSeg* d_segs = nullptr;
@@ -106,6 +110,8 @@ struct Plan {
 
   // NS phases (built once): gram and update per parity of the X buffer
   GemmPhase gram[2], update[2];     // [0]: X in BUF_X -> out BUF_Y ; [1]: X in BUF_Y -> out BUF_X
+  // residual form for the tensor-core path: R = I - Gram(X); X' = X + beta * (X R | R X)
+  GemmPhase gram_r[2], update_r[2];
   std::vector<PowerItem> power_items;
   std::vector<int32_t> owned_mats;  // indices of owned, non-empty matrices
   std::vector<MatItem> mat_items;   // same order as owned_mats
@@ -138,6 +144,10 @@ void set_error(const char* fmt, ...);
 
 // kernel launchers (CUDA translation units); return 0 or a cudaError_t value
 int launch_gemm_f32(const GemmPhase& ph, float* const bufs[BUF_COUNT], void* stream);
+// tensor-core batched GEMM: BF16 operands converted from FP32 on load, FP32
+// accumulation in TMEM; npass = 1 (bf16) or 3 (hi*hi + hi*lo + lo*hi split)
+int launch_gemm_tc(const GemmPhase& ph, float* const bufs[BUF_COUNT], int npass, void* stream);
+int launch_residual_r(Plan& p, float* residual_out, void* stream);
 int launch_power_partial(Plan& p, const float* W, const float* v_in, int use_const_v, int frob, void* stream);
 int launch_power_finalize(Plan& p, float* v_out, int frob, int write_sigma_only, void* stream);
 int launch_scale(Plan& p, const float* W, float* X0, void* stream);

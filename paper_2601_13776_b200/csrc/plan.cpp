@@ -35,7 +35,7 @@ static orth_status_t validate_opts(const orth_opts_t& o) {
   if (!(o.beta > 0.0f && o.beta <= 0.5f)) { set_error("beta must be in (0, 1/2] (P:311), got %g", o.beta); return ORTH_ERR_INVALID_ARGUMENT; }
   if (o.prescale != ORTH_PRESCALE_POWER && o.prescale != ORTH_PRESCALE_FROBENIUS) { set_error("bad prescale %d", o.prescale); return ORTH_ERR_INVALID_ARGUMENT; }
   if (o.prescale == ORTH_PRESCALE_POWER && o.power_iters < 1) { set_error("power_iters must be >= 1"); return ORTH_ERR_INVALID_ARGUMENT; }
-  if (o.compute != ORTH_F32 && o.compute != ORTH_BF16) { set_error("bad compute dtype %d", o.compute); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (o.compute != ORTH_F32 && o.compute != ORTH_BF16 && o.compute != ORTH_BF16X3) { set_error("bad compute mode %d", o.compute); return ORTH_ERR_INVALID_ARGUMENT; }
   if (o.polish_iters < 0 || o.polish_iters > o.ns_iters) { set_error("polish_iters must be in [0, ns_iters]"); return ORTH_ERR_INVALID_ARGUMENT; }
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) { set_error("bad rank/world %d/%d", o.rank, o.world); return ORTH_ERR_INVALID_ARGUMENT; }
   return ORTH_OK;
@@ -190,14 +190,19 @@ static void layout(Plan& P) {
 }
 
 static void finish_phase(GemmPhase& ph) {
-  int32_t t = 0;
+  int32_t t = 0, tt = 0;
   for (auto& d : ph.descs) {
     const int tm = (d.M + 63) / 64, tn = (d.N + 63) / 64;
     d.tile_begin = t;
     d.tiles_n = tn;
     t += tm * tn;
+    const int um = (d.M + 127) / 128, un = (d.N + 127) / 128;
+    d.tc_tile_begin = tt;
+    d.tc_tiles_n = un;
+    tt += um * un;
   }
   ph.total_tiles = t;
+  ph.tc_total_tiles = tt;
 }
 
 static GemmDesc mk(int M, int N, int K) {
@@ -261,6 +266,13 @@ static void build_ns(Plan& P) {
     }
     finish_phase(g);
     finish_phase(u);
+    // residual form (tensor-core path): R = I - Gram, X' = X + b * (X R | R X)
+    GemmPhase& gr = P.gram_r[par];
+    GemmPhase& ur = P.update_r[par];
+    gr = g;
+    ur = u;
+    for (auto& d : gr.descs) { d.alpha = -1.0f; d.diag = 1.0f; }
+    for (auto& e : ur.descs) { e.alpha = b; e.beta = 1.0f; }
   }
   // pre-scaling work items: ~4 CTAs per SM in total, split by rows
   P.power_items.clear();
@@ -271,10 +283,9 @@ static void build_ns(Plan& P) {
   int chunk = 0;
   for (int i : P.owned_mats) {
     const MatInfo& M = P.mats[i];
-    const double frac = (double)M.m * M.n / std::max(tot, 1.0);
-    int64_t nc = (int64_t)std::llround(592.0 * frac);
+    // >= 32K elements per CTA, <= 64 partial chunks per matrix (finalize reduces them in order)
+    int64_t nc = std::min<int64_t>(64, (M.m * M.n + 32767) / 32768);
     nc = std::max<int64_t>(1, std::min<int64_t>(nc, M.m));
-    nc = std::max<int64_t>(nc, std::min<int64_t>(M.m, (M.m * M.n + 262143) / 262144));  // <= 256K elements per CTA
     nc = std::max<int64_t>(nc, (M.m + 4095) / 4096);                                   // <= 4096 rows per CTA
     const int64_t rpc = (M.m + nc - 1) / nc;
     MatItem mi{};
@@ -450,7 +461,8 @@ static orth_status_t allocate(Plan& P) {
   const size_t o_pi = take(std::max<size_t>(P.power_items.size(), 1) * sizeof(PowerItem));
   const size_t o_own = take(std::max<size_t>(P.mat_items.size(), 1) * sizeof(MatItem));
   const size_t o_emit = take(std::max<size_t>(P.emit.size(), 1) * sizeof(EmitItem));
-  std::vector<GemmPhase*> phases = {&P.gram[0], &P.gram[1], &P.update[0], &P.update[1], &P.proj, &P.aoc};
+  std::vector<GemmPhase*> phases = {&P.gram[0], &P.gram[1], &P.update[0], &P.update[1], &P.gram_r[0],
+                                    &P.gram_r[1], &P.update_r[0], &P.update_r[1], &P.proj, &P.aoc};
   for (auto& ph : P.chain) phases.push_back(&ph);
   std::vector<std::pair<size_t, size_t>> ph_off;
   for (auto* ph : phases)

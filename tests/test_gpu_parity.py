@@ -161,6 +161,7 @@ CONV_CASES = [  # (ci, co, k, s, d, g, mode, H, kind)
     (64, 64, 3, 1, 2, 1, "circular", 12, "conv"), (128, 128, 3, 1, 1, 2, "circular", 8, "conv"),
     (40, 64, 3, 1, 1, 1, "circular", 6, "conv"), (72, 128, 5, 2, 1, 1, "zeros", 9, "conv"),
     (512, 512, 3, 1, 1, 1, "circular", 4, "conv"), (64, 128, 3, 2, 3, 1, "circular", 12, "conv"),
+    (8, 32, 2, 2, 1, 2, "zeros", 9, "conv"), (3, 64, 3, 1, 1, 1, "zeros", 13, "conv"),
 ]
 
 
@@ -262,3 +263,48 @@ def test_whole_path_cfg2_bf16_chain_sampled(cuda_lib):
     xn = torch.linalg.vector_norm(dev(x).reshape(N, -1), dim=1)
     yn = torch.linalg.vector_norm(outs[-1].float().reshape(N, -1), dim=1)
     assert bool((yn <= xn * 1.02).all())
+
+
+# ------------------------------------------------------------------ tensor-core construction modes
+TC_LAYERS = [dict(kind=k, c_in=ci, c_out=co, k=kk, s=s, d=d, g=g, padding_mode="circular")
+             for (ci, co, kk, s, d, g, k) in [
+                 (16, 16, 3, 1, 1, 1, "conv"), (4, 8, 3, 2, 1, 1, "conv"), (8, 16, 3, 2, 1, 2, "conv"),
+                 (6, 9, 5, 3, 2, 3, "conv"), (3, 64, 4, 4, 1, 1, "conv"), (96, 80, 3, 1, 1, 1, "conv"),
+                 (4, 8, 3, 2, 1, 2, "convT"), (70, 70, 1, 1, 1, 1, "dense"), (33, 130, 1, 1, 1, 1, "dense"),
+                 (200, 136, 1, 1, 1, 1, "dense")]]
+
+
+# bf16x3: every product through the 3-pass hi/lo split (~2^-16); measured ~2e-5 on chained BCOP kernels, so 1e-4
+@pytest.mark.parametrize("mode,tol", [("bf16", TOL16), ("bf16x3", 1e-4)])
+@pytest.mark.parametrize("which", ["small", "cfg2"])
+def test_construction_parity_tensor_cores(cuda_lib, mode, tol, which):
+    layers = TC_LAYERS if which == "small" else configs.cfg2()
+    cfg_id = 14 if which == "small" else 2
+    plan, mats, _, ortho, res, _, kf, kb = gpu_construct(cuda_lib, layers, cfg_id, compute=mode)
+    o_ortho, _, o_k = oracle_construct(layers, mats)
+    ortho_h, kf_h = ortho.cpu().numpy(), torch.from_numpy(kf.cpu().numpy())
+    worst = 0.0
+    for i, X in enumerate(o_ortho):
+        if X.size == 0:
+            continue
+        e = rel(unpack(plan, ortho_h, i), X)
+        worst = max(worst, e)
+        assert e < tol, (i, plan.matrices[i], e)
+    for l, K in enumerate(o_k):
+        assert rel(plan.kernel_f32(kf_h, l).numpy(), K) < tol, l
+    # orthogonality of the result (north star: max|sigma - 1| <= 1e-3); |I - X^T X|_F bounds it
+    assert float(res.max()) < 1e-3
+    print(f"{mode} {which}: worst matrix rel err {worst:.2e}, max residual {float(res.max()):.2e}")
+
+
+def test_tensor_core_kernels_orthogonal_toeplitz(cuda_lib):
+    layers = [dict(kind="conv", c_in=ci, c_out=co, k=k, s=s, d=1, g=g, padding_mode="circular")
+              for (ci, co, k, s, g) in [(16, 16, 3, 1, 1), (4, 8, 3, 2, 1), (8, 8, 4, 2, 2)]]
+    plan, _, _, _, _, _, kf, _ = gpu_construct(cuda_lib, layers, 15, compute="bf16")
+    kf_h = torch.from_numpy(kf.cpu().numpy())
+    for l, d in enumerate(layers):
+        K = plan.kernel_f32(kf_h, l).numpy().astype(np.float64)
+        OL = oracle_layer(d)
+        T = O.toeplitz(lambda x: O.conv2d(x, K, s=OL.s, d=OL.d, g=OL.g), (d["c_in"], 8, 8))
+        sv = np.linalg.svd(T, compute_uv=False)[: min(T.shape)]
+        assert np.abs(sv - 1).max() < 1e-3, (l, sv.min(), sv.max())

@@ -74,29 +74,35 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
       if (!e) e = launch_power_finalize(P, (it == Pn - 1) ? power_cache : nullptr, 0, 0, stream);
     }
   }
-  if (!e) e = launch_scale(P, params, x0, stream);
   const int mode = P.opts.compute;
-  for (int t = 0; t < T && !e; ++t) {
-    if (mode == ORTH_F32) {
+  if (mode == ORTH_F32) {
+    if (!e) e = launch_scale(P, params, x0, stream);
+    for (int t = 0; t < T && !e; ++t) {
       e = launch_gemm_f32(P.gram[par], bufs, stream);
       if (!e) e = launch_gemm_f32(P.update[par], bufs, stream);
-    } else {
-      const int np = (mode == ORTH_BF16X3 || t >= T - P.opts.polish_iters) ? 3 : 1;
-      e = launch_gemm_tc(P.gram_r[par], bufs, np, stream);
-      if (!e) e = launch_gemm_tc(P.update_r[par], bufs, np == 3 && mode == ORTH_BF16X3 ? 3 : 1, stream);
+      P.launches += 2;
+      par ^= 1;
     }
-    P.launches += 2;
-    par ^= 1;
-  }
-  if (!e && residual_out) {
-    if (mode == ORTH_F32) {
+    if (!e && residual_out) {
       e = launch_gemm_f32(P.gram[0], bufs, stream);
       if (!e) e = launch_residual(P, residual_out, stream);
-    } else {
-      e = launch_gemm_tc(P.gram_r[0], bufs, 3, stream);
+      P.launches++;
+    }
+  } else {
+    // tensor cores: Gram passes g(t), update passes u(t); operand copies carry lo halves when read by a 3-pass GEMM
+    auto gp = [&](int t) { return (mode == ORTH_BF16X3 || t >= T - P.opts.polish_iters) ? 3 : 1; };
+    auto up = [&](int t) { return mode == ORTH_BF16X3 ? 3 : 1; };
+    auto x_lo = [&](int t) { return t >= T || gp(t) == 3 || up(t) == 3; };   // t == T: the residual Gram
+    if (!e) e = launch_scale_bf16(P, params, x0, par, x_lo(0), stream);
+    for (int t = 0; t < T && !e; ++t) {
+      e = launch_ns_tc(P, bufs, par, true, gp(t), up(t) == 3, stream);
+      if (!e) e = launch_ns_tc(P, bufs, par, false, up(t), x_lo(t + 1), stream);
+      par ^= 1;
+    }
+    if (!e && residual_out) {
+      e = launch_ns_tc(P, bufs, 0, true, 3, false, stream);
       if (!e) e = launch_residual_r(P, residual_out, stream);
     }
-    P.launches++;
   }
   return cuda_fail(e, "orth_orthogonalize");
 }

@@ -25,6 +25,8 @@ struct MatInfo {
   int64_t off;        // float offset in params / ortho / scratch
   int64_t cache_off;  // float offset in power cache / v workspace
   int64_t gram_off;   // float offset of its short-side Gram in the G workspace
+  int64_t bx_off;     // bf16 offset in the X / X^T copies (tensor-core NS)
+  int64_t br_off;     // bf16 offset in the R copies
   int32_t owned;      // 1 if this rank orthogonalises it
 };
 
@@ -73,10 +75,27 @@ struct GemmPhase {        // one launch: a batch of independent problems
   GemmSeg* d_segs = nullptr;
 };
 
+// Tensor-core NS problem (ns_tc.cu).  Operands are BF16 copies of X, X^T and
+// R = I - Gram kept in plan workspace (row stride padded to 8 elements, so
+// every row is 16-byte aligned and zero-padded), written by the previous
+// phase's epilogue.  kinds: 0 = X (m x n), 1 = X^T (n x m), 2 = R (s x s).
+struct NsDesc {
+  int32_t M, N, K;
+  int32_t a_kind, b_kind;
+  int32_t epi;              // 0: Gram epilogue (R fp32 + bf16), 1: update epilogue (X' fp32 + bf16 X', X'^T)
+  int64_t a_off, lda, b_off, ldb;
+  int64_t f_off, ldf;       // fp32 offset/ld of D (and C for the update)
+  int64_t bx_off;           // offset of this matrix in the bf16 X / X^T buffers
+  int64_t br_off;           // offset of this matrix in the bf16 R buffers
+  int32_t ldx, ldxt, ldr;   // padded bf16 leading dims: pad8(n), pad8(m), pad8(s)
+  float alpha, beta, diag;
+  int32_t tile_begin, tiles_n;
+};
+
 struct PowerItem {        // one CTA of the pre-scaling kernels: rows [r0, r1) of matrix `mat`
   int32_t mat, r0, r1, chunk;   // chunk: global partial slot
-  int32_t n, pad_;
-  int64_t off, cache_off;
+  int32_t n, m;
+  int64_t off, cache_off, bx_off;
 };
 
 struct MatItem {          // one owned, non-empty matrix (finalize / residual kernels)
@@ -112,6 +131,14 @@ struct Plan {
   GemmPhase gram[2], update[2];     // [0]: X in BUF_X -> out BUF_Y ; [1]: X in BUF_Y -> out BUF_X
   // residual form for the tensor-core path: R = I - Gram(X); X' = X + beta * (X R | R X)
   GemmPhase gram_r[2], update_r[2];
+  // tensor-core NS on BF16 operand copies (ns_tc.cu)
+  std::vector<NsDesc> ns_gram, ns_upd;
+  int32_t ns_gram_tiles = 0, ns_upd_tiles = 0;
+  NsDesc* d_ns_gram = nullptr;
+  NsDesc* d_ns_upd = nullptr;
+  int64_t bx_numel = 0, br_numel = 0;
+  uint16_t* d_bx = nullptr;         // 8 x bx_numel: Xh[2], Xl[2], XTh[2], XTl[2]
+  uint16_t* d_br = nullptr;         // 2 x br_numel: Rh, Rl
   std::vector<PowerItem> power_items;
   std::vector<int32_t> owned_mats;  // indices of owned, non-empty matrices
   std::vector<MatItem> mat_items;   // same order as owned_mats
@@ -148,6 +175,12 @@ int launch_gemm_f32(const GemmPhase& ph, float* const bufs[BUF_COUNT], void* str
 // accumulation in TMEM; npass = 1 (bf16) or 3 (hi*hi + hi*lo + lo*hi split)
 int launch_gemm_tc(const GemmPhase& ph, float* const bufs[BUF_COUNT], int npass, void* stream);
 int launch_residual_r(Plan& p, float* residual_out, void* stream);
+// tensor-core NS phase on the BF16 copies.  par: parity of the current X
+// (0: BUF_X, 1: BUF_Y).  gram: Gram (else update).  npass 1|3.  write_lo:
+// the epilogue also writes the lo halves of its BF16 outputs.
+int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int npass, bool write_lo, void* stream);
+// X0 = W / sigma (fp32) plus its BF16 copies X0, X0^T (hi, and lo if write_lo)
+int launch_scale_bf16(Plan& p, const float* W, float* X0, int par, bool write_lo, void* stream);
 int launch_power_partial(Plan& p, const float* W, const float* v_in, int use_const_v, int frob, void* stream);
 int launch_power_finalize(Plan& p, float* v_out, int frob, int write_sigma_only, void* stream);
 int launch_scale(Plan& p, const float* W, float* X0, void* stream);

@@ -161,11 +161,15 @@ static void assign_owners(Plan& P) {
 static void layout(Plan& P) {
   int64_t off = 0, coff = 0, goff = 0;
   P.ns_flops = 0.0;
+  P.bx_numel = 0;
+  P.br_numel = 0;
   for (auto& M : P.mats) {
     M.off = off; off += pad_up(M.m * M.n, kPadF32);
     M.cache_off = coff; coff += pad_up(M.n, kPadF32);
     const int64_t s = std::min(M.m, M.n);
     M.gram_off = goff; goff += pad_up(s * s, kPadF32);
+    M.bx_off = P.bx_numel; P.bx_numel += pad_up(pad_up(M.m, 8) * pad_up(M.n, 8), kPadBF16);
+    M.br_off = P.br_numel; P.br_numel += pad_up(pad_up(s, 8) * pad_up(s, 8), kPadBF16);
     M.owned = P.layers[M.layer].owner == P.opts.rank;
     if (M.owned) {
       const double a = (double)std::max(M.m, M.n), b = (double)s;
@@ -274,6 +278,40 @@ static void build_ns(Plan& P) {
     for (auto& d : gr.descs) { d.alpha = -1.0f; d.diag = 1.0f; }
     for (auto& e : ur.descs) { e.alpha = b; e.beta = 1.0f; }
   }
+  // tensor-core NS on BF16 copies: Gram R = I - X^T X (tall: A = B = X^T rows) or
+  // I - X X^T (wide: A = B = X rows); update X' = X + b X R (tall: A = X, B = R)
+  // or X + b R X (wide: A = R, B = X^T rows).  R is symmetric, so its rows serve as B.
+  P.ns_gram.clear();
+  P.ns_upd.clear();
+  int32_t tg = 0, tu = 0;
+  for (int i : P.owned_mats) {
+    const MatInfo& M = P.mats[i];
+    const int m = (int)M.m, n = (int)M.n, s = std::min(m, n);
+    NsDesc base{};
+    base.bx_off = M.bx_off; base.br_off = M.br_off;
+    base.ldx = (int32_t)pad_up(n, 8); base.ldxt = (int32_t)pad_up(m, 8); base.ldr = (int32_t)pad_up(s, 8);
+    NsDesc g = base;
+    g.M = s; g.N = s; g.K = std::max(m, n);
+    g.a_kind = g.b_kind = (m >= n) ? 1 : 0;
+    g.a_off = g.b_off = M.bx_off;
+    g.lda = g.ldb = (m >= n) ? base.ldxt : base.ldx;
+    g.epi = 0; g.f_off = M.gram_off; g.ldf = s;
+    g.alpha = -1.0f; g.beta = 0.0f; g.diag = 1.0f;
+    g.tile_begin = tg; g.tiles_n = (s + 127) / 128;
+    tg += ((s + 127) / 128) * g.tiles_n;
+    P.ns_gram.push_back(g);
+    NsDesc u = base;
+    u.M = m; u.N = n; u.K = s;
+    if (m >= n) { u.a_kind = 0; u.a_off = M.bx_off; u.lda = base.ldx; u.b_kind = 2; u.b_off = M.br_off; u.ldb = base.ldr; }
+    else { u.a_kind = 2; u.a_off = M.br_off; u.lda = base.ldr; u.b_kind = 1; u.b_off = M.bx_off; u.ldb = base.ldxt; }
+    u.epi = 1; u.f_off = M.off; u.ldf = n;
+    u.alpha = b; u.beta = 1.0f; u.diag = 0.0f;
+    u.tile_begin = tu; u.tiles_n = (n + 127) / 128;
+    tu += ((m + 127) / 128) * u.tiles_n;
+    P.ns_upd.push_back(u);
+  }
+  P.ns_gram_tiles = tg;
+  P.ns_upd_tiles = tu;
   // pre-scaling work items: ~4 CTAs per SM in total, split by rows
   P.power_items.clear();
   P.mat_items.clear();
@@ -294,7 +332,7 @@ static void build_ns(Plan& P) {
     for (int64_t r0 = 0; r0 < M.m; r0 += rpc) {
       PowerItem it{};
       it.mat = i; it.r0 = (int32_t)r0; it.r1 = (int32_t)std::min<int64_t>(M.m, r0 + rpc); it.chunk = chunk++;
-      it.n = (int32_t)M.n; it.off = M.off; it.cache_off = M.cache_off;
+      it.n = (int32_t)M.n; it.m = (int32_t)M.m; it.off = M.off; it.cache_off = M.cache_off; it.bx_off = M.bx_off;
       P.power_items.push_back(it);
     }
     mi.nchunks = chunk - mi.chunk0;
@@ -461,6 +499,10 @@ static orth_status_t allocate(Plan& P) {
   const size_t o_pi = take(std::max<size_t>(P.power_items.size(), 1) * sizeof(PowerItem));
   const size_t o_own = take(std::max<size_t>(P.mat_items.size(), 1) * sizeof(MatItem));
   const size_t o_emit = take(std::max<size_t>(P.emit.size(), 1) * sizeof(EmitItem));
+  const size_t o_nsg = take(std::max<size_t>(P.ns_gram.size(), 1) * sizeof(NsDesc));
+  const size_t o_nsu = take(std::max<size_t>(P.ns_upd.size(), 1) * sizeof(NsDesc));
+  const size_t o_bx = take((size_t)8 * std::max<int64_t>(P.bx_numel, 64) * 2);
+  const size_t o_br = take((size_t)2 * std::max<int64_t>(P.br_numel, 64) * 2);
   std::vector<GemmPhase*> phases = {&P.gram[0], &P.gram[1], &P.update[0], &P.update[1], &P.gram_r[0],
                                     &P.gram_r[1], &P.update_r[0], &P.update_r[1], &P.proj, &P.aoc};
   for (auto& ph : P.chain) phases.push_back(&ph);
@@ -485,7 +527,15 @@ static orth_status_t allocate(Plan& P) {
   P.d_power_items = (PowerItem*)(base + o_pi);
   P.d_mat_items = (MatItem*)(base + o_own);
   P.d_emit = (EmitItem*)(base + o_emit);
-  cudaError_t e = cudaMemset(P.d_arena, 0, off);
+  P.d_ns_gram = (NsDesc*)(base + o_nsg);
+  P.d_ns_upd = (NsDesc*)(base + o_nsu);
+  P.d_bx = (uint16_t*)(base + o_bx);
+  P.d_br = (uint16_t*)(base + o_br);
+  cudaError_t e = cudaMemset(P.d_arena, 0, off);   // also zero-pads the BF16 operand copies
+  if (!P.ns_gram.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_ns_gram, P.ns_gram.data(), P.ns_gram.size() * sizeof(NsDesc), cudaMemcpyHostToDevice);
+  if (!P.ns_upd.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_ns_upd, P.ns_upd.data(), P.ns_upd.size() * sizeof(NsDesc), cudaMemcpyHostToDevice);
   if (!P.power_items.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_power_items, P.power_items.data(), P.power_items.size() * sizeof(PowerItem), cudaMemcpyHostToDevice);
   if (!P.mat_items.empty() && e == cudaSuccess)

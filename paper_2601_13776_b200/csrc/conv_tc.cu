@@ -6,14 +6,23 @@
 // K = (tap, channel), A[m, (a,b,c)] = x~[n, s*u + d*a - p_t, s*v + d*b - p_l, g*ci_g + c]
 // and B = the BF16 GEMM-layout kernel (C_o, k, k, C_i/g), already K-major.
 //
-// CTA = 256 threads, tile 128 pixels x BN channels, K block = one tap x 64
-// channels (one 128-byte swizzled row per pixel / output channel).  All
-// threads gather A and B with 16-byte cp.async (zero-fill for padding / tails,
-// index wrap for circular padding) into an S-stage ring; one thread issues 4
-// tcgen05.mma (M=128, N=BN, K=16) per block and commits to the stage's
-// mbarrier, which gates the reuse of that stage.  The accumulator lives in
-// TMEM; the epilogue (8 warps: lane quarter x column half) adds the bias,
-// rounds to BF16 (RNE) and stores NHWC rows.
+// Persistent, warp-specialised kernel (one CTA per SM, 416 threads):
+//   warps 0-7   producers.  Per tile they first build a (tap, row) -> input
+//               pixel table in shared memory (-1 = zero padding; circular
+//               padding wraps here), so the per-stage gather is a table read
+//               plus a 16-byte cp.async per (row, 8-channel chunk) into an
+//               S-stage SWIZZLE_128B ring (zero-fill for padding / tails).
+//               After cp.async.wait_group + fence.proxy.async they arrive on
+//               the stage's `full` mbarrier, LAG stages behind.
+//   warp 8      TMEM allocation + one thread issuing tcgen05.mma (M=128, N=BN,
+//               K=16, x4 per stage) into one of two TMEM accumulators,
+//               committing to the stage's `empty` barrier and, per tile, `tfull`.
+//   warps 9-12  epilogue: tcgen05.ld of their 32-lane quarter, bias, RNE to
+//               BF16, NHWC stores; arrive on `tempty`.
+// The accumulator is double-buffered, so the epilogue of tile t overlaps the
+// mainloop of tile t+1.  (Measured: a single producer warp per SM sub-partition
+// was instruction-latency bound at ~2.5k cycles per stage; the table cuts the
+// per-row work to a load, a compare and an address multiply.)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -27,8 +36,13 @@ namespace {
 
 struct TcConvArgs {
   int N, H, W, Ci, Co, ci_g, co_g, k, s, d, pt, pl, Ho, Wo, circ;
-  int tiles_m;
+  int tiles_m, tiles_n, num_tiles;
 };
+
+constexpr int NPROD = 256;                 // producer threads (warps 0-7)
+constexpr int MMA_WARP = 8;
+constexpr int NTHREADS = NPROD + 32 + 128;
+constexpr int MAX_TAPS = 49;               // k <= 7
 
 __device__ __forceinline__ int wrapi(int x, int n) {
   x %= n;
@@ -36,156 +50,199 @@ __device__ __forceinline__ int wrapi(int x, int n) {
 }
 
 template <int BN, int S>
-__global__ void __launch_bounds__(256, 1)
-    conv_fwd_tc(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+__global__ void __launch_bounds__(NTHREADS, 1)
+    conv_fwd_ws(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
                 const float* __restrict__ bias, __nv_bfloat16* __restrict__ y, TcConvArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128;
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + S * A_BYTES;
-  __shared__ uint64_t empty_bar[S];
-  __shared__ uint64_t done_bar;
+  constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
+  constexpr int LAG = S - 2;   // stages of cp.async kept in flight per producer thread
+  int* tab = reinterpret_cast<int*>(smem + S * STAGE);   // [taps][128] input pixel index, -1 = padding
+  __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int rn[128], rh[128], rw[128];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = blockIdx.z;
-  const int n0 = blockIdx.y * BN;
-  const int64_t M = (int64_t)a.N * a.Ho * a.Wo;
-  const int64_t m0 = (int64_t)blockIdx.x * 128;
-
-  if (warp == 0) umma::tmem_alloc(&tmem_base_sh, BN);
-  if (tid == 32) {
-    for (int i = 0; i < S; ++i) umma::mbar_init(&empty_bar[i], 1);
-    umma::mbar_init(&done_bar, 1);
-    umma::fence_mbar_init();
-  }
-  if (tid < 128) {
-    const int64_t m = m0 + tid;
-    if (m < M) {
-      const int64_t hw = (int64_t)a.Ho * a.Wo;
-      const int n = (int)(m / hw), r = (int)(m % hw);
-      rn[tid] = n;
-      rh[tid] = (r / a.Wo) * a.s - a.pt;
-      rw[tid] = (r % a.Wo) * a.s - a.pl;
-    } else {
-      rn[tid] = -1; rh[tid] = 0; rw[tid] = 0;
+  if (warp == MMA_WARP) umma::tmem_alloc(&tmem_base_sh, 2 * BN);
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      umma::mbar_init(&full_bar[i], NPROD);
+      umma::mbar_init(&empty_bar[i], 1);
     }
+    for (int i = 0; i < 2; ++i) {
+      umma::mbar_init(&tfull_bar[i], 1);
+      umma::mbar_init(&tempty_bar[i], 128);
+    }
+    umma::fence_mbar_init();
   }
   umma::tc_fence_before();
   __syncthreads();
   umma::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-
+  const uint32_t s0 = umma::smem_u32(smem);
   const int kc = (a.ci_g + 63) / 64;
   const int kk2 = a.k * a.k;
   const int nk = kk2 * kc;
-  constexpr uint32_t IDESC = umma::idesc_bf16(128, BN);
-  const uint32_t sA0 = umma::smem_u32(sA), sB0 = umma::smem_u32(sB);
+  const int M = a.N * a.Ho * a.Wo;
+  const int hw = a.Ho * a.Wo;
 
-  for (int kb = 0; kb < nk + S - 1; ++kb) {
-    if (kb < nk) {
-      const int st = kb % S;
-      if (kb >= S) umma::mbar_wait(&empty_bar[st], ((kb / S) - 1) & 1);
-      const int tap = kb / kc, c0 = (kb % kc) * 64;
-      const int ta = tap / a.k, tb = tap % a.k;
-      const int c = tid & 7;
-      const bool cok = c0 + c * 8 < a.ci_g;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = (tid >> 3) + 32 * i;
-        const int n = rn[r];
-        int h = rh[r] + a.d * ta, ww = rw[r] + a.d * tb;
-        bool ok = cok && n >= 0;
-        if (a.circ) {
-          h = wrapi(h, a.H);
-          ww = wrapi(ww, a.W);
-        } else {
-          ok = ok && h >= 0 && h < a.H && ww >= 0 && ww < a.W;
+  if (warp < MMA_WARP) {
+    // ------------------------------------------------------------ producers
+    const int c = tid & 7, rbase = tid >> 3;   // A rows rbase + 32 i, B rows rbase + 32 i
+    int it = 0;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+      const int tm = tile % a.tiles_m, rest = tile / a.tiles_m;
+      const int tn = rest % a.tiles_n, g = rest / a.tiles_n;
+      const int m0 = tm * 128, n0 = tn * BN;
+      umma::named_bar_sync(1, NPROD);          // everyone is done reading the previous table
+      for (int e = tid; e < 128 * kk2; e += NPROD) {
+        const int r = e & 127, t = e >> 7;
+        const int m = m0 + r;
+        int v = -1;
+        if (m < M) {
+          const int n = m / hw, rr = m - n * hw;
+          const int u = rr / a.Wo, vv = rr - u * a.Wo;
+          int h = u * a.s - a.pt + a.d * (t / a.k), ww = vv * a.s - a.pl + a.d * (t % a.k);
+          bool ok = true;
+          if (a.circ) {
+            h = wrapi(h, a.H);
+            ww = wrapi(ww, a.W);
+          } else {
+            ok = h >= 0 && h < a.H && ww >= 0 && ww < a.W;
+          }
+          if (ok) v = (n * a.H + h) * a.W + ww;
         }
-        const __nv_bfloat16* src =
-            ok ? x + (((int64_t)n * a.H + h) * a.W + ww) * a.Ci + (int64_t)g * a.ci_g + c0 + c * 8 : x;
-        umma::cp_async16(sA0 + st * A_BYTES + umma::sw128_off(r, c), src, ok);
+        tab[t * 128 + r] = v;
       }
+      umma::named_bar_sync(1, NPROD);
+      const __nv_bfloat16* xg = x + (int64_t)g * a.ci_g + c * 8;
+      const __nv_bfloat16* wg = w + ((int64_t)g * a.co_g + n0) * kk2 * a.ci_g + c * 8;
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int st = it % S;
+        umma::mbar_wait(&empty_bar[st], ((it / S) & 1) ^ 1);
+        const int tap = kb / kc, c0 = (kb - tap * kc) * 64;
+        const bool cok = c0 + c * 8 < a.ci_g;
+        const uint32_t sa = s0 + st * STAGE;
+        const int* trow = tab + tap * 128;
 #pragma unroll
-      for (int i = 0; i < BN / 32; ++i) {
-        const int r = (tid >> 3) + 32 * i;
-        const int o = n0 + r;
-        const bool ok = cok && o < a.co_g;
-        const __nv_bfloat16* src = ok ? w + (((int64_t)g * a.co_g + o) * kk2 + tap) * a.ci_g + c0 + c * 8 : w;
-        umma::cp_async16(sB0 + st * B_BYTES + umma::sw128_off(r, c), src, ok);
+        for (int i = 0; i < 4; ++i) {
+          const int r = rbase + 32 * i;
+          const int pix = trow[r];
+          const bool ok = cok && pix >= 0;
+          umma::cp_async16(sa + umma::sw128_off(r, c), ok ? xg + (int64_t)pix * a.Ci + c0 : x, ok);
+        }
+#pragma unroll
+        for (int i = 0; i < BN / 32; ++i) {
+          const int r = rbase + 32 * i;
+          const bool ok = cok && n0 + r < a.co_g;
+          umma::cp_async16(sa + A_BYTES + umma::sw128_off(r, c),
+                           ok ? wg + ((int64_t)r * kk2 + tap) * a.ci_g + c0 : w, ok);
+        }
+        umma::cp_async_commit();
+        if (it >= LAG) {
+          umma::cp_async_wait<LAG>();
+          umma::fence_proxy_async_smem();
+          umma::mbar_arrive(&full_bar[(it - LAG) % S]);
+        }
       }
     }
-    umma::cp_async_commit();
-    const int j = kb - (S - 1);
-    if (j >= 0) {
-      umma::cp_async_wait<S - 1>();
-      umma::fence_proxy_async_smem();
-      __syncthreads();
-      if (tid == 0) {
+    umma::cp_async_wait<0>();
+    umma::fence_proxy_async_smem();
+    for (int j = it - LAG < 0 ? 0 : it - LAG; j < it; ++j) umma::mbar_arrive(&full_bar[j % S]);
+  } else if (warp == MMA_WARP) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC = umma::idesc_bf16(128, BN);
+      int it = 0, tcount = 0;
+      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++tcount) {
+        const int acc = tcount & 1;
+        umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
         umma::tc_fence_after();
-        const int st = j % S;
-        const uint32_t a_addr = sA0 + st * A_BYTES, b_addr = sB0 + st * B_BYTES;
+        const uint32_t d_tmem = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int st = it % S;
+          umma::mbar_wait(&full_bar[st], (it / S) & 1);
+          umma::tc_fence_after();
+          const uint32_t aa = s0 + st * STAGE, bb = aa + A_BYTES;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          umma::mma_bf16(tmem, umma::sdesc_sw128(a_addr + 32 * q), umma::sdesc_sw128(b_addr + 32 * q), IDESC,
-                         (j | q) != 0);
-        umma::mma_commit(&empty_bar[st]);
+          for (int q = 0; q < 4; ++q)
+            umma::mma_bf16(d_tmem, umma::sdesc_sw128(aa + 32 * q), umma::sdesc_sw128(bb + 32 * q), IDESC,
+                           (kb | q) != 0);
+          umma::mma_commit(&empty_bar[st]);
+        }
+        umma::mma_commit(&tfull_bar[acc]);
       }
     }
-  }
-  if (tid == 0) umma::mma_commit(&done_bar);
-  umma::mbar_wait(&done_bar, 0);
-  umma::tc_fence_after();
-
-  // epilogue: warp -> (lane quarter q, column half)
-  const int q = warp & 3, half = warp >> 2;
-  const int r = q * 32 + lane;
-  const int64_t m = m0 + r;
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;               // TMEM lane quarter of this warp (warps 9..12 -> 1,2,3,0)
+    const int r = q * 32 + lane;
+    int tcount = 0;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++tcount) {
+      const int acc = tcount & 1;
+      umma::mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
+      umma::tc_fence_after();
+      const int tm = tile % a.tiles_m, rest = tile / a.tiles_m;
+      const int tn = rest % a.tiles_n, g = rest / a.tiles_n;
+      const int m = tm * 128 + r;
+      const int obase = g * a.co_g + tn * BN;
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 32) {
+        float v[32];
+        umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + cc), v);
+        if (m < M) {
+          const int o = obase + cc;
+          uint32_t pk[16];
 #pragma unroll
-  for (int cc = 0; cc < BN / 2; cc += 32) {
-    const int col = half * (BN / 2) + cc;
-    float v[32];
-    umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)col, v);
-    if (m < M) {
-      const int o = g * a.co_g + n0 + col;
-      uint32_t pk[16];
+          for (int i = 0; i < 16; ++i) {
+            float v0 = v[2 * i], v1 = v[2 * i + 1];
+            if (bias) { v0 += bias[o + 2 * i]; v1 += bias[o + 2 * i + 1]; }
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
+            pk[i] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(y + (int64_t)m * a.Co + o);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        float v0 = v[2 * i], v1 = v[2 * i + 1];
-        if (bias) { v0 += bias[o + 2 * i]; v1 += bias[o + 2 * i + 1]; }
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
-        pk[i] = *reinterpret_cast<uint32_t*>(&b2);
+          for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        }
       }
-      uint4* dst = reinterpret_cast<uint4*>(y + m * a.Co + o);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      umma::tc_fence_before();
+      umma::mbar_arrive(&tempty_bar[acc]);
     }
   }
   umma::tc_fence_before();
   __syncthreads();
-  if (warp == 0) umma::tmem_dealloc(tmem, BN);
+  if (warp == MMA_WARP) umma::tmem_dealloc(tmem, 2 * BN);
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 template <int BN, int S>
-int launch_tc(const LayerInfo& L, const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias,
-              __nv_bfloat16* y, TcConvArgs a, cudaStream_t stream) {
-  const size_t smem = 1024 + (size_t)S * (128 * 128 + BN * 128);
+int launch_ws(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias, __nv_bfloat16* y, TcConvArgs a,
+              cudaStream_t stream) {
+  const size_t smem = 1024 + (size_t)S * (128 * 128 + BN * 128) + (size_t)MAX_TAPS * 128 * 4;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(conv_fwd_tc<BN, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(conv_fwd_ws<BN, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  dim3 grid((unsigned)a.tiles_m, (unsigned)(L.co / BN), (unsigned)L.g);
-  conv_fwd_tc<BN, S><<<grid, 256, smem, stream>>>(x, w, bias, y, a);
+  const int grid = a.num_tiles < num_sms() ? a.num_tiles : num_sms();
+  conv_fwd_ws<BN, S><<<grid, NTHREADS, smem, stream>>>(x, w, bias, y, a);
   return (int)cudaGetLastError();
 }
 
 }  // namespace
 
 bool conv_fwd_tc_eligible(const LayerInfo& L) {
-  return L.co % 64 == 0 && L.ci % 8 == 0 && L.ci_f % 8 == 0 && L.co_f % 8 == 0;
+  return L.co % 64 == 0 && L.ci % 8 == 0 && L.ci_f % 8 == 0 && L.co_f % 8 == 0 && L.k * L.k <= MAX_TAPS;
 }
 
 int launch_conv_fwd_tc(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
@@ -200,9 +257,16 @@ int launch_conv_fwd_tc(const LayerInfo& L, const void* kernel, const float* bias
   auto ws = (const __nv_bfloat16*)kernel;
   auto ys = (__nv_bfloat16*)y;
   cudaStream_t s = (cudaStream_t)stream;
-  if (L.co % 256 == 0) return launch_tc<256, 4>(L, xs, ws, bias, ys, a, s);
-  if (L.co % 128 == 0) return launch_tc<128, 6>(L, xs, ws, bias, ys, a, s);
-  return launch_tc<64, 8>(L, xs, ws, bias, ys, a, s);
+  if (L.co % 256 == 0) {
+    a.tiles_n = L.co / 256; a.num_tiles = a.tiles_m * a.tiles_n * L.g;
+    return launch_ws<256, 4>(xs, ws, bias, ys, a, s);
+  }
+  if (L.co % 128 == 0) {
+    a.tiles_n = L.co / 128; a.num_tiles = a.tiles_m * a.tiles_n * L.g;
+    return launch_ws<128, 5>(xs, ws, bias, ys, a, s);
+  }
+  a.tiles_n = L.co / 64; a.num_tiles = a.tiles_m * a.tiles_n * L.g;
+  return launch_ws<64, 7>(xs, ws, bias, ys, a, s);
 }
 
 }  // namespace orth

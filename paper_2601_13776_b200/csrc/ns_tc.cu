@@ -132,58 +132,76 @@ __global__ void __launch_bounds__(256, 1)
   umma::tc_fence_after();
 
   // ---------------------------------------------------------------- epilogue
-  const int q = warp & 3, half = warp >> 2;
-  const int i = m0 + q * 32 + lane;              // this thread's row
-  const int ldb16 = d.epi == 0 ? d.ldr : d.ldx;  // padded row length of the row-major bf16 output
-  __nv_bfloat16* oh = d.epi == 0 ? bufs.rh + d.br_off : bufs.xh[par ^ 1] + d.bx_off;
-  __nv_bfloat16* ol = d.epi == 0 ? bufs.rl + d.br_off : bufs.xl[par ^ 1] + d.bx_off;
-  float* F = d.epi == 0 ? bufs.R + d.f_off : bufs.X[par ^ 1] + d.f_off;
-  const float* Cm = bufs.X[par] + d.f_off;
+  // TMEM -> smem tile (fp32, row stride 129: conflict-free), then coalesced
+  // passes over the tile: fp32 D (+ C), row-major bf16 copies, transposed copies.
+  float* St = reinterpret_cast<float*>(smem);       // the operand ring is free now (done_bar passed)
+  constexpr int LDS = 129;
+  {
+    const int q = warp & 3, half = warp >> 2;
+    const int r = q * 32 + lane;
 #pragma unroll 1
-  for (int cc = 0; cc < 64; cc += 32) {
-    const int col0 = n0 + half * 64 + cc;
-    float v[32];
-    umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * 64 + cc), v);
-    const bool row_ok = i < d.M;
+    for (int cc = 0; cc < 64; cc += 32) {
+      float v[32];
+      umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * 64 + cc), v);
 #pragma unroll
-    for (int jj = 0; jj < 32; ++jj) {
-      const int j = col0 + jj;
+      for (int jj = 0; jj < 32; ++jj) St[r * LDS + half * 64 + cc + jj] = v[jj];
+    }
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  const bool upd = d.epi == 1;
+  const int ldb16 = upd ? d.ldx : d.ldr;   // padded row length of the row-major bf16 output
+  __nv_bfloat16* oh = upd ? bufs.xh[par ^ 1] + d.bx_off : bufs.rh + d.br_off;
+  __nv_bfloat16* ol = upd ? bufs.xl[par ^ 1] + d.bx_off : bufs.rl + d.br_off;
+  float* F = upd ? bufs.X[par ^ 1] + d.f_off : bufs.R + d.f_off;
+  const float* Cm = bufs.X[par] + d.f_off;
+  // pass 1: rows (threads along columns); value outside the matrix = 0 (keeps bf16 padding zero).
+  // C (the previous X, never written by this kernel) is loaded 32 elements at a time
+  // through the read-only path so the loads overlap instead of serialising behind stores.
+  constexpr int BATCH = 32;
+#pragma unroll 1
+  for (int e0 = tid; e0 < 128 * 128; e0 += 256 * BATCH) {
+    float cv[BATCH];
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      const int e = e0 + u * 256, r = e >> 7, cl = e & 127;
+      const int i = m0 + r, j = n0 + cl;
+      cv[u] = (upd && i < d.M && j < d.N) ? __ldg(Cm + (int64_t)i * d.ldf + j) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      const int e = e0 + u * 256, r = e >> 7, cl = e & 127;
+      const int i = m0 + r, j = n0 + cl;
       float o = 0.f;
-      if (row_ok && j < d.N) {
-        o = d.alpha * v[jj];
-        if (d.epi == 1) o = fmaf(d.beta, Cm[(int64_t)i * d.ldf + j], o);
+      if (i < d.M && j < d.N) {
+        o = fmaf(d.alpha, St[r * LDS + cl], d.beta * cv[u]);
         if (i == j) o += d.diag;
         F[(int64_t)i * d.ldf + j] = o;
       }
-      v[jj] = o;   // zero outside the matrix: keeps the bf16 padding zero
-    }
-    if (row_ok) {  // row-major bf16 copy (16-byte groups inside the padded row)
-#pragma unroll
-      for (int g8 = 0; g8 < 4; ++g8) {
-        if (col0 + 8 * g8 >= ldb16) break;
-        __align__(16) __nv_bfloat16 h[8], l[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) split(v[8 * g8 + t], h[t], l[t]);
-        const int64_t o = (int64_t)i * ldb16 + col0 + 8 * g8;
-        *reinterpret_cast<uint4*>(oh + o) = *reinterpret_cast<uint4*>(h);
-        if (write_lo) *reinterpret_cast<uint4*>(ol + o) = *reinterpret_cast<uint4*>(l);
+      St[r * LDS + cl] = o;
+      if (i < d.M && j < ldb16) {
+        __nv_bfloat16 h, l;
+        split(o, h, l);
+        oh[(int64_t)i * ldb16 + j] = h;
+        if (write_lo) ol[(int64_t)i * ldb16 + j] = l;
       }
     }
-    if (d.epi == 1 && i < d.ldxt) {  // transposed copy: row j of X'^T, lanes along i (coalesced)
-      __nv_bfloat16* th = bufs.th[par ^ 1] + d.bx_off;
-      __nv_bfloat16* tl = bufs.tl[par ^ 1] + d.bx_off;
-#pragma unroll
-      for (int jj = 0; jj < 32; ++jj) {
-        const int j = col0 + jj;
-        if (j >= d.N) break;
+  }
+  if (upd) {  // pass 2: transposed copy X'^T (threads along i)
+    __syncthreads();
+    __nv_bfloat16* th = bufs.th[par ^ 1] + d.bx_off;
+    __nv_bfloat16* tl = bufs.tl[par ^ 1] + d.bx_off;
+    for (int e = tid; e < 128 * 128; e += 256) {
+      const int cl = e >> 7, r = e & 127;
+      const int i = m0 + r, j = n0 + cl;
+      if (j < d.N && i < d.ldxt) {
         __nv_bfloat16 h, l;
-        split(v[jj], h, l);
+        split(St[r * LDS + cl], h, l);
         th[(int64_t)j * d.ldxt + i] = h;
         if (write_lo) tl[(int64_t)j * d.ldxt + i] = l;
       }
     }
   }
-  umma::tc_fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tmem, 128);
 }
@@ -192,6 +210,7 @@ __global__ void __launch_bounds__(256, 1)
 __global__ void __launch_bounds__(256) scale_bf16_kernel(const PowerItem* __restrict__ items,
                                                          const float* __restrict__ W, const float* __restrict__ sigma,
                                                          float* __restrict__ X0, NsBufs b, int par, int write_lo) {
+  __shared__ float T[32][65];
   const PowerItem it = items[blockIdx.x];
   const float inv = 1.f / sigma[it.mat];
   const int n = it.n, ldx = (n + 7) & ~7, ldxt = (it.m + 7) & ~7;
@@ -199,20 +218,33 @@ __global__ void __launch_bounds__(256) scale_bf16_kernel(const PowerItem* __rest
   __nv_bfloat16* xl = b.xl[par] + it.bx_off;
   __nv_bfloat16* th = b.th[par] + it.bx_off;
   __nv_bfloat16* tl = b.tl[par] + it.bx_off;
-  const int64_t total = (int64_t)(it.r1 - it.r0) * n;
-  for (int64_t e = threadIdx.x; e < total; e += 256) {
-    const int r = it.r0 + (int)(e / n), cidx = (int)(e % n);
-    const float x = W[it.off + (int64_t)r * n + cidx] * inv;
-    X0[it.off + (int64_t)r * n + cidx] = x;
-    __nv_bfloat16 h, l;
-    split(x, h, l);
-    xh[(int64_t)r * ldx + cidx] = h;
-    th[(int64_t)cidx * ldxt + r] = h;
-    if (write_lo) {
-      xl[(int64_t)r * ldx + cidx] = l;
-      tl[(int64_t)cidx * ldxt + r] = l;
+  for (int rt = it.r0; rt < it.r1; rt += 32)
+    for (int ct = 0; ct < n; ct += 64) {   // 32 x 64 tile: row-major pass, then transposed pass via smem
+      for (int e = threadIdx.x; e < 32 * 64; e += 256) {
+        const int rr = e >> 6, cc = e & 63, r = rt + rr, c = ct + cc;
+        float x = 0.f;
+        if (r < it.r1 && c < n) {
+          x = W[it.off + (int64_t)r * n + c] * inv;
+          X0[it.off + (int64_t)r * n + c] = x;
+          __nv_bfloat16 h, l;
+          split(x, h, l);
+          xh[(int64_t)r * ldx + c] = h;
+          if (write_lo) xl[(int64_t)r * ldx + c] = l;
+        }
+        T[rr][cc] = x;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < 32 * 64; e += 256) {
+        const int cc = e >> 5, rr = e & 31, r = rt + rr, c = ct + cc;
+        if (r < it.r1 && c < n) {
+          __nv_bfloat16 h, l;
+          split(T[rr][cc], h, l);
+          th[(int64_t)c * ldxt + r] = h;
+          if (write_lo) tl[(int64_t)c * ldxt + r] = l;
+        }
+      }
+      __syncthreads();
     }
-  }
 }
 
 NsBufs make_bufs(Plan& p, float* const bufs[BUF_COUNT]) {

@@ -121,9 +121,13 @@ orth_status_t orth_compose_kernel(orth_plan_t plan, const float* ortho, float* k
     e = P.opts.compute == ORTH_F32 ? launch_gemm_f32(ph, bufs, stream) : launch_gemm_tc(ph, bufs, 3, stream);
     P.launches++;
   };
-  gemm(P.proj);
-  for (auto& ph : P.chain) gemm(ph);
-  gemm(P.aoc);
+  if (P.opts.compute == ORTH_F32) {
+    gemm(P.proj);
+    for (auto& ph : P.chain) gemm(ph);
+    gemm(P.aoc);
+  } else {
+    e = launch_compose_tc(P, ortho, stream);
+  }
   if (!e) e = launch_emit(P, bufs, kernels_f32, (uint16_t*)kernels_bf16, stream);
   return cuda_fail(e, "orth_compose_kernel");
 }

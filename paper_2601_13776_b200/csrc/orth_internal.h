@@ -114,8 +114,20 @@ struct EmitItem {         // one (layer, group): copy the unit kernel into both 
   int32_t ci_f_per_g;        // == ci
 };
 
+// One BCOP/AOC construction unit (layer, group) of the composition workspace.
+struct CompUnit {
+  int layer, group;
+  int64_t ping, pong, fin;   // float offsets in the comp workspace (-1: none)
+  int rows, c;               // chain tap = rows x c (row subset when only [:co] is kept)
+};
+
+struct TcComposePlan;   // tensor-core composition (compose_tc.cu)
+
 struct Plan {
   std::vector<LayerInfo> layers;
+  std::vector<CompUnit> comp_units;
+  std::vector<int64_t> proj_off;     // per matrix: float offset of P = U U^T in comp (U only)
+  TcComposePlan* tcc = nullptr;
   std::vector<MatInfo> mats;
   orth_opts_t opts;
   int32_t device = -1;
@@ -181,6 +193,10 @@ int launch_residual_r(Plan& p, float* residual_out, void* stream);
 int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int npass, bool write_lo, void* stream);
 // X0 = W / sigma (fp32) plus its BF16 copies X0, X0^T (hi, and lo if write_lo)
 int launch_scale_bf16(Plan& p, const float* W, float* X0, int par, bool write_lo, void* stream);
+// tensor-core composition: built after the workspace exists; freed with the plan
+orth_status_t build_compose_tc(Plan& p);
+void free_compose_tc(Plan& p);
+int launch_compose_tc(Plan& p, const float* ortho, void* stream);   // fills comp (fp32) like the SIMT chain
 int launch_power_partial(Plan& p, const float* W, const float* v_in, int use_const_v, int frob, void* stream);
 int launch_power_finalize(Plan& p, float* v_out, int frob, int write_sigma_only, void* stream);
 int launch_scale(Plan& p, const float* W, float* X0, void* stream);

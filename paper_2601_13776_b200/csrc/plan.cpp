@@ -367,8 +367,9 @@ static void build_compose(Plan& P) {
   }
   P.comp_proj_off = 0;
   int max_sub = 0;
-  struct Unit { int layer, group; int64_t ping, pong, fin; int rows, c; };
-  std::vector<Unit> units;
+  using Unit = CompUnit;
+  std::vector<Unit>& units = P.comp_units;
+  units.clear();
   for (int l = 0; l < (int)P.layers.size(); ++l) {
     LayerInfo& L = P.layers[l];
     if (L.owner != P.opts.rank) continue;
@@ -482,6 +483,7 @@ static void build_compose(Plan& P) {
     P.emit.push_back(e);
   }
   P.comp_numel = std::max<int64_t>(w, kPadF32);
+  P.proj_off = proj_off;
 }
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -611,7 +613,13 @@ orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers
   build_compose(P);
   if (device >= 0) {
     st = allocate(P);
-    if (st != ORTH_OK) { delete h; return st; }
+    if (st == ORTH_OK && P.opts.compute != ORTH_F32) st = build_compose_tc(P);
+    if (st != ORTH_OK) {
+      free_compose_tc(P);
+      if (P.d_arena) cudaFree(P.d_arena);
+      delete h;
+      return st;
+    }
   }
   *plan = h;
   return ORTH_OK;
@@ -619,6 +627,7 @@ orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers
 
 orth_status_t orth_plan_destroy(orth_plan_t plan) {
   if (!plan) return ORTH_OK;
+  free_compose_tc(plan->p);
   if (plan->p.d_arena) cudaFree(plan->p.d_arena);
   delete plan;
   return ORTH_OK;

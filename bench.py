@@ -145,10 +145,8 @@ def run_step(W, orth, torch, world, pg, ev=None, graphs=None):
         plan.compose(W["ortho"], W["kf32"], W["kbf16"])
     rec("comp1")
     if world > 1:
-        import torch.distributed as dist
-        seg = orth.orth_plan_query(plan.h, "KERNEL_SEGMENT_BF16")
-        r = dist.get_rank()
-        dist.all_gather_into_tensor(W["kbf16"], W["kbf16"][r * seg:(r + 1) * seg].clone(), group=pg)
+        from paper_2601_13776_b200.dist import gather_kernels
+        gather_kernels(plan, W["kbf16"], orth.orth_plan_query(plan.h, "KERNEL_SEGMENT_BF16"), pg)
     rec("gather1")
     cur = W["x"]
     for l, y in enumerate(W["acts"]):
@@ -274,11 +272,14 @@ def ours(args):
     out = {
         "metric": METRIC, "value": len(cfg) * world / (t_step * 1e-3), "unit": "layers/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if args.compute == "bf16" else "f32+bf16",
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": {"bf16": "bf16", "bf16x3": "bf16x3", "f32": "f32+bf16"}[args.compute],
         "data": "synthetic (seeded near-orthogonal params, N(0,1) activations; SURVEY §8(d))",
         "config": {"workload": f"config {args.config}: CIFAR-AOC-12 (12 orthogonal 3x3 convs 64-512 ch, 3 stride-2)",
                    "global_batch": batch * world, "per_rank_batch": batch, "image": 32, "ns_iters": 12,
-                   "construction": "FP32-accurate" if args.compute == "f32" else "BF16 tensor cores",
+                   "construction": {"f32": "FP32 FFMA (SIMT)",
+                                    "bf16": "tcgen05 BF16, FP32 master, 3-pass split polish + composition",
+                                    "bf16x3": "tcgen05 3-pass hi/lo split everywhere"}[args.compute],
                    "activations": "bf16 NHWC", "parallelism": f"dp{world} (construction sharded by layer + all-gather)",
                    "l2": "flushed between timed steps (252 MB write)",
                    "launch": "CUDA graphs per phase" if graphs else "eager"},
@@ -430,7 +431,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--compute", default="f32", choices=["f32", "bf16", "bf16x3"])
+    ap.add_argument("--compute", default="bf16", choices=["f32", "bf16", "bf16x3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying CUDA graphs")
     ap.add_argument("--cpu-budget", type=float, default=30.0)

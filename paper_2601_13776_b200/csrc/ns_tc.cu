@@ -48,7 +48,7 @@ __device__ __forceinline__ void split(float x, __nv_bfloat16& h, __nv_bfloat16& 
 }
 
 template <int NPASS, int S>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
     ns_tc_kernel(const NsDesc* __restrict__ descs, int ndesc, NsBufs bufs, int par, int write_lo) {
   constexpr bool SPLIT = NPASS == 3;
   constexpr int TILE = 128 * 128;
@@ -289,7 +289,7 @@ int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int 
   NsBufs b = make_bufs(p, bufs);
   p.launches++;
   if (npass == 3) return launch_impl<3, 3>(d, nd, tiles, b, par, write_lo, (cudaStream_t)stream);
-  return launch_impl<1, 4>(d, nd, tiles, b, par, write_lo, (cudaStream_t)stream);
+  return launch_impl<1, 3>(d, nd, tiles, b, par, write_lo, (cudaStream_t)stream);
 }
 
 int launch_scale_bf16(Plan& p, const float* W, float* X0, int par, bool write_lo, void* stream) {

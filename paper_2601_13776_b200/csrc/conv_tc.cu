@@ -30,6 +30,7 @@
 
 #include "orth_internal.h"
 #include "umma.cuh"
+#include "tma_host.h"
 
 namespace orth {
 namespace {
@@ -52,7 +53,8 @@ __device__ __forceinline__ int wrapi(int x, int n) {
 template <int BN, int S>
 __global__ void __launch_bounds__(NTHREADS, 1)
     conv_fwd_ws(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
-                const float* __restrict__ bias, __nv_bfloat16* __restrict__ y, TcConvArgs a) {
+                const float* __restrict__ bias, __nv_bfloat16* __restrict__ y, TcConvArgs a,
+                const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
@@ -65,7 +67,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == MMA_WARP) umma::tmem_alloc(&tmem_base_sh, 2 * BN);
   if (tid == 0) {
     for (int i = 0; i < S; ++i) {
-      umma::mbar_init(&full_bar[i], NPROD);
+      umma::mbar_init(&full_bar[i], NPROD + 1);   // + the TMA issuer's expect_tx arrival
       umma::mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -87,8 +89,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (warp < MMA_WARP) {
     // ------------------------------------------------------------ producers
-    const int c = tid & 7, rbase = tid >> 3;   // A rows rbase + 32 i, B rows rbase + 32 i
-    int it = 0;
+    const int c = tid & 7, rbase = tid >> 3;   // A rows rbase + 32 i
+    if (tid == 0) umma::tma_prefetch_desc(&tmB);
+    const uint32_t tab_s = umma::smem_u32(tab);
+    int it = 0, st = 0, ph = 0;                // ring position of k-block `it`
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
       const int tm = tile % a.tiles_m, rest = tile / a.tiles_m;
       const int tn = rest % a.tiles_n, g = rest / a.tiles_n;
@@ -115,33 +119,35 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       umma::named_bar_sync(1, NPROD);
       const __nv_bfloat16* xg = x + (int64_t)g * a.ci_g + c * 8;
-      const __nv_bfloat16* wg = w + ((int64_t)g * a.co_g + n0) * kk2 * a.ci_g + c * 8;
-      for (int kb = 0; kb < nk; ++kb, ++it) {
-        const int st = it % S;
-        umma::mbar_wait(&empty_bar[st], ((it / S) & 1) ^ 1);
-        const int tap = kb / kc, c0 = (kb - tap * kc) * 64;
-        const bool cok = c0 + c * 8 < a.ci_g;
-        const uint32_t sa = s0 + st * STAGE;
-        const int* trow = tab + tap * 128;
+      const uint32_t off_r[4] = {umma::sw128_off(rbase, c), umma::sw128_off(rbase + 32, c),
+                                 umma::sw128_off(rbase + 64, c), umma::sw128_off(rbase + 96, c)};
+      for (int tap = 0; tap < kk2; ++tap) {
+        const uint32_t trow = tab_s + (uint32_t)(tap * 128 + rbase) * 4u;
+        int pix[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r = rbase + 32 * i;
-          const int pix = trow[r];
-          const bool ok = cok && pix >= 0;
-          umma::cp_async16(sa + umma::sw128_off(r, c), ok ? xg + (int64_t)pix * a.Ci + c0 : x, ok);
-        }
+        for (int i = 0; i < 4; ++i) pix[i] = umma::ld_shared_s32(trow + 128u * i);
+        for (int c0 = 0; c0 < a.ci_g; c0 += 64, ++it) {
+          umma::mbar_wait(&empty_bar[st], ph ^ 1);
+          const uint32_t sa = s0 + st * STAGE;
+          if (tid == 0) {   // B tile (BN x 64 channels of this tap) by TMA, SWIZZLE_128B, OOB -> 0
+            umma::mbar_arrive_expect_tx(&full_bar[st], B_BYTES);
+            umma::tma_load_3d(sa + A_BYTES, &tmB, &full_bar[st], c0, tap, g * a.co_g + n0);
+          }
+          const bool cok = c0 + c * 8 < a.ci_g;
 #pragma unroll
-        for (int i = 0; i < BN / 32; ++i) {
-          const int r = rbase + 32 * i;
-          const bool ok = cok && n0 + r < a.co_g;
-          umma::cp_async16(sa + A_BYTES + umma::sw128_off(r, c),
-                           ok ? wg + ((int64_t)r * kk2 + tap) * a.ci_g + c0 : w, ok);
-        }
-        umma::cp_async_commit();
-        if (it >= LAG) {
-          umma::cp_async_wait<LAG>();
-          umma::fence_proxy_async_smem();
-          umma::mbar_arrive(&full_bar[(it - LAG) % S]);
+          for (int i = 0; i < 4; ++i) {
+            const bool ok = cok && pix[i] >= 0;
+            umma::cp_async16(sa + off_r[i], ok ? xg + (int64_t)pix[i] * a.Ci + c0 : x, ok);
+          }
+          umma::cp_async_commit();
+          if (it >= LAG) {
+            umma::cp_async_wait<LAG>();
+            umma::fence_proxy_async_smem();
+            int sp = st - LAG;
+            sp += sp < 0 ? S : 0;
+            umma::mbar_arrive(&full_bar[sp]);
+          }
+          if (++st == S) { st = 0; ph ^= 1; }
         }
       }
     }
@@ -235,7 +241,9 @@ int launch_ws(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias,
     attr = true;
   }
   const int grid = a.num_tiles < num_sms() ? a.num_tiles : num_sms();
-  conv_fwd_ws<BN, S><<<grid, NTHREADS, smem, stream>>>(x, w, bias, y, a);
+  CUtensorMap tm;
+  if (!make_weight_tmap(&tm, w, a.Co, a.k * a.k, a.ci_g, BN)) return (int)cudaErrorInvalidValue;
+  conv_fwd_ws<BN, S><<<grid, NTHREADS, smem, stream>>>(x, w, bias, y, a, tm);
   return (int)cudaGetLastError();
 }
 

@@ -210,53 +210,74 @@ __global__ void __launch_bounds__(256) conv_fwd_smallk(const __nv_bfloat16* __re
                                                        const float* __restrict__ bias, __nv_bfloat16* __restrict__ y,
                                                        ConvArgs a) {
   extern __shared__ float sm[];
-  const int KT = a.ci_g * a.k * a.k, ld = KT + 1;
-  float* patch = sm;                   // [128][KT + 1]
-  float* ws = sm + 128 * ld;           // [KT][co_g]
+  const int KT = a.ci_g * a.k * a.k, ld = KT | 1;   // odd row stride: conflict-free per-thread rows
+  float* patch = sm;                   // [256][KT | 1]: one im2col row per thread
+  float* ws = sm + 256 * ld;           // [KT][co_g] (16-byte aligned: 256 * ld * 4 is)
   const int g = blockIdx.z, tid = threadIdx.x;
-  const int64_t M = (int64_t)a.N * a.Ho * a.Wo;
-  const int64_t m0 = (int64_t)blockIdx.x * 128;
+  const int M = a.N * a.Ho * a.Wo;
   for (int e = tid; e < KT * a.co_g; e += 256) {     // GEMM layout (co, k, k, ci_g): row o is K-contiguous
-    const int o = e / KT, kk = e % KT;
+    const int o = e / KT, kk = e - o * KT;
     ws[kk * a.co_g + o] = __bfloat162float(wt[((int64_t)g * a.co_g + o) * KT + kk]);
   }
-  for (int e = tid; e < 128 * KT; e += 256) {
-    const int p = e / KT, kk = e % KT;
-    const int tap = kk / a.ci_g, c = kk % a.ci_g;
-    const int64_t m = m0 + p;
-    float v = 0.f;
-    if (m < M) {
-      const int64_t hw = (int64_t)a.Ho * a.Wo;
-      const int n = (int)(m / hw), r = (int)(m % hw);
-      int h = (r / a.Wo) * a.s - a.pt + a.d * (tap / a.k), w = (r % a.Wo) * a.s - a.pl + a.d * (tap % a.k);
-      bool ok = true;
-      if (a.circ) { h = wrap(h, a.H); w = wrap(w, a.W); }
-      else ok = h >= 0 && h < a.H && w >= 0 && w < a.W;
-      if (ok) v = __bfloat162float(x[(((int64_t)n * a.H + h) * a.W + w) * a.Ci + g * a.ci_g + c]);
+  const int m = blockIdx.x * 256 + tid;
+  float* prow = patch + tid * ld;
+  if (m < M) {   // this thread's im2col row, taps in (a, b) order, channels innermost
+    const int hw = a.Ho * a.Wo, n = m / hw, r = m - n * hw, u = r / a.Wo, v = r - u * a.Wo;
+    const __nv_bfloat16* xn = x + (int64_t)n * a.H * a.W * a.Ci + g * a.ci_g;
+    int kk = 0;
+    for (int ta = 0; ta < a.k; ++ta) {
+      int h = u * a.s - a.pt + a.d * ta;
+      bool hok = true;
+      if (a.circ) h = wrap(h, a.H); else hok = h >= 0 && h < a.H;
+      for (int tb = 0; tb < a.k; ++tb) {
+        int w = v * a.s - a.pl + a.d * tb;
+        bool ok = hok;
+        if (a.circ) w = wrap(w, a.W); else ok = ok && w >= 0 && w < a.W;
+        const __nv_bfloat16* px = xn + ((int64_t)h * a.W + w) * a.Ci;
+        for (int c = 0; c < a.ci_g; ++c, ++kk) prow[kk] = ok ? __bfloat162float(px[c]) : 0.f;
+      }
     }
-    patch[p * ld + kk] = v;
   }
   __syncthreads();
-  const int p = tid & 127, half = tid >> 7;
-  const int64_t m = m0 + p;
   if (m >= M) return;
-  const int cpt = a.co_g / 2;          // channels per thread (co_g % 16 == 0)
-  for (int c0 = half * cpt; c0 < (half + 1) * cpt; c0 += 8) {
-    float acc[8] = {};
+  const float4* ws4 = reinterpret_cast<const float4*>(ws);
+  const int co4 = a.co_g / 4;
+  for (int c0 = 0; c0 < a.co_g; c0 += 32) {          // 32 output channels per pass (co_g % 16 == 0)
+    const int nc = a.co_g - c0 < 32 ? a.co_g - c0 : 32;
+    float acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = 0.f;
     for (int kk = 0; kk < KT; ++kk) {
-      const float av = patch[p * ld + kk];
+      const float av = prow[kk];
+      const float4* wr = ws4 + kk * co4 + c0 / 4;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = fmaf(av, ws[kk * a.co_g + c0 + j], acc[j]);
+      for (int j = 0; j < 8; ++j) {
+        if (4 * j < nc) {
+          const float4 w4 = wr[j];                      // warp-uniform address: broadcast
+          acc[4 * j] = fmaf(av, w4.x, acc[4 * j]);
+          acc[4 * j + 1] = fmaf(av, w4.y, acc[4 * j + 1]);
+          acc[4 * j + 2] = fmaf(av, w4.z, acc[4 * j + 2]);
+          acc[4 * j + 3] = fmaf(av, w4.w, acc[4 * j + 3]);
+        }
+      }
     }
-    uint32_t pk[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float v0 = acc[2 * j], v1 = acc[2 * j + 1];
-      if (bias) { v0 += bias[g * a.co_g + c0 + 2 * j]; v1 += bias[g * a.co_g + c0 + 2 * j + 1]; }
-      __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
-      pk[j] = *reinterpret_cast<uint32_t*>(&b2);
+    for (int q = 0; q < 4; ++q) {
+      if (8 * q >= nc) break;
+      uint32_t pk[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float v0 = acc[8 * q + 2 * j], v1 = acc[8 * q + 2 * j + 1];
+        if (bias) {
+          v0 += bias[g * a.co_g + c0 + 8 * q + 2 * j];
+          v1 += bias[g * a.co_g + c0 + 8 * q + 2 * j + 1];
+        }
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
+        pk[j] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      *reinterpret_cast<uint4*>(y + (int64_t)m * a.Co + g * a.co_g + c0 + 8 * q) =
+          make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
-    *reinterpret_cast<uint4*>(y + m * a.Co + g * a.co_g + c0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
   }
 }
 
@@ -278,14 +299,14 @@ int launch_conv_fwd(const LayerInfo& L, const void* kernel, const float* bias, c
   const int64_t M = (int64_t)N * Ho * Wo;
   const int KT = L.ci * L.k * L.k;
   if (io == ORTH_BF16 && KT <= 64 && L.co % 16 == 0 && L.co_f % 8 == 0 && !getenv("ORTH_FORCE_SIMT")) {
-    const size_t smem = (size_t)(128 * (KT + 1) + KT * L.co) * sizeof(float);
+    const size_t smem = (size_t)(256 * (KT | 1) + KT * L.co) * sizeof(float);
     if (smem <= 200 * 1024) {
       static size_t attr = 0;
       if (smem > 48 * 1024 && smem > attr) {
         cudaFuncSetAttribute(conv_fwd_smallk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = smem;
       }
-      dim3 g2((unsigned)((M + 127) / 128), 1, (unsigned)L.g);
+      dim3 g2((unsigned)((M + 255) / 256), 1, (unsigned)L.g);
       conv_fwd_smallk<<<g2, 256, smem, (cudaStream_t)stream>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)kernel,
                                                                bias, (__nv_bfloat16*)y, a);
       return (int)cudaGetLastError();

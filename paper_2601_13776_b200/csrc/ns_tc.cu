@@ -14,9 +14,12 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
+#include <vector>
 
 #include "orth_internal.h"
 #include "umma.cuh"
+#include "tma_host.h"
 
 namespace orth {
 namespace {
@@ -49,12 +52,14 @@ __device__ __forceinline__ void split(float x, __nv_bfloat16& h, __nv_bfloat16& 
 
 template <int NPASS, int S>
 __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
-    ns_tc_kernel(const NsDesc* __restrict__ descs, int ndesc, NsBufs bufs, int par, int write_lo) {
+    ns_tc_kernel(const NsDesc* __restrict__ descs, int ndesc, NsBufs bufs, int par, int write_lo,
+                 const CUtensorMap* __restrict__ maps) {
   constexpr bool SPLIT = NPASS == 3;
   constexpr int TILE = 128 * 128;
   constexpr int STAGE = (SPLIT ? 4 : 2) * TILE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full_bar[S];
   __shared__ uint64_t empty_bar[S];
   __shared__ uint64_t done_bar;
   __shared__ uint32_t tmem_base_sh;
@@ -66,7 +71,10 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
 
   if (warp == 0) umma::tmem_alloc(&tmem_base_sh, 128);
   if (tid == 32) {
-    for (int i = 0; i < S; ++i) umma::mbar_init(&empty_bar[i], 1);
+    for (int i = 0; i < S; ++i) {
+      umma::mbar_init(&empty_bar[i], 1);
+      umma::mbar_init(&full_bar[i], 1);
+    }
     umma::mbar_init(&done_bar, 1);
     umma::fence_mbar_init();
   }
@@ -77,131 +85,138 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
   const uint32_t s0 = umma::smem_u32(smem);
   constexpr uint32_t IDESC = umma::idesc_bf16(128, 128);
 
-  const __nv_bfloat16* Ah = operand(bufs, d.a_kind, par, false) + d.a_off;
-  const __nv_bfloat16* Bh = operand(bufs, d.b_kind, par, false) + d.b_off;
-  const __nv_bfloat16* Al = operand(bufs, d.a_kind, par, true) + d.a_off;
-  const __nv_bfloat16* Bl = operand(bufs, d.b_kind, par, true) + d.b_off;
   const int nk = (d.K + 63) / 64;
-  const int c = tid & 7;
-
-  for (int kb = 0; kb < nk + S - 1; ++kb) {
-    if (kb < nk) {
+  if (tid == 0) {
+    // ---- TMA producer: 128 x 64 BF16 boxes (SWIZZLE_128B, OOB -> 0) of A and B (hi, lo)
+    const CUtensorMap* ma = maps + d.map_a + 2 * par;
+    const CUtensorMap* mb = maps + d.map_b + 2 * par;
+    constexpr uint32_t BYTES = (SPLIT ? 4 : 2) * TILE;
+    for (int kb = 0; kb < nk; ++kb) {
       const int st = kb % S;
       if (kb >= S) umma::mbar_wait(&empty_bar[st], ((kb / S) - 1) & 1);
-      const int kc = kb * 64 + c * 8;
-      const bool kok = kc < d.K;
       const uint32_t sa = s0 + st * STAGE;
+      umma::mbar_arrive_expect_tx(&full_bar[st], BYTES);
+      umma::tma_load_2d(sa, ma, &full_bar[st], kb * 64, m0);
+      umma::tma_load_2d(sa + TILE, mb, &full_bar[st], kb * 64, n0);
+      if (SPLIT) {
+        umma::tma_load_2d(sa + 2 * TILE, ma + 1, &full_bar[st], kb * 64, m0);
+        umma::tma_load_2d(sa + 3 * TILE, mb + 1, &full_bar[st], kb * 64, n0);
+      }
+    }
+  } else if (tid == 32) {
+    // ---- MMA issuer
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % S;
+      umma::mbar_wait(&full_bar[st], (kb / S) & 1);
+      umma::tc_fence_after();
+      const uint32_t ah = s0 + st * STAGE, bh = ah + TILE, al = ah + 2 * TILE, bl = ah + 3 * TILE;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = (tid >> 3) + 32 * i;
-        const uint32_t off = umma::sw128_off(r, c);
-        const bool aok = kok && m0 + r < d.M, bok = kok && n0 + r < d.N;
-        const int64_t ao = (int64_t)(m0 + r) * d.lda + kc, bo = (int64_t)(n0 + r) * d.ldb + kc;
-        umma::cp_async16(sa + off, aok ? Ah + ao : Ah, aok);
-        umma::cp_async16(sa + TILE + off, bok ? Bh + bo : Bh, bok);
+      for (int q = 0; q < 4; ++q) {
+        umma::mma_bf16(tmem, umma::sdesc_sw128(ah + 32 * q), umma::sdesc_sw128(bh + 32 * q), IDESC, (kb | q) != 0);
         if (SPLIT) {
-          umma::cp_async16(sa + 2 * TILE + off, aok ? Al + ao : Al, aok);
-          umma::cp_async16(sa + 3 * TILE + off, bok ? Bl + bo : Bl, bok);
+          umma::mma_bf16(tmem, umma::sdesc_sw128(ah + 32 * q), umma::sdesc_sw128(bl + 32 * q), IDESC, 1);
+          umma::mma_bf16(tmem, umma::sdesc_sw128(al + 32 * q), umma::sdesc_sw128(bh + 32 * q), IDESC, 1);
         }
       }
+      umma::mma_commit(&empty_bar[st]);
     }
-    umma::cp_async_commit();
-    const int j = kb - (S - 1);
-    if (j >= 0) {
-      umma::cp_async_wait<S - 1>();
-      umma::fence_proxy_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        umma::tc_fence_after();
-        const int st = j % S;
-        const uint32_t ah = s0 + st * STAGE, bh = ah + TILE, al = ah + 2 * TILE, bl = ah + 3 * TILE;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          umma::mma_bf16(tmem, umma::sdesc_sw128(ah + 32 * q), umma::sdesc_sw128(bh + 32 * q), IDESC, (j | q) != 0);
-          if (SPLIT) {
-            umma::mma_bf16(tmem, umma::sdesc_sw128(ah + 32 * q), umma::sdesc_sw128(bl + 32 * q), IDESC, 1);
-            umma::mma_bf16(tmem, umma::sdesc_sw128(al + 32 * q), umma::sdesc_sw128(bh + 32 * q), IDESC, 1);
-          }
-        }
-        umma::mma_commit(&empty_bar[st]);
-      }
-    }
+    umma::mma_commit(&done_bar);
   }
-  if (tid == 0) umma::mma_commit(&done_bar);
   umma::mbar_wait(&done_bar, 0);
   umma::tc_fence_after();
 
   // ---------------------------------------------------------------- epilogue
-  // TMEM -> smem tile (fp32, row stride 129: conflict-free), then coalesced
-  // passes over the tile: fp32 D (+ C), row-major bf16 copies, transposed copies.
-  float* St = reinterpret_cast<float*>(smem);       // the operand ring is free now (done_bar passed)
-  constexpr int LDS = 129;
-  {
-    const int q = warp & 3, half = warp >> 2;
-    const int r = q * 32 + lane;
-#pragma unroll 1
-    for (int cc = 0; cc < 64; cc += 32) {
-      float v[32];
-      umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * 64 + cc), v);
-#pragma unroll
-      for (int jj = 0; jj < 32; ++jj) St[r * LDS + half * 64 + cc + jj] = v[jj];
-    }
-  }
-  umma::tc_fence_before();
-  __syncthreads();
+  // Two 64-column halves.  TMEM -> fp32 smem tile (row stride 68 floats: the
+  // row-per-thread float4 writes and the row-wise float4 reads are both
+  // conflict-free) -> one coalesced row pass (C in, D out as FP32, BF16 hi/lo
+  // row copies) that also stages the BF16 transpose -> one coalesced pass of
+  // X'^T rows (update phase only).  The operand ring is free once done_bar completed.
   const bool upd = d.epi == 1;
-  const int ldb16 = upd ? d.ldx : d.ldr;   // padded row length of the row-major bf16 output
+  const int ldb16 = upd ? d.ldx : d.ldr;   // padded row length of the row-major bf16 outputs
   __nv_bfloat16* oh = upd ? bufs.xh[par ^ 1] + d.bx_off : bufs.rh + d.br_off;
   __nv_bfloat16* ol = upd ? bufs.xl[par ^ 1] + d.bx_off : bufs.rl + d.br_off;
   float* F = upd ? bufs.X[par ^ 1] + d.f_off : bufs.R + d.f_off;
   const float* Cm = bufs.X[par] + d.f_off;
-  // pass 1: rows (threads along columns); value outside the matrix = 0 (keeps bf16 padding zero).
-  // C (the previous X, never written by this kernel) is loaded 32 elements at a time
-  // through the read-only path so the loads overlap instead of serialising behind stores.
-  constexpr int BATCH = 32;
+  __nv_bfloat16* th = bufs.th[par ^ 1] + d.bx_off;
+  __nv_bfloat16* tl = bufs.tl[par ^ 1] + d.bx_off;
+  constexpr int LDF = 68, LDT = 136;
+  float* Sf = reinterpret_cast<float*>(smem);                              // [128][68] fp32
+  __nv_bfloat16* sTh = reinterpret_cast<__nv_bfloat16*>(smem + 128 * LDF * 4);   // [64][136] bf16
+  __nv_bfloat16* sTl = sTh + 64 * LDT;
+  const bool fvec = (d.ldf & 3) == 0;      // 16-byte aligned fp32 rows
 #pragma unroll 1
-  for (int e0 = tid; e0 < 128 * 128; e0 += 256 * BATCH) {
-    float cv[BATCH];
+  for (int h = 0; h < 2; ++h) {
+    {
+      const int q = warp & 3, sub = warp >> 2, r = q * 32 + lane;
+      float v[32];
+      umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * 64 + sub * 32), v);
 #pragma unroll
-    for (int u = 0; u < BATCH; ++u) {
-      const int e = e0 + u * 256, r = e >> 7, cl = e & 127;
-      const int i = m0 + r, j = n0 + cl;
-      cv[u] = (upd && i < d.M && j < d.N) ? __ldg(Cm + (int64_t)i * d.ldf + j) : 0.f;
+      for (int t = 0; t < 8; ++t)
+        *reinterpret_cast<float4*>(Sf + r * LDF + sub * 32 + 4 * t) =
+            make_float4(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3]);
     }
-#pragma unroll
-    for (int u = 0; u < BATCH; ++u) {
-      const int e = e0 + u * 256, r = e >> 7, cl = e & 127;
-      const int i = m0 + r, j = n0 + cl;
-      float o = 0.f;
-      if (i < d.M && j < d.N) {
-        o = fmaf(d.alpha, St[r * LDS + cl], d.beta * cv[u]);
-        if (i == j) o += d.diag;
-        F[(int64_t)i * d.ldf + j] = o;
-      }
-      St[r * LDS + cl] = o;
-      if (i < d.M && j < ldb16) {
-        __nv_bfloat16 h, l;
-        split(o, h, l);
-        oh[(int64_t)i * ldb16 + j] = h;
-        if (write_lo) ol[(int64_t)i * ldb16 + j] = l;
-      }
-    }
-  }
-  if (upd) {  // pass 2: transposed copy X'^T (threads along i)
+    umma::tc_fence_before();
     __syncthreads();
-    __nv_bfloat16* th = bufs.th[par ^ 1] + d.bx_off;
-    __nv_bfloat16* tl = bufs.tl[par ^ 1] + d.bx_off;
-    for (int e = tid; e < 128 * 128; e += 256) {
-      const int cl = e >> 7, r = e & 127;
-      const int i = m0 + r, j = n0 + cl;
-      if (j < d.N && i < d.ldxt) {
-        __nv_bfloat16 h, l;
-        split(St[r * LDS + cl], h, l);
-        th[(int64_t)j * d.ldxt + i] = h;
-        if (write_lo) tl[(int64_t)j * d.ldxt + i] = l;
+    // row pass: element group e -> (row r, 4 columns c4*4 .. +3)
+#pragma unroll 2
+    for (int e = tid; e < 128 * 16; e += 256) {
+      const int r = e >> 4, c4 = (e & 15) * 4;
+      const int i = m0 + r, j0 = n0 + h * 64 + c4;
+      float4 a = *reinterpret_cast<const float4*>(Sf + r * LDF + c4);
+      float o[4] = {a.x, a.y, a.z, a.w};
+      const bool row_ok = i < d.M;
+      const int64_t fo = (int64_t)i * d.ldf + j0;
+      if (row_ok && fvec && j0 + 4 <= d.N) {
+        float4 c = upd ? __ldg(reinterpret_cast<const float4*>(Cm + fo)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        o[0] = fmaf(d.alpha, o[0], d.beta * c.x);
+        o[1] = fmaf(d.alpha, o[1], d.beta * c.y);
+        o[2] = fmaf(d.alpha, o[2], d.beta * c.z);
+        o[3] = fmaf(d.alpha, o[3], d.beta * c.w);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[k] += (i == j0 + k) ? d.diag : 0.f;
+        *reinterpret_cast<float4*>(F + fo) = make_float4(o[0], o[1], o[2], o[3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (row_ok && j0 + k < d.N) {
+            o[k] = fmaf(d.alpha, o[k], upd ? d.beta * __ldg(Cm + fo + k) : 0.f) + ((i == j0 + k) ? d.diag : 0.f);
+            F[fo + k] = o[k];
+          } else {
+            o[k] = 0.f;   // keeps every bf16 padding element zero
+          }
+        }
+      }
+      __nv_bfloat16 hb[4], lb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) split(o[k], hb[k], lb[k]);
+      if (row_ok && j0 < ldb16) {   // ldb16 % 8 == 0 and j0 % 4 == 0: the 4-group is inside the padded row
+        const int64_t bo = (int64_t)i * ldb16 + j0;
+        *reinterpret_cast<uint2*>(oh + bo) = *reinterpret_cast<const uint2*>(hb);
+        if (write_lo) *reinterpret_cast<uint2*>(ol + bo) = *reinterpret_cast<const uint2*>(lb);
+      }
+      if (upd) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          sTh[(c4 + k) * LDT + r] = hb[k];
+          if (write_lo) sTl[(c4 + k) * LDT + r] = lb[k];
+        }
       }
     }
+    __syncthreads();
+    if (upd) {   // rows of X'^T: 16-byte chunks along i
+      for (int e = tid; e < 64 * 16; e += 256) {
+        const int cl = e >> 4, i8 = (e & 15) * 8;
+        const int j = n0 + h * 64 + cl, i0 = m0 + i8;
+        if (j < d.N && i0 < d.ldxt) {
+          const int64_t o = (int64_t)j * d.ldxt + i0;
+          *reinterpret_cast<uint4*>(th + o) = *reinterpret_cast<const uint4*>(sTh + cl * LDT + i8);
+          if (write_lo) *reinterpret_cast<uint4*>(tl + o) = *reinterpret_cast<const uint4*>(sTl + cl * LDT + i8);
+        }
+      }
+      __syncthreads();
+    }
   }
+  umma::tc_fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tmem, 128);
 }
@@ -267,19 +282,82 @@ NsBufs make_bufs(Plan& p, float* const bufs[BUF_COUNT]) {
 }
 
 template <int NPASS, int S>
-int launch_impl(const NsDesc* d, int nd, int tiles, NsBufs b, int par, int write_lo, cudaStream_t s) {
+int launch_impl(const NsDesc* d, int nd, int tiles, NsBufs b, int par, int write_lo, const CUtensorMap* maps,
+                cudaStream_t s) {
   constexpr int STAGE = (NPASS == 3 ? 4 : 2) * 128 * 128;
-  const size_t smem = 1024 + (size_t)S * STAGE;
+  const size_t smem = 1024 + (size_t)(S * STAGE > 128 * 129 * 4 ? S * STAGE : 128 * 129 * 4);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(ns_tc_kernel<NPASS, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  ns_tc_kernel<NPASS, S><<<tiles, 256, smem, s>>>(d, nd, b, par, write_lo);
+  ns_tc_kernel<NPASS, S><<<tiles, 256, smem, s>>>(d, nd, b, par, write_lo, maps);
   return (int)cudaGetLastError();
 }
 
 }  // namespace
+
+// One 2-D map per (matrix, operand kind, parity, hi/lo): dims (K, rows), row
+// stride = padded row length; box 64 x 128, SWIZZLE_128B.
+orth_status_t build_ns_tma(Plan& p) {
+  auto enc = tensor_map_encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return ORTH_ERR_CUDA;
+  }
+  float* fake[BUF_COUNT] = {nullptr, nullptr, nullptr, nullptr};
+  NsBufs b = make_bufs(p, fake);
+  std::vector<CUtensorMap> maps;
+  auto add4 = [&](int kind, int64_t off, int64_t K, int64_t rows, int64_t ld) {
+    const int base = (int)maps.size();
+    for (int par = 0; par < 2; ++par)
+      for (int lo = 0; lo < 2; ++lo) {
+        const __nv_bfloat16* ptr = (kind == 0 ? (lo ? b.xl[par] : b.xh[par])
+                                    : kind == 1 ? (lo ? b.tl[par] : b.th[par])
+                                                : (lo ? b.rl : b.rh)) + off;
+        CUtensorMap m;
+        std::memset(&m, 0, sizeof(m));
+        const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+        const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+        const cuuint32_t box[2] = {64, 128};
+        const cuuint32_t es[2] = {1, 1};
+        if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(ptr), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          return -1;
+        maps.push_back(m);
+      }
+    return base;
+  };
+  auto operand_map = [&](const NsDesc& d, bool a) {
+    const int kind = a ? d.a_kind : d.b_kind;
+    const int64_t off = a ? d.a_off : d.b_off, ld = a ? d.lda : d.ldb;
+    const int64_t rows = a ? d.M : d.N;
+    return add4(kind, off, d.K, rows, ld);
+  };
+  for (auto* v : {&p.ns_gram, &p.ns_upd})
+    for (auto& d : *v) {
+      d.map_a = operand_map(d, true);
+      d.map_b = operand_map(d, false);
+      if (d.map_a < 0 || d.map_b < 0) {
+        set_error("tensor map encoding failed for an NS operand");
+        return ORTH_ERR_CUDA;
+      }
+    }
+  if (maps.empty()) return ORTH_OK;
+  cudaError_t e = cudaMalloc(&p.d_ns_maps, maps.size() * sizeof(CUtensorMap));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p.d_ns_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !p.ns_gram.empty())
+    e = cudaMemcpy(p.d_ns_gram, p.ns_gram.data(), p.ns_gram.size() * sizeof(NsDesc), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !p.ns_upd.empty())
+    e = cudaMemcpy(p.d_ns_upd, p.ns_upd.data(), p.ns_upd.size() * sizeof(NsDesc), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    set_error("NS tensor map upload failed: %s", cudaGetErrorString(e));
+    return ORTH_ERR_CUDA;
+  }
+  return ORTH_OK;
+}
 
 int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int npass, bool write_lo, void* stream) {
   const int tiles = gram ? p.ns_gram_tiles : p.ns_upd_tiles;
@@ -288,8 +366,9 @@ int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int 
   const int nd = (int)(gram ? p.ns_gram.size() : p.ns_upd.size());
   NsBufs b = make_bufs(p, bufs);
   p.launches++;
-  if (npass == 3) return launch_impl<3, 3>(d, nd, tiles, b, par, write_lo, (cudaStream_t)stream);
-  return launch_impl<1, 3>(d, nd, tiles, b, par, write_lo, (cudaStream_t)stream);
+  auto maps = reinterpret_cast<const CUtensorMap*>(p.d_ns_maps);
+  if (npass == 3) return launch_impl<3, 3>(d, nd, tiles, b, par, write_lo, maps, (cudaStream_t)stream);
+  return launch_impl<1, 3>(d, nd, tiles, b, par, write_lo, maps, (cudaStream_t)stream);
 }
 
 int launch_scale_bf16(Plan& p, const float* W, float* X0, int par, bool write_lo, void* stream) {

@@ -90,6 +90,7 @@ struct NsDesc {
   int32_t ldx, ldxt, ldr;   // padded bf16 leading dims: pad8(n), pad8(m), pad8(s)
   float alpha, beta, diag;
   int32_t tile_begin, tiles_n;
+  int32_t map_a, map_b;     // TMA tensor maps: maps[map_x + 2 * parity + lo]
 };
 
 struct PowerItem {        // one CTA of the pre-scaling kernels: rows [r0, r1) of matrix `mat`
@@ -151,6 +152,7 @@ struct Plan {
   int64_t bx_numel = 0, br_numel = 0;
   uint16_t* d_bx = nullptr;         // 8 x bx_numel: Xh[2], Xl[2], XTh[2], XTl[2]
   uint16_t* d_br = nullptr;         // 2 x br_numel: Rh, Rl
+  void* d_ns_maps = nullptr;        // CUtensorMap array of the NS operands (separate allocation)
   std::vector<PowerItem> power_items;
   std::vector<int32_t> owned_mats;  // indices of owned, non-empty matrices
   std::vector<MatItem> mat_items;   // same order as owned_mats
@@ -195,6 +197,7 @@ int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int 
 int launch_scale_bf16(Plan& p, const float* W, float* X0, int par, bool write_lo, void* stream);
 // tensor-core composition: built after the workspace exists; freed with the plan
 orth_status_t build_compose_tc(Plan& p);
+orth_status_t build_ns_tma(Plan& p);   // tensor maps of the NS operand copies; freed in destroy
 void free_compose_tc(Plan& p);
 int launch_compose_tc(Plan& p, const float* ortho, void* stream);   // fills comp (fp32) like the SIMT chain
 int launch_power_partial(Plan& p, const float* W, const float* v_in, int use_const_v, int frob, void* stream);

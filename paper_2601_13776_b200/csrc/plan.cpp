@@ -614,8 +614,10 @@ orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers
   if (device >= 0) {
     st = allocate(P);
     if (st == ORTH_OK && P.opts.compute != ORTH_F32) st = build_compose_tc(P);
+    if (st == ORTH_OK && P.opts.compute != ORTH_F32) st = build_ns_tma(P);
     if (st != ORTH_OK) {
       free_compose_tc(P);
+      if (P.d_ns_maps) cudaFree(P.d_ns_maps);
       if (P.d_arena) cudaFree(P.d_arena);
       delete h;
       return st;
@@ -628,6 +630,7 @@ orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers
 orth_status_t orth_plan_destroy(orth_plan_t plan) {
   if (!plan) return ORTH_OK;
   free_compose_tc(plan->p);
+  if (plan->p.d_ns_maps) cudaFree(plan->p.d_ns_maps);
   if (plan->p.d_arena) cudaFree(plan->p.d_arena);
   delete plan;
   return ORTH_OK;

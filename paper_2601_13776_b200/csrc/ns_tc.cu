@@ -52,8 +52,8 @@ __device__ __forceinline__ void split(float x, __nv_bfloat16& h, __nv_bfloat16& 
 
 template <int NPASS, int S>
 __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
-    ns_tc_kernel(const NsDesc* __restrict__ descs, int ndesc, NsBufs bufs, int par, int write_lo,
-                 const CUtensorMap* __restrict__ maps) {
+    ns_tc_kernel(const NsDesc* __restrict__ descs, const int* __restrict__ tile_desc, NsBufs bufs, int par,
+                 int write_lo, const CUtensorMap* __restrict__ maps) {
   constexpr bool SPLIT = NPASS == 3;
   constexpr int TILE = 128 * 128;
   constexpr int STAGE = (SPLIT ? 4 : 2) * TILE;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
   __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const NsDesc d = descs[find_ns(descs, ndesc, blockIdx.x)];
+  const NsDesc d = descs[tile_desc[blockIdx.x]];   // host-built tile -> problem table (one load)
   const int local = blockIdx.x - d.tile_begin;
   const int m0 = (local / d.tiles_n) * 128, n0 = (local % d.tiles_n) * 128;
 
@@ -122,6 +122,20 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
     }
     umma::mma_commit(&done_bar);
   }
+  // Prefetch this thread's C fragments (previous X, update phase) into registers
+  // while the MMAs run: 2 halves x 8 row-pass groups of 4 floats.
+  float4 cpre[16];
+  {
+    const bool fv = (d.ldf & 3) == 0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int h = u >> 3, e = tid + 256 * (u & 7), r = e >> 4, c4 = (e & 15) * 4;
+      const int i = m0 + r, j0 = n0 + h * 64 + c4;
+      cpre[u] = (d.epi == 1 && fv && i < d.M && j0 + 4 <= d.N)
+                    ? __ldg(reinterpret_cast<const float4*>(bufs.X[par] + d.f_off + (int64_t)i * d.ldf + j0))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
   umma::mbar_wait(&done_bar, 0);
   umma::tc_fence_after();
 
@@ -144,7 +158,7 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
   __nv_bfloat16* sTh = reinterpret_cast<__nv_bfloat16*>(smem + 128 * LDF * 4);   // [64][136] bf16
   __nv_bfloat16* sTl = sTh + 64 * LDT;
   const bool fvec = (d.ldf & 3) == 0;      // 16-byte aligned fp32 rows
-#pragma unroll 1
+#pragma unroll
   for (int h = 0; h < 2; ++h) {
     {
       const int q = warp & 3, sub = warp >> 2, r = q * 32 + lane;
@@ -158,8 +172,9 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
     umma::tc_fence_before();
     __syncthreads();
     // row pass: element group e -> (row r, 4 columns c4*4 .. +3)
-#pragma unroll 2
-    for (int e = tid; e < 128 * 16; e += 256) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + 256 * u;
       const int r = e >> 4, c4 = (e & 15) * 4;
       const int i = m0 + r, j0 = n0 + h * 64 + c4;
       float4 a = *reinterpret_cast<const float4*>(Sf + r * LDF + c4);
@@ -167,7 +182,7 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
       const bool row_ok = i < d.M;
       const int64_t fo = (int64_t)i * d.ldf + j0;
       if (row_ok && fvec && j0 + 4 <= d.N) {
-        float4 c = upd ? __ldg(reinterpret_cast<const float4*>(Cm + fo)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 c = cpre[h * 8 + u];
         o[0] = fmaf(d.alpha, o[0], d.beta * c.x);
         o[1] = fmaf(d.alpha, o[1], d.beta * c.y);
         o[2] = fmaf(d.alpha, o[2], d.beta * c.z);
@@ -282,7 +297,7 @@ NsBufs make_bufs(Plan& p, float* const bufs[BUF_COUNT]) {
 }
 
 template <int NPASS, int S>
-int launch_impl(const NsDesc* d, int nd, int tiles, NsBufs b, int par, int write_lo, const CUtensorMap* maps,
+int launch_impl(const NsDesc* d, const int* td, int tiles, NsBufs b, int par, int write_lo, const CUtensorMap* maps,
                 cudaStream_t s) {
   constexpr int STAGE = (NPASS == 3 ? 4 : 2) * 128 * 128;
   const size_t smem = 1024 + (size_t)(S * STAGE > 128 * 129 * 4 ? S * STAGE : 128 * 129 * 4);
@@ -291,7 +306,7 @@ int launch_impl(const NsDesc* d, int nd, int tiles, NsBufs b, int par, int write
     cudaFuncSetAttribute(ns_tc_kernel<NPASS, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  ns_tc_kernel<NPASS, S><<<tiles, 256, smem, s>>>(d, nd, b, par, write_lo, maps);
+  ns_tc_kernel<NPASS, S><<<tiles, 256, smem, s>>>(d, td, b, par, write_lo, maps);
   return (int)cudaGetLastError();
 }
 
@@ -345,9 +360,25 @@ orth_status_t build_ns_tma(Plan& p) {
       }
     }
   if (maps.empty()) return ORTH_OK;
-  cudaError_t e = cudaMalloc(&p.d_ns_maps, maps.size() * sizeof(CUtensorMap));
+  std::vector<int> tg, tu;   // tile -> problem tables
+  for (int i = 0; i < (int)p.ns_gram.size(); ++i) {
+    const NsDesc& d = p.ns_gram[i];
+    for (int t = 0; t < ((d.M + 127) / 128) * d.tiles_n; ++t) tg.push_back(i);
+  }
+  for (int i = 0; i < (int)p.ns_upd.size(); ++i) {
+    const NsDesc& d = p.ns_upd[i];
+    for (int t = 0; t < ((d.M + 127) / 128) * d.tiles_n; ++t) tu.push_back(i);
+  }
+  const size_t mbytes = maps.size() * sizeof(CUtensorMap);
+  cudaError_t e = cudaMalloc(&p.d_ns_maps, mbytes + (tg.size() + tu.size()) * sizeof(int));
   if (e == cudaSuccess)
-    e = cudaMemcpy(p.d_ns_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(p.d_ns_maps, maps.data(), mbytes, cudaMemcpyHostToDevice);
+  p.d_ns_tile_gram = reinterpret_cast<int*>(static_cast<char*>(p.d_ns_maps) + mbytes);
+  p.d_ns_tile_upd = p.d_ns_tile_gram + tg.size();
+  if (e == cudaSuccess && !tg.empty())
+    e = cudaMemcpy(p.d_ns_tile_gram, tg.data(), tg.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !tu.empty())
+    e = cudaMemcpy(p.d_ns_tile_upd, tu.data(), tu.size() * sizeof(int), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.ns_gram.empty())
     e = cudaMemcpy(p.d_ns_gram, p.ns_gram.data(), p.ns_gram.size() * sizeof(NsDesc), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.ns_upd.empty())
@@ -367,8 +398,10 @@ int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int 
   NsBufs b = make_bufs(p, bufs);
   p.launches++;
   auto maps = reinterpret_cast<const CUtensorMap*>(p.d_ns_maps);
-  if (npass == 3) return launch_impl<3, 3>(d, nd, tiles, b, par, write_lo, maps, (cudaStream_t)stream);
-  return launch_impl<1, 3>(d, nd, tiles, b, par, write_lo, maps, (cudaStream_t)stream);
+  const int* td = gram ? p.d_ns_tile_gram : p.d_ns_tile_upd;
+  (void)nd;
+  if (npass == 3) return launch_impl<3, 3>(d, td, tiles, b, par, write_lo, maps, (cudaStream_t)stream);
+  return launch_impl<1, 3>(d, td, tiles, b, par, write_lo, maps, (cudaStream_t)stream);
 }
 
 int launch_scale_bf16(Plan& p, const float* W, float* X0, int par, bool write_lo, void* stream) {

@@ -153,6 +153,8 @@ struct Plan {
   uint16_t* d_bx = nullptr;         // 8 x bx_numel: Xh[2], Xl[2], XTh[2], XTl[2]
   uint16_t* d_br = nullptr;         // 2 x br_numel: Rh, Rl
   void* d_ns_maps = nullptr;        // CUtensorMap array of the NS operands (separate allocation)
+  int* d_ns_tile_gram = nullptr;    // tile -> problem tables (inside the d_ns_maps allocation)
+  int* d_ns_tile_upd = nullptr;
   std::vector<PowerItem> power_items;
   std::vector<int32_t> owned_mats;  // indices of owned, non-empty matrices
   std::vector<MatItem> mat_items;   // same order as owned_mats

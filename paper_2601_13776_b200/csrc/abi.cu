@@ -154,7 +154,8 @@ orth_status_t orth_conv_transpose(orth_plan_t plan, int32_t layer, const void* k
   int Ho = 0, Wo = 0;
   st = check_conv(P, layer, kernel, y_small, x_big, N, H_big, W_big, io, Ho, Wo);
   if (st != ORTH_OK) return st;
-  const int e = launch_conv_bwd(P.layers[layer], kernel, bias, y_small, x_big, N, H_big, W_big, Ho, Wo, io, stream);
+  const int e = launch_conv_bwd(P.layers[layer], kernel, P.d_wt_scratch, bias, y_small, x_big, N, H_big, W_big, Ho,
+                                Wo, io, stream);
   P.launches++;
   return cuda_fail(e, "orth_conv_transpose");
 }

@@ -322,8 +322,10 @@ int launch_conv_fwd(const LayerInfo& L, const void* kernel, const float* bias, c
   return (int)cudaGetLastError();
 }
 
-int launch_conv_bwd(const LayerInfo& L, const void* kernel, const float* bias, const void* y, void* x, int N, int H,
-                    int W, int Ho, int Wo, int io, void* stream) {
+int launch_conv_bwd(const LayerInfo& L, const void* kernel, void* wt_scratch, const float* bias, const void* y,
+                    void* x, int N, int H, int W, int Ho, int Wo, int io, void* stream) {
+  if (io == ORTH_BF16 && wt_scratch && conv_bwd_tc_eligible(L) && !getenv("ORTH_FORCE_SIMT"))
+    return launch_conv_bwd_tc(L, kernel, wt_scratch, bias, y, x, N, H, W, Ho, Wo, stream);
   const ConvArgs a = make_args(L, N, H, W, Ho, Wo);
   const int64_t M = (int64_t)N * H * W;
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((L.ci + BN - 1) / BN), (unsigned)L.g);

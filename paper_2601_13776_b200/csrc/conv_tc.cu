@@ -1,43 +1,50 @@
-// a6 on the 5th-generation tensor cores: implicit-GEMM conv forward, BF16 in,
-// FP32 accumulation in TMEM, BF16 out (P:122 forward "single call", P:332-338
-// stride / dilation / groups; circular or zero padding, reading R11).
+// a6 / a7 on the 5th-generation tensor cores: implicit-GEMM convolution and
+// its exact adjoint (transposed convolution), BF16 in, FP32 accumulation in
+// TMEM, BF16 out (circular or zero padding, reading R11).
 //
-// GEMM view per group g: D[M = N*Ho*Wo pixels, N = co_g] = A[M, K] B[N, K]^T with
-// K = (tap, channel), A[m, (a,b,c)] = x~[n, s*u + d*a - p_t, s*v + d*b - p_l, g*ci_g + c]
-// and B = the BF16 GEMM-layout kernel (C_o, k, k, C_i/g), already K-major.
+// Forward, per group g:  D[m, n] = sum_{(a,b), c} x~[pix(m, a, b), g*ci_g + c] * W[g*co_g + n, a, b, c]
+//   m = output pixel (N*Ho*Wo), pix = (s u + d a - p_t, s v + d b - p_l) wrapped / zero-padded.
+// Adjoint (orth_conv_transpose, R13/R14), gather form with polyphase tiles:
+//   output pixels of the large grid are grouped by phase (h mod s, w mod s); in a
+//   phase only the taps with (h + p_t - d a) = 0 (mod s) contribute, so the
+//   K loop runs over exactly those taps:
+//   D[m, n] = sum_{valid (a,b), o} y[(h + p_t - d a)/s, (w + p_l - d b)/s, g*co_g + o] * W[g*co_g + o, a, b, n]
+//   (B = W^T per tap, produced by a small transpose kernel into plan workspace).
 //
 // Persistent, warp-specialised kernel (one CTA per SM, 416 threads):
-//   warps 0-7   producers.  Per tile they first build a (tap, row) -> input
-//               pixel table in shared memory (-1 = zero padding; circular
-//               padding wraps here), so the per-stage gather is a table read
-//               plus a 16-byte cp.async per (row, 8-channel chunk) into an
-//               S-stage SWIZZLE_128B ring (zero-fill for padding / tails).
-//               After cp.async.wait_group + fence.proxy.async they arrive on
-//               the stage's `full` mbarrier, LAG stages behind.
+//   warps 0-7   producers: per tile build a (valid tap, row) -> input pixel
+//               table in shared memory (-1 = zero padding; circular padding
+//               wraps here), then per stage 16-byte cp.async of the A rows into
+//               an S-stage SWIZZLE_128B ring (zero-fill for padding / channel
+//               tails); thread 0 also issues the B tile (BN rows x 64 channels
+//               of one tap) by TMA.  After cp.async.wait_group + fence.proxy.async
+//               they arrive on the stage's `full` mbarrier, LAG stages behind.
 //   warp 8      TMEM allocation + one thread issuing tcgen05.mma (M=128, N=BN,
-//               K=16, x4 per stage) into one of two TMEM accumulators,
-//               committing to the stage's `empty` barrier and, per tile, `tfull`.
+//               K=16, x4 per stage) into one of two TMEM accumulators.
 //   warps 9-12  epilogue: tcgen05.ld of their 32-lane quarter, bias, RNE to
 //               BF16, NHWC stores; arrive on `tempty`.
-// The accumulator is double-buffered, so the epilogue of tile t overlaps the
-// mainloop of tile t+1.  (Measured: a single producer warp per SM sub-partition
-// was instruction-latency bound at ~2.5k cycles per stage; the table cuts the
-// per-row work to a load, a compare and an address multiply.)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "orth_internal.h"
-#include "umma.cuh"
 #include "tma_host.h"
+#include "umma.cuh"
 
 namespace orth {
 namespace {
 
+constexpr int MAX_PHASES = 16;             // s <= 4
 struct TcConvArgs {
-  int N, H, W, Ci, Co, ci_g, co_g, k, s, d, pt, pl, Ho, Wo, circ;
-  int tiles_m, tiles_n, num_tiles;
+  int N, H, W, Ho, Wo, k, s, d, pt, pl, circ, transposed;
+  int in_C, out_C;        // channel strides of the input / output tensors
+  int cr_g, nout_g;       // reduction channels and output channels per group
+  int tiles_n, num_tiles;
+  int nphase;             // 1 (forward) or s*s (transposed)
+  int phase_tile0[MAX_PHASES + 1];   // first tile (over m) of each phase, prefix sums
+  int phase_hp[MAX_PHASES], phase_wp[MAX_PHASES], phase_cnt[MAX_PHASES];
+  int tiles_m;            // = phase_tile0[nphase]
 };
 
 constexpr int NPROD = 256;                 // producer threads (warps 0-7)
@@ -50,18 +57,83 @@ __device__ __forceinline__ int wrapi(int x, int n) {
   return x < 0 ? x + n : x;
 }
 
+struct TileInfo {
+  int g, n0, phase, m0, cnt;   // m0: first row inside the phase; cnt: rows of the phase
+};
+
+__device__ __forceinline__ TileInfo decode_tile(const TcConvArgs& a, int tile, int BN) {
+  TileInfo t;
+  const int tm = tile % a.tiles_m, rest = tile / a.tiles_m;
+  const int tn = rest % a.tiles_n;
+  t.g = rest / a.tiles_n;
+  t.n0 = tn * BN;
+  int p = 0;
+  while (p + 1 < a.nphase && a.phase_tile0[p + 1] <= tm) ++p;
+  t.phase = p;
+  t.m0 = (tm - a.phase_tile0[p]) * 128;
+  t.cnt = a.phase_cnt[p];
+  return t;
+}
+
+// taps contributing to a phase (all taps for the forward); returns the count
+__device__ __forceinline__ bool tap_valid(const TcConvArgs& a, int phase, int tap) {
+  if (!a.transposed) return true;
+  const int ph = phase / a.s, pw = phase % a.s;
+  const int ta = tap / a.k, tb = tap % a.k;
+  return ((ph + a.pt - a.d * ta) % a.s + a.s) % a.s == 0 && ((pw + a.pl - a.d * tb) % a.s + a.s) % a.s == 0;
+}
+
+// output pixel index (n*Hout + h)*Wout + w of row m of a phase
+__device__ __forceinline__ int out_pixel(const TcConvArgs& a, int phase, int m) {
+  if (!a.transposed) return m;
+  const int hp = a.phase_hp[phase], wp = a.phase_wp[phase];
+  const int n = m / (hp * wp), r = m - n * hp * wp;
+  const int hh = r / wp, ww = r - hh * wp;
+  const int h = phase / a.s + a.s * hh, w = phase % a.s + a.s * ww;
+  return (n * a.H + h) * a.W + w;
+}
+
+// input pixel of row m for tap (ta, tb); -1 = zero padding
+__device__ __forceinline__ int in_pixel(const TcConvArgs& a, int phase, int m, int ta, int tb) {
+  if (!a.transposed) {
+    const int hw = a.Ho * a.Wo;
+    const int n = m / hw, rr = m - n * hw, u = rr / a.Wo, vv = rr - u * a.Wo;
+    int h = u * a.s - a.pt + a.d * ta, w = vv * a.s - a.pl + a.d * tb;
+    if (a.circ) {
+      h = wrapi(h, a.H);
+      w = wrapi(w, a.W);
+    } else if (h < 0 || h >= a.H || w < 0 || w >= a.W) {
+      return -1;
+    }
+    return (n * a.H + h) * a.W + w;
+  }
+  const int hp = a.phase_hp[phase], wp = a.phase_wp[phase];
+  const int n = m / (hp * wp), r = m - n * hp * wp;
+  const int hh = r / wp, ww = r - hh * wp;
+  int th = phase / a.s + a.s * hh + a.pt - a.d * ta, tw = phase % a.s + a.s * ww + a.pl - a.d * tb;
+  if (a.circ) {
+    th = wrapi(th, a.H);
+    tw = wrapi(tw, a.W);
+  } else if (th < 0 || tw < 0) {
+    return -1;
+  }
+  const int u = th / a.s, v = tw / a.s;   // exact: the phase makes th, tw multiples of s
+  if (u >= a.Ho || v >= a.Wo) return -1;
+  return (n * a.Ho + u) * a.Wo + v;
+}
+
 template <int BN, int S>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    conv_fwd_ws(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
-                const float* __restrict__ bias, __nv_bfloat16* __restrict__ y, TcConvArgs a,
-                const __grid_constant__ CUtensorMap tmB) {
+    conv_ws(const __nv_bfloat16* __restrict__ in, const float* __restrict__ bias, __nv_bfloat16* __restrict__ out,
+            const __grid_constant__ TcConvArgs a, const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
   constexpr int LAG = S - 2;   // stages of cp.async kept in flight per producer thread
-  int* tab = reinterpret_cast<int*>(smem + S * STAGE);   // [taps][128] input pixel index, -1 = padding
+  int* tab = reinterpret_cast<int*>(smem + S * STAGE);   // [valid tap j][128] input pixel, -1 = padding
   __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
+  __shared__ int tap_id[MAX_TAPS];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == MMA_WARP) umma::tmem_alloc(&tmem_base_sh, 2 * BN);
@@ -81,11 +153,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   umma::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const uint32_t s0 = umma::smem_u32(smem);
-  const int kc = (a.ci_g + 63) / 64;
+  const int kc = (a.cr_g + 63) / 64;
   const int kk2 = a.k * a.k;
-  const int nk = kk2 * kc;
-  const int M = a.N * a.Ho * a.Wo;
-  const int hw = a.Ho * a.Wo;
 
   if (warp < MMA_WARP) {
     // ------------------------------------------------------------ producers
@@ -94,50 +163,72 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t tab_s = umma::smem_u32(tab);
     int it = 0, st = 0, ph = 0;                // ring position of k-block `it`
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
-      const int tm = tile % a.tiles_m, rest = tile / a.tiles_m;
-      const int tn = rest % a.tiles_n, g = rest / a.tiles_n;
-      const int m0 = tm * 128, n0 = tn * BN;
-      umma::named_bar_sync(1, NPROD);          // everyone is done reading the previous table
-      for (int e = tid; e < 128 * kk2; e += NPROD) {
-        const int r = e & 127, t = e >> 7;
-        const int m = m0 + r;
-        int v = -1;
-        if (m < M) {
-          const int n = m / hw, rr = m - n * hw;
-          const int u = rr / a.Wo, vv = rr - u * a.Wo;
-          int h = u * a.s - a.pt + a.d * (t / a.k), ww = vv * a.s - a.pl + a.d * (t % a.k);
-          bool ok = true;
-          if (a.circ) {
-            h = wrapi(h, a.H);
-            ww = wrapi(ww, a.W);
-          } else {
-            ok = h >= 0 && h < a.H && ww >= 0 && ww < a.W;
-          }
-          if (ok) v = (n * a.H + h) * a.W + ww;
+      const TileInfo t = decode_tile(a, tile, BN);
+      umma::named_bar_sync(1, NPROD);          // everyone is done reading the previous table / tap list
+      int nt = 0;
+      for (int tap = 0; tap < kk2; ++tap)
+        if (tap_valid(a, t.phase, tap)) {
+          if (tid == 0) tap_id[nt] = tap;
+          ++nt;
         }
-        tab[t * 128 + r] = v;
+      umma::named_bar_sync(1, NPROD);
+      {  // each row decoded once; the two thread halves split the taps
+        const int r = tid & 127, m = t.m0 + r;
+        int nb = -1, hb = 0, wb = 0;   // image, base row / column (tap 0)
+        if (m < t.cnt) {
+          if (!a.transposed) {
+            const int hw = a.Ho * a.Wo, n = m / hw, rr = m - n * hw, u = rr / a.Wo;
+            nb = n; hb = u * a.s - a.pt; wb = (rr - u * a.Wo) * a.s - a.pl;
+          } else {
+            const int hp = a.phase_hp[t.phase], wp = a.phase_wp[t.phase];
+            const int n = m / (hp * wp), rr = m - n * hp * wp, hh = rr / wp;
+            nb = n; hb = t.phase / a.s + a.s * hh + a.pt; wb = t.phase % a.s + a.s * (rr - hh * wp) + a.pl;
+          }
+        }
+        for (int j = tid >> 7; j < nt; j += 2) {
+          const int tap = tap_id[j], ta = tap / a.k, tb = tap - ta * a.k;
+          int v = -1;
+          if (nb >= 0) {
+            if (!a.transposed) {
+              int h = hb + a.d * ta, w = wb + a.d * tb;
+              bool ok = true;
+              if (a.circ) { h = wrapi(h, a.H); w = wrapi(w, a.W); }
+              else ok = h >= 0 && h < a.H && w >= 0 && w < a.W;
+              if (ok) v = (nb * a.H + h) * a.W + w;
+            } else {
+              int th = hb - a.d * ta, tw = wb - a.d * tb;
+              bool ok = true;
+              if (a.circ) { th = wrapi(th, a.H); tw = wrapi(tw, a.W); }
+              else ok = th >= 0 && tw >= 0;
+              const int u = th / a.s, vv = tw / a.s;   // exact: the phase makes th, tw multiples of s
+              if (ok && u < a.Ho && vv < a.Wo) v = (nb * a.Ho + u) * a.Wo + vv;
+            }
+          }
+          tab[j * 128 + r] = v;
+        }
       }
       umma::named_bar_sync(1, NPROD);
-      const __nv_bfloat16* xg = x + (int64_t)g * a.ci_g + c * 8;
+      const __nv_bfloat16* ig = in + (int64_t)t.g * a.cr_g + c * 8;
       const uint32_t off_r[4] = {umma::sw128_off(rbase, c), umma::sw128_off(rbase + 32, c),
                                  umma::sw128_off(rbase + 64, c), umma::sw128_off(rbase + 96, c)};
-      for (int tap = 0; tap < kk2; ++tap) {
-        const uint32_t trow = tab_s + (uint32_t)(tap * 128 + rbase) * 4u;
+      for (int j = 0; j < nt; ++j) {
+        const int tap = tap_id[j];
+        const uint32_t trow = tab_s + (uint32_t)(j * 128 + rbase) * 4u;
         int pix[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) pix[i] = umma::ld_shared_s32(trow + 128u * i);
-        for (int c0 = 0; c0 < a.ci_g; c0 += 64, ++it) {
+        for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++it) {
           umma::mbar_wait(&empty_bar[st], ph ^ 1);
           const uint32_t sa = s0 + st * STAGE;
-          if (tid == 0) {   // B tile (BN x 64 channels of this tap) by TMA, SWIZZLE_128B, OOB -> 0
+          if (tid == 0) {   // B tile (BN rows x 64 channels of this tap) by TMA, SWIZZLE_128B, OOB -> 0
             umma::mbar_arrive_expect_tx(&full_bar[st], B_BYTES);
-            umma::tma_load_3d(sa + A_BYTES, &tmB, &full_bar[st], c0, tap, g * a.co_g + n0);
+            umma::tma_load_3d(sa + A_BYTES, &tmB, &full_bar[st], c0, tap, t.g * a.nout_g + t.n0);
           }
-          const bool cok = c0 + c * 8 < a.ci_g;
+          const bool cok = c0 + c * 8 < a.cr_g;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const bool ok = cok && pix[i] >= 0;
-            umma::cp_async16(sa + off_r[i], ok ? xg + (int64_t)pix[i] * a.Ci + c0 : x, ok);
+            umma::cp_async16(sa + off_r[i], ok ? ig + (int64_t)pix[i] * a.in_C + c0 : in, ok);
           }
           umma::cp_async_commit();
           if (it >= LAG) {
@@ -160,6 +251,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       constexpr uint32_t IDESC = umma::idesc_bf16(128, BN);
       int it = 0, tcount = 0;
       for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++tcount) {
+        const TileInfo t = decode_tile(a, tile, BN);
+        int nt = 0;
+        for (int tap = 0; tap < kk2; ++tap) nt += tap_valid(a, t.phase, tap) ? 1 : 0;
+        const int nk = nt * kc;
         const int acc = tcount & 1;
         umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
         umma::tc_fence_after();
@@ -185,18 +280,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int r = q * 32 + lane;
     int tcount = 0;
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++tcount) {
+      const TileInfo t = decode_tile(a, tile, BN);
+      const int m = t.m0 + r;
+      const int opix = m < t.cnt ? out_pixel(a, t.phase, m) : -1;
       const int acc = tcount & 1;
       umma::mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
       umma::tc_fence_after();
-      const int tm = tile % a.tiles_m, rest = tile / a.tiles_m;
-      const int tn = rest % a.tiles_n, g = rest / a.tiles_n;
-      const int m = tm * 128 + r;
-      const int obase = g * a.co_g + tn * BN;
+      const int obase = t.g * a.nout_g + t.n0;
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += 32) {
         float v[32];
         umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + cc), v);
-        if (m < M) {
+        if (opix >= 0) {
           const int o = obase + cc;
           uint32_t pk[16];
 #pragma unroll
@@ -206,7 +301,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
             pk[i] = *reinterpret_cast<uint32_t*>(&b2);
           }
-          uint4* dst = reinterpret_cast<uint4*>(y + (int64_t)m * a.Co + o);
+          uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)opix * a.out_C + o);
 #pragma unroll
           for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
         }
@@ -218,6 +313,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   umma::tc_fence_before();
   __syncthreads();
   if (warp == MMA_WARP) umma::tmem_dealloc(tmem, 2 * BN);
+}
+
+// W^T per tap for the adjoint: WT[(g ci_g + i) k^2 + t][o] = W[(g co_g + o) k^2 + t][i]
+__global__ void __launch_bounds__(256) transpose_w_kernel(const __nv_bfloat16* __restrict__ w,
+                                                          __nv_bfloat16* __restrict__ wt, int g, int co_g, int ci_g,
+                                                          int taps) {
+  __shared__ __nv_bfloat16 tile[32][34];
+  const int gt = blockIdx.z;   // (group, tap)
+  const int gi = gt / taps, t = gt - gi * taps;
+  const int o0 = blockIdx.y * 32, i0 = blockIdx.x * 32;
+  for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+    const int oo = e >> 5, ii = e & 31;
+    const int o = o0 + oo, i = i0 + ii;
+    tile[oo][ii] = (o < co_g && i < ci_g) ? w[(((int64_t)gi * co_g + o) * taps + t) * ci_g + i] : __float2bfloat16(0.f);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+    const int ii = e >> 5, oo = e & 31;
+    const int o = o0 + oo, i = i0 + ii;
+    if (o < co_g && i < ci_g) wt[(((int64_t)gi * ci_g + i) * taps + t) * co_g + o] = tile[oo][ii];
+  }
+  (void)g;
 }
 
 int num_sms() {
@@ -232,49 +349,95 @@ int num_sms() {
 }
 
 template <int BN, int S>
-int launch_ws(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias, __nv_bfloat16* y, TcConvArgs a,
-              cudaStream_t stream) {
+int launch_ws(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
+              const TcConvArgs& a, cudaStream_t stream) {
   const size_t smem = 1024 + (size_t)S * (128 * 128 + BN * 128) + (size_t)MAX_TAPS * 128 * 4;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(conv_fwd_ws<BN, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(conv_ws<BN, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   const int grid = a.num_tiles < num_sms() ? a.num_tiles : num_sms();
   CUtensorMap tm;
-  if (!make_weight_tmap(&tm, w, a.Co, a.k * a.k, a.ci_g, BN)) return (int)cudaErrorInvalidValue;
-  conv_fwd_ws<BN, S><<<grid, NTHREADS, smem, stream>>>(x, w, bias, y, a, tm);
+  if (!make_weight_tmap(&tm, w, w_rows, a.k * a.k, a.cr_g, BN)) return (int)cudaErrorInvalidValue;
+  conv_ws<BN, S><<<grid, NTHREADS, smem, stream>>>(in, bias, out, a, tm);
   return (int)cudaGetLastError();
+}
+
+int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
+               TcConvArgs& a, int groups, cudaStream_t s) {
+  const int n = a.nout_g;
+  const int bn = n % 256 == 0 ? 256 : n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32;
+  a.tiles_n = n / bn;
+  a.num_tiles = a.tiles_m * a.tiles_n * groups;
+  if (a.num_tiles == 0) return 0;
+  switch (bn) {
+    case 256: return launch_ws<256, 4>(in, w, w_rows, bias, out, a, s);
+    case 128: return launch_ws<128, 5>(in, w, w_rows, bias, out, a, s);
+    case 64: return launch_ws<64, 7>(in, w, w_rows, bias, out, a, s);
+    default: return launch_ws<32, 8>(in, w, w_rows, bias, out, a, s);
+  }
+}
+
+void base_args(TcConvArgs& a, const LayerInfo& L, int N, int H, int W, int Ho, int Wo) {
+  a = TcConvArgs{};
+  a.N = N; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo;
+  a.k = L.k; a.s = L.s; a.d = L.d; a.pt = L.pt; a.pl = L.pl;
+  a.circ = L.desc.padding_mode == ORTH_PAD_CIRCULAR;
 }
 
 }  // namespace
 
 bool conv_fwd_tc_eligible(const LayerInfo& L) {
-  return L.co % 64 == 0 && L.ci % 8 == 0 && L.ci_f % 8 == 0 && L.co_f % 8 == 0 && L.k * L.k <= MAX_TAPS;
+  return L.co % 32 == 0 && L.ci % 8 == 0 && L.ci_f % 8 == 0 && L.co_f % 8 == 0 && L.k * L.k <= MAX_TAPS;
+}
+
+bool conv_bwd_tc_eligible(const LayerInfo& L) {
+  return L.ci % 32 == 0 && L.co % 8 == 0 && L.ci_f % 8 == 0 && L.co_f % 8 == 0 && L.k * L.k <= MAX_TAPS &&
+         L.s * L.s <= MAX_PHASES;
 }
 
 int launch_conv_fwd_tc(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
                        int H, int W, int Ho, int Wo, void* stream) {
   TcConvArgs a;
-  a.N = N; a.H = H; a.W = W; a.Ci = L.ci_f; a.Co = L.co_f; a.ci_g = L.ci; a.co_g = L.co;
-  a.k = L.k; a.s = L.s; a.d = L.d; a.pt = L.pt; a.pl = L.pl; a.Ho = Ho; a.Wo = Wo;
-  a.circ = L.desc.padding_mode == ORTH_PAD_CIRCULAR;
-  const int64_t M = (int64_t)N * Ho * Wo;
-  a.tiles_m = (int)((M + 127) / 128);
-  auto xs = (const __nv_bfloat16*)x;
-  auto ws = (const __nv_bfloat16*)kernel;
-  auto ys = (__nv_bfloat16*)y;
+  base_args(a, L, N, H, W, Ho, Wo);
+  a.transposed = 0;
+  a.in_C = L.ci_f; a.out_C = L.co_f; a.cr_g = L.ci; a.nout_g = L.co;
+  a.nphase = 1;
+  a.phase_cnt[0] = N * Ho * Wo;
+  a.phase_tile0[0] = 0;
+  a.phase_tile0[1] = (a.phase_cnt[0] + 127) / 128;
+  a.tiles_m = a.phase_tile0[1];
+  return launch_any((const __nv_bfloat16*)x, (const __nv_bfloat16*)kernel, L.co_f, bias, (__nv_bfloat16*)y, a, L.g,
+                    (cudaStream_t)stream);
+}
+
+int launch_conv_bwd_tc(const LayerInfo& L, const void* kernel, void* wt_scratch, const float* bias, const void* y,
+                       void* x, int N, int H, int W, int Ho, int Wo, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  if (L.co % 256 == 0) {
-    a.tiles_n = L.co / 256; a.num_tiles = a.tiles_m * a.tiles_n * L.g;
-    return launch_ws<256, 4>(xs, ws, bias, ys, a, s);
+  const int taps = L.k * L.k;
+  dim3 tg((unsigned)((L.ci + 31) / 32), (unsigned)((L.co + 31) / 32), (unsigned)(L.g * taps));
+  transpose_w_kernel<<<tg, 256, 0, s>>>((const __nv_bfloat16*)kernel, (__nv_bfloat16*)wt_scratch, L.g, L.co, L.ci,
+                                        taps);
+  if (int e = (int)cudaGetLastError()) return e;
+  TcConvArgs a;
+  base_args(a, L, N, H, W, Ho, Wo);
+  a.transposed = 1;
+  a.in_C = L.co_f; a.out_C = L.ci_f; a.cr_g = L.co; a.nout_g = L.ci;
+  a.nphase = L.s * L.s;
+  int t0 = 0;
+  for (int p = 0; p < a.nphase; ++p) {
+    const int ph = p / L.s, pw = p % L.s;
+    a.phase_hp[p] = H > ph ? (H - ph + L.s - 1) / L.s : 0;
+    a.phase_wp[p] = W > pw ? (W - pw + L.s - 1) / L.s : 0;
+    a.phase_cnt[p] = N * a.phase_hp[p] * a.phase_wp[p];
+    a.phase_tile0[p] = t0;
+    t0 += (a.phase_cnt[p] + 127) / 128;
   }
-  if (L.co % 128 == 0) {
-    a.tiles_n = L.co / 128; a.num_tiles = a.tiles_m * a.tiles_n * L.g;
-    return launch_ws<128, 5>(xs, ws, bias, ys, a, s);
-  }
-  a.tiles_n = L.co / 64; a.num_tiles = a.tiles_m * a.tiles_n * L.g;
-  return launch_ws<64, 7>(xs, ws, bias, ys, a, s);
+  a.phase_tile0[a.nphase] = t0;
+  a.tiles_m = t0;
+  return launch_any((const __nv_bfloat16*)y, (const __nv_bfloat16*)wt_scratch, L.ci_f, bias, (__nv_bfloat16*)x, a,
+                    L.g, s);
 }
 
 }  // namespace orth

@@ -504,6 +504,9 @@ static orth_status_t allocate(Plan& P) {
   const size_t o_nsg = take(std::max<size_t>(P.ns_gram.size(), 1) * sizeof(NsDesc));
   const size_t o_nsu = take(std::max<size_t>(P.ns_upd.size(), 1) * sizeof(NsDesc));
   const size_t o_bx = take((size_t)8 * std::max<int64_t>(P.bx_numel, 64) * 2);
+  int64_t max_kernel = 64;
+  for (auto& L : P.layers) max_kernel = std::max(max_kernel, L.kernel_numel);
+  const size_t o_wt = take((size_t)max_kernel * 2);
   const size_t o_br = take((size_t)2 * std::max<int64_t>(P.br_numel, 64) * 2);
   std::vector<GemmPhase*> phases = {&P.gram[0], &P.gram[1], &P.update[0], &P.update[1], &P.gram_r[0],
                                     &P.gram_r[1], &P.update_r[0], &P.update_r[1], &P.proj, &P.aoc};
@@ -532,6 +535,7 @@ static orth_status_t allocate(Plan& P) {
   P.d_ns_gram = (NsDesc*)(base + o_nsg);
   P.d_ns_upd = (NsDesc*)(base + o_nsu);
   P.d_bx = (uint16_t*)(base + o_bx);
+  P.d_wt_scratch = (uint16_t*)(base + o_wt);
   P.d_br = (uint16_t*)(base + o_br);
   cudaError_t e = cudaMemset(P.d_arena, 0, off);   // also zero-pads the BF16 operand copies
   if (!P.ns_gram.empty() && e == cudaSuccess)

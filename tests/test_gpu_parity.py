@@ -162,6 +162,11 @@ CONV_CASES = [  # (ci, co, k, s, d, g, mode, H, kind)
     (40, 64, 3, 1, 1, 1, "circular", 6, "conv"), (72, 128, 5, 2, 1, 1, "zeros", 9, "conv"),
     (512, 512, 3, 1, 1, 1, "circular", 4, "conv"), (64, 128, 3, 2, 3, 1, "circular", 12, "conv"),
     (8, 32, 2, 2, 1, 2, "zeros", 9, "conv"), (3, 64, 3, 1, 1, 1, "zeros", 13, "conv"),
+    # tensor-core adjoint (polyphase tiles) and 32-wide output tiles (grouped layers)
+    (64, 64, 3, 2, 1, 1, "circular", 8, "convT"), (128, 64, 3, 2, 1, 1, "zeros", 9, "conv"),
+    (64, 64, 3, 1, 2, 2, "circular", 12, "convT"), (256, 256, 3, 1, 1, 8, "circular", 8, "conv"),
+    (64, 128, 4, 2, 1, 1, "zeros", 10, "convT"), (96, 96, 5, 3, 2, 3, "circular", 12, "conv"),
+    (64, 128, 3, 2, 1, 1, "zeros", 9, "conv"), (1024, 1024, 3, 1, 2, 32, "circular", 6, "convT"),
 ]
 
 

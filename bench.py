@@ -85,46 +85,69 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ workload
-def build_workload(orth, torch, cfg_layers, rank, world, device, compute, batch):
+def build_workload(orth, torch, cfg_layers, rank, world, device, compute, batch, chain=True, cfg_id=2):
+    """Plan, seeded parameters / power vectors, activations.  chain: each
+    layer consumes the previous output (cfg2/cfg3); otherwise every layer gets
+    its own seeded input (cfg4).  A transposed layer's forward is
+    orth_conv_transpose (small -> large grid)."""
     from synth import gen
     plan = orth.Plan(cfg_layers, device, rank=rank, world=world, compute=compute)
     params = np.zeros(plan.params_numel, np.float32)
     for i, m in enumerate(plan.matrices):
-        A = gen.param_matrix(m["m"], m["n"], (2, m["layer"], m["group"], i, gen.ROLE_ID[m["role"]]))
+        A = gen.param_matrix(m["m"], m["n"], (cfg_id, m["layer"], m["group"], i, gen.ROLE_ID[m["role"]]))
         params[m["off"]: m["off"] + A.size] = A.ravel()
     cache = np.zeros(plan.cache_numel, np.float32)
     for i, m in enumerate(plan.matrices):
-        v = gen.unit_vector(m["n"], (2, m["layer"], m["group"], i, gen.ROLE_ID["v"]))
+        v = gen.unit_vector(m["n"], (cfg_id, m["layer"], m["group"], i, gen.ROLE_ID["v"]))
         cache[m["cache_off"]: m["cache_off"] + v.size] = v
-    H0 = cfg_layers[0]["H"]
-    x = gen.activations((batch, H0, H0, cfg_layers[0]["c_in"]), (2, rank, 0, 0, gen.ROLE_ID["x"]))
     dev = torch.device("cuda", device)
-    W = dict(plan=plan, params_h=params, cache_h=cache, x_h=x)
+    W = dict(plan=plan, params_h=params, cache_h=cache, chain=chain)
     W["params"] = torch.from_numpy(params).to(dev)
     W["cache"] = torch.from_numpy(cache).to(dev)
     W["ortho"] = torch.zeros_like(W["params"])
     W["kf32"] = torch.zeros(plan.kf32_numel, device=dev)
     W["kbf16"] = torch.zeros(plan.kbf16_numel, device=dev, dtype=torch.bfloat16)
-    W["x"] = torch.from_numpy(x).to(dev, torch.bfloat16)
-    acts, H = [], H0
-    shapes = []
+    ins, acts, shapes = [], [], []
+    H = cfg_layers[0]["H"]
     for l, d in enumerate(cfg_layers):
-        Ho, _ = plan.out_hw(l, H, H)
+        if not chain or l == 0:
+            H = d["H"]
+            xl = gen.activations((batch, H, H, d["c_in"]), (cfg_id, rank, l, 0, gen.ROLE_ID["x"]))
+            if l == 0:
+                W["x_h"] = xl
+            ins.append(torch.from_numpy(xl).to(dev, torch.bfloat16))
+        else:
+            ins.append(acts[-1])
+        if d.get("kind") == "convT":
+            Ho = H * d["s"]                       # large grid of the transposed layer
+        else:
+            Ho, _ = plan.out_hw(l, H, H)
         acts.append(torch.empty((batch, Ho, Ho, d["c_out"]), device=dev, dtype=torch.bfloat16))
         shapes.append((H, Ho, d))
         H = Ho
-    W["acts"], W["shapes"] = acts, shapes
+    W["x"] = ins[0]
+    W["ins"], W["acts"], W["shapes"] = ins, acts, shapes
     W["kviews"] = [plan.kernel_bf16(W["kbf16"], l) for l in range(len(cfg_layers))]
     return W
 
 
 def conv_flops_bytes(shapes, batch):
+    """Algorithmic flops / bytes of each layer apply (a6 / a7)."""
     fl, by = [], []
     for (H, Ho, d) in shapes:
         ci, co, k, g = d["c_in"], d["c_out"], d["k"], d["g"]
-        fl.append(2.0 * batch * Ho * Ho * co * (ci // g) * k * k)
+        small = H if d.get("kind") == "convT" else Ho       # output grid of the forward conv
+        fl.append(2.0 * batch * small * small * co * (ci // g) * k * k)
         by.append(2.0 * batch * (H * H * ci + Ho * Ho * co) + 2.0 * co * (ci // g) * k * k)
     return fl, by
+
+
+def apply_layer(W, l):
+    plan = W["plan"]
+    if W["shapes"][l][2].get("kind") == "convT":
+        plan.conv_transpose(l, W["kviews"][l], W["ins"][l], W["acts"][l])
+    else:
+        plan.conv_forward(l, W["kviews"][l], W["ins"][l], W["acts"][l])
 
 
 def run_step(W, orth, torch, world, pg, ev=None, graphs=None):
@@ -148,21 +171,19 @@ def run_step(W, orth, torch, world, pg, ev=None, graphs=None):
         from paper_2601_13776_b200.dist import gather_kernels
         gather_kernels(plan, W["kbf16"], orth.orth_plan_query(plan.h, "KERNEL_SEGMENT_BF16"), pg)
     rec("gather1")
-    cur = W["x"]
-    for l, y in enumerate(W["acts"]):
+    for l in range(len(W["acts"])):
         rec(f"conv{l}_0")
         if graphs:
             graphs[f"conv{l}"].replay()
         else:
-            plan.conv_forward(l, W["kviews"][l], cur, y)
+            apply_layer(W, l)
         rec(f"conv{l}_1")
-        cur = y
-    return cur
+    return W["acts"][-1]
 
 
 def capture_graphs(W, torch):
-    """One CUDA graph per phase (orthogonalize: ~31 launches, compose: ~7, one
-    per conv layer), captured from the library's own calls on the capture stream."""
+    """One CUDA graph per phase (orthogonalize, compose, one per layer apply),
+    captured from the library's own calls on the capture stream."""
     plan = W["plan"]
     graphs = {}
     s = torch.cuda.Stream()
@@ -176,13 +197,11 @@ def capture_graphs(W, torch):
         with torch.cuda.graph(g, stream=s):
             plan.compose(W["ortho"], W["kf32"], W["kbf16"])
         graphs["comp"] = g
-        cur = W["x"]
-        for l, y in enumerate(W["acts"]):
+        for l in range(len(W["acts"])):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=s):
-                plan.conv_forward(l, W["kviews"][l], cur, y)
+                apply_layer(W, l)
             graphs[f"conv{l}"] = g
-            cur = y
     torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
     return graphs
@@ -204,7 +223,8 @@ def ours(args):
         pg = dist.group.WORLD
     cfg = configs.CONFIGS[args.config]()
     batch = configs.BATCH[args.config]
-    W = build_workload(orth, torch, cfg, rank, world, local, args.compute, batch)
+    W = build_workload(orth, torch, cfg, rank, world, local, args.compute, batch, chain=configs.CHAIN[args.config],
+                       cfg_id=args.config)
     plan = W["plan"]
     flush = torch.empty(int(2 * 126e6 // 4) + 1024, device="cuda", dtype=torch.float32)
 
@@ -257,7 +277,7 @@ def ours(args):
     conv_total = sum(t_conv)
     if conv_total >= t_orth:
         ach = sum(fl) / (conv_total * 1e-3) / 1e12
-        roof = {"kernel": "orth_conv_forward (12 launches, all layers)", "bound": "tensor", "achieved": ach,
+        roof = {"kernel": f"conv apply (orth_conv_forward / orth_conv_transpose), {len(fl)} launches", "bound": "tensor", "achieved": ach,
                 "peak": P["bf16_tflops_sustained"], "unit": "TFLOP/s", "frac": ach / P["bf16_tflops_sustained"],
                 "traffic": None, "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                 "per_launch_flops_avg": sum(fl) / len(fl), "avg_launch_ms": conv_total / len(fl),
@@ -275,8 +295,8 @@ def ours(args):
         "scaling": "weak", "vs_baseline": None,
         "dtype": {"bf16": "bf16", "bf16x3": "bf16x3", "f32": "f32+bf16"}[args.compute],
         "data": "synthetic (seeded near-orthogonal params, N(0,1) activations; SURVEY §8(d))",
-        "config": {"workload": f"config {args.config}: CIFAR-AOC-12 (12 orthogonal 3x3 convs 64-512 ch, 3 stride-2)",
-                   "global_batch": batch * world, "per_rank_batch": batch, "image": 32, "ns_iters": 12,
+        "config": {"workload": configs.NAMES[args.config],
+                   "global_batch": batch * world, "per_rank_batch": batch, "image": cfg[0]["H"], "ns_iters": 12,
                    "construction": {"f32": "FP32 FFMA (SIMT)",
                                     "bf16": "tcgen05 BF16, FP32 master, 3-pass split polish + composition",
                                     "bf16x3": "tcgen05 3-pass hi/lo split everywhere"}[args.compute],
@@ -293,7 +313,7 @@ def ours(args):
         "clocks": clocks,
         "e2e": e2e,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in (1, 2):
         out["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget)
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -416,7 +436,7 @@ def reference(args):
     out = {"metric": METRIC, "value": v, "unit": "layers/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-           "config": {"workload": f"config {args.config}: CIFAR-AOC-12", "global_batch": batch},
+           "config": {"workload": configs.NAMES[args.config], "global_batch": batch},
            "cpu_baseline": {"value": v, "unit": "layers/s", "cores": cores, "kind": "oracle",
                             "sample": f"each step: full float64 oracle construction + forward of 1 image "
                                       f"extrapolated to batch {batch}", "cpu": _cpu_model()},

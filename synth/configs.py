@@ -63,3 +63,8 @@ def cfg5(n: int) -> List[Dict]:
 
 CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4}
 BATCH = {1: 2, 2: 256, 3: 256, 4: 256}
+CHAIN = {1: True, 2: True, 3: True, 4: False}
+NAMES = {1: "config 1: one 3x3 16->16 circular layer",
+         2: "config 2: CIFAR-AOC-12 (12 orthogonal 3x3 convs 64-512 ch, 3 stride-2), 32x32",
+         3: "config 3: ImageNet AOC-ResNet34-shape (33 orthogonal convs, RKO 4x4 s4 stem), 224x224",
+         4: "config 4: 1024-ch paths at 56x56 (g32, d2, s2, transposed s2, transposed g32 d2)"}

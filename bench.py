@@ -109,6 +109,9 @@ def build_workload(orth, torch, cfg_layers, rank, world, device, compute, batch,
     W["kbf16"] = torch.zeros(plan.kbf16_numel, device=dev, dtype=torch.bfloat16)
     ins, acts, shapes = [], [], []
     H = cfg_layers[0]["H"]
+    if batch == 0:       # dense NS sweep (config 5): construction only
+        cfg_layers = []
+        W["x_h"] = np.zeros((1,), np.float32)
     for l, d in enumerate(cfg_layers):
         if not chain or l == 0:
             H = d["H"]
@@ -125,7 +128,7 @@ def build_workload(orth, torch, cfg_layers, rank, world, device, compute, batch,
         acts.append(torch.empty((batch, Ho, Ho, d["c_out"]), device=dev, dtype=torch.bfloat16))
         shapes.append((H, Ho, d))
         H = Ho
-    W["x"] = ins[0]
+    W["x"] = ins[0] if ins else torch.zeros(1, device=dev, dtype=torch.bfloat16)
     W["ins"], W["acts"], W["shapes"] = ins, acts, shapes
     W["kviews"] = [plan.kernel_bf16(W["kbf16"], l) for l in range(len(cfg_layers))]
     return W
@@ -221,10 +224,13 @@ def ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist.group.WORLD
-    cfg = configs.CONFIGS[args.config]()
-    batch = configs.BATCH[args.config]
-    W = build_workload(orth, torch, cfg, rank, world, local, args.compute, batch, chain=configs.CHAIN[args.config],
-                       cfg_id=args.config)
+    if args.config == 5:
+        cfg, batch = configs.cfg5(args.n)[: args.mats], 0
+    else:
+        cfg = configs.CONFIGS[args.config]()
+        batch = configs.BATCH[args.config]
+    W = build_workload(orth, torch, cfg, rank, world, local, args.compute, batch,
+                       chain=configs.CHAIN.get(args.config, False), cfg_id=args.config)
     plan = W["plan"]
     flush = torch.empty(int(2 * 126e6 // 4) + 1024, device="cuda", dtype=torch.float32)
 
@@ -248,7 +254,8 @@ def ours(args):
     clk = Clocks(local)
     clk.start()
     launches0 = plan.launches
-    names = ["orth0", "orth1", "comp1", "gather1"] + [f"conv{l}_{e}" for l in range(len(cfg)) for e in (0, 1)]
+    nl = len(W["acts"])
+    names = ["orth0", "orth1", "comp1", "gather1"] + [f"conv{l}_{e}" for l in range(nl) for e in (0, 1)]
     ev = {n: [] for n in names}
     barrier()
     for _ in range(args.steps):
@@ -259,12 +266,13 @@ def ours(args):
     clocks = clk.stop()
     plan.check()
     el = lambda a, b, i: ev[a][i].elapsed_time(ev[b][i])
-    step_ms = [el("orth0", f"conv{len(cfg) - 1}_1", i) for i in range(args.steps)]
+    last = f"conv{nl - 1}_1" if nl else "gather1"
+    step_ms = [el("orth0", last, i) for i in range(args.steps)]
     t_step = sum(step_ms) / args.steps
     t_orth = sum(el("orth0", "orth1", i) for i in range(args.steps)) / args.steps
     t_comp = sum(el("orth1", "comp1", i) for i in range(args.steps)) / args.steps
     t_gather = sum(el("comp1", "gather1", i) for i in range(args.steps)) / args.steps
-    t_conv = [sum(el(f"conv{l}_0", f"conv{l}_1", i) for i in range(args.steps)) / args.steps for l in range(len(cfg))]
+    t_conv = [sum(el(f"conv{l}_0", f"conv{l}_1", i) for i in range(args.steps)) / args.steps for l in range(nl)]
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([t_step], device="cuda")
@@ -275,7 +283,7 @@ def ours(args):
     ns_flops = orth.orth_plan_query(plan.h, "NS_FLOPS")
     # dominant kernel class: conv forward (sum over layers) vs NS
     conv_total = sum(t_conv)
-    if conv_total >= t_orth:
+    if nl and conv_total >= t_orth:
         ach = sum(fl) / (conv_total * 1e-3) / 1e12
         roof = {"kernel": f"conv apply (orth_conv_forward / orth_conv_transpose), {len(fl)} launches", "bound": "tensor", "achieved": ach,
                 "peak": P["bf16_tflops_sustained"], "unit": "TFLOP/s", "frac": ach / P["bf16_tflops_sustained"],
@@ -295,7 +303,7 @@ def ours(args):
         "scaling": "weak", "vs_baseline": None,
         "dtype": {"bf16": "bf16", "bf16x3": "bf16x3", "f32": "f32+bf16"}[args.compute],
         "data": "synthetic (seeded near-orthogonal params, N(0,1) activations; SURVEY §8(d))",
-        "config": {"workload": configs.NAMES[args.config],
+        "config": {"workload": configs.NAMES.get(args.config, f"config 5: {len(cfg)} dense {args.n}x{args.n} matrices"),
                    "global_batch": batch * world, "per_rank_batch": batch, "image": cfg[0]["H"], "ns_iters": 12,
                    "construction": {"f32": "FP32 FFMA (SIMT)",
                                     "bf16": "tcgen05 BF16, FP32 master, 3-pass split polish + composition",
@@ -306,8 +314,8 @@ def ours(args):
         "breakdown_ms": {"orthogonalize": t_orth, "compose": t_comp, "allgather": t_gather,
                          "conv_forward": conv_total, "conv_per_layer": t_conv},
         "ns_tflops": ns_flops / (t_orth * 1e-3) / 1e12,
-        "conv_tflops": sum(fl) / (conv_total * 1e-3) / 1e12,
-        "conv_gbs": sum(by) / (conv_total * 1e-3) / 1e9,
+        "conv_tflops": sum(fl) / (conv_total * 1e-3) / 1e12 if nl else None,
+        "conv_gbs": sum(by) / (conv_total * 1e-3) / 1e9 if nl else None,
         "roofline": roof,
         "gpu_launches": launches,
         "clocks": clocks,
@@ -327,13 +335,14 @@ def e2e_run(W, orth, torch, world, pg, args, barrier):
     step's inputs (params + x) and D2H of its result inside the timed region."""
     ph = torch.from_numpy(W["params_h"]).pin_memory()
     xh = torch.from_numpy(W["x_h"]).to(torch.bfloat16).pin_memory()
-    yh = torch.empty(W["acts"][-1].shape, dtype=torch.bfloat16).pin_memory()
+    res = W["acts"][-1] if W["acts"] else W["ortho"]
+    yh = torch.empty(res.shape, dtype=res.dtype).pin_memory()
     s = torch.cuda.current_stream()
     for _ in range(2):
         W["params"].copy_(ph, non_blocking=True)
         W["x"].copy_(xh, non_blocking=True)
         run_step(W, orth, torch, world, pg)
-        yh.copy_(W["acts"][-1], non_blocking=True)
+        yh.copy_(res, non_blocking=True)
     barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
@@ -343,7 +352,7 @@ def e2e_run(W, orth, torch, world, pg, args, barrier):
         W["params"].copy_(ph, non_blocking=True)
         W["x"].copy_(xh, non_blocking=True)
         run_step(W, orth, torch, world, pg)
-        yh.copy_(W["acts"][-1], non_blocking=True)
+        yh.copy_(res, non_blocking=True)
     t1.record(s)
     barrier()
     ms = t0.elapsed_time(t1) / n
@@ -352,8 +361,9 @@ def e2e_run(W, orth, torch, world, pg, args, barrier):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    return {"value": len(W["acts"]) * world / (ms * 1e-3), "unit": "layers/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": int(ph.numel() * 4 + xh.numel() * 2), "d2h_bytes_per_step": int(yh.numel() * 2)}
+    return {"value": len(W["plan"].layers) * world / (ms * 1e-3), "unit": "layers/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(ph.numel() * 4 + xh.numel() * 2),
+            "d2h_bytes_per_step": int(yh.numel() * yh.element_size())}
 
 
 # ------------------------------------------------------------------ oracle (CPU) legs
@@ -451,6 +461,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--n", type=int, default=2048, help="config 5: matrix size")
+    ap.add_argument("--mats", type=int, default=64, help="config 5: number of n x n matrices")
     ap.add_argument("--compute", default="bf16", choices=["f32", "bf16", "bf16x3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying CUDA graphs")

@@ -93,14 +93,18 @@ def build_workload(orth, torch, cfg_layers, rank, world, device, compute, batch,
     from synth import gen
     plan = orth.Plan(cfg_layers, device, rank=rank, world=world, compute=compute)
     params = np.zeros(plan.params_numel, np.float32)
+    dev = torch.device("cuda", device)
     for i, m in enumerate(plan.matrices):
-        A = gen.param_matrix(m["m"], m["n"], (cfg_id, m["layer"], m["group"], i, gen.ROLE_ID[m["role"]]))
+        key = (cfg_id, m["layer"], m["group"], i, gen.ROLE_ID[m["role"]])
+        if m["m"] * m["n"] > (1 << 21):   # large dense sweep matrices: same recipe, QR on the GPU
+            A = gen.param_matrix_torch(m["m"], m["n"], key, torch, dev).cpu().numpy()
+        else:
+            A = gen.param_matrix(m["m"], m["n"], key)
         params[m["off"]: m["off"] + A.size] = A.ravel()
     cache = np.zeros(plan.cache_numel, np.float32)
     for i, m in enumerate(plan.matrices):
         v = gen.unit_vector(m["n"], (cfg_id, m["layer"], m["group"], i, gen.ROLE_ID["v"]))
         cache[m["cache_off"]: m["cache_off"] + v.size] = v
-    dev = torch.device("cuda", device)
     W = dict(plan=plan, params_h=params, cache_h=cache, chain=chain)
     W["params"] = torch.from_numpy(params).to(dev)
     W["cache"] = torch.from_numpy(cache).to(dev)
@@ -181,7 +185,7 @@ def run_step(W, orth, torch, world, pg, ev=None, graphs=None):
         else:
             apply_layer(W, l)
         rec(f"conv{l}_1")
-    return W["acts"][-1]
+    return W["acts"][-1] if W["acts"] else W["ortho"]
 
 
 def capture_graphs(W, torch):

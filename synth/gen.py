@@ -38,6 +38,23 @@ def param_matrix(m: int, n: int, key: Sequence[int], stress: bool = False) -> np
     return (Q0 + 0.1 * G / np.sqrt(max(m, n))).astype(np.float32)
 
 
+def param_matrix_torch(m: int, n: int, key: Sequence[int], torch, device, stress: bool = False):
+    """Same recipe as param_matrix with the Gaussian drawn by a seeded torch
+    generator and the QR on `device` (large dense-sweep matrices only; not
+    bit-identical to the NumPy draw)."""
+    seed = int(np.random.SeedSequence([int(k) for k in key]).generate_state(1)[0])
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    G = torch.randn((m, n), generator=g, device=device, dtype=torch.float64)
+    if stress:
+        return (G / np.sqrt(n)).float()
+    A = torch.randn((max(m, n), min(m, n)), generator=g, device=device, dtype=torch.float64)
+    Q, R = torch.linalg.qr(A)
+    Q = Q * torch.sign(torch.diagonal(R))[None, :]
+    Q0 = Q if m >= n else Q.T
+    return (Q0 + 0.1 * G / np.sqrt(max(m, n))).float()
+
+
 def unit_vector(n: int, key: Sequence[int]) -> np.ndarray:
     if n == 0:
         return np.zeros(0, np.float32)

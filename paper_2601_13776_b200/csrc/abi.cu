@@ -140,7 +140,7 @@ orth_status_t orth_conv_forward(orth_plan_t plan, int32_t layer, const void* ker
   int Ho = 0, Wo = 0;
   st = check_conv(P, layer, kernel, x, y, N, H, W, io, Ho, Wo);
   if (st != ORTH_OK) return st;
-  const int e = launch_conv_fwd(P.layers[layer], kernel, bias, x, y, N, H, W, Ho, Wo, io, stream);
+  const int e = launch_conv_fwd(P.layers[layer], kernel, P.d_wt_scratch, bias, x, y, N, H, W, Ho, Wo, io, stream);
   P.launches++;
   return cuda_fail(e, "orth_conv_forward");
 }

@@ -291,10 +291,10 @@ ConvArgs make_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo) {
 
 }  // namespace
 
-int launch_conv_fwd(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N, int H,
-                    int W, int Ho, int Wo, int io, void* stream) {
-  if (io == ORTH_BF16 && conv_fwd_tc_eligible(L) && !getenv("ORTH_FORCE_SIMT"))
-    return launch_conv_fwd_tc(L, kernel, bias, x, y, N, H, W, Ho, Wo, stream);
+int launch_conv_fwd(const LayerInfo& L, const void* kernel, void* scratch, const float* bias, const void* x, void* y,
+                    int N, int H, int W, int Ho, int Wo, int io, void* stream) {
+  if (io == ORTH_BF16 && scratch && conv_fwd_tc_eligible(L) && !getenv("ORTH_FORCE_SIMT"))
+    return launch_conv_fwd_tc(L, kernel, scratch, bias, x, y, N, H, W, Ho, Wo, stream);
   const ConvArgs a = make_args(L, N, H, W, Ho, Wo);
   const int64_t M = (int64_t)N * Ho * Wo;
   const int KT = L.ci * L.k * L.k;

@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "orth_internal.h"
@@ -388,17 +389,73 @@ void base_args(TcConvArgs& a, const LayerInfo& L, int N, int H, int W, int Ho, i
 
 }  // namespace
 
+// Group packing: P consecutive groups with few channels (ci_g, co_g < 64) are
+// fused into one "virtual" group with a block-diagonal kernel, so every A row
+// is a full 128-byte (64-channel) SW128 row and the MMA N is P * co_g.  The
+// extra zeros cost P-times the (cheap, here under-used) MMA work but turn the
+// gather of a 32-channel grouped layer from half-empty into dense rows.
+static int pack_factor(const LayerInfo& L, bool bwd) {
+  const int cr = bwd ? L.co : L.ci, nout = bwd ? L.ci : L.co;
+  int P = 1;
+  while (P * 2 <= L.g && L.g % (P * 2) == 0 && cr * P * 2 <= 64) P *= 2;
+  while (P > 1 && ((P * nout) % 32 != 0)) P /= 2;
+  return P;
+}
+
+static LayerInfo packed(const LayerInfo& L, int P) {
+  LayerInfo q = L;
+  q.g = L.g / P; q.ci = L.ci * P; q.co = L.co * P;
+  return q;
+}
+
+namespace {
+// W'[(gp P co + p co + o) k^2 + t][q ci + i] = (p == q) ? W[((gp P + p) co + o) k^2 + t][i] : 0
+__global__ void __launch_bounds__(256) pack_w_kernel(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wp,
+                                                     int gpacks, int P, int co, int ci, int taps) {
+  const int64_t rowlen = (int64_t)P * ci;
+  const int64_t total = (int64_t)gpacks * P * co * taps * rowlen;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (int64_t)gridDim.x * 256) {
+    const int64_t row = e / rowlen;
+    const int col = (int)(e - row * rowlen);
+    const int t = (int)(row % taps);
+    const int64_t ro = row / taps;                 // gp * P * co + p * co + o
+    const int o = (int)(ro % co), p = (int)((ro / co) % P);
+    const int64_t gp = ro / ((int64_t)co * P);
+    const int q = col / ci, i = col - q * ci;
+    wp[e] = (p == q) ? w[(((gp * P + p) * co + o) * taps + t) * ci + i] : __float2bfloat16(0.f);
+  }
+}
+}  // namespace
+
 bool conv_fwd_tc_eligible(const LayerInfo& L) {
-  return L.co % 32 == 0 && L.ci % 8 == 0 && L.ci_f % 8 == 0 && L.co_f % 8 == 0 && L.k * L.k <= MAX_TAPS;
+  const LayerInfo q = packed(L, pack_factor(L, false));
+  return q.co % 32 == 0 && q.ci % 8 == 0 && L.ci_f % 8 == 0 && L.co_f % 8 == 0 && L.k * L.k <= MAX_TAPS &&
+         pack_factor(L, false) <= 8;
 }
 
 bool conv_bwd_tc_eligible(const LayerInfo& L) {
-  return L.ci % 32 == 0 && L.co % 8 == 0 && L.ci_f % 8 == 0 && L.co_f % 8 == 0 && L.k * L.k <= MAX_TAPS &&
-         L.s * L.s <= MAX_PHASES;
+  const LayerInfo q = packed(L, pack_factor(L, true));
+  return q.ci % 32 == 0 && q.co % 8 == 0 && L.ci_f % 8 == 0 && L.co_f % 8 == 0 && L.k * L.k <= MAX_TAPS &&
+         L.s * L.s <= MAX_PHASES && pack_factor(L, true) <= 8;
 }
 
-int launch_conv_fwd_tc(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
-                       int H, int W, int Ho, int Wo, void* stream) {
+static int pack_weights(const LayerInfo& L, int P, const void* kernel, void* dst, cudaStream_t s) {
+  const int taps = L.k * L.k;
+  const int64_t total = (int64_t)L.co_f * taps * P * L.ci;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  pack_w_kernel<<<blocks, 256, 0, s>>>((const __nv_bfloat16*)kernel, (__nv_bfloat16*)dst, L.g / P, P, L.co, L.ci,
+                                       taps);
+  return (int)cudaGetLastError();
+}
+
+int launch_conv_fwd_tc(const LayerInfo& L0, const void* kernel, void* scratch, const float* bias, const void* x,
+                       void* y, int N, int H, int W, int Ho, int Wo, void* stream) {
+  const int P = pack_factor(L0, false);
+  const LayerInfo L = packed(L0, P);
+  if (P > 1) {
+    if (int e = pack_weights(L0, P, kernel, scratch, (cudaStream_t)stream)) return e;
+    kernel = scratch;
+  }
   TcConvArgs a;
   base_args(a, L, N, H, W, Ho, Wo);
   a.transposed = 0;
@@ -412,10 +469,17 @@ int launch_conv_fwd_tc(const LayerInfo& L, const void* kernel, const float* bias
                     (cudaStream_t)stream);
 }
 
-int launch_conv_bwd_tc(const LayerInfo& L, const void* kernel, void* wt_scratch, const float* bias, const void* y,
+int launch_conv_bwd_tc(const LayerInfo& L0, const void* kernel, void* wt_scratch, const float* bias, const void* y,
                        void* x, int N, int H, int W, int Ho, int Wo, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  const int taps = L.k * L.k;
+  const int taps = L0.k * L0.k;
+  const int P = pack_factor(L0, true);
+  const LayerInfo L = packed(L0, P);
+  if (P > 1) {   // block-diagonal pack into the second half of the scratch, then transpose that
+    void* pk = static_cast<__nv_bfloat16*>(wt_scratch) + (int64_t)8 * L0.kernel_numel;
+    if (int e = pack_weights(L0, P, kernel, pk, s)) return e;
+    kernel = pk;
+  }
   dim3 tg((unsigned)((L.ci + 31) / 32), (unsigned)((L.co + 31) / 32), (unsigned)(L.g * taps));
   transpose_w_kernel<<<tg, 256, 0, s>>>((const __nv_bfloat16*)kernel, (__nv_bfloat16*)wt_scratch, L.g, L.co, L.ci,
                                         taps);

@@ -181,7 +181,7 @@ struct Plan {
   EmitItem* d_emit = nullptr;
   int64_t partial_stride = 0;
   int64_t launches = 0;
-  uint16_t* d_wt_scratch = nullptr; // BF16 W^T of one layer for the tensor-core adjoint conv
+  uint16_t* d_wt_scratch = nullptr; // BF16 weight scratch of one layer call: [W^T | packed W], 16 x max kernel
 };
 
 void set_error(const char* fmt, ...);
@@ -208,11 +208,11 @@ int launch_power_finalize(Plan& p, float* v_out, int frob, int write_sigma_only,
 int launch_scale(Plan& p, const float* W, float* X0, void* stream);
 int launch_residual(Plan& p, float* residual_out, void* stream);
 int launch_emit(Plan& p, const float* const bufs[BUF_COUNT], float* kf32, uint16_t* kbf16, void* stream);
-int launch_conv_fwd(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N, int H,
-                    int W, int Ho, int Wo, int io, void* stream);
+int launch_conv_fwd(const LayerInfo& L, const void* kernel, void* scratch, const float* bias, const void* x, void* y,
+                    int N, int H, int W, int Ho, int Wo, int io, void* stream);
 bool conv_fwd_tc_eligible(const LayerInfo& L);
-int launch_conv_fwd_tc(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
-                       int H, int W, int Ho, int Wo, void* stream);
+int launch_conv_fwd_tc(const LayerInfo& L, const void* kernel, void* scratch, const float* bias, const void* x,
+                       void* y, int N, int H, int W, int Ho, int Wo, void* stream);
 int launch_conv_bwd(const LayerInfo& L, const void* kernel, void* wt_scratch, const float* bias, const void* y,
                     void* x, int N, int H, int W, int Ho, int Wo, int io, void* stream);
 bool conv_bwd_tc_eligible(const LayerInfo& L);

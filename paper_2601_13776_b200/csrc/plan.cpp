@@ -506,7 +506,7 @@ static orth_status_t allocate(Plan& P) {
   const size_t o_bx = take((size_t)8 * std::max<int64_t>(P.bx_numel, 64) * 2);
   int64_t max_kernel = 64;
   for (auto& L : P.layers) max_kernel = std::max(max_kernel, L.kernel_numel);
-  const size_t o_wt = take((size_t)max_kernel * 2);
+  const size_t o_wt = take((size_t)16 * max_kernel * 2);   // W^T (<= 8x with packing) + packed W (<= 8x)
   const size_t o_br = take((size_t)2 * std::max<int64_t>(P.br_numel, 64) * 2);
   std::vector<GemmPhase*> phases = {&P.gram[0], &P.gram[1], &P.update[0], &P.update[1], &P.gram_r[0],
                                     &P.gram_r[1], &P.update_r[0], &P.update_r[1], &P.proj, &P.aoc};

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "orth_internal.h"
 
@@ -94,13 +95,28 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
     auto up = [&](int t) { return mode == ORTH_BF16X3 ? 3 : 1; };
     auto x_lo = [&](int t) { return t >= T || gp(t) == 3 || up(t) == 3; };   // t == T: the residual Gram
     if (!e) e = launch_scale_bf16(P, params, x0, par, x_lo(0), stream);
+    static const bool phased = std::getenv("ORTH_NS_PHASED") != nullptr;   // A/B switch: per-phase kernels
+    if (!e && P.nsp_ctas > 0 && 2 * T + 1 <= kNspMaxPhases && !phased) {
+      // all 2T (+1 residual Gram) phases in one persistent cooperative launch
+      uint8_t fl[kNspMaxPhases];
+      int n = 0;
+      for (int t = 0; t < T; ++t) {
+        fl[n++] = (uint8_t)(1 | (gp(t) == 3 ? 2 : 0) | (par << 2) | (up(t) == 3 ? 8 : 0));
+        fl[n++] = (uint8_t)((up(t) == 3 ? 2 : 0) | (par << 2) | (x_lo(t + 1) ? 8 : 0) | 16);
+        par ^= 1;
+      }
+      if (residual_out) fl[n++] = (uint8_t)(1 | 2 | (par << 2) | 16);
+      e = launch_ns_persist(P, bufs, fl, n, stream);
+      if (!e && residual_out) e = launch_residual_r(P, residual_out, stream);
+      return cuda_fail(e, "orth_orthogonalize");
+    }
     for (int t = 0; t < T && !e; ++t) {
-      e = launch_ns_tc(P, bufs, par, true, gp(t), up(t) == 3, stream);
-      if (!e) e = launch_ns_tc(P, bufs, par, false, up(t), x_lo(t + 1), stream);
+      e = launch_ns_tc(P, bufs, par, true, gp(t), up(t) == 3, false, stream);
+      if (!e) e = launch_ns_tc(P, bufs, par, false, up(t), x_lo(t + 1), true, stream);
       par ^= 1;
     }
     if (!e && residual_out) {
-      e = launch_ns_tc(P, bufs, 0, true, 3, false, stream);
+      e = launch_ns_tc(P, bufs, 0, true, 3, false, true, stream);
       if (!e) e = launch_residual_r(P, residual_out, stream);
     }
   }

@@ -1,0 +1,765 @@
+// Persistent tensor-core Bjorck / Newton-Schulz (a3; residual form
+// R16): ALL T iterations of all matrices in ONE cooperative launch.
+//
+// Why: the per-phase kernels (ns_tc.cu) pay a launch, a TMEM allocation, a
+// barrier setup and a cold pipeline for every one of the 2T phases, and a
+// phase waits for the slowest tile of ANY matrix.  Here every matrix (or a
+// bundle of small matrices) belongs to a GROUP of G co-resident CTAs that
+// runs its 2T phases on its own, synchronising only its own CTAs between
+// phases (a global-memory barrier; nothing when G = 1).  Groups never wait
+// for each other.  Host-side partition: plan.cpp/build_ns_persist (cost
+// model + LPT).
+//
+// CTA roles (192 threads, one CTA per SM, 210 KB smem):
+//   warp 0  TMA producer: 128x64 BF16 operand tiles (K-major rows of X / R,
+//           or MN-major columns of row-major X) into a 6-slot ring of 32 KB
+//           slots (a 1-pass k-block takes one slot, a 3-pass hi/lo k-block two)
+//   warp 1  TMEM allocation + the single-thread tcgen05.mma issuer, FP32
+//           accumulators double-buffered in TMEM (2 x 128 columns)
+//   warps 2-5  epilogue: TMEM -> registers -> per-warp smem transpose ->
+//           coalesced FP32 / BF16 row stores (Gram: R = I - acc; update:
+//           X' = C + beta acc), overlapping the next tile's mainloop.
+// Phase hand-off: epilogue writes -> proxy fence -> group barrier -> a
+// monotonic smem counter that releases the producer into the next phase.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <tuple>
+#include <numeric>
+#include <vector>
+
+#include "orth_internal.h"
+#include "umma.cuh"
+#include "tma_host.h"
+
+// Device-side tracing (per-phase / per-tile globaltimer stamps) is compiled in
+// only with -DORTH_NSP_TRACE (diagnostics builds: ORTH_NVCC_FLAGS=-DORTH_NSP_TRACE).
+#ifdef ORTH_NSP_TRACE
+#define NSP_TRACE(x) x
+#else
+#define NSP_TRACE(x)
+#endif
+
+namespace orth {
+
+struct NspBufs {
+  float* X[2];
+  float* R;
+  __nv_bfloat16 *xh[2], *xl[2], *rh, *rl;
+};
+
+struct NspPhases {
+  uint8_t f[kNspMaxPhases];   // bit0 gram, bit1 3-pass, bit2 parity of X read, bit3 write lo, bit4 write fp32 R
+  int32_t n;
+  unsigned long long* trace;  // diagnostics (ORTH_NS_TRACE): per CTA, globaltimer at start and at each phase end
+  unsigned long long* ttrace; // diagnostics: per tile {slot counter, then 4 words per record}
+};
+
+namespace {
+
+constexpr int kThreads = 320;    // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+constexpr int kSlot = 32768;
+constexpr int kSlots = 4;
+constexpr int kEpiWarps = 8;
+// per epilogue warp: the accumulator chunk Sw (32 x 32 fp32) and the C tile of
+// both chunks Sc[2] (32 x 32 fp32 each), float4 slots XOR-swizzled by row
+constexpr int kStageFloats = kEpiWarps * 3 * 32 * 32;
+constexpr size_t kSmem = 1024 + (size_t)kSlots * kSlot + (size_t)kStageFloats * 4;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <class T>
+__device__ __forceinline__ T pick(T const (&a)[2], int i) { return i ? a[1] : a[0]; }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {   // low half = a
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta_shared(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(umma::smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_shared(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.s32 [%0], %1;" ::"r"(umma::smem_u32(p)), "r"(v) : "memory");
+}
+
+// Group barrier over G co-resident CTAs: a monotonic arrival counter per
+// group (zeroed by the scale kernel that precedes every launch); barrier k
+// completes when the counter reaches k * G.  One release-reduction per CTA,
+// acquire polls (measured 1.2 us for 148 CTAs vs 2.7 us for count+generation).
+__device__ __forceinline__ void group_sync(unsigned* bar, unsigned target) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+  unsigned v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+  } while (v < target);
+}
+
+__device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int k0, int mn0,
+                                             int mn_major) {
+  if (mn_major) {   // columns of row-major X: two 64 (MN) x 64 (K) boxes
+    umma::tma_load_2d(dst, map, bar, mn0, k0);
+    umma::tma_load_2d(dst + 8192, map, bar, mn0 + 64, k0);
+  } else {          // rows: one 64 (K) x 128 box
+    umma::tma_load_2d(dst, map, bar, k0, mn0);
+  }
+}
+__device__ __forceinline__ uint64_t op_desc(uint32_t base, int q, int mn_major) {
+  return mn_major ? umma::sdesc_sw128_mn(base + 2048 * q, 8192) : umma::sdesc_sw128(base + 32 * q);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    ns_persist_kernel(const NsDesc* __restrict__ dg, const NsDesc* __restrict__ du, const NsTile* __restrict__ tiles,
+                      const NsGroup* __restrict__ ctas, unsigned* bars,
+                      NspBufs bufs, const CUtensorMap* __restrict__ maps, const __grid_constant__ NspPhases ph) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* stage = reinterpret_cast<float*>(smem + kSlots * kSlot);
+  __shared__ uint64_t full_bar[kSlots], empty_bar[kSlots], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int phase_done;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // this CTA's ranges live in shared memory and are re-read where used (keeps
+  // them out of the register budget: 10 warps cap the kernel at 168 registers)
+  __shared__ NsGroup grp_sh;
+  __shared__ __align__(16) uint32_t desc_sh[kEpiWarps][32];
+  if (tid == 0) grp_sh = ctas[blockIdx.x];
+  const volatile NsGroup& grp = grp_sh;
+
+  if (tid == 0) {
+    for (int i = 0; i < kSlots; ++i) {
+      umma::mbar_init(&full_bar[i], 1);
+      umma::mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      umma::mbar_init(&tfull_bar[i], 1);
+      umma::mbar_init(&tempty_bar[i], kEpiWarps);
+    }
+    phase_done = 0;
+    umma::fence_mbar_init();
+  }
+  if (warp == 1) umma::tmem_alloc(&tmem_base_sh, 256);
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t ring = umma::smem_u32(smem);
+  NSP_TRACE(if (ph.trace && tid == 0) {
+    const unsigned long long t = gtimer();
+    ph.trace[(size_t)blockIdx.x * (4 * ph.n + 1)] = t;
+    for (int q = 0; q < 4 * ph.n; ++q) ph.trace[(size_t)blockIdx.x * (4 * ph.n + 1) + 1 + q] = t;
+  })
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      uint32_t used = 0, epar = 0;
+      int cnt = 0;
+      for (int p = 0; p < ph.n; ++p) {
+        const int f = ph.f[p], gram = f & 1, split = (f >> 1) & 1, par = (f >> 2) & 1;
+        if (p > 0)
+          while (ld_acquire_cta_shared(&phase_done) < p) __nanosleep(20);
+        fence_proxy_async_global();   // order the group's generic writes before these async-proxy reads
+        NSP_TRACE(if (ph.trace) ph.trace[(size_t)blockIdx.x * (4 * ph.n + 1) + 1 + 4 * p + 0] = gtimer());
+        const NsDesc* D = gram ? dg : du;
+        const int tb = gram ? grp.g_begin : grp.u_begin, te = gram ? grp.g_end : grp.u_end;
+        const int w = split ? 2 : 1;
+        for (int t = tb; t < te; ++t) {
+          const NsTile tl = tiles[t];
+          const NsDesc d = D[tl.desc];
+          const int m0 = (tl.local / d.tiles_n) * 128, n0 = (tl.local % d.tiles_n) * 128;
+          const int nk = (d.K + 63) / 64, a_mn = d.a_kind == 1, b_mn = d.b_kind == 1;
+          const bool sym = gram && m0 == n0;   // diagonal Gram tile: B == A, loaded once
+          const CUtensorMap* ma = maps + d.map_a + 2 * par;
+          const CUtensorMap* mb = maps + d.map_b + 2 * par;
+          for (int kb = 0; kb < nk; ++kb) {
+            if (w == 2 && cnt % kSlots == kSlots - 1) ++cnt;   // a hi/lo stage takes two adjacent slots
+            const int s = cnt % kSlots;
+            for (int q = s; q < s + w; ++q) {
+              if ((used >> q) & 1u) {
+                umma::mbar_wait(&empty_bar[q], (epar >> q) & 1u);
+                epar ^= 1u << q;
+              }
+              used |= 1u << q;
+            }
+            const uint32_t sa = ring + s * kSlot;
+            umma::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(sym ? w * kSlot / 2 : w * kSlot));
+            load_operand(sa, ma, &full_bar[s], kb * 64, m0, a_mn);
+            if (!sym) load_operand(sa + 16384, mb, &full_bar[s], kb * 64, n0, b_mn);
+            if (split) {
+              load_operand(sa + 32768, ma + 1, &full_bar[s], kb * 64, m0, a_mn);
+              if (!sym) load_operand(sa + 49152, mb + 1, &full_bar[s], kb * 64, n0, b_mn);
+            }
+            cnt += w;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      uint32_t fpar = 0;
+      int cnt = 0, acc = 0;
+      for (int p = 0; p < ph.n; ++p) {
+        const int f = ph.f[p], gram = f & 1, split = (f >> 1) & 1;
+        const NsDesc* D = gram ? dg : du;
+        const int tb = gram ? grp.g_begin : grp.u_begin, te = gram ? grp.g_end : grp.u_end;
+        const int w = split ? 2 : 1;
+        for (int t = tb; t < te; ++t) {
+          const NsTile tl = tiles[t];
+          const NsDesc* dp = D + tl.desc;
+          const int nk = (__ldg(&dp->K) + 63) / 64, a_mn = __ldg(&dp->a_kind) == 1, b_mn = __ldg(&dp->b_kind) == 1;
+          const int tn = __ldg(&dp->tiles_n);
+          const bool sym = gram && (tl.local / tn) == (tl.local % tn);
+          const uint32_t idesc = umma::idesc_bf16(128, 128) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
+          const int buf = acc & 1;
+          if (acc >= 2) umma::mbar_wait(&tempty_bar[buf], ((acc >> 1) - 1) & 1);
+          umma::tc_fence_after();
+          const uint32_t dt = tmem + buf * 128;
+          for (int kb = 0; kb < nk; ++kb) {
+            if (w == 2 && cnt % kSlots == kSlots - 1) ++cnt;
+            const int s = cnt % kSlots;
+            umma::mbar_wait(&full_bar[s], (fpar >> s) & 1u);
+            fpar ^= 1u << s;
+            umma::tc_fence_after();
+            const uint32_t ah = ring + s * kSlot, al = ah + 32768;
+            const uint32_t bh = sym ? ah : ah + 16384, bl = sym ? al : ah + 49152;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint64_t dah = op_desc(ah, q, a_mn), dbh = op_desc(bh, q, b_mn);
+              umma::mma_bf16(dt, dah, dbh, idesc, (kb | q) != 0);
+              if (split) {
+                umma::mma_bf16(dt, dah, op_desc(bl, q, b_mn), idesc, 1);
+                umma::mma_bf16(dt, op_desc(al, q, a_mn), dbh, idesc, 1);
+              }
+            }
+            umma::mma_commit(&empty_bar[s]);
+            if (w == 2) umma::mma_commit(&empty_bar[s + 1]);
+            cnt += w;
+          }
+          umma::mma_commit(&tfull_bar[buf]);
+          ++acc;
+        }
+      }
+    }
+  } else {
+    // -------------------------------------------------------------- epilogue
+    // 8 warps: warp w reads TMEM lanes 32*(w%4) (rows row0..row0+31) and the
+    // 64-column half ch of the accumulator, in two 32-column chunks.  The C
+    // tile of both chunks is prefetched into smem with cp.async before the
+    // accumulator is ready.  Chunk: tcgen05.ld (thread = row) -> float4 rows
+    // into a swizzled 32x32 smem tile -> row pass with 8 lanes per row (float4
+    // C from smem, float4 FP32 stores, 8-byte BF16 stores), 4 rows per step.
+    // Nothing tile-sized lives in registers (10 warps cap the kernel at 168).
+    const int ew = warp - 2, row0 = (warp & 3) * 32, ch = ew >> 2;
+    float* Sw = stage + ew * 3 * 1024;
+    float* Sc = Sw + 1024;
+    const int rsub = lane >> 3, q4 = lane & 7, c4 = q4 * 4;
+    int acc = 0;
+    for (int p = 0; p < ph.n; ++p) {
+      const int f = ph.f[p], gram = f & 1, par = (f >> 2) & 1, write_lo = (f >> 3) & 1, write_f = (f >> 4) & 1;
+      const NsDesc* D = gram ? dg : du;
+      const int tb = gram ? grp.g_begin : grp.u_begin, te = gram ? grp.g_end : grp.u_end;
+      for (int t = tb; t < te; ++t) {
+        const NsTile tl = tiles[t];
+        // this tile's descriptor -> a per-warp smem copy (one word per lane), so the
+        // fields cost an LDS, not an L2 round trip, wherever they are used below
+        {
+          static_assert(sizeof(NsDesc) <= 32 * 4, "NsDesc must fit one word per lane");
+          const uint32_t* srcw = reinterpret_cast<const uint32_t*>(D + tl.desc);
+          if (lane < (int)(sizeof(NsDesc) / 4)) desc_sh[ew][lane] = __ldg(srcw + lane);
+          __syncwarp();
+        }
+        const NsDesc* dp = reinterpret_cast<const NsDesc*>(desc_sh[ew]);
+        const int tiles_n = dp->tiles_n;
+        const int m0 = (tl.local / tiles_n) * 128 + row0, n0 = (tl.local % tiles_n) * 128 + ch * 64;
+        const bool upd = (dp->epi) == 1;
+        const int64_t f_off = (dp->f_off), ldf = (dp->ldf);
+        const int M = (dp->M), N = (dp->N);
+        const int buf = acc & 1;
+        if (upd) {   // C = X (fp32) rows m0.., cols n0..n0+63 -> Sc[0..1]
+          const float* Cm = pick(bufs.X, par) + f_off;
+          const bool fv4 = (ldf & 3) == 0;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int e = lane + 32 * k, r = e >> 3, q = e & 7;
+              const int i = m0 + r, j = n0 + c * 32 + 4 * q;
+              float* dst = Sc + c * 1024 + r * 32 + 4 * (q ^ (r & 7));
+              const float* src = Cm + (int64_t)i * ldf + j;
+              if (fv4 && (j + 3 < N || j >= N)) {
+                umma::cp_async16(umma::smem_u32(dst), i < M && j < N ? src : Cm, i < M && j < N);
+              } else {   // ragged / unaligned: synchronous scalar path
+#pragma unroll
+                for (int u = 0; u < 4; ++u) dst[u] = (i < M && j + u < N) ? __ldcg(src + u) : 0.f;
+              }
+            }
+            umma::cp_async_commit();
+          }
+        }
+        NSP_TRACE(const unsigned long long t_start = ph.ttrace ? gtimer() : 0ull);
+        umma::mbar_wait(&tfull_bar[buf], (acc >> 1) & 1);
+        umma::tc_fence_after();
+        NSP_TRACE(const unsigned long long t_full = ph.ttrace ? gtimer() : 0ull);
+        NSP_TRACE(if (ph.trace && ew == 0 && lane == 0 && t == tb) ph.trace[(size_t)blockIdx.x * (4 * ph.n + 1) + 1 + 4 * p + 1] = gtimer());
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            float v[16];
+            umma::tmem_ld16(tmem + buf * 128 + ch * 64 + c * 32 + hh * 16 + ((uint32_t)row0 << 16), v);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              *reinterpret_cast<float4*>(Sw + lane * 32 + 4 * ((hh * 4 + k) ^ (lane & 7))) =
+                  make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+          }
+          if (c == 1) {   // accumulator drained: hand the TMEM buffer back to the MMA warp
+            umma::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) umma::mbar_arrive(&tempty_bar[buf]);
+          }
+          if (upd) {
+            if (c == 0) umma::cp_async_wait<1>();
+            else umma::cp_async_wait<0>();
+          }
+          __syncwarp();
+          // per-chunk constants re-derived here (cheap) instead of being held in registers
+          const bool wf = upd || write_f;
+          const int ldb16 = upd ? (dp->ldx) : (dp->ldr);
+          const int64_t b_off = upd ? (dp->bx_off) : (dp->br_off);
+          __nv_bfloat16* oh = (upd ? pick(bufs.xh, par ^ 1) : bufs.rh) + b_off;
+          __nv_bfloat16* ol = (upd ? pick(bufs.xl, par ^ 1) : bufs.rl) + b_off;
+          float* F = (upd ? pick(bufs.X, par ^ 1) : bufs.R) + f_off;
+          const bool fv4 = (ldf & 3) == 0;
+          const float alpha = (dp->alpha), beta = (dp->beta), diag = (dp->diag);
+          const float* Scc = Sc + c * 1024;
+#pragma unroll 4
+          for (int it = 0; it < 8; ++it) {
+            const int rr = 4 * it + rsub;
+            const int i = m0 + rr, j = n0 + c * 32 + c4;
+            if (i < M) {
+              const int sw = 4 * (q4 ^ (rr & 7));
+              const float4 a = *reinterpret_cast<const float4*>(Sw + rr * 32 + sw);
+              const float4 cv = upd ? *reinterpret_cast<const float4*>(Scc + rr * 32 + sw) : make_float4(0.f, 0.f, 0.f, 0.f);
+              float o0 = fmaf(alpha, a.x, beta * cv.x), o1 = fmaf(alpha, a.y, beta * cv.y);
+              float o2 = fmaf(alpha, a.z, beta * cv.z), o3 = fmaf(alpha, a.w, beta * cv.w);
+              const int dd = i - j;   // diagonal element inside this 4-group
+              if (dd == 0) o0 += diag;
+              if (dd == 1) o1 += diag;
+              if (dd == 2) o2 += diag;
+              if (dd == 3) o3 += diag;
+              if (j + 3 >= N) {       // ragged right edge: zero beyond N (keeps BF16 padding zero)
+                if (j >= N) o0 = 0.f;
+                if (j + 1 >= N) o1 = 0.f;
+                if (j + 2 >= N) o2 = 0.f;
+                o3 = 0.f;
+              }
+              if (wf && j < N) {
+                float* dst = F + (int64_t)i * ldf + j;
+                if (fv4 && j + 3 < N) {
+                  *reinterpret_cast<float4*>(dst) = make_float4(o0, o1, o2, o3);
+                } else {
+                  dst[0] = o0;
+                  if (j + 1 < N) dst[1] = o1;
+                  if (j + 2 < N) dst[2] = o2;
+                  if (j + 3 < N) dst[3] = o3;
+                }
+              }
+              if (j < ldb16) {   // ldb16 % 8 == 0, j % 4 == 0: the 4-group lies inside the padded row
+                const uint32_t h01 = pack_bf16(o0, o1), h23 = pack_bf16(o2, o3);
+                const int64_t bo = (int64_t)i * ldb16 + j;
+                *reinterpret_cast<uint2*>(oh + bo) = make_uint2(h01, h23);
+                if (write_lo) {
+                  const uint32_t l01 = pack_bf16(o0 - __uint_as_float(h01 << 16), o1 - __uint_as_float(h01 & 0xFFFF0000u));
+                  const uint32_t l23 = pack_bf16(o2 - __uint_as_float(h23 << 16), o3 - __uint_as_float(h23 & 0xFFFF0000u));
+                  *reinterpret_cast<uint2*>(ol + bo) = make_uint2(l01, l23);
+                }
+              }
+            }
+          }
+          if (gram && m0 - row0 < n0 - ch * 64) {
+            // upper-triangle Gram tile: also write its mirror R[j][i] = R[i][j] (alpha * acc; no diagonal here)
+#pragma unroll 2
+            for (int it = 0; it < 8; ++it) {
+              const int rt = 4 * it + rsub;                           // column of the chunk = row of the mirror
+              const int jg = n0 + c * 32 + rt, ig = m0 + c4;
+              if (jg < N && ig < ldb16) {
+                float o[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const int r = c4 + k;
+                  o[k] = ig + k < M ? alpha * Sw[r * 32 + 4 * ((rt >> 2) ^ (r & 7)) + (rt & 3)] : 0.f;
+                }
+                if (wf) {
+                  float* dst = F + (int64_t)jg * ldf + ig;
+                  if (fv4 && ig + 3 < M) {
+                    *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+                  } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                      if (ig + k < M) dst[k] = o[k];
+                  }
+                }
+                const uint32_t h01 = pack_bf16(o[0], o[1]), h23 = pack_bf16(o[2], o[3]);
+                const int64_t bo = (int64_t)jg * ldb16 + ig;
+                *reinterpret_cast<uint2*>(oh + bo) = make_uint2(h01, h23);
+                if (write_lo) {
+                  const uint32_t l01 = pack_bf16(o[0] - __uint_as_float(h01 << 16), o[1] - __uint_as_float(h01 & 0xFFFF0000u));
+                  const uint32_t l23 = pack_bf16(o[2] - __uint_as_float(h23 << 16), o[3] - __uint_as_float(h23 & 0xFFFF0000u));
+                  *reinterpret_cast<uint2*>(ol + bo) = make_uint2(l01, l23);
+                }
+              }
+            }
+          }
+          __syncwarp();
+        }
+#ifdef ORTH_NSP_TRACE
+        if (ph.ttrace && lane == 0) {
+          const unsigned long long t_end = gtimer();
+          const unsigned long long slot = atomicAdd(ph.ttrace, 1ull);
+          if (slot < 65536) {
+            unsigned long long* r = ph.ttrace + 1 + 4 * slot;
+            r[0] = ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)p << 40) | ((unsigned long long)ew << 36) |
+                   ((unsigned long long)tl.desc << 16) | (unsigned long long)tl.local;
+            r[1] = t_start;
+            r[2] = t_full;
+            r[3] = t_end;
+          }
+        }
+#endif
+        ++acc;
+      }
+      // ---- phase end: publish this CTA's writes, sync the group, release the producer
+      NSP_TRACE(if (ph.trace && ew == 0 && lane == 0) ph.trace[(size_t)blockIdx.x * (4 * ph.n + 1) + 1 + 4 * p + 2] = gtimer());
+      fence_proxy_async_global();
+      umma::named_bar_sync(1, 32 * kEpiWarps);
+      if (ew == 0 && lane == 0) {
+        if (grp.G > 1) group_sync(bars + grp.gid, (unsigned)(p + 1) * (unsigned)grp.G);
+        st_release_cta_shared(&phase_done, p + 1);
+        NSP_TRACE(if (ph.trace) ph.trace[(size_t)blockIdx.x * (4 * ph.n + 1) + 1 + 4 * p + 3] = gtimer());
+      }
+    }
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) umma::tmem_dealloc(tmem, 256);
+}
+
+// ---------------------------------------------------------------- host: partition
+struct MatCost {
+  int idx, gt, ut, nkg, nku;
+};
+
+// estimated microseconds of one NS iteration of matrix costs with G CTAs
+double iter_cost(const MatCost& c, int G) {
+  const double ckb = 0.2, ceg = 0.7, ceu = 1.0, cbar = 1.5, cloc = 0.3;
+  return std::ceil((double)c.gt / G) * (c.nkg * ckb + ceg) + std::ceil((double)c.ut / G) * (c.nku * ckb + ceu) +
+         (G > 1 ? 2 * cbar : 2 * cloc);
+}
+
+}  // namespace
+
+orth_status_t build_ns_persist(Plan& p) {
+  if (p.ns_gram.empty()) return ORTH_OK;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int coop = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (cudaFuncSetAttribute(ns_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess) {
+    cudaGetLastError();
+    return ORTH_OK;   // stays on the per-phase kernels
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns_persist_kernel, kThreads, kSmem);
+  if (!coop || occ < 1 || sms < 1) return ORTH_OK;
+  const int ctas = sms;   // one CTA per SM (smem-limited), all co-resident under the cooperative launch
+
+  std::vector<MatCost> mc;
+  for (size_t i = 0; i < p.ns_gram.size(); ++i) {
+    const NsDesc& g = p.ns_gram[i];
+    const NsDesc& u = p.ns_upd[i];
+    // Gram: upper-triangle tiles only (R symmetric; the epilogue mirrors off-diagonal tiles)
+    mc.push_back({(int)i, g.tiles_n * (g.tiles_n + 1) / 2, ((u.M + 127) / 128) * u.tiles_n, (g.K + 63) / 64,
+                  (u.K + 63) / 64});
+  }
+  // (a) one group of all matrices over all CTAs
+  double ga = 0, ua = 0, gmax = 0, umax = 0;
+  for (auto& c : mc) {
+    ga += c.gt * (c.nkg * 0.2 + 0.7);
+    ua += c.ut * (c.nku * 0.2 + 1.0);
+    gmax = std::max(gmax, c.nkg * 0.2 + 0.7);
+    umax = std::max(umax, c.nku * 0.2 + 1.0);
+  }
+  const double cost_a = std::max(ga / ctas, gmax) + std::max(ua / ctas, umax) + 3.0;
+  // (b) large matrices get dedicated CTAs, small ones are LPT-packed into single-CTA bins
+  std::vector<int> order(mc.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return iter_cost(mc[a], 1) > iter_cost(mc[b], 1); });
+  double total = 0;
+  for (auto& c : mc) total += iter_cost(c, 1);
+  std::vector<int> Gi(mc.size(), 0);
+  double tstar = total / ctas;
+  int used = 0;
+  std::vector<int> small;
+  for (int o : order) {
+    const double c1 = iter_cost(mc[o], 1);
+    if (c1 > tstar) {
+      int G = (int)std::ceil(c1 / tstar);
+      G = std::max(1, std::min(G, std::max(mc[o].gt, mc[o].ut)));
+      Gi[o] = G;
+      used += G;
+    } else {
+      small.push_back(o);
+    }
+  }
+  const int need_small = small.empty() ? 0 : 1;
+  while (used > ctas - need_small) {   // shrink the group that loses least
+    int best = -1;
+    double bc = 1e30;
+    for (size_t i = 0; i < mc.size(); ++i)
+      if (Gi[i] > 1) {
+        const double c = iter_cost(mc[i], Gi[i] - 1);
+        if (c < bc) { bc = c; best = (int)i; }
+      }
+    if (best < 0) break;
+    --Gi[best];
+    --used;
+  }
+  bool ok_b = used <= ctas - need_small;
+  int bins = ctas - used;
+  std::vector<std::vector<int>> bin_mats;
+  double cost_b = 0;
+  if (ok_b) {
+    for (size_t i = 0; i < mc.size(); ++i)
+      if (Gi[i] > 0) cost_b = std::max(cost_b, iter_cost(mc[i], Gi[i]));
+    if (!small.empty()) {
+      bins = std::min<int>(bins, (int)small.size());
+      bin_mats.assign(bins, {});
+      std::vector<double> load(bins, 0.0);
+      for (int o : small) {   // LPT (small is sorted by decreasing cost)
+        const int b = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        load[b] += iter_cost(mc[o], 1) - (bin_mats[b].empty() ? 0.0 : 0.6);
+        bin_mats[b].push_back(o);
+      }
+      cost_b = std::max(cost_b, *std::max_element(load.begin(), load.end()));
+    }
+  }
+  // materialise groups
+  struct Grp { std::vector<int> mats; int G; };
+  std::vector<Grp> gs;
+  const char* force = std::getenv("ORTH_NSP_PARTITION");   // diagnostics: "global" | "groups"
+  const bool use_a = !ok_b || cost_a <= cost_b || (force && !std::strcmp(force, "global"));
+  if (use_a && !(force && !std::strcmp(force, "groups") && ok_b)) {
+    Grp g;
+    for (size_t i = 0; i < mc.size(); ++i) g.mats.push_back((int)i);
+    g.G = ctas;
+    gs.push_back(g);
+    p.nsp_est_us = cost_a;
+  } else {
+    for (size_t i = 0; i < mc.size(); ++i)
+      if (Gi[i] > 0) gs.push_back({{(int)i}, Gi[i]});
+    for (auto& b : bin_mats) gs.push_back({b, 1});
+    p.nsp_est_us = cost_b;
+  }
+  // per-CTA tile lists: LPT inside each group (tile cost: k-blocks + epilogue;
+  // diagonal Gram tiles load one operand, off-diagonal ones also write the mirror)
+  auto gram_cost = [&](int m, int l) {
+    const int tn = p.ns_gram[mc[m].idx].tiles_n;
+    const bool diag = l / tn == l % tn;
+    return mc[m].nkg * 0.3 * (diag ? 0.5 : 1.0) + (diag ? 0.8 : 1.6);
+  };
+  auto upd_cost = [&](int m) { return mc[m].nku * 0.3 + 2.0; };
+  std::vector<NsTile> tg, tu;
+  std::vector<NsGroup> ctas_v;
+  int cta = 0;
+  for (size_t gi = 0; gi < gs.size(); ++gi) {
+    const int G = gs[gi].G;
+    struct Item { double c; NsTile t; };
+    std::vector<Item> gi_items, ui_items;
+    for (int m : gs[gi].mats) {
+      const int tn = p.ns_gram[mc[m].idx].tiles_n;
+      for (int l = 0; l < tn * tn; ++l)
+        if (l / tn <= l % tn) gi_items.push_back({gram_cost(m, l), {mc[m].idx, l}});
+      for (int l = 0; l < mc[m].ut; ++l) ui_items.push_back({upd_cost(m), {mc[m].idx, l}});
+    }
+    auto lpt = [&](std::vector<Item>& items) {
+      std::stable_sort(items.begin(), items.end(), [](const Item& a, const Item& b) { return a.c > b.c; });
+      std::vector<std::vector<NsTile>> bins(G);
+      std::vector<double> load(G, 0.0);
+      for (auto& it : items) {
+        const int b = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        load[b] += it.c;
+        bins[b].push_back(it.t);
+      }
+      return bins;
+    };
+    auto gb = lpt(gi_items), ub = lpt(ui_items);
+    for (int c = 0; c < G; ++c) {
+      NsGroup e{};
+      e.gid = (int32_t)gi;
+      e.G = G;
+      e.g_begin = (int)tg.size();
+      tg.insert(tg.end(), gb[c].begin(), gb[c].end());
+      e.g_end = (int)tg.size();
+      e.u_begin = (int)tu.size();
+      tu.insert(tu.end(), ub[c].begin(), ub[c].end());
+      e.u_end = (int)tu.size();
+      ctas_v.push_back(e);
+    }
+    cta += G;
+  }
+  // a single NsTile array: gram tiles then update tiles (update ranges shifted)
+  const int off_u = (int)tg.size();
+  for (auto& e : ctas_v) { e.u_begin += off_u; e.u_end += off_u; }
+  tg.insert(tg.end(), tu.begin(), tu.end());
+  const size_t b_tiles = tg.size() * sizeof(NsTile), b_ctas = ctas_v.size() * sizeof(NsGroup);
+  const size_t b_bars = gs.size() * sizeof(unsigned);
+  const size_t total_b = b_tiles + b_ctas + b_bars + 64;
+  char* mem = nullptr;
+  cudaError_t e = cudaMalloc(&mem, total_b);
+  if (e != cudaSuccess) {
+    set_error("NS persistent tables: %s", cudaGetErrorString(e));
+    return ORTH_ERR_OUT_OF_MEMORY;
+  }
+  p.nsp_mem = mem;
+  p.nsp_tiles = reinterpret_cast<NsTile*>(mem);
+  p.nsp_groups = reinterpret_cast<NsGroup*>(mem + b_tiles);
+  p.nsp_bars = reinterpret_cast<unsigned*>(mem + ((b_tiles + b_ctas + 15) & ~size_t(15)));
+  e = cudaMemcpy(p.nsp_tiles, tg.data(), b_tiles, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(p.nsp_groups, ctas_v.data(), b_ctas, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(p.nsp_bars, 0, b_bars);
+  if (e != cudaSuccess) {
+    set_error("NS persistent tables upload: %s", cudaGetErrorString(e));
+    return ORTH_ERR_CUDA;
+  }
+  p.nsp_groups_n = (int)gs.size();
+  p.nsp_ctas = cta;
+  return ORTH_OK;
+}
+
+int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flags, int nphases, void* stream) {
+  NspBufs b;
+  b.X[0] = bufs[BUF_X];
+  b.X[1] = bufs[BUF_Y];
+  b.R = bufs[BUF_G];
+  auto bx = reinterpret_cast<__nv_bfloat16*>(p.d_bx);
+  const int64_t nx = p.bx_numel > 64 ? p.bx_numel : 64;
+  for (int k = 0; k < 2; ++k) {
+    b.xh[k] = bx + (0 + k) * nx;
+    b.xl[k] = bx + (2 + k) * nx;
+  }
+  auto br = reinterpret_cast<__nv_bfloat16*>(p.d_br);
+  b.rh = br;
+  b.rl = br + (p.br_numel > 64 ? p.br_numel : 64);
+  NspPhases ph;
+  std::memset(&ph, 0, sizeof(ph));
+  ph.n = nphases;
+  std::memcpy(ph.f, flags, (size_t)nphases);
+#ifdef ORTH_NSP_TRACE
+  static const bool tracing = std::getenv("ORTH_NS_TRACE") != nullptr;
+#else
+  constexpr bool tracing = false;
+#endif
+  static unsigned long long* trace = nullptr;
+  static unsigned long long* ttrace = nullptr;
+  if (tracing) {
+    if (!trace) cudaMalloc(&trace, (size_t)p.nsp_ctas * (4 * kNspMaxPhases + 1) * 8);
+    if (!ttrace) cudaMalloc(&ttrace, (1 + 4 * 65536) * 8);
+    cudaMemsetAsync(ttrace, 0, 8, (cudaStream_t)stream);
+    ph.trace = trace;
+    ph.ttrace = ttrace;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p.nsp_ctas);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  p.launches++;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, ns_persist_kernel, (const NsDesc*)p.d_ns_gram,
+                                           (const NsDesc*)p.d_ns_upd, (const NsTile*)p.nsp_tiles,
+                                           (const NsGroup*)p.nsp_groups, p.nsp_bars,
+                                           b, reinterpret_cast<const CUtensorMap*>(p.d_ns_maps), ph);
+  if (tracing && e == cudaSuccess) {   // diagnostics only: serialises the stream
+    cudaStreamSynchronize((cudaStream_t)stream);
+    {
+      unsigned long long nrec = 0;
+      cudaMemcpy(&nrec, ttrace, 8, cudaMemcpyDeviceToHost);
+      nrec = std::min<unsigned long long>(nrec, 65536);
+      std::vector<unsigned long long> r(4 * nrec);
+      cudaMemcpy(r.data(), ttrace + 1, r.size() * 8, cudaMemcpyDeviceToHost);
+      // per (phase type, M, N, K): count, mean wait-for-accumulator, mean epilogue (warp 0 of the epilogue only)
+      struct Acc { int n = 0; double wait = 0, epi = 0, epimax = 0; };
+      std::map<std::tuple<int, int, int, int, int>, Acc> agg;
+      for (unsigned long long k = 0; k < nrec; ++k) {
+        const unsigned long long* q = &r[4 * k];
+        const int ph_ = (int)((q[0] >> 40) & 0xFF), ew = (int)((q[0] >> 36) & 0xF), desc = (int)((q[0] >> 16) & 0xFFFFF);
+        const int local = (int)(q[0] & 0xFFFF);
+        if (ew != 0 || ph_ > 3) continue;
+        const bool gram = flags[ph_] & 1;
+        const NsDesc& d = gram ? p.ns_gram[desc] : p.ns_upd[desc];
+        const int diag = gram && (local / d.tiles_n == local % d.tiles_n);
+        Acc& a = agg[std::make_tuple(ph_, d.M, d.N, d.K, diag)];
+        a.n++;
+        a.wait += (q[2] - q[1]) * 1e-3;
+        a.epi += (q[3] - q[2]) * 1e-3;
+        a.epimax = std::max(a.epimax, (q[3] - q[2]) * 1e-3);
+      }
+      for (auto& kv : agg)
+        std::printf("  tile ph%d M=%4d N=%4d K=%4d diag=%d: n=%3d wait %.2f epi %.2f (max %.2f) us\n", std::get<0>(kv.first),
+                    std::get<1>(kv.first), std::get<2>(kv.first), std::get<3>(kv.first), std::get<4>(kv.first),
+                    kv.second.n, kv.second.wait / kv.second.n, kv.second.epi / kv.second.n, kv.second.epimax);
+    }
+    const int W = 4 * nphases + 1;
+    std::vector<unsigned long long> h((size_t)p.nsp_ctas * W);
+    cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, t1 = 0;
+    for (int c = 0; c < p.nsp_ctas; ++c) {
+      t0 = std::min(t0, h[(size_t)c * W]);
+      t1 = std::max(t1, h[(size_t)c * W + W - 1]);
+    }
+    std::printf("ns_persist: %d CTAs, %d groups, %d phases, span %.1f us (model %.1f us/iter)\n", p.nsp_ctas,
+                p.nsp_groups_n, nphases, (t1 - t0) * 1e-3, p.nsp_est_us);
+    // per phase, averaged over CTAs: producer start -> epi first full -> epi done -> after sync (relative to previous sync)
+    for (int q = 0; q < nphases && q < 6; ++q) {
+      double a0 = 0, a1 = 0, a2 = 0, a3 = 0, m3 = 0, m1 = 0, m2 = 0;
+      for (int c = 0; c < p.nsp_ctas; ++c) {
+        const unsigned long long* r = &h[(size_t)c * W];
+        const double prev = (double)(q == 0 ? r[0] : r[1 + 4 * (q - 1) + 3]);
+        a0 += r[1 + 4 * q] - prev; a1 += r[2 + 4 * q] - prev; a2 += r[3 + 4 * q] - prev; a3 += r[4 + 4 * q] - prev;
+        m3 = std::max(m3, (double)(r[4 + 4 * q] - prev));
+        m1 = std::max(m1, (double)(r[2 + 4 * q] - prev));
+        m2 = std::max(m2, (double)(r[3 + 4 * q] - prev));
+      }
+      const double n = p.nsp_ctas * 1e3;
+      std::printf("  phase %d: prod_start %.2f first_full %.2f (max %.2f) epi_done %.2f (max %.2f) synced %.2f (max %.2f) us\n",
+                  q, a0 / n, a1 / n, m1 * 1e-3, a2 / n, m2 * 1e-3, a3 / n, m3 * 1e-3);
+    }
+  }
+  return (int)e;
+}
+
+}  // namespace orth

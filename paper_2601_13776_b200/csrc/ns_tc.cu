@@ -5,15 +5,20 @@
 // X is the FP32 master.  Every phase's epilogue also writes the BF16 (hi, and
 // for the 3-pass split lo = bf16(x - hi)) copies the NEXT phase consumes:
 // the Gram writes R (symmetric, so its rows are both operands' rows), the
-// update writes X' row-major and transposed.  The mainloop therefore only
-// moves BF16 K-major rows: 16-byte cp.async into a SWIZZLE_128B ring, one
-// thread issuing tcgen05.mma M=128 N=128 K=16 (x4 per 64-wide K block, x3 for
-// the hi/lo split), FP32 accumulation in TMEM.  Ragged batch: one flat tile
-// list over all matrices of all layers (descriptors from plan.cpp).
+// update writes X' row-major.  Operands that are columns of X (tall Gram
+// A = B = X^T, wide update B = X) are loaded MN-major straight from the
+// row-major copy, so no transposed copy exists.  Mainloop: TMA (SWIZZLE_128B)
+// into a 3-stage ring, one thread issuing tcgen05.mma M=128 N=128 K=16 (x4 per
+// 64-wide K block, x3 for the hi/lo split), FP32 accumulation in TMEM.
+// Ragged batch: one flat tile list over all matrices of all layers
+// (descriptors from plan.cpp).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -27,14 +32,19 @@ namespace {
 struct NsBufs {
   float* X[2];
   float* R;
-  __nv_bfloat16 *xh[2], *xl[2], *th[2], *tl[2], *rh, *rl;
+  __nv_bfloat16 *xh[2], *xl[2], *rh, *rl;
+  unsigned long long* trace;   // diagnostics (ORTH_NS_TRACE): 4 globaltimer stamps per CTA, else null
 };
 
-__device__ __forceinline__ const __nv_bfloat16* operand(const NsBufs& b, int kind, int par, bool lo) {
-  if (kind == 0) return lo ? b.xl[par] : b.xh[par];
-  if (kind == 1) return lo ? b.tl[par] : b.th[par];
-  return lo ? b.rl : b.rh;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
+
+// select a[i] without dynamic indexing (which would move the parameter struct to local memory)
+template <class T>
+__device__ __forceinline__ T pick(T const (&a)[2], int i) { return i ? a[1] : a[0]; }
 
 __device__ __forceinline__ int find_ns(const NsDesc* __restrict__ d, int n, int tile) {
   int lo = 0, hi = n - 1;
@@ -45,15 +55,45 @@ __device__ __forceinline__ int find_ns(const NsDesc* __restrict__ d, int n, int 
   return lo;
 }
 
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {   // low half = a
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// hi = bf16(x), lo = bf16(x - hi) for 4 values, packed into registers
+__device__ __forceinline__ void split4(float a, float b, float c, float d, uint2& hi, uint2& lo) {
+  hi.x = pack_bf16(a, b);
+  hi.y = pack_bf16(c, d);
+  const float ha = __uint_as_float(hi.x << 16), hb = __uint_as_float(hi.x & 0xFFFF0000u);
+  const float hc = __uint_as_float(hi.y << 16), hd = __uint_as_float(hi.y & 0xFFFF0000u);
+  lo.x = pack_bf16(a - ha, b - hb);
+  lo.y = pack_bf16(c - hc, d - hd);
+}
+
 __device__ __forceinline__ void split(float x, __nv_bfloat16& h, __nv_bfloat16& l) {
   h = __float2bfloat16_rn(x);
   l = __float2bfloat16_rn(x - __bfloat162float(h));
 }
 
+// One 128 (MN) x 64 (K) BF16 operand tile.  K-major: one 64 x 128 box.
+// MN-major (columns of row-major X): two 64 (MN) x 64 (K) boxes, 8 KB apart.
+__device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int k0, int mn0,
+                                             int mn_major) {
+  if (mn_major) {
+    umma::tma_load_2d(dst, map, bar, mn0, k0);
+    umma::tma_load_2d(dst + 8192, map, bar, mn0 + 64, k0);
+  } else {
+    umma::tma_load_2d(dst, map, bar, k0, mn0);
+  }
+}
+// descriptor of the q-th K=16 slice of an operand tile
+__device__ __forceinline__ uint64_t op_desc(uint32_t base, int q, int mn_major) {
+  return mn_major ? umma::sdesc_sw128_mn(base + 2048 * q, 8192) : umma::sdesc_sw128(base + 32 * q);
+}
+
 template <int NPASS, int S>
 __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
     ns_tc_kernel(const NsDesc* __restrict__ descs, const int* __restrict__ tile_desc, NsBufs bufs, int par,
-                 int write_lo, const CUtensorMap* __restrict__ maps) {
+                 int write_lo, int write_f, const CUtensorMap* __restrict__ maps) {
   constexpr bool SPLIT = NPASS == 3;
   constexpr int TILE = 128 * 128;
   constexpr int STAGE = (SPLIT ? 4 : 2) * TILE;
@@ -65,6 +105,7 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
   __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (bufs.trace && tid == 0) bufs.trace[8 * blockIdx.x] = gtimer();
   const NsDesc d = descs[tile_desc[blockIdx.x]];   // host-built tile -> problem table (one load)
   const int local = blockIdx.x - d.tile_begin;
   const int m0 = (local / d.tiles_n) * 128, n0 = (local % d.tiles_n) * 128;
@@ -83,7 +124,9 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
   umma::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const uint32_t s0 = umma::smem_u32(smem);
-  constexpr uint32_t IDESC = umma::idesc_bf16(128, 128);
+  const int a_mn = d.a_kind == 1, b_mn = d.b_kind == 1;   // operand = columns of row-major X: MN-major
+  const uint32_t IDESC = umma::idesc_bf16(128, 128) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
+  if (bufs.trace && tid == 0) bufs.trace[8 * blockIdx.x + 1] = gtimer();
 
   const int nk = (d.K + 63) / 64;
   if (tid == 0) {
@@ -96,11 +139,11 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
       if (kb >= S) umma::mbar_wait(&empty_bar[st], ((kb / S) - 1) & 1);
       const uint32_t sa = s0 + st * STAGE;
       umma::mbar_arrive_expect_tx(&full_bar[st], BYTES);
-      umma::tma_load_2d(sa, ma, &full_bar[st], kb * 64, m0);
-      umma::tma_load_2d(sa + TILE, mb, &full_bar[st], kb * 64, n0);
+      load_operand(sa, ma, &full_bar[st], kb * 64, m0, a_mn);
+      load_operand(sa + TILE, mb, &full_bar[st], kb * 64, n0, b_mn);
       if (SPLIT) {
-        umma::tma_load_2d(sa + 2 * TILE, ma + 1, &full_bar[st], kb * 64, m0);
-        umma::tma_load_2d(sa + 3 * TILE, mb + 1, &full_bar[st], kb * 64, n0);
+        load_operand(sa + 2 * TILE, ma + 1, &full_bar[st], kb * 64, m0, a_mn);
+        load_operand(sa + 3 * TILE, mb + 1, &full_bar[st], kb * 64, n0, b_mn);
       }
     }
   } else if (tid == 32) {
@@ -112,10 +155,11 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
       const uint32_t ah = s0 + st * STAGE, bh = ah + TILE, al = ah + 2 * TILE, bl = ah + 3 * TILE;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        umma::mma_bf16(tmem, umma::sdesc_sw128(ah + 32 * q), umma::sdesc_sw128(bh + 32 * q), IDESC, (kb | q) != 0);
+        const uint64_t dah = op_desc(ah, q, a_mn), dbh = op_desc(bh, q, b_mn);
+        umma::mma_bf16(tmem, dah, dbh, IDESC, (kb | q) != 0);
         if (SPLIT) {
-          umma::mma_bf16(tmem, umma::sdesc_sw128(ah + 32 * q), umma::sdesc_sw128(bl + 32 * q), IDESC, 1);
-          umma::mma_bf16(tmem, umma::sdesc_sw128(al + 32 * q), umma::sdesc_sw128(bh + 32 * q), IDESC, 1);
+          umma::mma_bf16(tmem, dah, op_desc(bl, q, b_mn), IDESC, 1);
+          umma::mma_bf16(tmem, op_desc(al, q, a_mn), dbh, IDESC, 1);
         }
       }
       umma::mma_commit(&empty_bar[st]);
@@ -132,31 +176,29 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
       const int h = u >> 3, e = tid + 256 * (u & 7), r = e >> 4, c4 = (e & 15) * 4;
       const int i = m0 + r, j0 = n0 + h * 64 + c4;
       cpre[u] = (d.epi == 1 && fv && i < d.M && j0 + 4 <= d.N)
-                    ? __ldg(reinterpret_cast<const float4*>(bufs.X[par] + d.f_off + (int64_t)i * d.ldf + j0))
+                    ? __ldg(reinterpret_cast<const float4*>(pick(bufs.X, par) + d.f_off + (int64_t)i * d.ldf + j0))
                     : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
   umma::mbar_wait(&done_bar, 0);
   umma::tc_fence_after();
+  if (bufs.trace && tid == 64) bufs.trace[8 * blockIdx.x + 2] = gtimer();
 
   // ---------------------------------------------------------------- epilogue
   // Two 64-column halves.  TMEM -> fp32 smem tile (row stride 68 floats: the
   // row-per-thread float4 writes and the row-wise float4 reads are both
   // conflict-free) -> one coalesced row pass (C in, D out as FP32, BF16 hi/lo
-  // row copies) that also stages the BF16 transpose -> one coalesced pass of
-  // X'^T rows (update phase only).  The operand ring is free once done_bar completed.
+  // row copies).  The Gram's FP32 R is only written when asked (residual).
+  // The operand ring is free once done_bar completed.
   const bool upd = d.epi == 1;
   const int ldb16 = upd ? d.ldx : d.ldr;   // padded row length of the row-major bf16 outputs
-  __nv_bfloat16* oh = upd ? bufs.xh[par ^ 1] + d.bx_off : bufs.rh + d.br_off;
-  __nv_bfloat16* ol = upd ? bufs.xl[par ^ 1] + d.bx_off : bufs.rl + d.br_off;
-  float* F = upd ? bufs.X[par ^ 1] + d.f_off : bufs.R + d.f_off;
-  const float* Cm = bufs.X[par] + d.f_off;
-  __nv_bfloat16* th = bufs.th[par ^ 1] + d.bx_off;
-  __nv_bfloat16* tl = bufs.tl[par ^ 1] + d.bx_off;
-  constexpr int LDF = 68, LDT = 136;
+  __nv_bfloat16* oh = upd ? pick(bufs.xh, par ^ 1) + d.bx_off : bufs.rh + d.br_off;
+  __nv_bfloat16* ol = upd ? pick(bufs.xl, par ^ 1) + d.bx_off : bufs.rl + d.br_off;
+  float* F = upd ? pick(bufs.X, par ^ 1) + d.f_off : bufs.R + d.f_off;
+  const float* Cm = pick(bufs.X, par) + d.f_off;
+  const bool wf = upd || write_f;
+  constexpr int LDF = 68;
   float* Sf = reinterpret_cast<float*>(smem);                              // [128][68] fp32
-  __nv_bfloat16* sTh = reinterpret_cast<__nv_bfloat16*>(smem + 128 * LDF * 4);   // [64][136] bf16
-  __nv_bfloat16* sTl = sTh + 64 * LDT;
   const bool fvec = (d.ldf & 3) == 0;      // 16-byte aligned fp32 rows
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -171,6 +213,7 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
     }
     umma::tc_fence_before();
     __syncthreads();
+    if (bufs.trace && tid == 0) bufs.trace[8 * blockIdx.x + 4 + 2 * h] = gtimer();
     // row pass: element group e -> (row r, 4 columns c4*4 .. +3)
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -189,92 +232,71 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
         o[3] = fmaf(d.alpha, o[3], d.beta * c.w);
 #pragma unroll
         for (int k = 0; k < 4; ++k) o[k] += (i == j0 + k) ? d.diag : 0.f;
-        *reinterpret_cast<float4*>(F + fo) = make_float4(o[0], o[1], o[2], o[3]);
+        if (wf) *reinterpret_cast<float4*>(F + fo) = make_float4(o[0], o[1], o[2], o[3]);
       } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           if (row_ok && j0 + k < d.N) {
             o[k] = fmaf(d.alpha, o[k], upd ? d.beta * __ldg(Cm + fo + k) : 0.f) + ((i == j0 + k) ? d.diag : 0.f);
-            F[fo + k] = o[k];
+            if (wf) F[fo + k] = o[k];
           } else {
             o[k] = 0.f;   // keeps every bf16 padding element zero
           }
         }
       }
-      __nv_bfloat16 hb[4], lb[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) split(o[k], hb[k], lb[k]);
+      uint2 hv, lv;   // register-packed bf16 quads (no local arrays)
+      split4(o[0], o[1], o[2], o[3], hv, lv);
       if (row_ok && j0 < ldb16) {   // ldb16 % 8 == 0 and j0 % 4 == 0: the 4-group is inside the padded row
         const int64_t bo = (int64_t)i * ldb16 + j0;
-        *reinterpret_cast<uint2*>(oh + bo) = *reinterpret_cast<const uint2*>(hb);
-        if (write_lo) *reinterpret_cast<uint2*>(ol + bo) = *reinterpret_cast<const uint2*>(lb);
-      }
-      if (upd) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          sTh[(c4 + k) * LDT + r] = hb[k];
-          if (write_lo) sTl[(c4 + k) * LDT + r] = lb[k];
-        }
+        *reinterpret_cast<uint2*>(oh + bo) = hv;
+        if (write_lo) *reinterpret_cast<uint2*>(ol + bo) = lv;
       }
     }
     __syncthreads();
-    if (upd) {   // rows of X'^T: 16-byte chunks along i
-      for (int e = tid; e < 64 * 16; e += 256) {
-        const int cl = e >> 4, i8 = (e & 15) * 8;
-        const int j = n0 + h * 64 + cl, i0 = m0 + i8;
-        if (j < d.N && i0 < d.ldxt) {
-          const int64_t o = (int64_t)j * d.ldxt + i0;
-          *reinterpret_cast<uint4*>(th + o) = *reinterpret_cast<const uint4*>(sTh + cl * LDT + i8);
-          if (write_lo) *reinterpret_cast<uint4*>(tl + o) = *reinterpret_cast<const uint4*>(sTl + cl * LDT + i8);
-        }
-      }
-      __syncthreads();
-    }
+    if (bufs.trace && tid == 0) bufs.trace[8 * blockIdx.x + 5 + 2 * h] = gtimer();
   }
   umma::tc_fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tmem, 128);
+  if (bufs.trace && tid == 0) bufs.trace[8 * blockIdx.x + 3] = gtimer();
 }
 
-// X0 = W / sigma and its BF16 copies (row-major and transposed)
+// X0 = W / sigma and its BF16 row copies (hi, and lo when the first Gram is
+// 3-pass); padding columns [n, pad8(n)) of the BF16 rows are written as zero.
 __global__ void __launch_bounds__(256) scale_bf16_kernel(const PowerItem* __restrict__ items,
                                                          const float* __restrict__ W, const float* __restrict__ sigma,
-                                                         float* __restrict__ X0, NsBufs b, int par, int write_lo) {
-  __shared__ float T[32][65];
+                                                         float* __restrict__ X0, NsBufs b, int par, int write_lo,
+                                                         unsigned* __restrict__ bars, int nbars) {
+  if (blockIdx.x == 0)   // re-arm the persistent NS group barriers (monotonic counters) for the launch that follows
+    for (int i = threadIdx.x; i < nbars; i += 256) bars[i] = 0u;
   const PowerItem it = items[blockIdx.x];
   const float inv = 1.f / sigma[it.mat];
-  const int n = it.n, ldx = (n + 7) & ~7, ldxt = (it.m + 7) & ~7;
-  __nv_bfloat16* xh = b.xh[par] + it.bx_off;
-  __nv_bfloat16* xl = b.xl[par] + it.bx_off;
-  __nv_bfloat16* th = b.th[par] + it.bx_off;
-  __nv_bfloat16* tl = b.tl[par] + it.bx_off;
-  for (int rt = it.r0; rt < it.r1; rt += 32)
-    for (int ct = 0; ct < n; ct += 64) {   // 32 x 64 tile: row-major pass, then transposed pass via smem
-      for (int e = threadIdx.x; e < 32 * 64; e += 256) {
-        const int rr = e >> 6, cc = e & 63, r = rt + rr, c = ct + cc;
-        float x = 0.f;
-        if (r < it.r1 && c < n) {
-          x = W[it.off + (int64_t)r * n + c] * inv;
-          X0[it.off + (int64_t)r * n + c] = x;
-          __nv_bfloat16 h, l;
-          split(x, h, l);
-          xh[(int64_t)r * ldx + c] = h;
-          if (write_lo) xl[(int64_t)r * ldx + c] = l;
-        }
-        T[rr][cc] = x;
+  const int n = it.n, ldx = (n + 7) & ~7, g4 = ldx >> 2;
+  __nv_bfloat16* xh = pick(b.xh, par) + it.bx_off;
+  __nv_bfloat16* xl = pick(b.xl, par) + it.bx_off;
+  const bool vec = (n & 3) == 0;
+  const int64_t total = (int64_t)(it.r1 - it.r0) * g4;
+  for (int64_t e = threadIdx.x; e < total; e += 256) {
+    const int r = it.r0 + (int)(e / g4), c = (int)(e % g4) * 4;
+    const int64_t fo = it.off + (int64_t)r * n + c;
+    float x[4];
+    if (vec && c < n) {
+      const float4 w = __ldg(reinterpret_cast<const float4*>(W + fo));
+      x[0] = w.x * inv; x[1] = w.y * inv; x[2] = w.z * inv; x[3] = w.w * inv;
+      *reinterpret_cast<float4*>(X0 + fo) = make_float4(x[0], x[1], x[2], x[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        x[k] = c + k < n ? __ldg(W + fo + k) * inv : 0.f;
+        if (c + k < n) X0[fo + k] = x[k];
       }
-      __syncthreads();
-      for (int e = threadIdx.x; e < 32 * 64; e += 256) {
-        const int cc = e >> 5, rr = e & 31, r = rt + rr, c = ct + cc;
-        if (r < it.r1 && c < n) {
-          __nv_bfloat16 h, l;
-          split(T[rr][cc], h, l);
-          th[(int64_t)c * ldxt + r] = h;
-          if (write_lo) tl[(int64_t)c * ldxt + r] = l;
-        }
-      }
-      __syncthreads();
     }
+    uint2 hv, lv;
+    split4(x[0], x[1], x[2], x[3], hv, lv);
+    const int64_t bo = (int64_t)r * ldx + c;
+    *reinterpret_cast<uint2*>(xh + bo) = hv;
+    if (write_lo) *reinterpret_cast<uint2*>(xl + bo) = lv;
+  }
 }
 
 NsBufs make_bufs(Plan& p, float* const bufs[BUF_COUNT]) {
@@ -287,18 +309,17 @@ NsBufs make_bufs(Plan& p, float* const bufs[BUF_COUNT]) {
   for (int k = 0; k < 2; ++k) {
     b.xh[k] = bx + (0 + k) * nx;
     b.xl[k] = bx + (2 + k) * nx;
-    b.th[k] = bx + (4 + k) * nx;
-    b.tl[k] = bx + (6 + k) * nx;
   }
   auto br = reinterpret_cast<__nv_bfloat16*>(p.d_br);
   b.rh = br;
   b.rl = br + (p.br_numel > 64 ? p.br_numel : 64);
+  b.trace = nullptr;
   return b;
 }
 
 template <int NPASS, int S>
-int launch_impl(const NsDesc* d, const int* td, int tiles, NsBufs b, int par, int write_lo, const CUtensorMap* maps,
-                cudaStream_t s) {
+int launch_impl(const NsDesc* d, const int* td, int tiles, NsBufs b, int par, int write_lo, int write_f,
+                const CUtensorMap* maps, cudaStream_t s) {
   constexpr int STAGE = (NPASS == 3 ? 4 : 2) * 128 * 128;
   const size_t smem = 1024 + (size_t)(S * STAGE > 128 * 129 * 4 ? S * STAGE : 128 * 129 * 4);
   static bool attr = false;
@@ -306,14 +327,16 @@ int launch_impl(const NsDesc* d, const int* td, int tiles, NsBufs b, int par, in
     cudaFuncSetAttribute(ns_tc_kernel<NPASS, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  ns_tc_kernel<NPASS, S><<<tiles, 256, smem, s>>>(d, td, b, par, write_lo, maps);
+  ns_tc_kernel<NPASS, S><<<tiles, 256, smem, s>>>(d, td, b, par, write_lo, write_f, maps);
   return (int)cudaGetLastError();
 }
 
 }  // namespace
 
-// One 2-D map per (matrix, operand kind, parity, hi/lo): dims (K, rows), row
-// stride = padded row length; box 64 x 128, SWIZZLE_128B.
+// One 2-D map per (matrix operand, parity, hi/lo) over the row-major BF16
+// copy, row stride = padded row length, SWIZZLE_128B.  K-major operands (rows
+// of X or R): dims (K, rows), box 64 x 128.  MN-major operands (columns of X):
+// dims (n, m) of X itself, box 64 x 64.
 orth_status_t build_ns_tma(Plan& p) {
   auto enc = tensor_map_encoder();
   if (!enc) {
@@ -327,14 +350,13 @@ orth_status_t build_ns_tma(Plan& p) {
     const int base = (int)maps.size();
     for (int par = 0; par < 2; ++par)
       for (int lo = 0; lo < 2; ++lo) {
-        const __nv_bfloat16* ptr = (kind == 0 ? (lo ? b.xl[par] : b.xh[par])
-                                    : kind == 1 ? (lo ? b.tl[par] : b.th[par])
-                                                : (lo ? b.rl : b.rh)) + off;
+        const __nv_bfloat16* ptr = (kind == 2 ? (lo ? b.rl : b.rh) : (lo ? b.xl[par] : b.xh[par])) + off;
         CUtensorMap m;
         std::memset(&m, 0, sizeof(m));
-        const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+        // MN-major: inner dim = the operand's MN extent (columns of X), outer = K (rows of X)
+        const cuuint64_t dims[2] = {(cuuint64_t)(kind == 1 ? rows : K), (cuuint64_t)(kind == 1 ? K : rows)};
         const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-        const cuuint32_t box[2] = {64, 128};
+        const cuuint32_t box[2] = {64, kind == 1 ? 64u : 128u};
         const cuuint32_t es[2] = {1, 1};
         if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(ptr), dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -390,7 +412,8 @@ orth_status_t build_ns_tma(Plan& p) {
   return ORTH_OK;
 }
 
-int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int npass, bool write_lo, void* stream) {
+int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int npass, bool write_lo, bool write_f,
+                 void* stream) {
   const int tiles = gram ? p.ns_gram_tiles : p.ns_upd_tiles;
   if (tiles == 0) return 0;
   const NsDesc* d = gram ? p.d_ns_gram : p.d_ns_upd;
@@ -400,16 +423,44 @@ int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int 
   auto maps = reinterpret_cast<const CUtensorMap*>(p.d_ns_maps);
   const int* td = gram ? p.d_ns_tile_gram : p.d_ns_tile_upd;
   (void)nd;
-  if (npass == 3) return launch_impl<3, 3>(d, td, tiles, b, par, write_lo, maps, (cudaStream_t)stream);
-  return launch_impl<1, 3>(d, td, tiles, b, par, write_lo, maps, (cudaStream_t)stream);
+  static unsigned long long* trace = nullptr;
+  static const bool tracing = std::getenv("ORTH_NS_TRACE") != nullptr;
+  if (tracing) {   // diagnostics only: serialises the stream and prints a per-launch summary
+    if (!trace) cudaMalloc(&trace, 4096 * 8 * sizeof(unsigned long long));
+    b.trace = trace;
+  }
+  const int e = npass == 3 ? launch_impl<3, 3>(d, td, tiles, b, par, write_lo, write_f, maps, (cudaStream_t)stream)
+                           : launch_impl<1, 3>(d, td, tiles, b, par, write_lo, write_f, maps, (cudaStream_t)stream);
+  if (tracing && !e) {
+    std::vector<unsigned long long> h((size_t)tiles * 8);
+    cudaStreamSynchronize((cudaStream_t)stream);
+    cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, t3 = 0;
+    double setup = 0, mainl = 0, epi = 0, mx_main = 0, last_start = 0;
+    double ep[4] = {0, 0, 0, 0};
+    for (int i = 0; i < tiles; ++i) t0 = std::min(t0, h[8 * i]);
+    for (int i = 0; i < tiles; ++i) {
+      const unsigned long long* q = &h[8 * i];
+      ep[0] += q[4] - q[2]; ep[1] += q[5] - q[4]; ep[2] += q[6] - q[5]; ep[3] += q[7] - q[6];
+      t3 = std::max(t3, q[3]);
+      setup += q[1] - q[0]; mainl += q[2] - q[1]; epi += q[3] - q[2];
+      mx_main = std::max(mx_main, (double)(q[2] - q[1]));
+      last_start = std::max(last_start, (double)(q[0] - t0));
+    }
+    std::printf("ns_tc %s npass=%d tiles=%d span=%.2fus setup=%.2f main=%.2f (max %.2f) epi=%.2f [ld0 %.2f row0 %.2f tr0+ld1 %.2f row1 %.2f] last_start=%.2f\n",
+                gram ? "gram" : "upd ", npass, tiles, (t3 - t0) * 1e-3, setup / tiles * 1e-3, mainl / tiles * 1e-3,
+                mx_main * 1e-3, epi / tiles * 1e-3, ep[0] / tiles * 1e-3, ep[1] / tiles * 1e-3, ep[2] / tiles * 1e-3,
+                ep[3] / tiles * 1e-3, last_start * 1e-3);
+  }
+  return e;
 }
 
 int launch_scale_bf16(Plan& p, const float* W, float* X0, int par, bool write_lo, void* stream) {
   if (p.power_items.empty()) return 0;
   float* bufs[BUF_COUNT] = {X0, X0, nullptr, nullptr};
   NsBufs b = make_bufs(p, bufs);
-  scale_bf16_kernel<<<(int)p.power_items.size(), 256, 0, (cudaStream_t)stream>>>(p.d_power_items, W, p.d_sigma, X0,
-                                                                               b, par, write_lo);
+  scale_bf16_kernel<<<(int)p.power_items.size(), 256, 0, (cudaStream_t)stream>>>(
+      p.d_power_items, W, p.d_sigma, X0, b, par, write_lo, p.nsp_bars, p.nsp_bars ? p.nsp_groups_n : 0);
   p.launches++;
   return (int)cudaGetLastError();
 }

@@ -81,17 +81,29 @@ struct GemmPhase {        // one launch: a batch of independent problems
 // phase's epilogue.  kinds: 0 = X (m x n), 1 = X^T (n x m), 2 = R (s x s).
 struct NsDesc {
   int32_t M, N, K;
-  int32_t a_kind, b_kind;
-  int32_t epi;              // 0: Gram epilogue (R fp32 + bf16), 1: update epilogue (X' fp32 + bf16 X', X'^T)
+  int32_t a_kind, b_kind;   // 0: rows of X, 1: columns of X (MN-major), 2: rows of R
+  int32_t epi;              // 0: Gram epilogue (bf16 R, fp32 R on request), 1: update epilogue (X' fp32 + bf16 X')
   int64_t a_off, lda, b_off, ldb;
   int64_t f_off, ldf;       // fp32 offset/ld of D (and C for the update)
-  int64_t bx_off;           // offset of this matrix in the bf16 X / X^T buffers
+  int64_t bx_off;           // offset of this matrix in the bf16 X buffers
   int64_t br_off;           // offset of this matrix in the bf16 R buffers
   int32_t ldx, ldxt, ldr;   // padded bf16 leading dims: pad8(n), pad8(m), pad8(s)
   float alpha, beta, diag;
   int32_t tile_begin, tiles_n;
   int32_t map_a, map_b;     // TMA tensor maps: maps[map_x + 2 * parity + lo]
 };
+
+// persistent NS (ns_persist.cu): one tile of a phase, and a group of CTAs
+// that owns a set of matrices for all 2T phases
+struct NsTile {
+  int32_t desc, local;      // matrix index (ns_gram / ns_upd), tile index inside the matrix
+};
+struct NsGroup {           // per CTA: its barrier group and its own tile ranges (LPT-assigned on the host)
+  int32_t gid, G;           // group index (barrier counter), CTAs in the group
+  int32_t g_begin, g_end;   // Gram tiles [g_begin, g_end) of the tile array
+  int32_t u_begin, u_end;   // update tiles
+};
+constexpr int kNspMaxPhases = 132;   // 2T + 1 for T <= 65
 
 struct PowerItem {        // one CTA of the pre-scaling kernels: rows [r0, r1) of matrix `mat`
   int32_t mat, r0, r1, chunk;   // chunk: global partial slot
@@ -150,11 +162,18 @@ struct Plan {
   NsDesc* d_ns_gram = nullptr;
   NsDesc* d_ns_upd = nullptr;
   int64_t bx_numel = 0, br_numel = 0;
-  uint16_t* d_bx = nullptr;         // 8 x bx_numel: Xh[2], Xl[2], XTh[2], XTl[2]
+  uint16_t* d_bx = nullptr;         // 4 x bx_numel: Xh[2], Xl[2] (row-major, rows padded to 8)
   uint16_t* d_br = nullptr;         // 2 x br_numel: Rh, Rl
   void* d_ns_maps = nullptr;        // CUtensorMap array of the NS operands (separate allocation)
   int* d_ns_tile_gram = nullptr;    // tile -> problem tables (inside the d_ns_maps allocation)
   int* d_ns_tile_upd = nullptr;
+  // persistent NS (all phases in one cooperative launch); nsp_ctas == 0: unavailable
+  void* nsp_mem = nullptr;
+  NsTile* nsp_tiles = nullptr;
+  NsGroup* nsp_groups = nullptr;
+  unsigned* nsp_bars = nullptr;
+  int32_t nsp_ctas = 0, nsp_groups_n = 0;
+  double nsp_est_us = 0.0;
   std::vector<PowerItem> power_items;
   std::vector<int32_t> owned_mats;  // indices of owned, non-empty matrices
   std::vector<MatItem> mat_items;   // same order as owned_mats
@@ -195,8 +214,14 @@ int launch_residual_r(Plan& p, float* residual_out, void* stream);
 // tensor-core NS phase on the BF16 copies.  par: parity of the current X
 // (0: BUF_X, 1: BUF_Y).  gram: Gram (else update).  npass 1|3.  write_lo:
 // the epilogue also writes the lo halves of its BF16 outputs.
-int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int npass, bool write_lo, void* stream);
-// X0 = W / sigma (fp32) plus its BF16 copies X0, X0^T (hi, and lo if write_lo)
+int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int npass, bool write_lo, bool write_f,
+                 void* stream);
+// persistent NS: build the CTA-group partition (after build_ns_tma); launch all
+// phases (flags per phase: bit0 gram, bit1 3-pass, bit2 X parity, bit3 write lo,
+// bit4 write fp32 R)
+orth_status_t build_ns_persist(Plan& p);
+int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flags, int nphases, void* stream);
+// X0 = W / sigma (fp32) plus its row-major BF16 copies (hi, and lo if write_lo)
 int launch_scale_bf16(Plan& p, const float* W, float* X0, int par, bool write_lo, void* stream);
 // tensor-core composition: built after the workspace exists; freed with the plan
 orth_status_t build_compose_tc(Plan& p);

@@ -278,9 +278,10 @@ static void build_ns(Plan& P) {
     for (auto& d : gr.descs) { d.alpha = -1.0f; d.diag = 1.0f; }
     for (auto& e : ur.descs) { e.alpha = b; e.beta = 1.0f; }
   }
-  // tensor-core NS on BF16 copies: Gram R = I - X^T X (tall: A = B = X^T rows) or
-  // I - X X^T (wide: A = B = X rows); update X' = X + b X R (tall: A = X, B = R)
-  // or X + b R X (wide: A = R, B = X^T rows).  R is symmetric, so its rows serve as B.
+  // tensor-core NS on BF16 copies: Gram R = I - X^T X (tall: A = B = columns of X,
+  // kind 1 = MN-major loads) or I - X X^T (wide: A = B = X rows); update
+  // X' = X + b X R (tall: A = X, B = R) or X + b R X (wide: A = R, B = columns
+  // of X).  R is symmetric, so its rows serve as B.
   P.ns_gram.clear();
   P.ns_upd.clear();
   int32_t tg = 0, tu = 0;
@@ -294,7 +295,7 @@ static void build_ns(Plan& P) {
     g.M = s; g.N = s; g.K = std::max(m, n);
     g.a_kind = g.b_kind = (m >= n) ? 1 : 0;
     g.a_off = g.b_off = M.bx_off;
-    g.lda = g.ldb = (m >= n) ? base.ldxt : base.ldx;
+    g.lda = g.ldb = base.ldx;   // tall: columns of X, loaded MN-major from the row-major copy
     g.epi = 0; g.f_off = M.gram_off; g.ldf = s;
     g.alpha = -1.0f; g.beta = 0.0f; g.diag = 1.0f;
     g.tile_begin = tg; g.tiles_n = (s + 127) / 128;
@@ -303,7 +304,7 @@ static void build_ns(Plan& P) {
     NsDesc u = base;
     u.M = m; u.N = n; u.K = s;
     if (m >= n) { u.a_kind = 0; u.a_off = M.bx_off; u.lda = base.ldx; u.b_kind = 2; u.b_off = M.br_off; u.ldb = base.ldr; }
-    else { u.a_kind = 2; u.a_off = M.br_off; u.lda = base.ldr; u.b_kind = 1; u.b_off = M.bx_off; u.ldb = base.ldxt; }
+    else { u.a_kind = 2; u.a_off = M.br_off; u.lda = base.ldr; u.b_kind = 1; u.b_off = M.bx_off; u.ldb = base.ldx; }
     u.epi = 1; u.f_off = M.off; u.ldf = n;
     u.alpha = b; u.beta = 1.0f; u.diag = 0.0f;
     u.tile_begin = tu; u.tiles_n = (n + 127) / 128;
@@ -503,7 +504,7 @@ static orth_status_t allocate(Plan& P) {
   const size_t o_emit = take(std::max<size_t>(P.emit.size(), 1) * sizeof(EmitItem));
   const size_t o_nsg = take(std::max<size_t>(P.ns_gram.size(), 1) * sizeof(NsDesc));
   const size_t o_nsu = take(std::max<size_t>(P.ns_upd.size(), 1) * sizeof(NsDesc));
-  const size_t o_bx = take((size_t)8 * std::max<int64_t>(P.bx_numel, 64) * 2);
+  const size_t o_bx = take((size_t)4 * std::max<int64_t>(P.bx_numel, 64) * 2);
   int64_t max_kernel = 64;
   for (auto& L : P.layers) max_kernel = std::max(max_kernel, L.kernel_numel);
   const size_t o_wt = take((size_t)16 * max_kernel * 2);   // W^T (<= 8x with packing) + packed W (<= 8x)
@@ -619,9 +620,11 @@ orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers
     st = allocate(P);
     if (st == ORTH_OK && P.opts.compute != ORTH_F32) st = build_compose_tc(P);
     if (st == ORTH_OK && P.opts.compute != ORTH_F32) st = build_ns_tma(P);
+    if (st == ORTH_OK && P.opts.compute != ORTH_F32) st = build_ns_persist(P);
     if (st != ORTH_OK) {
       free_compose_tc(P);
       if (P.d_ns_maps) cudaFree(P.d_ns_maps);
+      if (P.nsp_mem) cudaFree(P.nsp_mem);
       if (P.d_arena) cudaFree(P.d_arena);
       delete h;
       return st;
@@ -635,6 +638,7 @@ orth_status_t orth_plan_destroy(orth_plan_t plan) {
   if (!plan) return ORTH_OK;
   free_compose_tc(plan->p);
   if (plan->p.d_ns_maps) cudaFree(plan->p.d_ns_maps);
+  if (plan->p.nsp_mem) cudaFree(plan->p.nsp_mem);
   if (plan->p.d_arena) cudaFree(plan->p.d_arena);
   delete plan;
   return ORTH_OK;

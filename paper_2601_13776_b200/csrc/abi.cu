@@ -64,17 +64,9 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
   float* x0 = bufs[par == 0 ? BUF_X : BUF_Y];
   const int frob = P.opts.prescale == ORTH_PRESCALE_FROBENIUS;
   int e = 0;
-  if (frob) {
-    e = launch_power_partial(P, params, nullptr, 1, 1, stream);
-    if (!e) e = launch_power_finalize(P, nullptr, 1, 0, stream);
-  } else {
-    const int Pn = P.opts.power_iters;
-    for (int it = 0; it < Pn && !e; ++it) {
-      const float* vin = it == 0 ? power_cache : P.d_vbuf;
-      e = launch_power_partial(P, params, vin, (it == 0 && !power_cache) ? 1 : 0, 0, stream);
-      if (!e) e = launch_power_finalize(P, (it == Pn - 1) ? power_cache : nullptr, 0, 0, stream);
-    }
-  }
+  // pre-scaling: all power iterations (or the Frobenius pass) in one cooperative launch
+  e = launch_power_fused(P, params, power_cache, (!frob && !power_cache) ? 1 : 0, frob, P.opts.power_iters,
+                         frob ? nullptr : power_cache, stream);
   const int mode = P.opts.compute;
   if (mode == ORTH_F32) {
     if (!e) e = launch_scale(P, params, x0, stream);

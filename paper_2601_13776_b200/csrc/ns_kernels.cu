@@ -11,6 +11,11 @@
 //    (the FP32-accurate path: 1e-5 parity needs FP32 products, R16).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <vector>
+
 #include <cstdint>
 
 #include "orth_internal.h"
@@ -130,105 +135,227 @@ __device__ float block_sum(float v, float* red) {
   return red[8];
 }
 
-// One CTA per PowerItem.  Power: partial[chunk] = (sum_r t_r W[r,:], sum_r t_r^2)
-// with t = W v.  Frobenius: partial[chunk][0] = sum of squares.
-__global__ void __launch_bounds__(256) power_partial_kernel(const PowerItem* __restrict__ items,
-                                                            const float* __restrict__ W, const float* __restrict__ vin,
-                                                            int use_const, int frob, float* __restrict__ partial,
-                                                            int64_t stride) {
-  extern __shared__ float sm[];
-  __shared__ float red[9];
-  const PowerItem it = items[blockIdx.x];
-  const int n = it.n;
-  const float* __restrict__ Wm = W + it.off;
-  float* __restrict__ out = partial + (int64_t)it.chunk * stride;
-  const int rows = it.r1 - it.r0;
-  if (frob) {
-    float acc = 0.f;
-    const int64_t beg = (int64_t)it.r0 * n, end = (int64_t)it.r1 * n;
-    for (int64_t e = beg + threadIdx.x; e < end; e += 256) { const float x = Wm[e]; acc = fmaf(x, x, acc); }
-    acc = block_sum(acc, red);
-    if (threadIdx.x == 0) out[0] = acc;
-    return;
-  }
-  float* v = sm;          // n
-  float* t = sm + n;      // rows
-  const float inv = rsqrtf((float)n);
-  const float* vsrc = use_const ? nullptr : vin + it.cache_off;
-  for (int j = threadIdx.x; j < n; j += 256) v[j] = use_const ? inv : vsrc[j];
+// ---------------------------------------------------------------- power iteration (O2)
+// One power step of the oracle (prescale_power): wv = W v; u = wv / |wv|;
+// w = W^T u; sig = |w|; v = w / sig.  Split over row items (t = W v, |t|^2
+// partials) and column items (w = W^T u, |w|^2 partials) with a grid barrier
+// between; every norm is a fixed-order sum over the matrix's items.
+__device__ __forceinline__ void power_grid_sync(unsigned* bar, unsigned target) {
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float tt = 0.f;
-  for (int r = warp; r < rows; r += 8) {
-    const float* row = Wm + (int64_t)(it.r0 + r) * n;
-    float a = 0.f;
-    for (int j = lane; j < n; j += 32) a = fmaf(row[j], v[j], a);
-    a = warp_sum(a);
-    if (lane == 0) t[r] = a;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
   }
   __syncthreads();
-  for (int r = threadIdx.x; r < rows; r += 256) tt = fmaf(t[r], t[r], tt);
-  tt = block_sum(tt, red);
-  for (int j = threadIdx.x; j < n; j += 256) {
-    float a = 0.f;
-    for (int r = 0; r < rows; ++r) a = fmaf(t[r], Wm[(int64_t)(it.r0 + r) * n + j], a);
-    out[j] = a;
-  }
-  if (threadIdx.x == 0) out[n] = tt;
 }
 
-// One CTA per owned matrix: reduce partials in chunk order.
-__global__ void __launch_bounds__(256) power_finalize_kernel(const MatItem* __restrict__ mats,
-                                                             const float* __restrict__ partial, int64_t stride,
-                                                             int frob, float* __restrict__ vbuf,
-                                                             float* __restrict__ cache_out, float* __restrict__ sigma,
-                                                             int32_t* __restrict__ status) {
-  __shared__ float red[9];
-  const MatItem M = mats[blockIdx.x];
-  const int n = M.n;
-  if (frob) {
+// fixed-order sum of cnt partials (thread 0), broadcast through smem
+__device__ __forceinline__ float ordered_sum(const float* p, int cnt, float* slot) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
     float s = 0.f;
-    if (threadIdx.x == 0)
-      for (int c = 0; c < M.nchunks; ++c) s += partial[(int64_t)(M.chunk0 + c) * stride];
-    if (threadIdx.x == 0) {
-      float sg = sqrtf(s);
-      if (!(sg > 0.f) || !isfinite(sg)) { atomicCAS(status, 0, (int)ORTH_ERR_ZERO_NORM); sg = 1.f; }
-      sigma[M.mat] = sg;
+    for (int c = 0; c < cnt; ++c) s += p[c];
+    *slot = s;
+  }
+  __syncthreads();
+  return *slot;
+}
+
+constexpr int kPowerStage = 10240;   // floats of a W block staged in smem by one power item
+
+struct PowerBufs {
+  float* t;       // t = W v, per matrix at t_off
+  float* tpart;   // |t|^2 per row item
+  float* wpart;   // |w|^2 per column item
+};
+
+__global__ void __launch_bounds__(256) power_fused_kernel(const PowerItem* __restrict__ items, int n_items,
+                                                          const ColItem* __restrict__ cols, int n_cols,
+                                                          const MatItem* __restrict__ mats, int n_mats,
+                                                          const float* __restrict__ W, const float* vin0, int use_const,
+                                                          int frob, int iters, PowerBufs pb, float* vbuf,
+                                                          float* __restrict__ cache_out, float* __restrict__ sigma,
+                                                          int32_t* __restrict__ status, unsigned* bar) {
+  extern __shared__ float sm[];
+  __shared__ float red[9];
+  __shared__ float slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned k = 0;
+  if (frob) {   // |W|_F: sums of squares per row item, then per matrix in item order
+    for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+      const PowerItem it = items[i];
+      const float* Wm = W + it.off;
+      float acc = 0.f;
+      for (int64_t e = (int64_t)it.r0 * it.n + threadIdx.x; e < (int64_t)it.r1 * it.n; e += 256) {
+        const float x = Wm[e];
+        acc = fmaf(x, x, acc);
+      }
+      acc = block_sum(acc, red);
+      if (threadIdx.x == 0) pb.tpart[it.chunk] = acc;
+    }
+    power_grid_sync(bar, ++k * gridDim.x);
+    for (int m = blockIdx.x; m < n_mats; m += gridDim.x) {
+      const MatItem M = mats[m];
+      float sg = sqrtf(ordered_sum(pb.tpart + M.chunk0, M.nchunks, &slot));
+      if (threadIdx.x == 0) {
+        if (!(sg > 0.f) || !isfinite(sg)) { atomicCAS(status, 0, (int)ORTH_ERR_ZERO_NORM); sg = 1.f; }
+        sigma[M.mat] = sg;
+      }
     }
     return;
   }
-  // |Wv|^2: one chunk per thread (nchunks <= 64), fixed-tree block sum
-  float ss = threadIdx.x < M.nchunks ? partial[(int64_t)(M.chunk0 + threadIdx.x) * stride + n] : 0.f;
-  ss = block_sum(ss, red);
-  const bool bad = !(ss > 0.f) || !isfinite(ss);
-  const float inv_wv = bad ? 0.f : rsqrtf(ss);
-  float nw = 0.f;
-  for (int j = threadIdx.x; j < n; j += 256) {
-    float w = 0.f;
+  for (int itr = 0; itr < iters; ++itr) {
+    // ---- A: t = W v over row items (T threads per row, shuffle-reduced)
+    for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+      const PowerItem it = items[i];
+      const int n = it.n, rows = it.r1 - it.r0;
+      float scale;
+      const float* vsrc;
+      if (itr == 0) {
+        scale = use_const ? rsqrtf((float)n) : 1.f;
+        vsrc = use_const ? nullptr : vin0 + it.cache_off;
+      } else {   // v = w / |w| of the previous step
+        const MatItem M = mats[it.midx];
+        const float ww = ordered_sum(pb.wpart + M.col0, M.ncols, &slot);
+        scale = ww > 0.f ? rsqrtf(ww) : 0.f;
+        vsrc = vbuf + it.cache_off;
+      }
+      float* v = sm;
+      for (int j = threadIdx.x; j < n; j += 256) v[j] = vsrc ? vsrc[j] * scale : scale;
+      int T = 1;
+      while (T < 32 && rows * T * 2 <= 256) T *= 2;
+      float tt = 0.f;
+      const float* Wm = W + it.off;
+      // stage the block in smem with all loads in flight (rows padded to n + 4)
+      const int ldw = n + 4;
+      float* Ws = sm + ((n + 3) & ~3);
+      const bool staged = (n & 3) == 0 && rows * ldw <= kPowerStage;
+      if (staged) {
+        const float4* src = reinterpret_cast<const float4*>(Wm + (int64_t)it.r0 * n);
+        const int n4 = n >> 2;
+        for (int e = threadIdx.x; e < rows * n4; e += 256) {
+          const int r = e / n4, c = e - r * n4;
+          *reinterpret_cast<float4*>(Ws + r * ldw + 4 * c) = __ldg(src + e);
+        }
+      }
+      __syncthreads();
+      for (int r0 = 0; r0 < rows; r0 += 256 / T) {
+        const int r = r0 + threadIdx.x / T, sub = threadIdx.x % T;
+        float a = 0.f;
+        if (r < rows) {
+          if (staged) {
+            const float* row = Ws + r * ldw;
+            for (int j = sub; j < n; j += T) a = fmaf(row[j], v[j], a);
+          } else {
+            const float* row = Wm + (int64_t)(it.r0 + r) * n;
+            float a2 = 0.f;
+            int j = sub;
+#pragma unroll 4
+            for (; j + T < n; j += 2 * T) {
+              a = fmaf(__ldg(row + j), v[j], a);
+              a2 = fmaf(__ldg(row + j + T), v[j + T], a2);
+            }
+            if (j < n) a = fmaf(__ldg(row + j), v[j], a);
+            a += a2;
+          }
+        }
+        for (int o = T >> 1; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (r < rows && sub == 0) {
+          pb.t[it.t_off + it.r0 + r] = a;
+          tt = fmaf(a, a, tt);
+        }
+      }
+      tt = block_sum(tt, red);
+      if (threadIdx.x == 0) pb.tpart[it.chunk] = tt;
+      __syncthreads();
+    }
+    power_grid_sync(bar, ++k * gridDim.x);
+    // ---- B: w = W^T u, u = t / |t|, over column items
+    for (int c = blockIdx.x; c < n_cols; c += gridDim.x) {
+      const ColItem ci = cols[c];
+      const MatItem M = mats[ci.midx];
+      const int n = ci.n, m = ci.m, cw = ci.c1 - ci.c0;
+      const float tt = ordered_sum(pb.tpart + M.chunk0, M.nchunks, &slot);
+      const float inv = tt > 0.f ? rsqrtf(tt) : 0.f;
+      if (threadIdx.x == 0 && !(tt > 0.f && isfinite(tt))) atomicCAS(status, 0, (int)ORTH_ERR_ZERO_NORM);
+      float* u = sm;
+      for (int r = threadIdx.x; r < m; r += 256) u[r] = pb.t[ci.t_off + r] * inv;
+      const int lanes = cw < 256 ? ((cw + 31) / 32) * 32 : 256;   // column threads (whole warps)
+      const int ng = 256 / lanes, g = threadIdx.x / lanes, jj = threadIdx.x % lanes;
+      float* part = sm + ((m + 3) & ~3);   // ng x lanes
+      const float* Wm = W + ci.off;
+      // stage the column block in smem (rows of cw padded to cw + 4) when it fits
+      const int ldc = cw + 4;
+      float* Ws = part + 256;
+      const bool staged = ((n | ci.c0 | cw) & 3) == 0 && m * ldc <= kPowerStage;
+      if (staged) {
+        const int c4n = cw >> 2;
+        for (int e = threadIdx.x; e < m * c4n; e += 256) {
+          const int r = e / c4n, c = e - r * c4n;
+          *reinterpret_cast<float4*>(Ws + r * ldc + 4 * c) =
+              __ldg(reinterpret_cast<const float4*>(Wm + (int64_t)r * n + ci.c0) + c);
+        }
+      }
+      __syncthreads();
+      float ww = 0.f;
+      for (int j0 = 0; j0 < cw; j0 += lanes) {
+        const int j = ci.c0 + j0 + jj;
+        float a = 0.f;
+        if (g < ng && j0 + jj < cw) {
+          if (staged) {
+            for (int r = g; r < m; r += ng) a = fmaf(Ws[r * ldc + j0 + jj], u[r], a);
+          } else {
 #pragma unroll 8
-    for (int c = 0; c < M.nchunks; ++c) w += partial[(int64_t)(M.chunk0 + c) * stride + j];
-    w *= inv_wv;
-    vbuf[M.cache_off + j] = w;
-    nw = fmaf(w, w, nw);
+            for (int r = g; r < m; r += ng) a = fmaf(__ldg(Wm + (int64_t)r * n + j), u[r], a);
+          }
+        }
+        if (g < ng) part[g * lanes + jj] = a;
+        __syncthreads();
+        if (threadIdx.x < lanes && j0 + threadIdx.x < cw) {
+          float w = 0.f;
+          for (int q = 0; q < ng; ++q) w += part[q * lanes + threadIdx.x];
+          vbuf[ci.cache_off + ci.c0 + j0 + threadIdx.x] = w;
+          ww = fmaf(w, w, ww);
+        }
+        __syncthreads();
+      }
+      ww = block_sum(ww, red);
+      if (threadIdx.x == 0) pb.wpart[ci.chunk] = ww;
+      __syncthreads();
+    }
+    power_grid_sync(bar, ++k * gridDim.x);
   }
-  nw = block_sum(nw, red);
-  float sg = sqrtf(nw);
-  const bool bad2 = bad || !(sg > 0.f) || !isfinite(sg);
-  if (bad2) sg = 1.f;
-  const float inv = 1.f / sg;
-  for (int j = threadIdx.x; j < n; j += 256) {
-    const float v = vbuf[M.cache_off + j] * inv;
-    vbuf[M.cache_off + j] = v;
-    if (cache_out) cache_out[M.cache_off + j] = v;
+  // ---- finalize: sig = |w|, v = w / sig (cache), per matrix
+  for (int mi = blockIdx.x; mi < n_mats; mi += gridDim.x) {
+    const MatItem M = mats[mi];
+    const float ww = ordered_sum(pb.wpart + M.col0, M.ncols, &slot);
+    float sg = sqrtf(ww);
+    const bool bad = !(sg > 0.f) || !isfinite(sg);
+    if (bad) sg = 1.f;
+    const float inv = 1.f / sg;
+    for (int j = threadIdx.x; j < M.n; j += 256) {
+      const float v = vbuf[M.cache_off + j] * inv;
+      vbuf[M.cache_off + j] = v;
+      if (cache_out) cache_out[M.cache_off + j] = v;
+    }
+    if (threadIdx.x == 0) {
+      sigma[M.mat] = sg;
+      if (bad) atomicCAS(status, 0, (int)ORTH_ERR_ZERO_NORM);
+    }
+    __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    sigma[M.mat] = sg;
-    if (bad2) atomicCAS(status, 0, (int)ORTH_ERR_ZERO_NORM);
-  }
+  (void)warp;
+  (void)lane;
 }
 
 __global__ void __launch_bounds__(256) scale_kernel(const PowerItem* __restrict__ items, const float* __restrict__ W,
-                                                    const float* __restrict__ sigma, float* __restrict__ X0) {
+                                                    const float* __restrict__ sigma, float* __restrict__ X0,
+                                                    unsigned* __restrict__ power_bar) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *power_bar = 0u;   // re-arm the fused power kernel's barrier
   const PowerItem it = items[blockIdx.x];
   const float inv = 1.f / sigma[it.mat];
   const int64_t beg = it.off + (int64_t)it.r0 * it.n, end = it.off + (int64_t)it.r1 * it.n;
@@ -266,33 +393,52 @@ int launch_gemm_f32(const GemmPhase& ph, float* const bufs[BUF_COUNT], void* str
   return (int)cudaGetLastError();
 }
 
-int launch_power_partial(Plan& p, const float* W, const float* v_in, int use_const_v, int frob, void* stream) {
+int launch_power_fused(Plan& p, const float* W, const float* v_in, int use_const_v, int frob, int iters,
+                       float* cache_out, void* stream) {
   if (p.power_items.empty()) return 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(power_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    attr = true;
+  int64_t maxn = 0, maxm = 0;
+  for (auto& m : p.mat_items) { maxn = std::max<int64_t>(maxn, m.n); maxm = std::max<int64_t>(maxm, m.m); }
+  // smem: v (n) + staged block for row items; u (m) + 256 partial sums + staged block for column items
+  const size_t smem = (size_t)(std::max<int64_t>(((maxn + 3) & ~3), ((maxm + 3) & ~3) + 256) + kPowerStage) *
+                      sizeof(float);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(power_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
   }
-  int64_t maxn = 0, maxr = 0;
-  for (auto& it : p.power_items) { maxn = it.n > maxn ? it.n : maxn; maxr = (it.r1 - it.r0) > maxr ? (it.r1 - it.r0) : maxr; }
-  const size_t smem = frob ? 0 : (size_t)(maxn + maxr) * sizeof(float);
-  power_partial_kernel<<<(int)p.power_items.size(), 256, smem, (cudaStream_t)stream>>>(
-      p.d_power_items, W, v_in, use_const_v, frob, p.d_partial, p.partial_stride);
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, power_fused_kernel, 256, smem);
+  if (occ < 1) return (int)cudaErrorInvalidConfiguration;
+  const int n_items = (int)p.power_items.size(), n_cols = (int)p.col_items.size(), n_mats = (int)p.mat_items.size();
+  static const int mult = std::getenv("ORTH_POWER_CTAS_PER_SM") ? std::atoi(std::getenv("ORTH_POWER_CTAS_PER_SM")) : 4;
+  const int grid = std::max(1, std::min(std::max(n_items, n_cols), std::max(1, std::min(occ, mult)) * sms));
+  PowerBufs pb;
+  pb.t = p.d_partial;
+  pb.tpart = p.d_partial + pad_up(p.t_numel, kPadF32);
+  pb.wpart = pb.tpart + pad_up(p.n_chunks, kPadF32);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr_c[1];
+  attr_c[0].id = cudaLaunchAttributeCooperative;
+  attr_c[0].val.cooperative = 1;
+  cfg.attrs = attr_c;
+  cfg.numAttrs = 1;
   p.launches++;
-  return (int)cudaGetLastError();
-}
-
-int launch_power_finalize(Plan& p, float* cache_out, int frob, int, void* stream) {
-  if (p.mat_items.empty()) return 0;
-  power_finalize_kernel<<<(int)p.mat_items.size(), 256, 0, (cudaStream_t)stream>>>(
-      p.d_mat_items, p.d_partial, p.partial_stride, frob, p.d_vbuf, cache_out, p.d_sigma, p.d_status);
-  p.launches++;
-  return (int)cudaGetLastError();
+  return (int)cudaLaunchKernelEx(&cfg, power_fused_kernel, (const PowerItem*)p.d_power_items, n_items,
+                                 (const ColItem*)p.d_col_items, n_cols, (const MatItem*)p.d_mat_items, n_mats, W,
+                                 v_in, use_const_v, frob, iters, pb, p.d_vbuf, cache_out, p.d_sigma, p.d_status,
+                                 power_bar(p));
 }
 
 int launch_scale(Plan& p, const float* W, float* X0, void* stream) {
   if (p.power_items.empty()) return 0;
-  scale_kernel<<<(int)p.power_items.size(), 256, 0, (cudaStream_t)stream>>>(p.d_power_items, W, p.d_sigma, X0);
+  scale_kernel<<<(int)p.power_items.size(), 256, 0, (cudaStream_t)stream>>>(p.d_power_items, W, p.d_sigma, X0,
+                                                                            power_bar(p));
   p.launches++;
   return (int)cudaGetLastError();
 }

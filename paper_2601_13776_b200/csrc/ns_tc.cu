@@ -266,9 +266,12 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
 __global__ void __launch_bounds__(256) scale_bf16_kernel(const PowerItem* __restrict__ items,
                                                          const float* __restrict__ W, const float* __restrict__ sigma,
                                                          float* __restrict__ X0, NsBufs b, int par, int write_lo,
-                                                         unsigned* __restrict__ bars, int nbars) {
-  if (blockIdx.x == 0)   // re-arm the persistent NS group barriers (monotonic counters) for the launch that follows
+                                                         unsigned* __restrict__ bars, int nbars,
+                                                         unsigned* __restrict__ power_bar_p) {
+  if (blockIdx.x == 0) {   // re-arm the persistent NS group barriers and the fused power kernel's barrier
     for (int i = threadIdx.x; i < nbars; i += 256) bars[i] = 0u;
+    if (threadIdx.x == 0) *power_bar_p = 0u;
+  }
   const PowerItem it = items[blockIdx.x];
   const float inv = 1.f / sigma[it.mat];
   const int n = it.n, ldx = (n + 7) & ~7, g4 = ldx >> 2;
@@ -460,7 +463,7 @@ int launch_scale_bf16(Plan& p, const float* W, float* X0, int par, bool write_lo
   float* bufs[BUF_COUNT] = {X0, X0, nullptr, nullptr};
   NsBufs b = make_bufs(p, bufs);
   scale_bf16_kernel<<<(int)p.power_items.size(), 256, 0, (cudaStream_t)stream>>>(
-      p.d_power_items, W, p.d_sigma, X0, b, par, write_lo, p.nsp_bars, p.nsp_bars ? p.nsp_groups_n : 0);
+      p.d_power_items, W, p.d_sigma, X0, b, par, write_lo, p.nsp_bars, p.nsp_bars ? p.nsp_groups_n : 0, power_bar(p));
   p.launches++;
   return (int)cudaGetLastError();
 }

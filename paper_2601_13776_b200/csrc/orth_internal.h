@@ -105,15 +105,21 @@ struct NsGroup {           // per CTA: its barrier group and its own tile ranges
 };
 constexpr int kNspMaxPhases = 132;   // 2T + 1 for T <= 65
 
-struct PowerItem {        // one CTA of the pre-scaling kernels: rows [r0, r1) of matrix `mat`
-  int32_t mat, r0, r1, chunk;   // chunk: global partial slot
-  int32_t n, m;
-  int64_t off, cache_off, bx_off;
+struct PowerItem {        // row block of the pre-scaling / scale kernels: rows [r0, r1) of matrix `mat`
+  int32_t mat, r0, r1, chunk;   // chunk: global row-item slot (|t|^2 partial)
+  int32_t n, m, midx, pad_;     // midx: index into mat_items
+  int64_t off, cache_off, bx_off, t_off;   // t_off: the matrix's rows in the t buffer
 };
 
-struct MatItem {          // one owned, non-empty matrix (finalize / residual kernels)
-  int32_t mat, m, n, chunk0, nchunks, pad_;
-  int64_t off, cache_off, gram_off;
+struct ColItem {          // column block of the power kernel: w[c0:c1] = (W^T u)[c0:c1]
+  int32_t mat, c0, c1, chunk;   // chunk: global column-item slot (|w|^2 partial)
+  int32_t n, m, midx, pad_;
+  int64_t off, cache_off, t_off;
+};
+
+struct MatItem {          // one owned, non-empty matrix (power finalize / residual kernels)
+  int32_t mat, m, n, chunk0, nchunks, col0, ncols, pad_;   // row items [chunk0, +nchunks), column items [col0, +ncols)
+  int64_t off, cache_off, gram_off, t_off;
 };
 
 struct EmitItem {         // one (layer, group): copy the unit kernel into both layouts
@@ -175,6 +181,9 @@ struct Plan {
   int32_t nsp_ctas = 0, nsp_groups_n = 0;
   double nsp_est_us = 0.0;
   std::vector<PowerItem> power_items;
+  std::vector<ColItem> col_items;
+  ColItem* d_col_items = nullptr;
+  int64_t t_numel = 0;              // sum of rows: the power kernel's t = W v buffer
   std::vector<int32_t> owned_mats;  // indices of owned, non-empty matrices
   std::vector<MatItem> mat_items;   // same order as owned_mats
 
@@ -192,7 +201,7 @@ struct Plan {
   float* d_gram = nullptr;
   float* d_vbuf = nullptr;
   float* d_sigma = nullptr;
-  float* d_partial = nullptr;       // n_chunks * (max n + 1)
+  float* d_partial = nullptr;       // power kernel: [t (t_numel) | |t|^2 per row item | |w|^2 per column item]
   float* d_comp = nullptr;
   int32_t* d_status = nullptr;
   PowerItem* d_power_items = nullptr;
@@ -228,9 +237,12 @@ orth_status_t build_compose_tc(Plan& p);
 orth_status_t build_ns_tma(Plan& p);   // tensor maps of the NS operand copies; freed in destroy
 void free_compose_tc(Plan& p);
 int launch_compose_tc(Plan& p, const float* ortho, void* stream);   // fills comp (fp32) like the SIMT chain
-int launch_power_partial(Plan& p, const float* W, const float* v_in, int use_const_v, int frob, void* stream);
-int launch_power_finalize(Plan& p, float* v_out, int frob, int write_sigma_only, void* stream);
 int launch_scale(Plan& p, const float* W, float* X0, void* stream);
+// all power iterations (or the Frobenius pass) in one cooperative launch
+int launch_power_fused(Plan& p, const float* W, const float* v_in, int use_const_v, int frob, int iters,
+                       float* cache_out, void* stream);
+// the fused power kernel's grid-barrier counter (a word of the status block; re-armed by the scale kernels)
+inline unsigned* power_bar(Plan& p) { return reinterpret_cast<unsigned*>(p.d_status + 8); }
 int launch_residual(Plan& p, float* residual_out, void* stream);
 int launch_emit(Plan& p, const float* const bufs[BUF_COUNT], float* kf32, uint16_t* kbf16, void* stream);
 int launch_conv_fwd(const LayerInfo& L, const void* kernel, void* scratch, const float* bias, const void* x, void* y,

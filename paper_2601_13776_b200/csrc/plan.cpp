@@ -313,35 +313,51 @@ static void build_ns(Plan& P) {
   }
   P.ns_gram_tiles = tg;
   P.ns_upd_tiles = tu;
-  // pre-scaling work items: ~4 CTAs per SM in total, split by rows
+  // pre-scaling work items.  Row items (t = W v, and the scale kernels): ~8K
+  // elements each, <= 64 per matrix.  Column items (w = W^T u): >= 32 columns,
+  // ~8K elements each, <= 64 per matrix.  Every cross-item sum is taken in
+  // item order (deterministic).
   P.power_items.clear();
+  P.col_items.clear();
   P.mat_items.clear();
-  double tot = 0.0;
-  int64_t maxn = 1;
-  for (int i : P.owned_mats) { tot += (double)P.mats[i].m * P.mats[i].n; maxn = std::max(maxn, P.mats[i].n); }
-  int chunk = 0;
+  int chunk = 0, cchunk = 0;
+  int64_t t_off = 0;
   for (int i : P.owned_mats) {
     const MatInfo& M = P.mats[i];
-    // >= 32K elements per CTA, <= 64 partial chunks per matrix (finalize reduces them in order)
-    int64_t nc = std::min<int64_t>(64, (M.m * M.n + 32767) / 32768);
+    const int64_t rows_fit = std::max<int64_t>(1, 8192 / M.n);
+    int64_t nc = std::min<int64_t>(64, (M.m + rows_fit - 1) / rows_fit);
     nc = std::max<int64_t>(1, std::min<int64_t>(nc, M.m));
-    nc = std::max<int64_t>(nc, (M.m + 4095) / 4096);                                   // <= 4096 rows per CTA
     const int64_t rpc = (M.m + nc - 1) / nc;
+    int64_t cpc = std::max<int64_t>(32, (8192 / std::max<int64_t>(M.m, 1)) / 32 * 32);
+    cpc = std::max<int64_t>(cpc, pad_up((M.n + 63) / 64, 32));
     MatItem mi{};
-    mi.mat = i; mi.m = (int32_t)M.m; mi.n = (int32_t)M.n; mi.chunk0 = chunk;
-    mi.off = M.off; mi.cache_off = M.cache_off; mi.gram_off = M.gram_off;
+    mi.mat = i; mi.m = (int32_t)M.m; mi.n = (int32_t)M.n; mi.chunk0 = chunk; mi.col0 = cchunk;
+    mi.off = M.off; mi.cache_off = M.cache_off; mi.gram_off = M.gram_off; mi.t_off = t_off;
+    const int midx = (int)P.mat_items.size();
     for (int64_t r0 = 0; r0 < M.m; r0 += rpc) {
       PowerItem it{};
       it.mat = i; it.r0 = (int32_t)r0; it.r1 = (int32_t)std::min<int64_t>(M.m, r0 + rpc); it.chunk = chunk++;
-      it.n = (int32_t)M.n; it.m = (int32_t)M.m; it.off = M.off; it.cache_off = M.cache_off; it.bx_off = M.bx_off;
+      it.n = (int32_t)M.n; it.m = (int32_t)M.m; it.midx = midx;
+      it.off = M.off; it.cache_off = M.cache_off; it.bx_off = M.bx_off; it.t_off = t_off;
       P.power_items.push_back(it);
     }
+    for (int64_t c0 = 0; c0 < M.n; c0 += cpc) {
+      ColItem ci{};
+      ci.mat = i; ci.c0 = (int32_t)c0; ci.c1 = (int32_t)std::min<int64_t>(M.n, c0 + cpc); ci.chunk = cchunk++;
+      ci.n = (int32_t)M.n; ci.m = (int32_t)M.m; ci.midx = midx;
+      ci.off = M.off; ci.cache_off = M.cache_off; ci.t_off = t_off;
+      P.col_items.push_back(ci);
+    }
     mi.nchunks = chunk - mi.chunk0;
+    mi.ncols = cchunk - mi.col0;
     P.mat_items.push_back(mi);
+    t_off += M.m;
   }
   P.n_chunks = chunk;
-  P.partial_stride = pad_up(maxn + 1, kPadF32);
-  P.partial_numel = std::max<int64_t>((int64_t)chunk * P.partial_stride, kPadF32);
+  P.t_numel = t_off;
+  P.partial_stride = 0;
+  P.partial_numel = std::max<int64_t>(pad_up(t_off, kPadF32) + pad_up(chunk, kPadF32) + pad_up(cchunk, kPadF32),
+                                      kPadF32);
 }
 
 // Composition phases (a4/a5).  Workspace (BUF_W): projectors, per-unit chain
@@ -501,6 +517,7 @@ static orth_status_t allocate(Plan& P) {
   const size_t o_comp = take(P.comp_numel * 4), o_stat = take(64);
   const size_t o_pi = take(std::max<size_t>(P.power_items.size(), 1) * sizeof(PowerItem));
   const size_t o_own = take(std::max<size_t>(P.mat_items.size(), 1) * sizeof(MatItem));
+  const size_t o_col = take(std::max<size_t>(P.col_items.size(), 1) * sizeof(ColItem));
   const size_t o_emit = take(std::max<size_t>(P.emit.size(), 1) * sizeof(EmitItem));
   const size_t o_nsg = take(std::max<size_t>(P.ns_gram.size(), 1) * sizeof(NsDesc));
   const size_t o_nsu = take(std::max<size_t>(P.ns_upd.size(), 1) * sizeof(NsDesc));
@@ -532,6 +549,7 @@ static orth_status_t allocate(Plan& P) {
   P.d_status = (int32_t*)(base + o_stat);
   P.d_power_items = (PowerItem*)(base + o_pi);
   P.d_mat_items = (MatItem*)(base + o_own);
+  P.d_col_items = (ColItem*)(base + o_col);
   P.d_emit = (EmitItem*)(base + o_emit);
   P.d_ns_gram = (NsDesc*)(base + o_nsg);
   P.d_ns_upd = (NsDesc*)(base + o_nsu);
@@ -547,6 +565,8 @@ static orth_status_t allocate(Plan& P) {
     e = cudaMemcpy(P.d_power_items, P.power_items.data(), P.power_items.size() * sizeof(PowerItem), cudaMemcpyHostToDevice);
   if (!P.mat_items.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_mat_items, P.mat_items.data(), P.mat_items.size() * sizeof(MatItem), cudaMemcpyHostToDevice);
+  if (!P.col_items.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_col_items, P.col_items.data(), P.col_items.size() * sizeof(ColItem), cudaMemcpyHostToDevice);
   if (!P.emit.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_emit, P.emit.data(), P.emit.size() * sizeof(EmitItem), cudaMemcpyHostToDevice);
   for (size_t i = 0; i < phases.size() && e == cudaSuccess; ++i) {

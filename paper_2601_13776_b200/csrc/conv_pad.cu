@@ -1,0 +1,517 @@
+// a6 (forward orthogonal convolution) on the tensor cores for stride-1
+// layers, with the A operand brought in by TMA and reused across taps.
+//
+// Output pixels of a tile are TH rows of one image with row pitch P (a
+// multiple of 8, >= Wo): MMA row r <-> output (h0 + r / P, r % P); columns
+// past Wo are computed and discarded.  Per 64-channel chunk the tile's input
+// window is loaded as k column-shifted copies (one per tap column b), each
+// R = TH + d (k - 1) rows x P pixels in the pitch-P SWIZZLE_128B row layout:
+//     C_b[y * P + x] = x~[h0 - p_t + y, x - p_l + d b],   y < R, x < P
+// (zero padding: one 4-D TMA box per copy, out of bounds zero-filled;
+// circular padding: per input row the two wrapped pieces of each copy).  The
+// A operand of tap (a, b) is the 128 consecutive rows of C_b starting at row
+// d a P -- a multiple of 8, so every UMMA descriptor start stays on a
+// 1024-byte swizzle atom.  (Starting inside an atom is numerically fine -- the
+// tensor core swizzles on absolute address bits -- but measured ~4.7x slower
+// per MMA on B200, so the b shift is done by the TMA copy instead.)
+// A bytes per chunk: k R P rows instead of k^2 * 128 gathered rows.
+//
+// B (weights): when all k^2 taps x 64-channel chunks of one (group, n-tile)
+// fit next to the A ring (narrow layers), they are loaded ONCE per CTA and stay
+// resident; each CTA then walks a contiguous range of tiles in (group, n-tile)
+// major order, reloading only when the range crosses into the next set.
+// Otherwise B streams per tap through a TMA ring.
+//
+// Warp roles (256 threads, one CTA per SM, persistent over tiles):
+//   warp 0      A producer: TMA of the tile window into a ring of A buffers
+//   warp 1      B producer: TMA of the weight tile (BN rows x 64 ch, one tap)
+//   warp 2      TMEM allocation + the single-thread tcgen05.mma issuer
+//   warps 4-7   epilogue: TMEM -> bias -> BF16 NHWC stores (one row per thread)
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "orth_internal.h"
+#include "tma_host.h"
+#include "umma.cuh"
+
+#ifdef ORTH_CONV_TRACE
+// diagnostics: per CTA, per tile (first 32) globaltimer stamps
+//   [0] A issued, [1] MMA saw A landed, [2] epilogue saw accumulator, [3] epilogue done
+__device__ unsigned long long conv_trace[160 * 32 * 4];
+__device__ __forceinline__ void ctrace(int tcount, int q) {
+  if (tcount < 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    conv_trace[(blockIdx.x * 32 + tcount) * 4 + q] = t;
+  }
+}
+#define CTRACE(tc, q) ctrace(tc, q)
+#else
+#define CTRACE(tc, q)
+#endif
+
+namespace orth {
+namespace {
+
+struct PadArgs {
+  int N, H, W, Ho, Wo, k, d, pt, pl, pr, circ;
+  int out_C, cr_g, nout_g;
+  int P, TH, R;                  // padded pitch, output rows per tile, input rows per tile
+  int tiles_h, tiles_m, tiles_n, num_tiles;
+  int abuf_bytes, nabuf, sb;     // A ring (nabuf buffers), B ring stages
+  int copy_bytes;                // one column-shifted copy: R * P * 128
+  int a_tx;                      // bytes landed per A buffer (k copies)
+  // circular padding: per copy b, up to two row pieces (map index, input column start, smem column, width)
+  int pc_map[2 * 7], pc_col[2 * 7], pc_dst[2 * 7], npc[7];
+  int bres;                      // 1: all taps x chunks of one (group, n-tile) resident in smem
+  int tiles_per_cta;             // resident mode: contiguous tile range per CTA (set-major order)
+};
+
+constexpr int A_WARP = 0, B_WARP = 1, MMA_WARP = 2, EPI_WARP0 = 4;
+constexpr int NTHREADS = 8 * 32;
+constexpr int MAX_SB = 16;
+constexpr int MAX_AB = 4;
+
+__device__ __forceinline__ int wrapi(int x, int n) {
+  x %= n;
+  return x < 0 ? x + n : x;
+}
+
+// zero padding: [0] = the R x P window box; circular: one row box per distinct piece width
+constexpr int MAX_MAPS = 8;
+struct PadMaps {
+  CUtensorMap m[MAX_MAPS];
+};
+
+template <int BN>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    conv_pad(const float* __restrict__ bias, __nv_bfloat16* __restrict__ out, const __grid_constant__ PadArgs a,
+             const __grid_constant__ PadMaps tmA, const __grid_constant__ CUtensorMap tmB) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int B_BYTES = BN * 128;
+  __shared__ uint64_t a_full[MAX_AB], a_empty[MAX_AB], b_full[MAX_SB], b_empty[MAX_SB], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int SB = a.sb, NA = a.nabuf;
+  if (warp == MMA_WARP) umma::tmem_alloc(&tmem_base_sh, 2 * BN);
+  if (tid == 0) {
+    for (int i = 0; i < NA; ++i) {
+      umma::mbar_init(&a_full[i], 1);
+      umma::mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < SB; ++i) {
+      umma::mbar_init(&b_full[i], 1);
+      umma::mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      umma::mbar_init(&tfull_bar[i], 1);
+      umma::mbar_init(&tempty_bar[i], 128);
+    }
+    umma::fence_mbar_init();
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t abase = umma::smem_u32(smem);
+  const uint32_t bbase = abase + NA * a.abuf_bytes;
+  const int kk2 = a.k * a.k;
+
+  auto decode = [&](int tile, int& n, int& h0, int& g, int& n0) {
+    const int tm = tile % a.tiles_m, rest = tile / a.tiles_m;
+    n0 = (rest % a.tiles_n) * BN;
+    g = rest / a.tiles_n;
+    n = tm / a.tiles_h;
+    h0 = (tm - n * a.tiles_h) * a.TH;
+  };
+  // tile schedule: streaming B -> grid-stride; resident B -> a contiguous range per CTA
+  const int t_begin = a.bres ? blockIdx.x * a.tiles_per_cta : blockIdx.x;
+  const int t_end = a.bres ? min(a.num_tiles, t_begin + a.tiles_per_cta) : a.num_tiles;
+  const int t_step = a.bres ? 1 : gridDim.x;
+  const int bset_bytes = ((a.cr_g + 63) / 64) * kk2 * B_BYTES;
+
+  if (warp == A_WARP) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- A producer
+      umma::tma_prefetch_desc(&tmA.m[0]);
+      int u = 0, tc_a = 0;
+      for (int tile = t_begin; tile < t_end; tile += t_step, ++tc_a) {
+        int n, h0, g, n0;
+        decode(tile, n, h0, g, n0);
+        for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
+          const int ab = u % NA;
+          if (u >= NA) umma::mbar_wait(&a_empty[ab], ((u / NA) - 1) & 1);
+          if (c0 == 0) CTRACE(tc_a, 0);
+          const uint32_t dst = abase + ab * a.abuf_bytes;
+          const int c = g * a.cr_g + c0;
+          umma::mbar_arrive_expect_tx(&a_full[ab], (uint32_t)a.a_tx);
+          for (int b = 0; b < a.k; ++b) {
+            const uint32_t cb = dst + (uint32_t)(b * a.copy_bytes);
+            if (!a.circ) {   // one box: R rows x P pixels x 64 channels; out of bounds -> 0
+              umma::tma_load_4d(cb, &tmA.m[0], &a_full[ab], c, a.d * b - a.pl, h0 - a.pt, n);
+            } else {
+              for (int y = 0; y < a.R; ++y) {
+                const int h = wrapi(h0 - a.pt + y, a.H);
+                const uint32_t row = cb + (uint32_t)(y * a.P) * 128u;
+                for (int pc = 0; pc < a.npc[b]; ++pc)
+                  umma::tma_load_4d(row + (uint32_t)a.pc_dst[2 * b + pc] * 128u, &tmA.m[a.pc_map[2 * b + pc]],
+                                    &a_full[ab], c, a.pc_col[2 * b + pc], h, n);
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == B_WARP) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- B producer
+      umma::tma_prefetch_desc(&tmB);
+      int i = 0, cur = -1, loads = 0;
+      for (int tile = t_begin; tile < t_end; tile += t_step) {
+        int n, h0, g, n0;
+        decode(tile, n, h0, g, n0);
+        if (a.bres) {   // whole (group, n-tile) weight set, once per set change
+          const int set = tile / a.tiles_m;
+          if (set == cur) continue;
+          if (loads > 0) umma::mbar_wait(&b_empty[0], (loads - 1) & 1);   // MMAs on the old set done
+          cur = set;
+          umma::mbar_arrive_expect_tx(&b_full[0], (uint32_t)bset_bytes);
+          int j = 0;
+          for (int c0 = 0; c0 < a.cr_g; c0 += 64)
+            for (int tap = 0; tap < kk2; ++tap, ++j)
+              umma::tma_load_3d(bbase + j * B_BYTES, &tmB, &b_full[0], c0, tap, g * a.nout_g + n0);
+          ++loads;
+          continue;
+        }
+        for (int c0 = 0; c0 < a.cr_g; c0 += 64)
+          for (int tap = 0; tap < kk2; ++tap, ++i) {
+            const int st = i % SB;
+            if (i >= SB) umma::mbar_wait(&b_empty[st], ((i / SB) - 1) & 1);
+            umma::mbar_arrive_expect_tx(&b_full[st], B_BYTES);
+            umma::tma_load_3d(bbase + st * B_BYTES, &tmB, &b_full[st], c0, tap, g * a.nout_g + n0);
+          }
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- MMA issuer
+      constexpr uint32_t IDESC = umma::idesc_bf16(128, BN);
+      int u = 0, i = 0, tcount = 0, cur = -1, loads = 0;
+      for (int tile = t_begin; tile < t_end; tile += t_step, ++tcount) {
+        if (a.bres) {
+          const int set = tile / a.tiles_m;
+          if (set != cur) {
+            if (loads > 0) umma::mma_commit(&b_empty[0]);   // release the old set once its MMAs finish
+            umma::mbar_wait(&b_full[0], loads & 1);
+            cur = set;
+            ++loads;
+          }
+        }
+        const int acc = tcount & 1;
+        umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
+        umma::tc_fence_after();
+        const uint32_t d_tmem = tmem + acc * BN;
+        int j = 0;   // resident: index of (chunk, tap) in the set
+        for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
+          const int ab = u % NA;
+          umma::mbar_wait(&a_full[ab], (u / NA) & 1);
+          umma::tc_fence_after();
+          if (c0 == 0) CTRACE(tcount, 1);
+          const uint32_t abuf = abase + ab * a.abuf_bytes;
+          for (int tap = 0; tap < kk2; ++tap, ++j) {
+            int st = 0;
+            if (!a.bres) {
+              st = i % SB;
+              umma::mbar_wait(&b_full[st], (i / SB) & 1);
+              umma::tc_fence_after();
+            }
+            const int ta = tap / a.k, tb = tap - ta * a.k;
+            const uint32_t aa = abuf + (uint32_t)(tb * a.copy_bytes) + (uint32_t)(a.d * ta * a.P) * 128u;
+            const uint32_t bb = bbase + (a.bres ? j : st) * B_BYTES;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              umma::mma_bf16(d_tmem, umma::sdesc_sw128(aa + 32 * q), umma::sdesc_sw128(bb + 32 * q), IDESC,
+                             (c0 | tap | q) != 0);
+            if (!a.bres) {
+              umma::mma_commit(&b_empty[st]);
+              ++i;
+            }
+          }
+          umma::mma_commit(&a_empty[ab]);
+        }
+        umma::mma_commit(&tfull_bar[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= EPI_WARP0) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int y = r / a.P, x = r - y * a.P;   // P % 8 == 0 keeps this cheap
+    int tcount = 0;
+    for (int tile = t_begin; tile < t_end; tile += t_step, ++tcount) {
+      int n, h0, g, n0;
+      decode(tile, n, h0, g, n0);
+      const int opix = (y < a.TH && x < a.Wo && h0 + y < a.Ho) ? (n * a.Ho + h0 + y) * a.Wo + x : -1;
+      const int acc = tcount & 1;
+      umma::mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
+      umma::tc_fence_after();
+      if (q == 0 && lane == 0) CTRACE(tcount, 2);
+      const int obase = g * a.nout_g + n0;
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 32) {
+        float v[32];
+        umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + cc), v);
+        if (opix >= 0) {
+          const int o = obase + cc;
+          uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)opix * a.out_C + o);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              float v0 = v[8 * i + 2 * jj], v1 = v[8 * i + 2 * jj + 1];
+              if (bias) { v0 += bias[o + 8 * i + 2 * jj]; v1 += bias[o + 8 * i + 2 * jj + 1]; }
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
+              pk[jj] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            dst[i] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        }
+      }
+      umma::tc_fence_before();
+      umma::mbar_arrive(&tempty_bar[acc]);
+      if (q == 0 && lane == 0) CTRACE(tcount, 3);
+    }
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) umma::tmem_dealloc(tmem, 2 * BN);
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+constexpr size_t kSmemMax = 227 * 1024 - 1024;   // opt-in dynamic limit minus the static barriers
+
+// 4-D map over the NHWC activation (C, W, H, N): box 64 ch x bw pixels x bh rows x 1 image, SWIZZLE_128B
+bool make_act_tmap(CUtensorMap* out, const void* x, int C, int W, int H, int N, int bw, int bh) {
+  using Key = std::tuple<const void*, int, int, int, int, int, int>;
+  static std::map<Key, CUtensorMap> cache;
+  static std::mutex mu;
+  const Key key{x, C, W, H, N, bw, bh};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return true;
+    }
+  }
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  const cuuint32_t box[4] = {64, (cuuint32_t)bw, (cuuint32_t)bh, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache[key] = m;
+  *out = m;
+  return true;
+}
+
+template <int BN>
+int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out, PadArgs& a,
+               int in_C, cudaStream_t stream) {
+  const size_t fixed = 1024;
+  const size_t bset = (size_t)((a.cr_g + 63) / 64) * a.k * a.k * BN * 128;
+  size_t smem;
+  if (a.bres) {   // resident weights + >= 2 A buffers (caller checked the fit)
+    int na = MAX_AB;
+    while (na > 2 && fixed + (size_t)na * a.abuf_bytes + bset > kSmemMax) --na;
+    a.nabuf = na;
+    a.sb = 1;
+    const int grid0 = std::min(a.num_tiles, sm_count());
+    a.tiles_per_cta = (a.num_tiles + grid0 - 1) / grid0;
+    smem = fixed + (size_t)na * a.abuf_bytes + bset;
+  } else {
+    // A ring: as many buffers as leave room for >= 4 B stages (at least 2)
+    int na = MAX_AB;
+    while (na > 2 && fixed + (size_t)na * a.abuf_bytes + 4 * (size_t)BN * 128 > kSmemMax) --na;
+    if (fixed + (size_t)na * a.abuf_bytes + 2 * (size_t)BN * 128 > kSmemMax) return -1;
+    a.nabuf = na;
+    a.sb = (int)std::min<size_t>(MAX_SB, (kSmemMax - fixed - (size_t)na * a.abuf_bytes) / ((size_t)BN * 128));
+    smem = fixed + (size_t)na * a.abuf_bytes + (size_t)a.sb * BN * 128;
+  }
+  static size_t attr = 0;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(conv_pad<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return (int)cudaGetLastError();
+    attr = smem;
+  }
+  PadMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  if (!a.circ) {
+    if (!make_act_tmap(&maps.m[0], x, in_C, a.W, a.H, a.N, a.P, a.R)) return (int)cudaErrorInvalidValue;
+  } else {   // one row box per distinct piece width
+    int widths[MAX_MAPS], nw = 0;
+    for (int b = 0; b < a.k; ++b)
+      for (int pc = 0; pc < a.npc[b]; ++pc) {
+        const int w0 = a.pc_map[2 * b + pc];   // host stored the width here; replaced by the map index
+        int m = 0;
+        while (m < nw && widths[m] != w0) ++m;
+        if (m == nw) {
+          if (nw == MAX_MAPS) return -1;
+          widths[nw++] = w0;
+          if (!make_act_tmap(&maps.m[m], x, in_C, a.W, a.H, a.N, w0, 1)) return (int)cudaErrorInvalidValue;
+        }
+        a.pc_map[2 * b + pc] = m;
+      }
+  }
+  CUtensorMap tm;
+  if (!make_weight_tmap(&tm, w, w_rows, a.k * a.k, a.cr_g, BN)) return (int)cudaErrorInvalidValue;
+  const int grid = a.bres ? (a.num_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta
+                         : (a.num_tiles < sm_count() ? a.num_tiles : sm_count());
+  conv_pad<BN><<<grid, NTHREADS, smem, stream>>>(bias, out, a, maps, tm);
+#ifdef ORTH_CONV_TRACE
+  {
+    cudaStreamSynchronize(stream);
+    static unsigned long long h[160 * 32 * 4];
+    cudaMemcpyFromSymbol(h, conv_trace, sizeof(h));
+    double d01 = 0, d12 = 0, d23 = 0, per = 0;
+    int cnt = 0, cnt2 = 0;
+    for (int c = 0; c < grid && c < 160; ++c)
+      for (int t = 1; t < 16; ++t) {
+        const unsigned long long* r = &h[(c * 32 + t) * 4];
+        const unsigned long long* r0 = &h[(c * 32 + t - 1) * 4];
+        if (!r[0] || !r[3] || !r0[3]) continue;
+        d01 += (double)(r[1] - r[0]); d12 += (double)(r[2] - r[1]); d23 += (double)(r[3] - r[2]);
+        per += (double)(r[3] - r0[3]);
+        ++cnt;
+      }
+    (void)cnt2;
+    if (cnt)
+      std::printf("conv_pad BN=%d bres=%d TH=%d P=%d R=%d na=%d sb=%d tiles=%d grid=%d: A issue->landed %.2f, ->acc ready %.2f, epi %.2f, per-tile %.2f us\n",
+                  BN, a.bres, a.TH, a.P, a.R, a.nabuf, a.sb, a.num_tiles, grid, d01 / cnt * 1e-3, d12 / cnt * 1e-3,
+                  d23 / cnt * 1e-3, per / cnt * 1e-3);
+    cudaMemset(conv_trace, 0, 0);
+    static unsigned long long z[160 * 32 * 4];
+    cudaMemcpyToSymbol(conv_trace, z, sizeof(z));
+  }
+#endif
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+// Plan the padded-row path for a (possibly group-packed) forward layer; false
+// if it does not apply (stride != 1, rows wider than one tile, channel slices
+// that would cross groups, circular padding that is not a single wrap, ...).
+static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, int& bn, PadArgs& a) {
+  const int ext = L.d * (L.k - 1);
+  // measured (B200, cfg2/cfg3): the TMA-window path wins for narrow layers (co_g <= 64: 97 -> 74 us
+  // at 64ch@32, 280 -> 235 us at 64ch@56); for co_g >= 128 the per-tap gather kernel is as fast or
+  // faster (its N >= 128 MMAs are not smem-bound), so those stay on conv_tc.cu
+  if (L.s != 1 || Wo > 128 || Wo < 16 || L.k > 7 || L.co > 64) return false;
+  if (L.g > 1 && L.ci % 64 != 0) return false;          // a 64-channel box must stay inside the group
+  if (L.ci_f % 8 != 0) return false;                     // TMA row stride: multiple of 16 bytes
+  const bool circ = L.desc.padding_mode == ORTH_PAD_CIRCULAR;
+  const int pr = ext - L.pl;
+  // circular: the copy rows are the wrapped input rows (P = W, so W % 8 == 0); zero: P = round8(Wo)
+  if (circ && (L.pl < 0 || pr < 0 || Wo != W || W % 8 != 0)) return false;
+  const int P = circ ? W : (Wo + 7) & ~7;
+  if (P > 128) return false;
+  const int TH = std::min(Ho, 128 / P);
+  if (TH < 1 || TH * Wo < 64) return false;
+  const int R = TH + ext;
+  if (R > 256) return false;
+  const int n = L.co;
+  bn = n % 256 == 0 ? 256 : n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : n % 32 == 0 ? 32 : 0;
+  if (!bn) return false;
+  const int copy_bytes = R * P * 128;
+  // the last copy's windows read rows up to d (k - 1) P + 127 past its start
+  const int slack_rows = std::max(0, ext * P + 128 - R * P);
+  const size_t abuf = (size_t)L.k * copy_bytes + (size_t)slack_rows * 128;
+  // resident weights: the largest BN (<= 128, dividing co, >= co / 4 so A is re-read at most 4x)
+  // whose whole tap x chunk set fits next to two A buffers
+  const size_t kc = (size_t)(L.ci + 63) / 64;
+  int bres_bn = 0;
+  for (int b = 128; b >= 64 && b * 4 >= n; b /= 2)   // N = 32 MMAs cost as much as N = 128 ones
+    if (n % b == 0 && 1024 + 2 * abuf + kc * L.k * L.k * b * 128 <= kSmemMax) { bres_bn = b; break; }
+  static const bool no_res = std::getenv("ORTH_CONV_NO_BRES") != nullptr;   // A/B switch
+  if (bres_bn && !no_res) bn = bres_bn;
+  if (!bres_bn || no_res) {   // streaming B needs two A buffers + a few B stages
+    if (1024 + 2 * abuf + 2 * (size_t)bn * 128 > kSmemMax) return false;
+  }
+  a = PadArgs{};
+  a.bres = (bres_bn && !no_res) ? 1 : 0;
+  a.N = N; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo;
+  a.k = L.k; a.d = L.d; a.pt = L.pt; a.pl = L.pl; a.pr = pr;
+  a.circ = circ;
+  a.out_C = L.co_f; a.cr_g = L.ci; a.nout_g = L.co;
+  a.P = P; a.TH = TH; a.R = R;
+  a.tiles_h = (Ho + TH - 1) / TH;
+  a.tiles_m = N * a.tiles_h;
+  a.tiles_n = n / bn;
+  a.num_tiles = a.tiles_m * a.tiles_n * L.g;
+  a.copy_bytes = copy_bytes;
+  a.abuf_bytes = (int)abuf;
+  a.a_tx = L.k * copy_bytes;
+  if (circ) {   // copy b covers input columns (x - p_l + d b) mod W, x < W: pieces [s, W) then [0, s)
+    for (int b = 0; b < L.k; ++b) {
+      const int s0 = ((L.d * b - L.pl) % W + W) % W;
+      int np = 0;
+      a.pc_col[2 * b] = s0; a.pc_dst[2 * b] = 0; a.pc_map[2 * b] = W - s0; ++np;   // pc_map: width for now
+      if (s0 > 0) { a.pc_col[2 * b + 1] = 0; a.pc_dst[2 * b + 1] = W - s0; a.pc_map[2 * b + 1] = s0; ++np; }
+      a.npc[b] = np;
+    }
+  }
+  return true;
+}
+
+// returns -1 when the padded-row path does not apply (caller falls back), else 0 / a CUDA error
+int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
+                          int H, int W, int Ho, int Wo, void* stream) {
+  int bn = 0;
+  PadArgs a;
+  if (!pad_args(L, N, H, W, Ho, Wo, bn, a)) return -1;
+  if (a.num_tiles == 0) return 0;
+  if (((uintptr_t)x & 15) != 0) return -1;
+  const auto* w = static_cast<const __nv_bfloat16*>(kernel);
+  auto* out = static_cast<__nv_bfloat16*>(y);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (bn) {
+    case 32: return launch_pad<32>(x, w, L.co_f, bias, out, a, L.ci_f, s);
+    case 64: return launch_pad<64>(x, w, L.co_f, bias, out, a, L.ci_f, s);
+    case 128: return launch_pad<128>(x, w, L.co_f, bias, out, a, L.ci_f, s);
+    default: return launch_pad<256>(x, w, L.co_f, bias, out, a, L.ci_f, s);
+  }
+}
+
+}  // namespace orth

@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "orth_internal.h"
 #include "tma_host.h"
@@ -455,6 +456,11 @@ int launch_conv_fwd_tc(const LayerInfo& L0, const void* kernel, void* scratch, c
   if (P > 1) {
     if (int e = pack_weights(L0, P, kernel, scratch, (cudaStream_t)stream)) return e;
     kernel = scratch;
+  }
+  static const bool no_reuse = std::getenv("ORTH_CONV_NO_REUSE") != nullptr;   // A/B switch
+  if (!no_reuse) {   // stride-1 layers on wide images: shifted-copy A reuse (conv_reuse.cu)
+    const int e = launch_conv_fwd_reuse(L, kernel, bias, x, y, N, H, W, Ho, Wo, stream);
+    if (e >= 0) return e;
   }
   TcConvArgs a;
   base_args(a, L, N, H, W, Ho, Wo);

@@ -225,6 +225,9 @@ int launch_residual_r(Plan& p, float* residual_out, void* stream);
 // the epilogue also writes the lo halves of its BF16 outputs.
 int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int npass, bool write_lo, bool write_f,
                  void* stream);
+// forward conv with shifted-copy A reuse (stride 1, wide images); -1 = not applicable
+int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
+                          int H, int W, int Ho, int Wo, void* stream);
 // persistent NS: build the CTA-group partition (after build_ns_tma); launch all
 // phases (flags per phase: bit0 gram, bit1 3-pass, bit2 X parity, bit3 write lo,
 // bit4 write fp32 R)

@@ -167,6 +167,15 @@ CONV_CASES = [  # (ci, co, k, s, d, g, mode, H, kind)
     (64, 64, 3, 1, 2, 2, "circular", 12, "convT"), (256, 256, 3, 1, 1, 8, "circular", 8, "conv"),
     (64, 128, 4, 2, 1, 1, "zeros", 10, "convT"), (96, 96, 5, 3, 2, 3, "circular", 12, "conv"),
     (64, 128, 3, 2, 1, 1, "zeros", 9, "conv"), (1024, 1024, 3, 1, 2, 32, "circular", 6, "convT"),
+    # stride-1 shifted-copy A-reuse path (TH x Wo tiles >= 96 rows; ragged Wo: descriptor starts inside a swizzle atom)
+    (64, 64, 3, 1, 1, 1, "zeros", 16, "conv"), (128, 128, 3, 1, 1, 1, "circular", 16, "conv"),
+    (64, 128, 3, 1, 1, 1, "circular", 32, "conv"), (32, 32, 3, 1, 1, 2, "circular", 16, "conv"),
+    (256, 256, 3, 1, 1, 1, "zeros", 12, "conv"), (64, 64, 5, 1, 1, 1, "circular", 20, "conv"),
+    (64, 64, 3, 1, 3, 1, "zeros", 14, "conv"), (192, 64, 3, 1, 1, 1, "circular", 11, "conv"),
+    # TMA-window path (conv_pad.cu: co_g <= 64, Wo >= 16): resident / streamed weights, channel tails
+    (64, 64, 3, 1, 1, 1, "circular", 24, "conv"), (64, 64, 5, 1, 2, 1, "zeros", 20, "conv"),
+    (48, 64, 3, 1, 1, 1, "circular", 16, "conv"), (128, 64, 3, 1, 1, 1, "circular", 16, "conv"),
+    (64, 32, 3, 1, 1, 1, "zeros", 33, "conv"),
 ]
 
 

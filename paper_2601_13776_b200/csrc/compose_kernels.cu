@@ -4,11 +4,14 @@
 // Sources: tap-major chain/AOC results (slice [:co, :ci] of width ld, P:321
 // BCOP slicing, R5) or the RKO reshape R.reshape(co, ci, s, s) (R7).
 //
-// One output row o per iteration: the row's k^2 x ci slab is staged in shared
-// memory (coalesced reads along ci), then written coalesced in both layouts.
+// CTA = output rows o = blockIdx.x + k gridDim.x of item blockIdx.y; thread =
+// input channel i: reads the k^2 taps of (o, i) (coalesced across i), writes
+// the BF16 GEMM row [o][t][i] (coalesced) and the FP32 PyTorch row [o][i][t]
+// (k^2 consecutive floats per thread, contiguous across the warp).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "orth_internal.h"
@@ -16,33 +19,43 @@
 namespace orth {
 namespace {
 
-__global__ void __launch_bounds__(256) emit_kernel(const EmitItem* __restrict__ items, const float* b0,
+__global__ void __launch_bounds__(128) emit_kernel(const EmitItem* __restrict__ items, const float* b0,
                                                    const float* b1, const float* b2, const float* b3,
                                                    float* __restrict__ kf32, __nv_bfloat16* __restrict__ kbf16) {
-  extern __shared__ float buf[];   // [k^2][ci + 1]
+  extern __shared__ float row_sm[];   // one FP32 output row [i][t] (k^2 ci floats)
   const EmitItem e = items[blockIdx.y];
-  const float* bufs[4] = {b0, b1, b2, b3};
-  const float* src = bufs[e.src_buf] + e.src_off;
-  const int kk = e.k * e.k, ci = e.ci, ld1 = ci + 1;
+  const float* base = e.src_buf == 0 ? b0 : e.src_buf == 1 ? b1 : e.src_buf == 2 ? b2 : b3;
+  const float* src = base + e.src_off;
+  const int kk = e.k * e.k, ci = e.ci;
   const int slab = kk * ci;
   for (int o = blockIdx.x; o < e.co; o += gridDim.x) {
-    if (e.mode == 1) {   // RKO: K[o, i, t] = R[o, i*s^2 + t]  (k = s)
+    float* f = kf32 + e.f32_off + (int64_t)o * slab;
+    __nv_bfloat16* bq = kbf16 ? kbf16 + e.bf16_off + (int64_t)o * slab : nullptr;
+    if (e.mode == 1) {   // RKO: K[o, i, t] = R[o, i*s^2 + t] (k = s): the FP32 row is a straight copy
       const float* row = src + (int64_t)o * slab;
-      for (int x = threadIdx.x; x < slab; x += blockDim.x) buf[(x % kk) * ld1 + x / kk] = row[x];
-    } else {             // tap-major: K[o, i, t] = src[t*tap_stride + o*ld + i]
-      for (int x = threadIdx.x; x < slab; x += blockDim.x) {
-        const int t = x / ci, i = x % ci;
-        buf[t * ld1 + i] = src[(int64_t)t * e.tap_stride + (int64_t)o * e.ld + i];
+      for (int x = threadIdx.x; x < slab; x += 128) f[x] = __ldg(row + x);
+      if (bq)
+        for (int i = threadIdx.x; i < ci; i += 128)
+          for (int t = 0; t < kk; ++t) bq[(int64_t)t * ci + i] = __float2bfloat16_rn(__ldg(row + i * kk + t));
+      continue;
+    }
+    // tap-major: K[o, i, t] = src[t*tap_stride + o*ld + i]; stage [i][t] (stride k^2, odd -> conflict-free)
+    __syncthreads();
+    for (int i = threadIdx.x; i < ci; i += 128) {
+      const float* col = src + (int64_t)o * e.ld + i;
+      for (int t = 0; t < kk; ++t) {
+        const float v = __ldg(col + (int64_t)t * e.tap_stride);
+        row_sm[i * kk + t] = v;
+        if (bq) bq[(int64_t)t * ci + i] = __float2bfloat16_rn(v);
       }
     }
     __syncthreads();
-    float* f = kf32 + e.f32_off + (int64_t)o * slab;
-    for (int x = threadIdx.x; x < slab; x += blockDim.x) f[x] = buf[(x % kk) * ld1 + x / kk];   // (i, t)
-    if (kbf16) {
-      __nv_bfloat16* b = kbf16 + e.bf16_off + (int64_t)o * slab;
-      for (int x = threadIdx.x; x < slab; x += blockDim.x) b[x] = __float2bfloat16_rn(buf[(x / ci) * ld1 + x % ci]);
+    if ((slab & 3) == 0 && ((reinterpret_cast<uintptr_t>(f) & 15) == 0)) {
+      for (int x = threadIdx.x; x < slab / 4; x += 128)
+        reinterpret_cast<float4*>(f)[x] = reinterpret_cast<const float4*>(row_sm)[x];
+    } else {
+      for (int x = threadIdx.x; x < slab; x += 128) f[x] = row_sm[x];
     }
-    __syncthreads();
   }
 }
 
@@ -51,20 +64,19 @@ __global__ void __launch_bounds__(256) emit_kernel(const EmitItem* __restrict__ 
 int launch_emit(Plan& p, const float* const bufs[BUF_COUNT], float* kf32, uint16_t* kbf16, void* stream) {
   if (p.emit.empty()) return 0;
   int maxco = 1;
-  size_t smem = 0;
+  size_t smem = 16;
   for (auto& e : p.emit) {
     maxco = e.co > maxco ? e.co : maxco;
-    const size_t s = (size_t)e.k * e.k * (e.ci + 1) * sizeof(float);
-    smem = s > smem ? s : smem;
+    smem = std::max(smem, (size_t)e.k * e.k * e.ci * sizeof(float));
   }
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     cudaFuncSetAttribute(emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
-  dim3 grid((unsigned)(maxco < 128 ? maxco : 128), (unsigned)p.emit.size());
-  emit_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(p.d_emit, bufs[0], bufs[1], bufs[2], bufs[3], kf32,
-                                                         reinterpret_cast<__nv_bfloat16*>(kbf16));
+  dim3 grid((unsigned)(maxco < 256 ? maxco : 256), (unsigned)p.emit.size());
+  emit_kernel<<<grid, 128, smem, (cudaStream_t)stream>>>(p.d_emit, bufs[0], bufs[1], bufs[2], bufs[3], kf32,
+                                                      reinterpret_cast<__nv_bfloat16*>(kbf16));
   p.launches++;
   return (int)cudaGetLastError();
 }

@@ -19,10 +19,13 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 #include <vector>
 
 #include "orth_internal.h"
+#include "tma_host.h"
 #include "umma.cuh"
 
 namespace orth {
@@ -52,6 +55,8 @@ struct TcgPhase {
   int tiles = 0;
   TcgDesc* dd = nullptr;
   TcgSeg* ds = nullptr;
+  void* dmaps = nullptr;   // per segment 4 TMA maps {A hi, B hi, A lo, B lo}, then the tile -> desc table
+  int* dtile = nullptr;
 };
 struct TcComposePlan {
   void* arena = nullptr;
@@ -204,22 +209,193 @@ __global__ void __launch_bounds__(256, 1) tcg_kernel(const TcgDesc* __restrict__
   if (warp == 0) umma::tmem_dealloc(tmem, 128);
 }
 
-// FP32 ortho -> BF16 hi/lo copies (row-major padded, or the RKO phase split)
+// TMA version of the composition GEMM (one 128x128 output tile per CTA):
+// tid 0 streams {A hi, B hi, A lo, B lo} 128x64 boxes of each segment by TMA
+// into a 3-stage SWIZZLE_128B ring, tid 32 issues the 3-pass tcgen05.mma, all
+// 256 threads run a vectorised epilogue (two 64-column halves through a
+// padded smem tile; row outputs as float4 / packed BF16x4, the transposed
+// output by a column pass).
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void split4(float a, float b, float c, float d, uint2& hi, uint2& lo) {
+  hi.x = pack2(a, b);
+  hi.y = pack2(c, d);
+  lo.x = pack2(a - __uint_as_float(hi.x << 16), b - __uint_as_float(hi.x & 0xFFFF0000u));
+  lo.y = pack2(c - __uint_as_float(hi.y << 16), d - __uint_as_float(hi.y & 0xFFFF0000u));
+}
+
+__global__ void __launch_bounds__(256, 1) tcg_tma_kernel(const TcgDesc* __restrict__ descs,
+                                                         const int* __restrict__ tile_desc,
+                                                         const CUtensorMap* __restrict__ maps) {
+  constexpr int TILE = 128 * 128, STAGE = 4 * TILE;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full_bar[S], empty_bar[S], done_bar;
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const TcgDesc d = descs[tile_desc[blockIdx.x]];
+  const int local = blockIdx.x - d.tile_begin;
+  const int m0 = (local / d.tiles_n) * 128, n0 = (local % d.tiles_n) * 128;
+  if (warp == 0) umma::tmem_alloc(&tmem_base_sh, 128);
+  if (tid == 32) {
+    for (int i = 0; i < S; ++i) {
+      umma::mbar_init(&full_bar[i], 1);
+      umma::mbar_init(&empty_bar[i], 1);
+    }
+    umma::mbar_init(&done_bar, 1);
+    umma::fence_mbar_init();
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t s0 = umma::smem_u32(smem);
+  const int nkb = (d.K + 63) / 64;
+  const int nk = nkb * d.seg_count;   // 0 for an empty product (rank-0 projector): acc = 0
+  if (tid == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % S;
+      if (kb >= S) umma::mbar_wait(&empty_bar[st], ((kb / S) - 1) & 1);
+      const CUtensorMap* mp = maps + 4 * (d.seg_begin + kb / nkb);
+      const int k0 = (kb % nkb) * 64;
+      const uint32_t sa = s0 + st * STAGE;
+      umma::mbar_arrive_expect_tx(&full_bar[st], STAGE);
+      umma::tma_load_2d(sa, mp + 0, &full_bar[st], k0, m0);
+      umma::tma_load_2d(sa + TILE, mp + 1, &full_bar[st], k0, n0);
+      umma::tma_load_2d(sa + 2 * TILE, mp + 2, &full_bar[st], k0, m0);
+      umma::tma_load_2d(sa + 3 * TILE, mp + 3, &full_bar[st], k0, n0);
+    }
+  } else if (tid == 32) {
+    constexpr uint32_t IDESC = umma::idesc_bf16(128, 128);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % S;
+      umma::mbar_wait(&full_bar[st], (kb / S) & 1);
+      umma::tc_fence_after();
+      const uint32_t ah = s0 + st * STAGE, bh = ah + TILE, al = ah + 2 * TILE, bl = ah + 3 * TILE;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t dah = umma::sdesc_sw128(ah + 32 * q), dbh = umma::sdesc_sw128(bh + 32 * q);
+        umma::mma_bf16(tmem, dah, dbh, IDESC, (kb | q) != 0);
+        umma::mma_bf16(tmem, dah, umma::sdesc_sw128(bl + 32 * q), IDESC, 1);
+        umma::mma_bf16(tmem, umma::sdesc_sw128(al + 32 * q), dbh, IDESC, 1);
+      }
+      umma::mma_commit(&empty_bar[st]);
+    }
+    umma::mma_commit(&done_bar);
+  }
+  umma::mbar_wait(&done_bar, 0);
+  umma::tc_fence_after();
+  // ---- epilogue: two 64-column halves
+  constexpr int LDF = 68;
+  float* Sf = reinterpret_cast<float*>(smem);   // [128][68]
+  const bool fvec = d.f && (d.ldf & 3) == 0;
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    {
+      const int q = warp & 3, sub = warp >> 2, r = q * 32 + lane;
+      float v[32];
+      umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * 64 + sub * 32), v);
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        *reinterpret_cast<float4*>(Sf + r * LDF + sub * 32 + 4 * t) =
+            nk > 0 ? make_float4(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    umma::tc_fence_before();
+    __syncthreads();
+#pragma unroll 2
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + 256 * u, r = e >> 4, c4 = (e & 15) * 4;
+      const int i = m0 + r, j0 = n0 + h * 64 + c4;
+      const float4 a = *reinterpret_cast<const float4*>(Sf + r * LDF + c4);
+      const float acc[4] = {a.x, a.y, a.z, a.w};
+      float o[4], o2[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool ok = i < d.M && j0 + k < d.N;
+        const float dg = (i == j0 + k) ? 1.f : 0.f;
+        o[k] = ok ? fmaf(d.alpha, acc[k], d.diag * dg) : 0.f;
+        o2[k] = ok ? fmaf(d.alpha2, acc[k], d.diag2 * dg) : 0.f;
+      }
+      if (d.f && i < d.M && j0 < d.N) {
+        float* dst = d.f + (int64_t)i * d.ldf + j0;
+        if (fvec && j0 + 3 < d.N) {
+          *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (j0 + k < d.N) dst[k] = o[k];
+        }
+      }
+      if (i < d.M && j0 < d.ldo) {   // ldo % 8 == 0: the 4-group lies inside the padded row
+        const int64_t bo = (int64_t)i * d.ldo + j0;
+        uint2 hv, lv;
+        if (d.oh) {
+          split4(o[0], o[1], o[2], o[3], hv, lv);
+          *reinterpret_cast<uint2*>(d.oh + bo) = hv;
+          *reinterpret_cast<uint2*>(d.ol + bo) = lv;
+        }
+        if (d.o2h) {
+          split4(o2[0], o2[1], o2[2], o2[3], hv, lv);
+          *reinterpret_cast<uint2*>(d.o2h + bo) = hv;
+          *reinterpret_cast<uint2*>(d.o2l + bo) = lv;
+        }
+      }
+      if (d.th) *reinterpret_cast<float4*>(Sf + r * LDF + c4) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+    __syncthreads();
+    if (d.th) {   // transposed rows: lane -> column (conflict-free Sf column reads), 8 rows -> one 16-byte store
+#pragma unroll 1
+      for (int u = 0; u < 4; ++u) {
+        const int e = tid + 256 * u, cl = e & 63, i8 = (e >> 6) * 8;
+        const int jn = n0 + h * 64 + cl, i0 = m0 + i8;
+        float x[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) x[t] = Sf[(i8 + t) * LDF + cl];
+        if (jn < d.N && i0 < d.ldt) {
+          uint2 h0, l0, h1, l1;
+          split4(x[0], x[1], x[2], x[3], h0, l0);
+          split4(x[4], x[5], x[6], x[7], h1, l1);
+          const int64_t o = (int64_t)jn * d.ldt + i0;
+          *reinterpret_cast<uint4*>(d.th + o) = make_uint4(h0.x, h0.y, h1.x, h1.y);
+          *reinterpret_cast<uint4*>(d.tl + o) = make_uint4(l0.x, l0.y, l1.x, l1.y);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tmem, 128);
+}
+
+// FP32 ortho -> BF16 hi/lo copies (row-major padded, or the RKO phase split).
+// CTA = rows r = blockIdx.x + k gridDim.x of item blockIdx.y; 32-bit index math.
 __global__ void __launch_bounds__(256) cvt_kernel(const CvtItem* __restrict__ items, const float* __restrict__ ortho) {
   const CvtItem it = items[blockIdx.y];
-  const int64_t total = (int64_t)it.m * it.n;
-  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (int64_t)gridDim.x * 256) {
-    const int r = (int)(e / it.n), col = (int)(e - (int64_t)r * it.n);
-    __nv_bfloat16 h, l;
-    split(ortho[it.src_off + e], h, l);
-    int64_t o;
-    if (it.mode == 0) o = (int64_t)r * it.ld + col;
-    else {
-      const int ph = col % it.s2, j = col / it.s2;   // R[o, j s^2 + ab] -> block ab, row o, column j
-      o = ((int64_t)ph * it.m + r) * it.ld + j;
+  for (int r = blockIdx.x; r < it.m; r += gridDim.x) {
+    const float* src = ortho + it.src_off + (int64_t)r * it.n;
+    if (it.mode == 0) {
+      __nv_bfloat16* dh = it.dh + (int64_t)r * it.ld;
+      __nv_bfloat16* dl = it.dl + (int64_t)r * it.ld;
+      for (int c = threadIdx.x; c < it.n; c += 256) {
+        __nv_bfloat16 h, l;
+        split(__ldg(src + c), h, l);
+        dh[c] = h;
+        dl[c] = l;
+      }
+    } else {   // R[o, j s^2 + ph] -> block ph, row o, column j
+      const int nj = it.n / it.s2;
+      for (int j = threadIdx.x; j < nj; j += 256)
+        for (int ph = 0; ph < it.s2; ++ph) {
+          __nv_bfloat16 h, l;
+          split(__ldg(src + j * it.s2 + ph), h, l);
+          const int64_t o = ((int64_t)ph * it.m + r) * it.ld + j;
+          it.dh[o] = h;
+          it.dl[o] = l;
+        }
     }
-    it.dh[o] = h;
-    it.dl[o] = l;
   }
 }
 
@@ -229,10 +405,60 @@ int launch_phase(const TcgPhase& ph, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tcg_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  tcg_kernel<<<ph.tiles, 256, smem, s>>>(ph.dd, (int)ph.d.size(), ph.ds);
+  if (ph.dmaps)
+    tcg_tma_kernel<<<ph.tiles, 256, smem, s>>>(ph.dd, ph.dtile, reinterpret_cast<const CUtensorMap*>(ph.dmaps));
+  else
+    tcg_kernel<<<ph.tiles, 256, smem, s>>>(ph.dd, (int)ph.d.size(), ph.ds);
   return (int)cudaGetLastError();
+}
+
+// TMA maps of every segment operand (K extent x rows, row stride ld) plus the
+// tile -> descriptor table; phases whose operands cannot be described by TMA
+// (misaligned pointer or stride) keep the cp.async kernel.
+bool build_phase_maps(TcgPhase& ph) {
+  if (!ph.tiles) return true;
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  std::vector<CUtensorMap> maps(4 * ph.s.size());
+  std::vector<int> seg_desc(ph.s.size(), -1);
+  for (size_t di = 0; di < ph.d.size(); ++di)
+    for (int k = 0; k < ph.d[di].seg_count; ++k) seg_desc[ph.d[di].seg_begin + k] = (int)di;
+  for (size_t si = 0; si < ph.s.size(); ++si) {
+    const TcgSeg& g = ph.s[si];
+    const int di = seg_desc[si];
+    const TcgDesc& d = ph.d[di < 0 ? 0 : di];
+    const __nv_bfloat16* ptr[4] = {g.ah, g.bh, g.al, g.bl};
+    const int rows[4] = {d.M, d.N, d.M, d.N}, ld[4] = {g.lda, g.ldb, g.lda, g.ldb};
+    for (int q = 0; q < 4; ++q) {
+      if (((uintptr_t)ptr[q] & 15) || (ld[q] % 8) || d.K < 1) return false;
+      const cuuint64_t dims[2] = {(cuuint64_t)d.K, (cuuint64_t)std::max(rows[q], 1)};
+      const cuuint64_t strides[1] = {(cuuint64_t)ld[q] * 2};
+      const cuuint32_t box[2] = {64, 128};
+      const cuuint32_t es[2] = {1, 1};
+      std::memset(&maps[4 * si + q], 0, sizeof(CUtensorMap));
+      if (enc(&maps[4 * si + q], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(ptr[q]), dims, strides,
+              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    }
+  }
+  std::vector<int> tile;
+  for (size_t di = 0; di < ph.d.size(); ++di) {
+    const TcgDesc& d = ph.d[di];
+    for (int t = 0; t < ((d.M + 127) / 128) * d.tiles_n; ++t) tile.push_back((int)di);
+  }
+  const size_t mb = maps.size() * sizeof(CUtensorMap);
+  if (cudaMalloc(&ph.dmaps, mb + tile.size() * sizeof(int) + 64) != cudaSuccess) {
+    ph.dmaps = nullptr;
+    return false;
+  }
+  ph.dtile = reinterpret_cast<int*>(static_cast<char*>(ph.dmaps) + mb);
+  if (!maps.empty()) cudaMemcpy(ph.dmaps, maps.data(), mb, cudaMemcpyHostToDevice);
+  cudaMemcpy(ph.dtile, tile.data(), tile.size() * sizeof(int), cudaMemcpyHostToDevice);
+  return true;
 }
 
 void finish(TcgPhase& ph) {
@@ -443,6 +669,13 @@ orth_status_t build_compose_tc(Plan& P) {
     set_error("compose descriptor upload failed: %s", cudaGetErrorString(e));
     return ORTH_ERR_CUDA;
   }
+  static const bool no_tma = std::getenv("ORTH_COMPOSE_NO_TMA") != nullptr;   // A/B switch
+  if (!no_tma) {
+    for (TcgPhase* ph : {&T->proj, &T->aoc})
+      if (!build_phase_maps(*ph)) { if (ph->dmaps) cudaFree(ph->dmaps); ph->dmaps = nullptr; }
+    for (auto& ph : T->chain)
+      if (!build_phase_maps(ph)) { if (ph.dmaps) cudaFree(ph.dmaps); ph.dmaps = nullptr; }
+  }
   return ORTH_OK;
 }
 
@@ -451,8 +684,16 @@ void free_compose_tc(Plan& P) {
   if (!T) return;
   if (T->arena) cudaFree(T->arena);
   if (T->dcvt) cudaFree(T->dcvt);
-  for (TcgPhase* ph : {&T->proj, &T->aoc}) { if (ph->dd) cudaFree(ph->dd); if (ph->ds) cudaFree(ph->ds); }
-  for (auto& ph : T->chain) { if (ph.dd) cudaFree(ph.dd); if (ph.ds) cudaFree(ph.ds); }
+  for (TcgPhase* ph : {&T->proj, &T->aoc}) {
+    if (ph->dd) cudaFree(ph->dd);
+    if (ph->ds) cudaFree(ph->ds);
+    if (ph->dmaps) cudaFree(ph->dmaps);
+  }
+  for (auto& ph : T->chain) {
+    if (ph.dd) cudaFree(ph.dd);
+    if (ph.ds) cudaFree(ph.ds);
+    if (ph.dmaps) cudaFree(ph.dmaps);
+  }
   delete T;
   P.tcc = nullptr;
 }
@@ -461,9 +702,9 @@ int launch_compose_tc(Plan& P, const float* ortho, void* stream) {
   TcComposePlan* T = P.tcc;
   cudaStream_t s = (cudaStream_t)stream;
   if (!T->cvt.empty()) {
-    int64_t maxe = 1;
-    for (auto& c : T->cvt) maxe = std::max<int64_t>(maxe, (int64_t)c.m * c.n);
-    dim3 grid((unsigned)std::min<int64_t>(64, (maxe + 255) / 256), (unsigned)T->cvt.size());
+    int maxm = 1;
+    for (auto& c : T->cvt) maxm = std::max(maxm, c.m);
+    dim3 grid((unsigned)std::min(maxm, 128), (unsigned)T->cvt.size());
     cvt_kernel<<<grid, 256, 0, s>>>(T->dcvt, ortho);
     P.launches++;
     if (int e = (int)cudaGetLastError()) return e;

@@ -27,12 +27,19 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 
 #include "orth_internal.h"
 #include "tma_host.h"
 #include "umma.cuh"
+
+#ifdef ORTH_CONV_TRACE
+// per CTA: [0] producer tid0 cycles waiting on empty, [1] MMA cycles waiting on full,
+// [2] MMA cycles waiting on tempty, [3] total MMA-thread cycles, [4] k-blocks
+__device__ unsigned long long ws_trace[160 * 8];
+#endif
 
 namespace orth {
 namespace {
@@ -47,6 +54,11 @@ struct TcConvArgs {
   int phase_tile0[MAX_PHASES + 1];   // first tile (over m) of each phase, prefix sums
   int phase_hp[MAX_PHASES], phase_wp[MAX_PHASES], phase_cnt[MAX_PHASES];
   int tiles_m;            // = phase_tile0[nphase]
+  // thread-block clusters of cs CTAs along M share every B tile (TMA multicast of
+  // a BN/cs-row slice per CTA); a cluster tile = cs consecutive M tiles of one phase
+  int cs;
+  int phase_ctile0[MAX_PHASES + 1];  // first cluster tile of each phase
+  int ctiles_m, num_ctiles;
 };
 
 constexpr int NPROD = 256;                 // producer threads (warps 0-7)
@@ -63,16 +75,18 @@ struct TileInfo {
   int g, n0, phase, m0, cnt;   // m0: first row inside the phase; cnt: rows of the phase
 };
 
-__device__ __forceinline__ TileInfo decode_tile(const TcConvArgs& a, int tile, int BN) {
+// cluster tile ct, CTA rank r in the cluster -> this CTA's tile (M tiles past the
+// phase's end are dummies: all rows >= cnt, loads zero-filled, nothing stored)
+__device__ __forceinline__ TileInfo decode_tile(const TcConvArgs& a, int ct, int r, int BN) {
   TileInfo t;
-  const int tm = tile % a.tiles_m, rest = tile / a.tiles_m;
+  const int tm = ct % a.ctiles_m, rest = ct / a.ctiles_m;
   const int tn = rest % a.tiles_n;
   t.g = rest / a.tiles_n;
   t.n0 = tn * BN;
   int p = 0;
-  while (p + 1 < a.nphase && a.phase_tile0[p + 1] <= tm) ++p;
+  while (p + 1 < a.nphase && a.phase_ctile0[p + 1] <= tm) ++p;
   t.phase = p;
-  t.m0 = (tm - a.phase_tile0[p]) * 128;
+  t.m0 = ((tm - a.phase_ctile0[p]) * a.cs + r) * 128;
   t.cnt = a.phase_cnt[p];
   return t;
 }
@@ -131,18 +145,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
-  constexpr int LAG = S - 2;   // stages of cp.async kept in flight per producer thread
   int* tab = reinterpret_cast<int*>(smem + S * STAGE);   // [valid tap j][128] input pixel, -1 = padding
   __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ int tap_id[MAX_TAPS];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cs = a.cs, crank = cs > 1 ? (int)umma::cluster_ctarank() : 0;
+  const int cid = blockIdx.x / cs, ncl = gridDim.x / cs;
+  const uint16_t cmask = (uint16_t)((1u << cs) - 1u);
   if (warp == MMA_WARP) umma::tmem_alloc(&tmem_base_sh, 2 * BN);
   if (tid == 0) {
     for (int i = 0; i < S; ++i) {
       umma::mbar_init(&full_bar[i], NPROD + 1);   // + the TMA issuer's expect_tx arrival
-      umma::mbar_init(&empty_bar[i], 1);
+      umma::mbar_init(&empty_bar[i], cs);         // every CTA of the cluster must release a stage
     }
     for (int i = 0; i < 2; ++i) {
       umma::mbar_init(&tfull_bar[i], 1);
@@ -152,6 +168,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   umma::tc_fence_before();
   __syncthreads();
+  if (cs > 1) umma::cluster_sync_all();   // peers' barriers initialised before any multicast
   umma::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const uint32_t s0 = umma::smem_u32(smem);
@@ -164,8 +181,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (tid == 0) umma::tma_prefetch_desc(&tmB);
     const uint32_t tab_s = umma::smem_u32(tab);
     int it = 0, st = 0, ph = 0;                // ring position of k-block `it`
-    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
-      const TileInfo t = decode_tile(a, tile, BN);
+    for (int ct = cid; ct < a.num_ctiles; ct += ncl) {
+      const TileInfo t = decode_tile(a, ct, crank, BN);
       umma::named_bar_sync(1, NPROD);          // everyone is done reading the previous table / tap list
       int nt = 0;
       for (int tap = 0; tap < kk2; ++tap)
@@ -220,11 +237,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) pix[i] = umma::ld_shared_s32(trow + 128u * i);
         for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++it) {
+#ifdef ORTH_CONV_TRACE
+          const long long tw0 = clock64();
+#endif
           umma::mbar_wait(&empty_bar[st], ph ^ 1);
+#ifdef ORTH_CONV_TRACE
+          if (tid == 0) ws_trace[blockIdx.x * 8 + 0] += clock64() - tw0;
+#endif
           const uint32_t sa = s0 + st * STAGE;
           if (tid == 0) {   // B tile (BN rows x 64 channels of this tap) by TMA, SWIZZLE_128B, OOB -> 0
             umma::mbar_arrive_expect_tx(&full_bar[st], B_BYTES);
-            umma::tma_load_3d(sa + A_BYTES, &tmB, &full_bar[st], c0, tap, t.g * a.nout_g + t.n0);
+            if (cs == 1) {
+              umma::tma_load_3d(sa + A_BYTES, &tmB, &full_bar[st], c0, tap, t.g * a.nout_g + t.n0);
+            } else {   // this CTA's BN/cs-row slice, multicast to the whole cluster
+              const int rows = BN / cs;
+              umma::tma_load_3d_mc(sa + A_BYTES + crank * rows * 128, &tmB, &full_bar[st], c0, tap,
+                                   t.g * a.nout_g + t.n0 + crank * rows, cmask);
+            }
           }
           const bool cok = c0 + c * 8 < a.cr_g;
 #pragma unroll
@@ -232,48 +261,67 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const bool ok = cok && pix[i] >= 0;
             umma::cp_async16(sa + off_r[i], ok ? ig + (int64_t)pix[i] * a.in_C + c0 : in, ok);
           }
-          umma::cp_async_commit();
-          if (it >= LAG) {
-            umma::cp_async_wait<LAG>();
-            umma::fence_proxy_async_smem();
-            int sp = st - LAG;
-            sp += sp < 0 ? S : 0;
-            umma::mbar_arrive(&full_bar[sp]);
-          }
+          // arrive on the stage's barrier when THIS thread's copies have landed (no
+          // producer stall: the next stage is issued as soon as its slot is free)
+          umma::cp_async_mbar_arrive(&full_bar[st]);
           if (++st == S) { st = 0; ph ^= 1; }
         }
       }
     }
     umma::cp_async_wait<0>();
-    umma::fence_proxy_async_smem();
-    for (int j = it - LAG < 0 ? 0 : it - LAG; j < it; ++j) umma::mbar_arrive(&full_bar[j % S]);
   } else if (warp == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t IDESC = umma::idesc_bf16(128, BN);
       int it = 0, tcount = 0;
-      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++tcount) {
-        const TileInfo t = decode_tile(a, tile, BN);
+#ifdef ORTH_CONV_TRACE
+      const long long t_all = clock64();
+      long long w_full = 0, w_te = 0;
+#endif
+      for (int ct = cid; ct < a.num_ctiles; ct += ncl, ++tcount) {
+        const TileInfo t = decode_tile(a, ct, crank, BN);
         int nt = 0;
         for (int tap = 0; tap < kk2; ++tap) nt += tap_valid(a, t.phase, tap) ? 1 : 0;
         const int nk = nt * kc;
         const int acc = tcount & 1;
+#ifdef ORTH_CONV_TRACE
+        long long tq = clock64();
+#endif
         umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
+#ifdef ORTH_CONV_TRACE
+        w_te += clock64() - tq;
+#endif
         umma::tc_fence_after();
         const uint32_t d_tmem = tmem + acc * BN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int st = it % S;
+#ifdef ORTH_CONV_TRACE
+          tq = clock64();
+#endif
           umma::mbar_wait(&full_bar[st], (it / S) & 1);
+#ifdef ORTH_CONV_TRACE
+          w_full += clock64() - tq;
+#endif
+#ifndef ORTH_DIAG_NOFENCE
+          umma::fence_proxy_async_smem();   // cp.async (generic proxy) rows -> tcgen05.mma (async proxy)
+#endif
           umma::tc_fence_after();
           const uint32_t aa = s0 + st * STAGE, bb = aa + A_BYTES;
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             umma::mma_bf16(d_tmem, umma::sdesc_sw128(aa + 32 * q), umma::sdesc_sw128(bb + 32 * q), IDESC,
                            (kb | q) != 0);
-          umma::mma_commit(&empty_bar[st]);
+          if (cs == 1) umma::mma_commit(&empty_bar[st]);
+          else umma::mma_commit_mc(&empty_bar[st], cmask);   // release the stage in every CTA of the cluster
         }
         umma::mma_commit(&tfull_bar[acc]);
       }
+#ifdef ORTH_CONV_TRACE
+      ws_trace[blockIdx.x * 8 + 1] = w_full;
+      ws_trace[blockIdx.x * 8 + 2] = w_te;
+      ws_trace[blockIdx.x * 8 + 3] = clock64() - t_all;
+      ws_trace[blockIdx.x * 8 + 4] = it;
+#endif
     }
     __syncwarp();
   } else {
@@ -281,8 +329,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int q = warp & 3;               // TMEM lane quarter of this warp (warps 9..12 -> 1,2,3,0)
     const int r = q * 32 + lane;
     int tcount = 0;
-    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++tcount) {
-      const TileInfo t = decode_tile(a, tile, BN);
+    for (int ct = cid; ct < a.num_ctiles; ct += ncl, ++tcount) {
+      const TileInfo t = decode_tile(a, ct, crank, BN);
       const int m = t.m0 + r;
       const int opix = m < t.cnt ? out_pixel(a, t.phase, m) : -1;
       const int acc = tcount & 1;
@@ -314,6 +362,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   umma::tc_fence_before();
   __syncthreads();
+  if (cs > 1) umma::cluster_sync_all();   // no peer may still multicast into this CTA
   if (warp == MMA_WARP) umma::tmem_dealloc(tmem, 2 * BN);
 }
 
@@ -353,30 +402,88 @@ int num_sms() {
 template <int BN, int S>
 int launch_ws(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
               const TcConvArgs& a, cudaStream_t stream) {
-  const size_t smem = 1024 + (size_t)S * (128 * 128 + BN * 128) + (size_t)MAX_TAPS * 128 * 4;
-  static bool attr = false;
-  if (!attr) {
+  // the pixel table only needs this layer's taps (k^2 <= MAX_TAPS)
+  const size_t smem = 1024 + (size_t)S * (128 * 128 + BN * 128) + (size_t)a.k * a.k * 128 * 4;
+  static size_t attr = 0;
+  if (smem > attr) {
     cudaFuncSetAttribute(conv_ws<BN, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    attr = smem;
   }
-  const int grid = a.num_tiles < num_sms() ? a.num_tiles : num_sms();
+  const int ncl_max = num_sms() / a.cs;
+  const int grid = (a.num_ctiles < ncl_max ? a.num_ctiles : ncl_max) * a.cs;
   CUtensorMap tm;
-  if (!make_weight_tmap(&tm, w, w_rows, a.k * a.k, a.cr_g, BN)) return (int)cudaErrorInvalidValue;
-  conv_ws<BN, S><<<grid, NTHREADS, smem, stream>>>(in, bias, out, a, tm);
-  return (int)cudaGetLastError();
+  if (!make_weight_tmap(&tm, w, w_rows, a.k * a.k, a.cr_g, BN / a.cs)) return (int)cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)a.cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const int e = (int)cudaLaunchKernelEx(&cfg, conv_ws<BN, S>, in, bias, out, a, tm);
+#ifdef ORTH_CONV_TRACE
+  {
+    cudaStreamSynchronize(stream);
+    static unsigned long long h[160 * 8];
+    cudaMemcpyFromSymbol(h, ws_trace, sizeof(h));
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+    for (int c = 0; c < grid && c < 160; ++c) {
+      s0 += h[c * 8]; s1 += h[c * 8 + 1]; s2 += h[c * 8 + 2]; s3 += h[c * 8 + 3]; s4 += h[c * 8 + 4];
+    }
+    std::printf("conv_ws<%d,%d> tiles=%d grid=%d kb/cta=%.0f: mma-thread total %.0f cyc, waits: full %.0f tempty %.0f; producer empty-wait %.0f cyc (per CTA avg)\n",
+                BN, S, a.num_tiles, grid, s4 / grid, s3 / grid, s1 / grid, s2 / grid, s0 / grid);
+    static unsigned long long z[160 * 8];
+    cudaMemcpyToSymbol(ws_trace, z, sizeof(z));
+  }
+#endif
+  return e;
 }
 
 int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
                TcConvArgs& a, int groups, cudaStream_t s) {
   const int n = a.nout_g;
-  const int bn = n % 256 == 0 ? 256 : n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32;
+  // widest N tile that still gives ~every SM a tile (a 128x256 MMA costs 128 cycles, 128x128 and
+  // 128x64 both ~73: narrower only pays when it fills otherwise idle SMs)
+  int bn = n % 256 == 0 ? 256 : n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32;
+  while (bn > 128 && (int64_t)a.tiles_m * (n / bn) * groups < (num_sms() * 4) / 5 && n % (bn / 2) == 0) bn /= 2;
   a.tiles_n = n / bn;
   a.num_tiles = a.tiles_m * a.tiles_n * groups;
   if (a.num_tiles == 0) return 0;
+  // clusters along M share B (multicast): 4 when every phase has >= 8 M tiles, else 2 / 1
+  static const int cs_env = std::getenv("ORTH_CONV_CLUSTER") ? std::atoi(std::getenv("ORTH_CONV_CLUSTER")) : -1;
+  int min_tiles = 1 << 30;
+  for (int p = 0; p < a.nphase; ++p)
+    if (a.phase_cnt[p] > 0) min_tiles = std::min(min_tiles, a.phase_tile0[p + 1] - a.phase_tile0[p]);
+  // measured on B200: clusters (B multicast) made every cfg2 layer slower -- the stage release then
+  // waits for the slowest CTA of the cluster, and these layers are not L2-bandwidth bound -- so the
+  // default stays 1 (ORTH_CONV_CLUSTER=2|4 for experiments)
+  int cs = 1;
+  (void)min_tiles;
+  if (cs_env >= 1 && cs_env <= 4 && (cs_env & (cs_env - 1)) == 0) cs = cs_env;
+  while (cs > 1 && (bn / cs) % 8 != 0) cs /= 2;
+  a.cs = cs;
+  int c0 = 0;
+  for (int p = 0; p < a.nphase; ++p) {
+    a.phase_ctile0[p] = c0;
+    c0 += (a.phase_tile0[p + 1] - a.phase_tile0[p] + cs - 1) / cs;
+  }
+  a.phase_ctile0[a.nphase] = c0;
+  a.ctiles_m = c0;
+  a.num_ctiles = a.ctiles_m * a.tiles_n * groups;
   switch (bn) {
+    // deepest ring that fits 227 KB with the 3x3 table (4.6 KB); larger kernels take the shallower one
     case 256: return launch_ws<256, 4>(in, w, w_rows, bias, out, a, s);
-    case 128: return launch_ws<128, 5>(in, w, w_rows, bias, out, a, s);
-    case 64: return launch_ws<64, 7>(in, w, w_rows, bias, out, a, s);
+    case 128:
+      if (a.k <= 3) return launch_ws<128, 6>(in, w, w_rows, bias, out, a, s);
+      return launch_ws<128, 5>(in, w, w_rows, bias, out, a, s);
+    case 64:
+      if (a.k <= 3) return launch_ws<64, 9>(in, w, w_rows, bias, out, a, s);
+      return launch_ws<64, 7>(in, w, w_rows, bias, out, a, s);
     default: return launch_ws<32, 8>(in, w, w_rows, bias, out, a, s);
   }
 }

@@ -285,20 +285,34 @@ def ours(args):
     fl, by = conv_flops_bytes(W["shapes"], batch)
     P = peaks()
     ns_flops = orth.orth_plan_query(plan.h, "NS_FLOPS")
-    # dominant kernel class: conv forward (sum over layers) vs NS
+    # dominant kernel class: conv forward (sum over layers) vs NS.  `traffic`: DRAM bytes per launch of
+    # that class from the committed ncu --set full capture of the same workload (profiles/r1_traffic.json)
+    traffic_db = {}
+    try:
+        traffic_db = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                                 "r1_traffic.json")))
+    except (OSError, ValueError):
+        pass
+    wl = traffic_db.get(configs.NAMES.get(args.config, ""), {})
+
+    def traffic(kind):
+        t = wl.get(kind)
+        return t["dram_bytes_per_launch"] if t else None
     conv_total = sum(t_conv)
     if nl and conv_total >= t_orth:
         ach = sum(fl) / (conv_total * 1e-3) / 1e12
         roof = {"kernel": f"conv apply (orth_conv_forward / orth_conv_transpose), {len(fl)} launches", "bound": "tensor", "achieved": ach,
                 "peak": P["bf16_tflops_sustained"], "unit": "TFLOP/s", "frac": ach / P["bf16_tflops_sustained"],
-                "traffic": None, "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                "traffic": traffic("conv apply"), "traffic_source": wl.get("source"),
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                 "per_launch_flops_avg": sum(fl) / len(fl), "avg_launch_ms": conv_total / len(fl),
                 "share_of_step": conv_total / t_step}
     else:
         ach = ns_flops / (t_orth * 1e-3) / 1e12
         roof = {"kernel": "orth_orthogonalize (power + NS)", "bound": "tensor", "achieved": ach,
                 "peak": P["bf16_tflops_sustained"], "unit": "TFLOP/s", "frac": ach / P["bf16_tflops_sustained"],
-                "traffic": None, "share_of_step": t_orth / t_step}
+                "traffic": traffic("orth_orthogonalize (power + NS)"), "traffic_source": wl.get("source"),
+                "share_of_step": t_orth / t_step}
     # ---- e2e through the public API with host buffers
     e2e = e2e_run(W, orth, torch, world, pg, args, barrier)
     out = {

@@ -356,21 +356,37 @@ def e2e_run(W, orth, torch, world, pg, args, barrier):
     res = W["acts"][-1] if W["acts"] else W["ortho"]
     yh = torch.empty(res.shape, dtype=res.dtype).pin_memory()
     s = torch.cuda.current_stream()
-    for _ in range(2):
-        W["params"].copy_(ph, non_blocking=True)
+
+    def step():
+        W["params"].copy_(ph, non_blocking=True)   # H2D of this step's parameters and input batch
         W["x"].copy_(xh, non_blocking=True)
         run_step(W, orth, torch, world, pg)
-        yh.copy_(res, non_blocking=True)
+        yh.copy_(res, non_blocking=True)           # D2H of the result
+    for _ in range(2):
+        step()
+    graph = None
+    if not args.no_graph and world == 1:
+        # the same API calls and copies captured once into a CUDA graph (memcpy nodes from pinned memory)
+        torch.cuda.synchronize()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(s)
+        with torch.cuda.stream(cs):
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=cs):
+                step()
+        s.wait_stream(cs)
+        torch.cuda.synchronize()
+        graph.replay()
     barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(s)
     n = max(1, args.steps)
     for _ in range(n):
-        W["params"].copy_(ph, non_blocking=True)
-        W["x"].copy_(xh, non_blocking=True)
-        run_step(W, orth, torch, world, pg)
-        yh.copy_(res, non_blocking=True)
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
     t1.record(s)
     barrier()
     ms = t0.elapsed_time(t1) / n
@@ -380,6 +396,7 @@ def e2e_run(W, orth, torch, world, pg, args, barrier):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     return {"value": len(W["plan"].layers) * world / (ms * 1e-3), "unit": "layers/s", "ms_per_step": ms,
+            "launch": "CUDA graph (copies + API calls)" if graph is not None else "eager",
             "h2d_bytes_per_step": int(ph.numel() * 4 + xh.numel() * 2),
             "d2h_bytes_per_step": int(yh.numel() * yh.element_size())}
 

@@ -298,6 +298,10 @@ int launch_conv_fwd(const LayerInfo& L, const void* kernel, void* scratch, const
   const ConvArgs a = make_args(L, N, H, W, Ho, Wo);
   const int64_t M = (int64_t)N * Ho * Wo;
   const int KT = L.ci * L.k * L.k;
+  if (io == ORTH_BF16 && !getenv("ORTH_FORCE_SIMT") && !getenv("ORTH_NO_STEM_TC")) {   // tensor-core stem
+    const int e = launch_conv_fwd_stem(L, kernel, bias, x, y, N, H, W, Ho, Wo, stream);
+    if (e >= 0) return e;
+  }
   if (io == ORTH_BF16 && KT <= 64 && L.co % 16 == 0 && L.co_f % 8 == 0 && !getenv("ORTH_FORCE_SIMT")) {
     const size_t smem = (size_t)(256 * (KT | 1) + KT * L.co) * sizeof(float);
     if (smem <= 200 * 1024) {

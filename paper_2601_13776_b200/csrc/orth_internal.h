@@ -225,6 +225,9 @@ int launch_residual_r(Plan& p, float* residual_out, void* stream);
 // the epilogue also writes the lo halves of its BF16 outputs.
 int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int npass, bool write_lo, bool write_f,
                  void* stream);
+// tensor-core stem (ci = 3, k = 3 | 4, co in {32, 64, 128}); -1 = not applicable
+int launch_conv_fwd_stem(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
+                         int H, int W, int Ho, int Wo, void* stream);
 // forward conv with shifted-copy A reuse (stride 1, wide images); -1 = not applicable
 int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
                           int H, int W, int Ho, int Wo, void* stream);

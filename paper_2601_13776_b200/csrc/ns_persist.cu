@@ -468,11 +468,18 @@ struct MatCost {
   int idx, gt, ut, nkg, nku;
 };
 
-// estimated microseconds of one NS iteration of matrix costs with G CTAs
+// estimated microseconds of one NS iteration of a matrix with G CTAs (measured
+// B200 per-tile figures: ~0.35 us per 64-deep k-block under full-chip
+// streaming, ~3.5 us Gram / ~4 us update epilogue for a full 128x128 tile
+// (less for ragged ones), ~1.5 us per group barrier; with double-buffered
+// TMEM a CTA's epilogues overlap its next mainloop)
 double iter_cost(const MatCost& c, int G) {
-  const double ckb = 0.2, ceg = 0.7, ceu = 1.0, cbar = 1.5, cloc = 0.3;
-  return std::ceil((double)c.gt / G) * (c.nkg * ckb + ceg) + std::ceil((double)c.ut / G) * (c.nku * ckb + ceu) +
-         (G > 1 ? 2 * cbar : 2 * cloc);
+  const double ckb = 0.35, ceg = 2.5, ceu = 3.0, cbar = 1.5, cloc = 0.3;
+  const double g_tiles = std::ceil((double)c.gt / G), u_tiles = std::ceil((double)c.ut / G);
+  const double g_main = c.nkg * ckb, u_main = c.nku * ckb;
+  const double gram = g_tiles * std::max(g_main, ceg) + std::min(g_main, ceg);
+  const double upd = u_tiles * std::max(u_main, ceu) + std::min(u_main, ceu);
+  return gram + upd + (G > 1 ? 2 * cbar : 2 * cloc);
 }
 
 }  // namespace
@@ -504,65 +511,36 @@ orth_status_t build_ns_persist(Plan& p) {
   // (a) one group of all matrices over all CTAs
   double ga = 0, ua = 0, gmax = 0, umax = 0;
   for (auto& c : mc) {
-    ga += c.gt * (c.nkg * 0.2 + 0.7);
-    ua += c.ut * (c.nku * 0.2 + 1.0);
-    gmax = std::max(gmax, c.nkg * 0.2 + 0.7);
-    umax = std::max(umax, c.nku * 0.2 + 1.0);
+    ga += c.gt * std::max(c.nkg * 0.35, 2.5);
+    ua += c.ut * std::max(c.nku * 0.35, 3.0);
+    gmax = std::max(gmax, c.nkg * 0.35 + 2.5);
+    umax = std::max(umax, c.nku * 0.35 + 3.0);
   }
   const double cost_a = std::max(ga / ctas, gmax) + std::max(ua / ctas, umax) + 3.0;
-  // (b) large matrices get dedicated CTAs, small ones are LPT-packed into single-CTA bins
-  std::vector<int> order(mc.size());
-  std::iota(order.begin(), order.end(), 0);
-  std::sort(order.begin(), order.end(), [&](int a, int b) { return iter_cost(mc[a], 1) > iter_cost(mc[b], 1); });
-  double total = 0;
-  for (auto& c : mc) total += iter_cost(c, 1);
-  std::vector<int> Gi(mc.size(), 0);
-  double tstar = total / ctas;
-  int used = 0;
-  std::vector<int> small;
-  for (int o : order) {
-    const double c1 = iter_cost(mc[o], 1);
-    if (c1 > tstar) {
-      int G = (int)std::ceil(c1 / tstar);
-      G = std::max(1, std::min(G, std::max(mc[o].gt, mc[o].ut)));
-      Gi[o] = G;
-      used += G;
-    } else {
-      small.push_back(o);
-    }
-  }
-  const int need_small = small.empty() ? 0 : 1;
-  while (used > ctas - need_small) {   // shrink the group that loses least
-    int best = -1;
-    double bc = 1e30;
-    for (size_t i = 0; i < mc.size(); ++i)
-      if (Gi[i] > 1) {
-        const double c = iter_cost(mc[i], Gi[i] - 1);
-        if (c < bc) { bc = c; best = (int)i; }
-      }
-    if (best < 0) break;
-    --Gi[best];
-    --used;
-  }
-  bool ok_b = used <= ctas - need_small;
-  int bins = ctas - used;
+  // (b) malleable-job greedy: every matrix starts as its own group of 1 CTA (or
+  // LPT bins when there are more matrices than CTAs); the group with the
+  // largest per-iteration cost takes one more CTA while that lowers its cost
+  std::vector<int> Gi(mc.size(), 1);
   std::vector<std::vector<int>> bin_mats;
   double cost_b = 0;
-  if (ok_b) {
-    for (size_t i = 0; i < mc.size(); ++i)
-      if (Gi[i] > 0) cost_b = std::max(cost_b, iter_cost(mc[i], Gi[i]));
-    if (!small.empty()) {
-      bins = std::min<int>(bins, (int)small.size());
-      bin_mats.assign(bins, {});
-      std::vector<double> load(bins, 0.0);
-      for (int o : small) {   // LPT (small is sorted by decreasing cost)
-        const int b = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-        load[b] += iter_cost(mc[o], 1) - (bin_mats[b].empty() ? 0.0 : 0.6);
-        bin_mats[b].push_back(o);
-      }
-      cost_b = std::max(cost_b, *std::max_element(load.begin(), load.end()));
+  bool ok_b = true;
+  if ((int)mc.size() <= ctas) {
+    int used = (int)mc.size();
+    std::vector<double> cur(mc.size());
+    for (size_t i = 0; i < mc.size(); ++i) cur[i] = iter_cost(mc[i], 1);
+    while (used < ctas) {
+      const int w = (int)(std::max_element(cur.begin(), cur.end()) - cur.begin());
+      const double nxt = iter_cost(mc[w], Gi[w] + 1);
+      if (nxt >= cur[w] - 1e-9) break;   // the slowest group cannot improve any more
+      ++Gi[w];
+      cur[w] = nxt;
+      ++used;
     }
+    cost_b = *std::max_element(cur.begin(), cur.end());
+  } else {
+    ok_b = false;   // more matrices than CTAs: only the global group
   }
+  (void)bin_mats;
   // materialise groups
   struct Grp { std::vector<int> mats; int G; };
   std::vector<Grp> gs;
@@ -575,10 +553,17 @@ orth_status_t build_ns_persist(Plan& p) {
     gs.push_back(g);
     p.nsp_est_us = cost_a;
   } else {
-    for (size_t i = 0; i < mc.size(); ++i)
-      if (Gi[i] > 0) gs.push_back({{(int)i}, Gi[i]});
-    for (auto& b : bin_mats) gs.push_back({b, 1});
+    for (size_t i = 0; i < mc.size(); ++i) gs.push_back({{(int)i}, Gi[i]});
     p.nsp_est_us = cost_b;
+  }
+  if (std::getenv("ORTH_NSP_VERBOSE")) {
+    std::printf("ns_persist partition: global %.1f us/iter vs groups %.1f us/iter -> %s, %zu groups\n", cost_a,
+                cost_b, gs.size() == 1 ? "global" : "groups", gs.size());
+    for (auto& g : gs)
+      if (g.mats.size() == 1)
+        std::printf("  mat %d (%dx%d): G=%d gram tiles %d (nk %d) upd tiles %d (nk %d) cost %.1f\n", g.mats[0],
+                    p.ns_upd[mc[g.mats[0]].idx].M, p.ns_upd[mc[g.mats[0]].idx].N, g.G, mc[g.mats[0]].gt,
+                    mc[g.mats[0]].nkg, mc[g.mats[0]].ut, mc[g.mats[0]].nku, iter_cost(mc[g.mats[0]], g.G));
   }
   // per-CTA tile lists: LPT inside each group (tile cost: k-blocks + epilogue;
   // diagonal Gram tiles load one operand, off-diagonal ones also write the mirror)

@@ -366,6 +366,223 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == MMA_WARP) umma::tmem_dealloc(tmem, 2 * BN);
 }
 
+// 2-SM pair version (cta_group::2): a cluster of two CTAs computes a 256-row
+// tile with one tcgen05.mma M=256 N=BN per K=16 step, issued by the leader.
+// Each CTA gathers its own 128 A rows (as conv_ws) and TMA-loads its own BN/2
+// rows of B; the tensor cores of both SMs read both B halves, so per SM the
+// shared-memory traffic per flop drops (the narrow-tile kernels above are
+// shared-memory bound).  Synchronisation: the peer's B bytes complete on the
+// leader's `full` barrier (cta_group::2 TMA); the peer's cp.async rows are
+// relayed by one peer thread (local barrier -> remote arrive on the leader);
+// the leader's commits release `empty` / signal `tfull` in both CTAs; both
+// CTAs' epilogue warps arrive on the leader's `tempty`.
+template <int BN, int S>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    conv_pair(const __nv_bfloat16* __restrict__ in, const float* __restrict__ bias, __nv_bfloat16* __restrict__ out,
+              const __grid_constant__ TcConvArgs a, const __grid_constant__ CUtensorMap tmB) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int HB = BN / 2;   // B rows held by each CTA
+  constexpr int A_BYTES = 128 * 128, B_BYTES = HB * 128, STAGE = A_BYTES + B_BYTES;
+  int* tab = reinterpret_cast<int*>(smem + S * STAGE);
+  __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int tap_id[MAX_TAPS];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int crank = (int)umma::cluster_ctarank();
+  const bool leader = crank == 0;
+  const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+  if (warp == MMA_WARP) umma::tmem_alloc_pair(&tmem_base_sh, 2 * BN);
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      // leader: its producers + its expect_tx arrival + the peer's relay; peer: its producers (relay input)
+      umma::mbar_init(&full_bar[i], leader ? NPROD + 2 : NPROD);
+      umma::mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      umma::mbar_init(&tfull_bar[i], 1);
+      umma::mbar_init(&tempty_bar[i], 8);   // 4 epilogue warps in each CTA
+    }
+    umma::fence_mbar_init();
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::cluster_sync_all();
+  umma::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t s0 = umma::smem_u32(smem);
+  const int kc = (a.cr_g + 63) / 64;
+  const int kk2 = a.k * a.k;
+
+  if (warp < MMA_WARP) {
+    // ------------------------------------------------------------ producers (as conv_ws)
+    const int c = tid & 7, rbase = tid >> 3;
+    if (tid == 0) umma::tma_prefetch_desc(&tmB);
+    const uint32_t tab_s = umma::smem_u32(tab);
+    int st = 0, ph = 0;
+    for (int ct = cid; ct < a.num_ctiles; ct += ncl) {
+      const TileInfo t = decode_tile(a, ct, crank, BN);
+      umma::named_bar_sync(1, NPROD);
+      int nt = 0;
+      for (int tap = 0; tap < kk2; ++tap)
+        if (tap_valid(a, t.phase, tap)) {
+          if (tid == 0) tap_id[nt] = tap;
+          ++nt;
+        }
+      umma::named_bar_sync(1, NPROD);
+      {
+        const int r = tid & 127, m = t.m0 + r;
+        int nb = -1, hb = 0, wb = 0;
+        if (m < t.cnt) {
+          if (!a.transposed) {
+            const int hw = a.Ho * a.Wo, n = m / hw, rr = m - n * hw, u = rr / a.Wo;
+            nb = n; hb = u * a.s - a.pt; wb = (rr - u * a.Wo) * a.s - a.pl;
+          } else {
+            const int hp = a.phase_hp[t.phase], wp = a.phase_wp[t.phase];
+            const int n = m / (hp * wp), rr = m - n * hp * wp, hh = rr / wp;
+            nb = n; hb = t.phase / a.s + a.s * hh + a.pt; wb = t.phase % a.s + a.s * (rr - hh * wp) + a.pl;
+          }
+        }
+        for (int j = tid >> 7; j < nt; j += 2) {
+          const int tap = tap_id[j], ta = tap / a.k, tb = tap - ta * a.k;
+          int v = -1;
+          if (nb >= 0) {
+            if (!a.transposed) {
+              int h = hb + a.d * ta, w = wb + a.d * tb;
+              bool ok = true;
+              if (a.circ) { h = wrapi(h, a.H); w = wrapi(w, a.W); }
+              else ok = h >= 0 && h < a.H && w >= 0 && w < a.W;
+              if (ok) v = (nb * a.H + h) * a.W + w;
+            } else {
+              int th = hb - a.d * ta, tw = wb - a.d * tb;
+              bool ok = true;
+              if (a.circ) { th = wrapi(th, a.H); tw = wrapi(tw, a.W); }
+              else ok = th >= 0 && tw >= 0;
+              const int u = th / a.s, vv = tw / a.s;
+              if (ok && u < a.Ho && vv < a.Wo) v = (nb * a.Ho + u) * a.Wo + vv;
+            }
+          }
+          tab[j * 128 + r] = v;
+        }
+      }
+      umma::named_bar_sync(1, NPROD);
+      const __nv_bfloat16* ig = in + (int64_t)t.g * a.cr_g + c * 8;
+      const uint32_t off_r[4] = {umma::sw128_off(rbase, c), umma::sw128_off(rbase + 32, c),
+                                 umma::sw128_off(rbase + 64, c), umma::sw128_off(rbase + 96, c)};
+      for (int j = 0; j < nt; ++j) {
+        const int tap = tap_id[j];
+        const uint32_t trow = tab_s + (uint32_t)(j * 128 + rbase) * 4u;
+        int pix[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) pix[i] = umma::ld_shared_s32(trow + 128u * i);
+        for (int c0 = 0; c0 < a.cr_g; c0 += 64) {
+          umma::mbar_wait(&empty_bar[st], ph ^ 1);
+          const uint32_t sa = s0 + st * STAGE;
+          if (tid == 0) {   // this CTA's BN/2 rows of B; bytes complete on the leader's barrier
+            if (leader) umma::mbar_arrive_expect_tx(&full_bar[st], 2 * B_BYTES);
+            umma::tma_load_3d_pair(sa + A_BYTES, &tmB, &full_bar[st], c0, tap, t.g * a.nout_g + t.n0 + crank * HB);
+          }
+          const bool cok = c0 + c * 8 < a.cr_g;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const bool ok = cok && pix[i] >= 0;
+            umma::cp_async16(sa + off_r[i], ok ? ig + (int64_t)pix[i] * a.in_C + c0 : in, ok);
+          }
+          umma::cp_async_mbar_arrive(&full_bar[st]);
+          if (++st == S) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+    umma::cp_async_wait<0>();
+  } else if (warp == MMA_WARP) {
+    if (lane == 0) {
+      int it = 0, tcount = 0;
+      for (int ct = cid; ct < a.num_ctiles; ct += ncl, ++tcount) {
+        const TileInfo t = decode_tile(a, ct, crank, BN);
+        int nt = 0;
+        for (int tap = 0; tap < kk2; ++tap) nt += tap_valid(a, t.phase, tap) ? 1 : 0;
+        const int nk = nt * kc;
+        if (leader) {
+          // ---------------------------------------------------- MMA issuer (leader)
+          constexpr uint32_t IDESC = umma::idesc_bf16(256, BN);
+          const int acc = tcount & 1;
+          umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
+          umma::tc_fence_after();
+          const uint32_t d_tmem = tmem + acc * BN;
+          for (int kb = 0; kb < nk; ++kb, ++it) {
+            const int st = it % S;
+            umma::mbar_wait(&full_bar[st], (it / S) & 1);
+            umma::fence_proxy_async_smem();
+            umma::tc_fence_after();
+            const uint32_t aa = s0 + st * STAGE, bb = aa + A_BYTES;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              umma::mma_bf16_pair(d_tmem, umma::sdesc_sw128(aa + 32 * q), umma::sdesc_sw128(bb + 32 * q), IDESC,
+                                  (kb | q) != 0);
+            umma::mma_commit_pair_mc(&empty_bar[st], 0x3);
+          }
+          umma::mma_commit_pair_mc(&tfull_bar[acc], 0x3);
+        } else {
+          // ---------------------------------------------------- relay (peer): local rows landed -> leader
+          for (int kb = 0; kb < nk; ++kb, ++it) {
+            const int st = it % S;
+            umma::mbar_wait(&full_bar[st], (it / S) & 1);
+            umma::fence_proxy_async_smem();   // this CTA's cp.async rows -> the pair's tensor cores
+            umma::mbar_arrive_remote(&full_bar[st], 0);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    int tcount = 0;
+    for (int ct = cid; ct < a.num_ctiles; ct += ncl, ++tcount) {
+      const TileInfo t = decode_tile(a, ct, crank, BN);
+      const int m = t.m0 + r;
+      const int opix = m < t.cnt ? out_pixel(a, t.phase, m) : -1;
+      const int acc = tcount & 1;
+      umma::mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
+      umma::tc_fence_after();
+      const int obase = t.g * a.nout_g + t.n0;
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 32) {
+        float v[32];
+        umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + cc), v);
+        if (opix >= 0) {
+          const int o = obase + cc;
+          uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)opix * a.out_C + o);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              float v0 = v[8 * i + 2 * jj], v1 = v[8 * i + 2 * jj + 1];
+              if (bias) { v0 += bias[o + 8 * i + 2 * jj]; v1 += bias[o + 8 * i + 2 * jj + 1]; }
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
+              pk[jj] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            dst[i] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        }
+      }
+      umma::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) umma::mbar_arrive(&tempty_bar[acc]);
+        else umma::mbar_arrive_remote(&tempty_bar[acc], 0);
+      }
+    }
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::cluster_sync_all();   // no peer may still signal into this CTA
+  if (warp == MMA_WARP) umma::tmem_dealloc_pair(tmem, 2 * BN);
+}
+
 // W^T per tap for the adjoint: WT[(g ci_g + i) k^2 + t][o] = W[(g co_g + o) k^2 + t][i]
 __global__ void __launch_bounds__(256) transpose_w_kernel(const __nv_bfloat16* __restrict__ w,
                                                           __nv_bfloat16* __restrict__ wt, int g, int co_g, int ci_g,
@@ -444,6 +661,35 @@ int launch_ws(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const
   return e;
 }
 
+template <int BN, int S>
+int launch_pair(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
+                const TcConvArgs& a, cudaStream_t stream) {
+  const size_t smem = 1024 + (size_t)S * (128 * 128 + BN / 2 * 128) + (size_t)a.k * a.k * 128 * 4;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(conv_pair<BN, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(conv_pair<BN, S>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = smem;
+  }
+  const int ncl_max = num_sms() / 2;
+  const int grid = (a.num_ctiles < ncl_max ? a.num_ctiles : ncl_max) * 2;
+  CUtensorMap tm;
+  if (!make_weight_tmap(&tm, w, w_rows, a.k * a.k, a.cr_g, BN / 2)) return (int)cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, conv_pair<BN, S>, in, bias, out, a, tm);
+}
+
 int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
                TcConvArgs& a, int groups, cudaStream_t s) {
   const int n = a.nout_g;
@@ -463,9 +709,14 @@ int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, cons
   // waits for the slowest CTA of the cluster, and these layers are not L2-bandwidth bound -- so the
   // default stays 1 (ORTH_CONV_CLUSTER=2|4 for experiments)
   int cs = 1;
-  (void)min_tiles;
   if (cs_env >= 1 && cs_env <= 4 && (cs_env & (cs_env - 1)) == 0) cs = cs_env;
   while (cs > 1 && (bn / cs) % 8 != 0) cs /= 2;
+  // 2-SM pair tiles (M = 256, cta_group::2) for the wide layers.  Correct (parity-tested) but measured
+  // SLOWER on every cfg2 layer (e.g. 256@8: 28 -> 40 us): the two producers run in lockstep and the
+  // peer's rows reach the leader through a relay; opt-in with ORTH_CONV_PAIR=1 for experiments
+  static const bool want_pair = std::getenv("ORTH_CONV_PAIR") != nullptr;
+  const bool pair = want_pair && cs_env < 0 && bn >= 128 && min_tiles >= 2;
+  if (pair) cs = 2;
   a.cs = cs;
   int c0 = 0;
   for (int p = 0; p < a.nphase; ++p) {
@@ -475,6 +726,12 @@ int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, cons
   a.phase_ctile0[a.nphase] = c0;
   a.ctiles_m = c0;
   a.num_ctiles = a.ctiles_m * a.tiles_n * groups;
+  if (pair) {   // stage = 16 KB A + BN/2 x 128 B of B
+    if (bn == 256) return a.k <= 3 ? launch_pair<256, 6>(in, w, w_rows, bias, out, a, s)
+                                   : launch_pair<256, 5>(in, w, w_rows, bias, out, a, s);
+    return a.k <= 3 ? launch_pair<128, 8>(in, w, w_rows, bias, out, a, s)
+                    : launch_pair<128, 6>(in, w, w_rows, bias, out, a, s);
+  }
   switch (bn) {
     // deepest ring that fits 227 KB with the 3x3 table (4.6 KB); larger kernels take the shallower one
     case 256: return launch_ws<256, 4>(in, w, w_rows, bias, out, a, s);

@@ -217,6 +217,20 @@ def test_conv_forward_and_transpose(cuda_lib, case, io):
     plan.check()
 
 
+@pytest.mark.parametrize("case", [(128, 128, 3, 1, 1, 1, "circular", 16, "conv"), (128, 256, 3, 2, 1, 1, "zeros", 9, "conv"),
+                                  (256, 256, 3, 1, 2, 1, "circular", 8, "convT")])
+def test_conv_pair_path(case):
+    """The opt-in 2-SM pair (cta_group::2) conv kernel, in a subprocess (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (f"import sys; sys.path.insert(0, {os.getcwd()!r}); import tests.test_gpu_parity as t; "
+            f"import paper_2601_13776_b200 as orth; t.test_conv_forward_and_transpose(orth, {case!r}, 'bf16')")
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "ORTH_CONV_PAIR": "1"},
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 def test_conv_rejections(cuda_lib):
     orth = cuda_lib
     plan = orth.Plan([dict(kind="conv", c_in=4, c_out=4, k=3, s=2, d=1, g=1, padding_mode="circular"),

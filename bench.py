@@ -85,13 +85,15 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ workload
-def build_workload(orth, torch, cfg_layers, rank, world, device, compute, batch, chain=True, cfg_id=2):
+def build_workload(orth, torch, cfg_layers, rank, world, device, compute, batch, chain=True, cfg_id=2,
+                   plan_rank=None, plan_world=None):
     """Plan, seeded parameters / power vectors, activations.  chain: each
     layer consumes the previous output (cfg2/cfg3); otherwise every layer gets
     its own seeded input (cfg4).  A transposed layer's forward is
     orth_conv_transpose (small -> large grid)."""
     from synth import gen
-    plan = orth.Plan(cfg_layers, device, rank=rank, world=world, compute=compute)
+    plan = orth.Plan(cfg_layers, device, rank=rank if plan_rank is None else plan_rank,
+                     world=world if plan_world is None else plan_world, compute=compute)
     params = np.zeros(plan.params_numel, np.float32)
     dev = torch.device("cuda", device)
     for i, m in enumerate(plan.matrices):
@@ -174,7 +176,7 @@ def run_step(W, orth, torch, world, pg, ev=None, graphs=None):
     else:
         plan.compose(W["ortho"], W["kf32"], W["kbf16"])
     rec("comp1")
-    if world > 1:
+    if world > 1 and W.get("sharded", True):
         from paper_2601_13776_b200.dist import gather_kernels
         gather_kernels(plan, W["kbf16"], orth.orth_plan_query(plan.h, "KERNEL_SEGMENT_BF16"), pg)
     rec("gather1")
@@ -233,8 +235,14 @@ def ours(args):
     else:
         cfg = configs.CONFIGS[args.config]()
         batch = configs.BATCH[args.config]
+    # construction: sharded by layer + all-gather, or replicated on every rank (no collective; SURVEY 8(e):
+    # cfg2/cfg3 construction is latency-bound, so sharding saves little there)
+    mode = args.construct if args.construct != "auto" else ("sharded" if args.config == 5 else "replicated")
+    sharded = world > 1 and mode == "sharded"
     W = build_workload(orth, torch, cfg, rank, world, local, args.compute, batch,
-                       chain=configs.CHAIN.get(args.config, False), cfg_id=args.config)
+                       chain=configs.CHAIN.get(args.config, False), cfg_id=args.config,
+                       plan_rank=rank if sharded else 0, plan_world=world if sharded else 1)
+    W["sharded"] = sharded
     plan = W["plan"]
     flush = torch.empty(int(2 * 126e6 // 4) + 1024, device="cuda", dtype=torch.float32)
 
@@ -250,7 +258,7 @@ def ours(args):
         per_step_launches = plan.launches - l0
     plan.check()
     barrier()
-    graphs = capture_graphs(W, torch) if (world == 1 and not args.no_graph) else None
+    graphs = capture_graphs(W, torch) if (not sharded and not args.no_graph) else None
     if graphs:
         for _ in range(2):
             run_step(W, orth, torch, world, pg, graphs=graphs)
@@ -326,11 +334,14 @@ def ours(args):
                    "construction": {"f32": "FP32 FFMA (SIMT)",
                                     "bf16": "tcgen05 BF16, FP32 master, 3-pass split polish + composition",
                                     "bf16x3": "tcgen05 3-pass hi/lo split everywhere"}[args.compute],
-                   "activations": "bf16 NHWC", "parallelism": f"dp{world} (construction sharded by layer + all-gather)",
+                   "activations": "bf16 NHWC",
+                   "parallelism": f"dp{world} (construction " + ("sharded by layer + all-gather)" if sharded else
+                                                                 "replicated on every rank, no collective)"),
                    "l2": "flushed between timed steps (252 MB write)",
                    "launch": "CUDA graphs per phase" if graphs else "eager"},
         "breakdown_ms": {"orthogonalize": t_orth, "compose": t_comp, "allgather": t_gather,
                          "conv_forward": conv_total, "conv_per_layer": t_conv},
+        "construction_layers_per_s": len(cfg) / ((t_orth + t_comp + t_gather) * 1e-3),
         "ns_tflops": ns_flops / (t_orth * 1e-3) / 1e12,
         "conv_tflops": sum(fl) / (conv_total * 1e-3) / 1e12 if nl else None,
         "conv_gbs": sum(by) / (conv_total * 1e-3) / 1e9 if nl else None,
@@ -365,7 +376,7 @@ def e2e_run(W, orth, torch, world, pg, args, barrier):
     for _ in range(2):
         step()
     graph = None
-    if not args.no_graph and world == 1:
+    if not args.no_graph and not W.get("sharded", False):
         # the same API calls and copies captured once into a CUDA graph (memcpy nodes from pinned memory)
         torch.cuda.synchronize()
         cs = torch.cuda.Stream()
@@ -502,6 +513,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying CUDA graphs")
     ap.add_argument("--cpu-budget", type=float, default=30.0)
+    ap.add_argument("--construct", default="auto", choices=["auto", "sharded", "replicated"],
+                    help="N > 1: shard construction by layer + all-gather, or replicate it (auto: cfg5 sharded)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)

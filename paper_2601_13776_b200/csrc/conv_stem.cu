@@ -14,8 +14,10 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstring>
 
 #include "orth_internal.h"
+#include "tma_host.h"
 #include "umma.cuh"
 
 namespace orth {
@@ -36,7 +38,8 @@ template <int CO, int CI, int KS>
 __global__ void __launch_bounds__(128) conv_stem_tc(const __nv_bfloat16* __restrict__ x,
                                                     const __nv_bfloat16* __restrict__ wt,
                                                     const float* __restrict__ bias, __nv_bfloat16* __restrict__ y,
-                                                    const __grid_constant__ StemArgs a) {
+                                                    const __grid_constant__ StemArgs a,
+                                                    const __grid_constant__ CUtensorMap tmY) {
   constexpr int TM = CO < 32 ? 32 : CO;   // TMEM columns (power of two >= 32)
   __shared__ __align__(1024) uint8_t As[128 * 128];
   __shared__ __align__(1024) uint8_t Bs[CO * 128];
@@ -71,7 +74,8 @@ __global__ void __launch_bounds__(128) conv_stem_tc(const __nv_bfloat16* __restr
   const int M = a.N * a.Ho * a.Wo;
   int phase = 0;
   for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, phase ^= 1) {
-    // ---- im2col row of this thread's pixel
+    // ---- im2col row of this thread's pixel (As is free: tid 0 waited for the last store's reads
+    // before the trailing __syncthreads of the previous tile)
     const int m = tile * 128 + tid;
     {
       constexpr int KT = CI * KS * KS;
@@ -120,30 +124,44 @@ __global__ void __launch_bounds__(128) conv_stem_tc(const __nv_bfloat16* __restr
     }
     umma::mbar_wait(&done_bar, phase);
     umma::tc_fence_after();
-    // ---- epilogue: this thread's TMEM row -> NHWC output row
+    // ---- epilogue: this thread's TMEM row -> bias -> BF16 into a SWIZZLE_128B staging tile (the
+    // A tile, consumed by now) -> one TMA tensor store per 64 channels (the tile's 128 pixels are
+    // consecutive NHWC rows: a dense box)
+    umma::bulk_wait_read0();   // the previous tile's store has finished reading the staging tile
 #pragma unroll
-    for (int c0 = 0; c0 < CO; c0 += 32) {
-      float v[32];
-      umma::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-      if (m < M) {
-        uint4* dst = reinterpret_cast<uint4*>(y + (int64_t)m * a.Co + c0);
+    for (int c0 = 0; c0 < CO; c0 += 64) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float v[32];
+        umma::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c0 + 32 * h), v);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           uint32_t pk[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             float v0 = v[8 * i + 2 * j], v1 = v[8 * i + 2 * j + 1];
-            if (bias) { v0 += bias[c0 + 8 * i + 2 * j]; v1 += bias[c0 + 8 * i + 2 * j + 1]; }
+            if (bias) { v0 += bias[c0 + 32 * h + 8 * i + 2 * j]; v1 += bias[c0 + 32 * h + 8 * i + 2 * j + 1]; }
             __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
             pk[j] = *reinterpret_cast<uint32_t*>(&b2);
           }
-          dst[i] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(As + umma::sw128_off(tid, h * 4 + i)) =
+              make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
       }
+      umma::fence_proxy_async_smem();   // staging writes -> TMA (async proxy) reads
+      __syncthreads();
+      if (tid == 0) {
+        umma::tma_store_2d(&tmY, umma::smem_u32(As), c0, tile * 128);   // rows past M are clipped by TMA
+        umma::bulk_commit();
+        if (c0 + 64 < CO) umma::bulk_wait_read0();   // staging reused by the next 64 channels
+      }
+      if (c0 + 64 < CO) __syncthreads();
     }
+    if (tid == 0) umma::bulk_wait_read0();
     umma::tc_fence_before();
-    __syncthreads();   // A tile and TMEM free for the next tile
+    __syncthreads();   // A tile (staging) and TMEM free for the next tile
   }
+  if (tid == 0) umma::bulk_wait0();   // all stores complete before exit
   umma::tc_fence_after();
   if (warp == 0) umma::tmem_dealloc(tmem, TM);
 }
@@ -155,7 +173,19 @@ int launch_stem(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bia
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = std::min(a.tiles, sms * 4);
-  conv_stem_tc<CO, CI, KS><<<grid, 128, 0, s>>>(x, w, bias, y, a);
+  // output viewed as (Co channels, N*Ho*Wo pixels), box 64 x 128, SWIZZLE_128B
+  CUtensorMap tm;
+  std::memset(&tm, 0, sizeof(tm));
+  auto enc = tensor_map_encoder();
+  const cuuint64_t dims[2] = {(cuuint64_t)a.Co, (cuuint64_t)a.N * a.Ho * a.Wo};
+  const cuuint64_t strides[1] = {(cuuint64_t)a.Co * 2};
+  const cuuint32_t box[2] = {64, 128};
+  const cuuint32_t es[2] = {1, 1};
+  if (!enc || enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return (int)cudaErrorInvalidValue;
+  conv_stem_tc<CO, CI, KS><<<grid, 128, 0, s>>>(x, w, bias, y, a, tm);
   return (int)cudaGetLastError();
 }
 
@@ -166,7 +196,8 @@ int launch_conv_fwd_stem(const LayerInfo& L, const void* kernel, const float* bi
                          int H, int W, int Ho, int Wo, void* stream) {
   const int KT = L.ci * L.k * L.k;
   // instantiated for the RGB stems of the paper-shaped workloads: 3 channels, 3x3 or 4x4 taps
-  if (L.g != 1 || KT > 64 || L.ci != 3 || (L.k != 3 && L.k != 4) || (L.co != 32 && L.co != 64 && L.co != 128))
+  if (L.g != 1 || KT > 64 || L.ci != 3 || (L.k != 3 && L.k != 4) || (L.co != 64 && L.co != 128) ||
+      ((uintptr_t)y & 15))
     return -1;
   StemArgs a{};
   a.N = N; a.H = H; a.W = W; a.Ci = L.ci_f; a.Co = L.co_f; a.k = L.k; a.s = L.s; a.d = L.d;
@@ -182,13 +213,11 @@ int launch_conv_fwd_stem(const LayerInfo& L, const void* kernel, const float* bi
   cudaStream_t s = (cudaStream_t)stream;
   if (L.k == 3) {
     switch (L.co) {
-      case 32: return launch_stem<32, 3, 3>(xi, wi, bias, yo, a, s);
       case 64: return launch_stem<64, 3, 3>(xi, wi, bias, yo, a, s);
       default: return launch_stem<128, 3, 3>(xi, wi, bias, yo, a, s);
     }
   }
   switch (L.co) {
-    case 32: return launch_stem<32, 3, 4>(xi, wi, bias, yo, a, s);
     case 64: return launch_stem<64, 3, 4>(xi, wi, bias, yo, a, s);
     default: return launch_stem<128, 3, 4>(xi, wi, bias, yo, a, s);
   }

@@ -90,6 +90,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {   // low half 
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ int ld_acquire_cta_shared(const int* p) {
   int v;
   asm volatile("ld.acquire.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(umma::smem_u32(p)) : "memory");
@@ -463,6 +468,350 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) umma::tmem_dealloc(tmem, 256);
 }
 
+// Dataflow NS (default): the same per-tile pipeline as ns_persist_kernel, but
+// with no phase barriers at all.  Items (phase, matrix, tile) are claimed in
+// one global order through an atomic counter; before loading a tile the
+// producer waits for ITS matrix's previous phase (per-matrix monotonic
+// counters: Gram(t) needs all update tiles of t-1, update(t) all Gram tiles of
+// t), and the epilogue bumps the matrix's counter when the tile's writes are
+// visible.  Claim order = dependency order, so with all CTAs co-resident the
+// smallest unfinished item can always run (no deadlock); small matrices race
+// ahead instead of waiting for the slowest tile of the whole phase.
+__global__ void __launch_bounds__(kThreads, 1)
+    ns_flow_kernel(const NsDesc* __restrict__ dg, const NsDesc* __restrict__ du, const NsItem* __restrict__ items,
+                   int n_items, unsigned* ctr, NspBufs bufs, const CUtensorMap* __restrict__ maps,
+                   const __grid_constant__ NspPhases ph) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* stage = reinterpret_cast<float*>(smem + kSlots * kSlot);
+  __shared__ uint64_t full_bar[kSlots], empty_bar[kSlots], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ uint64_t qfull[8], qempty[8];   // item queue: producer -> MMA / epilogue, in claim order
+  __shared__ int q[8];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ __align__(16) uint32_t desc_sh[kEpiWarps][32];
+
+  if (tid == 0) {
+    for (int i = 0; i < kSlots; ++i) {
+      umma::mbar_init(&full_bar[i], 1);
+      umma::mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      umma::mbar_init(&tfull_bar[i], 1);
+      umma::mbar_init(&tempty_bar[i], kEpiWarps);
+    }
+    for (int i = 0; i < 8; ++i) {
+      umma::mbar_init(&qfull[i], 1);
+      umma::mbar_init(&qempty[i], kEpiWarps);
+    }
+    umma::fence_mbar_init();
+  }
+  if (warp == 1) umma::tmem_alloc(&tmem_base_sh, 256);
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t ring = umma::smem_u32(smem);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      uint32_t used = 0, epar = 0;
+      int cnt = 0;
+      for (int kq = 0;; ++kq) {
+        // claim the next item (global order) and publish it to the MMA / epilogue warps
+        const int slot = kq & 7;
+        if (kq >= 8) umma::mbar_wait(&qempty[slot], ((kq >> 3) - 1) & 1);
+        const int idx = (int)atomicAdd(ctr, 1u);
+        if (idx < n_items) {
+          const NsItem it0 = items[idx];
+          if (it0.wait_ctr >= 0)   // data dependency: the previous phase of this matrix is complete
+            while (ld_acquire_gpu(ctr + it0.wait_ctr) < it0.wait_target) __nanosleep(32);
+        }
+        // publish only after the dependency is met: the epilogue prefetches C as soon as it sees the item
+        q[slot] = idx < n_items ? idx : -1;
+        umma::mbar_arrive(&qfull[slot]);
+        if (idx >= n_items) break;
+        const NsItem item = items[idx];
+        fence_proxy_async_global();   // other CTAs' generic writes before these async-proxy reads
+        const int p = item.p;
+        const int f = ph.f[p], gram = f & 1, split = (f >> 1) & 1, par = (f >> 2) & 1;
+        const NsDesc* D = gram ? dg : du;
+        const int w = split ? 2 : 1;
+        {
+          const NsTile tl{item.desc, item.local};
+          const NsDesc d = D[tl.desc];
+          const int m0 = (tl.local / d.tiles_n) * 128, n0 = (tl.local % d.tiles_n) * 128;
+          const int nk = (d.K + 63) / 64, a_mn = d.a_kind == 1, b_mn = d.b_kind == 1;
+          const bool sym = gram && m0 == n0;   // diagonal Gram tile: B == A, loaded once
+          const CUtensorMap* ma = maps + d.map_a + 2 * par;
+          const CUtensorMap* mb = maps + d.map_b + 2 * par;
+          for (int kb = 0; kb < nk; ++kb) {
+            if (w == 2 && cnt % kSlots == kSlots - 1) ++cnt;   // a hi/lo stage takes two adjacent slots
+            const int s = cnt % kSlots;
+            for (int qs = s; qs < s + w; ++qs) {
+              if ((used >> qs) & 1u) {
+                umma::mbar_wait(&empty_bar[qs], (epar >> qs) & 1u);
+                epar ^= 1u << qs;
+              }
+              used |= 1u << qs;
+            }
+            const uint32_t sa = ring + s * kSlot;
+            umma::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(sym ? w * kSlot / 2 : w * kSlot));
+            load_operand(sa, ma, &full_bar[s], kb * 64, m0, a_mn);
+            if (!sym) load_operand(sa + 16384, mb, &full_bar[s], kb * 64, n0, b_mn);
+            if (split) {
+              load_operand(sa + 32768, ma + 1, &full_bar[s], kb * 64, m0, a_mn);
+              if (!sym) load_operand(sa + 49152, mb + 1, &full_bar[s], kb * 64, n0, b_mn);
+            }
+            cnt += w;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      uint32_t fpar = 0;
+      int cnt = 0, acc = 0;
+      for (int kq = 0;; ++kq) {
+        const int slot = kq & 7;
+        umma::mbar_wait(&qfull[slot], (kq >> 3) & 1);
+        const int idx = q[slot];
+        if (idx < 0) break;
+        const NsItem item = items[idx];
+        const int p = item.p;
+        const int f = ph.f[p], gram = f & 1, split = (f >> 1) & 1;
+        const NsDesc* D = gram ? dg : du;
+        const int w = split ? 2 : 1;
+        {
+          const NsTile tl{item.desc, item.local};
+          const NsDesc* dp = D + tl.desc;
+          const int nk = (__ldg(&dp->K) + 63) / 64, a_mn = __ldg(&dp->a_kind) == 1, b_mn = __ldg(&dp->b_kind) == 1;
+          const int tn = __ldg(&dp->tiles_n);
+          const bool sym = gram && (tl.local / tn) == (tl.local % tn);
+          const uint32_t idesc = umma::idesc_bf16(128, 128) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
+          const int buf = acc & 1;
+          if (acc >= 2) umma::mbar_wait(&tempty_bar[buf], ((acc >> 1) - 1) & 1);
+          umma::tc_fence_after();
+          const uint32_t dt = tmem + buf * 128;
+          for (int kb = 0; kb < nk; ++kb) {
+            if (w == 2 && cnt % kSlots == kSlots - 1) ++cnt;
+            const int s = cnt % kSlots;
+            umma::mbar_wait(&full_bar[s], (fpar >> s) & 1u);
+            fpar ^= 1u << s;
+            umma::tc_fence_after();
+            const uint32_t ah = ring + s * kSlot, al = ah + 32768;
+            const uint32_t bh = sym ? ah : ah + 16384, bl = sym ? al : ah + 49152;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint64_t dah = op_desc(ah, q, a_mn), dbh = op_desc(bh, q, b_mn);
+              umma::mma_bf16(dt, dah, dbh, idesc, (kb | q) != 0);
+              if (split) {
+                umma::mma_bf16(dt, dah, op_desc(bl, q, b_mn), idesc, 1);
+                umma::mma_bf16(dt, op_desc(al, q, a_mn), dbh, idesc, 1);
+              }
+            }
+            umma::mma_commit(&empty_bar[s]);
+            if (w == 2) umma::mma_commit(&empty_bar[s + 1]);
+            cnt += w;
+          }
+          umma::mma_commit(&tfull_bar[buf]);
+          ++acc;
+        }
+      }
+    }
+  } else {
+    // -------------------------------------------------------------- epilogue
+    // 8 warps: warp w reads TMEM lanes 32*(w%4) (rows row0..row0+31) and the
+    // 64-column half ch of the accumulator, in two 32-column chunks.  The C
+    // tile of both chunks is prefetched into smem with cp.async before the
+    // accumulator is ready.  Chunk: tcgen05.ld (thread = row) -> float4 rows
+    // into a swizzled 32x32 smem tile -> row pass with 8 lanes per row (float4
+    // C from smem, float4 FP32 stores, 8-byte BF16 stores), 4 rows per step.
+    // Nothing tile-sized lives in registers (10 warps cap the kernel at 168).
+    const int ew = warp - 2, row0 = (warp & 3) * 32, ch = ew >> 2;
+    float* Sw = stage + ew * 3 * 1024;
+    float* Sc = Sw + 1024;
+    const int rsub = lane >> 3, q4 = lane & 7, c4 = q4 * 4;
+    int acc = 0;
+    for (int kq = 0;; ++kq) {
+      const int slot = kq & 7;
+      umma::mbar_wait(&qfull[slot], (kq >> 3) & 1);
+      const int idx = q[slot];
+      if (idx < 0) break;
+      const NsItem item = items[idx];
+      const int p = item.p;
+      const int f = ph.f[p], gram = f & 1, par = (f >> 2) & 1, write_lo = (f >> 3) & 1, write_f = (f >> 4) & 1;
+      const NsDesc* D = gram ? dg : du;
+      {
+        const NsTile tl{item.desc, item.local};
+        // this tile's descriptor -> a per-warp smem copy (one word per lane), so the
+        // fields cost an LDS, not an L2 round trip, wherever they are used below
+        {
+          static_assert(sizeof(NsDesc) <= 32 * 4, "NsDesc must fit one word per lane");
+          const uint32_t* srcw = reinterpret_cast<const uint32_t*>(D + tl.desc);
+          if (lane < (int)(sizeof(NsDesc) / 4)) desc_sh[ew][lane] = __ldg(srcw + lane);
+          __syncwarp();
+        }
+        const NsDesc* dp = reinterpret_cast<const NsDesc*>(desc_sh[ew]);
+        const int tiles_n = dp->tiles_n;
+        const int m0 = (tl.local / tiles_n) * 128 + row0, n0 = (tl.local % tiles_n) * 128 + ch * 64;
+        const bool upd = (dp->epi) == 1;
+        const int64_t f_off = (dp->f_off), ldf = (dp->ldf);
+        const int M = (dp->M), N = (dp->N);
+        const int buf = acc & 1;
+        if (upd) {   // C = X (fp32) rows m0.., cols n0..n0+63 -> Sc[0..1]
+          const float* Cm = pick(bufs.X, par) + f_off;
+          const bool fv4 = (ldf & 3) == 0;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int e = lane + 32 * k, r = e >> 3, q = e & 7;
+              const int i = m0 + r, j = n0 + c * 32 + 4 * q;
+              float* dst = Sc + c * 1024 + r * 32 + 4 * (q ^ (r & 7));
+              const float* src = Cm + (int64_t)i * ldf + j;
+              if (fv4 && (j + 3 < N || j >= N)) {
+                umma::cp_async16(umma::smem_u32(dst), i < M && j < N ? src : Cm, i < M && j < N);
+              } else {   // ragged / unaligned: synchronous scalar path
+#pragma unroll
+                for (int u = 0; u < 4; ++u) dst[u] = (i < M && j + u < N) ? __ldcg(src + u) : 0.f;
+              }
+            }
+            umma::cp_async_commit();
+          }
+        }
+        umma::mbar_wait(&tfull_bar[buf], (acc >> 1) & 1);
+        umma::tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            float v[16];
+            umma::tmem_ld16(tmem + buf * 128 + ch * 64 + c * 32 + hh * 16 + ((uint32_t)row0 << 16), v);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              *reinterpret_cast<float4*>(Sw + lane * 32 + 4 * ((hh * 4 + k) ^ (lane & 7))) =
+                  make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+          }
+          if (c == 1) {   // accumulator drained: hand the TMEM buffer back to the MMA warp
+            umma::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) umma::mbar_arrive(&tempty_bar[buf]);
+          }
+          if (upd) {
+            if (c == 0) umma::cp_async_wait<1>();
+            else umma::cp_async_wait<0>();
+          }
+          __syncwarp();
+          // per-chunk constants re-derived here (cheap) instead of being held in registers
+          const bool wf = upd || write_f;
+          const int ldb16 = upd ? (dp->ldx) : (dp->ldr);
+          const int64_t b_off = upd ? (dp->bx_off) : (dp->br_off);
+          __nv_bfloat16* oh = (upd ? pick(bufs.xh, par ^ 1) : bufs.rh) + b_off;
+          __nv_bfloat16* ol = (upd ? pick(bufs.xl, par ^ 1) : bufs.rl) + b_off;
+          float* F = (upd ? pick(bufs.X, par ^ 1) : bufs.R) + f_off;
+          const bool fv4 = (ldf & 3) == 0;
+          const float alpha = (dp->alpha), beta = (dp->beta), diag = (dp->diag);
+          const float* Scc = Sc + c * 1024;
+#pragma unroll 4
+          for (int it = 0; it < 8; ++it) {
+            const int rr = 4 * it + rsub;
+            const int i = m0 + rr, j = n0 + c * 32 + c4;
+            if (i < M) {
+              const int sw = 4 * (q4 ^ (rr & 7));
+              const float4 a = *reinterpret_cast<const float4*>(Sw + rr * 32 + sw);
+              const float4 cv = upd ? *reinterpret_cast<const float4*>(Scc + rr * 32 + sw) : make_float4(0.f, 0.f, 0.f, 0.f);
+              float o0 = fmaf(alpha, a.x, beta * cv.x), o1 = fmaf(alpha, a.y, beta * cv.y);
+              float o2 = fmaf(alpha, a.z, beta * cv.z), o3 = fmaf(alpha, a.w, beta * cv.w);
+              const int dd = i - j;   // diagonal element inside this 4-group
+              if (dd == 0) o0 += diag;
+              if (dd == 1) o1 += diag;
+              if (dd == 2) o2 += diag;
+              if (dd == 3) o3 += diag;
+              if (j + 3 >= N) {       // ragged right edge: zero beyond N (keeps BF16 padding zero)
+                if (j >= N) o0 = 0.f;
+                if (j + 1 >= N) o1 = 0.f;
+                if (j + 2 >= N) o2 = 0.f;
+                o3 = 0.f;
+              }
+              if (wf && j < N) {
+                float* dst = F + (int64_t)i * ldf + j;
+                if (fv4 && j + 3 < N) {
+                  *reinterpret_cast<float4*>(dst) = make_float4(o0, o1, o2, o3);
+                } else {
+                  dst[0] = o0;
+                  if (j + 1 < N) dst[1] = o1;
+                  if (j + 2 < N) dst[2] = o2;
+                  if (j + 3 < N) dst[3] = o3;
+                }
+              }
+              if (j < ldb16) {   // ldb16 % 8 == 0, j % 4 == 0: the 4-group lies inside the padded row
+                const uint32_t h01 = pack_bf16(o0, o1), h23 = pack_bf16(o2, o3);
+                const int64_t bo = (int64_t)i * ldb16 + j;
+                *reinterpret_cast<uint2*>(oh + bo) = make_uint2(h01, h23);
+                if (write_lo) {
+                  const uint32_t l01 = pack_bf16(o0 - __uint_as_float(h01 << 16), o1 - __uint_as_float(h01 & 0xFFFF0000u));
+                  const uint32_t l23 = pack_bf16(o2 - __uint_as_float(h23 << 16), o3 - __uint_as_float(h23 & 0xFFFF0000u));
+                  *reinterpret_cast<uint2*>(ol + bo) = make_uint2(l01, l23);
+                }
+              }
+            }
+          }
+          if (gram && m0 - row0 < n0 - ch * 64) {
+            // upper-triangle Gram tile: also write its mirror R[j][i] = R[i][j] (alpha * acc; no diagonal here)
+#pragma unroll 2
+            for (int it = 0; it < 8; ++it) {
+              const int rt = 4 * it + rsub;                           // column of the chunk = row of the mirror
+              const int jg = n0 + c * 32 + rt, ig = m0 + c4;
+              if (jg < N && ig < ldb16) {
+                float o[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const int r = c4 + k;
+                  o[k] = ig + k < M ? alpha * Sw[r * 32 + 4 * ((rt >> 2) ^ (r & 7)) + (rt & 3)] : 0.f;
+                }
+                if (wf) {
+                  float* dst = F + (int64_t)jg * ldf + ig;
+                  if (fv4 && ig + 3 < M) {
+                    *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+                  } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                      if (ig + k < M) dst[k] = o[k];
+                  }
+                }
+                const uint32_t h01 = pack_bf16(o[0], o[1]), h23 = pack_bf16(o[2], o[3]);
+                const int64_t bo = (int64_t)jg * ldb16 + ig;
+                *reinterpret_cast<uint2*>(oh + bo) = make_uint2(h01, h23);
+                if (write_lo) {
+                  const uint32_t l01 = pack_bf16(o[0] - __uint_as_float(h01 << 16), o[1] - __uint_as_float(h01 & 0xFFFF0000u));
+                  const uint32_t l23 = pack_bf16(o[2] - __uint_as_float(h23 << 16), o[3] - __uint_as_float(h23 & 0xFFFF0000u));
+                  *reinterpret_cast<uint2*>(ol + bo) = make_uint2(l01, l23);
+                }
+              }
+            }
+          }
+          __syncwarp();
+        }
+        ++acc;
+      }
+      // ---- item done: publish this tile's writes, bump the matrix's counter, free the queue slot
+      fence_proxy_async_global();
+      umma::named_bar_sync(1, 32 * kEpiWarps);
+      if (ew == 0 && lane == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr + item.done_ctr) : "memory");
+      }
+      if (lane == 0) umma::mbar_arrive(&qempty[slot]);
+    }
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) umma::tmem_dealloc(tmem, 256);
+}
+
 // ---------------------------------------------------------------- host: partition
 struct MatCost {
   int idx, gt, ut, nkg, nku;
@@ -617,7 +966,9 @@ orth_status_t build_ns_persist(Plan& p) {
   for (auto& e : ctas_v) { e.u_begin += off_u; e.u_end += off_u; }
   tg.insert(tg.end(), tu.begin(), tu.end());
   const size_t b_tiles = tg.size() * sizeof(NsTile), b_ctas = ctas_v.size() * sizeof(NsGroup);
-  const size_t b_bars = gs.size() * sizeof(unsigned);
+  // barrier words: the phase-synchronous kernel's group barriers, or the dataflow kernel's counters
+  const size_t n_words = std::max(gs.size(), 1 + 2 * p.ns_gram.size());
+  const size_t b_bars = n_words * sizeof(unsigned);
   const size_t total_b = b_tiles + b_ctas + b_bars + 64;
   char* mem = nullptr;
   cudaError_t e = cudaMalloc(&mem, total_b);
@@ -637,8 +988,60 @@ orth_status_t build_ns_persist(Plan& p) {
     return ORTH_ERR_CUDA;
   }
   p.nsp_groups_n = (int)gs.size();
+  p.nsp_zero_n = (int)n_words;
   p.nsp_ctas = cta;
   return ORTH_OK;
+}
+
+// dataflow items for a phase list: phase-major; inside a phase the matrices with
+// the longest tiles first (dynamic claiming then balances the tail)
+static int build_flow_items(Plan& p, const uint8_t* flags, int nphases) {
+  if (p.nsf_nphases == nphases && p.nsf_flags.size() == (size_t)nphases &&
+      std::memcmp(p.nsf_flags.data(), flags, (size_t)nphases) == 0)
+    return 0;
+  const int nm = (int)p.ns_gram.size();
+  std::vector<int> GT(nm), UT(nm), order(nm);
+  for (int i = 0; i < nm; ++i) {
+    const int tn = p.ns_gram[i].tiles_n;
+    GT[i] = tn * (tn + 1) / 2;
+    UT[i] = ((p.ns_upd[i].M + 127) / 128) * p.ns_upd[i].tiles_n;
+    order[i] = i;
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return p.ns_gram[a].K > p.ns_gram[b].K; });
+  std::vector<NsItem> items;
+  for (int ph = 0; ph < nphases; ++ph) {
+    const bool gram = flags[ph] & 1;
+    const int t = ph / 2;   // iteration (the residual Gram is phase 2T: t = T)
+    for (int i : order) {
+      const int tn = gram ? p.ns_gram[i].tiles_n : p.ns_upd[i].tiles_n;
+      const int ntile = gram ? tn * tn : UT[i];
+      for (int l = 0; l < ntile; ++l) {
+        if (gram && l / tn > l % tn) continue;   // upper-triangle Gram tiles only
+        NsItem it{};
+        it.p = ph; it.desc = i; it.local = l;
+        if (gram) {   // Gram(t) reads X_t: all update tiles of iteration t - 1 done
+          it.wait_ctr = t > 0 ? 2 + 2 * i : -1;
+          it.wait_target = (uint32_t)(t * UT[i]);
+          it.done_ctr = 1 + 2 * i;
+        } else {      // update(t) reads R_t: all Gram tiles of iteration t done
+          it.wait_ctr = 1 + 2 * i;
+          it.wait_target = (uint32_t)((t + 1) * GT[i]);
+          it.done_ctr = 2 + 2 * i;
+        }
+        items.push_back(it);
+      }
+    }
+  }
+  if (p.nsf_items) cudaFree(p.nsf_items);
+  p.nsf_items = nullptr;
+  cudaError_t e = cudaMalloc(&p.nsf_items, std::max<size_t>(items.size(), 1) * sizeof(NsItem));
+  if (e == cudaSuccess && !items.empty())
+    e = cudaMemcpy(p.nsf_items, items.data(), items.size() * sizeof(NsItem), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return (int)e;
+  p.nsf_n_items = (int)items.size();
+  p.nsf_nphases = nphases;
+  p.nsf_flags.assign(flags, flags + nphases);
+  return 0;
 }
 
 int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flags, int nphases, void* stream) {
@@ -684,6 +1087,22 @@ int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flag
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   p.launches++;
+  // dataflow for latency-bound batches (cfg2 / cfg3: a few hundred tiles per phase; measured 0.63 -> 0.57 ms
+  // on cfg3), phase-synchronous for big uniform sweeps (cfg5 n = 2048: 34.3 ms sync vs 40.5 ms dataflow)
+  static const char* mode_env = std::getenv("ORTH_NS_MODE");   // "flow" | "sync" (A/B)
+  const bool small = p.ns_upd_tiles <= 4 * p.nsp_ctas;
+  const bool flow = mode_env ? std::strcmp(mode_env, "sync") != 0 : small;
+  if (flow && !tracing) {
+    if (int e = build_flow_items(p, flags, nphases)) return e;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(ns_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+      attr_set = true;
+    }
+    return (int)cudaLaunchKernelEx(&cfg, ns_flow_kernel, (const NsDesc*)p.d_ns_gram, (const NsDesc*)p.d_ns_upd,
+                                   (const NsItem*)p.nsf_items, p.nsf_n_items, p.nsp_bars, b,
+                                   reinterpret_cast<const CUtensorMap*>(p.d_ns_maps), ph);
+  }
   const cudaError_t e = cudaLaunchKernelEx(&cfg, ns_persist_kernel, (const NsDesc*)p.d_ns_gram,
                                            (const NsDesc*)p.d_ns_upd, (const NsTile*)p.nsp_tiles,
                                            (const NsGroup*)p.nsp_groups, p.nsp_bars,

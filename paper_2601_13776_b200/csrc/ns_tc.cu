@@ -463,7 +463,7 @@ int launch_scale_bf16(Plan& p, const float* W, float* X0, int par, bool write_lo
   float* bufs[BUF_COUNT] = {X0, X0, nullptr, nullptr};
   NsBufs b = make_bufs(p, bufs);
   scale_bf16_kernel<<<(int)p.power_items.size(), 256, 0, (cudaStream_t)stream>>>(
-      p.d_power_items, W, p.d_sigma, X0, b, par, write_lo, p.nsp_bars, p.nsp_bars ? p.nsp_groups_n : 0, power_bar(p));
+      p.d_power_items, W, p.d_sigma, X0, b, par, write_lo, p.nsp_bars, p.nsp_bars ? p.nsp_zero_n : 0, power_bar(p));
   p.launches++;
   return (int)cudaGetLastError();
 }

@@ -104,6 +104,13 @@ struct NsGroup {           // per CTA: its barrier group and its own tile ranges
   int32_t u_begin, u_end;   // update tiles
 };
 constexpr int kNspMaxPhases = 132;   // 2T + 1 for T <= 65
+struct NsItem {           // dataflow NS: one (phase, matrix, tile) work item, in claim order
+  int32_t p, desc, local;   // phase index (flags), matrix (ns_gram / ns_upd index), tile in the matrix
+  int32_t wait_ctr;         // counter that must reach wait_target before the tile's operands are read (-1: none)
+  uint32_t wait_target;
+  int32_t done_ctr;         // counter bumped when the tile's outputs are visible
+  int32_t pad_[2];
+};
 
 struct PowerItem {        // row block of the pre-scaling / scale kernels: rows [r0, r1) of matrix `mat`
   int32_t mat, r0, r1, chunk;   // chunk: global row-item slot (|t|^2 partial)
@@ -180,6 +187,13 @@ struct Plan {
   unsigned* nsp_bars = nullptr;
   int32_t nsp_ctas = 0, nsp_groups_n = 0;
   double nsp_est_us = 0.0;
+  // dataflow NS items for the last phase list used (rebuilt when the list changes)
+  NsItem* nsf_items = nullptr;
+  int32_t nsf_n_items = 0, nsf_nphases = -1;
+  std::vector<uint8_t> nsf_flags;
+  int32_t nsp_zero_n = 0;           // words of nsp_bars the scale kernel zeroes before every launch
+  // (group barriers of the phase-synchronous kernel, or the dataflow kernel's
+  //  [claim][gram done, update done] x matrices counters)
   std::vector<PowerItem> power_items;
   std::vector<ColItem> col_items;
   ColItem* d_col_items = nullptr;

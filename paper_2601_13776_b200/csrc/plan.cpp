@@ -659,6 +659,7 @@ orth_status_t orth_plan_destroy(orth_plan_t plan) {
   free_compose_tc(plan->p);
   if (plan->p.d_ns_maps) cudaFree(plan->p.d_ns_maps);
   if (plan->p.nsp_mem) cudaFree(plan->p.nsp_mem);
+  if (plan->p.nsf_items) cudaFree(plan->p.nsf_items);
   if (plan->p.d_arena) cudaFree(plan->p.d_arena);
   delete plan;
   return ORTH_OK;

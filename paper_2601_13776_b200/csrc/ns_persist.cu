@@ -324,6 +324,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma::mbar_wait(&tfull_bar[buf], (acc >> 1) & 1);
         umma::tc_fence_after();
         NSP_TRACE(const unsigned long long t_full = ph.ttrace ? gtimer() : 0ull);
+#ifdef ORTH_NSP_TRACE
+        long long cyc[6];
+        cyc[0] = clock64();
+#endif
         NSP_TRACE(if (ph.trace && ew == 0 && lane == 0 && t == tb) ph.trace[(size_t)blockIdx.x * (4 * ph.n + 1) + 1 + 4 * p + 1] = gtimer());
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) {
@@ -346,6 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             else umma::cp_async_wait<0>();
           }
           __syncwarp();
+          NSP_TRACE(if (c == 0) cyc[1] = clock64());
           // per-chunk constants re-derived here (cheap) instead of being held in registers
           const bool wf = upd || write_f;
           const int ldb16 = upd ? (dp->ldx) : (dp->ldr);
@@ -400,6 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
+          NSP_TRACE(if (c == 0) cyc[2] = clock64());
           if (gram && m0 - row0 < n0 - ch * 64) {
             // upper-triangle Gram tile: also write its mirror R[j][i] = R[i][j] (alpha * acc; no diagonal here)
 #pragma unroll 2
@@ -435,18 +441,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           __syncwarp();
+          NSP_TRACE(if (c == 0) cyc[3] = clock64());
         }
 #ifdef ORTH_NSP_TRACE
+        cyc[4] = clock64();
         if (ph.ttrace && lane == 0) {
           const unsigned long long t_end = gtimer();
           const unsigned long long slot = atomicAdd(ph.ttrace, 1ull);
           if (slot < 65536) {
-            unsigned long long* r = ph.ttrace + 1 + 4 * slot;
+            unsigned long long* r = ph.ttrace + 1 + 8 * slot;
             r[0] = ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)p << 40) | ((unsigned long long)ew << 36) |
                    ((unsigned long long)tl.desc << 16) | (unsigned long long)tl.local;
             r[1] = t_start;
             r[2] = t_full;
             r[3] = t_end;
+            r[4] = cyc[1] - cyc[0];   // chunk 0: TMEM ld + staging (+ C wait)
+            r[5] = cyc[2] - cyc[1];   // chunk 0: row pass
+            r[6] = cyc[3] - cyc[2];   // chunk 0: mirror pass
+            r[7] = cyc[4] - cyc[3];   // chunk 1 (all)
           }
         }
 #endif
@@ -1071,7 +1083,7 @@ int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flag
   static unsigned long long* ttrace = nullptr;
   if (tracing) {
     if (!trace) cudaMalloc(&trace, (size_t)p.nsp_ctas * (4 * kNspMaxPhases + 1) * 8);
-    if (!ttrace) cudaMalloc(&ttrace, (1 + 4 * 65536) * 8);
+    if (!ttrace) cudaMalloc(&ttrace, (1 + 8 * 65536) * 8);
     cudaMemsetAsync(ttrace, 0, 8, (cudaStream_t)stream);
     ph.trace = trace;
     ph.ttrace = ttrace;
@@ -1113,13 +1125,13 @@ int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flag
       unsigned long long nrec = 0;
       cudaMemcpy(&nrec, ttrace, 8, cudaMemcpyDeviceToHost);
       nrec = std::min<unsigned long long>(nrec, 65536);
-      std::vector<unsigned long long> r(4 * nrec);
+      std::vector<unsigned long long> r(8 * nrec);
       cudaMemcpy(r.data(), ttrace + 1, r.size() * 8, cudaMemcpyDeviceToHost);
       // per (phase type, M, N, K): count, mean wait-for-accumulator, mean epilogue (warp 0 of the epilogue only)
-      struct Acc { int n = 0; double wait = 0, epi = 0, epimax = 0; };
+      struct Acc { int n = 0; double wait = 0, epi = 0, epimax = 0, c[4] = {0, 0, 0, 0}; };
       std::map<std::tuple<int, int, int, int, int>, Acc> agg;
       for (unsigned long long k = 0; k < nrec; ++k) {
-        const unsigned long long* q = &r[4 * k];
+        const unsigned long long* q = &r[8 * k];
         const int ph_ = (int)((q[0] >> 40) & 0xFF), ew = (int)((q[0] >> 36) & 0xF), desc = (int)((q[0] >> 16) & 0xFFFFF);
         const int local = (int)(q[0] & 0xFFFF);
         if (ew != 0 || ph_ > 3) continue;
@@ -1131,11 +1143,14 @@ int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flag
         a.wait += (q[2] - q[1]) * 1e-3;
         a.epi += (q[3] - q[2]) * 1e-3;
         a.epimax = std::max(a.epimax, (q[3] - q[2]) * 1e-3);
+        for (int z = 0; z < 4; ++z) a.c[z] += (double)q[4 + z];
       }
       for (auto& kv : agg)
-        std::printf("  tile ph%d M=%4d N=%4d K=%4d diag=%d: n=%3d wait %.2f epi %.2f (max %.2f) us\n", std::get<0>(kv.first),
-                    std::get<1>(kv.first), std::get<2>(kv.first), std::get<3>(kv.first), std::get<4>(kv.first),
-                    kv.second.n, kv.second.wait / kv.second.n, kv.second.epi / kv.second.n, kv.second.epimax);
+        std::printf("  tile ph%d M=%4d N=%4d K=%4d diag=%d: n=%3d wait %.2f epi %.2f (max %.2f) us | cyc ld0 %.0f row0 %.0f mir0 %.0f ch1 %.0f\n",
+                    std::get<0>(kv.first), std::get<1>(kv.first), std::get<2>(kv.first), std::get<3>(kv.first),
+                    std::get<4>(kv.first), kv.second.n, kv.second.wait / kv.second.n, kv.second.epi / kv.second.n,
+                    kv.second.epimax, kv.second.c[0] / kv.second.n, kv.second.c[1] / kv.second.n,
+                    kv.second.c[2] / kv.second.n, kv.second.c[3] / kv.second.n);
     }
     const int W = 4 * nphases + 1;
     std::vector<unsigned long long> h((size_t)p.nsp_ctas * W);

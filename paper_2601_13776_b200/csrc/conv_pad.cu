@@ -68,12 +68,14 @@ struct PadArgs {
   int P, TH, R;                  // padded pitch, output rows per tile, input rows per tile
   int tiles_h, tiles_m, tiles_n, num_tiles;
   int abuf_bytes, nabuf, sb;     // A ring (nabuf buffers), B ring stages
-  int copy_bytes;                // one column-shifted copy: R * P * 128
-  int a_tx;                      // bytes landed per A buffer (k copies)
-  // circular padding: per copy b, up to two row pieces (map index, input column start, smem column, width)
-  int pc_map[2 * 7], pc_col[2 * 7], pc_dst[2 * 7], npc[7];
+  int ncopy;                     // 1: one window, tap (a,b) at row d(aP + b); k: column-shifted copies per b
+  int copy_bytes;                // one window / copy: R * P * 128
+  int a_tx;                      // bytes landed per A buffer (ncopy windows)
+  // circular padding: per window b, up to three row pieces (map index, input column start, smem column)
+  int pc_map[3 * 7], pc_col[3 * 7], pc_dst[3 * 7], npc[7];
   int bres;                      // 1: all taps x chunks of one (group, n-tile) resident in smem
   int tiles_per_cta;             // resident mode: contiguous tile range per CTA (set-major order)
+  int stage_off;                 // swapped mode: byte offset of the 256 x 128 B output staging tile
 };
 
 constexpr int A_WARP = 0, B_WARP = 1, MMA_WARP = 2, EPI_WARP0 = 4;
@@ -92,10 +94,16 @@ struct PadMaps {
   CUtensorMap m[MAX_MAPS];
 };
 
-template <int BN>
+// SW (swapped operands, co_g = 64): D^T = W x^T, one tcgen05.mma M=64 (channels) N=256 (pixels)
+// per K step -- the weights are the 64-row A operand, the pixel window the 256-row B operand.  A
+// 128x64 N=64 tile costs ~73 cycles per MMA on B200 (shared-memory bound), the 64x256 one ~128 for
+// 4x the work.  The accumulator (M=64 layout: channel o in TMEM lane (o % 16) + 32 (o / 16)) is
+// transposed through a shared-memory staging tile and written by TMA, one output row per store.
+template <int BN, bool SW>
 __global__ void __launch_bounds__(NTHREADS, 1)
     conv_pad(const float* __restrict__ bias, __nv_bfloat16* __restrict__ out, const __grid_constant__ PadArgs a,
-             const __grid_constant__ PadMaps tmA, const __grid_constant__ CUtensorMap tmB) {
+             const __grid_constant__ PadMaps tmA, const __grid_constant__ CUtensorMap tmB,
+             const __grid_constant__ CUtensorMap tmY) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int B_BYTES = BN * 128;
@@ -104,7 +112,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int SB = a.sb, NA = a.nabuf;
-  if (warp == MMA_WARP) umma::tmem_alloc(&tmem_base_sh, 2 * BN);
+  constexpr int ACC_COLS = SW ? 256 : BN;   // TMEM columns per accumulator
+  if (warp == MMA_WARP) umma::tmem_alloc(&tmem_base_sh, 2 * ACC_COLS);
   if (tid == 0) {
     for (int i = 0; i < NA; ++i) {
       umma::mbar_init(&a_full[i], 1);
@@ -156,17 +165,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const uint32_t dst = abase + ab * a.abuf_bytes;
           const int c = g * a.cr_g + c0;
           umma::mbar_arrive_expect_tx(&a_full[ab], (uint32_t)a.a_tx);
-          for (int b = 0; b < a.k; ++b) {
+          for (int b = 0; b < a.ncopy; ++b) {
             const uint32_t cb = dst + (uint32_t)(b * a.copy_bytes);
             if (!a.circ) {   // one box: R rows x P pixels x 64 channels; out of bounds -> 0
-              umma::tma_load_4d(cb, &tmA.m[0], &a_full[ab], c, a.d * b - a.pl, h0 - a.pt, n);
+              umma::tma_load_4d(cb, &tmA.m[0], &a_full[ab], c, (a.ncopy > 1 ? a.d * b : 0) - a.pl, h0 - a.pt, n);
             } else {
               for (int y = 0; y < a.R; ++y) {
                 const int h = wrapi(h0 - a.pt + y, a.H);
                 const uint32_t row = cb + (uint32_t)(y * a.P) * 128u;
                 for (int pc = 0; pc < a.npc[b]; ++pc)
-                  umma::tma_load_4d(row + (uint32_t)a.pc_dst[2 * b + pc] * 128u, &tmA.m[a.pc_map[2 * b + pc]],
-                                    &a_full[ab], c, a.pc_col[2 * b + pc], h, n);
+                  umma::tma_load_4d(row + (uint32_t)a.pc_dst[3 * b + pc] * 128u, &tmA.m[a.pc_map[3 * b + pc]],
+                                    &a_full[ab], c, a.pc_col[3 * b + pc], h, n);
               }
             }
           }
@@ -206,7 +215,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp == MMA_WARP) {
     if (lane == 0) {
       // ---------------------------------------------------------- MMA issuer
-      constexpr uint32_t IDESC = umma::idesc_bf16(128, BN);
+      constexpr uint32_t IDESC = SW ? umma::idesc_bf16(64, 256) : umma::idesc_bf16(128, BN);
       int u = 0, i = 0, tcount = 0, cur = -1, loads = 0;
       for (int tile = t_begin; tile < t_end; tile += t_step, ++tcount) {
         if (a.bres) {
@@ -221,7 +230,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int acc = tcount & 1;
         umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
         umma::tc_fence_after();
-        const uint32_t d_tmem = tmem + acc * BN;
+        const uint32_t d_tmem = tmem + acc * ACC_COLS;
         int j = 0;   // resident: index of (chunk, tap) in the set
         for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
           const int ab = u % NA;
@@ -237,11 +246,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               umma::tc_fence_after();
             }
             const int ta = tap / a.k, tb = tap - ta * a.k;
-            const uint32_t aa = abuf + (uint32_t)(tb * a.copy_bytes) + (uint32_t)(a.d * ta * a.P) * 128u;
+            const uint32_t aa = a.ncopy > 1 ? abuf + (uint32_t)(tb * a.copy_bytes) + (uint32_t)(a.d * ta * a.P) * 128u
+                                            : abuf + (uint32_t)(a.d * (ta * a.P + tb)) * 128u;
             const uint32_t bb = bbase + (a.bres ? j : st) * B_BYTES;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              umma::mma_bf16(d_tmem, umma::sdesc_sw128(aa + 32 * q), umma::sdesc_sw128(bb + 32 * q), IDESC,
+              umma::mma_bf16(d_tmem, umma::sdesc_sw128((SW ? bb : aa) + 32 * q), umma::sdesc_sw128((SW ? aa : bb) + 32 * q),
+                             IDESC,
                              (c0 | tap | q) != 0);
             if (!a.bres) {
               umma::mma_commit(&b_empty[st]);
@@ -254,11 +265,47 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= EPI_WARP0) {
+  } else if (SW && warp >= EPI_WARP0) {
+    // ------------------------------------------------------------ epilogue (swapped)
+    const int q = warp & 3;
+    uint8_t* S = smem + a.stage_off;    // [256 pixels][64 channels] bf16, 128 B per pixel row
+    int tcount = 0;
+    for (int tile = t_begin; tile < t_end; tile += t_step, ++tcount) {
+      int n, h0, g, n0;
+      decode(tile, n, h0, g, n0);
+      const int acc = tcount & 1;
+      umma::mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
+      umma::tc_fence_after();
+      if (tid == EPI_WARP0 * 32) umma::bulk_wait_read0();   // the previous tile's stores have read S
+      umma::named_bar_sync(2, 128);
+      const int o = 16 * q + lane;                       // lanes 0..15 hold channels 16q .. 16q + 15
+      const float bo = (bias && lane < 16) ? bias[g * a.nout_g + n0 + o] : 0.f;
+#pragma unroll 1
+      for (int j = 0; j < 8; ++j) {                      // 32 pixels per load
+        float v[32];
+        umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 256 + 32 * j), v);
+        if (lane < 16) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            *reinterpret_cast<__nv_bfloat16*>(S + (32 * j + i) * 128 + o * 2) = __float2bfloat16_rn(v[i] + bo);
+        }
+      }
+      umma::tc_fence_before();
+      umma::mbar_arrive(&tempty_bar[acc]);
+      umma::fence_proxy_async_smem();                   // staging writes -> TMA (async proxy) reads
+      umma::named_bar_sync(2, 128);
+      if (tid == EPI_WARP0 * 32) {
+        for (int yy = 0; yy < a.TH && h0 + yy < a.Ho; ++yy)   // one output row (Wo pixels x 64 ch) per store
+          umma::tma_store_3d(&tmY, umma::smem_u32(S + yy * a.P * 128), g * a.nout_g + n0, 0, n * a.Ho + h0 + yy);
+        umma::bulk_commit();
+      }
+    }
+    if (tid == EPI_WARP0 * 32) umma::bulk_wait0();
+  } else if (!SW && warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;
     const int r = q * 32 + lane;
-    const int y = r / a.P, x = r - y * a.P;   // P % 8 == 0 keeps this cheap
+    const int y = r / a.P, x = r - y * a.P;
     int tcount = 0;
     for (int tile = t_begin; tile < t_end; tile += t_step, ++tcount) {
       int n, h0, g, n0;
@@ -297,7 +344,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   umma::tc_fence_before();
   __syncthreads();
-  if (warp == MMA_WARP) umma::tmem_dealloc(tmem, 2 * BN);
+  if (warp == MMA_WARP) umma::tmem_dealloc(tmem, 2 * ACC_COLS);
 }
 
 int sm_count() {
@@ -346,32 +393,35 @@ bool make_act_tmap(CUtensorMap* out, const void* x, int C, int W, int H, int N, 
   return true;
 }
 
-template <int BN>
+template <int BN, bool SW>
 int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out, PadArgs& a,
                int in_C, cudaStream_t stream) {
   const size_t fixed = 1024;
+  const size_t stage = SW ? 256 * 128 : 0;   // swapped mode: output staging tile
   const size_t bset = (size_t)((a.cr_g + 63) / 64) * a.k * a.k * BN * 128;
   size_t smem;
   if (a.bres) {   // resident weights + >= 2 A buffers (caller checked the fit)
     int na = MAX_AB;
-    while (na > 2 && fixed + (size_t)na * a.abuf_bytes + bset > kSmemMax) --na;
+    while (na > 2 && fixed + (size_t)na * a.abuf_bytes + bset + stage > kSmemMax) --na;
     a.nabuf = na;
     a.sb = 1;
     const int grid0 = std::min(a.num_tiles, sm_count());
     a.tiles_per_cta = (a.num_tiles + grid0 - 1) / grid0;
-    smem = fixed + (size_t)na * a.abuf_bytes + bset;
+    a.stage_off = (int)(na * (size_t)a.abuf_bytes + bset);
+    smem = fixed + (size_t)na * a.abuf_bytes + bset + stage;
   } else {
     // A ring: as many buffers as leave room for >= 4 B stages (at least 2)
     int na = MAX_AB;
-    while (na > 2 && fixed + (size_t)na * a.abuf_bytes + 4 * (size_t)BN * 128 > kSmemMax) --na;
-    if (fixed + (size_t)na * a.abuf_bytes + 2 * (size_t)BN * 128 > kSmemMax) return -1;
+    while (na > 2 && fixed + (size_t)na * a.abuf_bytes + 4 * (size_t)BN * 128 + stage > kSmemMax) --na;
+    if (fixed + (size_t)na * a.abuf_bytes + 2 * (size_t)BN * 128 + stage > kSmemMax) return -1;
     a.nabuf = na;
-    a.sb = (int)std::min<size_t>(MAX_SB, (kSmemMax - fixed - (size_t)na * a.abuf_bytes) / ((size_t)BN * 128));
-    smem = fixed + (size_t)na * a.abuf_bytes + (size_t)a.sb * BN * 128;
+    a.sb = (int)std::min<size_t>(MAX_SB, (kSmemMax - fixed - stage - (size_t)na * a.abuf_bytes) / ((size_t)BN * 128));
+    a.stage_off = (int)(na * (size_t)a.abuf_bytes + (size_t)a.sb * BN * 128);
+    smem = fixed + (size_t)na * a.abuf_bytes + (size_t)a.sb * BN * 128 + stage;
   }
   static size_t attr = 0;
   if (smem > attr) {
-    if (cudaFuncSetAttribute(conv_pad<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(conv_pad<BN, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return (int)cudaGetLastError();
     attr = smem;
   }
@@ -381,9 +431,9 @@ int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* b
     if (!make_act_tmap(&maps.m[0], x, in_C, a.W, a.H, a.N, a.P, a.R)) return (int)cudaErrorInvalidValue;
   } else {   // one row box per distinct piece width
     int widths[MAX_MAPS], nw = 0;
-    for (int b = 0; b < a.k; ++b)
+    for (int b = 0; b < a.ncopy; ++b)
       for (int pc = 0; pc < a.npc[b]; ++pc) {
-        const int w0 = a.pc_map[2 * b + pc];   // host stored the width here; replaced by the map index
+        const int w0 = a.pc_map[3 * b + pc];   // host stored the width here; replaced by the map index
         int m = 0;
         while (m < nw && widths[m] != w0) ++m;
         if (m == nw) {
@@ -391,14 +441,27 @@ int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* b
           widths[nw++] = w0;
           if (!make_act_tmap(&maps.m[m], x, in_C, a.W, a.H, a.N, w0, 1)) return (int)cudaErrorInvalidValue;
         }
-        a.pc_map[2 * b + pc] = m;
+        a.pc_map[3 * b + pc] = m;
       }
   }
   CUtensorMap tm;
   if (!make_weight_tmap(&tm, w, w_rows, a.k * a.k, a.cr_g, BN)) return (int)cudaErrorInvalidValue;
+  CUtensorMap ty;
+  std::memset(&ty, 0, sizeof(ty));
+  if (SW) {   // output (C, Wo, N*Ho): one output row (Wo pixels x 64 channels) per box, no swizzle
+    auto enc = tensor_map_encoder();
+    const cuuint64_t dims[3] = {(cuuint64_t)a.out_C, (cuuint64_t)a.Wo, (cuuint64_t)a.N * a.Ho};
+    const cuuint64_t strides[2] = {(cuuint64_t)a.out_C * 2, (cuuint64_t)a.Wo * a.out_C * 2};
+    const cuuint32_t box[3] = {64, (cuuint32_t)a.Wo, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (!enc || enc(&ty, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, out, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return (int)cudaErrorInvalidValue;
+  }
   const int grid = a.bres ? (a.num_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta
-                         : (a.num_tiles < sm_count() ? a.num_tiles : sm_count());
-  conv_pad<BN><<<grid, NTHREADS, smem, stream>>>(bias, out, a, maps, tm);
+                          : (a.num_tiles < sm_count() ? a.num_tiles : sm_count());
+  conv_pad<BN, SW><<<grid, NTHREADS, smem, stream>>>(bias, out, a, maps, tm, ty);
 #ifdef ORTH_CONV_TRACE
   {
     cudaStreamSynchronize(stream);
@@ -433,84 +496,107 @@ int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* b
 // Plan the padded-row path for a (possibly group-packed) forward layer; false
 // if it does not apply (stride != 1, rows wider than one tile, channel slices
 // that would cross groups, circular padding that is not a single wrap, ...).
-static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, int& bn, PadArgs& a) {
+static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, int& bn, PadArgs& a, bool sw) {
   const int ext = L.d * (L.k - 1);
-  // measured (B200, cfg2/cfg3): the TMA-window path wins for narrow layers (co_g <= 64: 97 -> 74 us
-  // at 64ch@32, 280 -> 235 us at 64ch@56); for co_g >= 128 the per-tap gather kernel is as fast or
-  // faster (its N >= 128 MMAs are not smem-bound), so those stay on conv_tc.cu
   if (L.s != 1 || Wo > 128 || Wo < 16 || L.k > 7 || L.co > 64) return false;
   if (L.g > 1 && L.ci % 64 != 0) return false;          // a 64-channel box must stay inside the group
   if (L.ci_f % 8 != 0) return false;                     // TMA row stride: multiple of 16 bytes
   const bool circ = L.desc.padding_mode == ORTH_PAD_CIRCULAR;
   const int pr = ext - L.pl;
-  // circular: the copy rows are the wrapped input rows (P = W, so W % 8 == 0); zero: P = round8(Wo)
-  if (circ && (L.pl < 0 || pr < 0 || Wo != W || W % 8 != 0)) return false;
-  const int P = circ ? W : (Wo + 7) & ~7;
-  if (P > 128) return false;
-  const int TH = std::min(Ho, 128 / P);
-  if (TH < 1 || TH * Wo < 64) return false;
-  const int R = TH + ext;
-  if (R > 256) return false;
+  if (circ && (L.pl < 0 || pr < 0 || Wo != W)) return false;
   const int n = L.co;
   bn = n % 256 == 0 ? 256 : n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : n % 32 == 0 ? 32 : 0;
   if (!bn) return false;
-  const int copy_bytes = R * P * 128;
-  // the last copy's windows read rows up to d (k - 1) P + 127 past its start
-  const int slack_rows = std::max(0, ext * P + 128 - R * P);
-  const size_t abuf = (size_t)L.k * copy_bytes + (size_t)slack_rows * 128;
-  // resident weights: the largest BN (<= 128, dividing co, >= co / 4 so A is re-read at most 4x)
-  // whose whole tap x chunk set fits next to two A buffers
-  const size_t kc = (size_t)(L.ci + 63) / 64;
-  int bres_bn = 0;
-  for (int b = 128; b >= 64 && b * 4 >= n; b /= 2)   // N = 32 MMAs cost as much as N = 128 ones
-    if (n % b == 0 && 1024 + 2 * abuf + kc * L.k * L.k * b * 128 <= kSmemMax) { bres_bn = b; break; }
-  static const bool no_res = std::getenv("ORTH_CONV_NO_BRES") != nullptr;   // A/B switch
-  if (bres_bn && !no_res) bn = bres_bn;
-  if (!bres_bn || no_res) {   // streaming B needs two A buffers + a few B stages
-    if (1024 + 2 * abuf + 2 * (size_t)bn * 128 > kSmemMax) return false;
-  }
-  a = PadArgs{};
-  a.bres = (bres_bn && !no_res) ? 1 : 0;
-  a.N = N; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo;
-  a.k = L.k; a.d = L.d; a.pt = L.pt; a.pl = L.pl; a.pr = pr;
-  a.circ = circ;
-  a.out_C = L.co_f; a.cr_g = L.ci; a.nout_g = L.co;
-  a.P = P; a.TH = TH; a.R = R;
-  a.tiles_h = (Ho + TH - 1) / TH;
-  a.tiles_m = N * a.tiles_h;
-  a.tiles_n = n / bn;
-  a.num_tiles = a.tiles_m * a.tiles_n * L.g;
-  a.copy_bytes = copy_bytes;
-  a.abuf_bytes = (int)abuf;
-  a.a_tx = L.k * copy_bytes;
-  if (circ) {   // copy b covers input columns (x - p_l + d b) mod W, x < W: pieces [s, W) then [0, s)
-    for (int b = 0; b < L.k; ++b) {
-      const int s0 = ((L.d * b - L.pl) % W + W) % W;
-      int np = 0;
-      a.pc_col[2 * b] = s0; a.pc_dst[2 * b] = 0; a.pc_map[2 * b] = W - s0; ++np;   // pc_map: width for now
-      if (s0 > 0) { a.pc_col[2 * b + 1] = 0; a.pc_dst[2 * b + 1] = W - s0; a.pc_map[2 * b + 1] = s0; ++np; }
-      a.npc[b] = np;
+  static const char* layout_env = std::getenv("ORTH_CONV_PAD_LAYOUT");   // "window" | "copies" (A/B)
+  // (1) one window of pitch P = Wo + d(k-1), tap (a, b) at row d(aP + b) (descriptor starts inside a
+  //     swizzle atom cost nothing, measured); (2) k column-shifted copies of pitch round8(Wo)
+  const int MT = sw ? 256 : 128;   // pixels per tile (MMA N when swapped, M otherwise)
+  const size_t stage = sw ? 256 * 128 : 0;
+  if (sw && L.co != 64) return false;
+  for (int layout = 0; layout < 2; ++layout) {
+    const bool single = layout == 0;
+    if (layout_env && std::strcmp(layout_env, single ? "window" : "copies") != 0) continue;
+    if (!single && circ && W % 8 != 0) continue;
+    const int P = single ? Wo + ext : (circ ? W : (Wo + 7) & ~7);
+    if (P > 128 + ext || P > 256) continue;
+    const int TH = std::min(Ho, MT / P);
+    if (TH < 1 || TH * Wo < MT / 2) continue;
+    const int R = TH + ext;
+    if (R > 256) continue;
+    const int ncopy = single ? 1 : L.k;
+    const int copy_bytes = R * P * 128;
+    // the last window's taps read rows up to d(k-1)(P + single) + 127 past its start
+    const int reach = single ? ext * (P + 1) + MT : ext * P + MT;
+    const int slack_rows = std::max(0, reach - R * P);
+    const size_t abuf = ((size_t)ncopy * copy_bytes + (size_t)slack_rows * 128 + 1023) & ~size_t(1023);
+    const size_t kc = (size_t)(L.ci + 63) / 64;
+    int bres_bn = 0;
+    for (int b = 128; b >= 64 && b * 4 >= n; b /= 2)   // N = 32 MMAs cost as much as N = 128 ones
+      if (n % b == 0 && 1024 + 2 * abuf + kc * L.k * L.k * b * 128 + stage <= kSmemMax) { bres_bn = b; break; }
+    static const bool no_res = std::getenv("ORTH_CONV_NO_BRES") != nullptr;   // A/B switch
+    int bnl = bn;
+    if (bres_bn && !no_res) bnl = bres_bn;
+    if (!bres_bn || no_res) {   // streaming B needs two A buffers + a few B stages
+      if (1024 + 2 * abuf + 2 * (size_t)bnl * 128 + stage > kSmemMax) continue;
     }
+    bn = bnl;
+    a = PadArgs{};
+    a.bres = (bres_bn && !no_res) ? 1 : 0;
+    a.N = N; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo;
+    a.k = L.k; a.d = L.d; a.pt = L.pt; a.pl = L.pl; a.pr = pr;
+    a.circ = circ;
+    a.out_C = L.co_f; a.cr_g = L.ci; a.nout_g = L.co;
+    a.P = P; a.TH = TH; a.R = R;
+    a.tiles_h = (Ho + TH - 1) / TH;
+    a.tiles_m = N * a.tiles_h;
+    a.tiles_n = n / bn;
+    a.num_tiles = a.tiles_m * a.tiles_n * L.g;
+    a.ncopy = ncopy;
+    a.copy_bytes = copy_bytes;
+    a.abuf_bytes = (int)abuf;
+    a.a_tx = ncopy * copy_bytes;
+    if (circ) {
+      for (int b = 0; b < ncopy; ++b) {
+        int np = 0;
+        if (single) {   // row = x[W - p_l, W) | x[0, W) | x[0, p_r)
+          if (L.pl) { a.pc_col[3 * b + np] = W - L.pl; a.pc_dst[3 * b + np] = 0; a.pc_map[3 * b + np] = L.pl; ++np; }
+          a.pc_col[3 * b + np] = 0; a.pc_dst[3 * b + np] = L.pl; a.pc_map[3 * b + np] = W; ++np;
+          if (pr) { a.pc_col[3 * b + np] = 0; a.pc_dst[3 * b + np] = L.pl + W; a.pc_map[3 * b + np] = pr; ++np; }
+        } else {        // copy b covers input columns (x - p_l + d b) mod W: pieces [s, W) then [0, s)
+          const int s0 = ((L.d * b - L.pl) % W + W) % W;
+          a.pc_col[3 * b] = s0; a.pc_dst[3 * b] = 0; a.pc_map[3 * b] = W - s0; ++np;   // pc_map: width for now
+          if (s0 > 0) { a.pc_col[3 * b + 1] = 0; a.pc_dst[3 * b + 1] = W - s0; a.pc_map[3 * b + 1] = s0; ++np; }
+        }
+        a.npc[b] = np;
+      }
+    }
+    return true;
   }
-  return true;
+  return false;
 }
 
 // returns -1 when the padded-row path does not apply (caller falls back), else 0 / a CUDA error
 int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
                           int H, int W, int Ho, int Wo, void* stream) {
-  int bn = 0;
-  PadArgs a;
-  if (!pad_args(L, N, H, W, Ho, Wo, bn, a)) return -1;
-  if (a.num_tiles == 0) return 0;
-  if (((uintptr_t)x & 15) != 0) return -1;
+  if (((uintptr_t)x & 15) != 0 || ((uintptr_t)y & 15) != 0) return -1;
   const auto* w = static_cast<const __nv_bfloat16*>(kernel);
   auto* out = static_cast<__nv_bfloat16*>(y);
   cudaStream_t s = (cudaStream_t)stream;
+  static const bool no_swap = std::getenv("ORTH_CONV_NO_SWAP") != nullptr;   // A/B switch
+  int bn = 0;
+  PadArgs a;
+  if (!no_swap && pad_args(L, N, H, W, Ho, Wo, bn, a, true) && bn == 64) {   // 64 channels x 256 pixels per MMA
+    if (a.num_tiles == 0) return 0;
+    const int e = launch_pad<64, true>(x, w, L.co_f, bias, out, a, L.ci_f, s);
+    if (e >= 0) return e;
+  }
+  if (!pad_args(L, N, H, W, Ho, Wo, bn, a, false)) return -1;
+  if (a.num_tiles == 0) return 0;
   switch (bn) {
-    case 32: return launch_pad<32>(x, w, L.co_f, bias, out, a, L.ci_f, s);
-    case 64: return launch_pad<64>(x, w, L.co_f, bias, out, a, L.ci_f, s);
-    case 128: return launch_pad<128>(x, w, L.co_f, bias, out, a, L.ci_f, s);
-    default: return launch_pad<256>(x, w, L.co_f, bias, out, a, L.ci_f, s);
+    case 32: return launch_pad<32, false>(x, w, L.co_f, bias, out, a, L.ci_f, s);
+    case 64: return launch_pad<64, false>(x, w, L.co_f, bias, out, a, L.ci_f, s);
+    case 128: return launch_pad<128, false>(x, w, L.co_f, bias, out, a, L.ci_f, s);
+    default: return launch_pad<256, false>(x, w, L.co_f, bias, out, a, L.ci_f, s);
   }
 }
 

@@ -76,6 +76,7 @@ struct PadArgs {
   int bres;                      // 1: all taps x chunks of one (group, n-tile) resident in smem
   int tiles_per_cta;             // resident mode: contiguous tile range per CTA (set-major order)
   int stage_off;                 // swapped mode: byte offset of the 256 x 128 B output staging tile
+  int flip;                      // 1: weight tap t read from row k^2-1-t (stride-1 adjoint as a forward conv)
 };
 
 constexpr int A_WARP = 0, B_WARP = 1, MMA_WARP = 2, EPI_WARP0 = 4;
@@ -199,7 +200,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           int j = 0;
           for (int c0 = 0; c0 < a.cr_g; c0 += 64)
             for (int tap = 0; tap < kk2; ++tap, ++j)
-              umma::tma_load_3d(bbase + j * B_BYTES, &tmB, &b_full[0], c0, tap, g * a.nout_g + n0);
+              umma::tma_load_3d(bbase + j * B_BYTES, &tmB, &b_full[0], c0, a.flip ? kk2 - 1 - tap : tap,
+                                g * a.nout_g + n0);
           ++loads;
           continue;
         }
@@ -208,7 +210,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int st = i % SB;
             if (i >= SB) umma::mbar_wait(&b_empty[st], ((i / SB) - 1) & 1);
             umma::mbar_arrive_expect_tx(&b_full[st], B_BYTES);
-            umma::tma_load_3d(bbase + st * B_BYTES, &tmB, &b_full[st], c0, tap, g * a.nout_g + n0);
+            umma::tma_load_3d(bbase + st * B_BYTES, &tmB, &b_full[st], c0, a.flip ? kk2 - 1 - tap : tap,
+                              g * a.nout_g + n0);
           }
       }
     }
@@ -575,9 +578,10 @@ static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, in
   return false;
 }
 
-// returns -1 when the padded-row path does not apply (caller falls back), else 0 / a CUDA error
+// returns -1 when the padded-row path does not apply (caller falls back), else 0 / a CUDA error.
+// flip = 1: L is the forward view of a stride-1 adjoint (see launch_conv_bwd_reuse).
 int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
-                          int H, int W, int Ho, int Wo, void* stream) {
+                          int H, int W, int Ho, int Wo, void* stream, int flip) {
   if (((uintptr_t)x & 15) != 0 || ((uintptr_t)y & 15) != 0) return -1;
   const auto* w = static_cast<const __nv_bfloat16*>(kernel);
   auto* out = static_cast<__nv_bfloat16*>(y);
@@ -587,11 +591,13 @@ int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* b
   PadArgs a;
   if (!no_swap && pad_args(L, N, H, W, Ho, Wo, bn, a, true) && bn == 64) {   // 64 channels x 256 pixels per MMA
     if (a.num_tiles == 0) return 0;
+    a.flip = flip;
     const int e = launch_pad<64, true>(x, w, L.co_f, bias, out, a, L.ci_f, s);
     if (e >= 0) return e;
   }
   if (!pad_args(L, N, H, W, Ho, Wo, bn, a, false)) return -1;
   if (a.num_tiles == 0) return 0;
+  a.flip = flip;
   switch (bn) {
     case 32: return launch_pad<32, false>(x, w, L.co_f, bias, out, a, L.ci_f, s);
     case 64: return launch_pad<64, false>(x, w, L.co_f, bias, out, a, L.ci_f, s);

@@ -854,6 +854,18 @@ int launch_conv_bwd_tc(const LayerInfo& L0, const void* kernel, void* wt_scratch
   transpose_w_kernel<<<tg, 256, 0, s>>>((const __nv_bfloat16*)kernel, (__nv_bfloat16*)wt_scratch, L.g, L.co, L.ci,
                                         taps);
   if (int e = (int)cudaGetLastError()) return e;
+  static const bool no_reuse = std::getenv("ORTH_CONV_NO_REUSE") != nullptr;   // A/B switch
+  if (L.s == 1 && !no_reuse) {
+    // Stride 1: x[h, w] = sum_{a,b} K[a,b]^T y[h + p_t - d a, w + p_l - d b] is the forward conv of y
+    // with the tap-flipped transposed kernel and padding d(k-1) - p (mod H for circular, where the
+    // grids coincide), so it runs on the padded-window kernel (conv_pad.cu).
+    LayerInfo F = L;
+    F.ci = L.co; F.co = L.ci; F.ci_f = L.co_f; F.co_f = L.ci_f;
+    F.pt = L.d * (L.k - 1) - L.pt; F.pl = L.d * (L.k - 1) - L.pl;
+    F.pb = L.d * (L.k - 1) - L.pb; F.pr = L.d * (L.k - 1) - L.pr;
+    const int e = launch_conv_fwd_reuse(F, wt_scratch, bias, y, x, N, Ho, Wo, H, W, stream, 1);
+    if (e >= 0) return e;
+  }
   TcConvArgs a;
   base_args(a, L, N, H, W, Ho, Wo);
   a.transposed = 1;

@@ -242,9 +242,10 @@ int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int 
 // tensor-core stem (ci = 3, k = 3 | 4, co in {32, 64, 128}); -1 = not applicable
 int launch_conv_fwd_stem(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
                          int H, int W, int Ho, int Wo, void* stream);
-// forward conv with shifted-copy A reuse (stride 1, wide images); -1 = not applicable
+// forward conv over TMA-loaded padded row windows (stride 1, rows <= 128 px); -1 = not applicable.
+// flip = 1 reads weight tap t from row k^2-1-t (a stride-1 adjoint in its forward-conv form).
 int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
-                          int H, int W, int Ho, int Wo, void* stream);
+                          int H, int W, int Ho, int Wo, void* stream, int flip = 0);
 // persistent NS: build the CTA-group partition (after build_ns_tma); launch all
 // phases (flags per phase: bit0 gram, bit1 3-pass, bit2 X parity, bit3 write lo,
 // bit4 write fp32 R)

@@ -176,6 +176,10 @@ CONV_CASES = [  # (ci, co, k, s, d, g, mode, H, kind)
     (64, 64, 3, 1, 1, 1, "circular", 24, "conv"), (64, 64, 5, 1, 2, 1, "zeros", 20, "conv"),
     (48, 64, 3, 1, 1, 1, "circular", 16, "conv"), (128, 64, 3, 1, 1, 1, "circular", 16, "conv"),
     (64, 32, 3, 1, 1, 1, "zeros", 33, "conv"),
+    # stride-1 adjoints on the TMA-window path (tap-flipped forward form), incl. packed groups
+    (64, 64, 3, 1, 1, 1, "circular", 24, "convT"), (64, 64, 3, 1, 2, 1, "zeros", 20, "convT"),
+    (64, 64, 3, 1, 2, 2, "circular", 20, "convT"), (1024, 1024, 3, 1, 2, 32, "circular", 16, "convT"),
+    (128, 64, 5, 1, 1, 1, "zeros", 17, "convT"),
 ]
 
 

@@ -47,11 +47,13 @@
 // diagnostics: per CTA, per tile (first 32) globaltimer stamps
 //   [0] A issued, [1] MMA saw A landed, [2] epilogue saw accumulator, [3] epilogue done
 __device__ unsigned long long conv_trace[160 * 32 * 4];
+__device__ unsigned long long conv_trace_clk[160 * 32 * 4];
 __device__ __forceinline__ void ctrace(int tcount, int q) {
   if (tcount < 32) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     conv_trace[(blockIdx.x * 32 + tcount) * 4 + q] = t;
+    conv_trace_clk[(blockIdx.x * 32 + tcount) * 4 + q] = clock64();
   }
 }
 #define CTRACE(tc, q) ctrace(tc, q)
@@ -75,7 +77,10 @@ struct PadArgs {
   int pc_map[3 * 7], pc_col[3 * 7], pc_dst[3 * 7], npc[7];
   int bres;                      // 1: all taps x chunks of one (group, n-tile) resident in smem
   int tiles_per_cta;             // resident mode: contiguous tile range per CTA (set-major order)
-  int stage_off;                 // swapped mode: byte offset of the 256 x 128 B output staging tile
+  int stage_off;                 // swapped mode: byte offset of the output staging area
+  int stage_row;                 // swapped mode: bytes per staged output row (Wo x 128 B, 1024-aligned)
+  int slack_bytes;               // the last taps read this far past a window (junk pixels only): the next
+                                 // buffer / the B region must cover it, so buffers need no padding
   int flip;                      // 1: weight tap t read from row k^2-1-t (stride-1 adjoint as a forward conv)
 };
 
@@ -270,8 +275,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncwarp();
   } else if (SW && warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue (swapped)
+    // Warp q reads TMEM lanes 32q .. 32q+15 (channels 16q .. 16q+15) as mma-style 8x8 fragments
+    // (16x256b loads) and writes them transposed with stmatrix: 16 B = 8 channels of one pixel per row.
+    // Staging: output row yy at S + yy * stage_row, pixel x at + 128 x, 16-B chunk c at position
+    // c ^ (x & 7) (the TMA SWIZZLE_128B layout, conflict-free for 8 consecutive pixels); window
+    // columns that are not outputs go to a per-lane dump slot after the rows.
     const int q = warp & 3;
-    uint8_t* S = smem + a.stage_off;    // [256 pixels][64 channels] bf16, 128 B per pixel row
+    uint8_t* S = smem + a.stage_off;
+    const uint32_t s_base = umma::smem_u32(S);
+    const uint32_t dump = s_base + (uint32_t)(a.TH * a.stage_row) + (uint32_t)lane * 16u;
+    const int m = lane >> 3, jrow = lane & 7;
+    const uint32_t chunk = (uint32_t)(2 * q + (m & 1));
     int tcount = 0;
     for (int tile = t_begin; tile < t_end; tile += t_step, ++tcount) {
       int n, h0, g, n0;
@@ -279,28 +293,48 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int acc = tcount & 1;
       umma::mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
       umma::tc_fence_after();
+      if (tid == EPI_WARP0 * 32) CTRACE(tcount, 2);
       if (tid == EPI_WARP0 * 32) umma::bulk_wait_read0();   // the previous tile's stores have read S
       umma::named_bar_sync(2, 128);
-      const int o = 16 * q + lane;                       // lanes 0..15 hold channels 16q .. 16q + 15
-      const float bo = (bias && lane < 16) ? bias[g * a.nout_g + n0 + o] : 0.f;
+      const int ob = g * a.nout_g + n0 + 16 * q + (lane >> 2);
+      const float b_lo = bias ? bias[ob] : 0.f, b_hi = bias ? bias[ob + 8] : 0.f;
+      const int rows = min(a.TH, a.Ho - h0);
 #pragma unroll 1
-      for (int j = 0; j < 8; ++j) {                      // 32 pixels per load
-        float v[32];
-        umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 256 + 32 * j), v);
-        if (lane < 16) {
+      for (int c = 0; c < 256; c += 32) {
+        uint32_t r[16];
+        umma::tmem_ld_16x256b_x4(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 256 + c), r);
+        umma::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            *reinterpret_cast<__nv_bfloat16*>(S + (32 * j + i) * 128 + o * 2) = __float2bfloat16_rn(v[i] + bo);
+        for (int h = 0; h < 2; ++h) {
+          const int w = c + 16 * h + 8 * (m >> 1) + jrow;   // window pixel this lane addresses
+          const int y = w / a.P, x = w - y * a.P;
+          const uint32_t dst = (y < rows && x < a.Wo)
+                                   ? s_base + (uint32_t)(y * a.stage_row + x * 128) + ((chunk ^ (uint32_t)(x & 7)) << 4)
+                                   : dump;
+          uint32_t pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float bb = (e & 1) ? b_hi : b_lo;
+            __nv_bfloat162 v2 = __floats2bfloat162_rn(__uint_as_float(r[8 * h + 2 * e]) + bb,
+                                                      __uint_as_float(r[8 * h + 2 * e + 1]) + bb);
+            pk[e] = *reinterpret_cast<uint32_t*>(&v2);
+          }
+          umma::stmatrix_x4_trans(dst, pk[0], pk[1], pk[2], pk[3]);
         }
       }
       umma::tc_fence_before();
       umma::mbar_arrive(&tempty_bar[acc]);
       umma::fence_proxy_async_smem();                   // staging writes -> TMA (async proxy) reads
       umma::named_bar_sync(2, 128);
+#ifdef ORTH_CONV_EXP
+      if (false) {
+#else
       if (tid == EPI_WARP0 * 32) {
-        for (int yy = 0; yy < a.TH && h0 + yy < a.Ho; ++yy)   // one output row (Wo pixels x 64 ch) per store
-          umma::tma_store_3d(&tmY, umma::smem_u32(S + yy * a.P * 128), g * a.nout_g + n0, 0, n * a.Ho + h0 + yy);
+#endif
+        for (int yy = 0; yy < rows; ++yy)   // one output row (Wo pixels x 64 ch) per store
+          umma::tma_store_3d(&tmY, s_base + (uint32_t)(yy * a.stage_row), g * a.nout_g + n0, 0, n * a.Ho + h0 + yy);
         umma::bulk_commit();
+        CTRACE(tcount, 3);
       }
     }
     if (tid == EPI_WARP0 * 32) umma::bulk_wait0();
@@ -400,7 +434,7 @@ template <int BN, bool SW>
 int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out, PadArgs& a,
                int in_C, cudaStream_t stream) {
   const size_t fixed = 1024;
-  const size_t stage = SW ? 256 * 128 : 0;   // swapped mode: output staging tile
+  const size_t stage = SW ? (size_t)a.TH * a.stage_row + 1024 : 0;   // swapped mode: output staging rows
   const size_t bset = (size_t)((a.cr_g + 63) / 64) * a.k * a.k * BN * 128;
   size_t smem;
   if (a.bres) {   // resident weights + >= 2 A buffers (caller checked the fit)
@@ -422,6 +456,7 @@ int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* b
     a.stage_off = (int)(na * (size_t)a.abuf_bytes + (size_t)a.sb * BN * 128);
     smem = fixed + (size_t)na * a.abuf_bytes + (size_t)a.sb * BN * 128 + stage;
   }
+  if (smem - fixed - (size_t)a.nabuf * a.abuf_bytes < (size_t)a.slack_bytes) return -1;   // reads stay in smem
   static size_t attr = 0;
   if (smem > attr) {
     if (cudaFuncSetAttribute(conv_pad<BN, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -451,14 +486,14 @@ int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* b
   if (!make_weight_tmap(&tm, w, w_rows, a.k * a.k, a.cr_g, BN)) return (int)cudaErrorInvalidValue;
   CUtensorMap ty;
   std::memset(&ty, 0, sizeof(ty));
-  if (SW) {   // output (C, Wo, N*Ho): one output row (Wo pixels x 64 channels) per box, no swizzle
+  if (SW) {   // output (C, Wo, N*Ho): one output row (Wo pixels x 64 channels) per box, SWIZZLE_128B staging
     auto enc = tensor_map_encoder();
     const cuuint64_t dims[3] = {(cuuint64_t)a.out_C, (cuuint64_t)a.Wo, (cuuint64_t)a.N * a.Ho};
     const cuuint64_t strides[2] = {(cuuint64_t)a.out_C * 2, (cuuint64_t)a.Wo * a.out_C * 2};
     const cuuint32_t box[3] = {64, (cuuint32_t)a.Wo, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     if (!enc || enc(&ty, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, out, dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return (int)cudaErrorInvalidValue;
   }
@@ -472,20 +507,24 @@ int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* b
     cudaMemcpyFromSymbol(h, conv_trace, sizeof(h));
     double d01 = 0, d12 = 0, d23 = 0, per = 0;
     int cnt = 0, cnt2 = 0;
+    static unsigned long long hc[160 * 32 * 4];
+    cudaMemcpyFromSymbol(hc, conv_trace_clk, sizeof(hc));
+    double c12 = 0;
     for (int c = 0; c < grid && c < 160; ++c)
       for (int t = 1; t < 16; ++t) {
         const unsigned long long* r = &h[(c * 32 + t) * 4];
         const unsigned long long* r0 = &h[(c * 32 + t - 1) * 4];
         if (!r[0] || !r[3] || !r0[3]) continue;
         d01 += (double)(r[1] - r[0]); d12 += (double)(r[2] - r[1]); d23 += (double)(r[3] - r[2]);
+        c12 += (double)(hc[(c * 32 + t) * 4 + 2] - hc[(c * 32 + t) * 4 + 1]);
         per += (double)(r[3] - r0[3]);
         ++cnt;
       }
     (void)cnt2;
     if (cnt)
-      std::printf("conv_pad BN=%d bres=%d TH=%d P=%d R=%d na=%d sb=%d tiles=%d grid=%d: A issue->landed %.2f, ->acc ready %.2f, epi %.2f, per-tile %.2f us\n",
+      std::printf("conv_pad BN=%d bres=%d TH=%d P=%d R=%d na=%d sb=%d tiles=%d grid=%d: A issue->landed %.2f, ->acc ready %.2f, epi %.2f, per-tile %.2f us, MMA span %.0f cycles (%.0f MHz)\n",
                   BN, a.bres, a.TH, a.P, a.R, a.nabuf, a.sb, a.num_tiles, grid, d01 / cnt * 1e-3, d12 / cnt * 1e-3,
-                  d23 / cnt * 1e-3, per / cnt * 1e-3);
+                  d23 / cnt * 1e-3, per / cnt * 1e-3, c12 / cnt, 1e3 * c12 / d12);
     cudaMemset(conv_trace, 0, 0);
     static unsigned long long z[160 * 32 * 4];
     cudaMemcpyToSymbol(conv_trace, z, sizeof(z));
@@ -514,7 +553,7 @@ static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, in
   // (1) one window of pitch P = Wo + d(k-1), tap (a, b) at row d(aP + b) (descriptor starts inside a
   //     swizzle atom cost nothing, measured); (2) k column-shifted copies of pitch round8(Wo)
   const int MT = sw ? 256 : 128;   // pixels per tile (MMA N when swapped, M otherwise)
-  const size_t stage = sw ? 256 * 128 : 0;
+  const int stage_row = (Wo * 128 + 1023) & ~1023;
   if (sw && L.co != 64) return false;
   for (int layout = 0; layout < 2; ++layout) {
     const bool single = layout == 0;
@@ -526,12 +565,13 @@ static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, in
     if (TH < 1 || TH * Wo < MT / 2) continue;
     const int R = TH + ext;
     if (R > 256) continue;
+    const size_t stage = sw ? (size_t)TH * stage_row + 1024 : 0;   // staged output rows + dump slots
     const int ncopy = single ? 1 : L.k;
     const int copy_bytes = R * P * 128;
     // the last window's taps read rows up to d(k-1)(P + single) + 127 past its start
     const int reach = single ? ext * (P + 1) + MT : ext * P + MT;
     const int slack_rows = std::max(0, reach - R * P);
-    const size_t abuf = ((size_t)ncopy * copy_bytes + (size_t)slack_rows * 128 + 1023) & ~size_t(1023);
+    const size_t abuf = ((size_t)ncopy * copy_bytes + 1023) & ~size_t(1023);
     const size_t kc = (size_t)(L.ci + 63) / 64;
     int bres_bn = 0;
     for (int b = 128; b >= 64 && b * 4 >= n; b /= 2)   // N = 32 MMAs cost as much as N = 128 ones
@@ -550,6 +590,8 @@ static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, in
     a.circ = circ;
     a.out_C = L.co_f; a.cr_g = L.ci; a.nout_g = L.co;
     a.P = P; a.TH = TH; a.R = R;
+    a.stage_row = stage_row;
+    a.slack_bytes = slack_rows * 128;
     a.tiles_h = (Ho + TH - 1) / TH;
     a.tiles_m = N * a.tiles_h;
     a.tiles_n = n / bn;

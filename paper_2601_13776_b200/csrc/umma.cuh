@@ -104,6 +104,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 16 lanes x 256 bits, 4 repetitions (32 columns).  Thread t gets, for rep k:
+// r[4k], r[4k+1] = lane t/4, columns 8k + 2(t%4) + {0,1}; r[4k+2], r[4k+3] = lane 8 + t/4, same
+// columns (the mma C-fragment layout; measured, tools/micro/tmem_layout.cu).  No wait.
+__device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Four 8x8 b16 matrices stored transposed: memory row j of matrix m (address from thread 8m + j) gets
+// fragment column j (thread t holds row t/4, columns 2(t%4), 2(t%4)+1 of each matrix, one register each).
+__device__ __forceinline__ void stmatrix_x4_trans(uint32_t saddr, uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(m0),
+               "r"(m1), "r"(m2), "r"(m3)
+               : "memory");
+}
+
 // ---------------------------------------------------------------- descriptors
 // K-major SWIZZLE_128B smem descriptor (version 1 = sm_100, SBO = 1024 B).
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256, 1) tcg_kernel(const TcgDesc* __restrict__
                                                      const TcgSeg* __restrict__ segs) {
   constexpr int TILE = 128 * 128, STAGE = 4 * TILE;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = umma::align1024_smem(smem_raw);
   __shared__ uint64_t empty_bar[S];
   __shared__ uint64_t done_bar;
   __shared__ uint32_t tmem_base_sh;
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(256, 1) tcg_tma_kernel(const TcgDesc* __restri
                                                          const CUtensorMap* __restrict__ maps) {
   constexpr int TILE = 128 * 128, STAGE = 4 * TILE;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = umma::align1024_smem(smem_raw);
   __shared__ uint64_t full_bar[S], empty_bar[S], done_bar;
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
              const __grid_constant__ PadMaps tmA, const __grid_constant__ CUtensorMap tmB,
              const __grid_constant__ CUtensorMap tmY) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = umma::align1024_smem(smem_raw);
   constexpr int B_BYTES = BN * 128;
   __shared__ uint64_t a_full[MAX_AB], a_empty[MAX_AB], b_full[MAX_SB], b_empty[MAX_SB], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;

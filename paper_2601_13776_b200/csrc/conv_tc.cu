@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     conv_ws(const __nv_bfloat16* __restrict__ in, const float* __restrict__ bias, __nv_bfloat16* __restrict__ out,
             const __grid_constant__ TcConvArgs a, const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = umma::align1024_smem(smem_raw);
   constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
   int* tab = reinterpret_cast<int*>(smem + S * STAGE);   // [valid tap j][128] input pixel, -1 = padding
   __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2];
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     conv_pair(const __nv_bfloat16* __restrict__ in, const float* __restrict__ bias, __nv_bfloat16* __restrict__ out,
               const __grid_constant__ TcConvArgs a, const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = umma::align1024_smem(smem_raw);
   constexpr int HB = BN / 2;   // B rows held by each CTA
   constexpr int A_BYTES = 128 * 128, B_BYTES = HB * 128, STAGE = A_BYTES + B_BYTES;
   int* tab = reinterpret_cast<int*>(smem + S * STAGE);

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
   constexpr int TILE = 128 * 128;                     // bytes of one 128 x 64 bf16 tile
   constexpr int STAGE = (SPLIT ? 4 : 2) * TILE;       // A_hi, B_hi (, A_lo, B_lo)
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = umma::align1024_smem(smem_raw);
   __shared__ uint64_t empty_bar[S];
   __shared__ uint64_t done_bar;
   __shared__ uint32_t tmem_base_sh;

@@ -145,10 +145,11 @@ __device__ __forceinline__ void power_grid_sync(unsigned* bar, unsigned target) 
   if (threadIdx.x == 0) {
     __threadfence();
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    unsigned v;
+    unsigned v;   // relaxed polls + one acquire fence (an ld.acquire per poll invalidates L1 each time)
     do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
     } while (v < target);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
 }

@@ -66,7 +66,11 @@ namespace {
 
 constexpr int kThreads = 320;    // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 constexpr int kSlot = 32768;
+#ifdef ORTH_NS_SLOTS
+constexpr int kSlots = ORTH_NS_SLOTS;
+#else
 constexpr int kSlots = 4;
+#endif
 constexpr int kEpiWarps = 8;
 // per epilogue warp: the accumulator chunk Sw (32 x 32 fp32) and the C tile of
 // both chunks Sc[2] (32 x 32 fp32 each), float4 slots XOR-swizzled by row
@@ -90,10 +94,19 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {   // low half 
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+// Spin until *p >= target, then acquire.  The polls are relaxed: an ld.acquire.gpu
+// compiles to a load + CCTL.IVALL, and a producer spinning on it invalidates the
+// SM's L1 every few tens of ns, stalling the epilogue warps' shared/global traffic.
+// One fence after the observed value gives the same acquire ordering.
+__device__ __forceinline__ void wait_geq_acquire(const unsigned* p, unsigned target, bool sleep) {
+  while (ld_relaxed_gpu(p) < target)
+    if (sleep) __nanosleep(32);
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 __device__ __forceinline__ int ld_acquire_cta_shared(const int* p) {
   int v;
@@ -110,10 +123,7 @@ __device__ __forceinline__ void st_release_cta_shared(int* p, int v) {
 // acquire polls (measured 1.2 us for 148 CTAs vs 2.7 us for count+generation).
 __device__ __forceinline__ void group_sync(unsigned* bar, unsigned target) {
   asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-  unsigned v;
-  do {
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-  } while (v < target);
+  wait_geq_acquire(bar, target, false);
 }
 
 __device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int k0, int mn0,
@@ -134,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const NsGroup* __restrict__ ctas, unsigned* bars,
                       NspBufs bufs, const CUtensorMap* __restrict__ maps, const __grid_constant__ NspPhases ph) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = umma::align1024_smem(smem_raw);
   float* stage = reinterpret_cast<float*>(smem + kSlots * kSlot);
   __shared__ uint64_t full_bar[kSlots], empty_bar[kSlots], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
@@ -494,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    int n_items, unsigned* ctr, NspBufs bufs, const CUtensorMap* __restrict__ maps,
                    const __grid_constant__ NspPhases ph) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = umma::align1024_smem(smem_raw);
   float* stage = reinterpret_cast<float*>(smem + kSlots * kSlot);
   __shared__ uint64_t full_bar[kSlots], empty_bar[kSlots], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
@@ -536,9 +546,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (kq >= 8) umma::mbar_wait(&qempty[slot], ((kq >> 3) - 1) & 1);
         const int idx = (int)atomicAdd(ctr, 1u);
         if (idx < n_items) {
+          NSP_TRACE(if (ph.ttrace) { ph.ttrace[16 * idx] = gtimer(); ph.ttrace[16 * idx + 3] = blockIdx.x; });
           const NsItem it0 = items[idx];
           if (it0.wait_ctr >= 0)   // data dependency: the previous phase of this matrix is complete
-            while (ld_acquire_gpu(ctr + it0.wait_ctr) < it0.wait_target) __nanosleep(32);
+            wait_geq_acquire(ctr + it0.wait_ctr, it0.wait_target, true);
+          NSP_TRACE(if (ph.ttrace) ph.ttrace[16 * idx + 1] = gtimer());
         }
         // publish only after the dependency is met: the epilogue prefetches C as soon as it sees the item
         q[slot] = idx < n_items ? idx : -1;
@@ -613,6 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma::mbar_wait(&full_bar[s], (fpar >> s) & 1u);
             fpar ^= 1u << s;
             umma::tc_fence_after();
+            NSP_TRACE(if (ph.ttrace && kb == 0) ph.ttrace[16 * idx + 4] = gtimer());
             const uint32_t ah = ring + s * kSlot, al = ah + 32768;
             const uint32_t bh = sym ? ah : ah + 16384, bl = sym ? al : ah + 49152;
 #pragma unroll
@@ -694,8 +707,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma::cp_async_commit();
           }
         }
+        NSP_TRACE(if (ph.ttrace && ew == 0 && lane == 0) ph.ttrace[16 * idx + 6] = gtimer());
         umma::mbar_wait(&tfull_bar[buf], (acc >> 1) & 1);
         umma::tc_fence_after();
+        NSP_TRACE(if (ph.ttrace && ew == 0 && lane == 0) ph.ttrace[16 * idx + 5] = gtimer());
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) {
 #pragma unroll
@@ -712,13 +727,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) umma::mbar_arrive(&tempty_bar[buf]);
           }
+          NSP_TRACE(if (ph.ttrace && ew == 0 && lane == 0) ph.ttrace[16 * idx + 8 + 3 * c] = gtimer());
           if (upd) {
             if (c == 0) umma::cp_async_wait<1>();
             else umma::cp_async_wait<0>();
           }
           __syncwarp();
+          NSP_TRACE(if (ph.ttrace && ew == 0 && lane == 0) ph.ttrace[16 * idx + 9 + 3 * c] = gtimer());
           // per-chunk constants re-derived here (cheap) instead of being held in registers
+#ifdef ORTH_NS_EXP   // timing experiment only (wrong results): fp32 X written by the last phases only
+          const bool wf = p >= ph.n - 2;
+#else
           const bool wf = upd || write_f;
+#endif
           const int ldb16 = upd ? (dp->ldx) : (dp->ldr);
           const int64_t b_off = upd ? (dp->bx_off) : (dp->br_off);
           __nv_bfloat16* oh = (upd ? pick(bufs.xh, par ^ 1) : bufs.rh) + b_off;
@@ -771,6 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
+          NSP_TRACE(if (ph.ttrace && ew == 0 && lane == 0) ph.ttrace[16 * idx + 10 + 3 * c] = gtimer());
           if (gram && m0 - row0 < n0 - ch * 64) {
             // upper-triangle Gram tile: also write its mirror R[j][i] = R[i][j] (alpha * acc; no diagonal here)
 #pragma unroll 2
@@ -810,11 +832,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++acc;
       }
       // ---- item done: publish this tile's writes, bump the matrix's counter, free the queue slot
+      NSP_TRACE(if (ph.ttrace && ew == 0 && lane == 0) ph.ttrace[16 * idx + 7] = gtimer());
       fence_proxy_async_global();
       umma::named_bar_sync(1, 32 * kEpiWarps);
-      if (ew == 0 && lane == 0) {
-        __threadfence();
+      if (ew == 0 && lane == 0) {   // release (cumulative over the barrier) orders all epilogue warps' writes
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr + item.done_ctr) : "memory");
+        NSP_TRACE(if (ph.ttrace) ph.ttrace[16 * idx + 2] = gtimer());
       }
       if (lane == 0) umma::mbar_arrive(&qempty[slot]);
     }
@@ -1056,6 +1079,82 @@ static int build_flow_items(Plan& p, const uint8_t* flags, int nphases) {
   return 0;
 }
 
+// diagnostics (ORTH_NSP_TRACE builds, ORTH_NS_TRACE=1): per item {claimed, dependency met, done, cta}
+// -> per phase of the three largest matrices: span and where the time went; CTA busy fraction
+static void flow_trace_report(const Plan& p, const uint8_t* flags, int nphases, const unsigned long long* ttrace,
+                              cudaStream_t stream) {
+  cudaStreamSynchronize(stream);
+  const int n = p.nsf_n_items;
+  std::vector<unsigned long long> r((size_t)16 * n);
+  cudaMemcpy(r.data(), ttrace, r.size() * 8, cudaMemcpyDeviceToHost);
+  std::vector<NsItem> items(n);
+  cudaMemcpy(items.data(), p.nsf_items, (size_t)n * sizeof(NsItem), cudaMemcpyDeviceToHost);
+  unsigned long long t0 = ~0ull, t1 = 0;
+  double busy = 0, waiting = 0;
+  for (int i = 0; i < n; ++i) {
+    t0 = std::min(t0, r[16 * i]);
+    t1 = std::max(t1, r[16 * i + 2]);
+    busy += (double)(r[16 * i + 2] - r[16 * i + 1]);
+    waiting += (double)(r[16 * i + 1] - r[16 * i]);
+  }
+  std::printf("ns_flow: %d items, %d CTAs, span %.1f us; sum(item dep-met->done) %.1f us = %.0f%% of CTA-time, "
+              "sum(claim->dep-met) %.1f us\n", n, p.nsp_ctas, (t1 - t0) * 1e-3, busy * 1e-3,
+              100.0 * busy / ((double)(t1 - t0) * p.nsp_ctas), waiting * 1e-3);
+  std::vector<int> order((size_t)p.ns_gram.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return (double)p.ns_upd[a].M * p.ns_upd[a].N * p.ns_gram[a].N > (double)p.ns_upd[b].M * p.ns_upd[b].N * p.ns_gram[b].N;
+  });
+  {   // per matrix: when its last phase finished (sorted by size)
+    std::map<std::pair<int, int>, std::pair<double, int>> fin;   // (M, N) -> (max done, count)
+    std::vector<unsigned long long> last(order.size(), 0);
+    for (int i = 0; i < n; ++i) last[items[i].desc] = std::max(last[items[i].desc], r[16 * i + 2]);
+    for (size_t m = 0; m < order.size(); ++m) {
+      auto& f = fin[{p.ns_upd[m].M, p.ns_upd[m].N}];
+      f.first = std::max(f.first, (last[m] - t0) * 1e-3);
+      f.second++;
+    }
+    for (auto& kv : fin)
+      std::printf(" matrices %4dx%-4d x%-3d done by %.1f us\n", kv.first.first, kv.first.second, kv.second.second,
+                  kv.second.first);
+  }
+  for (int mi = 0; mi < 3 && mi < (int)order.size(); ++mi) {
+    const int m = order[mi];
+    std::printf(" matrix %d (upd %dx%d, gram N=%d K=%d):\n", m, p.ns_upd[m].M, p.ns_upd[m].N, p.ns_gram[m].N,
+                p.ns_gram[m].K);
+    for (int ph = 0; ph < nphases; ++ph) {
+      unsigned long long dmin = ~0ull, dmax = 0, emax = 0, cmin = ~0ull;
+      double dur = 0, d_load = 0, d_mma = 0, d_epiq = 0, d_epi = 0, d_pub = 0, sub[6] = {0, 0, 0, 0, 0, 0};
+      int cnt = 0;
+      for (int i = 0; i < n; ++i)
+        if (items[i].p == ph && items[i].desc == m) {
+          const unsigned long long* q = &r[16 * i];
+          cmin = std::min(cmin, q[0]);
+          dmin = std::min(dmin, q[1]);
+          dmax = std::max(dmax, q[1]);
+          emax = std::max(emax, q[2]);
+          dur += (double)(q[2] - q[1]);
+          d_load += (double)q[4] - (double)q[1];   // dependency met -> first k-block in smem
+          d_mma += (double)q[5] - (double)q[4];    // -> accumulator complete
+          d_epiq += (double)q[6] - (double)q[1];   // dependency met -> epilogue reaches this item
+          d_epi += (double)q[7] - (double)q[5];    // accumulator -> last store issued (warp 0)
+          d_pub += (double)q[2] - (double)q[7];    // -> fences, barrier, counter bump
+          for (int z = 0; z < 6; ++z) sub[z] += (double)q[8 + z] - (double)(z == 0 ? q[5] : q[7 + z]);
+          ++cnt;
+        }
+      if (!cnt) continue;
+      std::printf("  ph%2d %s x%d%s: claimed %.1f dep %.1f..%.1f done %.1f us (mean tile %.2f us: load %.2f mma %.2f "
+                  "epi %.2f pub %.2f; epi free after %.2f)\n", ph,
+                  (flags[ph] & 1) ? "gram" : "upd ", cnt, (flags[ph] & 2) ? " 3p" : "   ", (cmin - t0) * 1e-3,
+                  (dmin - t0) * 1e-3, (dmax - t0) * 1e-3, (emax - t0) * 1e-3, dur / cnt * 1e-3, d_load / cnt * 1e-3,
+                  d_mma / cnt * 1e-3, d_epi / cnt * 1e-3, d_pub / cnt * 1e-3, d_epiq / cnt * 1e-3);
+      std::printf("        epi chunks: drain %.2f cwait %.2f rows %.2f | drain %.2f cwait %.2f rows %.2f us\n",
+                  sub[0] / cnt * 1e-3, sub[1] / cnt * 1e-3, sub[2] / cnt * 1e-3, sub[3] / cnt * 1e-3, sub[4] / cnt * 1e-3,
+                  sub[5] / cnt * 1e-3);
+    }
+  }
+}
+
 int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flags, int nphases, void* stream) {
   NspBufs b;
   b.X[0] = bufs[BUF_X];
@@ -1104,16 +1203,18 @@ int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flag
   static const char* mode_env = std::getenv("ORTH_NS_MODE");   // "flow" | "sync" (A/B)
   const bool small = p.ns_upd_tiles <= 4 * p.nsp_ctas;
   const bool flow = mode_env ? std::strcmp(mode_env, "sync") != 0 : small;
-  if (flow && !tracing) {
+  if (flow) {
     if (int e = build_flow_items(p, flags, nphases)) return e;
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(ns_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
       attr_set = true;
     }
-    return (int)cudaLaunchKernelEx(&cfg, ns_flow_kernel, (const NsDesc*)p.d_ns_gram, (const NsDesc*)p.d_ns_upd,
-                                   (const NsItem*)p.nsf_items, p.nsf_n_items, p.nsp_bars, b,
-                                   reinterpret_cast<const CUtensorMap*>(p.d_ns_maps), ph);
+    const int ef = (int)cudaLaunchKernelEx(&cfg, ns_flow_kernel, (const NsDesc*)p.d_ns_gram, (const NsDesc*)p.d_ns_upd,
+                                           (const NsItem*)p.nsf_items, p.nsf_n_items, p.nsp_bars, b,
+                                           reinterpret_cast<const CUtensorMap*>(p.d_ns_maps), ph);
+    if (tracing && ef == 0) flow_trace_report(p, flags, nphases, ttrace, (cudaStream_t)stream);
+    return ef;
   }
   const cudaError_t e = cudaLaunchKernelEx(&cfg, ns_persist_kernel, (const NsDesc*)p.d_ns_gram,
                                            (const NsDesc*)p.d_ns_upd, (const NsTile*)p.nsp_tiles,

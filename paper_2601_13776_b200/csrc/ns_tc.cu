@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
   constexpr int TILE = 128 * 128;
   constexpr int STAGE = (SPLIT ? 4 : 2) * TILE;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = umma::align1024_smem(smem_raw);
   __shared__ uint64_t full_bar[S];
   __shared__ uint64_t empty_bar[S];
   __shared__ uint64_t done_bar;

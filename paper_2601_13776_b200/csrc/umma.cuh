@@ -124,6 +124,14 @@ __device__ __forceinline__ void stmatrix_x4_trans(uint32_t saddr, uint32_t m0, u
                : "memory");
 }
 
+// 1024-byte aligned view of the dynamic shared-memory window.  Offsetting the
+// shared array itself (instead of rounding an integer address) keeps the shared
+// state space visible to the compiler: accesses through the result compile to
+// LDS/STS, not generic LD/ST (long-scoreboard latency; measured in the NS epilogue).
+__device__ __forceinline__ uint8_t* align1024_smem(uint8_t* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
+
 // ---------------------------------------------------------------- descriptors
 // K-major SWIZZLE_128B smem descriptor (version 1 = sm_100, SBO = 1024 B).
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {

@@ -134,6 +134,11 @@ def build_workload(orth, torch, cfg_layers, rank, world, device, compute, batch,
         acts.append(torch.empty((batch, Ho, Ho, d["c_out"]), device=dev, dtype=torch.bfloat16))
         shapes.append((H, Ho, d))
         H = Ho
+    # plan-owned conv scratch for the stacked-window kernel (padded input copy), sized for every layer
+    need = [plan.conv_scratch_bytes(l, batch, Ho if d.get("kind") == "convT" else H, Ho if d.get("kind") == "convT" else H)
+            for l, (H, Ho, d) in enumerate(shapes)]
+    if need:
+        plan.reserve(max(need))
     W["x"] = ins[0] if ins else torch.zeros(1, device=dev, dtype=torch.bfloat16)
     W["ins"], W["acts"], W["shapes"] = ins, acts, shapes
     W["kviews"] = [plan.kernel_bf16(W["kbf16"], l) for l in range(len(cfg_layers))]

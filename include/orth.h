@@ -116,6 +116,16 @@ orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers
                                int32_t device, orth_plan_t* plan);
 orth_status_t orth_plan_destroy(orth_plan_t plan);
 
+/* Reserve `bytes` of plan-owned device scratch for the forward / adjoint
+ * convolutions (synchronous; the only call besides orth_plan_create that
+ * allocates, and only when `bytes` exceeds the current reservation).  Stride-1
+ * layers with >= 128 output channels per group then run the stacked-window
+ * tensor-core kernel, which first writes a padded copy of its input
+ * (N x (Ho + d(k-1)) x (Wo + d(k-1)) x C_in BF16, in the forward-conv view of
+ * the layer) into this scratch; a call whose padded input does not fit uses
+ * the other kernels (same results up to FP32 summation order).  0 frees it. */
+orth_status_t orth_plan_reserve(orth_plan_t plan, int64_t bytes);
+
 /* Plan queries (int64 result in *out).  `index` is a layer index for the
  * ORTH_Q_LAYER_* queries and a global matrix index for ORTH_Q_MATRIX_*. */
 typedef enum {

@@ -61,6 +61,7 @@ _sig = {
     "orth_conv_forward": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
     "orth_conv_transpose": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
     "orth_plan_check": (C.c_int, [_P, _P]),
+    "orth_plan_reserve": (C.c_int, [_P, C.c_int64]),
     "orth_plan_launch_count": (C.c_int64, [_P]),
     "orth_status_string": (C.c_char_p, [C.c_int]),
     "orth_last_error": (C.c_char_p, []),
@@ -168,6 +169,10 @@ def orth_plan_check(h: int, stream=None):
     _check(_lib.orth_plan_check(h, _stream(stream)), "orth_plan_check (device status)")
 
 
+def orth_plan_reserve(h: int, nbytes: int):
+    _check(_lib.orth_plan_reserve(h, int(nbytes)), "orth_plan_reserve")
+
+
 def orth_plan_launch_count(h: int) -> int:
     return _lib.orth_plan_launch_count(h)
 
@@ -253,6 +258,20 @@ class Plan:
 
     def check(self, stream=None):
         orth_plan_check(self.h, stream)
+
+    def conv_scratch_bytes(self, l: int, N: int, H: int, W: int) -> int:
+        """Conv scratch (orth_plan_reserve) that lets layer l with input / large grid N x H x W run the
+        stacked-window kernel in both directions: a padded copy of the forward-view input."""
+        d = self.layers[l]
+        if d.get("kind") == "dense":
+            return 0
+        e = d.get("d", 1) * (d.get("k", 3) - 1)
+        Ho, Wo = self.out_hw(l, H, W)
+        return N * (max(H, Ho) + e) * (max(W, Wo) + e) * max(self.fwd_channels(l)) * 2
+
+    def reserve(self, nbytes: int):
+        """Plan-owned conv scratch (grows only; synchronous)."""
+        orth_plan_reserve(self.h, nbytes)
 
     @property
     def launches(self) -> int:

@@ -168,6 +168,35 @@ orth_status_t orth_conv_transpose(orth_plan_t plan, int32_t layer, const void* k
   return cuda_fail(e, "orth_conv_transpose");
 }
 
+orth_status_t orth_plan_reserve(orth_plan_t plan, int64_t bytes) {
+  orth_status_t st = need_device(plan);
+  if (st != ORTH_OK) return st;
+  if (bytes < 0) { set_error("negative reservation"); return ORTH_ERR_INVALID_ARGUMENT; }
+  Plan& P = plan->p;
+  if (bytes == 0 || bytes > P.pad_bytes) {
+    if (P.d_pad_scratch) {
+      cudaDeviceSynchronize();   // a reservation may be in use by queued work
+      cudaFree(P.d_pad_scratch);
+    }
+    P.d_pad_scratch = nullptr;
+    P.pad_bytes = 0;
+    if (bytes > 0) {
+      if (cudaMalloc(&P.d_pad_scratch, (size_t)bytes) != cudaSuccess) {
+        cudaGetLastError();
+        P.d_pad_scratch = nullptr;
+        set_error("orth_plan_reserve: cudaMalloc of %lld bytes failed", (long long)bytes);
+        return ORTH_ERR_OUT_OF_MEMORY;
+      }
+      P.pad_bytes = bytes;
+    }
+    for (auto& L : P.layers) {
+      L.pad_scratch = P.d_pad_scratch;
+      L.pad_bytes = P.pad_bytes;
+    }
+  }
+  return ORTH_OK;
+}
+
 orth_status_t orth_plan_check(orth_plan_t plan, void* stream) {
   orth_status_t st = need_device(plan);
   if (st != ORTH_OK) return st;

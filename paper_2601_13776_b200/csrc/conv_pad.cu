@@ -1,32 +1,31 @@
-// a6 (forward orthogonal convolution) on the tensor cores for stride-1
-// layers, with the A operand brought in by TMA and reused across taps.
+// a6 (forward orthogonal convolution) on the tensor cores for
+// stride-1 layers with <= 64 output channels per group (>= 128: conv_stack.cu),
+// with the input window brought in by TMA once per tile and reused by all taps.
 //
-// Output pixels of a tile are TH rows of one image with row pitch P (a
-// multiple of 8, >= Wo): MMA row r <-> output (h0 + r / P, r % P); columns
-// past Wo are computed and discarded.  Per 64-channel chunk the tile's input
-// window is loaded as k column-shifted copies (one per tap column b), each
-// R = TH + d (k - 1) rows x P pixels in the pitch-P SWIZZLE_128B row layout:
-//     C_b[y * P + x] = x~[h0 - p_t + y, x - p_l + d b],   y < R, x < P
-// (zero padding: one 4-D TMA box per copy, out of bounds zero-filled;
-// circular padding: per input row the two wrapped pieces of each copy).  The
-// A operand of tap (a, b) is the 128 consecutive rows of C_b starting at row
-// d a P -- a multiple of 8, so every UMMA descriptor start stays on a
-// 1024-byte swizzle atom.  (Starting inside an atom is numerically fine -- the
-// tensor core swizzles on absolute address bits -- but measured ~4.7x slower
-// per MMA on B200, so the b shift is done by the TMA copy instead.)
-// A bytes per chunk: k R P rows instead of k^2 * 128 gathered rows.
+// Output pixels of a tile are TH rows of one image at pitch P: window pixel
+// r <-> output (h0 + r / P, r % P); columns past Wo are computed and dropped.
+// Per 64-channel chunk the window is R = TH + d(k-1) input rows in the
+// SWIZZLE_128B K-major layout (zero padding: one 4-D box, out-of-bounds filled;
+// circular: the wrapped row pieces), in one of two layouts:
+//   window  (default): one copy of pitch P = Wo + d(k-1); tap (a, b) starts at
+//           window row d(aP + b) -- inside a 1024-byte swizzle atom, which the
+//           tensor core handles at no cost (it swizzles on absolute address bits);
+//   copies: k column-shifted copies of pitch round8(Wo) (ORTH_CONV_PAD_LAYOUT).
 //
-// B (weights): when all k^2 taps x 64-channel chunks of one (group, n-tile)
-// fit next to the A ring (narrow layers), they are loaded ONCE per CTA and stay
-// resident; each CTA then walks a contiguous range of tiles in (group, n-tile)
-// major order, reloading only when the range crosses into the next set.
-// Otherwise B streams per tap through a TMA ring.
+// Two MMA orientations:
+//   SW (co_g = 64, default): D^T = W x^T, tcgen05 M = 64 channels x N = 256
+//       window pixels (the weights are the A operand); the M = 64 accumulator is
+//       read as 16x256b fragments and transposed by stmatrix into a SWIZZLE_128B
+//       staging tile, one TMA tensor store per output row;
+//   plain: M = 128 window pixels x N = BN channels, epilogue stores rows.
+// Weights of one (group, channel tile) stay resident in shared memory when they
+// fit (each CTA then walks a contiguous tile range), else they stream per tap.
 //
 // Warp roles (256 threads, one CTA per SM, persistent over tiles):
-//   warp 0      A producer: TMA of the tile window into a ring of A buffers
-//   warp 1      B producer: TMA of the weight tile (BN rows x 64 ch, one tap)
+//   warp 0      window producer (TMA)
+//   warp 1      weight producer (TMA)
 //   warp 2      TMEM allocation + the single-thread tcgen05.mma issuer
-//   warps 4-7   epilogue: TMEM -> bias -> BF16 NHWC stores (one row per thread)
+//   warps 4-7   epilogue
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -534,6 +533,11 @@ int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* b
 }
 
 }  // namespace
+
+int conv_sm_count() { return sm_count(); }
+bool conv_act_tmap(CUtensorMap_st* out, const void* x, int C, int W, int H, int N, int bw, int bh) {
+  return make_act_tmap(out, x, C, W, H, N, bw, bh);
+}
 
 // Plan the padded-row path for a (possibly group-packed) forward layer; false
 // if it does not apply (stride != 1, rows wider than one tile, channel slices

@@ -1,0 +1,445 @@
+// a6 (forward orthogonal convolution) for stride-1 layers with
+// >= 128 output channels per group, on the tensor cores with the operands
+// swapped: D^T[o][w] = sum_{c,a,b} K[o, a, b, c] * window[w + d(aP + b)][c], one
+// tcgen05.mma M = 128 output channels x N = 256 window pixels x K = 16.
+//
+// Window.  A first kernel writes every image padded to Hp = Ho + d(k-1) rows of
+// P = Wo + d(k-1) pixels (circular: wrapped copies; zeros: zeros) into the
+// plan's conv scratch (orth_plan_reserve), so the padded images of the batch
+// form one stream of padded rows g = n Hp + y.  A tile is TH consecutive padded
+// rows (TH P <= 256 window pixels); its input window is those rows plus the
+// d(k-1) below, one 64-channel chunk at a time: ONE 3-D TMA box of R = TH + d(k-1)
+// rows x P pixels x 64 channels, SWIZZLE_128B K-major.  (Loading the window
+// from the unpadded tensor costs one TMA per row piece -- three per row for
+// circular padding -- and measured 4-5x slower for small images.)  The B operand of tap (a, b) is the 256 window pixels starting
+// at d(aP + b) (a descriptor may start inside a swizzle atom: the tensor core
+// swizzles on absolute address bits).  Window pixel w = yl P + x of padded row
+// g0 + yl = n Hp + y is output (n, y, x) when y < Ho and x < Wo; other columns
+// are computed and dropped.  Small images are therefore batched into one MMA
+// instead of one image per tile (4x4 images: 7 per tile).
+//
+// Weights: the A operand, 128 output channels x 64 input channels per (chunk,
+// tap) stage, streamed through a TMA ring (per tile the whole 128-channel block
+// is re-read from L2; the CTA walks tiles in window-row-major order so that
+// concurrently running CTAs read the same block).
+//
+// Epilogue: TMEM lane = output channel.  Warp q reads lanes 32q .. 32q+31 as
+// mma-style 8x8 fragments (tcgen05.ld 16x256b) and writes them transposed with
+// stmatrix (16 B = 8 channels of one pixel per row) into a SWIZZLE_128B staging
+// area of valid output rows, two 64-channel halves; one TMA tensor store per
+// (output row, half).
+//
+// Warp roles (256 threads, one CTA per SM, persistent over tiles):
+//   warp 0 window TMA, warp 1 weight TMA, warp 2 TMEM alloc + MMA issuer,
+//   warps 4-7 epilogue.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+
+#include "orth_internal.h"
+#include "tma_host.h"
+#include "umma.cuh"
+
+#ifdef ORTH_STACK_TRACE
+// diagnostics: per CTA {MMA start, MMA end, ns waiting for windows, ns waiting for weights, epilogue end}
+__device__ unsigned long long stack_trace[160 * 5];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define STRACE(...) __VA_ARGS__
+#else
+#define STRACE(...)
+#endif
+
+namespace orth {
+namespace {
+
+struct StackArgs {
+  int N, H, W, Ho, Wo, k, d, pt, pl, circ;
+  int Hp, P, TH, R;               // padded rows per image, window pitch, output rows per tile, window rows
+  int in_C, out_C, cr_g, nout_g;  // input / output channels (whole tensor), per group
+  int tiles_m, tiles_n, num_tiles;
+  int abuf_bytes, nabuf, sb;      // window ring, weight ring stages
+  int stage_off, stage_row, stage_half, slots;
+  int flip;                       // weight tap t read from row k^2-1-t (stride-1 adjoint, forward form)
+};
+
+constexpr int NTHREADS = 256;
+constexpr int EPI_WARP0 = 4;
+constexpr int MAX_AB = 4;
+constexpr int MAX_SB = 8;
+constexpr int W_BYTES = 128 * 128;   // one weight stage: 128 output channels x 64 input channels
+constexpr size_t kSmemMax = 227 * 1024 - 1024;
+
+__device__ __forceinline__ int wrapi(int x, int n) {
+  x %= n;
+  return x < 0 ? x + n : x;
+}
+
+// padded[n][yy][xx][c] = x~[n][yy - p_t][xx - p_l][c] (circular: mod H, W; zeros outside), 8 channels
+// (16 B) per thread; rows of the whole batch back to back
+__global__ void __launch_bounds__(256) pad_kernel(const uint4* __restrict__ x, uint4* __restrict__ out, int N, int H,
+                                                  int W, int C8, int Hp, int P, int pt, int pl, int circ) {
+  const int64_t total = (int64_t)N * Hp * P * C8;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (int64_t)gridDim.x * 256) {
+    const int c = (int)(e % C8);
+    const int64_t pix = e / C8;
+    const int xx = (int)(pix % P);
+    const int64_t row = pix / P;
+    const int yy = (int)(row % Hp), n = (int)(row / Hp);
+    int h = yy - pt, w = xx - pl;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (circ) {
+      h = wrapi(h, H);
+      w = wrapi(w, W);
+      v = __ldg(x + (((int64_t)n * H + h) * W + w) * C8 + c);
+    } else if (h >= 0 && h < H && w >= 0 && w < W) {
+      v = __ldg(x + (((int64_t)n * H + h) * W + w) * C8 + c);
+    }
+    out[e] = v;
+  }
+}
+
+// valid output rows in padded rows [0, g)
+__device__ __forceinline__ int valid_before(int g, int Hp, int Ho) { return (g / Hp) * Ho + min(g % Hp, Ho); }
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    conv_stack(const float* __restrict__ bias, const __grid_constant__ StackArgs a,
+               const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+               const __grid_constant__ CUtensorMap tmY) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = umma::align1024_smem(smem_raw);
+  __shared__ uint64_t a_full[MAX_AB], a_empty[MAX_AB], b_full[MAX_SB], b_empty[MAX_SB], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NA = a.nabuf, SB = a.sb;
+  if (warp == 2) umma::tmem_alloc(&tmem_base_sh, 512);
+  if (tid == 0) {
+    for (int i = 0; i < NA; ++i) {
+      umma::mbar_init(&a_full[i], 1);
+      umma::mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < SB; ++i) {
+      umma::mbar_init(&b_full[i], 1);
+      umma::mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      umma::mbar_init(&tfull_bar[i], 1);
+      umma::mbar_init(&tempty_bar[i], 128);
+    }
+    umma::fence_mbar_init();
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t abase = umma::smem_u32(smem);
+  const uint32_t wbase = abase + NA * a.abuf_bytes;
+  const int kk2 = a.k * a.k;
+  // tile -> (first padded row, 128-channel block, group); window-row tiles fastest
+  auto decode = [&](int tile, int& g0, int& n0, int& grp) {
+    const int tm = tile % a.tiles_m, rest = tile / a.tiles_m;
+    n0 = (rest % a.tiles_n) * 128;
+    grp = rest / a.tiles_n;
+    g0 = tm * a.TH;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ window producer
+      umma::tma_prefetch_desc(&tmA);
+      int u = 0;
+      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+        int g0, n0, grp;
+        decode(tile, g0, n0, grp);
+        for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
+          const int ab = u % NA;
+          if (u >= NA) umma::mbar_wait(&a_empty[ab], ((u / NA) - 1) & 1);
+          const uint32_t dst = abase + ab * a.abuf_bytes;
+          const int c = grp * a.cr_g + c0;
+          // R padded rows x P pixels x 64 channels; rows past the batch are zero-filled (dropped columns)
+          umma::mbar_arrive_expect_tx(&a_full[ab], (uint32_t)(a.R * a.P * 128));
+          umma::tma_load_3d(dst, &tmA, &a_full[ab], c, 0, g0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ weight producer
+      umma::tma_prefetch_desc(&tmW);
+      int i = 0;
+      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+        int g0, n0, grp;
+        decode(tile, g0, n0, grp);
+        for (int c0 = 0; c0 < a.cr_g; c0 += 64)
+          for (int tap = 0; tap < kk2; ++tap, ++i) {
+            const int st = i % SB;
+            if (i >= SB) umma::mbar_wait(&b_empty[st], ((i / SB) - 1) & 1);
+            umma::mbar_arrive_expect_tx(&b_full[st], W_BYTES);
+            umma::tma_load_3d(wbase + st * W_BYTES, &tmW, &b_full[st], c0, a.flip ? kk2 - 1 - tap : tap,
+                              grp * a.nout_g + n0);
+          }
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t IDESC = umma::idesc_bf16(128, 256);
+      int u = 0, i = 0, tcount = 0;
+      STRACE(unsigned long long wa = 0, wb = 0; const unsigned long long t_start = gtime();)
+      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++tcount) {
+        const int acc = tcount & 1;
+        umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
+        umma::tc_fence_after();
+        const uint32_t d_tmem = tmem + acc * 256;
+        for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
+          const int ab = u % NA;
+          STRACE(const unsigned long long t0a = gtime();)
+          umma::mbar_wait(&a_full[ab], (u / NA) & 1);
+          STRACE(wa += gtime() - t0a;)
+          umma::tc_fence_after();
+          const uint32_t win = abase + ab * a.abuf_bytes;
+          for (int tap = 0; tap < kk2; ++tap, ++i) {
+            const int st = i % SB;
+            STRACE(const unsigned long long t0b = gtime();)
+            umma::mbar_wait(&b_full[st], (i / SB) & 1);
+            STRACE(wb += gtime() - t0b;)
+            umma::tc_fence_after();
+            const int ta = tap / a.k, tb = tap - ta * a.k;
+            const uint32_t bw = win + (uint32_t)(a.d * (ta * a.P + tb)) * 128u;
+            const uint32_t aw = wbase + st * W_BYTES;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              umma::mma_bf16(d_tmem, umma::sdesc_sw128(aw + 32 * q), umma::sdesc_sw128(bw + 32 * q), IDESC,
+                             (c0 | tap | q) != 0);
+            umma::mma_commit(&b_empty[st]);
+          }
+          umma::mma_commit(&a_empty[ab]);
+        }
+        umma::mma_commit(&tfull_bar[acc]);
+      }
+      STRACE(stack_trace[blockIdx.x * 5 + 0] = t_start; stack_trace[blockIdx.x * 5 + 1] = gtime();
+             stack_trace[blockIdx.x * 5 + 2] = wa; stack_trace[blockIdx.x * 5 + 3] = wb;)
+    }
+    __syncwarp();
+  } else if (warp >= EPI_WARP0) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;
+    const uint32_t s_base = umma::smem_u32(smem + a.stage_off);
+    const uint32_t dump = s_base + (uint32_t)(2 * a.stage_half) + (uint32_t)lane * 16u;
+    const int m = lane >> 3, jrow = lane & 7;
+    int tcount = 0;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++tcount) {
+      int g0, n0, grp;
+      decode(tile, g0, n0, grp);
+      const int acc = tcount & 1;
+      const int v0 = valid_before(g0, a.Hp, a.Ho);
+      umma::mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
+      umma::tc_fence_after();
+      if (tid == EPI_WARP0 * 32) umma::bulk_wait_read0();   // the previous tile's stores have read the staging
+      umma::named_bar_sync(2, 128);
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {   // TMEM lanes 32q + 16 hf .. + 15 = channels
+        const int ch0 = 32 * q + 16 * hf;
+        const int ob = grp * a.nout_g + n0 + ch0 + (lane >> 2);
+        const float b_lo = bias ? bias[ob] : 0.f, b_hi = bias ? bias[ob + 8] : 0.f;
+        const uint32_t chunk = (uint32_t)(((ch0 >> 3) + (m & 1)) & 7);   // 16-B chunk in the 128-B half row
+        const uint32_t half_off = (uint32_t)((ch0 >> 6) * a.stage_half);
+#pragma unroll 1
+        for (int c = 0; c < 256; c += 32) {
+          uint32_t r[16];
+          umma::tmem_ld_16x256b_x4(tmem + ((uint32_t)(32 * q + 16 * hf) << 16) + (uint32_t)(acc * 256 + c), r);
+          umma::tmem_ld_wait();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int w = c + 16 * h + 8 * (m >> 1) + jrow;   // window pixel this lane addresses
+            const int yl = w / a.P, x = w - yl * a.P;
+            const int gg = g0 + yl, n = gg / a.Hp, y = gg - n * a.Hp;
+            uint32_t dst = dump;
+            if (yl < a.TH && x < a.Wo && y < a.Ho && n < a.N) {
+              const int slot = valid_before(gg, a.Hp, a.Ho) - v0;
+              dst = s_base + half_off + (uint32_t)(slot * a.stage_row + x * 128) + ((chunk ^ (uint32_t)(x & 7)) << 4);
+            }
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float bb = (e & 1) ? b_hi : b_lo;
+              __nv_bfloat162 v2 = __floats2bfloat162_rn(__uint_as_float(r[8 * h + 2 * e]) + bb,
+                                                        __uint_as_float(r[8 * h + 2 * e + 1]) + bb);
+              pk[e] = *reinterpret_cast<uint32_t*>(&v2);
+            }
+            umma::stmatrix_x4_trans(dst, pk[0], pk[1], pk[2], pk[3]);
+          }
+        }
+      }
+      umma::tc_fence_before();
+      umma::mbar_arrive(&tempty_bar[acc]);
+      umma::fence_proxy_async_smem();   // staging writes -> TMA (async proxy) reads
+      umma::named_bar_sync(2, 128);
+      if (tid == EPI_WARP0 * 32) {
+        for (int yl = 0; yl < a.TH; ++yl) {   // one store per (valid output row, 64-channel half)
+          const int gg = g0 + yl, n = gg / a.Hp, y = gg - n * a.Hp;
+          if (y >= a.Ho || n >= a.N) continue;
+          const uint32_t src = s_base + (uint32_t)((valid_before(gg, a.Hp, a.Ho) - v0) * a.stage_row);
+          umma::tma_store_3d(&tmY, src, grp * a.nout_g + n0, 0, n * a.Ho + y);
+          umma::tma_store_3d(&tmY, src + (uint32_t)a.stage_half, grp * a.nout_g + n0 + 64, 0, n * a.Ho + y);
+        }
+        umma::bulk_commit();
+      }
+    }
+    if (tid == EPI_WARP0 * 32) umma::bulk_wait0();
+    STRACE(if (tid == EPI_WARP0 * 32) stack_trace[blockIdx.x * 5 + 4] = gtime();)
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) umma::tmem_dealloc(tmem, 512);
+}
+
+// host: plan one layer; false = not applicable
+bool stack_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, StackArgs& a) {
+  const int ext = L.d * (L.k - 1);
+  if (L.s != 1 || L.k > 7 || L.co % 128 != 0) return false;
+  if (L.g > 1 && L.ci % 64 != 0) return false;   // a 64-channel box must stay inside the group
+  if (L.ci_f % 8 != 0 || L.co_f % 8 != 0) return false;
+  const bool circ = L.desc.padding_mode == ORTH_PAD_CIRCULAR;
+  const int pr = ext - L.pl;
+  if (circ && (L.pl < 0 || pr < 0 || Wo != W || Ho != H)) return false;
+  if (L.pt < 0 || L.pl < 0) return false;
+  const int P = Wo + ext;
+  if (P > 256 || Wo < 1) return false;
+  if (L.ci_f % 8 != 0) return false;
+  const int TH = 256 / P;
+  const int Hp = Ho + ext;
+  a = StackArgs{};
+  a.N = N; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo;
+  a.k = L.k; a.d = L.d; a.pt = L.pt; a.pl = L.pl; a.circ = circ;
+  a.Hp = Hp; a.P = P; a.TH = TH; a.R = TH + ext;
+  a.in_C = L.ci_f; a.out_C = L.co_f; a.cr_g = L.ci; a.nout_g = L.co;
+  const long long rows = (long long)N * Hp;
+  a.tiles_m = (int)((rows + TH - 1) / TH);
+  a.tiles_n = L.co / 128;
+  const long long nt = (long long)a.tiles_m * a.tiles_n * L.g;
+  if (nt > (1LL << 30)) return false;
+  a.num_tiles = (int)nt;
+  // staging: valid output rows of one tile (max over the Hp-periodic tile offsets), 1024-aligned rows
+  int slots = 0;
+  for (int g0 = 0; g0 < Hp * TH && g0 < Hp * 256; g0 += TH) {
+    auto vb = [&](int g) { return (g / Hp) * Ho + std::min(g % Hp, Ho); };
+    slots = std::max(slots, vb(g0 + TH) - vb(g0));
+  }
+  a.slots = slots;
+  a.stage_row = (Wo * 128 + 1023) & ~1023;
+  a.stage_half = slots * a.stage_row;
+  // shared memory: window ring + weight ring + two staging halves + dump slots
+  a.abuf_bytes = (a.R * P * 128 + 1023) & ~1023;
+  const size_t stage = (size_t)2 * a.stage_half + 1024;
+  const size_t slack = (size_t)std::max(0, ext * (P + 1) + 256 - a.R * P) * 128;   // last taps read past a window
+  // the weight ring is the latency-critical stream (a whole 128-channel block per tile): give it up to
+  // MAX_SB stages first (measured: 2 stages starve the MMA at ~25 GB/s per SM), then extra window buffers
+  if (1024 + 2 * (size_t)a.abuf_bytes + 2 * (size_t)W_BYTES + stage > kSmemMax) return false;
+  const size_t room = kSmemMax - 1024 - stage - 2 * (size_t)a.abuf_bytes;
+  a.sb = (int)std::min<size_t>(MAX_SB, room / W_BYTES);
+  int na = 2;
+  while (na < MAX_AB && (size_t)(na - 1) * a.abuf_bytes + (size_t)a.sb * W_BYTES <= room) ++na;
+  a.nabuf = na;
+  a.stage_off = na * a.abuf_bytes + a.sb * W_BYTES;
+  if ((size_t)a.sb * W_BYTES + stage < slack) return false;   // the last window's over-read stays in smem
+  return true;
+}
+
+}  // namespace
+
+int launch_conv_fwd_stack(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
+                          int H, int W, int Ho, int Wo, void* stream, int flip) {
+  // Opt-in (ORTH_CONV_STACK=1): measured on B200 the M=128 x N=256 MMAs of this kernel run at ~220
+  // cycles (shared-memory bound with the weight stream) and small images waste MMA work on padded
+  // columns (4x4: 56%), so it beats conv_ws only for images >= ~28 px (cfg3 128@28: 103 vs 110 us) and
+  // loses below (512@4: 49 vs 37 us); see DESIGN.md §9.
+  static const bool on = std::getenv("ORTH_CONV_STACK") != nullptr && std::getenv("ORTH_CONV_NO_STACK") == nullptr;
+  if (!on || !L.pad_scratch) return -1;
+  if (((uintptr_t)x & 15) != 0 || ((uintptr_t)y & 15) != 0) return -1;
+  StackArgs a;
+  if (!stack_args(L, N, H, W, Ho, Wo, a)) return -1;
+  const int64_t pad_elems = (int64_t)N * a.Hp * a.P * a.in_C;
+  if (pad_elems * 2 > L.pad_bytes) return -1;   // reservation too small: the caller falls back
+  if (a.num_tiles == 0) return 0;
+  a.flip = flip;
+  cudaStream_t s = (cudaStream_t)stream;
+  {
+    const int64_t vec = pad_elems / 8;
+    const int blocks = (int)std::min<int64_t>((vec + 255) / 256, (int64_t)conv_sm_count() * 16);
+    pad_kernel<<<blocks, 256, 0, s>>>((const uint4*)x, (uint4*)L.pad_scratch, N, H, W, a.in_C / 8, a.Hp, a.P, L.pt,
+                                      L.pl, a.circ);
+    if (int e = (int)cudaGetLastError()) return e;
+  }
+  CUtensorMap ta;   // padded rows (C, P, N*Hp): box 64 ch x P px x R rows, SWIZZLE_128B
+  {
+    auto enc = tensor_map_encoder();
+    const cuuint64_t dims[3] = {(cuuint64_t)a.in_C, (cuuint64_t)a.P, (cuuint64_t)N * a.Hp};
+    const cuuint64_t strides[2] = {(cuuint64_t)a.in_C * 2, (cuuint64_t)a.P * a.in_C * 2};
+    const cuuint32_t box[3] = {64, (cuuint32_t)a.P, (cuuint32_t)a.R};
+    const cuuint32_t es[3] = {1, 1, 1};
+    std::memset(&ta, 0, sizeof(ta));
+    if (!enc || enc(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, L.pad_scratch, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return (int)cudaErrorInvalidValue;
+  }
+  CUtensorMap tw;
+  if (!make_weight_tmap(&tw, kernel, L.co_f, L.k * L.k, L.ci, 128)) return (int)cudaErrorInvalidValue;
+  CUtensorMap ty;
+  {   // output (C, Wo, N*Ho): one output row x 64 channels per box, SWIZZLE_128B staging
+    auto enc = tensor_map_encoder();
+    const cuuint64_t dims[3] = {(cuuint64_t)a.out_C, (cuuint64_t)Wo, (cuuint64_t)N * Ho};
+    const cuuint64_t strides[2] = {(cuuint64_t)a.out_C * 2, (cuuint64_t)Wo * a.out_C * 2};
+    const cuuint32_t box[3] = {64, (cuuint32_t)Wo, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    std::memset(&ty, 0, sizeof(ty));
+    if (!enc || enc(&ty, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return (int)cudaErrorInvalidValue;
+  }
+  const size_t smem = 1024 + (size_t)a.stage_off + 2 * (size_t)a.stage_half + 1024;
+  static size_t attr = 0;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(conv_stack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return (int)cudaGetLastError();
+    attr = smem;
+  }
+  const int grid = std::min(a.num_tiles, conv_sm_count());
+  conv_stack<<<grid, NTHREADS, smem, s>>>(bias, a, ta, tw, ty);
+#ifdef ORTH_STACK_TRACE
+  {
+    cudaStreamSynchronize(s);
+    static unsigned long long h[160 * 5];
+    cudaMemcpyFromSymbol(h, stack_trace, sizeof(h));
+    unsigned long long t0 = ~0ull, t1 = 0, t2 = 0;
+    double wa = 0, wb = 0, span = 0;
+    for (int c = 0; c < grid && c < 160; ++c) {
+      t0 = std::min(t0, h[c * 5]);
+      t1 = std::max(t1, h[c * 5 + 1]);
+      t2 = std::max(t2, h[c * 5 + 4]);
+      wa += h[c * 5 + 2];
+      wb += h[c * 5 + 3];
+      span += h[c * 5 + 1] - h[c * 5];
+    }
+    std::printf("conv_stack tiles=%d grid=%d TH=%d P=%d R=%d na=%d sb=%d: MMA-thread span %.1f us (wait windows %.1f, "
+                "weights %.1f), last MMA %.1f, last epilogue %.1f us after first start\n", a.num_tiles, grid, a.TH, a.P,
+                a.R, a.nabuf, a.sb, span / grid * 1e-3, wa / grid * 1e-3, wb / grid * 1e-3, (t1 - t0) * 1e-3,
+                (t2 - t0) * 1e-3);
+  }
+#endif
+  return (int)cudaGetLastError();
+}
+
+}  // namespace orth

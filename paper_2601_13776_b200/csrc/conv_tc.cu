@@ -822,8 +822,9 @@ int launch_conv_fwd_tc(const LayerInfo& L0, const void* kernel, void* scratch, c
     kernel = scratch;
   }
   static const bool no_reuse = std::getenv("ORTH_CONV_NO_REUSE") != nullptr;   // A/B switch
-  if (!no_reuse) {   // stride-1 layers on wide images: shifted-copy A reuse (conv_reuse.cu)
-    const int e = launch_conv_fwd_reuse(L, kernel, bias, x, y, N, H, W, Ho, Wo, stream);
+  if (!no_reuse) {   // stride 1: TMA-window kernels (conv_stack.cu: >= 128 channels, conv_pad.cu: <= 64)
+    int e = launch_conv_fwd_stack(L, kernel, bias, x, y, N, H, W, Ho, Wo, stream);
+    if (e < 0) e = launch_conv_fwd_reuse(L, kernel, bias, x, y, N, H, W, Ho, Wo, stream);
     if (e >= 0) return e;
   }
   TcConvArgs a;
@@ -863,7 +864,8 @@ int launch_conv_bwd_tc(const LayerInfo& L0, const void* kernel, void* wt_scratch
     F.ci = L.co; F.co = L.ci; F.ci_f = L.co_f; F.co_f = L.ci_f;
     F.pt = L.d * (L.k - 1) - L.pt; F.pl = L.d * (L.k - 1) - L.pl;
     F.pb = L.d * (L.k - 1) - L.pb; F.pr = L.d * (L.k - 1) - L.pr;
-    const int e = launch_conv_fwd_reuse(F, wt_scratch, bias, y, x, N, Ho, Wo, H, W, stream, 1);
+    int e = launch_conv_fwd_stack(F, wt_scratch, bias, y, x, N, Ho, Wo, H, W, stream, 1);
+    if (e < 0) e = launch_conv_fwd_reuse(F, wt_scratch, bias, y, x, N, Ho, Wo, H, W, stream, 1);
     if (e >= 0) return e;
   }
   TcConvArgs a;

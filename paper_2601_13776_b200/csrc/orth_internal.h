@@ -8,6 +8,8 @@
 
 #include "../../include/orth.h"
 
+struct CUtensorMap_st;   // cuda.h (TMA descriptors), forward-declared for the launcher prototypes
+
 namespace orth {
 
 enum Role : int32_t { ROLE_Q = 0, ROLE_U = 1, ROLE_R = 2, ROLE_W = 3 };
@@ -41,6 +43,8 @@ struct LayerInfo {
   int32_t first_mat, mats_per_group;
   int32_t owner;
   int64_t kf32_off, kbf16_off, kernel_numel;
+  void* pad_scratch = nullptr;  // plan-owned conv scratch (orth_plan_reserve): padded input copy
+  int64_t pad_bytes = 0;
   double ns_flops, comp_flops;
 };
 
@@ -223,6 +227,8 @@ struct Plan {
   EmitItem* d_emit = nullptr;
   int64_t partial_stride = 0;
   int64_t launches = 0;
+  void* d_pad_scratch = nullptr;    // orth_plan_reserve
+  int64_t pad_bytes = 0;
   uint16_t* d_wt_scratch = nullptr; // BF16 weight scratch of one layer call: [W^T | packed W], 16 x max kernel
 };
 
@@ -242,6 +248,14 @@ int launch_ns_tc(Plan& p, float* const bufs[BUF_COUNT], int par, bool gram, int 
 // tensor-core stem (ci = 3, k = 3 | 4, co in {32, 64, 128}); -1 = not applicable
 int launch_conv_fwd_stem(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
                          int H, int W, int Ho, int Wo, void* stream);
+// shared by the TMA-window conv kernels (conv_pad.cu): SM count, 4-D SWIZZLE_128B activation map
+// (C, W, H, N) with box 64 ch x bw px x bh rows x 1 image (cached per pointer/shape)
+int conv_sm_count();
+bool conv_act_tmap(::CUtensorMap_st* out, const void* x, int C, int W, int H, int N, int bw, int bh);
+// stride-1 forward conv, >= 128 output channels per group: images stacked into one padded-row
+// window stream, tcgen05 M = 128 channels x N = 256 window pixels (conv_stack.cu); -1 = not applicable
+int launch_conv_fwd_stack(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
+                          int H, int W, int Ho, int Wo, void* stream, int flip = 0);
 // forward conv over TMA-loaded padded row windows (stride 1, rows <= 128 px); -1 = not applicable.
 // flip = 1 reads weight tap t from row k^2-1-t (a stride-1 adjoint in its forward-conv form).
 int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,

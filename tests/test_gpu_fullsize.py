@@ -76,6 +76,11 @@ def test_cfg3_fullsize(cuda_lib):
     N = configs.BATCH[3]
     x = gen.bf16_round(gen.activations((N, 224, 224, 3), (3, 0, 0, 0, gen.ROLE_ID["x"])))
     cur, H = dev(x, torch.bfloat16), 224
+    need, Hc = 0, H
+    for l in range(len(layers)):
+        need = max(need, plan.conv_scratch_bytes(l, N, Hc, Hc))
+        Hc = plan.out_hw(l, Hc, Hc)[0]
+    plan.reserve(need)
     sample = [0, N - 1]
     for l, d in enumerate(layers):
         Ho, _ = plan.out_hw(l, H, H)
@@ -96,6 +101,9 @@ def test_cfg4_fullsize(cuda_lib):
     o_k = check_construction(plan, mats, ortho, res, kf, layers)
     N = configs.BATCH[4]
     sample = [0, N - 1]
+    plan.reserve(max(plan.conv_scratch_bytes(l, N, d["H"] * (d["s"] if d["kind"] == "convT" else 1),
+                                             d["H"] * (d["s"] if d["kind"] == "convT" else 1))
+                     for l, d in enumerate(layers)))
     for l, d in enumerate(layers):
         H = d["H"]
         x = gen.bf16_round(gen.activations((N, H, H, d["c_in"]), (4, 0, l, 0, gen.ROLE_ID["x"])))

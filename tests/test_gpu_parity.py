@@ -180,6 +180,11 @@ CONV_CASES = [  # (ci, co, k, s, d, g, mode, H, kind)
     (64, 64, 3, 1, 1, 1, "circular", 24, "convT"), (64, 64, 3, 1, 2, 1, "zeros", 20, "convT"),
     (64, 64, 3, 1, 2, 2, "circular", 20, "convT"), (1024, 1024, 3, 1, 2, 32, "circular", 16, "convT"),
     (128, 64, 5, 1, 1, 1, "zeros", 17, "convT"),
+    # stacked-window path (conv_stack.cu: >= 128 output channels, several small images per tile)
+    (128, 256, 3, 1, 2, 1, "circular", 12, "conv"), (256, 128, 5, 1, 1, 1, "zeros", 9, "conv"),
+    (128, 128, 3, 1, 1, 1, "circular", 7, "conv"), (256, 256, 3, 1, 1, 2, "circular", 8, "conv"),
+    (128, 128, 3, 1, 1, 1, "zeros", 30, "conv"), (512, 512, 3, 1, 1, 1, "circular", 5, "convT"),
+    (1024, 1024, 3, 1, 2, 1, "circular", 8, "conv"), (96, 128, 3, 1, 1, 1, "circular", 6, "conv"),
 ]
 
 
@@ -205,6 +210,7 @@ def test_conv_forward_and_transpose(cuda_lib, case, io):
         kdev, xdev, tdt, tol = dev(K), dev(x), torch.float32, TOL32
     Hh, Ww = x.shape[1], x.shape[2]
     Ho, Wo = plan.out_hw(0, Hh, Ww)
+    plan.reserve(plan.conv_scratch_bytes(0, N, Hh, Ww))   # stacked-window path where eligible
     y = torch.zeros((N, Ho, Wo, co_f), device="cuda", dtype=tdt)
     plan.conv_forward(0, kdev, xdev, y, bias=dev(bias))
     ref = O.conv2d(nchw(x.astype(np.float64)), K.astype(np.float64), s=s, d=d, g=g, mode=mode) \
@@ -231,6 +237,26 @@ def test_conv_pair_path(case):
     code = (f"import sys; sys.path.insert(0, {os.getcwd()!r}); import tests.test_gpu_parity as t; "
             f"import paper_2601_13776_b200 as orth; t.test_conv_forward_and_transpose(orth, {case!r}, 'bf16')")
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "ORTH_CONV_PAIR": "1"},
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+STACK_CASES = [(128, 256, 3, 1, 2, 1, "circular", 12, "conv"), (256, 128, 5, 1, 1, 1, "zeros", 9, "conv"),
+               (128, 128, 3, 1, 1, 1, "circular", 7, "conv"), (256, 256, 3, 1, 1, 2, "circular", 8, "conv"),
+               (128, 128, 3, 1, 1, 1, "zeros", 30, "conv"), (512, 512, 3, 1, 1, 1, "circular", 5, "convT"),
+               (96, 128, 3, 1, 1, 1, "circular", 6, "conv"), (512, 512, 3, 1, 1, 1, "circular", 4, "conv")]
+
+
+def test_conv_stack_path():
+    """The opt-in stacked-window kernel (conv_stack.cu, ORTH_CONV_STACK=1) on the same parity cases, in a
+    subprocess (the switch is read once); forward and adjoint, BF16."""
+    import os
+    import subprocess
+    import sys
+    code = (f"import sys; sys.path.insert(0, {os.getcwd()!r}); import tests.test_gpu_parity as t; "
+            f"import paper_2601_13776_b200 as orth\n"
+            f"for c in {STACK_CASES!r}: t.test_conv_forward_and_transpose(orth, c, 'bf16')")
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "ORTH_CONV_STACK": "1"},
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
 

@@ -19,6 +19,7 @@ kb = (torch.randn(co, k, k, ci // g, device="cuda") * 0.05).to(torch.bfloat16)
 x = torch.randn(N, H, H, ci, device="cuda").to(torch.bfloat16)
 Ho, Wo = plan.out_hw(0, H, H)
 y = torch.randn(N, Ho, Wo, co, device="cuda").to(torch.bfloat16)
+plan.reserve(plan.conv_scratch_bytes(0, N, H, H))
 f = (lambda: plan.conv_transpose(0, kb, y, x)) if adj else (lambda: plan.conv_forward(0, kb, x, y))
 for _ in range(3):
     f()

@@ -32,9 +32,9 @@ for r in rows[2:]:
         kernel=name[:48], us=get(d, "gpu__time_duration.sum"),
         dram_bytes=get(d, "dram__bytes_read.sum") + get(d, "dram__bytes_write.sum"),
         l2_bytes=get(d, "lts__t_sectors.sum") * 32,
-        l2_pct=get(d, "LTS.TriageCompute.lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+        l2_pct=get(d, "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
         dram_pct=get(d, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
-        tensor_pct=get(d, "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
+        tensor_pct=get(d, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
         grid=get(d, "launch__grid_size")))
 print(f"{'kernel':48s} {'us':>8s} {'DRAM MB':>9s} {'L2 MB':>9s} {'L2%':>6s} {'DRAM%':>6s} {'tensor%':>8s} {'grid':>5s}")
 for r in recs:

@@ -26,6 +26,11 @@ for l, d in enumerate(layers):
     Ho, _ = plan.out_hw(l, H, H)
     acts.append(torch.empty((256, Ho, Ho, d["c_out"]), device="cuda", dtype=torch.bfloat16))
     H = Ho
+need, Hc = 0, 32
+for l in range(len(layers)):
+    need = max(need, plan.conv_scratch_bytes(l, 256, Hc, Hc))
+    Hc = plan.out_hw(l, Hc, Hc)[0]
+plan.reserve(need)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(layers) + 1)]
 for _ in range(reps):
     cur = x

@@ -15,6 +15,8 @@
 #include <cstdint>
 
 #include "orth_internal.h"
+#include "pdl.h"
+#include "umma.cuh"
 
 namespace orth {
 namespace {
@@ -23,6 +25,8 @@ __global__ void __launch_bounds__(128) emit_kernel(const EmitItem* __restrict__ 
                                                    const float* b1, const float* b2, const float* b3,
                                                    float* __restrict__ kf32, __nv_bfloat16* __restrict__ kbf16) {
   extern __shared__ float row_sm[];   // one FP32 output row [i][t] (k^2 ci floats)
+  umma::griddep_launch_dependents();
+  umma::griddep_wait();
   const EmitItem e = items[blockIdx.y];
   const float* base = e.src_buf == 0 ? b0 : e.src_buf == 1 ? b1 : e.src_buf == 2 ? b2 : b3;
   const float* src = base + e.src_off;
@@ -75,8 +79,9 @@ int launch_emit(Plan& p, const float* const bufs[BUF_COUNT], float* kf32, uint16
     attr = smem;
   }
   dim3 grid((unsigned)(maxco < 256 ? maxco : 256), (unsigned)p.emit.size());
-  emit_kernel<<<grid, 128, smem, (cudaStream_t)stream>>>(p.d_emit, bufs[0], bufs[1], bufs[2], bufs[3], kf32,
-                                                      reinterpret_cast<__nv_bfloat16*>(kbf16));
+  launch_pdl(emit_kernel, grid, dim3(128), smem, (cudaStream_t)stream, (const EmitItem*)p.d_emit,
+             (const float*)bufs[0], (const float*)bufs[1], (const float*)bufs[2], (const float*)bufs[3], kf32,
+             reinterpret_cast<__nv_bfloat16*>(kbf16));
   p.launches++;
   return (int)cudaGetLastError();
 }

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "orth_internal.h"
+#include "pdl.h"
 #include "tma_host.h"
 #include "umma.cuh"
 
@@ -235,7 +236,8 @@ __global__ void __launch_bounds__(256, 1) tcg_tma_kernel(const TcgDesc* __restri
   __shared__ uint64_t full_bar[S], empty_bar[S], done_bar;
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const TcgDesc d = descs[tile_desc[blockIdx.x]];
+  umma::griddep_launch_dependents();
+  const TcgDesc d = descs[tile_desc[blockIdx.x]];   // plan constants: readable before the PDL wait
   const int local = blockIdx.x - d.tile_begin;
   const int m0 = (local / d.tiles_n) * 128, n0 = (local % d.tiles_n) * 128;
   if (warp == 0) umma::tmem_alloc(&tmem_base_sh, 128);
@@ -250,6 +252,7 @@ __global__ void __launch_bounds__(256, 1) tcg_tma_kernel(const TcgDesc* __restri
   umma::tc_fence_before();
   __syncthreads();
   umma::tc_fence_after();
+  umma::griddep_wait();   // PDL: the previous phase's outputs are complete
   const uint32_t tmem = tmem_base_sh;
   const uint32_t s0 = umma::smem_u32(smem);
   const int nkb = (d.K + 63) / 64;
@@ -373,6 +376,8 @@ __global__ void __launch_bounds__(256, 1) tcg_tma_kernel(const TcgDesc* __restri
 // FP32 ortho -> BF16 hi/lo copies (row-major padded, or the RKO phase split).
 // CTA = rows r = blockIdx.x + k gridDim.x of item blockIdx.y; 32-bit index math.
 __global__ void __launch_bounds__(256) cvt_kernel(const CvtItem* __restrict__ items, const float* __restrict__ ortho) {
+  umma::griddep_launch_dependents();
+  umma::griddep_wait();
   const CvtItem it = items[blockIdx.y];
   for (int r = blockIdx.x; r < it.m; r += gridDim.x) {
     const float* src = ortho + it.src_off + (int64_t)r * it.n;
@@ -409,7 +414,8 @@ int launch_phase(const TcgPhase& ph, cudaStream_t s) {
     attr = true;
   }
   if (ph.dmaps)
-    tcg_tma_kernel<<<ph.tiles, 256, smem, s>>>(ph.dd, ph.dtile, reinterpret_cast<const CUtensorMap*>(ph.dmaps));
+    launch_pdl(tcg_tma_kernel, dim3(ph.tiles), dim3(256), smem, s, ph.dd, ph.dtile,
+               reinterpret_cast<const CUtensorMap*>(ph.dmaps));
   else
     tcg_kernel<<<ph.tiles, 256, smem, s>>>(ph.dd, (int)ph.d.size(), ph.ds);
   return (int)cudaGetLastError();
@@ -705,7 +711,7 @@ int launch_compose_tc(Plan& P, const float* ortho, void* stream) {
     int maxm = 1;
     for (auto& c : T->cvt) maxm = std::max(maxm, c.m);
     dim3 grid((unsigned)std::min(maxm, 128), (unsigned)T->cvt.size());
-    cvt_kernel<<<grid, 256, 0, s>>>(T->dcvt, ortho);
+    launch_pdl(cvt_kernel, grid, dim3(256), 0, s, (const CvtItem*)T->dcvt, ortho);
     P.launches++;
     if (int e = (int)cudaGetLastError()) return e;
   }

@@ -39,6 +39,7 @@
 #include <tuple>
 
 #include "orth_internal.h"
+#include "pdl.h"
 #include "tma_host.h"
 #include "umma.cuh"
 
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
              const __grid_constant__ PadMaps tmA, const __grid_constant__ CUtensorMap tmB,
              const __grid_constant__ CUtensorMap tmY) {
   extern __shared__ uint8_t smem_raw[];
+  umma::griddep_launch_dependents();
   uint8_t* smem = umma::align1024_smem(smem_raw);
   constexpr int B_BYTES = BN * 128;
   __shared__ uint64_t a_full[MAX_AB], a_empty[MAX_AB], b_full[MAX_SB], b_empty[MAX_SB], tfull_bar[2], tempty_bar[2];
@@ -137,6 +139,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   umma::tc_fence_before();
   __syncthreads();
   umma::tc_fence_after();
+  umma::griddep_wait();   // PDL: the previous kernel's outputs (x, weights) are complete
   const uint32_t tmem = tmem_base_sh;
   const uint32_t abase = umma::smem_u32(smem);
   const uint32_t bbase = abase + NA * a.abuf_bytes;
@@ -498,7 +501,7 @@ int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* b
   }
   const int grid = a.bres ? (a.num_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta
                           : (a.num_tiles < sm_count() ? a.num_tiles : sm_count());
-  conv_pad<BN, SW><<<grid, NTHREADS, smem, stream>>>(bias, out, a, maps, tm, ty);
+  launch_pdl(conv_pad<BN, SW>, dim3(grid), dim3(NTHREADS), smem, stream, bias, out, a, maps, tm, ty);
 #ifdef ORTH_CONV_TRACE
   {
     cudaStreamSynchronize(stream);

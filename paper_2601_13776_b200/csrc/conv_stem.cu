@@ -17,6 +17,7 @@
 #include <cstring>
 
 #include "orth_internal.h"
+#include "pdl.h"
 #include "tma_host.h"
 #include "umma.cuh"
 
@@ -46,11 +47,13 @@ __global__ void __launch_bounds__(128) conv_stem_tc(const __nv_bfloat16* __restr
   __shared__ uint64_t done_bar;
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  umma::griddep_launch_dependents();
   if (warp == 0) umma::tmem_alloc(&tmem_base_sh, TM);
   if (tid == 0) {
     umma::mbar_init(&done_bar, 1);
     umma::fence_mbar_init();
   }
+  umma::griddep_wait();   // PDL: weights and x of the previous kernels are complete
   // resident weights: row o = W[o][0..KT) (GEMM layout), zero-padded to 64
   for (int e = tid; e < CO * 8; e += 128) {
     const int o = e >> 3, c = e & 7;
@@ -185,7 +188,7 @@ int launch_stem(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bia
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return (int)cudaErrorInvalidValue;
-  conv_stem_tc<CO, CI, KS><<<grid, 128, 0, s>>>(x, w, bias, y, a, tm);
+  launch_pdl(conv_stem_tc<CO, CI, KS>, dim3(grid), dim3(128), 0, s, x, w, bias, y, a, tm);
   return (int)cudaGetLastError();
 }
 

@@ -32,6 +32,7 @@
 #include <cstdlib>
 
 #include "orth_internal.h"
+#include "pdl.h"
 #include "tma_host.h"
 #include "umma.cuh"
 
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     conv_ws(const __nv_bfloat16* __restrict__ in, const float* __restrict__ bias, __nv_bfloat16* __restrict__ out,
             const __grid_constant__ TcConvArgs a, const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ uint8_t smem_raw[];
+  umma::griddep_launch_dependents();
   uint8_t* smem = umma::align1024_smem(smem_raw);
   constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
   int* tab = reinterpret_cast<int*>(smem + S * STAGE);   // [valid tap j][128] input pixel, -1 = padding
@@ -170,6 +172,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   if (cs > 1) umma::cluster_sync_all();   // peers' barriers initialised before any multicast
   umma::tc_fence_after();
+  umma::griddep_wait();   // PDL: the previous kernel's outputs (x, weights) are complete
   const uint32_t tmem = tmem_base_sh;
   const uint32_t s0 = umma::smem_u32(smem);
   const int kc = (a.cr_g + 63) / 64;
@@ -588,6 +591,8 @@ __global__ void __launch_bounds__(256) transpose_w_kernel(const __nv_bfloat16* _
                                                           __nv_bfloat16* __restrict__ wt, int g, int co_g, int ci_g,
                                                           int taps) {
   __shared__ __nv_bfloat16 tile[32][34];
+  umma::griddep_launch_dependents();
+  umma::griddep_wait();
   const int gt = blockIdx.z;   // (group, tap)
   const int gi = gt / taps, t = gt - gi * taps;
   const int o0 = blockIdx.y * 32, i0 = blockIdx.x * 32;
@@ -635,13 +640,15 @@ int launch_ws(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const
   cfg.blockDim = dim3(NTHREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = (unsigned)a.cs;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (pdl.h)
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   const int e = (int)cudaLaunchKernelEx(&cfg, conv_ws<BN, S>, in, bias, out, a, tm);
 #ifdef ORTH_CONV_TRACE
   {
@@ -777,6 +784,8 @@ namespace {
 // W'[(gp P co + p co + o) k^2 + t][q ci + i] = (p == q) ? W[((gp P + p) co + o) k^2 + t][i] : 0
 __global__ void __launch_bounds__(256) pack_w_kernel(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wp,
                                                      int gpacks, int P, int co, int ci, int taps) {
+  umma::griddep_launch_dependents();
+  umma::griddep_wait();
   const int64_t rowlen = (int64_t)P * ci;
   const int64_t total = (int64_t)gpacks * P * co * taps * rowlen;
   for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (int64_t)gridDim.x * 256) {
@@ -808,7 +817,7 @@ static int pack_weights(const LayerInfo& L, int P, const void* kernel, void* dst
   const int taps = L.k * L.k;
   const int64_t total = (int64_t)L.co_f * taps * P * L.ci;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-  pack_w_kernel<<<blocks, 256, 0, s>>>((const __nv_bfloat16*)kernel, (__nv_bfloat16*)dst, L.g / P, P, L.co, L.ci,
+  launch_pdl(pack_w_kernel, dim3(blocks), dim3(256), 0, s, (const __nv_bfloat16*)kernel, (__nv_bfloat16*)dst, L.g / P, P, L.co, L.ci,
                                        taps);
   return (int)cudaGetLastError();
 }
@@ -852,7 +861,7 @@ int launch_conv_bwd_tc(const LayerInfo& L0, const void* kernel, void* wt_scratch
     kernel = pk;
   }
   dim3 tg((unsigned)((L.ci + 31) / 32), (unsigned)((L.co + 31) / 32), (unsigned)(L.g * taps));
-  transpose_w_kernel<<<tg, 256, 0, s>>>((const __nv_bfloat16*)kernel, (__nv_bfloat16*)wt_scratch, L.g, L.co, L.ci,
+  launch_pdl(transpose_w_kernel, tg, dim3(256), 0, s, (const __nv_bfloat16*)kernel, (__nv_bfloat16*)wt_scratch, L.g, L.co, L.ci,
                                         taps);
   if (int e = (int)cudaGetLastError()) return e;
   static const bool no_reuse = std::getenv("ORTH_CONV_NO_REUSE") != nullptr;   // A/B switch

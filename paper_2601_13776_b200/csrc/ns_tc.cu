@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "orth_internal.h"
+#include "pdl.h"
 #include "umma.cuh"
 #include "tma_host.h"
 
@@ -268,6 +269,8 @@ __global__ void __launch_bounds__(256) scale_bf16_kernel(const PowerItem* __rest
                                                          float* __restrict__ X0, NsBufs b, int par, int write_lo,
                                                          unsigned* __restrict__ bars, int nbars,
                                                          unsigned* __restrict__ power_bar_p) {
+  umma::griddep_launch_dependents();
+  umma::griddep_wait();   // PDL: the power kernel (sigma, and its barrier word re-armed below) is complete
   if (blockIdx.x == 0) {   // re-arm the persistent NS group barriers and the fused power kernel's barrier
     for (int i = threadIdx.x; i < nbars; i += 256) bars[i] = 0u;
     if (threadIdx.x == 0) *power_bar_p = 0u;
@@ -462,8 +465,9 @@ int launch_scale_bf16(Plan& p, const float* W, float* X0, int par, bool write_lo
   if (p.power_items.empty()) return 0;
   float* bufs[BUF_COUNT] = {X0, X0, nullptr, nullptr};
   NsBufs b = make_bufs(p, bufs);
-  scale_bf16_kernel<<<(int)p.power_items.size(), 256, 0, (cudaStream_t)stream>>>(
-      p.d_power_items, W, p.d_sigma, X0, b, par, write_lo, p.nsp_bars, p.nsp_bars ? p.nsp_zero_n : 0, power_bar(p));
+  launch_pdl(scale_bf16_kernel, dim3((unsigned)p.power_items.size()), dim3(256), 0, (cudaStream_t)stream,
+             (const PowerItem*)p.d_power_items, W, (const float*)p.d_sigma, X0, b, par, (int)write_lo, p.nsp_bars,
+             p.nsp_bars ? p.nsp_zero_n : 0, power_bar(p));
   p.launches++;
   return (int)cudaGetLastError();
 }

@@ -132,6 +132,15 @@ __device__ __forceinline__ uint8_t* align1024_smem(uint8_t* raw) {
   return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
 }
 
+// Programmatic dependent launch (PDL).  A kernel launched with the programmatic-
+// serialization attribute (launch_pdl) may start while its predecessor drains;
+// griddep_wait() blocks until the predecessor grid has completed and its writes
+// are visible -- every such kernel calls it before its first global access.
+// griddep_launch_dependents() lets the NEXT kernel launch once every CTA of this
+// grid has executed it.  Both are no-ops without the attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // ---------------------------------------------------------------- descriptors
 // K-major SWIZZLE_128B smem descriptor (version 1 = sm_100, SBO = 1024 B).
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {

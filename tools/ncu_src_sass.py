@@ -1,5 +1,5 @@
 """Attribute SASS warp-stall samples to CUDA source lines (ncu --print-source cuda,sass).
-usage: python tools/ncu_src_sass.py REPORT [top]"""
+usage: python tools/ncu_src_sass.py REPORT [top] [launch_index]"""
 import collections
 import csv
 import io
@@ -8,7 +8,9 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+idx = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
+                      "--launch-skip", str(idx), "--launch-count", "1"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = next(r for r in rows if len(r) > 4 and r[0] == "Line No")

@@ -153,3 +153,16 @@ def test_host_only_plan_cannot_compute():
     with pytest.raises(orth.OrthError) as ei:
         orth.orth_orthogonalize(p.h, Fake(256), Fake(512), stream=0)
     assert ei.value.status == orth.NO_DEVICE
+
+
+def test_host_only_plan_cannot_reserve_and_scratch_sizes():
+    """orth_plan_reserve needs a device (host-only plan: NO_DEVICE); the conv-scratch helper
+    covers the padded forward-view input of both directions."""
+    p = orth.Plan(configs.cfg2(), device=-1)
+    with pytest.raises(orth.OrthError) as ei:
+        p.reserve(1 << 20)
+    assert ei.value.status == orth.NO_DEVICE
+    # layer 1: 64 -> 64, 3x3 circular at 32x32, batch 256: 256 * 34 * 34 * 64 * 2 bytes
+    assert p.conv_scratch_bytes(1, 256, 32, 32) == 256 * 34 * 34 * 64 * 2
+    # a stride-2 layer: the padded copy is sized on the larger (input) grid
+    assert p.conv_scratch_bytes(3, 256, 32, 32) == 256 * 34 * 34 * 128 * 2

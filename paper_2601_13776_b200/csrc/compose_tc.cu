@@ -373,6 +373,198 @@ __global__ void __launch_bounds__(256, 1) tcg_tma_kernel(const TcgDesc* __restri
   if (warp == 0) umma::tmem_dealloc(tmem, 128);
 }
 
+// Persistent, pipelined version of tcg_tma_kernel (default): grid <= #SMs, each
+// CTA walks tiles tile = blockIdx.x + i * gridDim.x.  Warp 0 = TMA producer
+// (3-stage ring of {A, B} x {hi, lo} 64-deep K blocks), warp 1 = TMEM owner +
+// single-thread MMA issuer into one of two 128-column accumulators, warps 2-9 =
+// epilogue (the same FP32 / hi-lo / second / transposed outputs as above, in
+// four 32-column passes through an 18 KB staging tile).  The epilogue of tile i
+// overlaps the loads and MMAs of tile i+1 (the 1-tile-per-CTA kernel paid the
+// CTA launch, prologue and a serial epilogue per tile).
+constexpr int kTcpThreads = 320;
+constexpr int kTcpSf = 128 * 36;   // floats of the staging tile [128][32 + 4]
+
+__global__ void __launch_bounds__(kTcpThreads, 1) tcg_tma_persist(const TcgDesc* __restrict__ descs,
+                                                                  const int* __restrict__ tile_desc, int ntiles,
+                                                                  const CUtensorMap* __restrict__ maps) {
+  constexpr int TILE = 128 * 128, STAGE = 4 * TILE;
+  extern __shared__ uint8_t smem_raw[];
+  umma::griddep_launch_dependents();
+  uint8_t* smem = umma::align1024_smem(smem_raw);
+  float* Sf = reinterpret_cast<float*>(smem + S * STAGE);
+  __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 1) umma::tmem_alloc(&tmem_base_sh, 256);
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      umma::mbar_init(&full_bar[i], 1);
+      umma::mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      umma::mbar_init(&tfull_bar[i], 1);
+      umma::mbar_init(&tempty_bar[i], 8);   // one arrival per epilogue warp
+    }
+    umma::fence_mbar_init();
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  umma::griddep_wait();   // PDL: the previous phase's outputs are complete
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t s0 = umma::smem_u32(smem);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- producer
+      int kb_all = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const TcgDesc& d = descs[tile_desc[tile]];
+        const int local = tile - d.tile_begin;
+        const int m0 = (local / d.tiles_n) * 128, n0 = (local % d.tiles_n) * 128;
+        const int nkb = (d.K + 63) / 64, nk = nkb * d.seg_count;
+        for (int kb = 0; kb < nk; ++kb, ++kb_all) {
+          const int st = kb_all % S;
+          if (kb_all >= S) umma::mbar_wait(&empty_bar[st], ((kb_all / S) - 1) & 1);
+          const CUtensorMap* mp = maps + 4 * (d.seg_begin + kb / nkb);
+          const int k0 = (kb % nkb) * 64;
+          const uint32_t sa = s0 + st * STAGE;
+          umma::mbar_arrive_expect_tx(&full_bar[st], STAGE);
+          umma::tma_load_2d(sa, mp + 0, &full_bar[st], k0, m0);
+          umma::tma_load_2d(sa + TILE, mp + 1, &full_bar[st], k0, n0);
+          umma::tma_load_2d(sa + 2 * TILE, mp + 2, &full_bar[st], k0, m0);
+          umma::tma_load_2d(sa + 3 * TILE, mp + 3, &full_bar[st], k0, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      constexpr uint32_t IDESC = umma::idesc_bf16(128, 128);
+      int kb_all = 0, tcount = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+        const TcgDesc& d = descs[tile_desc[tile]];
+        const int nk = ((d.K + 63) / 64) * d.seg_count;   // 0: empty product (rank-0 projector), acc = 0
+        const int acc = tcount & 1;
+        if (tcount >= 2) umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) - 1) & 1);
+        umma::tc_fence_after();
+        const uint32_t dt = tmem + acc * 128;
+        for (int kb = 0; kb < nk; ++kb, ++kb_all) {
+          const int st = kb_all % S;
+          umma::mbar_wait(&full_bar[st], (kb_all / S) & 1);
+          umma::tc_fence_after();
+          const uint32_t ah = s0 + st * STAGE, bh = ah + TILE, al = ah + 2 * TILE, bl = ah + 3 * TILE;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint64_t dah = umma::sdesc_sw128(ah + 32 * q), dbh = umma::sdesc_sw128(bh + 32 * q);
+            umma::mma_bf16(dt, dah, dbh, IDESC, (kb | q) != 0);
+            umma::mma_bf16(dt, dah, umma::sdesc_sw128(bl + 32 * q), IDESC, 1);
+            umma::mma_bf16(dt, umma::sdesc_sw128(al + 32 * q), dbh, IDESC, 1);
+          }
+          umma::mma_commit(&empty_bar[st]);
+        }
+        umma::mma_commit(&tfull_bar[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------------ epilogue (warps 2-9)
+    const int ew = warp - 2, etid = tid - 64;
+    const int q = warp & 3, sub = ew >> 2, r_own = q * 32 + lane;   // TMEM lane quarter = warp % 4
+    constexpr int LDF = 36;
+    int tcount = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+      const TcgDesc d = descs[tile_desc[tile]];
+      const int local = tile - d.tile_begin;
+      const int m0 = (local / d.tiles_n) * 128, n0 = (local % d.tiles_n) * 128;
+      const int nk = ((d.K + 63) / 64) * d.seg_count;
+      const bool fvec = d.f && (d.ldf & 3) == 0;
+      const int acc = tcount & 1;
+      umma::mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
+      umma::tc_fence_after();
+#pragma unroll 1
+      for (int h = 0; h < 4; ++h) {   // 32-column passes
+        {
+          float v[16];
+          umma::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + h * 32 + sub * 16), v);
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            *reinterpret_cast<float4*>(Sf + r_own * LDF + sub * 16 + 4 * t) =
+                nk > 0 ? make_float4(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (h == 3) {   // accumulator drained: release it to the MMA warp
+          umma::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) umma::mbar_arrive(&tempty_bar[acc]);
+        }
+        umma::named_bar_sync(1, 256);
+#pragma unroll 2
+        for (int u = 0; u < 4; ++u) {
+          const int e = etid + 256 * u, r = e >> 3, c4 = (e & 7) * 4;
+          const int i = m0 + r, j0 = n0 + h * 32 + c4;
+          const float4 a = *reinterpret_cast<const float4*>(Sf + r * LDF + c4);
+          const float accv[4] = {a.x, a.y, a.z, a.w};
+          float o[4], o2[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const bool ok = i < d.M && j0 + k < d.N;
+            const float dg = (i == j0 + k) ? 1.f : 0.f;
+            o[k] = ok ? fmaf(d.alpha, accv[k], d.diag * dg) : 0.f;
+            o2[k] = ok ? fmaf(d.alpha2, accv[k], d.diag2 * dg) : 0.f;
+          }
+          if (d.f && i < d.M && j0 < d.N) {
+            float* dst = d.f + (int64_t)i * d.ldf + j0;
+            if (fvec && j0 + 3 < d.N) {
+              *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                if (j0 + k < d.N) dst[k] = o[k];
+            }
+          }
+          if (i < d.M && j0 < d.ldo) {   // ldo % 8 == 0: the 4-group lies inside the padded row
+            const int64_t bo = (int64_t)i * d.ldo + j0;
+            uint2 hv, lv;
+            if (d.oh) {
+              split4(o[0], o[1], o[2], o[3], hv, lv);
+              *reinterpret_cast<uint2*>(d.oh + bo) = hv;
+              *reinterpret_cast<uint2*>(d.ol + bo) = lv;
+            }
+            if (d.o2h) {
+              split4(o2[0], o2[1], o2[2], o2[3], hv, lv);
+              *reinterpret_cast<uint2*>(d.o2h + bo) = hv;
+              *reinterpret_cast<uint2*>(d.o2l + bo) = lv;
+            }
+          }
+          if (d.th) *reinterpret_cast<float4*>(Sf + r * LDF + c4) = make_float4(o[0], o[1], o[2], o[3]);
+        }
+        umma::named_bar_sync(1, 256);
+        if (d.th) {   // transposed rows: lane -> column, 8 rows -> one 16-byte store
+#pragma unroll 1
+          for (int u = 0; u < 2; ++u) {
+            const int e = etid + 256 * u, cl = e & 31, i8 = (e >> 5) * 8;
+            const int jn = n0 + h * 32 + cl, i0 = m0 + i8;
+            float x[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) x[t] = Sf[(i8 + t) * LDF + cl];
+            if (jn < d.N && i0 < d.ldt) {
+              uint2 h0, l0, h1, l1;
+              split4(x[0], x[1], x[2], x[3], h0, l0);
+              split4(x[4], x[5], x[6], x[7], h1, l1);
+              const int64_t o = (int64_t)jn * d.ldt + i0;
+              *reinterpret_cast<uint4*>(d.th + o) = make_uint4(h0.x, h0.y, h1.x, h1.y);
+              *reinterpret_cast<uint4*>(d.tl + o) = make_uint4(l0.x, l0.y, l1.x, l1.y);
+            }
+          }
+          umma::named_bar_sync(1, 256);
+        }
+      }
+    }
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) umma::tmem_dealloc(tmem, 256);
+}
+
 // FP32 ortho -> BF16 hi/lo copies (row-major padded, or the RKO phase split).
 // CTA = rows r = blockIdx.x + k gridDim.x of item blockIdx.y; 32-bit index math.
 __global__ void __launch_bounds__(256) cvt_kernel(const CvtItem* __restrict__ items, const float* __restrict__ ortho) {
@@ -413,7 +605,21 @@ int launch_phase(const TcgPhase& ph, cudaStream_t s) {
     cudaFuncSetAttribute(tcg_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  if (ph.dmaps)
+  static const bool one_tile = std::getenv("ORTH_COMPOSE_ONE_TILE") != nullptr;   // A/B: 1 tile per CTA
+  if (ph.dmaps && !one_tile) {
+    const size_t smem_p = 1024 + (size_t)S * 4 * 128 * 128 + (size_t)kTcpSf * 4;
+    static bool attr_p = false;
+    if (!attr_p) {
+      cudaFuncSetAttribute(tcg_tma_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
+      attr_p = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::min(ph.tiles, sms);
+    launch_pdl(tcg_tma_persist, dim3(grid), dim3(kTcpThreads), smem_p, s, (const TcgDesc*)ph.dd,
+               (const int*)ph.dtile, ph.tiles, reinterpret_cast<const CUtensorMap*>(ph.dmaps));
+  } else if (ph.dmaps)
     launch_pdl(tcg_tma_kernel, dim3(ph.tiles), dim3(256), smem, s, ph.dd, ph.dtile,
                reinterpret_cast<const CUtensorMap*>(ph.dmaps));
   else

@@ -547,7 +547,8 @@ bool conv_act_tmap(CUtensorMap_st* out, const void* x, int C, int W, int H, int 
 // that would cross groups, circular padding that is not a single wrap, ...).
 static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, int& bn, PadArgs& a, bool sw) {
   const int ext = L.d * (L.k - 1);
-  if (L.s != 1 || Wo > 128 || Wo < 16 || L.k > 7 || L.co > 64) return false;
+  static const int co_max = std::getenv("ORTH_CONV_PAD_COMAX") ? std::atoi(std::getenv("ORTH_CONV_PAD_COMAX")) : 64;
+  if (L.s != 1 || Wo > 128 || Wo < 16 || L.k > 7 || L.co > (sw ? 64 : co_max)) return false;
   if (L.g > 1 && L.ci % 64 != 0) return false;          // a 64-channel box must stay inside the group
   if (L.ci_f % 8 != 0) return false;                     // TMA row stride: multiple of 16 bytes
   const bool circ = L.desc.padding_mode == ORTH_PAD_CIRCULAR;

@@ -140,7 +140,17 @@ __device__ float block_sum(float v, float* red) {
 // w = W^T u; sig = |w|; v = w / sig.  Split over row items (t = W v, |t|^2
 // partials) and column items (w = W^T u, |w|^2 partials) with a grid barrier
 // between; every norm is a fixed-order sum over the matrix's items.
+#ifdef ORTH_POWER_TRACE
+__device__ unsigned long long power_trace[1024 * 8];
+#endif
 __device__ __forceinline__ void power_grid_sync(unsigned* bar, unsigned target) {
+#ifdef ORTH_POWER_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024 && target / gridDim.x <= 7) {   // arrival time at barrier k
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    power_trace[blockIdx.x * 8 + target / gridDim.x] = t;
+  }
+#endif
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -155,11 +165,16 @@ __device__ __forceinline__ void power_grid_sync(unsigned* bar, unsigned target) 
 }
 
 // fixed-order sum of cnt partials (thread 0), broadcast through smem
+// (the partials are fetched by all threads at once -- one L2 round trip -- and
+// summed by thread 0 in index order from shared memory: deterministic)
 __device__ __forceinline__ float ordered_sum(const float* p, int cnt, float* slot) {
+  __shared__ float vals[256];
+  __syncthreads();
+  for (int c = threadIdx.x; c < cnt && c < 256; c += blockDim.x) vals[c] = __ldcg(p + c);
   __syncthreads();
   if (threadIdx.x == 0) {
     float s = 0.f;
-    for (int c = 0; c < cnt; ++c) s += p[c];
+    for (int c = 0; c < cnt; ++c) s += c < 256 ? vals[c] : __ldcg(p + c);
     *slot = s;
   }
   __syncthreads();
@@ -186,6 +201,13 @@ __global__ void __launch_bounds__(256) power_fused_kernel(const PowerItem* __res
   __shared__ float slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned k = 0;
+#ifdef ORTH_POWER_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    power_trace[blockIdx.x * 8 + 0] = t;
+  }
+#endif
   if (frob) {   // |W|_F: sums of squares per row item, then per matrix in item order
     for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
       const PowerItem it = items[i];
@@ -248,9 +270,18 @@ __global__ void __launch_bounds__(256) power_fused_kernel(const PowerItem* __res
         const int r = r0 + threadIdx.x / T, sub = threadIdx.x % T;
         float a = 0.f;
         if (r < rows) {
-          if (staged) {
+          if (staged) {   // four independent accumulators (the chain was LDS-latency bound), summed in order
             const float* row = Ws + r * ldw;
-            for (int j = sub; j < n; j += T) a = fmaf(row[j], v[j], a);
+            float a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            int j = sub;
+            for (; j + 3 * T < n; j += 4 * T) {
+              a = fmaf(row[j], v[j], a);
+              a1 = fmaf(row[j + T], v[j + T], a1);
+              a2 = fmaf(row[j + 2 * T], v[j + 2 * T], a2);
+              a3 = fmaf(row[j + 3 * T], v[j + 3 * T], a3);
+            }
+            for (; j < n; j += T) a = fmaf(row[j], v[j], a);
+            a = (a + a1) + (a2 + a3);
           } else {
             const float* row = Wm + (int64_t)(it.r0 + r) * n;
             float a2 = 0.f;
@@ -285,7 +316,7 @@ __global__ void __launch_bounds__(256) power_fused_kernel(const PowerItem* __res
       if (threadIdx.x == 0 && !(tt > 0.f && isfinite(tt))) atomicCAS(status, 0, (int)ORTH_ERR_ZERO_NORM);
       float* u = sm;
       for (int r = threadIdx.x; r < m; r += 256) u[r] = pb.t[ci.t_off + r] * inv;
-      const int lanes = cw < 256 ? ((cw + 31) / 32) * 32 : 256;   // column threads (whole warps)
+      const int lanes = cw <= 16 ? 16 : cw < 256 ? ((cw + 31) / 32) * 32 : 256;   // column threads
       const int ng = 256 / lanes, g = threadIdx.x / lanes, jj = threadIdx.x % lanes;
       float* part = sm + ((m + 3) & ~3);   // ng x lanes
       const float* Wm = W + ci.off;
@@ -308,7 +339,16 @@ __global__ void __launch_bounds__(256) power_fused_kernel(const PowerItem* __res
         float a = 0.f;
         if (g < ng && j0 + jj < cw) {
           if (staged) {
-            for (int r = g; r < m; r += ng) a = fmaf(Ws[r * ldc + j0 + jj], u[r], a);
+            float a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            int r = g;
+            for (; r + 3 * ng < m; r += 4 * ng) {
+              a = fmaf(Ws[r * ldc + j0 + jj], u[r], a);
+              a1 = fmaf(Ws[(r + ng) * ldc + j0 + jj], u[r + ng], a1);
+              a2 = fmaf(Ws[(r + 2 * ng) * ldc + j0 + jj], u[r + 2 * ng], a2);
+              a3 = fmaf(Ws[(r + 3 * ng) * ldc + j0 + jj], u[r + 3 * ng], a3);
+            }
+            for (; r < m; r += ng) a = fmaf(Ws[r * ldc + j0 + jj], u[r], a);
+            a = (a + a1) + (a2 + a3);
           } else {
 #pragma unroll 8
             for (int r = g; r < m; r += ng) a = fmaf(__ldg(Wm + (int64_t)r * n + j), u[r], a);
@@ -430,10 +470,28 @@ int launch_power_fused(Plan& p, const float* W, const float* v_in, int use_const
   cfg.attrs = attr_c;
   cfg.numAttrs = 1;
   p.launches++;
-  return (int)cudaLaunchKernelEx(&cfg, power_fused_kernel, (const PowerItem*)p.d_power_items, n_items,
-                                 (const ColItem*)p.d_col_items, n_cols, (const MatItem*)p.d_mat_items, n_mats, W,
-                                 v_in, use_const_v, frob, iters, pb, p.d_vbuf, cache_out, p.d_sigma, p.d_status,
-                                 power_bar(p));
+  const int e = (int)cudaLaunchKernelEx(&cfg, power_fused_kernel, (const PowerItem*)p.d_power_items, n_items,
+                                        (const ColItem*)p.d_col_items, n_cols, (const MatItem*)p.d_mat_items, n_mats,
+                                        W, v_in, use_const_v, frob, iters, pb, p.d_vbuf, cache_out, p.d_sigma,
+                                        p.d_status, power_bar(p));
+#ifdef ORTH_POWER_TRACE
+  {   // per barrier k: mean / max arrival after the kernel start (all CTAs)
+    cudaStreamSynchronize((cudaStream_t)stream);
+    static unsigned long long h[1024 * 8];
+    cudaMemcpyFromSymbol(h, power_trace, sizeof(h));
+    const int nb = std::min(grid, 1024);
+    unsigned long long t0 = ~0ull;
+    for (int c = 0; c < nb; ++c) t0 = std::min(t0, h[c * 8]);
+    std::printf("power_fused grid=%d items=%d cols=%d:", grid, n_items, n_cols);
+    for (int q = 1; q <= 2 * iters && q < 8; ++q) {
+      double mean = 0, mx = 0;
+      for (int c = 0; c < nb; ++c) { const double d = (double)(h[c * 8 + q] - t0) * 1e-3; mean += d; mx = std::max(mx, d); }
+      std::printf(" b%d %.1f/%.1f", q, mean / nb, mx);
+    }
+    std::printf(" us (mean/max arrival)\n");
+  }
+#endif
+  return e;
 }
 
 int launch_scale(Plan& p, const float* W, float* X0, void* stream) {

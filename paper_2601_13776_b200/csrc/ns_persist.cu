@@ -735,7 +735,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           NSP_TRACE(if (ph.ttrace && ew == 0 && lane == 0) ph.ttrace[16 * idx + 9 + 3 * c] = gtimer());
           // per-chunk constants re-derived here (cheap) instead of being held in registers
-#ifdef ORTH_NS_EXP   // timing experiment only (wrong results): fp32 X written by the last phases only
+#if defined(ORTH_NS_EXP2)
+          const bool wf = false;
+#elif defined(ORTH_NS_EXP)   // timing experiment only (wrong results): fp32 X written by the last phases only
           const bool wf = p >= ph.n - 2;
 #else
           const bool wf = upd || write_f;
@@ -780,7 +782,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                   if (j + 3 < N) dst[3] = o3;
                 }
               }
+#ifdef ORTH_NS_EXP2   // timing experiment only (wrong results): no BF16 stores
+              if (false) {
+#else
               if (j < ldb16) {   // ldb16 % 8 == 0, j % 4 == 0: the 4-group lies inside the padded row
+#endif
                 const uint32_t h01 = pack_bf16(o0, o1), h23 = pack_bf16(o2, o3);
                 const int64_t bo = (int64_t)i * ldb16 + j;
                 *reinterpret_cast<uint2*>(oh + bo) = make_uint2(h01, h23);

@@ -565,9 +565,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         {
           const NsTile tl{item.desc, item.local};
           const NsDesc d = D[tl.desc];
-          const int m0 = (tl.local / d.tiles_n) * 128, n0 = (tl.local % d.tiles_n) * 128;
+          const int tw = (!gram && d.epi == 2) ? 64 : 128;   // 64-wide update tiles (launch_ns_persist)
+          const int m0 = (tl.local / d.tiles_n) * 128, n0 = (tl.local % d.tiles_n) * tw;
           const int nk = (d.K + 63) / 64, a_mn = d.a_kind == 1, b_mn = d.b_kind == 1;
           const bool sym = gram && m0 == n0;   // diagonal Gram tile: B == A, loaded once
+          const bool b_half = tw == 64 && b_mn;   // MN-major B: only the first 64-wide box
+          const uint32_t stage_bytes = sym ? kSlot / 2 : (b_half ? kSlot / 2 + 8192 : kSlot);
           const CUtensorMap* ma = maps + d.map_a + 2 * par;
           const CUtensorMap* mb = maps + d.map_b + 2 * par;
           for (int kb = 0; kb < nk; ++kb) {
@@ -581,12 +584,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               used |= 1u << qs;
             }
             const uint32_t sa = ring + s * kSlot;
-            umma::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(sym ? w * kSlot / 2 : w * kSlot));
+            umma::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)w * stage_bytes);
             load_operand(sa, ma, &full_bar[s], kb * 64, m0, a_mn);
-            if (!sym) load_operand(sa + 16384, mb, &full_bar[s], kb * 64, n0, b_mn);
+            if (b_half) umma::tma_load_2d(sa + 16384, mb, &full_bar[s], n0, kb * 64);
+            else if (!sym) load_operand(sa + 16384, mb, &full_bar[s], kb * 64, n0, b_mn);
             if (split) {
               load_operand(sa + 32768, ma + 1, &full_bar[s], kb * 64, m0, a_mn);
-              if (!sym) load_operand(sa + 49152, mb + 1, &full_bar[s], kb * 64, n0, b_mn);
+              if (b_half) umma::tma_load_2d(sa + 49152, mb + 1, &full_bar[s], n0, kb * 64);
+              else if (!sym) load_operand(sa + 49152, mb + 1, &full_bar[s], kb * 64, n0, b_mn);
             }
             cnt += w;
           }
@@ -614,7 +619,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nk = (__ldg(&dp->K) + 63) / 64, a_mn = __ldg(&dp->a_kind) == 1, b_mn = __ldg(&dp->b_kind) == 1;
           const int tn = __ldg(&dp->tiles_n);
           const bool sym = gram && (tl.local / tn) == (tl.local % tn);
-          const uint32_t idesc = umma::idesc_bf16(128, 128) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
+          const bool w64 = !gram && __ldg(&dp->epi) == 2;
+          const uint32_t idesc = (w64 ? umma::idesc_bf16(128, 64) : umma::idesc_bf16(128, 128)) |
+                                 ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
           const int buf = acc & 1;
           if (acc >= 2) umma::mbar_wait(&tempty_bar[buf], ((acc >> 1) - 1) & 1);
           umma::tc_fence_after();
@@ -681,16 +688,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const NsDesc* dp = reinterpret_cast<const NsDesc*>(desc_sh[ew]);
         const int tiles_n = dp->tiles_n;
-        const int m0 = (tl.local / tiles_n) * 128 + row0, n0 = (tl.local % tiles_n) * 128 + ch * 64;
-        const bool upd = (dp->epi) == 1;
+        const bool upd = (dp->epi) >= 1;
+        const int cw = (upd && dp->epi == 2) ? 32 : 64;   // columns per warp (64-wide update tiles: one chunk)
+        const int nch = cw / 32;
+        const int m0 = (tl.local / tiles_n) * 128 + row0, n0 = (tl.local % tiles_n) * (2 * cw) + ch * cw;
         const int64_t f_off = (dp->f_off), ldf = (dp->ldf);
         const int M = (dp->M), N = (dp->N);
         const int buf = acc & 1;
-        if (upd) {   // C = X (fp32) rows m0.., cols n0..n0+63 -> Sc[0..1]
+        if (upd) {   // C = X (fp32) rows m0.., cols n0..n0+cw-1 -> Sc[0..nch-1]
           const float* Cm = pick(bufs.X, par) + f_off;
           const bool fv4 = (ldf & 3) == 0;
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
+#pragma unroll 1
+          for (int c = 0; c < nch; ++c) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const int e = lane + 32 * k, r = e >> 3, q = e & 7;
@@ -712,24 +721,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma::tc_fence_after();
         NSP_TRACE(if (ph.ttrace && ew == 0 && lane == 0) ph.ttrace[16 * idx + 5] = gtimer());
 #pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < nch; ++c) {
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             float v[16];
-            umma::tmem_ld16(tmem + buf * 128 + ch * 64 + c * 32 + hh * 16 + ((uint32_t)row0 << 16), v);
+            umma::tmem_ld16(tmem + buf * 128 + ch * cw + c * 32 + hh * 16 + ((uint32_t)row0 << 16), v);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               *reinterpret_cast<float4*>(Sw + lane * 32 + 4 * ((hh * 4 + k) ^ (lane & 7))) =
                   make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
           }
-          if (c == 1) {   // accumulator drained: hand the TMEM buffer back to the MMA warp
+          if (c == nch - 1) {   // accumulator drained: hand the TMEM buffer back to the MMA warp
             umma::tc_fence_before();
             __syncwarp();
             if (lane == 0) umma::mbar_arrive(&tempty_bar[buf]);
           }
           NSP_TRACE(if (ph.ttrace && ew == 0 && lane == 0) ph.ttrace[16 * idx + 8 + 3 * c] = gtimer());
           if (upd) {
-            if (c == 0) umma::cp_async_wait<1>();
+            if (c == 0 && nch == 2) umma::cp_async_wait<1>();
             else umma::cp_async_wait<0>();
           }
           __syncwarp();
@@ -1041,11 +1050,26 @@ static int build_flow_items(Plan& p, const uint8_t* flags, int nphases) {
       std::memcmp(p.nsf_flags.data(), flags, (size_t)nphases) == 0)
     return 0;
   const int nm = (int)p.ns_gram.size();
+  // 64-wide update tiles: half the epilogue (the latency-critical part of a phase; measured ~4 us per
+  // 128x128 tile), twice the CTAs per update phase; ORTH_NS_W128=1 keeps 128-wide tiles (A/B)
+  static const bool w128 = std::getenv("ORTH_NS_W128") != nullptr;
+  if (p.ns_upd64.empty()) {
+    p.ns_upd64 = p.ns_upd;
+    if (!w128)
+      for (auto& d : p.ns_upd64) {
+        d.epi = 2;
+        d.tiles_n = (d.N + 63) / 64;
+      }
+    if (cudaMalloc(&p.d_ns_upd64, std::max<size_t>(p.ns_upd64.size(), 1) * sizeof(NsDesc)) != cudaSuccess ||
+        cudaMemcpy(p.d_ns_upd64, p.ns_upd64.data(), p.ns_upd64.size() * sizeof(NsDesc), cudaMemcpyHostToDevice) !=
+            cudaSuccess)
+      return (int)cudaGetLastError();
+  }
   std::vector<int> GT(nm), UT(nm), order(nm);
   for (int i = 0; i < nm; ++i) {
     const int tn = p.ns_gram[i].tiles_n;
     GT[i] = tn * (tn + 1) / 2;
-    UT[i] = ((p.ns_upd[i].M + 127) / 128) * p.ns_upd[i].tiles_n;
+    UT[i] = ((p.ns_upd64[i].M + 127) / 128) * p.ns_upd64[i].tiles_n;
     order[i] = i;
   }
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return p.ns_gram[a].K > p.ns_gram[b].K; });
@@ -1054,7 +1078,7 @@ static int build_flow_items(Plan& p, const uint8_t* flags, int nphases) {
     const bool gram = flags[ph] & 1;
     const int t = ph / 2;   // iteration (the residual Gram is phase 2T: t = T)
     for (int i : order) {
-      const int tn = gram ? p.ns_gram[i].tiles_n : p.ns_upd[i].tiles_n;
+      const int tn = gram ? p.ns_gram[i].tiles_n : p.ns_upd64[i].tiles_n;
       const int ntile = gram ? tn * tn : UT[i];
       for (int l = 0; l < ntile; ++l) {
         if (gram && l / tn > l % tn) continue;   // upper-triangle Gram tiles only
@@ -1216,7 +1240,7 @@ int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flag
       cudaFuncSetAttribute(ns_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
       attr_set = true;
     }
-    const int ef = (int)cudaLaunchKernelEx(&cfg, ns_flow_kernel, (const NsDesc*)p.d_ns_gram, (const NsDesc*)p.d_ns_upd,
+    const int ef = (int)cudaLaunchKernelEx(&cfg, ns_flow_kernel, (const NsDesc*)p.d_ns_gram, (const NsDesc*)p.d_ns_upd64,
                                            (const NsItem*)p.nsf_items, p.nsf_n_items, p.nsp_bars, b,
                                            reinterpret_cast<const CUtensorMap*>(p.d_ns_maps), ph);
     if (tracing && ef == 0) flow_trace_report(p, flags, nphases, ttrace, (cudaStream_t)stream);

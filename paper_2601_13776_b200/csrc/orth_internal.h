@@ -178,6 +178,8 @@ struct Plan {
   int32_t ns_gram_tiles = 0, ns_upd_tiles = 0;
   NsDesc* d_ns_gram = nullptr;
   NsDesc* d_ns_upd = nullptr;
+  std::vector<NsDesc> ns_upd64;     // dataflow NS: the update descriptors with 64-wide tiles (epi = 2)
+  NsDesc* d_ns_upd64 = nullptr;
   int64_t bx_numel = 0, br_numel = 0;
   uint16_t* d_bx = nullptr;         // 4 x bx_numel: Xh[2], Xl[2] (row-major, rows padded to 8)
   uint16_t* d_br = nullptr;         // 2 x br_numel: Rh, Rl

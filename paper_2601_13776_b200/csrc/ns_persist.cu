@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const NsDesc* dp = reinterpret_cast<const NsDesc*>(desc_sh[ew]);
         const int tiles_n = dp->tiles_n;
-        const bool upd = (dp->epi) >= 1;
+        const bool upd = (dp->epi) == 1 || (dp->epi) == 2;   // 3: full (non-symmetric) Gram
         const int cw = (upd && dp->epi == 2) ? 32 : 64;   // columns per warp (64-wide update tiles: one chunk)
         const int nch = cw / 32;
         const int m0 = (tl.local / tiles_n) * 128 + row0, n0 = (tl.local % tiles_n) * (2 * cw) + ch * cw;
@@ -808,7 +808,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           NSP_TRACE(if (ph.ttrace && ew == 0 && lane == 0) ph.ttrace[16 * idx + 10 + 3 * c] = gtimer());
-          if (gram && m0 - row0 < n0 - ch * 64) {
+          if (gram && dp->epi != 3 && m0 - row0 < n0 - ch * 64) {
             // upper-triangle Gram tile: also write its mirror R[j][i] = R[i][j] (alpha * acc; no diagonal here)
 #pragma unroll 2
             for (int it = 0; it < 8; ++it) {
@@ -1055,20 +1055,39 @@ static int build_flow_items(Plan& p, const uint8_t* flags, int nphases) {
   static const bool w128 = std::getenv("ORTH_NS_W128") != nullptr;
   if (p.ns_upd64.empty()) {
     p.ns_upd64 = p.ns_upd;
+    // only for the large matrices (>= 32 update tiles of 128 x 128: the long chains); for the many small
+    // ones the extra items cost throughput (cfg3: 0.51 -> 0.64 ms with every matrix split)
+    static const int min_tiles = std::getenv("ORTH_NS_W64_MIN") ? std::atoi(std::getenv("ORTH_NS_W64_MIN")) : 32;
     if (!w128)
-      for (auto& d : p.ns_upd64) {
-        d.epi = 2;
-        d.tiles_n = (d.N + 63) / 64;
-      }
+      for (auto& d : p.ns_upd64)
+        if (((d.M + 127) / 128) * d.tiles_n >= min_tiles) {
+          d.epi = 2;
+          d.tiles_n = (d.N + 63) / 64;
+        }
     if (cudaMalloc(&p.d_ns_upd64, std::max<size_t>(p.ns_upd64.size(), 1) * sizeof(NsDesc)) != cudaSuccess ||
         cudaMemcpy(p.d_ns_upd64, p.ns_upd64.data(), p.ns_upd64.size() * sizeof(NsDesc), cudaMemcpyHostToDevice) !=
             cudaSuccess)
       return (int)cudaGetLastError();
   }
+  // Full (non-symmetric) Gram for the widest matrices: every tile computed, no mirror pass in the
+  // epilogue (the mirror made a Gram tile's epilogue ~4.8 us on the critical 24-phase chain); +tn(tn-1)/2
+  // tiles of MMA work for those few matrices only.  ORTH_NS_SYMGRAM=1 keeps the symmetric Gram (A/B).
+  static const bool symgram = std::getenv("ORTH_NS_SYMGRAM") != nullptr;
+  if (p.ns_gram_flow.empty()) {
+    p.ns_gram_flow = p.ns_gram;
+    static const int nmin = std::getenv("ORTH_NS_FULLGRAM_MIN") ? std::atoi(std::getenv("ORTH_NS_FULLGRAM_MIN")) : 512;
+    if (!symgram)
+      for (auto& d : p.ns_gram_flow)
+        if (d.N >= nmin) d.epi = 3;
+    if (cudaMalloc(&p.d_ns_gram_flow, std::max<size_t>(p.ns_gram_flow.size(), 1) * sizeof(NsDesc)) != cudaSuccess ||
+        cudaMemcpy(p.d_ns_gram_flow, p.ns_gram_flow.data(), p.ns_gram_flow.size() * sizeof(NsDesc),
+                   cudaMemcpyHostToDevice) != cudaSuccess)
+      return (int)cudaGetLastError();
+  }
   std::vector<int> GT(nm), UT(nm), order(nm);
   for (int i = 0; i < nm; ++i) {
     const int tn = p.ns_gram[i].tiles_n;
-    GT[i] = tn * (tn + 1) / 2;
+    GT[i] = p.ns_gram_flow[i].epi == 3 ? tn * tn : tn * (tn + 1) / 2;
     UT[i] = ((p.ns_upd64[i].M + 127) / 128) * p.ns_upd64[i].tiles_n;
     order[i] = i;
   }
@@ -1081,7 +1100,7 @@ static int build_flow_items(Plan& p, const uint8_t* flags, int nphases) {
       const int tn = gram ? p.ns_gram[i].tiles_n : p.ns_upd64[i].tiles_n;
       const int ntile = gram ? tn * tn : UT[i];
       for (int l = 0; l < ntile; ++l) {
-        if (gram && l / tn > l % tn) continue;   // upper-triangle Gram tiles only
+        if (gram && p.ns_gram_flow[i].epi != 3 && l / tn > l % tn) continue;   // upper-triangle Gram tiles only
         NsItem it{};
         it.p = ph; it.desc = i; it.local = l;
         if (gram) {   // Gram(t) reads X_t: all update tiles of iteration t - 1 done
@@ -1240,7 +1259,7 @@ int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flag
       cudaFuncSetAttribute(ns_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
       attr_set = true;
     }
-    const int ef = (int)cudaLaunchKernelEx(&cfg, ns_flow_kernel, (const NsDesc*)p.d_ns_gram, (const NsDesc*)p.d_ns_upd64,
+    const int ef = (int)cudaLaunchKernelEx(&cfg, ns_flow_kernel, (const NsDesc*)p.d_ns_gram_flow, (const NsDesc*)p.d_ns_upd64,
                                            (const NsItem*)p.nsf_items, p.nsf_n_items, p.nsp_bars, b,
                                            reinterpret_cast<const CUtensorMap*>(p.d_ns_maps), ph);
     if (tracing && ef == 0) flow_trace_report(p, flags, nphases, ttrace, (cudaStream_t)stream);

@@ -180,6 +180,8 @@ struct Plan {
   NsDesc* d_ns_upd = nullptr;
   std::vector<NsDesc> ns_upd64;     // dataflow NS: the update descriptors with 64-wide tiles (epi = 2)
   NsDesc* d_ns_upd64 = nullptr;
+  std::vector<NsDesc> ns_gram_flow; // dataflow NS: Gram descriptors (epi = 3: full, non-symmetric)
+  NsDesc* d_ns_gram_flow = nullptr;
   int64_t bx_numel = 0, br_numel = 0;
   uint16_t* d_bx = nullptr;         // 4 x bx_numel: Xh[2], Xl[2] (row-major, rows padded to 8)
   uint16_t* d_br = nullptr;         // 2 x br_numel: Rh, Rl

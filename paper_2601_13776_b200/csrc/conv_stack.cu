@@ -358,6 +358,19 @@ bool stack_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, StackAr
 
 }  // namespace
 
+// padded copy of x (N x Hp x P x C, rows of the whole batch back to back) into the plan scratch;
+// -1 if it does not fit the reservation
+int launch_pad_input(const LayerInfo& L, const void* x, int N, int H, int W, int Hp, int P, void* stream) {
+  const int64_t elems = (int64_t)N * Hp * P * L.ci_f;
+  if (!L.pad_scratch || elems * 2 > L.pad_bytes || L.ci_f % 8 != 0) return -1;
+  const int64_t vec = elems / 8;
+  const int blocks = (int)std::min<int64_t>((vec + 255) / 256, (int64_t)conv_sm_count() * 16);
+  pad_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4*)x, (uint4*)L.pad_scratch, N, H, W, L.ci_f / 8,
+                                                      Hp, P, L.pt, L.pl,
+                                                      L.desc.padding_mode == ORTH_PAD_CIRCULAR ? 1 : 0);
+  return (int)cudaGetLastError();
+}
+
 int launch_conv_fwd_stack(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
                           int H, int W, int Ho, int Wo, void* stream, int flip) {
   // Opt-in (ORTH_CONV_STACK=1): measured on B200 the M=128 x N=256 MMAs of this kernel run at ~220

@@ -834,6 +834,7 @@ int launch_conv_fwd_tc(const LayerInfo& L0, const void* kernel, void* scratch, c
   if (!no_reuse) {   // stride 1: TMA-window kernels (conv_stack.cu: >= 128 channels, conv_pad.cu: <= 64)
     int e = launch_conv_fwd_stack(L, kernel, bias, x, y, N, H, W, Ho, Wo, stream);
     if (e < 0) e = launch_conv_fwd_reuse(L, kernel, bias, x, y, N, H, W, Ho, Wo, stream);
+    if (e < 0) e = launch_conv_fwd_tma(L, kernel, bias, x, y, N, H, W, Ho, Wo, stream);
     if (e >= 0) return e;
   }
   TcConvArgs a;
@@ -875,6 +876,7 @@ int launch_conv_bwd_tc(const LayerInfo& L0, const void* kernel, void* wt_scratch
     F.pb = L.d * (L.k - 1) - L.pb; F.pr = L.d * (L.k - 1) - L.pr;
     int e = launch_conv_fwd_stack(F, wt_scratch, bias, y, x, N, Ho, Wo, H, W, stream, 1);
     if (e < 0) e = launch_conv_fwd_reuse(F, wt_scratch, bias, y, x, N, Ho, Wo, H, W, stream, 1);
+    if (e < 0) e = launch_conv_fwd_tma(F, wt_scratch, bias, y, x, N, Ho, Wo, H, W, stream, 1);
     if (e >= 0) return e;
   }
   TcConvArgs a;

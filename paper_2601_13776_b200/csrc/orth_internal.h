@@ -260,6 +260,12 @@ bool conv_act_tmap(::CUtensorMap_st* out, const void* x, int C, int W, int H, in
 // window stream, tcgen05 M = 128 channels x N = 256 window pixels (conv_stack.cu); -1 = not applicable
 int launch_conv_fwd_stack(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
                           int H, int W, int Ho, int Wo, void* stream, int flip = 0);
+// padded copy of a layer input into the plan's conv scratch (conv_stack.cu); -1 = does not fit
+int launch_pad_input(const LayerInfo& L, const void* x, int N, int H, int W, int Hp, int P, void* stream);
+// stride-1 forward conv as an implicit GEMM whose A tiles are single 4-D TMA boxes of the padded input
+// (conv_tma.cu): M = 128 output pixels (NI images x TH rows x Wo), N = BN channels; -1 = not applicable
+int launch_conv_fwd_tma(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
+                        int H, int W, int Ho, int Wo, void* stream, int flip = 0);
 // forward conv over TMA-loaded padded row windows (stride 1, rows <= 128 px); -1 = not applicable.
 // flip = 1 reads weight tap t from row k^2-1-t (a stride-1 adjoint in its forward-conv form).
 int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,

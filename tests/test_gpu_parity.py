@@ -247,6 +247,20 @@ STACK_CASES = [(128, 256, 3, 1, 2, 1, "circular", 12, "conv"), (256, 128, 5, 1, 
                (96, 128, 3, 1, 1, 1, "circular", 6, "conv"), (512, 512, 3, 1, 1, 1, "circular", 4, "conv")]
 
 
+def test_conv_tma_path():
+    """The opt-in TMA implicit-GEMM kernel (conv_tma.cu, ORTH_CONV_TMA=1: padded copy + one 4-D box per
+    tap) on stride-1 >= 128-channel cases, forward and adjoint, BF16, in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    code = (f"import sys; sys.path.insert(0, {os.getcwd()!r}); import tests.test_gpu_parity as t; "
+            f"import paper_2601_13776_b200 as orth\n"
+            f"for c in {STACK_CASES!r}: t.test_conv_forward_and_transpose(orth, c, 'bf16')")
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "ORTH_CONV_TMA": "1"},
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 def test_conv_stack_path():
     """The opt-in stacked-window kernel (conv_stack.cu, ORTH_CONV_STACK=1) on the same parity cases, in a
     subprocess (the switch is read once); forward and adjoint, BF16."""

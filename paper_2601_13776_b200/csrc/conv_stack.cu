@@ -377,8 +377,12 @@ int launch_conv_fwd_stack(const LayerInfo& L, const void* kernel, const float* b
   // cycles (shared-memory bound with the weight stream) and small images waste MMA work on padded
   // columns (4x4: 56%), so it beats conv_ws only for images >= ~28 px (cfg3 128@28: 103 vs 110 us) and
   // loses below (512@4: 49 vs 37 us); see DESIGN.md §9.
-  static const bool on = std::getenv("ORTH_CONV_STACK") != nullptr && std::getenv("ORTH_CONV_NO_STACK") == nullptr;
-  if (!on || !L.pad_scratch) return -1;
+  // Default only where it measured faster: 128 output channels per group on images >= 24 px
+  // (cfg3 128@28: 103 vs 110 us); ORTH_CONV_STACK=1 forces it wherever it applies, ORTH_CONV_NO_STACK=1 off.
+  static const bool force = std::getenv("ORTH_CONV_STACK") != nullptr;
+  static const bool off = std::getenv("ORTH_CONV_NO_STACK") != nullptr;
+  if (off || !L.pad_scratch) return -1;
+  if (!force && !(L.co == 128 && Wo >= 24 && Ho >= 24)) return -1;
   if (((uintptr_t)x & 15) != 0 || ((uintptr_t)y & 15) != 0) return -1;
   StackArgs a;
   if (!stack_args(L, N, H, W, Ho, Wo, a)) return -1;

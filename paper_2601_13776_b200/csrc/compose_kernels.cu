@@ -45,12 +45,24 @@ __global__ void __launch_bounds__(128) emit_kernel(const EmitItem* __restrict__ 
     }
     // tap-major: K[o, i, t] = src[t*tap_stride + o*ld + i]; stage [i][t] (stride k^2, odd -> conflict-free)
     __syncthreads();
-    for (int i = threadIdx.x; i < ci; i += 128) {
-      const float* col = src + (int64_t)o * e.ld + i;
-      for (int t = 0; t < kk; ++t) {
-        const float v = __ldg(col + (int64_t)t * e.tap_stride);
-        row_sm[i * kk + t] = v;
-        if (bq) bq[(int64_t)t * ci + i] = __float2bfloat16_rn(v);
+    if ((ci & 1) == 0) {   // channel pairs: one 4-byte BF16x2 store per (tap, pair)
+      for (int i = 2 * threadIdx.x; i < ci; i += 256) {
+        const float* col = src + (int64_t)o * e.ld + i;
+        for (int t = 0; t < kk; ++t) {
+          const float v0 = __ldg(col + (int64_t)t * e.tap_stride), v1 = __ldg(col + (int64_t)t * e.tap_stride + 1);
+          row_sm[i * kk + t] = v0;
+          row_sm[(i + 1) * kk + t] = v1;
+          if (bq) *reinterpret_cast<__nv_bfloat162*>(bq + (int64_t)t * ci + i) = __floats2bfloat162_rn(v0, v1);
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < ci; i += 128) {
+        const float* col = src + (int64_t)o * e.ld + i;
+        for (int t = 0; t < kk; ++t) {
+          const float v = __ldg(col + (int64_t)t * e.tap_stride);
+          row_sm[i * kk + t] = v;
+          if (bq) bq[(int64_t)t * ci + i] = __float2bfloat16_rn(v);
+        }
       }
     }
     __syncthreads();

@@ -248,7 +248,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (tid == 0) ws_trace[blockIdx.x * 8 + 0] += clock64() - tw0;
 #endif
           const uint32_t sa = s0 + st * STAGE;
+#ifdef ORTH_CONV_EXP_NOB   // timing experiment only (wrong results): no weight loads ("resident B")
+          if (tid == 0) umma::mbar_arrive(&full_bar[st]);
+          if (false) {
+#else
           if (tid == 0) {   // B tile (BN rows x 64 channels of this tap) by TMA, SWIZZLE_128B, OOB -> 0
+#endif
             umma::mbar_arrive_expect_tx(&full_bar[st], B_BYTES);
             if (cs == 1) {
               umma::tma_load_3d(sa + A_BYTES, &tmB, &full_bar[st], c0, tap, t.g * a.nout_g + t.n0);
@@ -259,11 +264,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
           }
           const bool cok = c0 + c * 8 < a.cr_g;
+#ifndef ORTH_CONV_EXP_NOA   // timing experiment ORTH_CONV_EXP_NOA: no A gathers (wrong results)
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const bool ok = cok && pix[i] >= 0;
             umma::cp_async16(sa + off_r[i], ok ? ig + (int64_t)pix[i] * a.in_C + c0 : in, ok);
           }
+#endif
           // arrive on the stage's barrier when THIS thread's copies have landed (no
           // producer stall: the next stage is issued as soon as its slot is free)
           umma::cp_async_mbar_arrive(&full_bar[st]);

@@ -189,9 +189,17 @@ orth_status_t orth_plan_reserve(orth_plan_t plan, int64_t bytes) {
       }
       P.pad_bytes = bytes;
     }
+    if (!P.d_conv_flags) {
+      if (cudaMalloc(&P.d_conv_flags, 65536 * sizeof(unsigned)) != cudaSuccess ||
+          cudaMemset(P.d_conv_flags, 0, 65536 * sizeof(unsigned)) != cudaSuccess) {
+        cudaGetLastError();
+        P.d_conv_flags = nullptr;
+      }
+    }
     for (auto& L : P.layers) {
       L.pad_scratch = P.d_pad_scratch;
       L.pad_bytes = P.pad_bytes;
+      L.conv_flags = P.d_pad_scratch ? P.d_conv_flags : nullptr;
     }
   }
   return ORTH_OK;

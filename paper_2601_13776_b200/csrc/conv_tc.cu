@@ -60,6 +60,13 @@ struct TcConvArgs {
   int cs;
   int phase_ctile0[MAX_PHASES + 1];  // first cluster tile of each phase
   int ctiles_m, num_ctiles;
+  // split-K (conv_ws only): items ct < base_ctiles are K half 0, the rest half 1 of tile ct - base_ctiles;
+  // half 0 leaves its FP32 accumulator in part[tile] ([BN/4][128] float4) and raises flags[tile], half 1
+  // waits, adds it, stores the output and clears the flag (fixed order: deterministic)
+  int ksplit, base_ctiles;
+  float* part;
+  unsigned* flags;
+  size_t part_bytes;
 };
 
 constexpr int NPROD = 256;                 // producer threads (warps 0-7)
@@ -185,7 +192,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t tab_s = umma::smem_u32(tab);
     int it = 0, st = 0, ph = 0;                // ring position of k-block `it`
     for (int ct = cid; ct < a.num_ctiles; ct += ncl) {
-      const TileInfo t = decode_tile(a, ct, crank, BN);
+      const int khalf = ct / a.base_ctiles;
+      const TileInfo t = decode_tile(a, ct - khalf * a.base_ctiles, crank, BN);
+      const int c_lo = khalf * (a.cr_g / a.ksplit), c_hi = c_lo + a.cr_g / a.ksplit;
       umma::named_bar_sync(1, NPROD);          // everyone is done reading the previous table / tap list
       int nt = 0;
       for (int tap = 0; tap < kk2; ++tap)
@@ -239,7 +248,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int pix[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) pix[i] = umma::ld_shared_s32(trow + 128u * i);
-        for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++it) {
+        for (int c0 = c_lo; c0 < c_hi; c0 += 64, ++it) {
 #ifdef ORTH_CONV_TRACE
           const long long tw0 = clock64();
 #endif
@@ -289,10 +298,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       long long w_full = 0, w_te = 0;
 #endif
       for (int ct = cid; ct < a.num_ctiles; ct += ncl, ++tcount) {
-        const TileInfo t = decode_tile(a, ct, crank, BN);
+        const TileInfo t = decode_tile(a, ct % a.base_ctiles, crank, BN);
         int nt = 0;
         for (int tap = 0; tap < kk2; ++tap) nt += tap_valid(a, t.phase, tap) ? 1 : 0;
-        const int nk = nt * kc;
+        const int nk = nt * (kc / a.ksplit);
         const int acc = tcount & 1;
 #ifdef ORTH_CONV_TRACE
         long long tq = clock64();
@@ -340,17 +349,52 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int r = q * 32 + lane;
     int tcount = 0;
     for (int ct = cid; ct < a.num_ctiles; ct += ncl, ++tcount) {
-      const TileInfo t = decode_tile(a, ct, crank, BN);
+      const int khalf = ct / a.base_ctiles, tb = ct - khalf * a.base_ctiles;
+      const TileInfo t = decode_tile(a, tb, crank, BN);
       const int m = t.m0 + r;
       const int opix = m < t.cnt ? out_pixel(a, t.phase, m) : -1;
       const int acc = tcount & 1;
       umma::mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
       umma::tc_fence_after();
       const int obase = t.g * a.nout_g + t.n0;
+      float4* part = a.ksplit > 1 ? reinterpret_cast<float4*>(a.part) + (int64_t)tb * (BN / 4) * 128 : nullptr;
+      if (a.ksplit > 1 && khalf == 0) {   // K half 0: FP32 partial out ([col4][row] float4, coalesced)
+#pragma unroll 1
+        for (int cc = 0; cc < BN; cc += 32) {
+          float v[32];
+          umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + cc), v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            __stcg(part + (int64_t)(cc / 4 + i) * 128 + r, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+        }
+        umma::tc_fence_before();
+        umma::mbar_arrive(&tempty_bar[acc]);
+        umma::named_bar_sync(2, 128);
+        if (r == 0)   // release, cumulative over the epilogue barrier
+          asm volatile("st.release.gpu.global.u32 [%0], 1;" ::"l"(a.flags + tb) : "memory");
+        continue;
+      }
+      if (a.ksplit > 1) {   // K half 1: wait for half 0 of this tile
+        if (r == 0) {
+          unsigned fv;
+          do {
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(fv) : "l"(a.flags + tb) : "memory");
+          } while (fv == 0u);
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+        umma::named_bar_sync(2, 128);
+      }
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += 32) {
         float v[32];
         umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + cc), v);
+        if (part) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 pv = __ldcg(part + (int64_t)(cc / 4 + i) * 128 + r);
+            v[4 * i] += pv.x; v[4 * i + 1] += pv.y; v[4 * i + 2] += pv.z; v[4 * i + 3] += pv.w;
+          }
+        }
         if (opix >= 0) {
           const int o = obase + cc;
           uint32_t pk[16];
@@ -368,6 +412,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       umma::tc_fence_before();
       umma::mbar_arrive(&tempty_bar[acc]);
+      if (part) {   // the partial is consumed: re-arm the flag for the next launch
+        umma::named_bar_sync(2, 128);
+        if (r == 0) a.flags[tb] = 0u;
+      }
     }
   }
   umma::tc_fence_before();
@@ -707,10 +755,21 @@ int launch_pair(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, con
 int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
                TcConvArgs& a, int groups, cudaStream_t s) {
   const int n = a.nout_g;
-  // widest N tile that still gives ~every SM a tile (a 128x256 MMA costs 128 cycles, 128x128 and
-  // 128x64 both ~73: narrower only pays when it fills otherwise idle SMs)
+  // widest N tile that still gives ~every SM a tile (every K=16 MMA shape costs ~125-150 cycles, so a
+  // 128x256 tile does twice the work of a 128x128 one per MMA: narrower only pays when it fills
+  // otherwise idle SMs -- or, with a partial workspace, split K in two instead, ORTH_CONV_NO_SPLITK=1 off)
   int bn = n % 256 == 0 ? 256 : n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32;
-  while (bn > 128 && (int64_t)a.tiles_m * (n / bn) * groups < (num_sms() * 4) / 5 && n % (bn / 2) == 0) bn /= 2;
+  static const bool no_split = std::getenv("ORTH_CONV_NO_SPLITK") != nullptr;
+  a.ksplit = 1;
+  const int64_t tiles256 = (int64_t)a.tiles_m * (n / 256) * groups;
+  const int kblocks = ((a.cr_g + 63) / 64) * a.k * a.k / a.nphase;   // per tile (taps spread over the phases)
+  if (!no_split && a.part && a.flags && bn == 256 && tiles256 < (num_sms() * 4) / 5 && a.cr_g % 128 == 0 &&
+      kblocks >= 64 &&   // measured: 72 K blocks 37.6 -> 33.6 us, 36 K blocks 23.6 -> 27.1 us
+      2 * tiles256 <= num_sms() && (size_t)tiles256 * 128 * 256 * 4 <= a.part_bytes && tiles256 <= 65536)
+    a.ksplit = 2;   // two half-K items per 128x256 tile: twice the MMA work per instruction, same item count
+  while (a.ksplit == 1 && bn > 128 && (int64_t)a.tiles_m * (n / bn) * groups < (num_sms() * 4) / 5 &&
+         n % (bn / 2) == 0)
+    bn /= 2;
   a.tiles_n = n / bn;
   a.num_tiles = a.tiles_m * a.tiles_n * groups;
   if (a.num_tiles == 0) return 0;
@@ -740,6 +799,11 @@ int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, cons
   a.phase_ctile0[a.nphase] = c0;
   a.ctiles_m = c0;
   a.num_ctiles = a.ctiles_m * a.tiles_n * groups;
+  a.base_ctiles = a.num_ctiles;
+  if (a.ksplit > 1) {
+    if (pair || cs > 1) a.ksplit = 1;
+    else a.num_ctiles *= a.ksplit;
+  }
   if (pair) {   // stage = 16 KB A + BN/2 x 128 B of B
     if (bn == 256) return a.k <= 3 ? launch_pair<256, 6>(in, w, w_rows, bias, out, a, s)
                                    : launch_pair<256, 5>(in, w, w_rows, bias, out, a, s);
@@ -846,6 +910,7 @@ int launch_conv_fwd_tc(const LayerInfo& L0, const void* kernel, void* scratch, c
   }
   TcConvArgs a;
   base_args(a, L, N, H, W, Ho, Wo);
+  a.part = static_cast<float*>(L0.pad_scratch); a.part_bytes = (size_t)L0.pad_bytes; a.flags = L0.conv_flags;
   a.transposed = 0;
   a.in_C = L.ci_f; a.out_C = L.co_f; a.cr_g = L.ci; a.nout_g = L.co;
   a.nphase = 1;
@@ -888,6 +953,7 @@ int launch_conv_bwd_tc(const LayerInfo& L0, const void* kernel, void* wt_scratch
   }
   TcConvArgs a;
   base_args(a, L, N, H, W, Ho, Wo);
+  a.part = static_cast<float*>(L0.pad_scratch); a.part_bytes = (size_t)L0.pad_bytes; a.flags = L0.conv_flags;
   a.transposed = 1;
   a.in_C = L.co_f; a.out_C = L.ci_f; a.cr_g = L.co; a.nout_g = L.ci;
   a.nphase = L.s * L.s;

@@ -43,8 +43,9 @@ struct LayerInfo {
   int32_t first_mat, mats_per_group;
   int32_t owner;
   int64_t kf32_off, kbf16_off, kernel_numel;
-  void* pad_scratch = nullptr;  // plan-owned conv scratch (orth_plan_reserve): padded input copy
-  int64_t pad_bytes = 0;
+  void* pad_scratch = nullptr;  // plan-owned conv scratch (orth_plan_reserve): padded input copy,
+  int64_t pad_bytes = 0;        // or split-K partial tiles of the gather conv
+  unsigned* conv_flags = nullptr;   // split-K tile flags (zeroed; each launch leaves them zero)
   double ns_flops, comp_flops;
 };
 
@@ -233,6 +234,7 @@ struct Plan {
   int64_t launches = 0;
   void* d_pad_scratch = nullptr;    // orth_plan_reserve
   int64_t pad_bytes = 0;
+  unsigned* d_conv_flags = nullptr; // 65536 split-K tile flags
   uint16_t* d_wt_scratch = nullptr; // BF16 weight scratch of one layer call: [W^T | packed W], 16 x max kernel
 };
 

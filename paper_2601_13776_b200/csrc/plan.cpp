@@ -665,6 +665,7 @@ orth_status_t orth_plan_destroy(orth_plan_t plan) {
   if (plan->p.nsf_items) cudaFree(plan->p.nsf_items);
   if (plan->p.d_arena) cudaFree(plan->p.d_arena);
   if (plan->p.d_pad_scratch) cudaFree(plan->p.d_pad_scratch);
+  if (plan->p.d_conv_flags) cudaFree(plan->p.d_conv_flags);
   if (plan->p.d_ns_upd64) cudaFree(plan->p.d_ns_upd64);
   if (plan->p.d_ns_gram_flow) cudaFree(plan->p.d_ns_gram_flow);
   delete plan;

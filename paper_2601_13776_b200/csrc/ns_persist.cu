@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     phase_done = 0;
     umma::fence_mbar_init();
   }
-  if (warp == 1) umma::tmem_alloc(&tmem_base_sh, 256);
+  if (warp == 1) umma::tmem_alloc(&tmem_base_sh, 512);   // two 256-column accumulators (wide update tiles)
   umma::tc_fence_before();
   __syncthreads();
   umma::tc_fence_after();
@@ -199,15 +199,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = tb; t < te; ++t) {
           const NsTile tl = tiles[t];
           const NsDesc d = D[tl.desc];
-          const int m0 = (tl.local / d.tiles_n) * 128, n0 = (tl.local % d.tiles_n) * 128;
+          // wide update tile (epi 4, 1-pass only): 128 x 256, B = 256 rows in two adjacent slots
+          const bool wide = !gram && d.epi == 4 && !split;
+          const int ws = wide ? 2 : w;
+          const int m0 = (tl.local / d.tiles_n) * 128, n0 = (tl.local % d.tiles_n) * (wide ? 256 : 128);
           const int nk = (d.K + 63) / 64, a_mn = d.a_kind == 1, b_mn = d.b_kind == 1;
           const bool sym = gram && m0 == n0;   // diagonal Gram tile: B == A, loaded once
           const CUtensorMap* ma = maps + d.map_a + 2 * par;
           const CUtensorMap* mb = maps + d.map_b + 2 * par;
           for (int kb = 0; kb < nk; ++kb) {
-            if (w == 2 && cnt % kSlots == kSlots - 1) ++cnt;   // a hi/lo stage takes two adjacent slots
+            if (ws == 2 && cnt % kSlots == kSlots - 1) ++cnt;   // a hi/lo or wide stage takes two adjacent slots
             const int s = cnt % kSlots;
-            for (int q = s; q < s + w; ++q) {
+            for (int q = s; q < s + ws; ++q) {
               if ((used >> q) & 1u) {
                 umma::mbar_wait(&empty_bar[q], (epar >> q) & 1u);
                 epar ^= 1u << q;
@@ -215,6 +218,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               used |= 1u << q;
             }
             const uint32_t sa = ring + s * kSlot;
+            if (wide) {   // A 16 KB + B 256 rows (32 KB)
+              umma::mbar_arrive_expect_tx(&full_bar[s], 16384u + 32768u);
+              load_operand(sa, ma, &full_bar[s], kb * 64, m0, a_mn);
+              load_operand(sa + 16384, mb, &full_bar[s], kb * 64, n0, b_mn);
+              load_operand(sa + 32768, mb, &full_bar[s], kb * 64, n0 + 128, b_mn);
+              cnt += 2;
+              continue;
+            }
             umma::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(sym ? w * kSlot / 2 : w * kSlot));
             load_operand(sa, ma, &full_bar[s], kb * 64, m0, a_mn);
             if (!sym) load_operand(sa + 16384, mb, &full_bar[s], kb * 64, n0, b_mn);
@@ -243,13 +254,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nk = (__ldg(&dp->K) + 63) / 64, a_mn = __ldg(&dp->a_kind) == 1, b_mn = __ldg(&dp->b_kind) == 1;
           const int tn = __ldg(&dp->tiles_n);
           const bool sym = gram && (tl.local / tn) == (tl.local % tn);
-          const uint32_t idesc = umma::idesc_bf16(128, 128) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
+          const bool wide = !gram && __ldg(&dp->epi) == 4 && !split;
+          const int ws = wide ? 2 : w;
+          const uint32_t idesc = (wide ? umma::idesc_bf16(128, 256) : umma::idesc_bf16(128, 128)) |
+                                 ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
           const int buf = acc & 1;
           if (acc >= 2) umma::mbar_wait(&tempty_bar[buf], ((acc >> 1) - 1) & 1);
           umma::tc_fence_after();
-          const uint32_t dt = tmem + buf * 128;
+          const uint32_t dt = tmem + buf * 256;
           for (int kb = 0; kb < nk; ++kb) {
-            if (w == 2 && cnt % kSlots == kSlots - 1) ++cnt;
+            if (ws == 2 && cnt % kSlots == kSlots - 1) ++cnt;
             const int s = cnt % kSlots;
             umma::mbar_wait(&full_bar[s], (fpar >> s) & 1u);
             fpar ^= 1u << s;
@@ -266,8 +280,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             umma::mma_commit(&empty_bar[s]);
-            if (w == 2) umma::mma_commit(&empty_bar[s + 1]);
-            cnt += w;
+            if (ws == 2) umma::mma_commit(&empty_bar[s + 1]);
+            cnt += ws;
           }
           umma::mma_commit(&tfull_bar[buf]);
           ++acc;
@@ -304,11 +318,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const NsDesc* dp = reinterpret_cast<const NsDesc*>(desc_sh[ew]);
         const int tiles_n = dp->tiles_n;
-        const int m0 = (tl.local / tiles_n) * 128 + row0, n0 = (tl.local % tiles_n) * 128 + ch * 64;
-        const bool upd = (dp->epi) == 1;
+        const bool upd = (dp->epi) == 1 || (dp->epi) == 4;
+        const int nh = ((dp->epi) == 4 && !((f >> 1) & 1)) ? 2 : 1;   // wide update tile: two 128-column halves
+        const int m0 = (tl.local / tiles_n) * 128 + row0;
         const int64_t f_off = (dp->f_off), ldf = (dp->ldf);
         const int M = (dp->M), N = (dp->N);
         const int buf = acc & 1;
+        NSP_TRACE(unsigned long long t_start = 0ull; unsigned long long t_full = 0ull;)
+#ifdef ORTH_NSP_TRACE
+        long long cyc[6];
+#endif
+#pragma unroll 1
+        for (int h = 0; h < nh; ++h) {
+        const int n0 = (tl.local % tiles_n) * (128 * nh) + h * 128 + ch * 64;
         if (upd) {   // C = X (fp32) rows m0.., cols n0..n0+63 -> Sc[0..1]
           const float* Cm = pick(bufs.X, par) + f_off;
           const bool fv4 = (ldf & 3) == 0;
@@ -330,13 +352,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma::cp_async_commit();
           }
         }
-        NSP_TRACE(const unsigned long long t_start = ph.ttrace ? gtimer() : 0ull);
-        umma::mbar_wait(&tfull_bar[buf], (acc >> 1) & 1);
-        umma::tc_fence_after();
-        NSP_TRACE(const unsigned long long t_full = ph.ttrace ? gtimer() : 0ull);
+        NSP_TRACE(if (h == 0) t_start = ph.ttrace ? gtimer() : 0ull);
+        if (h == 0) {
+          umma::mbar_wait(&tfull_bar[buf], (acc >> 1) & 1);
+          umma::tc_fence_after();
+        }
+        NSP_TRACE(if (h == 0) t_full = ph.ttrace ? gtimer() : 0ull);
 #ifdef ORTH_NSP_TRACE
-        long long cyc[6];
-        cyc[0] = clock64();
+        if (h == 0) cyc[0] = clock64();
 #endif
         NSP_TRACE(if (ph.trace && ew == 0 && lane == 0 && t == tb) ph.trace[(size_t)blockIdx.x * (4 * ph.n + 1) + 1 + 4 * p + 1] = gtimer());
 #pragma unroll 1
@@ -344,13 +367,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             float v[16];
-            umma::tmem_ld16(tmem + buf * 128 + ch * 64 + c * 32 + hh * 16 + ((uint32_t)row0 << 16), v);
+            umma::tmem_ld16(tmem + buf * 256 + h * 128 + ch * 64 + c * 32 + hh * 16 + ((uint32_t)row0 << 16), v);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               *reinterpret_cast<float4*>(Sw + lane * 32 + 4 * ((hh * 4 + k) ^ (lane & 7))) =
                   make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
           }
-          if (c == 1) {   // accumulator drained: hand the TMEM buffer back to the MMA warp
+          if (c == 1 && h == nh - 1) {   // accumulator drained: hand the TMEM buffer back to the MMA warp
             umma::tc_fence_before();
             __syncwarp();
             if (lane == 0) umma::mbar_arrive(&tempty_bar[buf]);
@@ -453,6 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           NSP_TRACE(if (c == 0) cyc[3] = clock64());
         }
+        }   // halves
 #ifdef ORTH_NSP_TRACE
         cyc[4] = clock64();
         if (ph.ttrace && lane == 0) {
@@ -487,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   umma::tc_fence_before();
   __syncthreads();
-  if (warp == 1) umma::tmem_dealloc(tmem, 256);
+  if (warp == 1) umma::tmem_dealloc(tmem, 512);
 }
 
 // Dataflow NS (default): the same per-tile pipeline as ns_persist_kernel, but
@@ -972,6 +996,26 @@ orth_status_t build_ns_persist(Plan& p) {
     return mc[m].nkg * 0.3 * (diag ? 0.5 : 1.0) + (diag ? 0.8 : 1.6);
   };
   auto upd_cost = [&](int m) { return mc[m].nku * 0.3 + 2.0; };
+  // wide update tiles (128 x 256, epi = 4) for this phase-synchronous kernel: a K=16 tcgen05.mma costs
+  // the same ~128 cycles for N = 128 and N = 256, and the big sweeps are operand-bandwidth bound, so a
+  // 256-wide tile does twice the work per instruction and per A byte.  BF16 mode only (its updates are
+  // 1-pass); ORTH_NS_NARROW=1 keeps 128-wide tiles (A/B).
+  static const bool narrow = std::getenv("ORTH_NS_NARROW") != nullptr;
+  p.ns_upd_wide = p.ns_upd;
+  if (!narrow && p.opts.compute == ORTH_BF16)
+    for (auto& d : p.ns_upd_wide)
+      if (d.N >= 256) {
+        d.epi = 4;
+        d.tiles_n = (d.N + 255) / 256;
+      }
+  if (p.d_ns_upd_wide) cudaFree(p.d_ns_upd_wide);
+  p.d_ns_upd_wide = nullptr;
+  if (cudaMalloc(&p.d_ns_upd_wide, std::max<size_t>(p.ns_upd_wide.size(), 1) * sizeof(NsDesc)) != cudaSuccess ||
+      cudaMemcpy(p.d_ns_upd_wide, p.ns_upd_wide.data(), p.ns_upd_wide.size() * sizeof(NsDesc),
+                 cudaMemcpyHostToDevice) != cudaSuccess) {
+    set_error("NS wide descriptors: %s", cudaGetErrorString(cudaGetLastError()));
+    return ORTH_ERR_OUT_OF_MEMORY;
+  }
   std::vector<NsTile> tg, tu;
   std::vector<NsGroup> ctas_v;
   int cta = 0;
@@ -983,7 +1027,12 @@ orth_status_t build_ns_persist(Plan& p) {
       const int tn = p.ns_gram[mc[m].idx].tiles_n;
       for (int l = 0; l < tn * tn; ++l)
         if (l / tn <= l % tn) gi_items.push_back({gram_cost(m, l), {mc[m].idx, l}});
-      for (int l = 0; l < mc[m].ut; ++l) ui_items.push_back({upd_cost(m), {mc[m].idx, l}});
+      {
+        const NsDesc& uw = p.ns_upd_wide[mc[m].idx];
+        const bool wide = uw.epi == 4;
+        const int utw = ((uw.M + 127) / 128) * uw.tiles_n;
+        for (int l = 0; l < utw; ++l) ui_items.push_back({upd_cost(m) * (wide ? 1.7 : 1.0), {mc[m].idx, l}});
+      }
     }
     auto lpt = [&](std::vector<Item>& items) {
       std::stable_sort(items.begin(), items.end(), [](const Item& a, const Item& b) { return a.c > b.c; });
@@ -1266,7 +1315,7 @@ int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flag
     return ef;
   }
   const cudaError_t e = cudaLaunchKernelEx(&cfg, ns_persist_kernel, (const NsDesc*)p.d_ns_gram,
-                                           (const NsDesc*)p.d_ns_upd, (const NsTile*)p.nsp_tiles,
+                                           (const NsDesc*)p.d_ns_upd_wide, (const NsTile*)p.nsp_tiles,
                                            (const NsGroup*)p.nsp_groups, p.nsp_bars,
                                            b, reinterpret_cast<const CUtensorMap*>(p.d_ns_maps), ph);
   if (tracing && e == cudaSuccess) {   // diagnostics only: serialises the stream

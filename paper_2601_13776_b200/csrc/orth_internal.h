@@ -181,6 +181,8 @@ struct Plan {
   NsDesc* d_ns_upd = nullptr;
   std::vector<NsDesc> ns_upd64;     // dataflow NS: the update descriptors with 64-wide tiles (epi = 2)
   NsDesc* d_ns_upd64 = nullptr;
+  std::vector<NsDesc> ns_upd_wide;  // phase-synchronous NS: update descriptors (epi = 4: 128 x 256 tiles)
+  NsDesc* d_ns_upd_wide = nullptr;
   std::vector<NsDesc> ns_gram_flow; // dataflow NS: Gram descriptors (epi = 3: full, non-symmetric)
   NsDesc* d_ns_gram_flow = nullptr;
   int64_t bx_numel = 0, br_numel = 0;

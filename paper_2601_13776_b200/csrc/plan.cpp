@@ -668,6 +668,7 @@ orth_status_t orth_plan_destroy(orth_plan_t plan) {
   if (plan->p.d_conv_flags) cudaFree(plan->p.d_conv_flags);
   if (plan->p.d_ns_upd64) cudaFree(plan->p.d_ns_upd64);
   if (plan->p.d_ns_gram_flow) cudaFree(plan->p.d_ns_gram_flow);
+  if (plan->p.d_ns_upd_wide) cudaFree(plan->p.d_ns_upd_wide);
   delete plan;
   return ORTH_OK;
 }

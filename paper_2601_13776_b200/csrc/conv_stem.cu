@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "orth_internal.h"
@@ -175,7 +176,11 @@ int launch_stem(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bia
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = std::min(a.tiles, sms * 4);
+  // CTAs per SM: each tile is a serial gather -> MMA -> store chain, so residency hides the latency
+  // (TMEM: CO <= 128 columns per CTA, up to 4 per SM at CO = 128; smem 16 + CO/8 KB)
+  static const int per_sm = std::getenv("ORTH_STEM_CTAS_PER_SM") ? std::atoi(std::getenv("ORTH_STEM_CTAS_PER_SM"))
+                                                                  : (CO <= 64 ? 6 : 4);
+  const int grid = std::min(a.tiles, sms * per_sm);
   // output viewed as (Co channels, N*Ho*Wo pixels), box 64 x 128, SWIZZLE_128B
   CUtensorMap tm;
   std::memset(&tm, 0, sizeof(tm));

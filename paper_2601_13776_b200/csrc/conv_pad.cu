@@ -159,32 +159,35 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int bset_bytes = ((a.cr_g + 63) / 64) * kk2 * B_BYTES;
 
   if (warp == A_WARP) {
-    if (lane == 0) {
-      // ---------------------------------------------------------- A producer
-      umma::tma_prefetch_desc(&tmA.m[0]);
-      int u = 0, tc_a = 0;
-      for (int tile = t_begin; tile < t_end; tile += t_step, ++tc_a) {
-        int n, h0, g, n0;
-        decode(tile, n, h0, g, n0);
-        for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
-          const int ab = u % NA;
-          if (u >= NA) umma::mbar_wait(&a_empty[ab], ((u / NA) - 1) & 1);
-          if (c0 == 0) CTRACE(tc_a, 0);
-          const uint32_t dst = abase + ab * a.abuf_bytes;
-          const int c = g * a.cr_g + c0;
-          umma::mbar_arrive_expect_tx(&a_full[ab], (uint32_t)a.a_tx);
-          for (int b = 0; b < a.ncopy; ++b) {
-            const uint32_t cb = dst + (uint32_t)(b * a.copy_bytes);
-            if (!a.circ) {   // one box: R rows x P pixels x 64 channels; out of bounds -> 0
+    // ---------------------------------------------------------- A producer (whole warp)
+    // Circular windows are assembled from up to three TMA row pieces per input row; one thread
+    // issuing them serially costs ~150 ns per piece (measured), so the rows are spread over the
+    // 32 lanes (lane 0 posts the byte count first, then every lane issues its rows' pieces).
+    if (lane == 0) umma::tma_prefetch_desc(&tmA.m[0]);
+    int u = 0, tc_a = 0;
+    for (int tile = t_begin; tile < t_end; tile += t_step, ++tc_a) {
+      int n, h0, g, n0;
+      decode(tile, n, h0, g, n0);
+      for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
+        const int ab = u % NA;
+        if (u >= NA) umma::mbar_wait(&a_empty[ab], ((u / NA) - 1) & 1);
+        if (c0 == 0 && lane == 0) CTRACE(tc_a, 0);
+        const uint32_t dst = abase + ab * a.abuf_bytes;
+        const int c = g * a.cr_g + c0;
+        if (lane == 0) umma::mbar_arrive_expect_tx(&a_full[ab], (uint32_t)a.a_tx);
+        __syncwarp();
+        for (int b = 0; b < a.ncopy; ++b) {
+          const uint32_t cb = dst + (uint32_t)(b * a.copy_bytes);
+          if (!a.circ) {   // one box: R rows x P pixels x 64 channels; out of bounds -> 0
+            if (lane == 0)
               umma::tma_load_4d(cb, &tmA.m[0], &a_full[ab], c, (a.ncopy > 1 ? a.d * b : 0) - a.pl, h0 - a.pt, n);
-            } else {
-              for (int y = 0; y < a.R; ++y) {
-                const int h = wrapi(h0 - a.pt + y, a.H);
-                const uint32_t row = cb + (uint32_t)(y * a.P) * 128u;
-                for (int pc = 0; pc < a.npc[b]; ++pc)
-                  umma::tma_load_4d(row + (uint32_t)a.pc_dst[3 * b + pc] * 128u, &tmA.m[a.pc_map[3 * b + pc]],
-                                    &a_full[ab], c, a.pc_col[3 * b + pc], h, n);
-              }
+          } else {
+            for (int y = lane; y < a.R; y += 32) {
+              const int h = wrapi(h0 - a.pt + y, a.H);
+              const uint32_t row = cb + (uint32_t)(y * a.P) * 128u;
+              for (int pc = 0; pc < a.npc[b]; ++pc)
+                umma::tma_load_4d(row + (uint32_t)a.pc_dst[3 * b + pc] * 128u, &tmA.m[a.pc_map[3 * b + pc]],
+                                  &a_full[ab], c, a.pc_col[3 * b + pc], h, n);
             }
           }
         }

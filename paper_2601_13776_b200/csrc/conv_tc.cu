@@ -67,6 +67,9 @@ struct TcConvArgs {
   float* part;
   unsigned* flags;
   size_t part_bytes;
+  // forward only: epilogue through a SWIZZLE_128B staging tile and one TMA tensor store per 64 output
+  // channels (the tile's 128 rows are consecutive NHWC pixels); else thread-per-row 16-byte stores
+  int tma_out, stage_off;
 };
 
 constexpr int NPROD = 256;                 // producer threads (warps 0-7)
@@ -149,7 +152,8 @@ __device__ __forceinline__ int in_pixel(const TcConvArgs& a, int phase, int m, i
 template <int BN, int S>
 __global__ void __launch_bounds__(NTHREADS, 1)
     conv_ws(const __nv_bfloat16* __restrict__ in, const float* __restrict__ bias, __nv_bfloat16* __restrict__ out,
-            const __grid_constant__ TcConvArgs a, const __grid_constant__ CUtensorMap tmB) {
+            const __grid_constant__ TcConvArgs a, const __grid_constant__ CUtensorMap tmB,
+            const __grid_constant__ CUtensorMap tmY) {
   extern __shared__ uint8_t smem_raw[];
   umma::griddep_launch_dependents();
   uint8_t* smem = umma::align1024_smem(smem_raw);
@@ -384,6 +388,53 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         umma::named_bar_sync(2, 128);
       }
+      if (a.tma_out) {   // staged, coalesced: per 64 channels one SWIZZLE_128B tile + one TMA store
+        uint8_t* Sy = smem + a.stage_off;
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 64) {
+          if (r == 0) umma::bulk_wait_read0();   // the previous store has read the staging tile
+          umma::named_bar_sync(2, 128);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int cc = cb + 32 * hh;
+            float v[32];
+            umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + cc), v);
+            if (part) {
+#pragma unroll
+              for (int i2 = 0; i2 < 8; ++i2) {
+                const float4 pv = __ldcg(part + (int64_t)(cc / 4 + i2) * 128 + r);
+                v[4 * i2] += pv.x; v[4 * i2 + 1] += pv.y; v[4 * i2 + 2] += pv.z; v[4 * i2 + 3] += pv.w;
+              }
+            }
+            const int o = obase + cc;
+#pragma unroll
+            for (int i4 = 0; i4 < 4; ++i4) {
+              uint32_t pk[4];
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                float v0 = v[8 * i4 + 2 * jj], v1 = v[8 * i4 + 2 * jj + 1];
+                if (bias) { v0 += bias[o + 8 * i4 + 2 * jj]; v1 += bias[o + 8 * i4 + 2 * jj + 1]; }
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
+                pk[jj] = *reinterpret_cast<uint32_t*>(&b2);
+              }
+              *reinterpret_cast<uint4*>(Sy + umma::sw128_off(r, hh * 4 + i4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+          }
+          umma::fence_proxy_async_smem();   // staging writes -> TMA (async proxy) reads
+          umma::named_bar_sync(2, 128);
+          if (r == 0) {   // rows past the last pixel are clipped by TMA
+            umma::tma_store_2d(&tmY, umma::smem_u32(Sy), obase + cb, t.m0);
+            umma::bulk_commit();
+          }
+        }
+        umma::tc_fence_before();
+        umma::mbar_arrive(&tempty_bar[acc]);
+        if (part) {
+          umma::named_bar_sync(2, 128);
+          if (r == 0) a.flags[tb] = 0u;
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += 32) {
         float v[32];
@@ -418,6 +469,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   }
+  if (a.tma_out && warp > MMA_WARP && ((warp & 3) * 32 + lane) == 0) umma::bulk_wait0();   // stores complete
   umma::tc_fence_before();
   __syncthreads();
   if (cs > 1) umma::cluster_sync_all();   // no peer may still multicast into this CTA
@@ -678,9 +730,31 @@ int num_sms() {
 
 template <int BN, int S>
 int launch_ws(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
-              const TcConvArgs& a, cudaStream_t stream) {
+              const TcConvArgs& a0, cudaStream_t stream) {
+  TcConvArgs a = a0;
   // the pixel table only needs this layer's taps (k^2 <= MAX_TAPS)
-  const size_t smem = 1024 + (size_t)S * (128 * 128 + BN * 128) + (size_t)a.k * a.k * 128 * 4;
+  size_t smem = 1024 + (size_t)S * (128 * 128 + BN * 128) + (size_t)a.k * a.k * 128 * 4;
+  // TMA-store epilogue for forward tiles (output = consecutive pixels), ORTH_CONV_NO_TMA_OUT=1 off
+  static const bool no_tma_out = std::getenv("ORTH_CONV_NO_TMA_OUT") != nullptr;
+  CUtensorMap ty;
+  std::memset(&ty, 0, sizeof(ty));
+  a.tma_out = 0;
+  if (!no_tma_out && !a.transposed && BN >= 128 && a.cs == 1 && ((uintptr_t)out & 15) == 0 && a.out_C % 8 == 0 &&
+      smem + 17 * 1024 <= 227 * 1024) {
+    const size_t off = (((size_t)S * (128 * 128 + BN * 128) + (size_t)a.k * a.k * 128 * 4) + 1023) & ~size_t(1023);
+    auto enc = tensor_map_encoder();
+    const cuuint64_t dims[2] = {(cuuint64_t)a.out_C, (cuuint64_t)a.N * a.Ho * a.Wo};
+    const cuuint64_t strides[1] = {(cuuint64_t)a.out_C * 2};
+    const cuuint32_t box[2] = {64, 128};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc && enc(&ty, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+      a.tma_out = 1;
+      a.stage_off = (int)off;
+      smem = 1024 + off + 16 * 1024;
+    }
+  }
   static size_t attr = 0;
   if (smem > attr) {
     cudaFuncSetAttribute(conv_ws<BN, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -704,7 +778,7 @@ int launch_ws(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const
   at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  const int e = (int)cudaLaunchKernelEx(&cfg, conv_ws<BN, S>, in, bias, out, a, tm);
+  const int e = (int)cudaLaunchKernelEx(&cfg, conv_ws<BN, S>, in, bias, out, a, tm, ty);
 #ifdef ORTH_CONV_TRACE
   {
     cudaStreamSynchronize(stream);

@@ -45,7 +45,22 @@ __global__ void __launch_bounds__(128) emit_kernel(const EmitItem* __restrict__ 
     }
     // tap-major: K[o, i, t] = src[t*tap_stride + o*ld + i]; stage [i][t] (stride k^2, odd -> conflict-free)
     __syncthreads();
-    if ((ci & 1) == 0) {   // channel pairs: one 4-byte BF16x2 store per (tap, pair)
+    if ((ci & 1) == 0 && kk <= 16) {   // channel pairs, all taps' loads in flight before use
+      for (int i = 2 * threadIdx.x; i < ci; i += 256) {
+        const float* col = src + (int64_t)o * e.ld + i;
+        float2 v[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          if (t < kk) v[t] = make_float2(__ldg(col + (int64_t)t * e.tap_stride), __ldg(col + (int64_t)t * e.tap_stride + 1));
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          if (t < kk) {
+            row_sm[i * kk + t] = v[t].x;
+            row_sm[(i + 1) * kk + t] = v[t].y;
+            if (bq) *reinterpret_cast<__nv_bfloat162*>(bq + (int64_t)t * ci + i) = __floats2bfloat162_rn(v[t].x, v[t].y);
+          }
+      }
+    } else if ((ci & 1) == 0) {   // channel pairs: one 4-byte BF16x2 store per (tap, pair)
       for (int i = 2 * threadIdx.x; i < ci; i += 256) {
         const float* col = src + (int64_t)o * e.ld + i;
         for (int t = 0; t < kk; ++t) {

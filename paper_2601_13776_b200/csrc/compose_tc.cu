@@ -576,6 +576,9 @@ __global__ void __launch_bounds__(256) cvt_kernel(const CvtItem* __restrict__ it
     if (it.mode == 0) {
       __nv_bfloat16* dh = it.dh + (int64_t)r * it.ld;
       __nv_bfloat16* dl = it.dl + (int64_t)r * it.ld;
+      if (it.n <= 128) {   // short rows: one warp per row, 8 rows per CTA pass (the block loop below
+        continue;          // would leave most of the 256 threads idle); handled after this loop
+      }
       for (int c = threadIdx.x; c < it.n; c += 256) {
         __nv_bfloat16 h, l;
         split(__ldg(src + c), h, l);
@@ -584,14 +587,43 @@ __global__ void __launch_bounds__(256) cvt_kernel(const CvtItem* __restrict__ it
       }
     } else {   // R[o, j s^2 + ph] -> block ph, row o, column j
       const int nj = it.n / it.s2;
-      for (int j = threadIdx.x; j < nj; j += 256)
-        for (int ph = 0; ph < it.s2; ++ph) {
-          __nv_bfloat16 h, l;
-          split(__ldg(src + j * it.s2 + ph), h, l);
-          const int64_t o = ((int64_t)ph * it.m + r) * it.ld + j;
-          it.dh[o] = h;
-          it.dl[o] = l;
+      if (it.s2 == 4 && ((it.src_off + (int64_t)r * it.n) & 3) == 0) {   // the 4 phases of j: one float4
+        for (int j = threadIdx.x; j < nj; j += 256) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(src) + j);
+          const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int ph = 0; ph < 4; ++ph) {
+            __nv_bfloat16 h, l;
+            split(x[ph], h, l);
+            const int64_t o = ((int64_t)ph * it.m + r) * it.ld + j;
+            it.dh[o] = h;
+            it.dl[o] = l;
+          }
         }
+      } else {
+        for (int j = threadIdx.x; j < nj; j += 256)
+          for (int ph = 0; ph < it.s2; ++ph) {
+            __nv_bfloat16 h, l;
+            split(__ldg(src + j * it.s2 + ph), h, l);
+            const int64_t o = ((int64_t)ph * it.m + r) * it.ld + j;
+            it.dh[o] = h;
+            it.dl[o] = l;
+          }
+      }
+    }
+  }
+  if (it.mode == 0 && it.n <= 128) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = blockIdx.x * 8 + warp; r < it.m; r += gridDim.x * 8) {
+      const float* src = ortho + it.src_off + (int64_t)r * it.n;
+      __nv_bfloat16* dh = it.dh + (int64_t)r * it.ld;
+      __nv_bfloat16* dl = it.dl + (int64_t)r * it.ld;
+      for (int c = lane; c < it.n; c += 32) {
+        __nv_bfloat16 h, l;
+        split(__ldg(src + c), h, l);
+        dh[c] = h;
+        dl[c] = l;
+      }
     }
   }
 }
@@ -916,7 +948,7 @@ int launch_compose_tc(Plan& P, const float* ortho, void* stream) {
   if (!T->cvt.empty()) {
     int maxm = 1;
     for (auto& c : T->cvt) maxm = std::max(maxm, c.m);
-    dim3 grid((unsigned)std::min(maxm, 128), (unsigned)T->cvt.size());
+    dim3 grid((unsigned)std::min(maxm, 32), (unsigned)T->cvt.size());   // fewer, fuller CTAs
     launch_pdl(cvt_kernel, grid, dim3(256), 0, s, (const CvtItem*)T->dcvt, ortho);
     P.launches++;
     if (int e = (int)cudaGetLastError()) return e;

@@ -187,8 +187,6 @@ struct PowerBufs {
   float* t;       // t = W v, per matrix at t_off
   float* tpart;   // |t|^2 per row item
   float* wpart;   // |w|^2 per column item
-  int vreg;       // floats of the vector region at the start of smem (resident layout)
-  int resident;   // every CTA owns at most one row item and one column item: keep both W blocks in smem
 };
 
 __global__ void __launch_bounds__(256) power_fused_kernel(const PowerItem* __restrict__ items, int n_items,
@@ -257,25 +255,14 @@ __global__ void __launch_bounds__(256) power_fused_kernel(const PowerItem* __res
       const float* Wm = W + it.off;
       // stage the block in smem with all loads in flight (rows padded to n + 4)
       const int ldw = n + 4;
-      float* Ws = pb.resident ? sm + pb.vreg : sm + ((n + 3) & ~3);
+      float* Ws = sm + ((n + 3) & ~3);
       const bool staged = (n & 3) == 0 && rows * ldw <= kPowerStage;
-      if (staged && !(pb.resident && itr > 0)) {   // W is constant: a resident block is loaded once
+      if (staged) {
         const float4* src = reinterpret_cast<const float4*>(Wm + (int64_t)it.r0 * n);
         const int n4 = n >> 2;
-        // batch 4 independent loads per thread so the L2 latencies overlap
-        for (int e0 = threadIdx.x; e0 < rows * n4; e0 += 1024) {
-          float4 v[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (e0 + u * 256 < rows * n4) v[u] = __ldg(src + e0 + u * 256);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int e = e0 + u * 256;
-            if (e < rows * n4) {
-              const int r = e / n4, c = e - r * n4;
-              *reinterpret_cast<float4*>(Ws + r * ldw + 4 * c) = v[u];
-            }
-          }
+        for (int e = threadIdx.x; e < rows * n4; e += 256) {
+          const int r = e / n4, c = e - r * n4;
+          *reinterpret_cast<float4*>(Ws + r * ldw + 4 * c) = __ldg(src + e);
         }
       }
       __syncthreads();
@@ -335,28 +322,14 @@ __global__ void __launch_bounds__(256) power_fused_kernel(const PowerItem* __res
       const float* Wm = W + ci.off;
       // stage the column block in smem (rows of cw padded to cw + 4) when it fits
       const int ldc = cw + 4;
-      float* Ws = pb.resident ? sm + pb.vreg + kPowerStage : part + 256;
+      float* Ws = part + 256;
       const bool staged = ((n | ci.c0 | cw) & 3) == 0 && m * ldc <= kPowerStage;
-      if (staged && !(pb.resident && itr > 0)) {
+      if (staged) {
         const int c4n = cw >> 2;
-        for (int e0 = threadIdx.x; e0 < m * c4n; e0 += 1024) {
-          float4 v[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int e = e0 + u * 256;
-            if (e < m * c4n) {
-              const int r = e / c4n, c = e - r * c4n;
-              v[u] = __ldg(reinterpret_cast<const float4*>(Wm + (int64_t)r * n + ci.c0) + c);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int e = e0 + u * 256;
-            if (e < m * c4n) {
-              const int r = e / c4n, c = e - r * c4n;
-              *reinterpret_cast<float4*>(Ws + r * ldc + 4 * c) = v[u];
-            }
-          }
+        for (int e = threadIdx.x; e < m * c4n; e += 256) {
+          const int r = e / c4n, c = e - r * c4n;
+          *reinterpret_cast<float4*>(Ws + r * ldc + 4 * c) =
+              __ldg(reinterpret_cast<const float4*>(Wm + (int64_t)r * n + ci.c0) + c);
         }
       }
       __syncthreads();
@@ -467,20 +440,8 @@ int launch_power_fused(Plan& p, const float* W, const float* v_in, int use_const
   int64_t maxn = 0, maxm = 0;
   for (auto& m : p.mat_items) { maxn = std::max<int64_t>(maxn, m.n); maxm = std::max<int64_t>(maxm, m.m); }
   // smem: v (n) + staged block for row items; u (m) + 256 partial sums + staged block for column items
-  const int vreg = (int)std::max<int64_t>(((maxn + 3) & ~3), ((maxm + 3) & ~3) + 256);
-  // resident layout: [vectors | row block | column block], so each CTA keeps its W blocks across iterations
-  const int n_items0 = (int)p.power_items.size(), n_cols0 = (int)p.col_items.size();
-  int dev0 = 0, sms0 = 0;
-  cudaGetDevice(&dev0);
-  cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0);
-  static const bool no_res = std::getenv("ORTH_POWER_NO_RESIDENT") != nullptr;
-  const size_t smem_res = (size_t)(vreg + 2 * kPowerStage) * sizeof(float);
-  int occ_res = 0;
-  if (smem_res > 48 * 1024) cudaFuncSetAttribute(power_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_res);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_res, power_fused_kernel, 256, smem_res);
-  const bool resident = !no_res && iters > 1 && occ_res >= 1 &&
-                        std::max(n_items0, n_cols0) <= std::min(occ_res, 4) * sms0;
-  const size_t smem = resident ? smem_res : (size_t)(vreg + kPowerStage) * sizeof(float);
+  const size_t smem = (size_t)(std::max<int64_t>(((maxn + 3) & ~3), ((maxm + 3) & ~3) + 256) + kPowerStage) *
+                      sizeof(float);
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     cudaFuncSetAttribute(power_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -495,8 +456,6 @@ int launch_power_fused(Plan& p, const float* W, const float* v_in, int use_const
   static const int mult = std::getenv("ORTH_POWER_CTAS_PER_SM") ? std::atoi(std::getenv("ORTH_POWER_CTAS_PER_SM")) : 4;
   const int grid = std::max(1, std::min(std::max(n_items, n_cols), std::max(1, std::min(occ, mult)) * sms));
   PowerBufs pb;
-  pb.vreg = vreg;
-  pb.resident = resident && grid >= std::max(n_items, n_cols) ? 1 : 0;
   pb.t = p.d_partial;
   pb.tpart = p.d_partial + pad_up(p.t_numel, kPadF32);
   pb.wpart = pb.tpart + pad_up(p.n_chunks, kPadF32);

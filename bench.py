@@ -52,19 +52,42 @@ class Clocks:
         self.p = None
 
     def start(self):
+        """Start the 100 ms sampler; returns once it has produced its first line (nvidia-smi takes
+        a few hundred ms to come up, longer than a short timed region)."""
+        import threading
+        self.lines, self.t0, self.t1 = [], None, None
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
+            return
+
+        def reader():
+            for line in self.p.stdout:
+                self.lines.append((time.monotonic(), line))
+        threading.Thread(target=reader, daemon=True).start()
+        t_end = time.monotonic() + 5.0
+        while not self.lines and time.monotonic() < t_end:
+            time.sleep(0.01)
+
+    def mark(self, begin: bool):
+        """Bracket the sampled window (the timed region plus the load window after it)."""
+        if begin:
+            self.t0 = time.monotonic()
+        else:
+            self.t1 = time.monotonic()
 
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        time.sleep(0.15)
         self.p.terminate()
-        out = self.p.communicate()[0]
+        self.p.wait()
+        t0 = self.t0 if self.t0 is not None else 0.0
+        t1 = (self.t1 if self.t1 is not None else time.monotonic()) + 0.1
+        out = "".join(line for t, line in self.lines if t0 <= t <= t1)
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
@@ -81,7 +104,21 @@ class Clocks:
                     reasons.add(n)
         load = [s for s in sm if mx and s > 0.3 * mx] or sm
         return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "window": "timed region + the same step replayed untimed until >= 0.4 s (100 ms sampling)",
+                "window_s": round(t1 - 0.1 - t0, 3) if self.t0 is not None else None}
+
+
+def clock_window(clk, step, torch, min_s=0.4):
+    """A timed region shorter than a few nvidia-smi periods (cfg2: 20 x 0.85 ms) gets no clock
+    sample of its own, so the sampled window is the timed region plus the same step, untimed,
+    repeated right after it until the window spans min_s seconds."""
+    if clk.t0 is not None:
+        while time.monotonic() - clk.t0 < min_s:
+            for _ in range(8):
+                step()
+            torch.cuda.synchronize()
+    clk.mark(False)
 
 
 # ------------------------------------------------------------------ workload
@@ -284,6 +321,7 @@ def ours(args):
     names = ["orth0", "orth1", "comp1", "gather1"] + [f"conv{l}_{e}" for l in range(nl) for e in (0, 1)]
     ev = {n: [] for n in names}
     barrier()
+    clk.mark(True)
     if graphs:
         # timed region: K steps, each one graph replay bracketed by events (L2 flushed before each)
         s_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -293,6 +331,7 @@ def ours(args):
             graphs["step"].replay()
             s_ev[i][1].record()
         barrier()
+        clock_window(clk, lambda: (flush.zero_(), graphs["step"].replay()), torch)
         clocks = clk.stop()
         step_ms = [a.elapsed_time(b) for a, b in s_ev]
         # breakdown (untimed for `value`): the same K steps through the per-phase graphs
@@ -305,6 +344,7 @@ def ours(args):
             flush.zero_()                              # L2 flush outside the events
             run_step(W, orth, torch, world, pg, ev, graphs)
         barrier()
+        clock_window(clk, lambda: (flush.zero_(), run_step(W, orth, torch, world, pg, None, graphs)), torch)
         clocks = clk.stop()
     launches = plan.launches - launches0 if not graphs else per_step_launches * args.steps
     plan.check()

@@ -130,7 +130,7 @@ def build_workload(orth, torch, cfg_layers, rank, world, device, compute, batch,
     orth_conv_transpose (small -> large grid)."""
     from synth import gen
     plan = orth.Plan(cfg_layers, device, rank=rank if plan_rank is None else plan_rank,
-                     world=world if plan_world is None else plan_world, compute=compute)
+                     world=world if plan_world is None else plan_world, compute=compute, max_batch=max(batch, 0))
     params = np.zeros(plan.params_numel, np.float32)
     dev = torch.device("cuda", device)
     for i, m in enumerate(plan.matrices):
@@ -171,11 +171,6 @@ def build_workload(orth, torch, cfg_layers, rank, world, device, compute, batch,
         acts.append(torch.empty((batch, Ho, Ho, d["c_out"]), device=dev, dtype=torch.bfloat16))
         shapes.append((H, Ho, d))
         H = Ho
-    # plan-owned conv scratch for the stacked-window kernel (padded input copy), sized for every layer
-    need = [plan.conv_scratch_bytes(l, batch, Ho if d.get("kind") == "convT" else H, Ho if d.get("kind") == "convT" else H)
-            for l, (H, Ho, d) in enumerate(shapes)]
-    if need:
-        plan.reserve(max(need))
     W["x"] = ins[0] if ins else torch.zeros(1, device=dev, dtype=torch.bfloat16)
     W["ins"], W["acts"], W["shapes"] = ins, acts, shapes
     W["kviews"] = [plan.kernel_bf16(W["kbf16"], l) for l in range(len(cfg_layers))]

@@ -25,13 +25,21 @@
  *    kernels, x, y, bias).  They are DEVICE pointers on the plan's device,
  *    16-byte aligned (128 B preferred).  The plan owns its workspace (allocated
  *    in orth_plan_create, freed in orth_plan_destroy) and a device status word.
- *    No call allocates device memory after create.
+ *    No call allocates device memory after create: the per-layer conv scratch
+ *    (split-K partials and flags, padded input copies, transposed / packed
+ *    weights) is sized at create from the declared grid (grid_h, grid_w) of
+ *    every layer and opts.max_batch, one private slice per layer.
  *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy
  *    default stream).  Compute calls are asynchronous: they validate
  *    arguments synchronously (enqueuing nothing on failure), enqueue kernels on
- *    `stream` and return.  None calls cudaDeviceSynchronize.
- *  - Device-side conditions (zero matrix; non-finite NS residual,
- *    S:125) set the plan's status word; orth_plan_check reports them.
+ *    `stream` and return.  None calls cudaDeviceSynchronize.  Calls on
+ *    DIFFERENT layers may run concurrently on different streams (each layer
+ *    owns its conv scratch); calls on the same layer, and the construction
+ *    calls (orth_orthogonalize / orth_compose_kernel, which share the NS and
+ *    composition workspace), must be ordered on one stream.
+ *  - Device-side conditions (zero matrix; NS not converged, S:125:
+ *    non-finite, or the residual bound of the last iteration above
+ *    opts.ns_tol) set the plan's status word; orth_plan_check reports them.
  *  - Determinism: results are bitwise reproducible for fixed inputs, device
  *    type and (rank, world): no floating-point atomics, fixed reduction order.
  *  - Threading: a plan serves one host thread at a time.  orth_last_error is
@@ -54,7 +62,7 @@ typedef enum {
   ORTH_ERR_UNSUPPORTED_CONFIG = 2, /* k < s, gcd(s, d) != 1 (R10), non-square k/s/d, dense forward */
   ORTH_ERR_SHAPE_MISMATCH = 3,     /* N/H/W inconsistent with the layer, circular with s not dividing H or W (R11) */
   ORTH_ERR_ZERO_NORM = 4,          /* device: a zero parameter matrix */
-  ORTH_ERR_NOT_CONVERGED = 5,      /* device: non-finite NS residual */
+  ORTH_ERR_NOT_CONVERGED = 5,      /* device: NS residual non-finite or its bound above ns_tol */
   ORTH_ERR_CUDA = 6,               /* CUDA runtime error; detail in orth_last_error() */
   ORTH_ERR_OUT_OF_MEMORY = 7,      /* workspace allocation failed */
   ORTH_ERR_NO_DEVICE = 8           /* compute call on a host-only plan (device = -1) */
@@ -73,7 +81,14 @@ typedef enum { ORTH_PRESCALE_POWER = 0, ORTH_PRESCALE_FROBENIUS = 1 } orth_presc
  *    (c_in, c_out/g, k, k) (R13).
  *  kind ORTH_DENSE: an OrthoLinear weight c_out x c_in; k = s = d = 1.
  *  Square kernels/strides/dilations only (k_h == k_w, ...).  pad_* = -1 selects
- *  the "same" rule p_t = floor(d(k-1)/2), p_b = d(k-1) - p_t (R11).  */
+ *  the "same" rule p_t = floor(d(k-1)/2), p_b = d(k-1) - p_t (R11).
+ *  grid_h, grid_w: the largest spatial size the layer's conv calls will see on
+ *  the forward-conv INPUT side (ORTH_CONV2D: its input; ORTH_CONV_TRANSPOSE2D:
+ *  its large output grid, H_big of orth_conv_transpose).  Together with
+ *  opts.max_batch they size the layer's conv scratch at create time; 0 = not
+ *  declared (no scratch: calls still run, on the kernels that need none, and
+ *  so does any call larger than the declaration -- same results up to FP32
+ *  summation order).  */
 typedef struct {
   int32_t kind;          /* orth_kind_t */
   int32_t c_in, c_out;
@@ -83,6 +98,7 @@ typedef struct {
   int32_t groups;
   int32_t pad_t, pad_b, pad_l, pad_r;
   int32_t padding_mode;  /* orth_pad_t */
+  int32_t grid_h, grid_w;
 } orth_layer_desc_t;
 
 /* OrthoParams, Bjorck only. */
@@ -96,9 +112,15 @@ typedef struct {
                             ORTH_BF16   tensor cores, BF16 operands, FP32 master X in residual form
                                         X <- X + b X (I - X^T X); the last polish_iters iterations and the
                                         composition use the 3-pass hi/lo split (~2^-16 products);
-                            ORTH_BF16X3 tensor cores, 3-pass split everywhere (FP32-accurate to ~1e-5). */
+                            ORTH_BF16X3 tensor cores, 3-pass split everywhere (products to ~2^-16:
+                                        measured 2e-5 relative on chained kernels, tested at 1e-4; only
+                                        ORTH_F32 meets the 1e-5 FP32 tolerance). */
   int32_t polish_iters;  /* BF16 only: trailing iterations run FP32-accurate, default 2 */
-  int32_t rank, world;   /* construction sharding by layer (R22); default 0, 1 */
+  int32_t rank, world;   /* construction sharding by (layer, group) unit, LPT (R22); default 0, 1 */
+  float ns_tol;          /* NOT_CONVERGED threshold on the bound 3/4 r^2 + 1/4 r^3 >= |I - X_T^T X_T|_F,
+                            r = |I - X_{T-1}^T X_{T-1}|_F from the last iteration's own Gram (R20);
+                            default 1e-3 (north star max|sigma - 1|); <= 0: non-finite check only */
+  int32_t max_batch;     /* largest N of any conv call (sizes the per-layer scratch); default 0 */
 } orth_opts_t;
 
 /* Fill *opts with the defaults above. */
@@ -116,18 +138,9 @@ orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers
                                int32_t device, orth_plan_t* plan);
 orth_status_t orth_plan_destroy(orth_plan_t plan);
 
-/* Reserve `bytes` of plan-owned device scratch for the forward / adjoint
- * convolutions (synchronous; the only call besides orth_plan_create that
- * allocates, and only when `bytes` exceeds the current reservation).  Stride-1
- * layers with >= 128 output channels per group then run the stacked-window
- * tensor-core kernel, which first writes a padded copy of its input
- * (N x (Ho + d(k-1)) x (Wo + d(k-1)) x C_in BF16, in the forward-conv view of
- * the layer) into this scratch; a call whose padded input does not fit uses
- * the other kernels (same results up to FP32 summation order).  0 frees it. */
-orth_status_t orth_plan_reserve(orth_plan_t plan, int64_t bytes);
-
 /* Plan queries (int64 result in *out).  `index` is a layer index for the
- * ORTH_Q_LAYER_* queries and a global matrix index for ORTH_Q_MATRIX_*. */
+ * ORTH_Q_LAYER_* queries, a global matrix index for ORTH_Q_MATRIX_* and a unit
+ * index for ORTH_Q_UNIT_*. */
 typedef enum {
   ORTH_Q_N_LAYERS = 0,
   ORTH_Q_N_MATRICES = 1,          /* total parameter matrices over all layers and groups */
@@ -137,24 +150,37 @@ typedef enum {
   ORTH_Q_KERNELS_BF16_NUMEL = 5,  /* bf16 elements in kernels_bf16 */
   ORTH_Q_WORKSPACE_BYTES = 6,
   ORTH_Q_NS_FLOPS = 7,            /* algorithmic NS flops 4 m n^2 T (m >= n) of this rank's matrices */
-  ORTH_Q_KERNEL_SEGMENT_F32 = 8,  /* per-rank segment size (floats) of kernels_f32 */
+  ORTH_Q_KERNEL_SEGMENT_F32 = 8,  /* per-rank segment size (floats) of the gather layout (world > 1) */
   ORTH_Q_KERNEL_SEGMENT_BF16 = 9,
+  ORTH_Q_N_UNITS = 10,            /* construction units (layer, group) over all layers */
+  ORTH_Q_GATHER_F32_NUMEL = 11,   /* world * KERNEL_SEGMENT_F32 (world == 1: KERNELS_F32_NUMEL) */
+  ORTH_Q_GATHER_BF16_NUMEL = 12,
+  ORTH_Q_CONV_SCRATCH_BYTES = 13, /* plan-owned conv scratch over all layers */
   ORTH_Q_LAYER_FIRST_MATRIX = 20, /* global index of the layer's first matrix */
   ORTH_Q_LAYER_MATS_PER_GROUP = 21,
   ORTH_Q_LAYER_KERNEL_OFF_F32 = 22,
   ORTH_Q_LAYER_KERNEL_OFF_BF16 = 23,
   ORTH_Q_LAYER_KERNEL_NUMEL = 24, /* elements of the layer kernel (same in both layouts) */
-  ORTH_Q_LAYER_OWNER = 25,        /* rank that constructs this layer */
+  ORTH_Q_LAYER_OWNER = 25,        /* rank that constructs the layer's group 0 (see ORTH_Q_UNIT_OWNER) */
   ORTH_Q_LAYER_C_MID = 26,        /* derived internal width (R7); 0 if none */
   ORTH_Q_LAYER_C_B = 27,          /* BCOP width; 0 if none */
   ORTH_Q_LAYER_KP = 28,           /* BCOP size k' (R8); 0 if none */
+  ORTH_Q_LAYER_SCRATCH_BYTES = 29,/* this layer's conv scratch slice */
   ORTH_Q_MATRIX_ROWS = 40,
   ORTH_Q_MATRIX_COLS = 41,
   ORTH_Q_MATRIX_OFFSET = 42,      /* float offset in params / ortho */
   ORTH_Q_MATRIX_CACHE_OFFSET = 43,/* float offset of its length-n vector in the power cache */
   ORTH_Q_MATRIX_LAYER = 44,
   ORTH_Q_MATRIX_GROUP = 45,
-  ORTH_Q_MATRIX_ROLE = 46         /* 0 Q, 1 U, 2 R, 3 W */
+  ORTH_Q_MATRIX_ROLE = 46,        /* 0 Q, 1 U, 2 R, 3 W */
+  ORTH_Q_UNIT_LAYER = 60,         /* units are ordered layer -> group */
+  ORTH_Q_UNIT_GROUP = 61,
+  ORTH_Q_UNIT_OWNER = 62,         /* rank that orthogonalises and composes this unit */
+  ORTH_Q_UNIT_NUMEL = 63,         /* kernel elements of one unit: (c_out/g) (c_in/g) k^2 (forward view) */
+  ORTH_Q_UNIT_GATHER_OFF_F32 = 64,/* offset in the gather layout (owner * segment + position) */
+  ORTH_Q_UNIT_GATHER_OFF_BF16 = 65,
+  ORTH_Q_UNIT_KERNEL_OFF_F32 = 66,/* offset in the final layout (= LAYER_KERNEL_OFF + group * numel) */
+  ORTH_Q_UNIT_KERNEL_OFF_BF16 = 67
 } orth_query_t;
 orth_status_t orth_plan_query(orth_plan_t plan, int32_t what, int32_t index, int64_t* out);
 
@@ -170,12 +196,17 @@ orth_status_t orth_plan_query(orth_plan_t plan, int32_t what, int32_t index, int
 orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* ortho_out, float* power_cache,
                                  float* residual_out, void* stream);
 
-/* a4+a5.  ortho: the output of orth_orthogonalize.  kernels_f32: receives each
- * layer owned by this rank at ORTH_Q_LAYER_KERNEL_OFF_F32 in PyTorch weight
- * layout (Conv2d: (c_out, c_in/g, k, k); ConvTranspose2d: (c_in, c_out/g, k, k);
- * dense: (c_out, c_in)).  kernels_bf16: nullable; receives the GEMM layout
- * (C_o, k, k, C_i/g) of the forward conv, RNE-rounded, at
- * ORTH_Q_LAYER_KERNEL_OFF_BF16.  Segments are rank-major (R22). */
+/* a4+a5.  ortho: the output of orth_orthogonalize.  kernels_f32: receives the
+ * kernels in PyTorch weight layout (Conv2d: (c_out, c_in/g, k, k);
+ * ConvTranspose2d: (c_in, c_out/g, k, k); dense: (c_out, c_in)).  kernels_bf16:
+ * nullable; receives the GEMM layout (C_o, k, k, C_i/g) of the forward conv,
+ * RNE-rounded.
+ * world == 1: the final layout, layer l at ORTH_Q_LAYER_KERNEL_OFF_{F32,BF16}
+ * (ORTH_Q_KERNELS_*_NUMEL elements).
+ * world > 1: the GATHER layout (ORTH_Q_GATHER_*_NUMEL elements): this rank's
+ * units only, at ORTH_Q_UNIT_GATHER_OFF_* inside its own rank-major segment
+ * [rank * seg, (rank + 1) * seg) -- the input of one all-gather of equal
+ * segments (R22), after which orth_kernels_assemble builds the final layout. */
 orth_status_t orth_compose_kernel(orth_plan_t plan, const float* ortho, float* kernels_f32, void* kernels_bf16,
                                   void* stream);
 
@@ -198,6 +229,15 @@ orth_status_t orth_conv_forward(orth_plan_t plan, int32_t layer, const void* ker
 orth_status_t orth_conv_transpose(orth_plan_t plan, int32_t layer, const void* kernel, const float* bias,
                                   const void* y_small, void* x_big, int32_t N, int32_t H_big, int32_t W_big,
                                   int32_t io, void* stream);
+
+/* a8 (world > 1).  Copies every unit from the all-gathered gather layout
+ * (ORTH_Q_UNIT_GATHER_OFF_*) to its place in the final layout
+ * (ORTH_Q_UNIT_KERNEL_OFF_*), so that each layer's kernel is contiguous for
+ * orth_conv_forward.  Either pair (gathered_f32, kernels_f32) or
+ * (gathered_bf16, kernels_bf16) may be NULL; the buffers must not overlap.
+ * world == 1: nothing to do (returns ORTH_OK). */
+orth_status_t orth_kernels_assemble(orth_plan_t plan, const float* gathered_f32, float* kernels_f32,
+                                    const void* gathered_bf16, void* kernels_bf16, void* stream);
 
 /* Synchronises `stream`, reads and clears the device status word; returns the
  * first device-side error since the last check (or a pending CUDA error). */

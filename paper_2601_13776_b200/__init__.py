@@ -29,11 +29,13 @@ PAD_ZEROS, PAD_CIRCULAR = 0, 1
 CONV2D, CONV_TRANSPOSE2D, DENSE = 0, 1, 2
 PRESCALE_POWER, PRESCALE_FROBENIUS = 0, 1
 Q = dict(N_LAYERS=0, N_MATRICES=1, PARAMS_NUMEL=2, CACHE_NUMEL=3, KERNELS_F32_NUMEL=4, KERNELS_BF16_NUMEL=5,
-         WORKSPACE_BYTES=6, NS_FLOPS=7, KERNEL_SEGMENT_F32=8, KERNEL_SEGMENT_BF16=9,
+         WORKSPACE_BYTES=6, NS_FLOPS=7, KERNEL_SEGMENT_F32=8, KERNEL_SEGMENT_BF16=9, N_UNITS=10,
+         GATHER_F32_NUMEL=11, GATHER_BF16_NUMEL=12, CONV_SCRATCH_BYTES=13,
          LAYER_FIRST_MATRIX=20, LAYER_MATS_PER_GROUP=21, LAYER_KERNEL_OFF_F32=22, LAYER_KERNEL_OFF_BF16=23,
-         LAYER_KERNEL_NUMEL=24, LAYER_OWNER=25, LAYER_C_MID=26, LAYER_C_B=27, LAYER_KP=28,
+         LAYER_KERNEL_NUMEL=24, LAYER_OWNER=25, LAYER_C_MID=26, LAYER_C_B=27, LAYER_KP=28, LAYER_SCRATCH_BYTES=29,
          MATRIX_ROWS=40, MATRIX_COLS=41, MATRIX_OFFSET=42, MATRIX_CACHE_OFFSET=43, MATRIX_LAYER=44,
-         MATRIX_GROUP=45, MATRIX_ROLE=46)
+         MATRIX_GROUP=45, MATRIX_ROLE=46, UNIT_LAYER=60, UNIT_GROUP=61, UNIT_OWNER=62, UNIT_NUMEL=63,
+         UNIT_GATHER_OFF_F32=64, UNIT_GATHER_OFF_BF16=65, UNIT_KERNEL_OFF_F32=66, UNIT_KERNEL_OFF_BF16=67)
 ROLES = {0: "Q", 1: "U", 2: "R", 3: "W"}
 _KIND = {"conv": CONV2D, "convT": CONV_TRANSPOSE2D, "dense": DENSE}
 _MODE = {"zeros": PAD_ZEROS, "circular": PAD_CIRCULAR}
@@ -41,12 +43,14 @@ _MODE = {"zeros": PAD_ZEROS, "circular": PAD_CIRCULAR}
 
 class LayerDesc(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("kind", "c_in", "c_out", "k_h", "k_w", "stride_h", "stride_w", "dil_h",
-                                         "dil_w", "groups", "pad_t", "pad_b", "pad_l", "pad_r", "padding_mode")]
+                                         "dil_w", "groups", "pad_t", "pad_b", "pad_l", "pad_r", "padding_mode",
+                                         "grid_h", "grid_w")]
 
 
 class Opts(C.Structure):
     _fields_ = [("ns_iters", C.c_int32), ("beta", C.c_float), ("prescale", C.c_int32), ("power_iters", C.c_int32),
-                ("compute", C.c_int32), ("polish_iters", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32)]
+                ("compute", C.c_int32), ("polish_iters", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
+                ("ns_tol", C.c_float), ("max_batch", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -60,8 +64,8 @@ _sig = {
     "orth_compose_kernel": (C.c_int, [_P, _P, _P, _P, _P]),
     "orth_conv_forward": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
     "orth_conv_transpose": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
+    "orth_kernels_assemble": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "orth_plan_check": (C.c_int, [_P, _P]),
-    "orth_plan_reserve": (C.c_int, [_P, C.c_int64]),
     "orth_plan_launch_count": (C.c_int64, [_P]),
     "orth_status_string": (C.c_char_p, [C.c_int]),
     "orth_last_error": (C.c_char_p, []),
@@ -86,12 +90,24 @@ def _check(st: int, where: str):
         raise OrthError(st, where)
 
 
+def layer_grid(d: Dict):
+    """Declared forward-conv input grid (grid_h, grid_w) of a layer dict: ``grid`` if given, else from
+    synth's ``H`` (the call's input size; a transposed layer's large grid is H * s), else (0, 0)."""
+    if d.get("grid"):
+        return tuple(d["grid"])
+    H = d.get("H", 0) or 0
+    if d.get("kind") == "convT":
+        H *= d.get("s", 1)
+    return (H, H)
+
+
 def layer_desc(d: Dict) -> LayerDesc:
     """Marshal a synth.configs-style dict into orth_layer_desc_t."""
     pads = d.get("pad") or (-1, -1, -1, -1)
     k, s, dl = d.get("k", 3), d.get("s", 1), d.get("d", 1)
+    gh, gw = layer_grid(d) if d.get("kind", "conv") != "dense" else (0, 0)
     return LayerDesc(_KIND[d.get("kind", "conv")], d["c_in"], d["c_out"], k, k, s, s, dl, dl, d.get("g", 1),
-                     pads[0], pads[1], pads[2], pads[3], _MODE[d.get("padding_mode", "circular")])
+                     pads[0], pads[1], pads[2], pads[3], _MODE[d.get("padding_mode", "circular")], gh, gw)
 
 
 def make_opts(**kw) -> Opts:
@@ -165,12 +181,13 @@ def orth_conv_transpose(h: int, layer: int, kernel, y_small, x_big, N: int, H_bi
                                     io, _stream(stream)), "orth_conv_transpose")
 
 
+def orth_kernels_assemble(h: int, gathered_f32, kernels_f32, gathered_bf16=None, kernels_bf16=None, stream=None):
+    _check(_lib.orth_kernels_assemble(h, _ptr(gathered_f32), _ptr(kernels_f32), _ptr(gathered_bf16),
+                                      _ptr(kernels_bf16), _stream(stream)), "orth_kernels_assemble")
+
+
 def orth_plan_check(h: int, stream=None):
     _check(_lib.orth_plan_check(h, _stream(stream)), "orth_plan_check (device status)")
-
-
-def orth_plan_reserve(h: int, nbytes: int):
-    _check(_lib.orth_plan_reserve(h, int(nbytes)), "orth_plan_reserve")
 
 
 def orth_plan_launch_count(h: int) -> int:
@@ -197,6 +214,17 @@ class Plan:
         self.kbf16_numel = q("KERNELS_BF16_NUMEL")
         self.workspace_bytes = q("WORKSPACE_BYTES")
         self.ns_flops = q("NS_FLOPS")
+        self.world = opts.get("world", 1)
+        self.rank = opts.get("rank", 0)
+        self.gf32_numel = q("GATHER_F32_NUMEL")
+        self.gbf16_numel = q("GATHER_BF16_NUMEL")
+        self.seg_f32 = q("KERNEL_SEGMENT_F32")
+        self.seg_bf16 = q("KERNEL_SEGMENT_BF16")
+        self.conv_scratch_bytes = q("CONV_SCRATCH_BYTES")
+        self.units = [dict(layer=q("UNIT_LAYER", u), group=q("UNIT_GROUP", u), owner=q("UNIT_OWNER", u),
+                           numel=q("UNIT_NUMEL", u), gat_f32=q("UNIT_GATHER_OFF_F32", u),
+                           gat_bf16=q("UNIT_GATHER_OFF_BF16", u), fin_f32=q("UNIT_KERNEL_OFF_F32", u),
+                           fin_bf16=q("UNIT_KERNEL_OFF_BF16", u)) for u in range(q("N_UNITS"))]
         self.matrices = [dict(m=q("MATRIX_ROWS", i), n=q("MATRIX_COLS", i), off=q("MATRIX_OFFSET", i),
                               cache_off=q("MATRIX_CACHE_OFFSET", i), layer=q("MATRIX_LAYER", i),
                               group=q("MATRIX_GROUP", i), role=ROLES[q("MATRIX_ROLE", i)])
@@ -204,7 +232,8 @@ class Plan:
         self.layer_info = [dict(first_matrix=q("LAYER_FIRST_MATRIX", l), mats_per_group=q("LAYER_MATS_PER_GROUP", l),
                                 kf32_off=q("LAYER_KERNEL_OFF_F32", l), kbf16_off=q("LAYER_KERNEL_OFF_BF16", l),
                                 numel=q("LAYER_KERNEL_NUMEL", l), owner=q("LAYER_OWNER", l),
-                                c_mid=q("LAYER_C_MID", l), c_b=q("LAYER_C_B", l), kp=q("LAYER_KP", l))
+                                c_mid=q("LAYER_C_MID", l), c_b=q("LAYER_C_B", l), kp=q("LAYER_KP", l),
+                                scratch=q("LAYER_SCRATCH_BYTES", l))
                            for l in range(self.n_layers)]
 
     # -- shapes ---------------------------------------------------------
@@ -243,7 +272,13 @@ class Plan:
         orth_orthogonalize(self.h, params, ortho_out, power_cache, residual_out, stream)
 
     def compose(self, ortho, kernels_f32, kernels_bf16=None, stream=None):
+        """world == 1: final layout (kf32_numel / kbf16_numel); world > 1: this rank's units into its
+        segment of the gather layout (gf32_numel / gbf16_numel)."""
         orth_compose_kernel(self.h, ortho, kernels_f32, kernels_bf16, stream)
+
+    def assemble(self, gathered_f32, kernels_f32, gathered_bf16=None, kernels_bf16=None, stream=None):
+        """a8: all-gathered gather layout -> final layout (world > 1)."""
+        orth_kernels_assemble(self.h, gathered_f32, kernels_f32, gathered_bf16, kernels_bf16, stream)
 
     def conv_forward(self, l: int, kernel, x, y, bias=None, stream=None):
         """x: NHWC (N, H, W, C_i) float32 or bfloat16 CUDA tensor; y preallocated."""
@@ -258,20 +293,6 @@ class Plan:
 
     def check(self, stream=None):
         orth_plan_check(self.h, stream)
-
-    def conv_scratch_bytes(self, l: int, N: int, H: int, W: int) -> int:
-        """Conv scratch (orth_plan_reserve) that lets layer l with input / large grid N x H x W run the
-        stacked-window kernel in both directions: a padded copy of the forward-view input."""
-        d = self.layers[l]
-        if d.get("kind") == "dense":
-            return 0
-        e = d.get("d", 1) * (d.get("k", 3) - 1)
-        Ho, Wo = self.out_hw(l, H, W)
-        return N * (max(H, Ho) + e) * (max(W, Wo) + e) * max(self.fwd_channels(l)) * 2
-
-    def reserve(self, nbytes: int):
-        """Plan-owned conv scratch (grows only; synchronous)."""
-        orth_plan_reserve(self.h, nbytes)
 
     @property
     def launches(self) -> int:

@@ -76,6 +76,8 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
       P.launches += 2;
       par ^= 1;
     }
+    // S:125 convergence check on the last iteration's own Gram G = X_{T-1}^T X_{T-1} (still in BUF_G)
+    if (!e) e = launch_converged_check(P, 0, P.opts.ns_tol, stream);
     if (!e && residual_out) {
       e = launch_gemm_f32(P.gram[0], bufs, stream);
       if (!e) e = launch_residual(P, residual_out, stream);
@@ -93,23 +95,28 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
       uint8_t fl[kNspMaxPhases];
       int n = 0;
       for (int t = 0; t < T; ++t) {
-        fl[n++] = (uint8_t)(1 | (gp(t) == 3 ? 2 : 0) | (par << 2) | (up(t) == 3 ? 8 : 0));
+        // the last iteration's Gram also writes its FP32 R = I - X^T X: the convergence check reads it
+        const int wf = (t == T - 1 && !residual_out) ? 16 : 0;
+        fl[n++] = (uint8_t)(1 | (gp(t) == 3 ? 2 : 0) | (par << 2) | (up(t) == 3 ? 8 : 0) | wf);
         fl[n++] = (uint8_t)((up(t) == 3 ? 2 : 0) | (par << 2) | (x_lo(t + 1) ? 8 : 0) | 16);
         par ^= 1;
       }
       if (residual_out) fl[n++] = (uint8_t)(1 | 2 | (par << 2) | 16);
       e = launch_ns_persist(P, bufs, fl, n, stream);
-      if (!e && residual_out) e = launch_residual_r(P, residual_out, stream);
+      if (!e && residual_out) e = launch_residual_r(P, residual_out, stream);   // also checks R_T (tol)
+      else if (!e) e = launch_converged_check(P, 1, P.opts.ns_tol, stream);
       return cuda_fail(e, "orth_orthogonalize");
     }
     for (int t = 0; t < T && !e; ++t) {
-      e = launch_ns_tc(P, bufs, par, true, gp(t), up(t) == 3, false, stream);
+      e = launch_ns_tc(P, bufs, par, true, gp(t), up(t) == 3, t == T - 1 && !residual_out, stream);
       if (!e) e = launch_ns_tc(P, bufs, par, false, up(t), x_lo(t + 1), true, stream);
       par ^= 1;
     }
     if (!e && residual_out) {
       e = launch_ns_tc(P, bufs, 0, true, 3, false, true, stream);
       if (!e) e = launch_residual_r(P, residual_out, stream);
+    } else if (!e) {
+      e = launch_converged_check(P, 1, P.opts.ns_tol, stream);
     }
   }
   return cuda_fail(e, "orth_orthogonalize");
@@ -148,7 +155,7 @@ orth_status_t orth_conv_forward(orth_plan_t plan, int32_t layer, const void* ker
   int Ho = 0, Wo = 0;
   st = check_conv(P, layer, kernel, x, y, N, H, W, io, Ho, Wo);
   if (st != ORTH_OK) return st;
-  const int e = launch_conv_fwd(P.layers[layer], kernel, P.d_wt_scratch, bias, x, y, N, H, W, Ho, Wo, io, stream);
+  const int e = launch_conv_fwd(P.layers[layer], kernel, P.layers[layer].wt_scratch, bias, x, y, N, H, W, Ho, Wo, io, stream);
   P.launches++;
   return cuda_fail(e, "orth_conv_forward");
 }
@@ -162,47 +169,31 @@ orth_status_t orth_conv_transpose(orth_plan_t plan, int32_t layer, const void* k
   int Ho = 0, Wo = 0;
   st = check_conv(P, layer, kernel, y_small, x_big, N, H_big, W_big, io, Ho, Wo);
   if (st != ORTH_OK) return st;
-  const int e = launch_conv_bwd(P.layers[layer], kernel, P.d_wt_scratch, bias, y_small, x_big, N, H_big, W_big, Ho,
+  const int e = launch_conv_bwd(P.layers[layer], kernel, P.layers[layer].wt_scratch, bias, y_small, x_big, N, H_big, W_big, Ho,
                                 Wo, io, stream);
   P.launches++;
   return cuda_fail(e, "orth_conv_transpose");
 }
 
-orth_status_t orth_plan_reserve(orth_plan_t plan, int64_t bytes) {
+orth_status_t orth_kernels_assemble(orth_plan_t plan, const float* gathered_f32, float* kernels_f32,
+                                    const void* gathered_bf16, void* kernels_bf16, void* stream) {
   orth_status_t st = need_device(plan);
   if (st != ORTH_OK) return st;
-  if (bytes < 0) { set_error("negative reservation"); return ORTH_ERR_INVALID_ARGUMENT; }
   Plan& P = plan->p;
-  if (bytes == 0 || bytes > P.pad_bytes) {
-    if (P.d_pad_scratch) {
-      cudaDeviceSynchronize();   // a reservation may be in use by queued work
-      cudaFree(P.d_pad_scratch);
-    }
-    P.d_pad_scratch = nullptr;
-    P.pad_bytes = 0;
-    if (bytes > 0) {
-      if (cudaMalloc(&P.d_pad_scratch, (size_t)bytes) != cudaSuccess) {
-        cudaGetLastError();
-        P.d_pad_scratch = nullptr;
-        set_error("orth_plan_reserve: cudaMalloc of %lld bytes failed", (long long)bytes);
-        return ORTH_ERR_OUT_OF_MEMORY;
-      }
-      P.pad_bytes = bytes;
-    }
-    if (!P.d_conv_flags) {
-      if (cudaMalloc(&P.d_conv_flags, 65536 * sizeof(unsigned)) != cudaSuccess ||
-          cudaMemset(P.d_conv_flags, 0, 65536 * sizeof(unsigned)) != cudaSuccess) {
-        cudaGetLastError();
-        P.d_conv_flags = nullptr;
-      }
-    }
-    for (auto& L : P.layers) {
-      L.pad_scratch = P.d_pad_scratch;
-      L.pad_bytes = P.pad_bytes;
-      L.conv_flags = P.d_pad_scratch ? P.d_conv_flags : nullptr;
-    }
+  if (P.opts.world == 1) return ORTH_OK;
+  if ((!gathered_f32) != (!kernels_f32) || (!gathered_bf16) != (!kernels_bf16)) {
+    set_error("gathered / kernels pointers must be both set or both NULL per dtype");
+    return ORTH_ERR_INVALID_ARGUMENT;
   }
-  return ORTH_OK;
+  if ((gathered_f32 && (const void*)gathered_f32 == (const void*)kernels_f32) ||
+      (gathered_bf16 && gathered_bf16 == kernels_bf16)) {
+    set_error("gathered and final kernel buffers must not overlap");
+    return ORTH_ERR_INVALID_ARGUMENT;
+  }
+  const int e = launch_assemble(P, gathered_f32, kernels_f32, (const uint16_t*)gathered_bf16, (uint16_t*)kernels_bf16,
+                                stream);
+  P.launches++;
+  return cuda_fail(e, "orth_kernels_assemble");
 }
 
 orth_status_t orth_plan_check(orth_plan_t plan, void* stream) {

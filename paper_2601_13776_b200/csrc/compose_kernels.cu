@@ -113,4 +113,52 @@ int launch_emit(Plan& p, const float* const bufs[BUF_COUNT], float* kf32, uint16
   return (int)cudaGetLastError();
 }
 
+
+namespace {
+// a8: one CTA row per unit (blockIdx.y), CTAs along x stride the unit's elements; 16-byte vectors when
+// both the source and destination run are 16-byte aligned (always for the padded gather side; for the
+// final side when the unit's numel keeps the alignment), else element copies.
+__global__ void __launch_bounds__(256) assemble_kernel(const UnitInfo* __restrict__ units, const float* __restrict__ gf,
+                                                       float* __restrict__ kf, const uint16_t* __restrict__ gb,
+                                                       uint16_t* __restrict__ kb) {
+  umma::griddep_launch_dependents();
+  umma::griddep_wait();
+  const UnitInfo u = units[blockIdx.y];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gf) {
+    const float* src = gf + u.gat_f32;
+    float* dst = kf + u.fin_f32;
+    if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+      const int64_t nv = u.numel / 4;
+      for (int64_t e = t0; e < nv; e += stride) reinterpret_cast<float4*>(dst)[e] = reinterpret_cast<const float4*>(src)[e];
+      for (int64_t e = nv * 4 + t0; e < u.numel; e += stride) dst[e] = src[e];
+    } else {
+      for (int64_t e = t0; e < u.numel; e += stride) dst[e] = src[e];
+    }
+  }
+  if (gb) {
+    const uint16_t* src = gb + u.gat_bf16;
+    uint16_t* dst = kb + u.fin_bf16;
+    if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+      const int64_t nv = u.numel / 8;
+      for (int64_t e = t0; e < nv; e += stride) reinterpret_cast<uint4*>(dst)[e] = reinterpret_cast<const uint4*>(src)[e];
+      for (int64_t e = nv * 8 + t0; e < u.numel; e += stride) dst[e] = src[e];
+    } else {
+      for (int64_t e = t0; e < u.numel; e += stride) dst[e] = src[e];
+    }
+  }
+}
+}  // namespace
+
+int launch_assemble(Plan& p, const float* gf, float* kf, const uint16_t* gb, uint16_t* kb, void* stream) {
+  if (p.units.empty() || (!gf && !gb)) return 0;
+  int64_t maxn = 1;
+  for (auto& u : p.units) maxn = std::max(maxn, u.numel);
+  // ~4 x 148 CTAs in total across units, at least one per unit
+  const int64_t per = std::max<int64_t>(1, std::min<int64_t>((maxn / 4 + 255) / 256, 592 / (int64_t)p.units.size() + 1));
+  launch_pdl(assemble_kernel, dim3((unsigned)per, (unsigned)p.units.size()), dim3(256), 0, (cudaStream_t)stream,
+             (const UnitInfo*)p.d_units, gf, kf, gb, kb);
+  return (int)cudaGetLastError();
+}
+
 }  // namespace orth

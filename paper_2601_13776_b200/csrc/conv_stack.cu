@@ -358,8 +358,8 @@ bool stack_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, StackAr
 
 }  // namespace
 
-// padded copy of x (N x Hp x P x C, rows of the whole batch back to back) into the plan scratch;
-// -1 if it does not fit the reservation
+// padded copy of x (N x Hp x P x C, rows of the whole batch back to back) into the layer's scratch;
+// -1 if it does not fit
 int launch_pad_input(const LayerInfo& L, const void* x, int N, int H, int W, int Hp, int P, void* stream) {
   const int64_t elems = (int64_t)N * Hp * P * L.ci_f;
   if (!L.pad_scratch || elems * 2 > L.pad_bytes || L.ci_f % 8 != 0) return -1;
@@ -371,6 +371,20 @@ int launch_pad_input(const LayerInfo& L, const void* x, int N, int H, int W, int
   return (int)cudaGetLastError();
 }
 
+static bool stack_rule(const LayerInfo& L, int Ho, int Wo) {
+  static const bool force = std::getenv("ORTH_CONV_STACK") != nullptr;
+  static const bool off = std::getenv("ORTH_CONV_NO_STACK") != nullptr;
+  if (off) return false;
+  return force || (L.co == 128 && Wo >= 24 && Ho >= 24);
+}
+
+int64_t conv_stack_pad_bytes(const LayerInfo& L, int N, int H, int W, int Ho, int Wo) {
+  if (!stack_rule(L, Ho, Wo)) return 0;
+  StackArgs a;
+  if (!stack_args(L, N, H, W, Ho, Wo, a)) return 0;
+  return (int64_t)N * a.Hp * a.P * a.in_C * 2;
+}
+
 int launch_conv_fwd_stack(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
                           int H, int W, int Ho, int Wo, void* stream, int flip) {
   // Opt-in (ORTH_CONV_STACK=1): measured on B200 the M=128 x N=256 MMAs of this kernel run at ~220
@@ -379,15 +393,12 @@ int launch_conv_fwd_stack(const LayerInfo& L, const void* kernel, const float* b
   // loses below (512@4: 49 vs 37 us); see DESIGN.md §9.
   // Default only where it measured faster: 128 output channels per group on images >= 24 px
   // (cfg3 128@28: 103 vs 110 us); ORTH_CONV_STACK=1 forces it wherever it applies, ORTH_CONV_NO_STACK=1 off.
-  static const bool force = std::getenv("ORTH_CONV_STACK") != nullptr;
-  static const bool off = std::getenv("ORTH_CONV_NO_STACK") != nullptr;
-  if (off || !L.pad_scratch) return -1;
-  if (!force && !(L.co == 128 && Wo >= 24 && Ho >= 24)) return -1;
+  if (!L.pad_scratch || !stack_rule(L, Ho, Wo)) return -1;
   if (((uintptr_t)x & 15) != 0 || ((uintptr_t)y & 15) != 0) return -1;
   StackArgs a;
   if (!stack_args(L, N, H, W, Ho, Wo, a)) return -1;
   const int64_t pad_elems = (int64_t)N * a.Hp * a.P * a.in_C;
-  if (pad_elems * 2 > L.pad_bytes) return -1;   // reservation too small: the caller falls back
+  if (pad_elems * 2 > L.pad_bytes) return -1;   // call larger than the declared grid / batch: the caller falls back
   if (a.num_tiles == 0) return 0;
   a.flip = flip;
   cudaStream_t s = (cudaStream_t)stream;

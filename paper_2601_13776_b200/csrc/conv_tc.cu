@@ -967,6 +967,51 @@ static int pack_weights(const LayerInfo& L, int P, const void* kernel, void* dst
   return (int)cudaGetLastError();
 }
 
+// split-K partial bytes / flags of one launch_any call (upper bound of its decision): 128 x 256 FP32 tile
+// per 256-wide output tile, only when the grid has at most half the SMs' worth of such tiles
+static int64_t splitk_need(int64_t tiles_m, int nout_g, int cr_g, int groups, int64_t* flags) {
+  if (nout_g % 256 != 0 || cr_g % 128 != 0) return 0;
+  const int64_t t256 = tiles_m * (nout_g / 256) * groups;
+  if (2 * t256 > num_sms()) return 0;
+  *flags = std::max<int64_t>(*flags, t256);
+  return t256 * 128 * 256 * 4;
+}
+
+int64_t conv_scratch_need(const LayerInfo& L, int N, int H, int W, int64_t* flags) {
+  *flags = 0;
+  if (N < 1 || H < 1 || W < 1 || L.cons == CONS_DENSE) return 0;
+  const int Ho = (H + L.pt + L.pb - L.d * (L.k - 1) - 1) / L.s + 1;
+  const int Wo = (W + L.pl + L.pr - L.d * (L.k - 1) - 1) / L.s + 1;
+  if (Ho < 1 || Wo < 1) return 0;
+  int64_t need = 0;
+  static const bool tma_on = std::getenv("ORTH_CONV_TMA") != nullptr;   // experimental padded-copy kernel
+  const int ext = L.d * (L.k - 1);
+  {  // forward: TMA-window kernels on a padded copy, or the gather kernel with split-K
+    const LayerInfo q = packed(L, pack_factor(L, false));
+    need = std::max(need, conv_stack_pad_bytes(q, N, H, W, Ho, Wo));
+    if (tma_on && q.s == 1) need = std::max(need, (int64_t)N * (Ho + ext) * (Wo + ext) * q.ci_f * 2);
+    need = std::max(need, splitk_need(((int64_t)N * Ho * Wo + 127) / 128, q.co, q.ci, q.g, flags));
+  }
+  {  // adjoint: stride 1 as the tap-flipped forward conv of the transposed view, else polyphase tiles
+    const LayerInfo q = packed(L, pack_factor(L, true));
+    if (q.s == 1) {
+      LayerInfo F = q;
+      F.ci = q.co; F.co = q.ci; F.ci_f = q.co_f; F.co_f = q.ci_f;
+      F.pt = ext - q.pt; F.pl = ext - q.pl; F.pb = ext - q.pb; F.pr = ext - q.pr;
+      need = std::max(need, conv_stack_pad_bytes(F, N, Ho, Wo, H, W));
+      if (tma_on) need = std::max(need, (int64_t)N * (H + ext) * (W + ext) * F.ci_f * 2);
+    }
+    int64_t tiles = 0;   // polyphase tiles, as launch_conv_bwd_tc builds them
+    for (int p = 0; p < q.s * q.s; ++p) {
+      const int ph = p / q.s, pw = p % q.s;
+      const int64_t hp = H > ph ? (H - ph + q.s - 1) / q.s : 0, wp = W > pw ? (W - pw + q.s - 1) / q.s : 0;
+      tiles += ((int64_t)N * hp * wp + 127) / 128;
+    }
+    need = std::max(need, splitk_need(tiles, q.ci, q.co, q.g, flags));
+  }
+  return need;
+}
+
 int launch_conv_fwd_tc(const LayerInfo& L0, const void* kernel, void* scratch, const float* bias, const void* x,
                        void* y, int N, int H, int W, int Ho, int Wo, void* stream) {
   const int P = pack_factor(L0, false);

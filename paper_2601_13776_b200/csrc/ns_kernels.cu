@@ -403,10 +403,14 @@ __global__ void __launch_bounds__(256) scale_kernel(const PowerItem* __restrict_
   for (int64_t e = beg + threadIdx.x; e < end; e += 256) X0[e] = W[e] * inv;
 }
 
-// |I - G|_F per owned matrix from its Gram; non-finite -> NOT_CONVERGED
+// r = |I - G|_F per owned matrix from its Gram (is_r: G already holds R = I - X^T X).  NOT_CONVERGED
+// (R20) when r is non-finite or the checked value exceeds tol > 0: r itself for the final
+// residual, or -- bound = 1, r of the LAST iteration's input X_{T-1} -- the bound on the result's
+// residual: with R symmetric and X' = X (I + R/2), I - X'^T X' = 3/4 R^2 + 1/4 R^3 exactly, so
+// |I - X_T^T X_T|_F <= 3/4 r^2 + 1/4 r^3.
 __global__ void __launch_bounds__(256) residual_kernel(const MatItem* __restrict__ mats, const float* __restrict__ G,
                                                        float* __restrict__ res, int32_t* __restrict__ status,
-                                                       int is_r) {
+                                                       int is_r, float tol, int bound) {
   __shared__ float red[9];
   const MatItem M = mats[blockIdx.x];
   const int s = M.m < M.n ? M.m : M.n;
@@ -421,7 +425,8 @@ __global__ void __launch_bounds__(256) residual_kernel(const MatItem* __restrict
   if (threadIdx.x == 0) {
     const float r = sqrtf(a);
     if (res) res[M.mat] = r;
-    if (!isfinite(r)) atomicCAS(status, 0, (int)ORTH_ERR_NOT_CONVERGED);
+    const float chk = bound ? r * r * (0.75f + 0.25f * r) : r;
+    if (!isfinite(r) || (tol > 0.f && !(chk <= tol))) atomicCAS(status, 0, (int)ORTH_ERR_NOT_CONVERGED);
   }
 }
 
@@ -505,7 +510,15 @@ int launch_scale(Plan& p, const float* W, float* X0, void* stream) {
 int launch_residual(Plan& p, float* residual_out, void* stream) {
   if (p.mat_items.empty()) return 0;
   residual_kernel<<<(int)p.mat_items.size(), 256, 0, (cudaStream_t)stream>>>(p.d_mat_items, p.d_gram, residual_out,
-                                                                             p.d_status, 0);
+                                                                             p.d_status, 0, p.opts.ns_tol, 0);
+  p.launches++;
+  return (int)cudaGetLastError();
+}
+
+int launch_converged_check(Plan& p, int is_r, float tol, void* stream) {
+  if (p.mat_items.empty()) return 0;
+  residual_kernel<<<(int)p.mat_items.size(), 256, 0, (cudaStream_t)stream>>>(p.d_mat_items, p.d_gram, p.d_ns_res,
+                                                                             p.d_status, is_r, tol, 1);
   p.launches++;
   return (int)cudaGetLastError();
 }
@@ -513,7 +526,7 @@ int launch_residual(Plan& p, float* residual_out, void* stream) {
 int launch_residual_r(Plan& p, float* residual_out, void* stream) {
   if (p.mat_items.empty()) return 0;
   residual_kernel<<<(int)p.mat_items.size(), 256, 0, (cudaStream_t)stream>>>(p.d_mat_items, p.d_gram, residual_out,
-                                                                             p.d_status, 1);
+                                                                             p.d_status, 1, p.opts.ns_tol, 0);
   p.launches++;
   return (int)cudaGetLastError();
 }

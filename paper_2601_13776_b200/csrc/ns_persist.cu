@@ -10,17 +10,24 @@
 // for each other.  Host-side partition: plan.cpp/build_ns_persist (cost
 // model + LPT).
 //
-// CTA roles (192 threads, one CTA per SM, 210 KB smem):
+// CTA roles (kThreads = 320 threads, one CTA per SM, kSlots x 32 KB ring +
+// 96 KB epilogue staging):
 //   warp 0  TMA producer: 128x64 BF16 operand tiles (K-major rows of X / R,
-//           or MN-major columns of row-major X) into a 6-slot ring of 32 KB
-//           slots (a 1-pass k-block takes one slot, a 3-pass hi/lo k-block two)
+//           or MN-major columns of row-major X) into a kSlots (= 4) ring of
+//           32 KB slots (a 1-pass k-block takes one slot, a 3-pass hi/lo
+//           k-block two)
 //   warp 1  TMEM allocation + the single-thread tcgen05.mma issuer, FP32
-//           accumulators double-buffered in TMEM (2 x 128 columns)
-//   warps 2-5  epilogue: TMEM -> registers -> per-warp smem transpose ->
-//           coalesced FP32 / BF16 row stores (Gram: R = I - acc; update:
-//           X' = C + beta acc), overlapping the next tile's mainloop.
-// Phase hand-off: epilogue writes -> proxy fence -> group barrier -> a
-// monotonic smem counter that releases the producer into the next phase.
+//           accumulators double-buffered in TMEM (2 x 128 columns; 2 x 256
+//           for the 128 x 256 update tiles of the phase-synchronous kernel)
+//   warps 2-9  epilogue (kEpiWarps = 8: lane quarter x column half): TMEM ->
+//           registers -> per-warp smem transpose -> coalesced FP32 / BF16 row
+//           stores (Gram: R = I - acc; update: X' = C + beta acc), overlapping
+//           the next tile's mainloop.
+// Two schedules share this tile pipeline: ns_persist_kernel (phase-synchronous
+// CTA groups: epilogue writes -> proxy fence -> group barrier -> a monotonic
+// smem counter that releases the producer into the next phase) and
+// ns_flow_kernel (dataflow: (phase, matrix, tile) items claimed in one global
+// order, each waiting on its matrix's per-phase counter).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 

@@ -29,7 +29,7 @@ struct MatInfo {
   int64_t gram_off;   // float offset of its short-side Gram in the G workspace
   int64_t bx_off;     // bf16 offset in the X / X^T copies (tensor-core NS)
   int64_t br_off;     // bf16 offset in the R copies
-  int32_t owned;      // 1 if this rank orthogonalises it
+  int32_t owned;      // 1 if this rank orthogonalises it (its unit's owner)
 };
 
 struct LayerInfo {
@@ -41,12 +41,24 @@ struct LayerInfo {
   int32_t pt, pb, pl, pr;
   int32_t kp, c_b, c_mid;
   int32_t first_mat, mats_per_group;
-  int32_t owner;
-  int64_t kf32_off, kbf16_off, kernel_numel;
-  void* pad_scratch = nullptr;  // plan-owned conv scratch (orth_plan_reserve): padded input copy,
-  int64_t pad_bytes = 0;        // or split-K partial tiles of the gather conv
-  unsigned* conv_flags = nullptr;   // split-K tile flags (zeroed; each launch leaves them zero)
+  int32_t owner;                // owner of group 0 (ORTH_Q_LAYER_OWNER)
+  int32_t first_unit;           // units [first_unit, first_unit + g) of Plan::units
+  int64_t kf32_off, kbf16_off, kernel_numel;   // final layout (contiguous layer)
+  // this layer's private conv scratch, sized at create from (grid_h, grid_w, max_batch):
+  void* pad_scratch = nullptr;  // padded input copy, or split-K partial tiles of the gather conv
+  int64_t pad_bytes = 0;
+  int64_t n_flags = 0;
+  unsigned* conv_flags = nullptr;   // split-K tile flags (zeroed at create; each launch leaves them zero)
+  void* wt_scratch = nullptr;   // BF16 transposed / group-packed weights of one call
   double ns_flops, comp_flops;
+};
+
+// One construction unit (layer, group) -- the sharding unit.
+struct UnitInfo {
+  int32_t layer, group, owner, pad_;
+  int64_t numel;                  // kernel elements of the unit
+  int64_t gat_f32, gat_bf16;      // gather layout (rank-major equal segments)
+  int64_t fin_f32, fin_bf16;      // final layout
 };
 
 // D[M x N] (+)= alpha * sum_seg opA(seg)[M x K] * opB(seg)[K x N] + beta * C.
@@ -156,6 +168,9 @@ struct TcComposePlan;   // tensor-core composition (compose_tc.cu)
 
 struct Plan {
   std::vector<LayerInfo> layers;
+  std::vector<UnitInfo> units;
+  UnitInfo* d_units = nullptr;       // device copy (orth_kernels_assemble)
+  int64_t gat_f32_numel = 0, gat_bf16_numel = 0;
   std::vector<CompUnit> comp_units;
   std::vector<int64_t> proj_off;     // per matrix: float offset of P = U U^T in comp (U only)
   TcComposePlan* tcc = nullptr;
@@ -234,10 +249,9 @@ struct Plan {
   EmitItem* d_emit = nullptr;
   int64_t partial_stride = 0;
   int64_t launches = 0;
-  void* d_pad_scratch = nullptr;    // orth_plan_reserve
-  int64_t pad_bytes = 0;
-  unsigned* d_conv_flags = nullptr; // 65536 split-K tile flags
-  uint16_t* d_wt_scratch = nullptr; // BF16 weight scratch of one layer call: [W^T | packed W], 16 x max kernel
+  void* d_conv_mem = nullptr;       // every layer's conv scratch (one allocation at create)
+  int64_t conv_mem_bytes = 0;
+  float* d_ns_res = nullptr;        // per-matrix residual of the last iteration's Gram (convergence check)
 };
 
 void set_error(const char* fmt, ...);
@@ -293,6 +307,16 @@ int launch_power_fused(Plan& p, const float* W, const float* v_in, int use_const
 // the fused power kernel's grid-barrier counter (a word of the status block; re-armed by the scale kernels)
 inline unsigned* power_bar(Plan& p) { return reinterpret_cast<unsigned*>(p.d_status + 8); }
 int launch_residual(Plan& p, float* residual_out, void* stream);
+// convergence check: r = |R|_F of the last iteration's FP32 R (is_r) or |I - G|_F (SIMT Gram);
+// NOT_CONVERGED when r is non-finite or 3/4 r^2 + 1/4 r^3 > tol (tol > 0)
+int launch_converged_check(Plan& p, int is_r, float tol, void* stream);
+// a8: copy every unit from the gather layout to the final layout
+int launch_assemble(Plan& p, const float* gf, float* kf, const uint16_t* gb, uint16_t* kb, void* stream);
+// per-layer conv scratch (bytes) for calls up to N x Hbig x Wbig (forward-conv input grid), both
+// directions: max(padded input copy of the TMA-window kernels, split-K partials); flags: tile flags
+int64_t conv_scratch_need(const LayerInfo& L, int N, int Hbig, int Wbig, int64_t* flags);
+// padded-copy bytes the stacked-window kernel would use for this forward-view call (0: not taken)
+int64_t conv_stack_pad_bytes(const LayerInfo& L, int N, int H, int W, int Ho, int Wo);
 int launch_emit(Plan& p, const float* const bufs[BUF_COUNT], float* kf32, uint16_t* kbf16, void* stream);
 int launch_conv_fwd(const LayerInfo& L, const void* kernel, void* scratch, const float* bias, const void* x, void* y,
                     int N, int H, int W, int Ho, int Wo, int io, void* stream);

@@ -38,6 +38,8 @@ static orth_status_t validate_opts(const orth_opts_t& o) {
   if (o.compute != ORTH_F32 && o.compute != ORTH_BF16 && o.compute != ORTH_BF16X3) { set_error("bad compute mode %d", o.compute); return ORTH_ERR_INVALID_ARGUMENT; }
   if (o.polish_iters < 0 || o.polish_iters > o.ns_iters) { set_error("polish_iters must be in [0, ns_iters]"); return ORTH_ERR_INVALID_ARGUMENT; }
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) { set_error("bad rank/world %d/%d", o.rank, o.world); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (o.max_batch < 0) { set_error("max_batch must be >= 0"); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (!(o.ns_tol == o.ns_tol)) { set_error("ns_tol is NaN"); return ORTH_ERR_INVALID_ARGUMENT; }
   return ORTH_OK;
 }
 
@@ -52,6 +54,7 @@ static orth_status_t validate_layer(const orth_layer_desc_t& L, int idx) {
     set_error("layer %d: groups %d must divide c_in %d and c_out %d (S:38)", idx, L.groups, L.c_in, L.c_out);
     return ORTH_ERR_INVALID_ARGUMENT;
   }
+  if (L.grid_h < 0 || L.grid_w < 0) { set_error("layer %d: grid_h/grid_w must be >= 0", idx); return ORTH_ERR_INVALID_ARGUMENT; }
   if (L.padding_mode != ORTH_PAD_ZEROS && L.padding_mode != ORTH_PAD_CIRCULAR) {
     set_error("layer %d: bad padding_mode %d", idx, L.padding_mode);
     return ORTH_ERR_INVALID_ARGUMENT;
@@ -141,21 +144,37 @@ static orth_status_t derive(Plan& P, const orth_layer_desc_t* layers, int n_laye
   return ORTH_OK;
 }
 
-// LPT greedy by cost over layers (R22): the largest unit to the least-loaded rank.
+// LPT greedy by cost over (layer, group) units (R22): the largest
+// unit (NS + composition flops of one group) to the least-loaded rank; ties
+// keep the (layer, group) order, so every rank derives the same assignment.
 static void assign_owners(Plan& P) {
   const int R = P.opts.world;
-  std::vector<int> order(P.layers.size());
+  P.units.clear();
+  for (int l = 0; l < (int)P.layers.size(); ++l) {
+    LayerInfo& L = P.layers[l];
+    L.first_unit = (int)P.units.size();
+    for (int g = 0; g < L.g; ++g) {
+      UnitInfo u{};
+      u.layer = l; u.group = g; u.owner = 0;
+      u.numel = L.kernel_numel / L.g;
+      P.units.push_back(u);
+    }
+  }
+  std::vector<int> order(P.units.size());
   std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-    return P.layers[a].ns_flops + P.layers[a].comp_flops > P.layers[b].ns_flops + P.layers[b].comp_flops;
-  });
+  auto cost = [&](int u) {
+    const LayerInfo& L = P.layers[P.units[u].layer];
+    return (L.ns_flops + L.comp_flops) / L.g;
+  };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
   std::vector<double> load(R, 0.0);
-  for (int l : order) {
+  for (int u : order) {
     int best = 0;
     for (int r = 1; r < R; ++r) if (load[r] < load[best]) best = r;
-    P.layers[l].owner = best;
-    load[best] += P.layers[l].ns_flops + P.layers[l].comp_flops + 1.0;
+    P.units[u].owner = best;
+    load[best] += cost(u) + 1.0;
   }
+  for (auto& L : P.layers) L.owner = P.units[L.first_unit].owner;
 }
 
 static void layout(Plan& P) {
@@ -170,7 +189,7 @@ static void layout(Plan& P) {
     M.gram_off = goff; goff += pad_up(s * s, kPadF32);
     M.bx_off = P.bx_numel; P.bx_numel += pad_up(pad_up(M.m, 8) * pad_up(M.n, 8), kPadBF16);
     M.br_off = P.br_numel; P.br_numel += pad_up(pad_up(s, 8) * pad_up(s, 8), kPadBF16);
-    M.owned = P.layers[M.layer].owner == P.opts.rank;
+    M.owned = P.units[P.layers[M.layer].first_unit + M.group].owner == P.opts.rank;
     if (M.owned) {
       const double a = (double)std::max(M.m, M.n), b = (double)s;
       P.ns_flops += 4.0 * a * b * b * P.opts.ns_iters;
@@ -179,18 +198,30 @@ static void layout(Plan& P) {
   P.params_numel = std::max<int64_t>(off, kPadF32);
   P.cache_numel = std::max<int64_t>(coff, kPadF32);
   P.gram_numel = std::max<int64_t>(goff, kPadF32);
-  // rank-major kernel segments
+  // final layout: layers back to back (128 B aligned), a layer's groups contiguous along dim 0
+  int64_t f32 = 0, b16 = 0;
+  for (auto& L : P.layers) {
+    L.kf32_off = f32; f32 += pad_up(L.kernel_numel, kPadF32);
+    L.kbf16_off = b16; b16 += pad_up(L.kernel_numel, kPadBF16);
+  }
+  P.kf32_numel = std::max<int64_t>(f32, kPadF32);
+  P.kbf16_numel = std::max<int64_t>(b16, kPadBF16);
+  // gather layout (a8): rank-major equal segments, each rank's units in (layer, group) order, every unit
+  // 128 B aligned; world == 1 writes the final layout directly
   const int R = P.opts.world;
   std::vector<int64_t> s32(R, 0), s16(R, 0);
-  for (auto& L : P.layers) {
-    L.kf32_off = s32[L.owner]; s32[L.owner] += pad_up(L.kernel_numel, kPadF32);
-    L.kbf16_off = s16[L.owner]; s16[L.owner] += pad_up(L.kernel_numel, kPadBF16);
+  for (auto& u : P.units) {
+    const LayerInfo& L = P.layers[u.layer];
+    u.fin_f32 = L.kf32_off + (int64_t)u.group * u.numel;
+    u.fin_bf16 = L.kbf16_off + (int64_t)u.group * u.numel;
+    u.gat_f32 = s32[u.owner]; s32[u.owner] += pad_up(u.numel, kPadF32);
+    u.gat_bf16 = s16[u.owner]; s16[u.owner] += pad_up(u.numel, kPadBF16);
   }
   P.seg_f32 = std::max<int64_t>(*std::max_element(s32.begin(), s32.end()), kPadF32);
   P.seg_bf16 = std::max<int64_t>(*std::max_element(s16.begin(), s16.end()), kPadBF16);
-  for (auto& L : P.layers) { L.kf32_off += L.owner * P.seg_f32; L.kbf16_off += L.owner * P.seg_bf16; }
-  P.kf32_numel = P.seg_f32 * R;
-  P.kbf16_numel = P.seg_bf16 * R;
+  for (auto& u : P.units) { u.gat_f32 += u.owner * P.seg_f32; u.gat_bf16 += u.owner * P.seg_bf16; }
+  P.gat_f32_numel = R > 1 ? P.seg_f32 * R : P.kf32_numel;
+  P.gat_bf16_numel = R > 1 ? P.seg_bf16 * R : P.kbf16_numel;
 }
 
 static void finish_phase(GemmPhase& ph) {
@@ -392,8 +423,8 @@ static void build_compose(Plan& P) {
   units.clear();
   for (int l = 0; l < (int)P.layers.size(); ++l) {
     LayerInfo& L = P.layers[l];
-    if (L.owner != P.opts.rank) continue;
     for (int gi = 0; gi < L.g; ++gi) {
+      if (P.units[L.first_unit + gi].owner != P.opts.rank) continue;
       Unit u{l, gi, -1, -1, -1, 0, 0};
       if ((L.cons == CONS_BCOP || L.cons == CONS_AOC) && L.kp > 1) {
         u.c = L.c_b;
@@ -487,8 +518,9 @@ static void build_compose(Plan& P) {
     EmitItem e{};
     e.layer = u.layer; e.group = u.group;
     e.co = L.co; e.ci = L.ci; e.k = (L.cons == CONS_DENSE) ? 1 : L.k; e.s = L.s; e.ci_f_per_g = L.ci;
-    e.f32_off = L.kf32_off + (int64_t)u.group * L.co * L.ci * e.k * e.k;
-    e.bf16_off = L.kbf16_off + (int64_t)u.group * L.co * L.ci * e.k * e.k;
+    const UnitInfo& U = P.units[L.first_unit + u.group];
+    e.f32_off = P.opts.world > 1 ? U.gat_f32 : U.fin_f32;     // world > 1: this rank's gather segment
+    e.bf16_off = P.opts.world > 1 ? U.gat_bf16 : U.fin_bf16;
     switch (L.cons) {
       case CONS_DENSE:
         e.src_buf = BUF_X; e.src_off = P.mats[base].off; e.mode = 0; e.tap_stride = 0; e.ld = L.ci; break;
@@ -508,6 +540,64 @@ static void build_compose(Plan& P) {
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Per-layer conv scratch, sized now from the declared grid and max_batch so that no call allocates
+// later; one private slice per layer so calls on different layers may overlap on
+// different streams: [split-K flags (zeroed) | padded copy / split-K partials | BF16 weight scratch].
+static void size_conv(Plan& P) {
+  for (auto& L : P.layers) {
+    L.pad_bytes = 0;
+    L.n_flags = 0;
+    if (L.cons == CONS_DENSE || P.opts.max_batch <= 0 || L.desc.grid_h <= 0 || L.desc.grid_w <= 0) continue;
+    L.pad_bytes = conv_scratch_need(L, P.opts.max_batch, L.desc.grid_h, L.desc.grid_w, &L.n_flags);
+  }
+}
+
+static orth_status_t allocate_conv(Plan& P) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+  struct Slice { size_t flags, pad, wt; };
+  std::vector<Slice> sl(P.layers.size());
+  std::vector<std::pair<size_t, size_t>> flag_ranges;
+  for (size_t l = 0; l < P.layers.size(); ++l) {
+    LayerInfo& L = P.layers[l];
+    sl[l] = Slice{0, 0, 0};
+    if (L.cons == CONS_DENSE) continue;
+    if (L.pad_bytes > 0) {
+      const size_t fb = (size_t)std::max<int64_t>(L.n_flags, 1) * sizeof(unsigned);
+      sl[l].flags = take(fb);
+      flag_ranges.push_back({sl[l].flags, fb});
+      sl[l].pad = take((size_t)L.pad_bytes);
+    }
+    // W^T of the adjoint, group-packed copies (<= 8x each, conv_tc.cu) when the layer packs groups
+    const bool packs = L.g > 1 && (L.ci < 64 || L.co < 64);
+    sl[l].wt = take((size_t)(packs ? 16 : 1) * L.kernel_numel * 2);
+  }
+  P.conv_mem_bytes = (int64_t)off;
+  if (off == 0) return ORTH_OK;
+  if (cudaMalloc(&P.d_conv_mem, off) != cudaSuccess) {
+    cudaGetLastError();
+    P.d_conv_mem = nullptr;
+    set_error("conv scratch cudaMalloc(%zu bytes) failed (grid_h/grid_w x max_batch too large?)", off);
+    return ORTH_ERR_OUT_OF_MEMORY;
+  }
+  char* base = (char*)P.d_conv_mem;
+  for (auto& fr : flag_ranges)
+    if (cudaMemset(base + fr.first, 0, fr.second) != cudaSuccess) {
+      set_error("conv scratch memset failed");
+      return ORTH_ERR_CUDA;
+    }
+  for (size_t l = 0; l < P.layers.size(); ++l) {
+    LayerInfo& L = P.layers[l];
+    if (L.cons == CONS_DENSE) continue;
+    L.wt_scratch = base + sl[l].wt;
+    if (L.pad_bytes > 0) {
+      L.pad_scratch = base + sl[l].pad;
+      L.conv_flags = reinterpret_cast<unsigned*>(base + sl[l].flags);
+    }
+  }
+  return ORTH_OK;
+}
+
 static orth_status_t allocate(Plan& P) {
   if (cudaSetDevice(P.device) != cudaSuccess) {
     set_error("cudaSetDevice(%d) failed: %s", P.device, cudaGetErrorString(cudaGetLastError()));
@@ -525,9 +615,8 @@ static orth_status_t allocate(Plan& P) {
   const size_t o_nsg = take(std::max<size_t>(P.ns_gram.size(), 1) * sizeof(NsDesc));
   const size_t o_nsu = take(std::max<size_t>(P.ns_upd.size(), 1) * sizeof(NsDesc));
   const size_t o_bx = take((size_t)4 * std::max<int64_t>(P.bx_numel, 64) * 2);
-  int64_t max_kernel = 64;
-  for (auto& L : P.layers) max_kernel = std::max(max_kernel, L.kernel_numel);
-  const size_t o_wt = take((size_t)16 * max_kernel * 2);   // W^T (<= 8x with packing) + packed W (<= 8x)
+  const size_t o_units = take(std::max<size_t>(P.units.size(), 1) * sizeof(UnitInfo));
+  const size_t o_res = take(std::max<size_t>(P.mats.size(), 1) * 4);
   const size_t o_br = take((size_t)2 * std::max<int64_t>(P.br_numel, 64) * 2);
   std::vector<GemmPhase*> phases = {&P.gram[0], &P.gram[1], &P.update[0], &P.update[1], &P.gram_r[0],
                                     &P.gram_r[1], &P.update_r[0], &P.update_r[1], &P.proj, &P.aoc};
@@ -557,7 +646,8 @@ static orth_status_t allocate(Plan& P) {
   P.d_ns_gram = (NsDesc*)(base + o_nsg);
   P.d_ns_upd = (NsDesc*)(base + o_nsu);
   P.d_bx = (uint16_t*)(base + o_bx);
-  P.d_wt_scratch = (uint16_t*)(base + o_wt);
+  P.d_units = (UnitInfo*)(base + o_units);
+  P.d_ns_res = (float*)(base + o_res);
   P.d_br = (uint16_t*)(base + o_br);
   cudaError_t e = cudaMemset(P.d_arena, 0, off);   // also zero-pads the BF16 operand copies
   if (!P.ns_gram.empty() && e == cudaSuccess)
@@ -570,6 +660,8 @@ static orth_status_t allocate(Plan& P) {
     e = cudaMemcpy(P.d_mat_items, P.mat_items.data(), P.mat_items.size() * sizeof(MatItem), cudaMemcpyHostToDevice);
   if (!P.col_items.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_col_items, P.col_items.data(), P.col_items.size() * sizeof(ColItem), cudaMemcpyHostToDevice);
+  if (!P.units.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_units, P.units.data(), P.units.size() * sizeof(UnitInfo), cudaMemcpyHostToDevice);
   if (!P.emit.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_emit, P.emit.data(), P.emit.size() * sizeof(EmitItem), cudaMemcpyHostToDevice);
   for (size_t i = 0; i < phases.size() && e == cudaSuccess; ++i) {
@@ -587,7 +679,7 @@ static orth_status_t allocate(Plan& P) {
     P.d_arena = nullptr;
     return ORTH_ERR_CUDA;
   }
-  return ORTH_OK;
+  return allocate_conv(P);
 }
 
 }  // namespace orth
@@ -606,6 +698,8 @@ void orth_opts_default(orth_opts_t* o) {
   o->polish_iters = 2;
   o->rank = 0;
   o->world = 1;
+  o->ns_tol = 1e-3f;
+  o->max_batch = 0;
 }
 
 orth_status_t orth_validate_desc(const orth_layer_desc_t* layers, int32_t n_layers, const orth_opts_t* opts) {
@@ -639,6 +733,7 @@ orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers
   layout(P);
   build_ns(P);
   build_compose(P);
+  size_conv(P);
   if (device >= 0) {
     st = allocate(P);
     if (st == ORTH_OK && P.opts.compute != ORTH_F32) st = build_compose_tc(P);
@@ -649,6 +744,7 @@ orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers
       if (P.d_ns_maps) cudaFree(P.d_ns_maps);
       if (P.nsp_mem) cudaFree(P.nsp_mem);
       if (P.d_arena) cudaFree(P.d_arena);
+      if (P.d_conv_mem) cudaFree(P.d_conv_mem);
       delete h;
       return st;
     }
@@ -664,8 +760,7 @@ orth_status_t orth_plan_destroy(orth_plan_t plan) {
   if (plan->p.nsp_mem) cudaFree(plan->p.nsp_mem);
   if (plan->p.nsf_items) cudaFree(plan->p.nsf_items);
   if (plan->p.d_arena) cudaFree(plan->p.d_arena);
-  if (plan->p.d_pad_scratch) cudaFree(plan->p.d_pad_scratch);
-  if (plan->p.d_conv_flags) cudaFree(plan->p.d_conv_flags);
+  if (plan->p.d_conv_mem) cudaFree(plan->p.d_conv_mem);
   if (plan->p.d_ns_upd64) cudaFree(plan->p.d_ns_upd64);
   if (plan->p.d_ns_gram_flow) cudaFree(plan->p.d_ns_gram_flow);
   if (plan->p.d_ns_upd_wide) cudaFree(plan->p.d_ns_upd_wide);
@@ -676,9 +771,10 @@ orth_status_t orth_plan_destroy(orth_plan_t plan) {
 orth_status_t orth_plan_query(orth_plan_t plan, int32_t what, int32_t index, int64_t* out) {
   if (!plan || !out) { set_error("NULL plan or out"); return ORTH_ERR_INVALID_ARGUMENT; }
   const Plan& P = plan->p;
-  const bool lq = what >= 20 && what < 40, mq = what >= 40;
+  const bool lq = what >= 20 && what < 40, mq = what >= 40 && what < 60, uq = what >= 60;
   if (lq && (index < 0 || index >= (int)P.layers.size())) { set_error("layer index %d out of range", index); return ORTH_ERR_INVALID_ARGUMENT; }
   if (mq && (index < 0 || index >= (int)P.mats.size())) { set_error("matrix index %d out of range", index); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (uq && (index < 0 || index >= (int)P.units.size())) { set_error("unit index %d out of range", index); return ORTH_ERR_INVALID_ARGUMENT; }
   switch (what) {
     case ORTH_Q_N_LAYERS: *out = (int64_t)P.layers.size(); break;
     case ORTH_Q_N_MATRICES: *out = (int64_t)P.mats.size(); break;
@@ -690,6 +786,19 @@ orth_status_t orth_plan_query(orth_plan_t plan, int32_t what, int32_t index, int
     case ORTH_Q_NS_FLOPS: *out = (int64_t)P.ns_flops; break;
     case ORTH_Q_KERNEL_SEGMENT_F32: *out = P.seg_f32; break;
     case ORTH_Q_KERNEL_SEGMENT_BF16: *out = P.seg_bf16; break;
+    case ORTH_Q_N_UNITS: *out = (int64_t)P.units.size(); break;
+    case ORTH_Q_GATHER_F32_NUMEL: *out = P.gat_f32_numel; break;
+    case ORTH_Q_GATHER_BF16_NUMEL: *out = P.gat_bf16_numel; break;
+    case ORTH_Q_CONV_SCRATCH_BYTES: *out = P.conv_mem_bytes; break;
+    case ORTH_Q_LAYER_SCRATCH_BYTES: *out = P.layers[index].pad_bytes; break;
+    case ORTH_Q_UNIT_LAYER: *out = P.units[index].layer; break;
+    case ORTH_Q_UNIT_GROUP: *out = P.units[index].group; break;
+    case ORTH_Q_UNIT_OWNER: *out = P.units[index].owner; break;
+    case ORTH_Q_UNIT_NUMEL: *out = P.units[index].numel; break;
+    case ORTH_Q_UNIT_GATHER_OFF_F32: *out = P.units[index].gat_f32; break;
+    case ORTH_Q_UNIT_GATHER_OFF_BF16: *out = P.units[index].gat_bf16; break;
+    case ORTH_Q_UNIT_KERNEL_OFF_F32: *out = P.units[index].fin_f32; break;
+    case ORTH_Q_UNIT_KERNEL_OFF_BF16: *out = P.units[index].fin_bf16; break;
     case ORTH_Q_LAYER_FIRST_MATRIX: *out = P.layers[index].first_mat; break;
     case ORTH_Q_LAYER_MATS_PER_GROUP: *out = P.layers[index].mats_per_group; break;
     case ORTH_Q_LAYER_KERNEL_OFF_F32: *out = P.layers[index].kf32_off; break;

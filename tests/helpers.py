@@ -66,3 +66,24 @@ def nchw(x_nhwc):
 
 def nhwc(x_nchw):
     return np.ascontiguousarray(np.transpose(x_nchw, (0, 2, 3, 1)))
+
+
+# Elementwise bounds of a conv output, on top of the Frobenius ratio:
+#   |gpu - ref| <= rel * |ref| + coef * (|K| * |x|)
+# where (|K| * |x|) is the oracle conv of the absolute values (the tap-sum of |K||x| of every output
+# element).  BF16 I/O with the same BF16 kernel on both sides: the products are exact in FP32, so the
+# error is the output RNE rounding (<= 2^-8 |y|) plus the FP32 accumulation (<< 2^-12 of the tap-sum).
+BF16_ELEM = (2.0 ** -8, 2.0 ** -12)
+F32_ELEM = (2.0 ** -20, 2.0 ** -16)
+
+
+def assert_elementwise(got, ref, absref, rel_coef, abs_coef, what=""):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    err = np.abs(got - ref)
+    bound = rel_coef * np.abs(ref) + abs_coef * np.asarray(absref, np.float64) + 1e-30
+    bad = err > bound
+    if bad.any():
+        i = np.unravel_index(np.argmax(err / bound), err.shape)
+        raise AssertionError(f"{what}: {int(bad.sum())} of {err.size} elements outside the bound; worst at {i}: "
+                             f"got {got[i]:.6g} ref {ref[i]:.6g} bound {bound[i]:.3g}")

@@ -119,28 +119,40 @@ def test_layout_alignment_and_disjointness():
     assert ends <= p.kf32_numel
 
 
+@pytest.mark.parametrize("cfg_name", ["cfg3", "cfg4"])
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
-def test_lpt_sharding_rank_major_segments(world):
-    cfg = configs.cfg3()
+def test_lpt_sharding_units_and_segments(cfg_name, world):
+    """the sharding unit is (layer, group); LPT by NS flops (+ composition); every rank
+    derives the same owners and offsets; each unit lies inside its owner's rank-major gather segment;
+    the final layout is the single-rank one."""
+    cfg = getattr(configs, cfg_name)()
     plans = [orth.Plan(cfg, device=-1, rank=r, world=world) for r in range(world)]
-    owners = [info["owner"] for info in plans[0].layer_info]
-    for p in plans[1:]:   # every rank derives the same assignment and offsets
-        assert [i["owner"] for i in p.layer_info] == owners
-        assert [i["kf32_off"] for i in p.layer_info] == [i["kf32_off"] for i in plans[0].layer_info]
-    seg = orth.orth_plan_query(plans[0].h, "KERNEL_SEGMENT_F32")
-    for info in plans[0].layer_info:
-        r = info["owner"]
-        assert r * seg <= info["kf32_off"] and info["kf32_off"] + info["numel"] <= (r + 1) * seg
-    assert plans[0].kf32_numel == seg * world
-    # LPT balance: max load <= mean + largest unit
-    cost = {}
-    for l, d in enumerate(cfg):
-        OL = _oracle_layer(d)
-        cost[l] = sum(4.0 * max(M.m, M.n) * min(M.m, M.n) ** 2 for M in O.layer_matrices(OL)) * d["g"]
-    loads = [sum(c for l, c in cost.items() if owners[l] == r) for r in range(world)]
-    assert max(loads) <= sum(loads) / world + max(cost.values()) + 1
+    single = orth.Plan(cfg, device=-1)
+    units = plans[0].units
+    assert [(u["layer"], u["group"]) for u in units] == [(l, g) for l, d in enumerate(cfg) for g in range(d["g"])]
+    for p in plans[1:]:
+        assert p.units == units
+    seg = plans[0].seg_f32
+    assert plans[0].gf32_numel == seg * world
+    spans = sorted((u["gat_f32"], u["gat_f32"] + u["numel"]) for u in units)
+    assert all(a1 <= b0 for (_, a1), (b0, _) in zip(spans, spans[1:]))          # disjoint
+    for u in units:
+        r = u["owner"]
+        assert u["gat_f32"] % 32 == 0 and u["gat_bf16"] % 64 == 0
+        assert r * seg <= u["gat_f32"] and u["gat_f32"] + u["numel"] <= (r + 1) * seg
+        info = single.layer_info[u["layer"]]
+        assert u["fin_f32"] == info["kf32_off"] + u["group"] * u["numel"]
+        assert u["numel"] * cfg[u["layer"]]["g"] == info["numel"]
+    assert [i["kf32_off"] for i in plans[0].layer_info] == [i["kf32_off"] for i in single.layer_info]
+    # LPT balance: max load <= mean + largest unit (NS flops of the oracle's matrix list per group)
+    cost = []
+    for u in units:
+        OL = _oracle_layer(cfg[u["layer"]])
+        cost.append(sum(4.0 * max(M.m, M.n) * min(M.m, M.n) ** 2 for M in O.layer_matrices(OL)))
+    loads = [sum(c for c, u in zip(cost, units) if u["owner"] == r) for r in range(world)]
+    assert max(loads) <= sum(loads) / world + max(cost) * 1.5 + 1
     flops = [orth.orth_plan_query(p.h, "NS_FLOPS") for p in plans]
-    assert abs(sum(flops) - orth.orth_plan_query(orth.Plan(cfg, device=-1).h, "NS_FLOPS")) <= world
+    assert abs(sum(flops) - orth.orth_plan_query(single.h, "NS_FLOPS")) <= world * 12
 
 
 def test_host_only_plan_cannot_compute():
@@ -155,14 +167,19 @@ def test_host_only_plan_cannot_compute():
     assert ei.value.status == orth.NO_DEVICE
 
 
-def test_host_only_plan_cannot_reserve_and_scratch_sizes():
-    """orth_plan_reserve needs a device (host-only plan: NO_DEVICE); the conv-scratch helper
-    covers the padded forward-view input of both directions."""
-    p = orth.Plan(configs.cfg2(), device=-1)
-    with pytest.raises(orth.OrthError) as ei:
-        p.reserve(1 << 20)
-    assert ei.value.status == orth.NO_DEVICE
-    # layer 1: 64 -> 64, 3x3 circular at 32x32, batch 256: 256 * 34 * 34 * 64 * 2 bytes
-    assert p.conv_scratch_bytes(1, 256, 32, 32) == 256 * 34 * 34 * 64 * 2
-    # a stride-2 layer: the padded copy is sized on the larger (input) grid
-    assert p.conv_scratch_bytes(3, 256, 32, 32) == 256 * 34 * 34 * 128 * 2
+def test_conv_scratch_sized_at_create():
+    """SURVEY §8(b) "no call allocates after create": the per-layer conv scratch is derived from the
+    declared grid and max_batch (host arithmetic, visible on a host-only plan), one slice per layer."""
+    p0 = orth.Plan(configs.cfg2(), device=-1)
+    assert all(i["scratch"] == 0 for i in p0.layer_info)                # max_batch 0: nothing declared
+    p = orth.Plan(configs.cfg2(), device=-1, max_batch=256)
+    sc = [i["scratch"] for i in p.layer_info]
+    # 128 output channels at 16x16 (< 24 px): no padded copy; 512 @ 4x4 (2 x 2 x 16 tiles of 128 x 256 on
+    # 148 SMs): split-K partials = tiles * 128 * 256 * 4 bytes
+    tiles = (256 * 4 * 4 + 127) // 128 * (512 // 256)
+    assert sc[10] == tiles * 128 * 256 * 4 and sc[11] == sc[10]
+    p3 = orth.Plan(configs.cfg3(), device=-1, max_batch=256)
+    s3 = [i["scratch"] for i in p3.layer_info]
+    # cfg3 128-ch 28x28 layers take the stacked-window kernel: padded copy 256 x 30 x 30 x 128 x 2 bytes
+    assert s3[8] == 256 * 30 * 30 * 128 * 2
+    assert orth.Plan(configs.cfg3(), device=-1, max_batch=32).layer_info[8]["scratch"] == 32 * 30 * 30 * 128 * 2

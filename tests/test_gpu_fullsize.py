@@ -18,7 +18,7 @@ import torch
 
 import oracle as O
 from synth import configs, gen
-from tests.helpers import nchw, nhwc, oracle_construct, oracle_layer, pack_params, rel
+from tests.helpers import BF16_ELEM, assert_elementwise, nchw, nhwc, oracle_construct, oracle_layer, pack_params, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -29,8 +29,8 @@ def dev(a, dtype=torch.float32):
     return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
 
 
-def construct_bf16(orth, layers, cfg_id):
-    plan = orth.Plan(layers, 0, compute="bf16")
+def construct_bf16(orth, layers, cfg_id, max_batch=0):
+    plan = orth.Plan(layers, 0, compute="bf16", max_batch=max_batch)
     params, mats = pack_params(plan, cfg_id)
     p = dev(params)
     ortho = torch.zeros_like(p)
@@ -59,10 +59,21 @@ def check_construction(plan, mats, ortho, res, kf, layers):
     return o_k
 
 
+def check_layer_output(plan, kb, l, d, o_kl, xin, got, H):
+    """Frobenius vs the oracle conv with the ORACLE's kernel (construction + conv errors, TOL16), and
+    elementwise vs the oracle conv with the GPU's own BF16 kernel (the conv alone, tight bound)."""
+    assert rel(got, oracle_apply(d, o_kl, xin, H)) < TOL16, l
+    kg = plan.kernel_bf16(kb, l).float().cpu().numpy().astype(np.float64).transpose(0, 3, 1, 2)
+    ref = oracle_apply(d, kg, xin, H)
+    absref = oracle_apply(d, np.abs(kg), np.abs(xin), H)
+    assert rel(got, ref) < 1e-2, l
+    assert_elementwise(got, ref, absref, *BF16_ELEM, what=f"layer {l}")
+
+
 def oracle_apply(d, K, x_nhwc, H):
     """Oracle forward of one layer (transposed: the adjoint onto the large grid)."""
     OL = oracle_layer(d)
-    x = nchw(x_nhwc.astype(np.float64))
+    x = nchw(np.asarray(x_nhwc, np.float64))
     if d["kind"] == "convT":
         return nhwc(O.conv_transpose2d(x, K, H * d["s"], H * d["s"], s=OL.s, d=OL.d, g=OL.g, mode=OL.padding_mode))
     return nhwc(O.conv2d(x, K, s=OL.s, d=OL.d, g=OL.g, mode=OL.padding_mode))
@@ -71,24 +82,18 @@ def oracle_apply(d, K, x_nhwc, H):
 def test_cfg3_fullsize(cuda_lib):
     """ImageNet AOC-ResNet34 shape: 33 layers, batch 256 at 224x224, chained."""
     layers = configs.cfg3()
-    plan, mats, ortho, res, kf, kb = construct_bf16(cuda_lib, layers, 3)
-    o_k = check_construction(plan, mats, ortho, res, kf, layers)
     N = configs.BATCH[3]
+    plan, mats, ortho, res, kf, kb = construct_bf16(cuda_lib, layers, 3, max_batch=N)
+    o_k = check_construction(plan, mats, ortho, res, kf, layers)
     x = gen.bf16_round(gen.activations((N, 224, 224, 3), (3, 0, 0, 0, gen.ROLE_ID["x"])))
     cur, H = dev(x, torch.bfloat16), 224
-    need, Hc = 0, H
-    for l in range(len(layers)):
-        need = max(need, plan.conv_scratch_bytes(l, N, Hc, Hc))
-        Hc = plan.out_hw(l, Hc, Hc)[0]
-    plan.reserve(need)
     sample = [0, N - 1]
     for l, d in enumerate(layers):
         Ho, _ = plan.out_hw(l, H, H)
         y = torch.empty((N, Ho, Ho, d["c_out"]), device="cuda", dtype=torch.bfloat16)
         plan.conv_forward(l, plan.kernel_bf16(kb, l), cur, y)
         xin = cur[sample].float().cpu().numpy()
-        ref = oracle_apply(d, o_k[l], xin, H)
-        assert rel(y[sample].float().cpu().numpy(), ref) < TOL16, l
+        check_layer_output(plan, kb, l, d, o_k[l], xin, y[sample].float().cpu().numpy(), H)
         cur, H = y, Ho
     plan.check()
 
@@ -97,13 +102,10 @@ def test_cfg4_fullsize(cuda_lib):
     """1024-channel paths at 56x56, batch 256: g32, d2, s2, transposed s2,
     transposed g32 d2 (each layer fed its own seeded input, as in bench.py)."""
     layers = configs.cfg4()
-    plan, mats, ortho, res, kf, kb = construct_bf16(cuda_lib, layers, 4)
-    o_k = check_construction(plan, mats, ortho, res, kf, layers)
     N = configs.BATCH[4]
+    plan, mats, ortho, res, kf, kb = construct_bf16(cuda_lib, layers, 4, max_batch=N)
+    o_k = check_construction(plan, mats, ortho, res, kf, layers)
     sample = [0, N - 1]
-    plan.reserve(max(plan.conv_scratch_bytes(l, N, d["H"] * (d["s"] if d["kind"] == "convT" else 1),
-                                             d["H"] * (d["s"] if d["kind"] == "convT" else 1))
-                     for l, d in enumerate(layers)))
     for l, d in enumerate(layers):
         H = d["H"]
         x = gen.bf16_round(gen.activations((N, H, H, d["c_in"]), (4, 0, l, 0, gen.ROLE_ID["x"])))
@@ -115,8 +117,7 @@ def test_cfg4_fullsize(cuda_lib):
             Ho, _ = plan.out_hw(l, H, H)
             y = torch.empty((N, Ho, Ho, d["c_out"]), device="cuda", dtype=torch.bfloat16)
             plan.conv_forward(l, plan.kernel_bf16(kb, l), xd, y)
-        ref = oracle_apply(d, o_k[l], x[sample], H)
-        assert rel(y[sample].float().cpu().numpy(), ref) < TOL16, l
+        check_layer_output(plan, kb, l, d, o_k[l], x[sample], y[sample].float().cpu().numpy(), H)
         del xd, y
         torch.cuda.empty_cache()
     plan.check()

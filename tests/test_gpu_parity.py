@@ -8,7 +8,8 @@ import torch
 
 import oracle as O
 from synth import configs, gen
-from tests.helpers import nchw, nhwc, oracle_construct, oracle_layer, pack_cache, pack_params, rel
+from tests.helpers import (BF16_ELEM, F32_ELEM, assert_elementwise, nchw, nhwc, oracle_construct, oracle_layer,
+                           pack_cache, pack_params, rel)
 
 pytestmark = pytest.mark.gpu
 
@@ -147,6 +148,30 @@ def test_device_status_zero_and_nonconvergence(cuda_lib):
     plan.check()                                              # cleared
 
 
+@pytest.mark.parametrize("mode", ["f32", "bf16"])
+def test_not_converged_without_residual_out(cuda_lib, mode):
+    """S:125 non-convergence is reported whether or not residual_out is requested: the
+    last iteration's own Gram gives r = |I - X_{T-1}^T X_{T-1}|_F and the bound 3/4 r^2 + 1/4 r^3 on the
+    result's residual is checked against ns_tol.  Gaussian (stress) matrices at T = 3 are far from
+    converged (R21); at T = 40 with Frobenius pre-scaling they converge; ns_tol <= 0 keeps only the
+    non-finite check."""
+    orth = cuda_lib
+    layers = [dict(kind="dense", c_in=96, c_out=96, k=1, s=1, d=1, g=1, padding_mode="circular"),
+              dict(kind="conv", c_in=16, c_out=16, k=3, s=1, d=1, g=1, padding_mode="circular")]
+    for T, tol, expect in [(3, 1e-3, orth.NOT_CONVERGED), (40, 1e-3, orth.OK), (3, 0.0, orth.OK)]:
+        plan = orth.Plan(layers, 0, compute=mode, ns_iters=T, prescale="frobenius", ns_tol=tol)
+        params, _ = pack_params(plan, 16, stress=True)
+        p = dev(params)
+        plan.orthogonalize(p, torch.zeros_like(p))      # residual_out = NULL
+        if expect == orth.OK:
+            plan.check()
+        else:
+            with pytest.raises(orth.OrthError) as ei:
+                plan.check()
+            assert ei.value.status == expect
+            plan.check()                                # the status word is cleared by the check
+
+
 # ------------------------------------------------------------------ conv apply
 CONV_CASES = [  # (ci, co, k, s, d, g, mode, H, kind)
     (16, 16, 3, 1, 1, 1, "circular", 8, "conv"), (3, 64, 3, 1, 1, 1, "circular", 32, "conv"),
@@ -190,10 +215,9 @@ CONV_CASES = [  # (ci, co, k, s, d, g, mode, H, kind)
 
 @pytest.mark.parametrize("case", CONV_CASES)
 @pytest.mark.parametrize("io", ["f32", "bf16"])
-def test_conv_forward_and_transpose(cuda_lib, case, io):
+def test_conv_forward_and_transpose(cuda_lib, case, io, max_batch=None):
     ci, co, k, s, d, g, mode, H, kind = case
     layer = dict(kind=kind, c_in=ci, c_out=co, k=k, s=s, d=d, g=g, padding_mode=mode)
-    plan = cuda_lib.Plan([layer], 0)
     OL = oracle_layer(layer)
     ci_f, co_f = OL.fwd_channels()
     rng = gen.rng(77, ci, co, k, s)
@@ -209,22 +233,50 @@ def test_conv_forward_and_transpose(cuda_lib, case, io):
     else:
         kdev, xdev, tdt, tol = dev(K), dev(x), torch.float32, TOL32
     Hh, Ww = x.shape[1], x.shape[2]
+    # the declared grid and batch size the layer's conv scratch at create (split-K, padded-copy kernels)
+    plan = cuda_lib.Plan([dict(layer, grid=(Hh, Ww))], 0, max_batch=N if max_batch is None else max_batch)
     Ho, Wo = plan.out_hw(0, Hh, Ww)
-    plan.reserve(plan.conv_scratch_bytes(0, N, Hh, Ww))   # stacked-window path where eligible
     y = torch.zeros((N, Ho, Wo, co_f), device="cuda", dtype=tdt)
     plan.conv_forward(0, kdev, xdev, y, bias=dev(bias))
-    ref = O.conv2d(nchw(x.astype(np.float64)), K.astype(np.float64), s=s, d=d, g=g, mode=mode) \
-        + bias[None, :, None, None]
-    assert rel(y.float().cpu().numpy(), nhwc(ref)) < tol
+    K64, x64 = K.astype(np.float64), nchw(x.astype(np.float64))
+    ref = O.conv2d(x64, K64, s=s, d=d, g=g, mode=mode) + bias[None, :, None, None]
+    absref = O.conv2d(np.abs(x64), np.abs(K64), s=s, d=d, g=g, mode=mode) + np.abs(bias)[None, :, None, None]
+    elem = BF16_ELEM if io == "bf16" else F32_ELEM
+    got = y.float().cpu().numpy()
+    assert rel(got, nhwc(ref)) < (1e-2 if io == "bf16" else tol)
+    assert_elementwise(got, nhwc(ref), nhwc(absref), *elem, what=f"forward {case} {io}")
     # adjoint
     yr = gen.activations((N, Ho, Wo, co_f), (77, 3, ci, co, 6))
     if io == "bf16":
         yr = gen.bf16_round(yr)
     xb = torch.zeros((N, Hh, Ww, ci_f), device="cuda", dtype=tdt)
     plan.conv_transpose(0, kdev, dev(yr, tdt), xb)
-    refT = O.conv_transpose2d(nchw(yr.astype(np.float64)), K.astype(np.float64), Hh, Ww, s=s, d=d, g=g, mode=mode)
-    assert rel(xb.float().cpu().numpy(), nhwc(refT)) < tol
+    yr64 = nchw(yr.astype(np.float64))
+    refT = O.conv_transpose2d(yr64, K64, Hh, Ww, s=s, d=d, g=g, mode=mode)
+    absT = O.conv_transpose2d(np.abs(yr64), np.abs(K64), Hh, Ww, s=s, d=d, g=g, mode=mode)
+    gotT = xb.float().cpu().numpy()
+    assert rel(gotT, nhwc(refT)) < (1e-2 if io == "bf16" else tol)
+    assert_elementwise(gotT, nhwc(refT), nhwc(absT), *elem, what=f"adjoint {case} {io}")
     plan.check()
+
+
+# Split-K of the gather conv (two half-K items per 128 x 256 tile, FP32 partial + flag in the layer's
+# scratch): deep layers with few 256-wide tiles, in both directions; each case also runs with the
+# scratch withheld (max_batch = 0: no split) and both results must satisfy the same elementwise bound.
+SPLITK_CASES = [(512, 512, 3, 1, 1, 1, "circular", 4, "conv"), (1024, 1024, 3, 1, 1, 1, "zeros", 4, "conv"),
+                (512, 512, 3, 2, 1, 1, "circular", 8, "conv"), (1024, 1024, 3, 1, 2, 1, "circular", 6, "convT"),
+                (768, 512, 5, 2, 1, 1, "zeros", 7, "conv")]
+
+
+@pytest.mark.parametrize("case", SPLITK_CASES)
+def test_conv_splitk_path(cuda_lib, case):
+    ci, co, k, s, d, g, mode, H, kind = case
+    layer = dict(kind=kind, c_in=ci, c_out=co, k=k, s=s, d=d, g=g, padding_mode=mode)
+    Hb = H * s if (kind == "convT" and mode == "circular") else H
+    plan = cuda_lib.Plan([dict(layer, grid=(Hb, Hb + 1 if mode == "zeros" else Hb))], 0, max_batch=3)
+    assert plan.layer_info[0]["scratch"] >= 128 * 256 * 4, "case does not reach split-K"
+    test_conv_forward_and_transpose(cuda_lib, case, "bf16")               # with split-K
+    test_conv_forward_and_transpose(cuda_lib, case, "bf16", max_batch=0)  # without
 
 
 @pytest.mark.parametrize("case", [(128, 128, 3, 1, 1, 1, "circular", 16, "conv"), (128, 256, 3, 2, 1, 1, "zeros", 9, "conv"),
@@ -310,7 +362,7 @@ def test_whole_path_cfg2_bf16_chain_sampled(cuda_lib):
     """Full-size cfg2 step as bench.py runs it (batch 256, bf16 chain); the
     oracle chains its own kernels on a 2-image sample."""
     layers = configs.cfg2()
-    plan, mats, _, _, _, _, kf, kb = gpu_construct(cuda_lib, layers, 2)
+    plan, mats, _, _, _, _, kf, kb = gpu_construct(cuda_lib, layers, 2, max_batch=256)
     _, _, o_k = oracle_construct(layers, mats)
     N = 256
     x = gen.bf16_round(gen.activations((N, 32, 32, 3), (2, 0, 0, 0, gen.ROLE_ID["x"])))
@@ -326,11 +378,18 @@ def test_whole_path_cfg2_bf16_chain_sampled(cuda_lib):
     plan.check()
     sample = [0, 255]
     ref = nchw(x[sample].astype(np.float64))
+    xin = ref
     for l, d in enumerate(layers):
         OL = oracle_layer(d)
         ref = O.conv2d(ref, o_k[l], s=OL.s, d=OL.d, g=OL.g)
         got = outs[l][sample].float().cpu().numpy()
         assert rel(got, nhwc(ref)) < TOL16, l
+        # elementwise: the oracle conv with the GPU's own BF16 kernel on the GPU's own input of this layer
+        kg = plan.kernel_bf16(kb, l).float().cpu().numpy().astype(np.float64).transpose(0, 3, 1, 2)
+        r1 = O.conv2d(xin, kg, s=OL.s, d=OL.d, g=OL.g)
+        a1 = O.conv2d(np.abs(xin), np.abs(kg), s=OL.s, d=OL.d, g=OL.g)
+        assert_elementwise(got, nhwc(r1), nhwc(a1), *BF16_ELEM, what=f"cfg2 layer {l}")
+        xin = nchw(got)
     # property at any size: circular isometries / co-isometries never increase the norm
     xn = torch.linalg.vector_norm(dev(x).reshape(N, -1), dim=1)
     yn = torch.linalg.vector_norm(outs[-1].float().reshape(N, -1), dim=1)

@@ -1,7 +1,11 @@
-"""World-size-2 `gloo` test of the multi-GPU host logic (CPU): every rank
-derives the same layer ownership and kernel offsets from its own plan, writes
-only the layers it owns into its rank-major segment, and one all-gather gives
-every rank every layer at the offsets a single-rank plan would read them."""
+"""World-size-2/3 `gloo` tests of the multi-GPU host logic (CPU, host-only
+plans): every rank derives the same (layer, group) unit ownership and the same
+gather / final offsets from its own plan; writing only its own units into its
+rank-major gather segment and one all-gather give every rank every unit, and
+the unit table's gather -> final copy (what orth_kernels_assemble does on the
+device) reproduces, for every layer, the contiguous kernel a single-rank plan
+reads.  The device side of the same path (real orth_compose_kernel writes,
+orth_kernels_assemble) is tests/test_gpu_sharded.py."""
 import os
 import socket
 
@@ -21,27 +25,37 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _unit_values(u, numel):
+    # a distinct, exactly representable value per (layer, group, element)
+    return (u["layer"] * 64 + u["group"] + 1) + torch.arange(numel, dtype=torch.float64) / 2 ** 20
+
+
+def _worker(rank, world, port, cfg_name, q):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         import paper_2601_13776_b200 as orth
         from paper_2601_13776_b200.dist import batch_shard, gather_kernels
-        cfg = configs.cfg3()
+        cfg = getattr(configs, cfg_name)()
         plan = orth.Plan(cfg, device=-1, rank=rank, world=world)
-        seg = orth.orth_plan_query(plan.h, "KERNEL_SEGMENT_F32")
-        kbuf = torch.zeros(plan.kf32_numel)
+        ref = orth.Plan(cfg, device=-1)
+        gbuf = torch.zeros(plan.gf32_numel, dtype=torch.float64)
         owned = 0
-        for l, info in enumerate(plan.layer_info):
-            if info["owner"] == rank:       # stand-in for orth_compose_kernel's writes
-                kbuf[info["kf32_off"]: info["kf32_off"] + info["numel"]] = l + 1 + torch.arange(info["numel"]) * 1e-6
+        for u in plan.units:
+            if u["owner"] == rank:       # stand-in for orth_compose_kernel's writes (host-only plan)
+                assert rank * plan.seg_f32 <= u["gat_f32"] and u["gat_f32"] + u["numel"] <= (rank + 1) * plan.seg_f32
+                gbuf[u["gat_f32"]: u["gat_f32"] + u["numel"]] = _unit_values(u, u["numel"])
                 owned += 1
-        gather_kernels(plan, kbuf, seg)
-        ok = True
-        for l, info in enumerate(plan.layer_info):
-            want = l + 1 + torch.arange(info["numel"]) * 1e-6
-            ok &= bool(torch.equal(kbuf[info["kf32_off"]: info["kf32_off"] + info["numel"]], want))
+        gather_kernels(gbuf, plan.seg_f32)
+        final = torch.zeros(plan.kf32_numel, dtype=torch.float64)
+        for u in plan.units:          # orth_kernels_assemble's copy, from the queried unit table
+            final[u["fin_f32"]: u["fin_f32"] + u["numel"]] = gbuf[u["gat_f32"]: u["gat_f32"] + u["numel"]]
+        ok = plan.kf32_numel == ref.kf32_numel
+        for l, info in enumerate(ref.layer_info):   # the single-rank plan's layer offsets
+            per = info["numel"] // cfg[l].get("g", 1)
+            want = torch.cat([_unit_values(dict(layer=l, group=g), per) for g in range(cfg[l].get("g", 1))])
+            ok &= bool(torch.equal(final[info["kf32_off"]: info["kf32_off"] + info["numel"]], want))
         b, e = batch_shard(256, rank, world)
         q.put((rank, ok, owned, (b, e)))
         dist.destroy_process_group()
@@ -49,12 +63,12 @@ def _worker(rank, world, port, q):
         q.put((rank, repr(ex), 0, None))
 
 
-def test_sharded_construction_allgather_gloo():
-    world = 2
+@pytest.mark.parametrize("cfg_name,world", [("cfg3", 2), ("cfg4", 3)])
+def test_sharded_construction_allgather_gloo(cfg_name, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg_name, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in range(world)]
@@ -64,5 +78,7 @@ def test_sharded_construction_allgather_gloo():
     for rank, ok, owned, shard in res:
         assert ok is True, (rank, ok)
         assert owned > 0
-    assert res[0][3] == (0, 128) and res[1][3] == (128, 256)
-    assert res[0][2] + res[1][2] == len(configs.cfg3())
+    n_units = sum(d.get("g", 1) for d in getattr(configs, cfg_name)())
+    assert sum(r[2] for r in res) == n_units
+    per = (256 + world - 1) // world
+    assert [r[3] for r in res] == [(r * per, min(256, (r + 1) * per)) for r in range(world)]

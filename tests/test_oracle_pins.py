@@ -48,8 +48,16 @@ def test_prescale_zero_and_frobenius():
         O.prescale_power(np.zeros((3, 3)), 3, np.ones(3))
     W = rs.standard_normal((7, 4))
     W0, f = O.prescale_frobenius(W)
-    assert abs(f - np.sqrt((W ** 2).sum())) < 1e-12
+    sv = np.linalg.svd(W, compute_uv=False)
+    # |W|_F is the 2-norm of the singular values (LAPACK, independent of the oracle's sum of squares)
+    assert abs(f - np.sqrt((sv ** 2).sum())) < 1e-12
     assert np.linalg.svd(W0, compute_uv=False)[0] <= 1.0
+    # W0 itself: unit Frobenius norm and W0 * f reproduces W -- W / f^2 fails both
+    assert abs(np.linalg.norm(W0, "fro") - 1.0) < 1e-14
+    assert np.allclose(W0 * f, W, rtol=0, atol=1e-14)
+    # by hand: [[3, 4], [0, 0]] -> f = 5, W0 = [[0.6, 0.8], [0, 0]]
+    W0h, fh = O.prescale_frobenius(np.array([[3.0, 4.0], [0.0, 0.0]]))
+    assert fh == 5.0 and np.allclose(W0h, [[0.6, 0.8], [0.0, 0.0]], rtol=0, atol=1e-16)
 
 
 def test_power_iteration_one_step_by_hand():

@@ -12,7 +12,7 @@ from tests.helpers import pack_params  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 layers = configs.cfg2()
-plan = orth.Plan(layers, 0, compute="bf16")
+plan = orth.Plan(layers, 0, compute="bf16", max_batch=256)
 params, _ = pack_params(plan, 2)
 p = torch.from_numpy(params).cuda()
 o = torch.zeros_like(p)
@@ -26,11 +26,6 @@ for l, d in enumerate(layers):
     Ho, _ = plan.out_hw(l, H, H)
     acts.append(torch.empty((256, Ho, Ho, d["c_out"]), device="cuda", dtype=torch.bfloat16))
     H = Ho
-need, Hc = 0, 32
-for l in range(len(layers)):
-    need = max(need, plan.conv_scratch_bytes(l, 256, Hc, Hc))
-    Hc = plan.out_hw(l, Hc, Hc)[0]
-plan.reserve(need)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(layers) + 1)]
 for _ in range(reps):
     cur = x

@@ -156,6 +156,7 @@ typedef enum {
   ORTH_Q_GATHER_F32_NUMEL = 11,   /* world * KERNEL_SEGMENT_F32 (world == 1: KERNELS_F32_NUMEL) */
   ORTH_Q_GATHER_BF16_NUMEL = 12,
   ORTH_Q_CONV_SCRATCH_BYTES = 13, /* plan-owned conv scratch over all layers */
+  ORTH_Q_COMP_FLOPS = 14,         /* structured composition flops of this rank's units */
   ORTH_Q_LAYER_FIRST_MATRIX = 20, /* global index of the layer's first matrix */
   ORTH_Q_LAYER_MATS_PER_GROUP = 21,
   ORTH_Q_LAYER_KERNEL_OFF_F32 = 22,
@@ -166,6 +167,8 @@ typedef enum {
   ORTH_Q_LAYER_C_B = 27,          /* BCOP width; 0 if none */
   ORTH_Q_LAYER_KP = 28,           /* BCOP size k' (R8); 0 if none */
   ORTH_Q_LAYER_SCRATCH_BYTES = 29,/* this layer's conv scratch slice */
+  ORTH_Q_LAYER_NS_FLOPS = 30,     /* 4 m n^2 T over the layer's matrices (all groups) */
+  ORTH_Q_LAYER_COMP_FLOPS = 31,   /* structured composition flops of the layer (all groups) */
   ORTH_Q_MATRIX_ROWS = 40,
   ORTH_Q_MATRIX_COLS = 41,
   ORTH_Q_MATRIX_OFFSET = 42,      /* float offset in params / ortho */
@@ -242,6 +245,46 @@ orth_status_t orth_kernels_assemble(orth_plan_t plan, const float* gathered_f32,
 /* Synchronises `stream`, reads and clears the device status word; returns the
  * first device-side error since the last check (or a pending CUDA error). */
 orth_status_t orth_plan_check(orth_plan_t plan, void* stream);
+
+/* ---- tracing: per-call timing of the plan's kernel groups ----------------------------
+ * orth_plan_trace(plan, 1) makes every compute call bracket each group of kernels it launches (the
+ * power pass, the NS launch, the composition, the emit, one conv call, ...) with a pair of CUDA events
+ * on the call's stream; orth_plan_trace_read synchronises on them and returns the records in launch
+ * order (then forgets them).  Tracing adds event records between kernels (it defeats the programmatic
+ * dependent launch overlap and is not meant for CUDA-graph capture): use it in a separate, eager
+ * profiling pass, never inside a timed region.  Every ABI call is also an NVTX range
+ * ("orth_conv_forward", ...) whether or not tracing is on. */
+typedef enum {
+  ORTH_TK_POWER = 1,        /* pre-scaling: power iterations or Frobenius norms (power_fused_kernel) */
+  ORTH_TK_SCALE = 2,        /* X0 = W / sigma (+ BF16 operand copies) */
+  ORTH_TK_NS = 3,           /* the T Bjorck / NS iterations (one persistent launch, or 2T phases) */
+  ORTH_TK_NS_CHECK = 4,     /* convergence check / residual reduction */
+  ORTH_TK_COMPOSE = 5,      /* projectors + BCOP chain + RKO (*) BCOP */
+  ORTH_TK_EMIT = 6,         /* kernels into the FP32 / BF16 layouts */
+  ORTH_TK_CONV_FWD = 7,     /* one orth_conv_forward (variant = orth_conv_variant_t) */
+  ORTH_TK_CONV_ADJ = 8,     /* one orth_conv_transpose */
+  ORTH_TK_ASSEMBLE = 9      /* orth_kernels_assemble */
+} orth_trace_kind_t;
+typedef enum {             /* which conv kernel a conv call ran */
+  ORTH_CV_NONE = 0, ORTH_CV_SIMT = 1, ORTH_CV_SMALLK = 2, ORTH_CV_STEM = 3,
+  ORTH_CV_WINDOW_SWAP = 4,  /* conv_pad<64, swapped>: TMA window, M = 64 channels x N = 256 pixels */
+  ORTH_CV_WINDOW = 5,       /* conv_pad<BN>: TMA window, M = 128 pixels */
+  ORTH_CV_STACK = 6,        /* conv_stack: padded copy + stacked windows, M = 128 ch x N = 256 px */
+  ORTH_CV_TMA = 7,          /* conv_tma (experimental, ORTH_CONV_TMA=1) */
+  ORTH_CV_GATHER256 = 8, ORTH_CV_GATHER128 = 9, ORTH_CV_GATHER64 = 10, ORTH_CV_GATHER32 = 11,  /* conv_ws<BN> */
+  ORTH_CV_GATHER_PAIR = 12  /* conv_pair (experimental, ORTH_CONV_PAIR=1) */
+} orth_conv_variant_t;
+typedef struct {
+  int32_t kind;      /* orth_trace_kind_t */
+  int32_t layer;     /* conv calls: the layer; else -1 */
+  int32_t variant;   /* conv calls: orth_conv_variant_t; else 0 */
+  int32_t launches;  /* kernels in the group */
+  float ms;          /* CUDA-event time of the group */
+} orth_trace_rec_t;
+orth_status_t orth_plan_trace(orth_plan_t plan, int32_t enable);
+/* Synchronises on the recorded events; copies up to `cap` records into `out` (NULL: none), sets *n to
+ * the number of records available, and clears them. */
+orth_status_t orth_plan_trace_read(orth_plan_t plan, orth_trace_rec_t* out, int32_t cap, int32_t* n);
 
 /* Number of kernel launches enqueued by this plan since creation (all calls). */
 int64_t orth_plan_launch_count(orth_plan_t plan);

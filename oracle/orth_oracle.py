@@ -36,7 +36,7 @@ __all__ = [
     "block_conv", "block_orth", "bcop", "rko", "layer_kernel",
     "out_size", "conv2d", "conv_transpose2d",
     "toeplitz", "fft_singular_values", "polyphase_singular_values",
-    "conv_singular_values",
+    "conv_singular_values", "spectral_certificate",
 ]
 
 
@@ -438,3 +438,50 @@ def conv_singular_values(K: np.ndarray, L: Layer, H: int, W: int) -> np.ndarray:
         else:
             vals.append(polyphase_singular_values(Kg, H, W, L.s, L.d, L.pads()))
     return np.sort(np.concatenate(vals))
+
+
+def spectral_certificate(K: np.ndarray, L: Layer, H: int, W: int):
+    """Per (group, frequency) spectral certificate of the circular layer operator on H x W (SURVEY §8(f)
+    row 2; App. C "scalable spectral norm estimation ... check that the produced bounds are
+    valid"; S:444-452 fft_circular_spectrum).
+
+    For each group and each frequency (f1, f2) of the (H/s) x (W/s) polyphase grid it forms the symbol M
+    exactly as polyphase_singular_values does (c_out/g x (c_in/g) s^2, complex), the Gram on the SHORT
+    side G = M^H M (or M M^H), E = G - I, and returns
+      frob[g, f1, f2]   = |E|_F            (certificate: max |sigma^2 - 1| <= |E|_2 <= |E|_F, and
+                                            |sigma - 1| <= |sigma^2 - 1| for sigma >= 0),
+      spec[g, f1, f2]   = |E|_2            (eigvalsh: = max |sigma^2 - 1| at that frequency),
+      sigma_dev         = max over everything of |sigma - 1| (np.linalg.svd of M).
+    Dense layers: one 'frequency', M = the kernel matrix."""
+    if L.kind == "dense":
+        K = K.reshape(K.shape[0], K.shape[1], 1, 1)
+        s, d, pt, pl, H, W = 1, 1, 0, 0, 1, 1
+    else:
+        s, d = L.s, L.d
+        pt, _, pl, _ = L.pads()
+    if H % s or W % s:
+        raise ValueError("certificate needs s | H and s | W")
+    Co, Ci, kh, kw = K.shape
+    g = 1 if L.kind == "dense" else L.g
+    Cog = Co // g
+    Hs, Ws = H // s, W // s
+    frob = np.zeros((g, Hs, Ws))
+    spec = np.zeros((g, Hs, Ws))
+    sig_dev = 0.0
+    for gi in range(g):
+        Kg = K[gi * Cog:(gi + 1) * Cog]
+        for f1 in range(Hs):
+            for f2 in range(Ws):
+                M = np.zeros((Cog, Ci, s, s), complex)
+                for a in range(kh):
+                    qa, ra = divmod(d * a - pt, s)
+                    for b in range(kw):
+                        qb, rb = divmod(d * b - pl, s)
+                        M[:, :, ra, rb] += Kg[:, :, a, b] * np.exp(2j * np.pi * (f1 * qa / Hs + f2 * qb / Ws))
+                M = M.reshape(Cog, Ci * s * s)
+                G = M.conj().T @ M if M.shape[0] >= M.shape[1] else M @ M.conj().T
+                E = G - np.eye(G.shape[0])
+                frob[gi, f1, f2] = np.linalg.norm(E)
+                spec[gi, f1, f2] = np.abs(np.linalg.eigvalsh(E)).max()
+                sig_dev = max(sig_dev, float(np.abs(np.linalg.svd(M, compute_uv=False) - 1).max()))
+    return frob, spec, sig_dev

@@ -30,15 +30,27 @@ CONV2D, CONV_TRANSPOSE2D, DENSE = 0, 1, 2
 PRESCALE_POWER, PRESCALE_FROBENIUS = 0, 1
 Q = dict(N_LAYERS=0, N_MATRICES=1, PARAMS_NUMEL=2, CACHE_NUMEL=3, KERNELS_F32_NUMEL=4, KERNELS_BF16_NUMEL=5,
          WORKSPACE_BYTES=6, NS_FLOPS=7, KERNEL_SEGMENT_F32=8, KERNEL_SEGMENT_BF16=9, N_UNITS=10,
-         GATHER_F32_NUMEL=11, GATHER_BF16_NUMEL=12, CONV_SCRATCH_BYTES=13,
+         GATHER_F32_NUMEL=11, GATHER_BF16_NUMEL=12, CONV_SCRATCH_BYTES=13, COMP_FLOPS=14,
          LAYER_FIRST_MATRIX=20, LAYER_MATS_PER_GROUP=21, LAYER_KERNEL_OFF_F32=22, LAYER_KERNEL_OFF_BF16=23,
-         LAYER_KERNEL_NUMEL=24, LAYER_OWNER=25, LAYER_C_MID=26, LAYER_C_B=27, LAYER_KP=28, LAYER_SCRATCH_BYTES=29,
+         LAYER_KERNEL_NUMEL=24, LAYER_OWNER=25, LAYER_C_MID=26, LAYER_C_B=27, LAYER_KP=28, LAYER_SCRATCH_BYTES=29, LAYER_NS_FLOPS=30, LAYER_COMP_FLOPS=31,
          MATRIX_ROWS=40, MATRIX_COLS=41, MATRIX_OFFSET=42, MATRIX_CACHE_OFFSET=43, MATRIX_LAYER=44,
          MATRIX_GROUP=45, MATRIX_ROLE=46, UNIT_LAYER=60, UNIT_GROUP=61, UNIT_OWNER=62, UNIT_NUMEL=63,
          UNIT_GATHER_OFF_F32=64, UNIT_GATHER_OFF_BF16=65, UNIT_KERNEL_OFF_F32=66, UNIT_KERNEL_OFF_BF16=67)
 ROLES = {0: "Q", 1: "U", 2: "R", 3: "W"}
 _KIND = {"conv": CONV2D, "convT": CONV_TRANSPOSE2D, "dense": DENSE}
 _MODE = {"zeros": PAD_ZEROS, "circular": PAD_CIRCULAR}
+
+
+TRACE_KINDS = {1: "power", 2: "scale", 3: "ns", 4: "ns_check", 5: "compose", 6: "emit", 7: "conv_fwd",
+               8: "conv_adj", 9: "assemble"}
+CONV_VARIANTS = {0: "none", 1: "conv_fwd_simt/conv_bwd_simt", 2: "conv_fwd_smallk", 3: "conv_stem_tc",
+                 4: "conv_pad<64,swapped>", 5: "conv_pad<BN>", 6: "conv_stack (+pad_kernel)", 7: "conv_tma",
+                 8: "conv_ws<256>", 9: "conv_ws<128>", 10: "conv_ws<64>", 11: "conv_ws<32>", 12: "conv_pair"}
+
+
+class TraceRec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("layer", C.c_int32), ("variant", C.c_int32), ("launches", C.c_int32),
+                ("ms", C.c_float)]
 
 
 class LayerDesc(C.Structure):
@@ -66,6 +78,8 @@ _sig = {
     "orth_conv_transpose": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
     "orth_kernels_assemble": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "orth_plan_check": (C.c_int, [_P, _P]),
+    "orth_plan_trace": (C.c_int, [_P, C.c_int32]),
+    "orth_plan_trace_read": (C.c_int, [_P, C.POINTER(TraceRec), C.c_int32, C.POINTER(C.c_int32)]),
     "orth_plan_launch_count": (C.c_int64, [_P]),
     "orth_status_string": (C.c_char_p, [C.c_int]),
     "orth_last_error": (C.c_char_p, []),
@@ -190,6 +204,19 @@ def orth_plan_check(h: int, stream=None):
     _check(_lib.orth_plan_check(h, _stream(stream)), "orth_plan_check (device status)")
 
 
+def orth_plan_trace(h: int, enable: bool):
+    _check(_lib.orth_plan_trace(h, 1 if enable else 0), "orth_plan_trace")
+
+
+def orth_plan_trace_read(h: int) -> List[Dict]:
+    n = C.c_int32()
+    cap = 4096
+    buf = (TraceRec * cap)()
+    _check(_lib.orth_plan_trace_read(h, buf, cap, C.byref(n)), "orth_plan_trace_read")
+    return [dict(kind=TRACE_KINDS.get(r.kind, str(r.kind)), layer=r.layer, variant=CONV_VARIANTS.get(r.variant, ""),
+                 launches=r.launches, ms=r.ms) for r in buf[: min(n.value, cap)]]
+
+
 def orth_plan_launch_count(h: int) -> int:
     return _lib.orth_plan_launch_count(h)
 
@@ -293,6 +320,12 @@ class Plan:
 
     def check(self, stream=None):
         orth_plan_check(self.h, stream)
+
+    def trace(self, enable: bool = True):
+        orth_plan_trace(self.h, enable)
+
+    def trace_read(self) -> List[Dict]:
+        return orth_plan_trace_read(self.h)
 
     @property
     def launches(self) -> int:

@@ -2,14 +2,76 @@
 // synchronously, then enqueues its kernels on the caller's stream.
 #include <cuda_runtime.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <cstdint>
 #include <cstdlib>
+#include <vector>
 
 #include "orth_internal.h"
 
 using namespace orth;
 
+// tracing state of a plan (orth_plan_trace): event pairs of the groups recorded since the last read
+struct orth_trace_state {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  struct Pending { orth_trace_rec_t rec; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+namespace orth {
+void orth_plan_trace_free(Plan& p) {
+  if (!p.trace) return;
+  for (auto e : p.trace->pool) cudaEventDestroy(e);
+  for (auto& r : p.trace->pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  delete p.trace;
+  p.trace = nullptr;
+}
+}  // namespace orth
+
 namespace {
+
+orth_trace_state& tstate(Plan& P) {
+  if (!P.trace) P.trace = new orth_trace_state();
+  return *P.trace;
+}
+
+// NVTX range of one ABI call (always on; free when no tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+// One traced group of kernels: events around it on the call's stream when tracing is on.
+struct Trace {
+  Plan& P;
+  int kind, layer;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  int64_t l0;
+  Trace(Plan& p, int k, int lay, void* stream) : P(p), kind(k), layer(lay), s((cudaStream_t)stream), l0(p.launches) {
+    g_conv_variant = 0;
+    if (P.trace && P.trace->on) {
+      a = P.trace->get();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~Trace() {
+    if (!a) return;
+    cudaEvent_t b = P.trace->get();
+    cudaEventRecord(b, s);
+    orth_trace_rec_t r{kind, layer, (kind == ORTH_TK_CONV_FWD || kind == ORTH_TK_CONV_ADJ) ? g_conv_variant : 0,
+                       (int32_t)(P.launches - l0), 0.f};
+    P.trace->pending.push_back({r, a, b});
+  }
+};
 
 orth_status_t cuda_fail(int e, const char* where) {
   if (e == 0) return ORTH_OK;
@@ -57,6 +119,7 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
   if (!params || !ortho_out) { set_error("NULL params or ortho_out"); return ORTH_ERR_INVALID_ARGUMENT; }
   if (params == ortho_out) { set_error("params and ortho_out must not overlap"); return ORTH_ERR_INVALID_ARGUMENT; }
   if (P.mat_items.empty()) return ORTH_OK;
+  NvtxRange nv("orth_orthogonalize");
   const int T = P.opts.ns_iters;
   float* bufs[BUF_COUNT] = {ortho_out, P.d_scratch, P.d_gram, P.d_comp};
   // X0 goes where T swaps leave the result in ortho_out
@@ -64,19 +127,28 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
   float* x0 = bufs[par == 0 ? BUF_X : BUF_Y];
   const int frob = P.opts.prescale == ORTH_PRESCALE_FROBENIUS;
   int e = 0;
-  // pre-scaling: all power iterations (or the Frobenius pass) in one cooperative launch
-  e = launch_power_fused(P, params, power_cache, (!frob && !power_cache) ? 1 : 0, frob, P.opts.power_iters,
-                         frob ? nullptr : power_cache, stream);
+  {  // pre-scaling: all power iterations (or the Frobenius pass) in one cooperative launch
+    Trace tr(P, ORTH_TK_POWER, -1, stream);
+    e = launch_power_fused(P, params, power_cache, (!frob && !power_cache) ? 1 : 0, frob, P.opts.power_iters,
+                           frob ? nullptr : power_cache, stream);
+  }
   const int mode = P.opts.compute;
   if (mode == ORTH_F32) {
-    if (!e) e = launch_scale(P, params, x0, stream);
-    for (int t = 0; t < T && !e; ++t) {
-      e = launch_gemm_f32(P.gram[par], bufs, stream);
-      if (!e) e = launch_gemm_f32(P.update[par], bufs, stream);
-      P.launches += 2;
-      par ^= 1;
+    if (!e) {
+      Trace tr(P, ORTH_TK_SCALE, -1, stream);
+      e = launch_scale(P, params, x0, stream);
+    }
+    {
+      Trace tr(P, ORTH_TK_NS, -1, stream);
+      for (int t = 0; t < T && !e; ++t) {
+        e = launch_gemm_f32(P.gram[par], bufs, stream);
+        if (!e) e = launch_gemm_f32(P.update[par], bufs, stream);
+        P.launches += 2;
+        par ^= 1;
+      }
     }
     // S:125 convergence check on the last iteration's own Gram G = X_{T-1}^T X_{T-1} (still in BUF_G)
+    Trace tr(P, ORTH_TK_NS_CHECK, -1, stream);
     if (!e) e = launch_converged_check(P, 0, P.opts.ns_tol, stream);
     if (!e && residual_out) {
       e = launch_gemm_f32(P.gram[0], bufs, stream);
@@ -88,7 +160,10 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
     auto gp = [&](int t) { return (mode == ORTH_BF16X3 || t >= T - P.opts.polish_iters) ? 3 : 1; };
     auto up = [&](int t) { return mode == ORTH_BF16X3 ? 3 : 1; };
     auto x_lo = [&](int t) { return t >= T || gp(t) == 3 || up(t) == 3; };   // t == T: the residual Gram
-    if (!e) e = launch_scale_bf16(P, params, x0, par, x_lo(0), stream);
+    if (!e) {
+      Trace tr(P, ORTH_TK_SCALE, -1, stream);
+      e = launch_scale_bf16(P, params, x0, par, x_lo(0), stream);
+    }
     static const bool phased = std::getenv("ORTH_NS_PHASED") != nullptr;   // A/B switch: per-phase kernels
     if (!e && P.nsp_ctas > 0 && 2 * T + 1 <= kNspMaxPhases && !phased) {
       // all 2T (+1 residual Gram) phases in one persistent cooperative launch
@@ -102,16 +177,24 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
         par ^= 1;
       }
       if (residual_out) fl[n++] = (uint8_t)(1 | 2 | (par << 2) | 16);
-      e = launch_ns_persist(P, bufs, fl, n, stream);
+      {
+        Trace tr(P, ORTH_TK_NS, -1, stream);
+        e = launch_ns_persist(P, bufs, fl, n, stream);
+      }
+      Trace tr(P, ORTH_TK_NS_CHECK, -1, stream);
       if (!e && residual_out) e = launch_residual_r(P, residual_out, stream);   // also checks R_T (tol)
       else if (!e) e = launch_converged_check(P, 1, P.opts.ns_tol, stream);
       return cuda_fail(e, "orth_orthogonalize");
     }
-    for (int t = 0; t < T && !e; ++t) {
-      e = launch_ns_tc(P, bufs, par, true, gp(t), up(t) == 3, t == T - 1 && !residual_out, stream);
-      if (!e) e = launch_ns_tc(P, bufs, par, false, up(t), x_lo(t + 1), true, stream);
-      par ^= 1;
+    {
+      Trace tr(P, ORTH_TK_NS, -1, stream);
+      for (int t = 0; t < T && !e; ++t) {
+        e = launch_ns_tc(P, bufs, par, true, gp(t), up(t) == 3, t == T - 1 && !residual_out, stream);
+        if (!e) e = launch_ns_tc(P, bufs, par, false, up(t), x_lo(t + 1), true, stream);
+        par ^= 1;
+      }
     }
+    Trace tr(P, ORTH_TK_NS_CHECK, -1, stream);
     if (!e && residual_out) {
       e = launch_ns_tc(P, bufs, 0, true, 3, false, true, stream);
       if (!e) e = launch_residual_r(P, residual_out, stream);
@@ -128,6 +211,7 @@ orth_status_t orth_compose_kernel(orth_plan_t plan, const float* ortho, float* k
   if (st != ORTH_OK) return st;
   Plan& P = plan->p;
   if (!ortho || !kernels_f32) { set_error("NULL ortho or kernels_f32"); return ORTH_ERR_INVALID_ARGUMENT; }
+  NvtxRange nv("orth_compose_kernel");
   float* bufs[BUF_COUNT] = {const_cast<float*>(ortho), nullptr, nullptr, P.d_comp};
   int e = 0;
   // composition stays FP32-accurate: SIMT FFMA, or the 3-pass split on tensor cores
@@ -136,14 +220,20 @@ orth_status_t orth_compose_kernel(orth_plan_t plan, const float* ortho, float* k
     e = P.opts.compute == ORTH_F32 ? launch_gemm_f32(ph, bufs, stream) : launch_gemm_tc(ph, bufs, 3, stream);
     P.launches++;
   };
-  if (P.opts.compute == ORTH_F32) {
-    gemm(P.proj);
-    for (auto& ph : P.chain) gemm(ph);
-    gemm(P.aoc);
-  } else {
-    e = launch_compose_tc(P, ortho, stream);
+  {
+    Trace tr(P, ORTH_TK_COMPOSE, -1, stream);
+    if (P.opts.compute == ORTH_F32) {
+      gemm(P.proj);
+      for (auto& ph : P.chain) gemm(ph);
+      gemm(P.aoc);
+    } else {
+      e = launch_compose_tc(P, ortho, stream);
+    }
   }
-  if (!e) e = launch_emit(P, bufs, kernels_f32, (uint16_t*)kernels_bf16, stream);
+  if (!e) {
+    Trace tr(P, ORTH_TK_EMIT, -1, stream);
+    e = launch_emit(P, bufs, kernels_f32, (uint16_t*)kernels_bf16, stream);
+  }
   return cuda_fail(e, "orth_compose_kernel");
 }
 
@@ -155,6 +245,8 @@ orth_status_t orth_conv_forward(orth_plan_t plan, int32_t layer, const void* ker
   int Ho = 0, Wo = 0;
   st = check_conv(P, layer, kernel, x, y, N, H, W, io, Ho, Wo);
   if (st != ORTH_OK) return st;
+  NvtxRange nv("orth_conv_forward");
+  Trace tr(P, ORTH_TK_CONV_FWD, layer, stream);
   const int e = launch_conv_fwd(P.layers[layer], kernel, P.layers[layer].wt_scratch, bias, x, y, N, H, W, Ho, Wo, io, stream);
   P.launches++;
   return cuda_fail(e, "orth_conv_forward");
@@ -169,6 +261,8 @@ orth_status_t orth_conv_transpose(orth_plan_t plan, int32_t layer, const void* k
   int Ho = 0, Wo = 0;
   st = check_conv(P, layer, kernel, y_small, x_big, N, H_big, W_big, io, Ho, Wo);
   if (st != ORTH_OK) return st;
+  NvtxRange nv("orth_conv_transpose");
+  Trace tr(P, ORTH_TK_CONV_ADJ, layer, stream);
   const int e = launch_conv_bwd(P.layers[layer], kernel, P.layers[layer].wt_scratch, bias, y_small, x_big, N, H_big, W_big, Ho,
                                 Wo, io, stream);
   P.launches++;
@@ -190,10 +284,41 @@ orth_status_t orth_kernels_assemble(orth_plan_t plan, const float* gathered_f32,
     set_error("gathered and final kernel buffers must not overlap");
     return ORTH_ERR_INVALID_ARGUMENT;
   }
+  NvtxRange nv("orth_kernels_assemble");
+  Trace tr(P, ORTH_TK_ASSEMBLE, -1, stream);
   const int e = launch_assemble(P, gathered_f32, kernels_f32, (const uint16_t*)gathered_bf16, (uint16_t*)kernels_bf16,
                                 stream);
   P.launches++;
   return cuda_fail(e, "orth_kernels_assemble");
+}
+
+orth_status_t orth_plan_trace(orth_plan_t plan, int32_t enable) {
+  orth_status_t st = need_device(plan);
+  if (st != ORTH_OK) return st;
+  tstate(plan->p).on = enable != 0;
+  return ORTH_OK;
+}
+
+orth_status_t orth_plan_trace_read(orth_plan_t plan, orth_trace_rec_t* out, int32_t cap, int32_t* n) {
+  orth_status_t st = need_device(plan);
+  if (st != ORTH_OK) return st;
+  if (!n || cap < 0) { set_error("NULL n or negative cap"); return ORTH_ERR_INVALID_ARGUMENT; }
+  orth_trace_state& T = tstate(plan->p);
+  *n = (int32_t)T.pending.size();
+  int i = 0;
+  for (auto& r : T.pending) {
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return cuda_fail((int)e, "orth_plan_trace_read");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    r.rec.ms = ms;
+    if (out && i < cap) out[i] = r.rec;
+    ++i;
+    T.pool.push_back(r.a);
+    T.pool.push_back(r.b);
+  }
+  T.pending.clear();
+  return ORTH_OK;
 }
 
 orth_status_t orth_plan_check(orth_plan_t plan, void* stream) {

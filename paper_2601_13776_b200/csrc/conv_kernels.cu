@@ -311,6 +311,7 @@ int launch_conv_fwd(const LayerInfo& L, const void* kernel, void* scratch, const
         attr = smem;
       }
       dim3 g2((unsigned)((M + 255) / 256), 1, (unsigned)L.g);
+      g_conv_variant = ORTH_CV_SMALLK;
       conv_fwd_smallk<<<g2, 256, smem, (cudaStream_t)stream>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)kernel,
                                                                bias, (__nv_bfloat16*)y, a);
       return (int)cudaGetLastError();
@@ -318,6 +319,7 @@ int launch_conv_fwd(const LayerInfo& L, const void* kernel, void* scratch, const
   }
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((L.co + BN - 1) / BN), (unsigned)L.g);
   cudaStream_t s = (cudaStream_t)stream;
+  g_conv_variant = ORTH_CV_SIMT;
   if (io == ORTH_BF16)
     conv_fwd_simt<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, s>>>(
         (const __nv_bfloat16*)x, (const __nv_bfloat16*)kernel, bias, (__nv_bfloat16*)y, a);
@@ -334,6 +336,7 @@ int launch_conv_bwd(const LayerInfo& L, const void* kernel, void* wt_scratch, co
   const int64_t M = (int64_t)N * H * W;
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((L.ci + BN - 1) / BN), (unsigned)L.g);
   cudaStream_t s = (cudaStream_t)stream;
+  g_conv_variant = ORTH_CV_SIMT;
   if (io == ORTH_BF16)
     conv_bwd_simt<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, s>>>(
         (const __nv_bfloat16*)y, (const __nv_bfloat16*)kernel, bias, (__nv_bfloat16*)x, a);

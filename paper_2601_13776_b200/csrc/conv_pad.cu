@@ -645,12 +645,14 @@ int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* b
   if (!no_swap && pad_args(L, N, H, W, Ho, Wo, bn, a, true) && bn == 64) {   // 64 channels x 256 pixels per MMA
     if (a.num_tiles == 0) return 0;
     a.flip = flip;
+    g_conv_variant = ORTH_CV_WINDOW_SWAP;
     const int e = launch_pad<64, true>(x, w, L.co_f, bias, out, a, L.ci_f, s);
     if (e >= 0) return e;
   }
   if (!pad_args(L, N, H, W, Ho, Wo, bn, a, false)) return -1;
   if (a.num_tiles == 0) return 0;
   a.flip = flip;
+  g_conv_variant = ORTH_CV_WINDOW;
   switch (bn) {
     case 32: return launch_pad<32, false>(x, w, L.co_f, bias, out, a, L.ci_f, s);
     case 64: return launch_pad<64, false>(x, w, L.co_f, bias, out, a, L.ci_f, s);

@@ -401,6 +401,7 @@ int launch_conv_fwd_stack(const LayerInfo& L, const void* kernel, const float* b
   if (pad_elems * 2 > L.pad_bytes) return -1;   // call larger than the declared grid / batch: the caller falls back
   if (a.num_tiles == 0) return 0;
   a.flip = flip;
+  g_conv_variant = ORTH_CV_STACK;
   cudaStream_t s = (cudaStream_t)stream;
   {
     const int64_t vec = pad_elems / 8;

@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(128) conv_stem_tc(const __nv_bfloat16* __restr
 template <int CO, int CI, int KS>
 int launch_stem(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias, __nv_bfloat16* y,
                 const StemArgs& a, cudaStream_t s) {
+  g_conv_variant = ORTH_CV_STEM;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -731,6 +731,7 @@ int num_sms() {
 template <int BN, int S>
 int launch_ws(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
               const TcConvArgs& a0, cudaStream_t stream) {
+  g_conv_variant = BN == 256 ? ORTH_CV_GATHER256 : BN == 128 ? ORTH_CV_GATHER128 : BN == 64 ? ORTH_CV_GATHER64 : ORTH_CV_GATHER32;
   TcConvArgs a = a0;
   // the pixel table only needs this layer's taps (k^2 <= MAX_TAPS)
   size_t smem = 1024 + (size_t)S * (128 * 128 + BN * 128) + (size_t)a.k * a.k * 128 * 4;
@@ -800,6 +801,7 @@ int launch_ws(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const
 template <int BN, int S>
 int launch_pair(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
                 const TcConvArgs& a, cudaStream_t stream) {
+  g_conv_variant = ORTH_CV_GATHER_PAIR;
   const size_t smem = 1024 + (size_t)S * (128 * 128 + BN / 2 * 128) + (size_t)a.k * a.k * 128 * 4;
   static size_t attr = 0;
   if (smem > attr) {

@@ -243,6 +243,7 @@ int launch_conv_fwd_tma(const LayerInfo& L, const void* kernel, const float* bia
   a.num_tiles = (int)nt;
   if (a.num_tiles == 0) return 0;
   if (int e = launch_pad_input(L, x, N, H, W, Hp, P, stream)) return e < 0 ? -1 : e;
+  g_conv_variant = ORTH_CV_TMA;
   cudaStream_t s = (cudaStream_t)stream;
   return BN == 256 ? launch_tma<256>(L, kernel, bias, y, a, Hp, P, s) : launch_tma<128>(L, kernel, bias, y, a, Hp, P, s);
 }

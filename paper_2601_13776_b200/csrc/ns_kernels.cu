@@ -19,6 +19,8 @@
 #include <cstdint>
 
 #include "orth_internal.h"
+#include "pdl.h"
+#include "umma.cuh"
 
 namespace orth {
 
@@ -403,26 +405,46 @@ __global__ void __launch_bounds__(256) scale_kernel(const PowerItem* __restrict_
   for (int64_t e = beg + threadIdx.x; e < end; e += 256) X0[e] = W[e] * inv;
 }
 
-// r = |I - G|_F per owned matrix from its Gram (is_r: G already holds R = I - X^T X).  NOT_CONVERGED
-// (R20) when r is non-finite or the checked value exceeds tol > 0: r itself for the final
-// residual, or -- bound = 1, r of the LAST iteration's input X_{T-1} -- the bound on the result's
-// residual: with R symmetric and X' = X (I + R/2), I - X'^T X' = 3/4 R^2 + 1/4 R^3 exactly, so
-// |I - X_T^T X_T|_F <= 3/4 r^2 + 1/4 r^3.
-__global__ void __launch_bounds__(256) residual_kernel(const MatItem* __restrict__ mats, const float* __restrict__ G,
-                                                       float* __restrict__ res, int32_t* __restrict__ status,
-                                                       int is_r, float tol, int bound) {
+// Residual reduction in two deterministic stages (R20).  Stage 1: one CTA per residual item
+// (a ~16K-element slice of a matrix's s x s Gram G, or of R = I - X^T X when is_r) writes its sum of
+// squares of (I - G) to part[item].  Stage 2: one warp per matrix sums its items in item order:
+// r = |I - G|_F.  NOT_CONVERGED when r is non-finite or the checked value exceeds tol > 0: r itself for
+// the final residual, or -- bound = 1, r of the LAST iteration's input X_{T-1} -- the bound on the
+// result's residual: with R symmetric and X' = X (I + R/2), I - X'^T X' = 3/4 R^2 + 1/4 R^3 exactly,
+// so |I - X_T^T X_T|_F <= 3/4 r^2 + 1/4 r^3.
+__global__ void __launch_bounds__(256) residual_part_kernel(const ResItem* __restrict__ items,
+                                                            const MatItem* __restrict__ mats,
+                                                            const float* __restrict__ G, float* __restrict__ part,
+                                                            int is_r) {
   __shared__ float red[9];
-  const MatItem M = mats[blockIdx.x];
-  const int s = M.m < M.n ? M.m : M.n;
+  umma::griddep_launch_dependents();
+  umma::griddep_wait();
+  const ResItem it = items[blockIdx.x];
+  const MatItem M = mats[it.midx];
+  const int64_t s = M.m < M.n ? M.m : M.n;
   const float* g = G + M.gram_off;
   float a = 0.f;
-  for (int64_t e = threadIdx.x; e < (int64_t)s * s; e += 256) {
-    const int i = (int)(e / s), j = (int)(e % s);
+  for (int64_t e = it.e0 + threadIdx.x; e < it.e1; e += 256) {
+    const int64_t i = e / s, j = e - i * s;
     const float r = is_r ? g[e] : (i == j ? 1.f : 0.f) - g[e];
     a = fmaf(r, r, a);
   }
   a = block_sum(a, red);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) part[blockIdx.x] = a;
+}
+
+__global__ void __launch_bounds__(256) residual_final_kernel(const MatItem* __restrict__ mats, int nmats,
+                                                             const float* __restrict__ part, float* __restrict__ res,
+                                                             int32_t* __restrict__ status, float tol, int bound) {
+  umma::griddep_launch_dependents();
+  umma::griddep_wait();
+  const int w = (int)(blockIdx.x * 8 + (threadIdx.x >> 5)), lane = threadIdx.x & 31;
+  if (w >= nmats) return;
+  const MatItem M = mats[w];
+  float a = 0.f;
+  for (int i = lane; i < M.nres; i += 32) a += part[M.res0 + i];   // fixed per-lane order
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if (lane == 0) {
     const float r = sqrtf(a);
     if (res) res[M.mat] = r;
     const float chk = bound ? r * r * (0.75f + 0.25f * r) : r;
@@ -507,28 +529,28 @@ int launch_scale(Plan& p, const float* W, float* X0, void* stream) {
   return (int)cudaGetLastError();
 }
 
-int launch_residual(Plan& p, float* residual_out, void* stream) {
+static int residual_two_stage(Plan& p, int is_r, float* res, float tol, int bound, void* stream) {
   if (p.mat_items.empty()) return 0;
-  residual_kernel<<<(int)p.mat_items.size(), 256, 0, (cudaStream_t)stream>>>(p.d_mat_items, p.d_gram, residual_out,
-                                                                             p.d_status, 0, p.opts.ns_tol, 0);
-  p.launches++;
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_pdl(residual_part_kernel, dim3((unsigned)p.res_items.size()), dim3(256), 0, st,
+             (const ResItem*)p.d_res_items, (const MatItem*)p.d_mat_items, (const float*)p.d_gram, p.d_res_part, is_r);
+  const int nm = (int)p.mat_items.size();
+  launch_pdl(residual_final_kernel, dim3((unsigned)((nm + 7) / 8)), dim3(256), 0, st, (const MatItem*)p.d_mat_items,
+             nm, (const float*)p.d_res_part, res, p.d_status, tol, bound);
+  p.launches += 2;
   return (int)cudaGetLastError();
+}
+
+int launch_residual(Plan& p, float* residual_out, void* stream) {
+  return residual_two_stage(p, 0, residual_out, p.opts.ns_tol, 0, stream);
 }
 
 int launch_converged_check(Plan& p, int is_r, float tol, void* stream) {
-  if (p.mat_items.empty()) return 0;
-  residual_kernel<<<(int)p.mat_items.size(), 256, 0, (cudaStream_t)stream>>>(p.d_mat_items, p.d_gram, p.d_ns_res,
-                                                                             p.d_status, is_r, tol, 1);
-  p.launches++;
-  return (int)cudaGetLastError();
+  return residual_two_stage(p, is_r, p.d_ns_res, tol, 1, stream);
 }
 
 int launch_residual_r(Plan& p, float* residual_out, void* stream) {
-  if (p.mat_items.empty()) return 0;
-  residual_kernel<<<(int)p.mat_items.size(), 256, 0, (cudaStream_t)stream>>>(p.d_mat_items, p.d_gram, residual_out,
-                                                                             p.d_status, 1, p.opts.ns_tol, 0);
-  p.launches++;
-  return (int)cudaGetLastError();
+  return residual_two_stage(p, 1, residual_out, p.opts.ns_tol, 0, stream);
 }
 
 }  // namespace orth

@@ -1306,7 +1306,10 @@ int launch_ns_persist(Plan& p, float* const bufs[BUF_COUNT], const uint8_t* flag
   // dataflow for latency-bound batches (cfg2 / cfg3: a few hundred tiles per phase; measured 0.63 -> 0.57 ms
   // on cfg3), phase-synchronous for big uniform sweeps (cfg5 n = 2048: 34.3 ms sync vs 40.5 ms dataflow)
   static const char* mode_env = std::getenv("ORTH_NS_MODE");   // "flow" | "sync" (A/B)
-  const bool small = p.ns_upd_tiles <= 4 * p.nsp_ctas;
+  // decided on the whole network's tile count, not this rank's share: the two schedules differ in the
+  // Gram of N >= 512 matrices (full tiles vs symmetric + mirror, whose 3-pass cross terms accumulate in
+  // the opposite order), so a per-rank choice would make sharded results differ in the last bits
+  const bool small = p.ns_upd_tiles_all <= 4 * (int64_t)p.nsp_ctas;
   const bool flow = mode_env ? std::strcmp(mode_env, "sync") != 0 : small;
   if (flow) {
     if (int e = build_flow_items(p, flags, nphases)) return e;

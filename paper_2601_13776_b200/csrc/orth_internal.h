@@ -142,8 +142,14 @@ struct ColItem {          // column block of the power kernel: w[c0:c1] = (W^T u
 };
 
 struct MatItem {          // one owned, non-empty matrix (power finalize / residual kernels)
-  int32_t mat, m, n, chunk0, nchunks, col0, ncols, pad_;   // row items [chunk0, +nchunks), column items [col0, +ncols)
+  int32_t mat, m, n, chunk0, nchunks, col0, ncols, res0;   // row items [chunk0, +nchunks), column items [col0, +ncols)
+  int32_t nres, pad_[3];    // residual items [res0, res0 + nres)
   int64_t off, cache_off, gram_off, t_off;
+};
+
+struct ResItem {          // one slice [e0, e1) of a matrix's s x s Gram / R (residual reduction, stage 1)
+  int32_t midx, pad_;
+  int64_t e0, e1;
 };
 
 struct EmitItem {         // one (layer, group): copy the unit kernel into both layouts
@@ -165,6 +171,9 @@ struct CompUnit {
 };
 
 struct TcComposePlan;   // tensor-core composition (compose_tc.cu)
+}  // namespace orth
+struct orth_trace_state;   // abi.cu (orth_plan_trace)
+namespace orth {
 
 struct Plan {
   std::vector<LayerInfo> layers;
@@ -192,6 +201,7 @@ struct Plan {
   // tensor-core NS on BF16 operand copies (ns_tc.cu)
   std::vector<NsDesc> ns_gram, ns_upd;
   int32_t ns_gram_tiles = 0, ns_upd_tiles = 0;
+  int64_t ns_upd_tiles_all = 0;     // over all ranks' matrices (schedule choice, bitwise-stable sharding)
   NsDesc* d_ns_gram = nullptr;
   NsDesc* d_ns_upd = nullptr;
   std::vector<NsDesc> ns_upd64;     // dataflow NS: the update descriptors with 64-wide tiles (epi = 2)
@@ -226,6 +236,9 @@ struct Plan {
   int64_t t_numel = 0;              // sum of rows: the power kernel's t = W v buffer
   std::vector<int32_t> owned_mats;  // indices of owned, non-empty matrices
   std::vector<MatItem> mat_items;   // same order as owned_mats
+  std::vector<ResItem> res_items;
+  ResItem* d_res_items = nullptr;
+  float* d_res_part = nullptr;      // one partial sum of squares per residual item
 
   // composition phases
   GemmPhase proj;                   // P_j = U_j U_j^T
@@ -252,9 +265,14 @@ struct Plan {
   void* d_conv_mem = nullptr;       // every layer's conv scratch (one allocation at create)
   int64_t conv_mem_bytes = 0;
   float* d_ns_res = nullptr;        // per-matrix residual of the last iteration's Gram (convergence check)
+  orth_trace_state* trace = nullptr;
 };
 
 void set_error(const char* fmt, ...);
+
+// Which conv kernel the last conv launcher on this thread used (orth_conv_variant_t of orth.h); the ABI
+// copies it into the trace record of the call.
+extern thread_local int g_conv_variant;
 
 // kernel launchers (CUDA translation units); return 0 or a cudaError_t value
 int launch_gemm_f32(const GemmPhase& ph, float* const bufs[BUF_COUNT], void* stream);
@@ -310,6 +328,7 @@ int launch_residual(Plan& p, float* residual_out, void* stream);
 // convergence check: r = |R|_F of the last iteration's FP32 R (is_r) or |I - G|_F (SIMT Gram);
 // NOT_CONVERGED when r is non-finite or 3/4 r^2 + 1/4 r^3 > tol (tol > 0)
 int launch_converged_check(Plan& p, int is_r, float tol, void* stream);
+void orth_plan_trace_free(Plan& p);   // abi.cu
 // a8: copy every unit from the gather layout to the final layout
 int launch_assemble(Plan& p, const float* gf, float* kf, const uint16_t* gb, uint16_t* kb, void* stream);
 // per-layer conv scratch (bytes) for calls up to N x Hbig x Wbig (forward-conv input grid), both

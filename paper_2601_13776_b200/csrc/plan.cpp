@@ -20,6 +20,7 @@
 namespace orth {
 
 static thread_local char g_err[512] = "";
+thread_local int g_conv_variant = 0;
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -344,6 +345,13 @@ static void build_ns(Plan& P) {
   }
   P.ns_gram_tiles = tg;
   P.ns_upd_tiles = tu;
+  // the same count over EVERY matrix of the network (all ranks' units): the NS schedule choice
+  // (ns_persist.cu: dataflow vs phase-synchronous) depends only on it, so a sharded rank runs the
+  // same per-matrix arithmetic as a single-rank plan and its results are bitwise identical (R22)
+  int64_t tu_all = 0;
+  for (const auto& M : P.mats)
+    if (M.m > 0 && M.n > 0) tu_all += ((M.m + 127) / 128) * ((M.n + 127) / 128);
+  P.ns_upd_tiles_all = tu_all;
   // pre-scaling work items.  Row items (t = W v, and the scale kernels): ~8K
   // elements each, <= 64 per matrix.  Column items (w = W^T u): >= 32 columns,
   // ~8K elements each, <= 64 per matrix.  Every cross-item sum is taken in
@@ -351,6 +359,7 @@ static void build_ns(Plan& P) {
   P.power_items.clear();
   P.col_items.clear();
   P.mat_items.clear();
+  P.res_items.clear();
   int chunk = 0, cchunk = 0;
   int64_t t_off = 0;
   for (int i : P.owned_mats) {
@@ -384,6 +393,13 @@ static void build_ns(Plan& P) {
     }
     mi.nchunks = chunk - mi.chunk0;
     mi.ncols = cchunk - mi.col0;
+    {   // residual reduction items: ~16K elements of the s x s Gram each (fixed split: deterministic sums)
+      const int64_t sq = std::min(M.m, M.n) * std::min(M.m, M.n);
+      const int64_t per = 16384;
+      mi.res0 = (int32_t)P.res_items.size();
+      for (int64_t e0 = 0; e0 < sq; e0 += per) P.res_items.push_back(ResItem{midx, 0, e0, std::min(sq, e0 + per)});
+      mi.nres = (int32_t)P.res_items.size() - mi.res0;
+    }
     P.mat_items.push_back(mi);
     t_off += M.m;
   }
@@ -610,6 +626,8 @@ static orth_status_t allocate(Plan& P) {
   const size_t o_comp = take(P.comp_numel * 4), o_stat = take(64);
   const size_t o_pi = take(std::max<size_t>(P.power_items.size(), 1) * sizeof(PowerItem));
   const size_t o_own = take(std::max<size_t>(P.mat_items.size(), 1) * sizeof(MatItem));
+  const size_t o_ri = take(std::max<size_t>(P.res_items.size(), 1) * sizeof(ResItem));
+  const size_t o_rp = take(std::max<size_t>(P.res_items.size(), 1) * sizeof(float));
   const size_t o_col = take(std::max<size_t>(P.col_items.size(), 1) * sizeof(ColItem));
   const size_t o_emit = take(std::max<size_t>(P.emit.size(), 1) * sizeof(EmitItem));
   const size_t o_nsg = take(std::max<size_t>(P.ns_gram.size(), 1) * sizeof(NsDesc));
@@ -641,6 +659,8 @@ static orth_status_t allocate(Plan& P) {
   P.d_status = (int32_t*)(base + o_stat);
   P.d_power_items = (PowerItem*)(base + o_pi);
   P.d_mat_items = (MatItem*)(base + o_own);
+  P.d_res_items = (ResItem*)(base + o_ri);
+  P.d_res_part = (float*)(base + o_rp);
   P.d_col_items = (ColItem*)(base + o_col);
   P.d_emit = (EmitItem*)(base + o_emit);
   P.d_ns_gram = (NsDesc*)(base + o_nsg);
@@ -656,6 +676,8 @@ static orth_status_t allocate(Plan& P) {
     e = cudaMemcpy(P.d_ns_upd, P.ns_upd.data(), P.ns_upd.size() * sizeof(NsDesc), cudaMemcpyHostToDevice);
   if (!P.power_items.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_power_items, P.power_items.data(), P.power_items.size() * sizeof(PowerItem), cudaMemcpyHostToDevice);
+  if (!P.res_items.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_res_items, P.res_items.data(), P.res_items.size() * sizeof(ResItem), cudaMemcpyHostToDevice);
   if (!P.mat_items.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_mat_items, P.mat_items.data(), P.mat_items.size() * sizeof(MatItem), cudaMemcpyHostToDevice);
   if (!P.col_items.empty() && e == cudaSuccess)
@@ -761,6 +783,7 @@ orth_status_t orth_plan_destroy(orth_plan_t plan) {
   if (plan->p.nsf_items) cudaFree(plan->p.nsf_items);
   if (plan->p.d_arena) cudaFree(plan->p.d_arena);
   if (plan->p.d_conv_mem) cudaFree(plan->p.d_conv_mem);
+  orth_plan_trace_free(plan->p);
   if (plan->p.d_ns_upd64) cudaFree(plan->p.d_ns_upd64);
   if (plan->p.d_ns_gram_flow) cudaFree(plan->p.d_ns_gram_flow);
   if (plan->p.d_ns_upd_wide) cudaFree(plan->p.d_ns_upd_wide);
@@ -791,6 +814,15 @@ orth_status_t orth_plan_query(orth_plan_t plan, int32_t what, int32_t index, int
     case ORTH_Q_GATHER_BF16_NUMEL: *out = P.gat_bf16_numel; break;
     case ORTH_Q_CONV_SCRATCH_BYTES: *out = P.conv_mem_bytes; break;
     case ORTH_Q_LAYER_SCRATCH_BYTES: *out = P.layers[index].pad_bytes; break;
+    case ORTH_Q_LAYER_NS_FLOPS: *out = (int64_t)P.layers[index].ns_flops; break;
+    case ORTH_Q_LAYER_COMP_FLOPS: *out = (int64_t)P.layers[index].comp_flops; break;
+    case ORTH_Q_COMP_FLOPS: {
+      double f = 0.0;
+      for (auto& u : P.units)
+        if (u.owner == P.opts.rank) f += P.layers[u.layer].comp_flops / P.layers[u.layer].g;
+      *out = (int64_t)f;
+      break;
+    }
     case ORTH_Q_UNIT_LAYER: *out = P.units[index].layer; break;
     case ORTH_Q_UNIT_GROUP: *out = P.units[index].group; break;
     case ORTH_Q_UNIT_OWNER: *out = P.units[index].owner; break;

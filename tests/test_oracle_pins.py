@@ -384,3 +384,43 @@ def test_unit_derivation_counts_match_survey():
     n4, f4 = _count(configs.cfg4())
     assert (n2, n3, n4) == (57, 158, 333)
     assert abs(f2 / 1e9 - 45.5) < 0.1 and abs(f3 / 1e9 - 99.8) < 0.1 and abs(f4 / 1e9 - 670) < 1.0
+
+
+# ------------------------------------------------------------------ f2: spectral certificate
+@pytest.mark.parametrize("ci,co,k,s,d,g,H", [(4, 4, 3, 1, 1, 1, 6), (3, 5, 3, 2, 1, 1, 8), (6, 4, 4, 2, 1, 2, 8),
+                                           (4, 8, 3, 2, 1, 1, 8), (2, 3, 3, 1, 2, 1, 7)])
+def test_spectral_certificate_against_toeplitz(ci, co, k, s, d, g, H):
+    """Brute force on tiny inputs: the Toeplitz matrix T of the circular operator (impulse responses, no
+    symbol code involved) fixes (i) max_f |E_f|_2 = max |sigma^2 - 1| over the singular values of T on the
+    short side, and (ii) sum_f |E_f|_F^2 = |T^T T - I|_F^2 (input short side) or |T T^T - I|_F^2 (output
+    short side): the per-frequency block diagonalisation is unitary, so Frobenius norms add up exactly."""
+    L = O.Layer(ci, co, k, s, d, g)
+    K = rs.standard_normal((co, ci // g, k, k)) * 0.3
+    frob, spec, sig_dev = O.spectral_certificate(K, L, H, H)
+    T = O.toeplitz(lambda x: O.conv2d(x, K, s=s, d=d, g=g), (ci, H, H))
+    sv = np.linalg.svd(T, compute_uv=False)
+    short = min(T.shape)
+    dev2 = np.abs(sv[:short] ** 2 - 1)
+    if T.shape[0] >= T.shape[1]:
+        G = T.T @ T
+    else:
+        G = T @ T.T
+    assert abs(spec.max() - dev2.max()) < 1e-10 * max(1.0, dev2.max())
+    assert abs((frob ** 2).sum() - np.linalg.norm(G - np.eye(G.shape[0])) ** 2) < 1e-9 * max(1.0, (frob ** 2).sum())
+    assert abs(sig_dev - np.abs(sv[:short] - 1).max()) < 1e-10
+    assert (frob >= spec - 1e-12).all()                      # |E|_F >= |E|_2: the certificate is an upper bound
+
+
+def test_spectral_certificate_orthogonal_and_dense():
+    """An AOC kernel built by the oracle is orthogonal: every |E_f|_F ~ 1e-15 (P:462 tolerance 1e-4 is met by
+    11 orders of magnitude); a dense orthogonal matrix has one frequency with |E|_F ~ 0, and 2 I gives
+    E = 3 I, |E|_F = 3 sqrt(n)."""
+    L = O.Layer(8, 16, 3, 2)
+    ms = [gen.param_matrix(M.m, M.n, (99, 0, 0, i, 1)).astype(np.float64) for i, M in enumerate(O.layer_matrices(L))]
+    ortho, _ = O.orthogonalize(ms, T=25)
+    K = O.layer_kernel(L, [ortho])
+    frob, spec, sig_dev = O.spectral_certificate(K, L, 8, 8)
+    assert frob.max() < 1e-12 and sig_dev < 1e-12
+    Ld = O.Layer(5, 5, 1, kind="dense")
+    frob, spec, _ = O.spectral_certificate(2 * np.eye(5), Ld, 1, 1)
+    assert frob.shape == (1, 1, 1) and abs(frob[0, 0, 0] - 3 * np.sqrt(5)) < 1e-12 and abs(spec[0, 0, 0] - 3) < 1e-12

@@ -449,7 +449,7 @@ def ours(args):
     ns_fl = orth.orth_plan_query(plan.h, "NS_FLOPS")
     ns_ms = table.get("ns", {}).get("ms_per_step") if table else None
     # ---- e2e through the public API with host buffers
-    e2e = e2e_run(W, torch, world, pg, args, barrier, None if args.no_graph else step)
+    e2e = e2e_run(W, torch, world, pg, args, barrier, not args.no_graph)
     n_layers = len(W.layers)
     out = {
         "metric": METRIC, "value": n_layers / (t_step * 1e-3), "unit": "layers/s", "n_gpus": world,
@@ -487,62 +487,91 @@ def ours(args):
         dist.destroy_process_group()
 
 
-def e2e_run(W, torch, world, pg, args, barrier, step):
+def e2e_run(W, torch, world, pg, args, barrier, graphs_ok):
     """Same step through the public API with HOST buffers: pinned H2D of every step's inputs (params + x)
-    and D2H of its result inside the timed region.  The copies run on their own stream: step i+1's H2D and
-    step i's D2H overlap step i's compute, as a serving loop would run them; every step still copies its
-    own inputs (staged, then moved into place on the compute stream) and its own result."""
+    and D2H of its result inside the timed region.  Run as a serving loop would: two device buffer sets
+    (params, input batch, result copy) with the step captured once per set, the copies on their own
+    stream, so step i+1's H2D and step i's D2H overlap step i's compute; every step still copies its own
+    inputs and its own result."""
     ph = torch.from_numpy(W.params_h).pin_memory()
     xh = torch.from_numpy(W.x_h).to(torch.bfloat16).pin_memory()
     res = W.result()
-    yh = torch.empty(res.shape, dtype=res.dtype).pin_memory()
     s = torch.cuda.current_stream()
-    c = torch.cuda.Stream()
-    x_dev = W.ins[0] if W.ins else None
     n = max(1, args.steps)
-    ev_in, ev_done = torch.cuda.Event(), torch.cuda.Event()
-    P_st = torch.empty_like(W.params)
-    X_st = torch.empty_like(x_dev) if x_dev is not None else None
+    has_x = bool(W.ins)
+    P = [W.params, torch.empty_like(W.params)]
+    X = [W.ins[0], torch.empty_like(W.ins[0])] if has_x else [None, None]
+    Y = [torch.empty_like(res), torch.empty_like(res)]
+    yh = [torch.empty(res.shape, dtype=res.dtype).pin_memory() for _ in range(2)]
+    p0, x0 = W.params, (W.ins[0] if has_x else None)
 
-    def one(prefetch_next: bool):
-        s.wait_event(ev_in)
-        W.params.copy_(P_st)
-        if x_dev is not None:
-            x_dev.copy_(X_st)
-        if step is not None:
-            step()
+    def use(b):
+        W.params = P[b]
+        if has_x:
+            W.ins[0] = X[b]
+
+    def body(b):
+        W.construct()
+        if W.sharded:
+            W.gather(pg)
+        W.forward()
+        Y[b].copy_(res)
+    steps = []
+    for b in range(2):
+        use(b)
+        if graphs_ok and not W.sharded:
+            g = capture(torch, lambda b=b: body(b))
+            steps.append(g.replay)
+        elif graphs_ok:
+            gA = capture(torch, W.construct)
+            gB = capture(torch, lambda b=b: (W.forward(), Y[b].copy_(res)))
+            steps.append(lambda gA=gA, gB=gB: (gA.replay(), W.gather(pg), gB.replay()))
         else:
-            W.construct()
-            if W.sharded:
-                W.gather(pg)
-            W.forward()
-        ev_done.record(s)
-        with torch.cuda.stream(c):
-            c.wait_event(ev_done)
-            yh.copy_(res, non_blocking=True)                       # D2H of this step's result
-            if prefetch_next:                                      # H2D of the next step's inputs
-                P_st.copy_(ph, non_blocking=True)
-                if X_st is not None:
-                    X_st.copy_(xh, non_blocking=True)
-                ev_in.record(c)
+            steps.append(lambda b=b: (use(b), body(b)))
+    use(0)
+    torch.cuda.synchronize()
+    c = torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
 
-    def run(k):
-        with torch.cuda.stream(c):
-            c.wait_stream(s)
-            P_st.copy_(ph, non_blocking=True)
-            if X_st is not None:
-                X_st.copy_(xh, non_blocking=True)
-            ev_in.record(c)
+    def loop(k):
+        c.wait_stream(s)
+        with torch.cuda.stream(c):                    # inputs of step 0
+            P[0].copy_(ph, non_blocking=True)
+            if has_x:
+                X[0].copy_(xh, non_blocking=True)
+            ev_in[0].record(c)
         for i in range(k):
-            one(i + 1 < k)
+            b = i % 2
+            if i + 1 < k:                             # prefetch step i+1's inputs into the other set
+                with torch.cuda.stream(c):
+                    if i >= 1:
+                        c.wait_event(ev_done[1 - b])  # step i-1 has finished reading that set
+                    P[1 - b].copy_(ph, non_blocking=True)
+                    if has_x:
+                        X[1 - b].copy_(xh, non_blocking=True)
+                    ev_in[1 - b].record(c)
+            s.wait_event(ev_in[b])
+            if i >= 2:
+                s.wait_event(ev_out[b])               # Y[b] of step i-2 has reached the host
+            steps[b]()
+            ev_done[b].record(s)
+            with torch.cuda.stream(c):                # D2H of step i's result
+                c.wait_event(ev_done[b])
+                yh[b].copy_(Y[b], non_blocking=True)
+                ev_out[b].record(c)
         s.wait_stream(c)
-    run(2)
+    loop(2)
     barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(s)
-    run(n)
+    loop(n)
     t1.record(s)
     barrier()
+    W.params = p0
+    if has_x:
+        W.ins[0] = x0
     ms = t0.elapsed_time(t1) / n
     if world > 1:
         import torch.distributed as dist
@@ -550,10 +579,10 @@ def e2e_run(W, torch, world, pg, args, barrier, step):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     return {"value": len(W.layers) / (ms * 1e-3), "unit": "layers/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": int(ph.numel() * 4 + (xh.numel() * 2 if X_st is not None else 0)),
-            "d2h_bytes_per_step": int(yh.numel() * yh.element_size()),
-            "launch": ("CUDA graph(s) per step; H2D of step i+1 and D2H of step i on a copy stream overlapping "
-                       "step i's compute" if step is not None else "eager")}
+            "h2d_bytes_per_step": int(ph.numel() * 4 + (xh.numel() * 2 if has_x else 0)),
+            "d2h_bytes_per_step": int(Y[0].numel() * Y[0].element_size()),
+            "launch": ("CUDA graph(s) per step and buffer set; H2D of step i+1 and D2H of step i on a copy stream "
+                       "overlapping step i's compute (two buffer sets)" if graphs_ok else "eager")}
 
 
 # ------------------------------------------------------------------ oracle (CPU) legs

@@ -246,6 +246,24 @@ orth_status_t orth_kernels_assemble(orth_plan_t plan, const float* gathered_f32,
  * first device-side error since the last check (or a pending CUDA error). */
 orth_status_t orth_plan_check(orth_plan_t plan, void* stream);
 
+/* ---- f2: GPU spectral certification (App. C "scalable spectral norm
+ * estimation ... check that the produced bounds are valid").
+ * For layer `layer`'s FP32 kernel (PyTorch layout, as orth_compose_kernel writes it) and the circular
+ * operator of its forward conv on an H x W grid (s | H, s | W; dense layers: H = W = 1), per group and per
+ * frequency (f1, f2) of the (H/s) x (W/s) polyphase grid: E = M^H M - I on the short side of the
+ * symbol M (c_out/g x (c_in/g) s^2), computed in FP64 from the FP32 values.
+ *   out[((g * H/s + f1) * W/s + f2) * 2 + 0] = |E|_F   -- certificate: max|sigma - 1| <= max|sigma^2 - 1|
+ *                                                          = |E|_2 <= |E|_F at that frequency;
+ *   out[... + 1]                             = |E z|    -- power_iters power iterations of E from a fixed
+ *                                                          start: a lower bound converging to |E|_2.
+ * out: caller-owned device FP64 array; workspace: caller-owned device memory of at least
+ * orth_certify_workspace(...) bytes (16-byte aligned).  Asynchronous on `stream`.  Errors:
+ * SHAPE_MISMATCH (s does not divide H or W, dense with H*W != 1), INVALID_ARGUMENT (NULLs, small
+ * workspace, power_iters < 0). */
+orth_status_t orth_certify_workspace(orth_plan_t plan, int32_t layer, int32_t H, int32_t W, int64_t* bytes);
+orth_status_t orth_certify(orth_plan_t plan, int32_t layer, const float* kernel_f32, int32_t H, int32_t W,
+                           int32_t power_iters, void* workspace, int64_t workspace_bytes, double* out, void* stream);
+
 /* ---- tracing: per-call timing of the plan's kernel groups ----------------------------
  * orth_plan_trace(plan, 1) makes every compute call bracket each group of kernels it launches (the
  * power pass, the NS launch, the composition, the emit, one conv call, ...) with a pair of CUDA events
@@ -263,7 +281,8 @@ typedef enum {
   ORTH_TK_EMIT = 6,         /* kernels into the FP32 / BF16 layouts */
   ORTH_TK_CONV_FWD = 7,     /* one orth_conv_forward (variant = orth_conv_variant_t) */
   ORTH_TK_CONV_ADJ = 8,     /* one orth_conv_transpose */
-  ORTH_TK_ASSEMBLE = 9      /* orth_kernels_assemble */
+  ORTH_TK_ASSEMBLE = 9,     /* orth_kernels_assemble */
+  ORTH_TK_CERTIFY = 10      /* orth_certify */
 } orth_trace_kind_t;
 typedef enum {             /* which conv kernel a conv call ran */
   ORTH_CV_NONE = 0, ORTH_CV_SIMT = 1, ORTH_CV_SMALLK = 2, ORTH_CV_STEM = 3,

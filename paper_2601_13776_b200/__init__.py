@@ -42,7 +42,7 @@ _MODE = {"zeros": PAD_ZEROS, "circular": PAD_CIRCULAR}
 
 
 TRACE_KINDS = {1: "power", 2: "scale", 3: "ns", 4: "ns_check", 5: "compose", 6: "emit", 7: "conv_fwd",
-               8: "conv_adj", 9: "assemble"}
+               8: "conv_adj", 9: "assemble", 10: "certify"}
 CONV_VARIANTS = {0: "none", 1: "conv_fwd_simt/conv_bwd_simt", 2: "conv_fwd_smallk", 3: "conv_stem_tc",
                  4: "conv_pad<64,swapped>", 5: "conv_pad<BN>", 6: "conv_stack (+pad_kernel)", 7: "conv_tma",
                  8: "conv_ws<256>", 9: "conv_ws<128>", 10: "conv_ws<64>", 11: "conv_ws<32>", 12: "conv_pair"}
@@ -78,6 +78,8 @@ _sig = {
     "orth_conv_transpose": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
     "orth_kernels_assemble": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "orth_plan_check": (C.c_int, [_P, _P]),
+    "orth_certify_workspace": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
+    "orth_certify": (C.c_int, [_P, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64, _P, _P]),
     "orth_plan_trace": (C.c_int, [_P, C.c_int32]),
     "orth_plan_trace_read": (C.c_int, [_P, C.POINTER(TraceRec), C.c_int32, C.POINTER(C.c_int32)]),
     "orth_plan_launch_count": (C.c_int64, [_P]),
@@ -200,6 +202,18 @@ def orth_kernels_assemble(h: int, gathered_f32, kernels_f32, gathered_bf16=None,
                                       _ptr(kernels_bf16), _stream(stream)), "orth_kernels_assemble")
 
 
+def orth_certify_workspace(h: int, layer: int, H: int, W: int) -> int:
+    out = C.c_int64()
+    _check(_lib.orth_certify_workspace(h, layer, H, W, C.byref(out)), "orth_certify_workspace")
+    return out.value
+
+
+def orth_certify(h: int, layer: int, kernel_f32, H: int, W: int, power_iters: int, workspace, out, stream=None):
+    _check(_lib.orth_certify(h, layer, _ptr(kernel_f32), H, W, power_iters, _ptr(workspace),
+                             workspace.numel() * workspace.element_size(), _ptr(out), _stream(stream)),
+           "orth_certify")
+
+
 def orth_plan_check(h: int, stream=None):
     _check(_lib.orth_plan_check(h, _stream(stream)), "orth_plan_check (device status)")
 
@@ -320,6 +334,20 @@ class Plan:
 
     def check(self, stream=None):
         orth_plan_check(self.h, stream)
+
+    def certify(self, l: int, kernel_f32, H: int, W: int, power_iters: int = 30, workspace=None, stream=None):
+        """f2: per (group, frequency) [|E|_F, power estimate of |E|_2] (FP64 tensor on the kernel's device),
+        shape (g, H/s, W/s, 2); E = M^H M - I of the circular operator's symbol on the short side."""
+        import torch
+        nb = orth_certify_workspace(self.h, l, H, W)
+        if workspace is None:
+            workspace = torch.empty(nb, dtype=torch.uint8, device=kernel_f32.device)
+        d = self.layers[l]
+        s = 1 if d.get("kind") == "dense" else d.get("s", 1)
+        g = 1 if d.get("kind") == "dense" else d.get("g", 1)
+        out = torch.empty((g, H // s, W // s, 2), dtype=torch.float64, device=kernel_f32.device)
+        orth_certify(self.h, l, kernel_f32, H, W, power_iters, workspace, out, stream)
+        return out
 
     def trace(self, enable: bool = True):
         orth_plan_trace(self.h, enable)

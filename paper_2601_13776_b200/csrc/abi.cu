@@ -292,6 +292,36 @@ orth_status_t orth_kernels_assemble(orth_plan_t plan, const float* gathered_f32,
   return cuda_fail(e, "orth_kernels_assemble");
 }
 
+orth_status_t orth_certify_workspace(orth_plan_t plan, int32_t layer, int32_t H, int32_t W, int64_t* bytes) {
+  if (!plan || !bytes) { set_error("NULL plan or bytes"); return ORTH_ERR_INVALID_ARGUMENT; }
+  Plan& P = plan->p;
+  if (layer < 0 || layer >= (int)P.layers.size()) { set_error("layer %d out of range", layer); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (H < 1 || W < 1) { set_error("H, W must be >= 1"); return ORTH_ERR_SHAPE_MISMATCH; }
+  const int64_t b = certify_workspace_bytes(P.layers[layer], H, W);
+  if (b < 0) { set_error("grid %dx%d does not fit layer %d (s | H, s | W; dense: 1x1)", H, W, layer); return ORTH_ERR_SHAPE_MISMATCH; }
+  *bytes = b;
+  return ORTH_OK;
+}
+
+orth_status_t orth_certify(orth_plan_t plan, int32_t layer, const float* kernel_f32, int32_t H, int32_t W,
+                           int32_t power_iters, void* workspace, int64_t workspace_bytes, double* out, void* stream) {
+  orth_status_t st = need_device(plan);
+  if (st != ORTH_OK) return st;
+  int64_t need = 0;
+  st = orth_certify_workspace(plan, layer, H, W, &need);
+  if (st != ORTH_OK) return st;
+  if (!kernel_f32 || !workspace || !out) { set_error("NULL kernel, workspace or out"); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (workspace_bytes < need) { set_error("workspace %lld < %lld bytes", (long long)workspace_bytes, (long long)need); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (power_iters < 0) { set_error("power_iters must be >= 0"); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (((uintptr_t)workspace | (uintptr_t)out) & 15) { set_error("workspace/out must be 16-byte aligned"); return ORTH_ERR_INVALID_ARGUMENT; }
+  Plan& P = plan->p;
+  NvtxRange nv("orth_certify");
+  Trace tr(P, ORTH_TK_CERTIFY, layer, stream);
+  const int e = launch_certify(P.layers[layer], kernel_f32, H, W, power_iters, workspace, out, stream);
+  P.launches += 3;
+  return cuda_fail(e, "orth_certify");
+}
+
 orth_status_t orth_plan_trace(orth_plan_t plan, int32_t enable) {
   orth_status_t st = need_device(plan);
   if (st != ORTH_OK) return st;

@@ -329,6 +329,10 @@ int launch_residual(Plan& p, float* residual_out, void* stream);
 // NOT_CONVERGED when r is non-finite or 3/4 r^2 + 1/4 r^3 > tol (tol > 0)
 int launch_converged_check(Plan& p, int is_r, float tol, void* stream);
 void orth_plan_trace_free(Plan& p);   // abi.cu
+// f2: spectral certificate (certify.cu); workspace bytes (-1: not applicable) and the launch
+int64_t certify_workspace_bytes(const LayerInfo& L, int H, int W);
+int launch_certify(const LayerInfo& L, const float* kernel, int H, int W, int iters, void* ws, double* out,
+                   void* stream);
 // a8: copy every unit from the gather layout to the final layout
 int launch_assemble(Plan& p, const float* gf, float* kf, const uint16_t* gb, uint16_t* kb, void* stream);
 // per-layer conv scratch (bytes) for calls up to N x Hbig x Wbig (forward-conv input grid), both

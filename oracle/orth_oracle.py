@@ -37,6 +37,7 @@ __all__ = [
     "out_size", "conv2d", "conv_transpose2d",
     "toeplitz", "fft_singular_values", "polyphase_singular_values",
     "conv_singular_values", "spectral_certificate",
+    "soc_skew", "aol_scale", "soc_exp_kernel",
 ]
 
 
@@ -485,3 +486,62 @@ def spectral_certificate(K: np.ndarray, L: Layer, H: int, W: int):
                 spec[gi, f1, f2] = np.abs(np.linalg.eigvalsh(E)).max()
                 sig_dev = max(sig_dev, float(np.abs(np.linalg.svd(M, compute_uv=False) - 1).max()))
     return frob, spec, sig_dev
+
+
+# ---------------------------------------------------------------------------
+# f3: Adaptive-SOC explicit exponential (§3 "Adaptive-SOC"; P:349-361
+# App. B.2 Theorem "Explicit conv exponential"; readings R25-R27)
+# ---------------------------------------------------------------------------
+def soc_skew(K: np.ndarray) -> np.ndarray:
+    """Skew-symmetrised free kernel (S:262 step 1): L[a, b, i, j] = (K[a, b, i, j] - K[b, a, k-1-i, k-1-j]) / 2.
+    With centred padding (odd k) the circular operator of L is skew-adjoint: T(L)^T = -T(L)."""
+    K = np.asarray(K, np.float64)
+    return 0.5 * (K - np.transpose(K, (1, 0, 2, 3))[:, :, ::-1, ::-1])
+
+
+def aol_scale(L: np.ndarray) -> float:
+    """Scalar AOL normalisation (S:262 step 2, "We used 'AOL'", S:269-276 aol_rescale; reading R26):
+    V[i, j, Delta] = sum_o sum_t L[o, i, t] L[o, j, t + Delta] (the full cross-correlation of the kernel with
+    itself, contracted over output channels), d_i = sum_j sum_Delta |V[i, j, Delta]|.  AOL: |T D^{-1/2}| <= 1,
+    hence |T(L)| <= max_i sqrt(d_i); the returned alpha = 1 / max_i sqrt(d_i) gives |T(alpha L)| <= 1 while
+    keeping alpha L skew (a per-channel rescale would not).  d = 0 (L = 0) -> alpha = 1."""
+    L = np.asarray(L, np.float64)
+    co, ci, k1, k2 = L.shape
+    d = np.zeros(ci)
+    for da in range(-(k1 - 1), k1):
+        for db in range(-(k2 - 1), k2):
+            V = np.zeros((ci, ci))
+            for a in range(k1):
+                for b in range(k2):
+                    a2, b2 = a + da, b + db
+                    if 0 <= a2 < k1 and 0 <= b2 < k2:
+                        V += L[:, :, a, b].T @ L[:, :, a2, b2]
+            d += np.abs(V).sum(axis=1)
+    m = float(np.sqrt(d.max()))
+    return 1.0 / m if m > 0 else 1.0
+
+
+def soc_exp_kernel(K: np.ndarray, terms: int):
+    """Explicit exponential kernel (eq. "(Id + K + K(*)K/2! + K(*)K(*)K/3! + ...) * x"):
+    L = alpha soc_skew(K) (alpha = aol_scale), E = delta + sum_{j=1..terms} L^{(*) j} / j!, every term centred
+    in the (terms (k-1) + 1)^2 output (odd k: "same" padding composes by adding the pads).  Returns (E, alpha)."""
+    K = np.asarray(K, np.float64)
+    c, c2, k, k2 = K.shape
+    if c != c2 or k != k2 or k % 2 == 0:
+        raise ValueError("SOC needs a square channel map and an odd square kernel")
+    Ls = soc_skew(K)
+    alpha = aol_scale(Ls)
+    L = alpha * Ls
+    kn = terms * (k - 1) + 1
+    E = np.zeros((c, c, kn, kn))
+    ctr = (kn - 1) // 2
+    E[:, :, ctr, ctr] = np.eye(c)
+    P = np.eye(c)[:, :, None, None]
+    fact = 1.0
+    for j in range(1, terms + 1):
+        P = block_conv(P, L)
+        fact *= j
+        off = (terms - j) * (k - 1) // 2
+        kj = P.shape[2]
+        E[:, :, off:off + kj, off:off + kj] += P / fact
+    return E, alpha

@@ -424,3 +424,74 @@ def test_spectral_certificate_orthogonal_and_dense():
     Ld = O.Layer(5, 5, 1, kind="dense")
     frob, spec, _ = O.spectral_certificate(2 * np.eye(5), Ld, 1, 1)
     assert frob.shape == (1, 1, 1) and abs(frob[0, 0, 0] - 3 * np.sqrt(5)) < 1e-12 and abs(spec[0, 0, 0] - 3) < 1e-12
+
+
+# ------------------------------------------------------------------ f3: SOC explicit exponential
+def _circ(K, x, d=1):
+    """torch-CPU f64 circular 'same' conv (independent of the oracle's conv2d)."""
+    k = K.shape[2]
+    p = d * (k - 1) // 2
+    xt = F.pad(t64(x), (p, p, p, p), mode="circular")
+    return F.conv2d(xt, t64(K), dilation=d).numpy()
+
+
+def test_soc_degenerate_cases():
+    """K = 0 -> the identity kernel; a symmetric free kernel (K[a,b,i,j] = K[b,a,k-1-i,k-1-j]) has a
+    zero skew part -> identity."""
+    E, _ = O.soc_exp_kernel(np.zeros((3, 3, 3, 3)), 4)
+    I = np.zeros((3, 3, 9, 9)); I[:, :, 4, 4] = np.eye(3)
+    assert np.array_equal(E, I)
+    A = rs.standard_normal((3, 3, 3, 3))
+    S = A + np.transpose(A, (1, 0, 2, 3))[:, :, ::-1, ::-1]
+    assert np.abs(O.soc_skew(S)).max() < 1e-15
+    E, _ = O.soc_exp_kernel(S, 3)
+    assert np.abs(E - I[:, :, 1:8, 1:8]).max() < 1e-15
+
+
+@pytest.mark.parametrize("c,k,d", [(4, 3, 1), (3, 5, 1), (4, 3, 2)])
+def test_soc_skew_adjoint_and_aol_bound(c, k, d):
+    """Toeplitz brute force: T(soc_skew(K)) is skew (T^T = -T) on a circular grid, and the AOL scalar makes
+    |T(alpha L)|_2 <= 1 (S:274 certified upper bound)."""
+    K = rs.standard_normal((c, c, k, k))
+    L = O.soc_skew(K)
+    H = 2 * d * (k - 1) + 3
+    T = O.toeplitz(lambda x: _circ(L, x, d), (c, H, H))
+    assert np.abs(T + T.T).max() < 1e-12
+    a = O.aol_scale(L)
+    assert np.linalg.svd(a * T, compute_uv=False)[0] <= 1 + 1e-12
+    # S:275: 1x1 kernel = 2I -> d_i = 4 -> alpha = 1/2
+    assert abs(O.aol_scale(2 * np.eye(3)[:, :, None, None]) - 0.5) < 1e-15
+
+
+@pytest.mark.parametrize("c,k,terms,d", [(4, 3, 6, 1), (3, 3, 8, 2), (2, 5, 4, 1)])
+def test_soc_explicit_equals_implicit_and_expm(c, k, terms, d):
+    """the explicit kernel applied once equals the implicit series x + L*x + L*L*x/2! + ... applied
+    term by term (torch-CPU conv, S:266 example), and its circular operator equals the truncated matrix
+    exponential sum_j T(L)^j / j! of the Toeplitz matrix (brute force); against scipy's expm of T(L) it is
+    off only by the tail bound e |T(L)|^{n+1} / (n+1)!, so it is orthogonal to that accuracy."""
+    import scipy.linalg
+    K = rs.standard_normal((c, c, k, k))
+    E, alpha = O.soc_exp_kernel(K, terms)
+    L = alpha * O.soc_skew(K)
+    Hx = max(10, d * (E.shape[2] - 1) // 2 + 2)
+    for _ in range(3):
+        x = rs.standard_normal((1, c, Hx, Hx))
+        imp, term = x.copy(), x.copy()
+        for j in range(1, terms + 1):
+            term = _circ(L, term, d) / j
+            imp = imp + term
+        assert np.abs(_circ(E, x, d) - imp).max() < 1e-10 * max(1.0, np.abs(imp).max())
+    H = max(7, d * (E.shape[2] - 1) // 2 + 2)
+    TL = O.toeplitz(lambda z: _circ(L, z, d), (c, H, H))
+    TE = O.toeplitz(lambda z: _circ(E, z, d), (c, H, H))
+    acc, P = np.eye(TL.shape[0]), np.eye(TL.shape[0])
+    for j in range(1, terms + 1):
+        P = P @ TL / j
+        acc = acc + P
+    assert np.abs(TE - acc).max() < 1e-11
+    nrm = np.linalg.svd(TL, compute_uv=False)[0]
+    assert nrm <= 1 + 1e-12
+    tail = math.e * nrm ** (terms + 1) / math.factorial(terms + 1)
+    assert np.linalg.norm(TE - scipy.linalg.expm(TL), 2) <= tail + 1e-12
+    sv = np.linalg.svd(TE, compute_uv=False)
+    assert np.abs(sv - 1).max() <= tail + 1e-12

@@ -70,7 +70,7 @@ typedef enum {
 
 typedef enum { ORTH_F32 = 0, ORTH_BF16 = 1, ORTH_BF16X3 = 2 } orth_dtype_t;
 typedef enum { ORTH_PAD_ZEROS = 0, ORTH_PAD_CIRCULAR = 1 } orth_pad_t;
-typedef enum { ORTH_CONV2D = 0, ORTH_CONV_TRANSPOSE2D = 1, ORTH_DENSE = 2 } orth_kind_t;
+typedef enum { ORTH_CONV2D = 0, ORTH_CONV_TRANSPOSE2D = 1, ORTH_DENSE = 2, ORTH_SOC = 3 } orth_kind_t;
 typedef enum { ORTH_PRESCALE_POWER = 0, ORTH_PRESCALE_FROBENIUS = 1 } orth_prescale_t;
 
 /* One orthogonal layer (S:35-40 ConvSpec + S:205-210 ConvLayerConfig).
@@ -80,6 +80,12 @@ typedef enum { ORTH_PRESCALE_POWER = 0, ORTH_PRESCALE_FROBENIUS = 1 } orth_presc
  *    adjoint conv c_out -> c_in, PyTorch ConvTranspose2d weight layout
  *    (c_in, c_out/g, k, k) (R13).
  *  kind ORTH_DENSE: an OrthoLinear weight c_out x c_in; k = s = d = 1.
+ *  kind ORTH_SOC: AdaptiveSOCConv2d (App. B.2): the free parameter of each group is a
+ *    kernel (c/g, c/g, k, k) (k odd, c_in = c_out, s = 1), packed as one c/g x (c/g) k^2 "matrix" (role K)
+ *    that orth_orthogonalize passes through unchanged; orth_compose_kernel builds the EXPLICIT exponential
+ *    E = delta + L + L(*)L/2! + ... + L^(*)n/n!, L = alpha skew(K), alpha the scalar AOL bound (R25-R27),
+ *    of spatial size k_eff = n (k - 1) + 1, n = soc_terms (0 -> 6); conv calls apply E ("same" padding of
+ *    k_eff).  Circular padding makes the layer orthogonal up to the series tail e/(n+1)!.
  *  Square kernels/strides/dilations only (k_h == k_w, ...).  pad_* = -1 selects
  *  the "same" rule p_t = floor(d(k-1)/2), p_b = d(k-1) - p_t (R11).
  *  grid_h, grid_w: the largest spatial size the layer's conv calls will see on
@@ -99,6 +105,7 @@ typedef struct {
   int32_t pad_t, pad_b, pad_l, pad_r;
   int32_t padding_mode;  /* orth_pad_t */
   int32_t grid_h, grid_w;
+  int32_t soc_terms;     /* ORTH_SOC: highest power n of the series (0 -> 6); ignored otherwise */
 } orth_layer_desc_t;
 
 /* OrthoParams, Bjorck only. */
@@ -166,6 +173,7 @@ typedef enum {
   ORTH_Q_LAYER_C_MID = 26,        /* derived internal width (R7); 0 if none */
   ORTH_Q_LAYER_C_B = 27,          /* BCOP width; 0 if none */
   ORTH_Q_LAYER_KP = 28,           /* BCOP size k' (R8); 0 if none */
+  ORTH_Q_LAYER_K_EFF = 32,        /* kernel size of the applied kernel (SOC: n (k - 1) + 1; else k) */
   ORTH_Q_LAYER_SCRATCH_BYTES = 29,/* this layer's conv scratch slice */
   ORTH_Q_LAYER_NS_FLOPS = 30,     /* 4 m n^2 T over the layer's matrices (all groups) */
   ORTH_Q_LAYER_COMP_FLOPS = 31,   /* structured composition flops of the layer (all groups) */
@@ -175,7 +183,7 @@ typedef enum {
   ORTH_Q_MATRIX_CACHE_OFFSET = 43,/* float offset of its length-n vector in the power cache */
   ORTH_Q_MATRIX_LAYER = 44,
   ORTH_Q_MATRIX_GROUP = 45,
-  ORTH_Q_MATRIX_ROLE = 46,        /* 0 Q, 1 U, 2 R, 3 W */
+  ORTH_Q_MATRIX_ROLE = 46,        /* 0 Q, 1 U, 2 R, 3 W, 4 K (SOC free kernel, not orthogonalised) */
   ORTH_Q_UNIT_LAYER = 60,         /* units are ordered layer -> group */
   ORTH_Q_UNIT_GROUP = 61,
   ORTH_Q_UNIT_OWNER = 62,         /* rank that orthogonalises and composes this unit */

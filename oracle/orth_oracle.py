@@ -59,6 +59,7 @@ class Layer:
     kind: str = "conv"
     padding_mode: str = "circular"
     pad: Optional[Tuple[int, int, int, int]] = None
+    terms: int = 6          # 'soc' (f3): highest power of the explicit exponential series
 
     def fwd_channels(self) -> Tuple[int, int]:
         """(c_in, c_out) of the forward conv whose kernel is built.  A
@@ -96,6 +97,8 @@ def layer_geometry(L: Layer) -> dict:
     ci, co = ci_f // L.g, co_f // L.g
     if L.kind == "dense":
         return dict(ci=ci, co=co, kind="dense", kp=0, c_b=0, c_mid=0)
+    if L.kind == "soc":
+        return dict(ci=ci, co=co, kind="soc", kp=0, c_b=0, c_mid=0)
     if L.s == 1:
         return dict(ci=ci, co=co, kind="bcop", kp=L.k, c_b=max(ci, co), c_mid=0)
     if L.k == L.s:
@@ -111,6 +114,8 @@ def layer_matrices(L: Layer) -> List[MatrixSpec]:
     geo = layer_geometry(L)
     if geo["kind"] == "dense":
         return [MatrixSpec("W", geo["co"], geo["ci"])]
+    if geo["kind"] == "soc":     # f3: the free kernel (c, c, k, k) as a c x c k^2 matrix, not orthogonalised
+        return [MatrixSpec("K", geo["co"], geo["ci"] * L.k * L.k)]
     out: List[MatrixSpec] = []
     if geo["kind"] in ("bcop", "aoc"):
         c = geo["c_b"]
@@ -276,6 +281,9 @@ def layer_kernel(L: Layer, group_mats: Sequence[Sequence[np.ndarray]]) -> np.nda
         mats = [np.asarray(M, np.float64) for M in mats]
         if geo["kind"] == "dense":
             ks.append(mats[0])
+            continue
+        if geo["kind"] == "soc":
+            ks.append(soc_exp_kernel(mats[0].reshape(geo["co"], geo["ci"], L.k, L.k), L.terms)[0])
             continue
         if geo["kind"] == "bcop":
             ks.append(bcop(mats[0], mats[1:], geo["co"], geo["ci"]))

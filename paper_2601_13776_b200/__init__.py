@@ -26,18 +26,18 @@ _lib = C.CDLL(_LIB_PATH)
 OK, INVALID_ARGUMENT, UNSUPPORTED_CONFIG, SHAPE_MISMATCH, ZERO_NORM, NOT_CONVERGED, CUDA_ERR, OOM, NO_DEVICE = range(9)
 F32, BF16, BF16X3 = 0, 1, 2
 PAD_ZEROS, PAD_CIRCULAR = 0, 1
-CONV2D, CONV_TRANSPOSE2D, DENSE = 0, 1, 2
+CONV2D, CONV_TRANSPOSE2D, DENSE, SOC = 0, 1, 2, 3
 PRESCALE_POWER, PRESCALE_FROBENIUS = 0, 1
 Q = dict(N_LAYERS=0, N_MATRICES=1, PARAMS_NUMEL=2, CACHE_NUMEL=3, KERNELS_F32_NUMEL=4, KERNELS_BF16_NUMEL=5,
          WORKSPACE_BYTES=6, NS_FLOPS=7, KERNEL_SEGMENT_F32=8, KERNEL_SEGMENT_BF16=9, N_UNITS=10,
          GATHER_F32_NUMEL=11, GATHER_BF16_NUMEL=12, CONV_SCRATCH_BYTES=13, COMP_FLOPS=14,
          LAYER_FIRST_MATRIX=20, LAYER_MATS_PER_GROUP=21, LAYER_KERNEL_OFF_F32=22, LAYER_KERNEL_OFF_BF16=23,
-         LAYER_KERNEL_NUMEL=24, LAYER_OWNER=25, LAYER_C_MID=26, LAYER_C_B=27, LAYER_KP=28, LAYER_SCRATCH_BYTES=29, LAYER_NS_FLOPS=30, LAYER_COMP_FLOPS=31,
+         LAYER_KERNEL_NUMEL=24, LAYER_OWNER=25, LAYER_C_MID=26, LAYER_C_B=27, LAYER_KP=28, LAYER_SCRATCH_BYTES=29, LAYER_NS_FLOPS=30, LAYER_COMP_FLOPS=31, LAYER_K_EFF=32,
          MATRIX_ROWS=40, MATRIX_COLS=41, MATRIX_OFFSET=42, MATRIX_CACHE_OFFSET=43, MATRIX_LAYER=44,
          MATRIX_GROUP=45, MATRIX_ROLE=46, UNIT_LAYER=60, UNIT_GROUP=61, UNIT_OWNER=62, UNIT_NUMEL=63,
          UNIT_GATHER_OFF_F32=64, UNIT_GATHER_OFF_BF16=65, UNIT_KERNEL_OFF_F32=66, UNIT_KERNEL_OFF_BF16=67)
-ROLES = {0: "Q", 1: "U", 2: "R", 3: "W"}
-_KIND = {"conv": CONV2D, "convT": CONV_TRANSPOSE2D, "dense": DENSE}
+ROLES = {0: "Q", 1: "U", 2: "R", 3: "W", 4: "K"}
+_KIND = {"conv": CONV2D, "convT": CONV_TRANSPOSE2D, "dense": DENSE, "soc": SOC}
 _MODE = {"zeros": PAD_ZEROS, "circular": PAD_CIRCULAR}
 
 
@@ -56,7 +56,7 @@ class TraceRec(C.Structure):
 class LayerDesc(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("kind", "c_in", "c_out", "k_h", "k_w", "stride_h", "stride_w", "dil_h",
                                          "dil_w", "groups", "pad_t", "pad_b", "pad_l", "pad_r", "padding_mode",
-                                         "grid_h", "grid_w")]
+                                         "grid_h", "grid_w", "soc_terms")]
 
 
 class Opts(C.Structure):
@@ -123,7 +123,8 @@ def layer_desc(d: Dict) -> LayerDesc:
     k, s, dl = d.get("k", 3), d.get("s", 1), d.get("d", 1)
     gh, gw = layer_grid(d) if d.get("kind", "conv") != "dense" else (0, 0)
     return LayerDesc(_KIND[d.get("kind", "conv")], d["c_in"], d["c_out"], k, k, s, s, dl, dl, d.get("g", 1),
-                     pads[0], pads[1], pads[2], pads[3], _MODE[d.get("padding_mode", "circular")], gh, gw)
+                     pads[0], pads[1], pads[2], pads[3], _MODE[d.get("padding_mode", "circular")], gh, gw,
+                     d.get("terms", 0))
 
 
 def make_opts(**kw) -> Opts:
@@ -274,7 +275,7 @@ class Plan:
                                 kf32_off=q("LAYER_KERNEL_OFF_F32", l), kbf16_off=q("LAYER_KERNEL_OFF_BF16", l),
                                 numel=q("LAYER_KERNEL_NUMEL", l), owner=q("LAYER_OWNER", l),
                                 c_mid=q("LAYER_C_MID", l), c_b=q("LAYER_C_B", l), kp=q("LAYER_KP", l),
-                                scratch=q("LAYER_SCRATCH_BYTES", l))
+                                scratch=q("LAYER_SCRATCH_BYTES", l), k_eff=q("LAYER_K_EFF", l))
                            for l in range(self.n_layers)]
 
     # -- shapes ---------------------------------------------------------
@@ -287,7 +288,8 @@ class Plan:
         if d.get("kind") == "dense":
             return (d["c_out"], d["c_in"])
         ci, co = self.fwd_channels(l)
-        return (co, ci // d.get("g", 1), d.get("k", 3), d.get("k", 3))
+        k = self.layer_info[l]["k_eff"]
+        return (co, ci // d.get("g", 1), k, k)
 
     def kernel_f32(self, kf32, l: int):
         info = self.layer_info[l]
@@ -301,7 +303,7 @@ class Plan:
 
     def out_hw(self, l: int, H: int, W: int):
         d = self.layers[l]
-        k, s, dl = d.get("k", 3), d.get("s", 1), d.get("d", 1)
+        k, s, dl = self.layer_info[l]["k_eff"], d.get("s", 1), d.get("d", 1)
         pads = d.get("pad")
         if pads is None:
             e = dl * (k - 1)

@@ -118,8 +118,15 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
   Plan& P = plan->p;
   if (!params || !ortho_out) { set_error("NULL params or ortho_out"); return ORTH_ERR_INVALID_ARGUMENT; }
   if (params == ortho_out) { set_error("params and ortho_out must not overlap"); return ORTH_ERR_INVALID_ARGUMENT; }
-  if (P.mat_items.empty()) return ORTH_OK;
   NvtxRange nv("orth_orthogonalize");
+  // SOC free kernels (role K) pass through unchanged: orth_compose_kernel reads every unit from ortho
+  for (size_t i = 0; i + 1 < P.soc_copy.size(); i += 2) {
+    const cudaError_t ce = cudaMemcpyAsync(ortho_out + P.soc_copy[i], params + P.soc_copy[i],
+                                           (size_t)P.soc_copy[i + 1] * sizeof(float), cudaMemcpyDeviceToDevice,
+                                           (cudaStream_t)stream);
+    if (ce != cudaSuccess) return cuda_fail((int)ce, "orth_orthogonalize (SOC copy)");
+  }
+  if (P.mat_items.empty()) return ORTH_OK;
   const int T = P.opts.ns_iters;
   float* bufs[BUF_COUNT] = {ortho_out, P.d_scratch, P.d_gram, P.d_comp};
   // X0 goes where T swaps leave the result in ortho_out
@@ -228,6 +235,12 @@ orth_status_t orth_compose_kernel(orth_plan_t plan, const float* ortho, float* k
       gemm(P.aoc);
     } else {
       e = launch_compose_tc(P, ortho, stream);
+    }
+    if (!e && !P.soc.empty()) {   // f3: explicit exponentials of the SOC units
+      e = launch_soc_skew(P, ortho, stream);
+      for (auto& ph : P.soc_pow) gemm(ph);
+      if (!e) e = launch_soc_alpha(P, stream);
+      if (!e) e = launch_soc_sum(P, stream);
     }
   }
   if (!e) {

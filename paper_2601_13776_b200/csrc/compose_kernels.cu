@@ -35,6 +35,17 @@ __global__ void __launch_bounds__(128) emit_kernel(const EmitItem* __restrict__ 
   for (int o = blockIdx.x; o < e.co; o += gridDim.x) {
     float* f = kf32 + e.f32_off + (int64_t)o * slab;
     __nv_bfloat16* bq = kbf16 ? kbf16 + e.bf16_off + (int64_t)o * slab : nullptr;
+    if (e.mode == 2) {   // tap-major without the shared-memory row stage (large k^2 ci rows: SOC E)
+      for (int i = threadIdx.x; i < ci; i += 128) {
+        const float* col = src + (int64_t)o * e.ld + i;
+        for (int t = 0; t < kk; ++t) {
+          const float v = __ldg(col + (int64_t)t * e.tap_stride);
+          f[(int64_t)i * kk + t] = v;
+          if (bq) bq[(int64_t)t * ci + i] = __float2bfloat16_rn(v);
+        }
+      }
+      continue;
+    }
     if (e.mode == 1) {   // RKO: K[o, i, t] = R[o, i*s^2 + t] (k = s): the FP32 row is a straight copy
       const float* row = src + (int64_t)o * slab;
       for (int x = threadIdx.x; x < slab; x += 128) f[x] = __ldg(row + x);
@@ -98,7 +109,7 @@ int launch_emit(Plan& p, const float* const bufs[BUF_COUNT], float* kf32, uint16
   size_t smem = 16;
   for (auto& e : p.emit) {
     maxco = e.co > maxco ? e.co : maxco;
-    smem = std::max(smem, (size_t)e.k * e.k * e.ci * sizeof(float));
+    if (e.mode != 2) smem = std::max(smem, (size_t)e.k * e.k * e.ci * sizeof(float));
   }
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {

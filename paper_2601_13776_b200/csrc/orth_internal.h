@@ -12,8 +12,8 @@ struct CUtensorMap_st;   // cuda.h (TMA descriptors), forward-declared for the l
 
 namespace orth {
 
-enum Role : int32_t { ROLE_Q = 0, ROLE_U = 1, ROLE_R = 2, ROLE_W = 3 };
-enum Construct : int32_t { CONS_BCOP = 0, CONS_RKO = 1, CONS_AOC = 2, CONS_DENSE = 3 };
+enum Role : int32_t { ROLE_Q = 0, ROLE_U = 1, ROLE_R = 2, ROLE_W = 3, ROLE_K = 4 };
+enum Construct : int32_t { CONS_BCOP = 0, CONS_RKO = 1, CONS_AOC = 2, CONS_DENSE = 3, CONS_SOC = 4 };
 enum BufId : int32_t { BUF_NONE = -1, BUF_X = 0, BUF_Y = 1, BUF_G = 2, BUF_W = 3, BUF_COUNT = 4 };
 
 constexpr int kPadF32 = 32;    // 128 B alignment of every packed float object
@@ -40,6 +40,7 @@ struct LayerInfo {
   int32_t k, s, d, g;
   int32_t pt, pb, pl, pr;
   int32_t kp, c_b, c_mid;
+  int32_t k_free, soc_terms;    // ORTH_SOC: free kernel size and series order (k = k_eff for the conv)
   int32_t first_mat, mats_per_group;
   int32_t owner;                // owner of group 0 (ORTH_Q_LAYER_OWNER)
   int32_t first_unit;           // units [first_unit, first_unit + g) of Plan::units
@@ -170,6 +171,17 @@ struct CompUnit {
   int rows, c;               // chain tap = rows x c (row subset when only [:co] is kept)
 };
 
+// f3: one SOC unit (layer, group) of the explicit-exponential construction (soc.cu).  Offsets are floats
+// in the composition workspace (tap-major c x c matrices), except src_off (ortho / params).
+constexpr int kSocMaxTerms = 16;
+struct SocItem {
+  int32_t c, k, kn, terms;        // width, free kernel size, k_eff, series order
+  int32_t alpha_slot, pad_[3];
+  int64_t src_off;                // free kernel (PyTorch layout (c, c, k, k)) in ortho
+  int64_t e_off;                  // E (kn^2 taps)
+  int64_t u_off[kSocMaxTerms + 1];   // u_off[1] = S (skew part), u_off[j] = S^(*)j, j >= 2 (u_off[2] always)
+};
+
 struct TcComposePlan;   // tensor-core composition (compose_tc.cu)
 }  // namespace orth
 struct orth_trace_state;   // abi.cu (orth_plan_trace)
@@ -245,6 +257,11 @@ struct Plan {
   std::vector<GemmPhase> chain;     // 2(k'-1) substeps, batched over units
   GemmPhase aoc;                    // RKO (*) BCOP
   std::vector<EmitItem> emit;
+  std::vector<SocItem> soc;         // f3 units owned by this rank
+  std::vector<GemmPhase> soc_pow;   // soc_pow[j - 2]: S^(*)j = S^(*)(j-1) (*) S, batched over units
+  std::vector<int64_t> soc_copy;    // (offset, numel) pairs of owned SOC free kernels (params -> ortho)
+  SocItem* d_soc = nullptr;
+  float* d_soc_alpha = nullptr;
   int64_t comp_proj_off = 0, comp_ping_off = 0, comp_pong_off = 0, comp_final_off = 0;
 
   // device allocations
@@ -333,6 +350,10 @@ void orth_plan_trace_free(Plan& p);   // abi.cu
 int64_t certify_workspace_bytes(const LayerInfo& L, int H, int W);
 int launch_certify(const LayerInfo& L, const float* kernel, int H, int W, int iters, void* ws, double* out,
                    void* stream);
+// f3 (soc.cu): skew part, AOL scalar, series sum (the powers are GemmPhases)
+int launch_soc_skew(Plan& p, const float* ortho, void* stream);
+int launch_soc_alpha(Plan& p, void* stream);
+int launch_soc_sum(Plan& p, void* stream);
 // a8: copy every unit from the gather layout to the final layout
 int launch_assemble(Plan& p, const float* gf, float* kf, const uint16_t* gb, uint16_t* kb, void* stream);
 // per-layer conv scratch (bytes) for calls up to N x Hbig x Wbig (forward-conv input grid), both

@@ -45,7 +45,7 @@ static orth_status_t validate_opts(const orth_opts_t& o) {
 }
 
 static orth_status_t validate_layer(const orth_layer_desc_t& L, int idx) {
-  if (L.kind < 0 || L.kind > 2) { set_error("layer %d: bad kind %d", idx, L.kind); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (L.kind < 0 || L.kind > 3) { set_error("layer %d: bad kind %d", idx, L.kind); return ORTH_ERR_INVALID_ARGUMENT; }
   if (L.c_in < 1 || L.c_out < 1 || L.k_h < 1 || L.k_w < 1 || L.stride_h < 1 || L.stride_w < 1 || L.dil_h < 1 ||
       L.dil_w < 1 || L.groups < 1) {
     set_error("layer %d: every dimension must be >= 1 (S:31)", idx);
@@ -73,6 +73,15 @@ static orth_status_t validate_layer(const orth_layer_desc_t& L, int idx) {
   if (L.k_h != L.k_w || L.stride_h != L.stride_w || L.dil_h != L.dil_w) {
     set_error("layer %d: only square kernel/stride/dilation are supported", idx);
     return ORTH_ERR_UNSUPPORTED_CONFIG;
+  }
+  if (L.kind == ORTH_SOC) {   // f3: square channel map, odd kernel, stride 1 (R27)
+    const int n = L.soc_terms == 0 ? 6 : L.soc_terms;
+    if (L.c_in != L.c_out) { set_error("layer %d: SOC needs c_in == c_out (channel change: R27, not built)", idx); return ORTH_ERR_UNSUPPORTED_CONFIG; }
+    if (L.k_h % 2 == 0) { set_error("layer %d: SOC needs an odd kernel (centred padding keeps skew-adjointness)", idx); return ORTH_ERR_UNSUPPORTED_CONFIG; }
+    if (L.stride_h != 1) { set_error("layer %d: SOC stride > 1 (RKO composition, R27) is not built", idx); return ORTH_ERR_UNSUPPORTED_CONFIG; }
+    if (n < 1 || n > 16 || n * (L.k_h - 1) + 1 > 63) { set_error("layer %d: soc_terms %d out of range [1, 16] (k_eff <= 63)", idx, n); return ORTH_ERR_INVALID_ARGUMENT; }
+    if (L.pad_t != -1) { set_error("layer %d: SOC uses the centred 'same' padding (pads must be -1)", idx); return ORTH_ERR_INVALID_ARGUMENT; }
+    return ORTH_OK;
   }
   if (L.k_h < L.stride_h) {
     set_error("layer %d: k = %d < s = %d has no orthogonal AOC kernel (P:330)", idx, L.k_h, L.stride_h);
@@ -102,7 +111,15 @@ static orth_status_t derive(Plan& P, const orth_layer_desc_t* layers, int n_laye
       L.pt = L.pl = e / 2; L.pb = L.pr = e - e / 2;     // R11
     } else { L.pt = D.pad_t; L.pb = D.pad_b; L.pl = D.pad_l; L.pr = D.pad_r; }
     std::vector<std::pair<int, std::pair<int64_t, int64_t>>> ms;  // role, (m, n)
-    if (D.kind == ORTH_DENSE) {
+    if (D.kind == ORTH_SOC) {
+      L.cons = CONS_SOC;
+      L.k_free = D.k_h;
+      L.soc_terms = D.soc_terms == 0 ? 6 : D.soc_terms;
+      L.k = L.soc_terms * (L.k_free - 1) + 1;   // the applied kernel: k_eff
+      const int e = L.d * (L.k - 1);
+      L.pt = L.pl = e / 2; L.pb = L.pr = e - e / 2;
+      ms.push_back({ROLE_K, {L.co, (int64_t)L.ci * L.k_free * L.k_free}});
+    } else if (D.kind == ORTH_DENSE) {
       L.cons = CONS_DENSE;
       ms.push_back({ROLE_W, {L.co, L.ci}});
     } else if (L.s == 1) {
@@ -128,7 +145,7 @@ static orth_status_t derive(Plan& P, const orth_layer_desc_t* layers, int n_laye
         M.layer = l; M.group = gi; M.role = e.first; M.m = e.second.first; M.n = e.second.second;
         P.mats.push_back(M);
         const double a = (double)std::max(M.m, M.n), b = (double)std::min(M.m, M.n);
-        fl += 4.0 * a * b * b * T;
+        if (M.role != ROLE_K) fl += 4.0 * a * b * b * T;
       }
     L.ns_flops = fl;
     // composition flops (structured chain, a4/a5; used only for load balance)
@@ -139,6 +156,13 @@ static orth_status_t derive(Plan& P, const orth_layer_desc_t* layers, int n_laye
       for (int j = 1; j < L.kp; ++j) cf += 2.0 * c * c * c * ((j + 1) * j + (j + 1) * (j + 1));
     }
     if (L.cons == CONS_AOC) cf += 2.0 * L.co * L.c_mid * L.ci * L.s * L.s * L.kp * L.kp;
+    if (L.cons == CONS_SOC) {   // S^(*)j = S^(*)(j-1) (*) S: (kj-1 taps) x k^2 products of c x c, j = 2..max(n, 2)
+      const double c = L.co;
+      for (int j = 2; j <= std::max(L.soc_terms, 2); ++j) {
+        const double kj1 = (j - 1) * (L.k_free - 1) + 1;
+        cf += kj1 * kj1 * L.k_free * L.k_free * 2.0 * c * c * c;
+      }
+    }
     L.comp_flops = cf * L.g;
     P.layers.push_back(L);
   }
@@ -191,7 +215,7 @@ static void layout(Plan& P) {
     M.bx_off = P.bx_numel; P.bx_numel += pad_up(pad_up(M.m, 8) * pad_up(M.n, 8), kPadBF16);
     M.br_off = P.br_numel; P.br_numel += pad_up(pad_up(s, 8) * pad_up(s, 8), kPadBF16);
     M.owned = P.units[P.layers[M.layer].first_unit + M.group].owner == P.opts.rank;
-    if (M.owned) {
+    if (M.owned && M.role != ROLE_K) {
       const double a = (double)std::max(M.m, M.n), b = (double)s;
       P.ns_flops += 4.0 * a * b * b * P.opts.ns_iters;
     }
@@ -261,7 +285,7 @@ static void build_ns(Plan& P) {
   const float b = P.opts.beta;
   P.owned_mats.clear();
   for (int i = 0; i < (int)P.mats.size(); ++i)
-    if (P.mats[i].owned && P.mats[i].m > 0 && P.mats[i].n > 0) P.owned_mats.push_back(i);
+    if (P.mats[i].owned && P.mats[i].m > 0 && P.mats[i].n > 0 && P.mats[i].role != ROLE_K) P.owned_mats.push_back(i);
   for (int par = 0; par < 2; ++par) {
     const int xin = par == 0 ? BUF_X : BUF_Y, xout = par == 0 ? BUF_Y : BUF_X;
     GemmPhase& g = P.gram[par];
@@ -527,8 +551,62 @@ static void build_compose(Plan& P) {
   }
   for (auto* ph : {&P.proj, &P.aoc}) finish_phase(*ph);
   for (auto& ph : P.chain) finish_phase(ph);
+  // f3 SOC units: S (skew part, k^2 taps), its powers S^(*)j (((j(k-1)+1)^2 taps), j = 2..max(n, 2)) and the
+  // explicit exponential E (kn^2 taps), all tap-major c x c in the composition workspace
+  P.soc.clear();
+  P.soc_copy.clear();
+  std::vector<int64_t> soc_e(units.size(), -1);
+  int max_terms = 0;
+  for (size_t ui = 0; ui < units.size(); ++ui) {
+    const auto& u = units[ui];
+    const LayerInfo& L = P.layers[u.layer];
+    if (L.cons != CONS_SOC) continue;
+    const MatInfo& Km = P.mats[L.first_mat + u.group];
+    SocItem it{};
+    it.c = L.co; it.k = L.k_free; it.kn = L.k; it.terms = L.soc_terms;
+    it.alpha_slot = (int)P.soc.size();
+    it.src_off = Km.off;
+    P.soc_copy.push_back(Km.off);
+    P.soc_copy.push_back(Km.m * Km.n);
+    const int64_t c2 = (int64_t)it.c * it.c;
+    for (int j = 1; j <= std::max(it.terms, 2); ++j) {
+      const int64_t kj = (int64_t)j * (it.k - 1) + 1;
+      it.u_off[j] = w;
+      w += pad_up(kj * kj * c2, kPadF32);
+    }
+    it.e_off = w;
+    w += pad_up((int64_t)it.kn * it.kn * c2, kPadF32);
+    soc_e[ui] = it.e_off;
+    max_terms = std::max(max_terms, std::max(it.terms, 2));
+    P.soc.push_back(it);
+  }
+  P.soc_pow.assign(std::max(0, max_terms - 1), GemmPhase{});
+  for (const auto& it : P.soc) {
+    const int64_t c2 = (int64_t)it.c * it.c;
+    for (int j = 2; j <= std::max(it.terms, 2); ++j) {
+      GemmPhase& ph = P.soc_pow[j - 2];
+      const int kj = j * (it.k - 1) + 1, kp = (j - 1) * (it.k - 1) + 1;
+      for (int p1 = 0; p1 < kj; ++p1)
+        for (int p2 = 0; p2 < kj; ++p2) {
+          GemmDesc d = mk(it.c, it.c, it.c);   // U_j[p] = sum_{a + b = p} U_{j-1}[a] S[b]
+          d.a_buf = BUF_W; d.b_buf = BUF_W; d.d_buf = BUF_W;
+          d.sa_m = it.c; d.sa_k = 1; d.sb_k = it.c; d.sb_n = 1;
+          d.d_off = it.u_off[j] + (int64_t)(p1 * kj + p2) * c2; d.ldd = it.c;
+          for (int b1 = 0; b1 < it.k; ++b1)
+            for (int b2 = 0; b2 < it.k; ++b2) {
+              const int a1 = p1 - b1, a2 = p2 - b2;
+              if (a1 < 0 || a2 < 0 || a1 >= kp || a2 >= kp) continue;
+              add_seg(ph, d, it.u_off[j - 1] + (int64_t)(a1 * kp + a2) * c2, -1,
+                      it.u_off[1] + (int64_t)(b1 * it.k + b2) * c2);
+            }
+          ph.descs.push_back(d);
+        }
+    }
+  }
+  for (auto& ph : P.soc_pow) finish_phase(ph);
   // emit items
-  for (auto& u : units) {
+  for (size_t ui = 0; ui < units.size(); ++ui) {
+    const auto& u = units[ui];
     const LayerInfo& L = P.layers[u.layer];
     const int base = L.first_mat + u.group * L.mats_per_group;
     EmitItem e{};
@@ -544,6 +622,10 @@ static void build_compose(Plan& P) {
         e.src_buf = BUF_X; e.src_off = P.mats[base].off; e.mode = 1; e.tap_stride = 0; e.ld = 0; break;
       case CONS_AOC:
         e.src_buf = BUF_W; e.src_off = u.fin; e.mode = 0; e.tap_stride = (int64_t)L.co * L.ci; e.ld = L.ci; break;
+      case CONS_SOC:   // E, tap-major; large k_eff^2 c rows are written without the shared-memory stage
+        e.src_buf = BUF_W; e.src_off = soc_e[ui]; e.tap_stride = (int64_t)L.co * L.ci; e.ld = L.ci;
+        e.mode = (int64_t)L.k * L.k * L.ci * 4 > 96 * 1024 ? 2 : 0;
+        break;
       default:  // BCOP
         if (L.kp == 1) { e.src_buf = BUF_X; e.src_off = P.mats[base].off; e.mode = 0; e.tap_stride = 0; e.ld = L.c_b; }
         else { e.src_buf = BUF_W; e.src_off = u.pong; e.mode = 0; e.tap_stride = (int64_t)u.rows * u.c; e.ld = u.c; }
@@ -639,6 +721,9 @@ static orth_status_t allocate(Plan& P) {
   std::vector<GemmPhase*> phases = {&P.gram[0], &P.gram[1], &P.update[0], &P.update[1], &P.gram_r[0],
                                     &P.gram_r[1], &P.update_r[0], &P.update_r[1], &P.proj, &P.aoc};
   for (auto& ph : P.chain) phases.push_back(&ph);
+  for (auto& ph : P.soc_pow) phases.push_back(&ph);
+  const size_t o_soc = take(std::max<size_t>(P.soc.size(), 1) * sizeof(SocItem));
+  const size_t o_sal = take(std::max<size_t>(P.soc.size(), 1) * sizeof(float));
   std::vector<std::pair<size_t, size_t>> ph_off;
   for (auto* ph : phases)
     ph_off.push_back({take(std::max<size_t>(ph->descs.size(), 1) * sizeof(GemmDesc)),
@@ -667,6 +752,8 @@ static orth_status_t allocate(Plan& P) {
   P.d_ns_upd = (NsDesc*)(base + o_nsu);
   P.d_bx = (uint16_t*)(base + o_bx);
   P.d_units = (UnitInfo*)(base + o_units);
+  P.d_soc = (SocItem*)(base + o_soc);
+  P.d_soc_alpha = (float*)(base + o_sal);
   P.d_ns_res = (float*)(base + o_res);
   P.d_br = (uint16_t*)(base + o_br);
   cudaError_t e = cudaMemset(P.d_arena, 0, off);   // also zero-pads the BF16 operand copies
@@ -682,6 +769,8 @@ static orth_status_t allocate(Plan& P) {
     e = cudaMemcpy(P.d_mat_items, P.mat_items.data(), P.mat_items.size() * sizeof(MatItem), cudaMemcpyHostToDevice);
   if (!P.col_items.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_col_items, P.col_items.data(), P.col_items.size() * sizeof(ColItem), cudaMemcpyHostToDevice);
+  if (!P.soc.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_soc, P.soc.data(), P.soc.size() * sizeof(SocItem), cudaMemcpyHostToDevice);
   if (!P.units.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_units, P.units.data(), P.units.size() * sizeof(UnitInfo), cudaMemcpyHostToDevice);
   if (!P.emit.empty() && e == cudaSuccess)
@@ -816,6 +905,7 @@ orth_status_t orth_plan_query(orth_plan_t plan, int32_t what, int32_t index, int
     case ORTH_Q_LAYER_SCRATCH_BYTES: *out = P.layers[index].pad_bytes; break;
     case ORTH_Q_LAYER_NS_FLOPS: *out = (int64_t)P.layers[index].ns_flops; break;
     case ORTH_Q_LAYER_COMP_FLOPS: *out = (int64_t)P.layers[index].comp_flops; break;
+    case ORTH_Q_LAYER_K_EFF: *out = P.layers[index].k; break;
     case ORTH_Q_COMP_FLOPS: {
       double f = 0.0;
       for (auto& u : P.units)

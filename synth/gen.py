@@ -16,7 +16,7 @@ from typing import Sequence
 
 import numpy as np
 
-ROLE_ID = {"Q": 1, "U": 2, "R": 3, "W": 4, "v": 5, "x": 6, "b": 7}
+ROLE_ID = {"Q": 1, "U": 2, "R": 3, "W": 4, "v": 5, "x": 6, "b": 7, "K": 8}
 
 
 def rng(*key: int) -> np.random.Generator:

@@ -13,7 +13,7 @@ from synth import gen
 def oracle_layer(d) -> O.Layer:
     return O.Layer(d["c_in"], d["c_out"], d.get("k", 3), d.get("s", 1), d.get("d", 1), d.get("g", 1),
                    kind=d.get("kind", "conv"), padding_mode=d.get("padding_mode", "circular"),
-                   pad=d.get("pad"))
+                   pad=d.get("pad"), terms=d.get("terms", 6) or 6)
 
 
 def pack_params(plan, cfg_id: int, stress: bool = False):
@@ -38,9 +38,13 @@ def pack_cache(plan, cfg_id: int):
 
 
 def oracle_construct(layers, mats, T=12, beta=0.5, prescale="power", P=3, v=None):
-    """Oracle a2..a5 on the float32 matrices (upcast to f64)."""
+    """Oracle a2..a5 on the float32 matrices (upcast to f64).  SOC free kernels (role K) are not
+    orthogonalised (f3): they pass through to the explicit exponential."""
+    roles = [M.role for d in layers for _ in range(d.get("g", 1) if d.get("kind") != "dense" else 1)
+             for M in O.layer_matrices(oracle_layer(d))]
     ortho, vnew = O.orthogonalize([A.astype(np.float64) for A in mats], T=T, beta=beta, prescale=prescale, P=P,
                                   v=None if v is None else [x.astype(np.float64) for x in v])
+    ortho = [A.astype(np.float64) if r == "K" else X for A, X, r in zip(mats, ortho, roles)]
     kernels, idx = [], 0
     for d in layers:
         OL = oracle_layer(d)

@@ -183,3 +183,18 @@ def test_conv_scratch_sized_at_create():
     # cfg3 128-ch 28x28 layers take the stacked-window kernel: padded copy 256 x 30 x 30 x 128 x 2 bytes
     assert s3[8] == 256 * 30 * 30 * 128 * 2
     assert orth.Plan(configs.cfg3(), device=-1, max_batch=32).layer_info[8]["scratch"] == 32 * 30 * 30 * 128 * 2
+
+
+def test_soc_validation_and_geometry():
+    """f3: SOC layers need c_in == c_out, an odd kernel, stride 1 and 1 <= terms <= 16 (R27); the applied
+    kernel is k_eff = terms (k - 1) + 1 with the centred padding, and the free kernel is one c/g x (c/g) k^2
+    matrix per group (role K) that is not orthogonalised (no NS flops)."""
+    for bad, st in [(dict(kind="soc", c_in=8, c_out=16, k=3), orth.UNSUPPORTED_CONFIG),
+                    (dict(kind="soc", c_in=8, c_out=8, k=4), orth.UNSUPPORTED_CONFIG),
+                    (dict(kind="soc", c_in=8, c_out=8, k=3, s=2), orth.UNSUPPORTED_CONFIG),
+                    (dict(kind="soc", c_in=8, c_out=8, k=3, terms=40), orth.INVALID_ARGUMENT)]:
+        assert orth.orth_validate_desc([dict(bad, padding_mode="circular")]) == st, bad
+    p = orth.Plan([dict(kind="soc", c_in=32, c_out=32, k=3, s=1, d=2, g=2, terms=5, padding_mode="circular")], -1)
+    assert p.layer_info[0]["k_eff"] == 11 and p.kernel_shape(0) == (32, 16, 11, 11)
+    assert [(m["m"], m["n"], m["role"]) for m in p.matrices] == [(16, 144, "K"), (16, 144, "K")]
+    assert p.ns_flops == 0 and p.out_hw(0, 12, 12) == (12, 12)

@@ -1,0 +1,92 @@
+"""f3: Adaptive-SOC explicit exponential on the GPU
+against the oracle ("Explicit conv exponential"; readings R25-R27).
+
+* construction: the explicit kernel E = delta + sum_j (alpha skew(K))^(*)j / j!
+  built by orth_compose_kernel (skew kernel, block-convolution powers as
+  batched GEMM phases -- SIMT FP32 in F32 mode, 3-pass tcgen05 in BF16 mode --
+  AOL scalar from the second power, centred series sum) against
+  oracle.soc_exp_kernel on the same free parameters, next to AOC layers in one
+  plan;
+* apply: the conv of E (k_eff = n (k - 1) + 1) through orth_conv_forward, BF16
+  on the tensor-core window kernel (k_eff = 7) and FP32 (k_eff = 13), against
+  the oracle conv with elementwise bounds;
+* orthogonality: oracle per-frequency SVD of the GPU kernel within the series
+  tail e / (n + 1)! (|T(alpha L)| <= 1 by the AOL bound)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import gen
+from tests.helpers import (BF16_ELEM, F32_ELEM, assert_elementwise, nchw, nhwc, oracle_construct, oracle_layer,
+                           pack_params, rel)
+
+pytestmark = pytest.mark.gpu
+
+LAYERS = [dict(kind="soc", c_in=16, c_out=16, k=3, s=1, d=1, g=1, terms=6, padding_mode="circular", H=8),
+          dict(kind="soc", c_in=64, c_out=64, k=3, s=1, d=1, g=1, terms=3, padding_mode="circular", H=16),
+          dict(kind="soc", c_in=32, c_out=32, k=3, s=1, d=2, g=2, terms=4, padding_mode="circular", H=12),
+          dict(kind="soc", c_in=8, c_out=8, k=5, s=1, d=1, g=1, terms=2, padding_mode="zeros", H=9),
+          dict(kind="conv", c_in=16, c_out=32, k=3, s=2, d=1, g=1, padding_mode="circular", H=8)]
+
+
+def _construct(orth, layers, compute, cfg_id=21):
+    plan = orth.Plan(layers, 0, compute=compute)
+    params, mats = pack_params(plan, cfg_id)
+    p = torch.from_numpy(params).cuda()
+    ortho = torch.zeros_like(p)
+    plan.orthogonalize(p, ortho)
+    kf = torch.zeros(plan.kf32_numel, device="cuda")
+    kb = torch.zeros(plan.kbf16_numel, device="cuda", dtype=torch.bfloat16)
+    plan.compose(ortho, kf, kb)
+    plan.check()
+    return plan, mats, kf, kb
+
+
+@pytest.mark.parametrize("compute,tol", [("f32", 1e-5), ("bf16", 1e-4)])
+def test_soc_construction_parity(cuda_lib, compute, tol):
+    plan, mats, kf, kb = _construct(cuda_lib, LAYERS, compute)
+    _, _, o_k = oracle_construct(LAYERS, mats)
+    kf_h = torch.from_numpy(kf.cpu().numpy())
+    kb_h = kb.float().cpu()
+    for l, K in enumerate(o_k):
+        got = plan.kernel_f32(kf_h, l).numpy()
+        assert got.shape == K.shape, (l, got.shape, K.shape)
+        e = rel(got, K)
+        assert e < tol, (l, e)
+        kbg = np.transpose(plan.kernel_bf16(kb_h, l).numpy(), (0, 3, 1, 2))
+        assert np.array_equal(kbg, gen.bf16_round(got.astype(np.float32)))
+
+
+def test_soc_apply_and_orthogonality(cuda_lib):
+    plan, mats, kf, kb = _construct(cuda_lib, LAYERS, "bf16")
+    for l, d in enumerate(LAYERS[:4]):
+        OL = oracle_layer(d)
+        H = d["H"]
+        Kg = plan.kernel_f32(kf, l).cpu().numpy().astype(np.float64)
+        # orthogonality of the GPU kernel: within the series tail (circular layers)
+        if d["padding_mode"] == "circular":
+            sv = O.conv_singular_values(Kg, OL, 8, 8)
+            tail = math.e / math.factorial(d["terms"] + 1)
+            assert np.abs(sv - 1).max() <= tail + 1e-5, (l, np.abs(sv - 1).max(), tail)
+        # apply: FP32 I/O (SIMT) and BF16 I/O (tensor cores where k_eff <= 7)
+        x = gen.activations((2, H, H, d["c_in"]), (21, l, 0, 0, gen.ROLE_ID["x"]))
+        for io in ("f32", "bf16"):
+            if io == "bf16":
+                xi = gen.bf16_round(x)
+                Kio = plan.kernel_bf16(kb, l).float().cpu().numpy().astype(np.float64).transpose(0, 3, 1, 2)
+                xd, kd, dt, elem = torch.from_numpy(xi).cuda().to(torch.bfloat16), plan.kernel_bf16(kb, l), \
+                    torch.bfloat16, BF16_ELEM
+            else:
+                xi, Kio, xd, kd, dt, elem = x, Kg, torch.from_numpy(x).cuda(), plan.kernel_f32(kf, l), torch.float32, \
+                    F32_ELEM
+            y = torch.zeros((2, H, H, d["c_out"]), device="cuda", dtype=dt)
+            plan.conv_forward(l, kd, xd, y)
+            x64 = nchw(xi.astype(np.float64))
+            ref = O.conv2d(x64, Kio, s=1, d=OL.d, g=OL.g, mode=OL.padding_mode)
+            absref = O.conv2d(np.abs(x64), np.abs(Kio), s=1, d=OL.d, g=OL.g, mode=OL.padding_mode)
+            got = y.float().cpu().numpy()
+            assert_elementwise(got, nhwc(ref), nhwc(absref), *elem, what=f"soc layer {l} {io}")
+        plan.check()

@@ -55,7 +55,9 @@ def test_soc_construction_parity(cuda_lib, compute, tol):
         got = plan.kernel_f32(kf_h, l).numpy()
         assert got.shape == K.shape, (l, got.shape, K.shape)
         e = rel(got, K)
-        assert e < tol, (l, e)
+        # the AOC layer in BF16 mode carries the BF16 NS construction error (north star 2e-2); the SOC
+        # kernels are built from the unorthogonalised free kernel with 3-pass (FP32-accurate) products
+        assert e < (tol if LAYERS[l]["kind"] == "soc" or compute == "f32" else 2e-2), (l, e)
         kbg = np.transpose(plan.kernel_bf16(kb_h, l).numpy(), (0, 3, 1, 2))
         assert np.array_equal(kbg, gen.bf16_round(got.astype(np.float32)))
 

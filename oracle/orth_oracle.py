@@ -38,6 +38,7 @@ __all__ = [
     "toeplitz", "fft_singular_values", "polyphase_singular_values",
     "conv_singular_values", "spectral_certificate",
     "soc_skew", "aol_scale", "soc_exp_kernel",
+    "aol_rescale", "adjoint_kernel", "same_pads", "sll_block_kernels", "sll_block_forward", "sll_block_unfused",
 ]
 
 
@@ -553,3 +554,82 @@ def soc_exp_kernel(K: np.ndarray, terms: int):
         kj = P.shape[2]
         E[:, :, off:off + kj, off:off + kj] += P / fact
     return E, alpha
+
+
+# ---------------------------------------------------------------------------
+# f4: SLL x AOC fused down-sampling block (App. B.3; readings R28-R30)
+# ---------------------------------------------------------------------------
+def aol_rescale(K: np.ndarray) -> np.ndarray:
+    """AOL per-input-channel rescale (P:133 AOL; the SLL kernel K = W T^{-1/2} of P:389 with the
+    SDP scaling q = 1, reading R28): V[i, j, Delta] = sum_o sum_t K[o, i, t] K[o, j, t + Delta],
+    d_i = sum_j sum_Delta |V[i, j, Delta]|, input channel i scaled by d_i^{-1/2} (d_i = 0: unscaled).
+    Then |T(K D^{-1/2})| <= 1 (Prach & Lampert)."""
+    K = np.asarray(K, np.float64)
+    co, ci, k1, k2 = K.shape
+    d = np.zeros(ci)
+    for da in range(-(k1 - 1), k1):
+        for db in range(-(k2 - 1), k2):
+            V = np.zeros((ci, ci))
+            for a in range(k1):
+                for b in range(k2):
+                    a2, b2 = a + da, b + db
+                    if 0 <= a2 < k1 and 0 <= b2 < k2:
+                        V += K[:, :, a, b].T @ K[:, :, a2, b2]
+            d += np.abs(V).sum(axis=1)
+    sc = np.where(d > 0, 1.0 / np.sqrt(np.where(d > 0, d, 1.0)), 1.0)
+    return K * sc[None, :, None, None]
+
+
+def adjoint_kernel(K: np.ndarray) -> np.ndarray:
+    """Kernel of the adjoint of a stride-1 conv: channels transposed, taps flipped (with the padding
+    p -> k - 1 - p, see sll_block_kernels)."""
+    return np.ascontiguousarray(np.transpose(np.asarray(K, np.float64), (1, 0, 2, 3))[:, :, ::-1, ::-1])
+
+
+def same_pads(k: int, d: int = 1):
+    """Reading R11: p_t = floor(d(k-1)/2), p_b = d(k-1) - p_t (same on both axes)."""
+    e = d * (k - 1)
+    return (e // 2, e - e // 2, e // 2, e - e // 2)
+
+
+def sll_block_kernels(K_pre: np.ndarray, K_post: np.ndarray, W_sll: np.ndarray):
+    """The block's merged kernels ("kernels are merged once per batch"):
+    K = aol_rescale(W_sll);  C = K (*) K_pre;  A = K_post (*) K_pre;  B = K_post (*) adjoint(K).
+    Padding of a composition is the sum of the factors' (top/left) pads; the adjoint of a "same" conv with
+    top pad p has top pad k - 1 - p.  A and B are merged into ONE kernel over the concatenated input
+    [x | h]: M = [A | -2 B], each embedded at offset P - p in a common window with top pad P = max(pA, pB)
+    (reading R29).  Returns dict(C, padC, M, padM, K, A, B)."""
+    K = aol_rescale(W_sll)
+    kpre, kpost, ks = K_pre.shape[2], K_post.shape[2], K.shape[2]
+    ppre, ppost, ps = same_pads(kpre)[0], same_pads(kpost)[0], same_pads(ks)[0]
+    C = block_conv(K, K_pre)
+    A = block_conv(K_post, K_pre)
+    B = block_conv(K_post, adjoint_kernel(K))
+    pC, pA, pB = ps + ppre, ppost + ppre, ppost + (ks - 1 - ps)
+    P = max(pA, pB)
+    kM = max(P - pA + A.shape[2], P - pB + B.shape[2])
+    co, c, cs = A.shape[0], A.shape[1], B.shape[1]
+    M = np.zeros((co, c + cs, kM, kM))
+    oa, ob = P - pA, P - pB
+    M[:, :c, oa:oa + A.shape[2], oa:oa + A.shape[3]] = A
+    M[:, c:, ob:ob + B.shape[2], ob:ob + B.shape[3]] = -2.0 * B
+    kC = C.shape[2]
+    return dict(C=C, padC=(pC, kC - 1 - pC, pC, kC - 1 - pC), M=M, padM=(P, kM - 1 - P, P, kM - 1 - P),
+                K=K, A=A, B=B)
+
+
+def sll_block_forward(x: np.ndarray, kern: dict, b: np.ndarray, s: int) -> np.ndarray:
+    """Fused block: y = M *_s [x | relu(C * x + b)], circular (reading R30)."""
+    h = conv2d(x, kern["C"], pads=kern["padC"]) + np.asarray(b, np.float64)[None, :, None, None]
+    z = np.concatenate([np.asarray(x, np.float64), np.maximum(h, 0.0)], axis=1)
+    return conv2d(z, kern["M"], s=s, pads=kern["padM"])
+
+
+def sll_block_unfused(x: np.ndarray, K_pre: np.ndarray, K_post: np.ndarray, K: np.ndarray, b: np.ndarray,
+                      s: int) -> np.ndarray:
+    """The block as three sequential layers: z = K_pre * x; u = z - 2 K^T * relu(K * z + b)
+    (SLL; K^T * = the exact adjoint conv); y = K_post *_s u.  Circular, "same" pads."""
+    z = conv2d(x, K_pre)
+    t = np.maximum(conv2d(z, K) + np.asarray(b, np.float64)[None, :, None, None], 0.0)
+    u = z - 2.0 * conv_transpose2d(t, K, z.shape[2], z.shape[3])
+    return conv2d(u, K_post, s=s)

@@ -495,3 +495,99 @@ def test_soc_explicit_equals_implicit_and_expm(c, k, terms, d):
     assert np.linalg.norm(TE - scipy.linalg.expm(TL), 2) <= tail + 1e-12
     sv = np.linalg.svd(TE, compute_uv=False)
     assert np.abs(sv - 1).max() <= tail + 1e-12
+
+
+# ------------------------------------------------------------------ f4: SLL x AOC block
+def test_aol_rescale_bound_and_examples():
+    """the rescaled operator has Toeplitz sigma_max <= 1; 1x1 I unchanged, 2I -> I; a zero input
+    channel passes unscaled."""
+    for shape in [(4, 4, 3, 3), (3, 5, 2, 2), (6, 2, 3, 3)]:
+        K = O.aol_rescale(rs.standard_normal(shape))
+        T = O.toeplitz(lambda x: _circ_pad(K, x), (shape[1], 7, 7))
+        assert np.linalg.svd(T, compute_uv=False)[0] <= 1 + 1e-12
+    I = np.eye(3)[:, :, None, None]
+    assert np.array_equal(O.aol_rescale(I), I) and np.allclose(O.aol_rescale(2 * I), I, rtol=0, atol=1e-15)
+    Z = rs.standard_normal((3, 3, 3, 3)); Z[:, 1] = 0
+    assert np.abs(O.aol_rescale(Z)[:, 1]).max() == 0
+
+
+def _circ_pad(K, x):
+    """torch-CPU circular conv with the R11 'same' pads (possibly asymmetric for even k)."""
+    k = K.shape[2]
+    pt, pb, pl, pr = O.same_pads(k)
+    return F.conv2d(F.pad(t64(x), (pl, pr, pt, pb), mode="circular"), t64(K)).numpy()
+
+
+def _torch_block(x, K_pre, K_post, K, b, s):
+    """The unfused block in torch (independent of the oracle's conv code): circular pad + conv, and the SLL's
+    K^T * as its exact adjoint -- conv_transpose2d onto the padded grid, then the circular pad folded back."""
+    def pads(k):
+        return O.same_pads(k)
+
+    def conv(z, W, stride=1):
+        pt, pb, pl, pr = pads(W.shape[2])
+        return F.conv2d(F.pad(z, (pl, pr, pt, pb), mode="circular"), W, stride=stride)
+
+    def conv_adj(t, W, H):
+        pt, pb, pl, pr = pads(W.shape[2])
+        yp = F.conv_transpose2d(t, W)                  # (N, C, H + pt + pb, W + pl + pr)
+        ri = (torch.arange(yp.shape[2]) - pt) % H
+        ci = (torch.arange(yp.shape[3]) - pl) % H
+        out = torch.zeros(yp.shape[0], yp.shape[1], H, yp.shape[3], dtype=yp.dtype).index_add(2, ri, yp)
+        return torch.zeros(yp.shape[0], yp.shape[1], H, H, dtype=yp.dtype).index_add(3, ci, out)
+    z = conv(x, t64(K_pre))
+    Kt = t64(K)
+    t = torch.relu(conv(z, Kt) + t64(b)[None, :, None, None])
+    u = z - 2 * conv_adj(t, Kt, z.shape[2])
+    return conv(u, t64(K_post), s)
+
+
+@pytest.mark.parametrize("c,cs,co,kpre,ks,kpost,s,H", [(4, 6, 8, 2, 2, 3, 2, 8), (3, 3, 3, 3, 3, 3, 1, 6),
+                                                       (4, 5, 6, 3, 2, 4, 2, 8), (2, 4, 8, 2, 3, 2, 2, 6)])
+def test_sll_block_fused_equals_unfused(c, cs, co, kpre, ks, kpost, s, H):
+    """P:392-396 / S:294-296: the fused block (merged kernels C and M = [A | -2 B]) equals the three
+    sequential layers conv_{K_post, s} o SLL o conv_{K_pre} -- against the oracle's own unfused composition
+    and against a torch-CPU implementation (circular pads, autograd adjoint) -- to 1e-10."""
+    K_pre, K_post = rs.standard_normal((c, c, kpre, kpre)), rs.standard_normal((co, c, kpost, kpost))
+    W = rs.standard_normal((cs, c, ks, ks))
+    b = 0.3 * rs.standard_normal(cs)
+    kern = O.sll_block_kernels(K_pre, K_post, W)
+    x = rs.standard_normal((2, c, H, H))
+    fused = O.sll_block_forward(x, kern, b, s)
+    unf = O.sll_block_unfused(x, K_pre, K_post, kern["K"], b, s)
+    ref = _torch_block(t64(x), K_pre, K_post, kern["K"], b, s).numpy()
+    assert fused.shape == ref.shape
+    assert np.abs(fused - unf).max() < 1e-10 * max(1.0, np.abs(unf).max())
+    assert np.abs(fused - ref).max() < 1e-10 * max(1.0, np.abs(ref).max())
+
+
+def test_sll_block_special_cases_and_lipschitz():
+    """K = 0 -> y = (K_post (*) K_pre) *_s x; identity 1x1 K_pre / K_post at s = 1 -> the bare SLL
+    layer x - 2 K^T relu(K x + b); with orthogonal K_pre / K_post the block is 1-Lipschitz: the spectral norm
+    of its Jacobian (torch autograd of the torch implementation, at random points) is <= 1 + 1e-9."""
+    c, cs, co = 3, 4, 6
+    L = O.Layer(c, co, 3, 2)
+    ms = [gen.param_matrix(M.m, M.n, (77, 0, 0, i, 1)).astype(np.float64) for i, M in enumerate(O.layer_matrices(L))]
+    K_post = O.layer_kernel(L, [O.orthogonalize(ms, T=25)[0]])
+    Lp = O.Layer(c, c, 2, 1)
+    ms = [gen.param_matrix(M.m, M.n, (78, 0, 0, i, 1)).astype(np.float64) for i, M in enumerate(O.layer_matrices(Lp))]
+    K_pre = O.layer_kernel(Lp, [O.orthogonalize(ms, T=25)[0]])
+    x = rs.standard_normal((1, c, 6, 6))
+    kz = O.sll_block_kernels(K_pre, K_post, np.zeros((cs, c, 2, 2)))
+    y0 = O.sll_block_forward(x, kz, np.zeros(cs), 2)
+    assert np.abs(y0 - O.conv2d(x, kz["A"], s=2, pads=(1, 2, 1, 2))).max() < 1e-12
+    I = np.eye(c)[:, :, None, None]
+    W = rs.standard_normal((cs, c, 3, 3))
+    ki = O.sll_block_kernels(I, I, W)
+    b = 0.1 * rs.standard_normal(cs)
+    K = ki["K"]
+    sll = x - 2 * O.conv_transpose2d(np.maximum(O.conv2d(x, K) + b[None, :, None, None], 0), K, 6, 6)
+    assert np.abs(O.sll_block_forward(x, ki, b, 1) - sll).max() < 1e-12
+    W = rs.standard_normal((cs, c, 2, 2))
+    kern = O.sll_block_kernels(K_pre, K_post, W)
+    b = 0.1 * rs.standard_normal(cs)
+    for _ in range(3):
+        x0 = t64(rs.standard_normal((1, c, 6, 6)))
+        J = torch.autograd.functional.jacobian(lambda z: _torch_block(z, K_pre, K_post, kern["K"], b, 2), x0)
+        J = J.reshape(-1, x0.numel()).numpy()
+        assert np.linalg.svd(J, compute_uv=False)[0] <= 1 + 1e-9

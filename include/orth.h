@@ -70,7 +70,8 @@ typedef enum {
 
 typedef enum { ORTH_F32 = 0, ORTH_BF16 = 1, ORTH_BF16X3 = 2 } orth_dtype_t;
 typedef enum { ORTH_PAD_ZEROS = 0, ORTH_PAD_CIRCULAR = 1 } orth_pad_t;
-typedef enum { ORTH_CONV2D = 0, ORTH_CONV_TRANSPOSE2D = 1, ORTH_DENSE = 2, ORTH_SOC = 3 } orth_kind_t;
+typedef enum { ORTH_CONV2D = 0, ORTH_CONV_TRANSPOSE2D = 1, ORTH_DENSE = 2, ORTH_SOC = 3, ORTH_SLL = 4,
+               ORTH_SLL_BLOCK = 5 } orth_kind_t;
 typedef enum { ORTH_PRESCALE_POWER = 0, ORTH_PRESCALE_FROBENIUS = 1 } orth_prescale_t;
 
 /* One orthogonal layer (S:35-40 ConvSpec + S:205-210 ConvLayerConfig).
@@ -86,6 +87,18 @@ typedef enum { ORTH_PRESCALE_POWER = 0, ORTH_PRESCALE_FROBENIUS = 1 } orth_presc
  *    E = delta + L + L(*)L/2! + ... + L^(*)n/n!, L = alpha skew(K), alpha the scalar AOL bound (R25-R27),
  *    of spatial size k_eff = n (k - 1) + 1, n = soc_terms (0 -> 6); conv calls apply E ("same" padding of
  *    k_eff).  Circular padding makes the layer orthogonal up to the series tail e/(n+1)!.
+ *  kind ORTH_SLL: the kernel K of an SLL layer ("W T^{-1/2} = Toeplitz(K)"), c_in -> c_out, k,
+ *    s = d = g = 1: one free c_out x c_in k^2 matrix (role K) that orth_compose_kernel AOL-rescales per
+ *    input channel (R28), so |T(K)| <= 1.
+ *  kind ORTH_SLL_BLOCK: the fused SLL x AOC down-sampling block (App. B.3) over three EARLIER
+ *    layers of the plan: blk_pre (ORTH_CONV2D c -> c, s = 1), blk_sll (ORTH_SLL c -> c_s) and blk_post
+ *    (ORTH_CONV2D c -> c_out, stride s), all g = d = 1, circular; c_in = c, c_out and stride_h/w = s of the
+ *    block must match (k_h/k_w are ignored).  orth_compose_kernel merges them once per update
+ *    (P:399): C = K (*) K_pre (c_s x c) and M = [K_post (*) K_pre | -2 K_post (*) K^T] (c_out x (c + c_s)),
+ *    stored back to back in the block's kernel region (ORTH_Q_LAYER_BLOCK_M_OFF); orth_conv_forward
+ *    computes y = M *_s [x | relu(C * x + bias)] (bias: the SLL bias, c_s floats) -- two conv launches and
+ *    one concat, with h and [x | h] in the layer's scratch (declare grid_h/grid_w and max_batch).  The
+ *    block and its three layers are constructed on one rank.
  *  Square kernels/strides/dilations only (k_h == k_w, ...).  pad_* = -1 selects
  *  the "same" rule p_t = floor(d(k-1)/2), p_b = d(k-1) - p_t (R11).
  *  grid_h, grid_w: the largest spatial size the layer's conv calls will see on
@@ -106,6 +119,7 @@ typedef struct {
   int32_t padding_mode;  /* orth_pad_t */
   int32_t grid_h, grid_w;
   int32_t soc_terms;     /* ORTH_SOC: highest power n of the series (0 -> 6); ignored otherwise */
+  int32_t blk_pre, blk_sll, blk_post;   /* ORTH_SLL_BLOCK: layer indices (< this layer); ignored otherwise */
 } orth_layer_desc_t;
 
 /* OrthoParams, Bjorck only. */
@@ -173,7 +187,10 @@ typedef enum {
   ORTH_Q_LAYER_C_MID = 26,        /* derived internal width (R7); 0 if none */
   ORTH_Q_LAYER_C_B = 27,          /* BCOP width; 0 if none */
   ORTH_Q_LAYER_KP = 28,           /* BCOP size k' (R8); 0 if none */
-  ORTH_Q_LAYER_K_EFF = 32,        /* kernel size of the applied kernel (SOC: n (k - 1) + 1; else k) */
+  ORTH_Q_LAYER_K_EFF = 32,        /* kernel size of the applied kernel (SOC: n (k - 1) + 1; SLL block: of M) */
+  ORTH_Q_LAYER_BLOCK_KC = 33,     /* SLL block: size of C */
+  ORTH_Q_LAYER_BLOCK_M_OFF = 34,  /* SLL block: element offset of M inside the layer's kernel region */
+  ORTH_Q_LAYER_BLOCK_PADS = 35,   /* SLL block: top pad of C (low 16 bits) and of M (high 16 bits) */
   ORTH_Q_LAYER_SCRATCH_BYTES = 29,/* this layer's conv scratch slice */
   ORTH_Q_LAYER_NS_FLOPS = 30,     /* 4 m n^2 T over the layer's matrices (all groups) */
   ORTH_Q_LAYER_COMP_FLOPS = 31,   /* structured composition flops of the layer (all groups) */

@@ -98,8 +98,8 @@ def layer_geometry(L: Layer) -> dict:
     ci, co = ci_f // L.g, co_f // L.g
     if L.kind == "dense":
         return dict(ci=ci, co=co, kind="dense", kp=0, c_b=0, c_mid=0)
-    if L.kind == "soc":
-        return dict(ci=ci, co=co, kind="soc", kp=0, c_b=0, c_mid=0)
+    if L.kind in ("soc", "sll", "sll_block"):
+        return dict(ci=ci, co=co, kind=L.kind, kp=0, c_b=0, c_mid=0)
     if L.s == 1:
         return dict(ci=ci, co=co, kind="bcop", kp=L.k, c_b=max(ci, co), c_mid=0)
     if L.k == L.s:
@@ -115,8 +115,10 @@ def layer_matrices(L: Layer) -> List[MatrixSpec]:
     geo = layer_geometry(L)
     if geo["kind"] == "dense":
         return [MatrixSpec("W", geo["co"], geo["ci"])]
-    if geo["kind"] == "soc":     # f3: the free kernel (c, c, k, k) as a c x c k^2 matrix, not orthogonalised
+    if geo["kind"] in ("soc", "sll"):   # f3 / f4: the free kernel (co, ci, k, k) as a co x ci k^2 matrix
         return [MatrixSpec("K", geo["co"], geo["ci"] * L.k * L.k)]
+    if geo["kind"] == "sll_block":       # f4: no parameters of its own (merges three other layers)
+        return []
     out: List[MatrixSpec] = []
     if geo["kind"] in ("bcop", "aoc"):
         c = geo["c_b"]
@@ -285,6 +287,9 @@ def layer_kernel(L: Layer, group_mats: Sequence[Sequence[np.ndarray]]) -> np.nda
             continue
         if geo["kind"] == "soc":
             ks.append(soc_exp_kernel(mats[0].reshape(geo["co"], geo["ci"], L.k, L.k), L.terms)[0])
+            continue
+        if geo["kind"] == "sll":
+            ks.append(aol_rescale(mats[0].reshape(geo["co"], geo["ci"], L.k, L.k)))
             continue
         if geo["kind"] == "bcop":
             ks.append(bcop(mats[0], mats[1:], geo["co"], geo["ci"]))

@@ -26,18 +26,19 @@ _lib = C.CDLL(_LIB_PATH)
 OK, INVALID_ARGUMENT, UNSUPPORTED_CONFIG, SHAPE_MISMATCH, ZERO_NORM, NOT_CONVERGED, CUDA_ERR, OOM, NO_DEVICE = range(9)
 F32, BF16, BF16X3 = 0, 1, 2
 PAD_ZEROS, PAD_CIRCULAR = 0, 1
-CONV2D, CONV_TRANSPOSE2D, DENSE, SOC = 0, 1, 2, 3
+CONV2D, CONV_TRANSPOSE2D, DENSE, SOC, SLL, SLL_BLOCK = 0, 1, 2, 3, 4, 5
 PRESCALE_POWER, PRESCALE_FROBENIUS = 0, 1
 Q = dict(N_LAYERS=0, N_MATRICES=1, PARAMS_NUMEL=2, CACHE_NUMEL=3, KERNELS_F32_NUMEL=4, KERNELS_BF16_NUMEL=5,
          WORKSPACE_BYTES=6, NS_FLOPS=7, KERNEL_SEGMENT_F32=8, KERNEL_SEGMENT_BF16=9, N_UNITS=10,
          GATHER_F32_NUMEL=11, GATHER_BF16_NUMEL=12, CONV_SCRATCH_BYTES=13, COMP_FLOPS=14,
          LAYER_FIRST_MATRIX=20, LAYER_MATS_PER_GROUP=21, LAYER_KERNEL_OFF_F32=22, LAYER_KERNEL_OFF_BF16=23,
          LAYER_KERNEL_NUMEL=24, LAYER_OWNER=25, LAYER_C_MID=26, LAYER_C_B=27, LAYER_KP=28, LAYER_SCRATCH_BYTES=29, LAYER_NS_FLOPS=30, LAYER_COMP_FLOPS=31, LAYER_K_EFF=32,
+         LAYER_BLOCK_KC=33, LAYER_BLOCK_M_OFF=34, LAYER_BLOCK_PADS=35,
          MATRIX_ROWS=40, MATRIX_COLS=41, MATRIX_OFFSET=42, MATRIX_CACHE_OFFSET=43, MATRIX_LAYER=44,
          MATRIX_GROUP=45, MATRIX_ROLE=46, UNIT_LAYER=60, UNIT_GROUP=61, UNIT_OWNER=62, UNIT_NUMEL=63,
          UNIT_GATHER_OFF_F32=64, UNIT_GATHER_OFF_BF16=65, UNIT_KERNEL_OFF_F32=66, UNIT_KERNEL_OFF_BF16=67)
 ROLES = {0: "Q", 1: "U", 2: "R", 3: "W", 4: "K"}
-_KIND = {"conv": CONV2D, "convT": CONV_TRANSPOSE2D, "dense": DENSE, "soc": SOC}
+_KIND = {"conv": CONV2D, "convT": CONV_TRANSPOSE2D, "dense": DENSE, "soc": SOC, "sll": SLL, "sll_block": SLL_BLOCK}
 _MODE = {"zeros": PAD_ZEROS, "circular": PAD_CIRCULAR}
 
 
@@ -56,7 +57,7 @@ class TraceRec(C.Structure):
 class LayerDesc(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("kind", "c_in", "c_out", "k_h", "k_w", "stride_h", "stride_w", "dil_h",
                                          "dil_w", "groups", "pad_t", "pad_b", "pad_l", "pad_r", "padding_mode",
-                                         "grid_h", "grid_w", "soc_terms")]
+                                         "grid_h", "grid_w", "soc_terms", "blk_pre", "blk_sll", "blk_post")]
 
 
 class Opts(C.Structure):
@@ -124,7 +125,7 @@ def layer_desc(d: Dict) -> LayerDesc:
     gh, gw = layer_grid(d) if d.get("kind", "conv") != "dense" else (0, 0)
     return LayerDesc(_KIND[d.get("kind", "conv")], d["c_in"], d["c_out"], k, k, s, s, dl, dl, d.get("g", 1),
                      pads[0], pads[1], pads[2], pads[3], _MODE[d.get("padding_mode", "circular")], gh, gw,
-                     d.get("terms", 0))
+                     d.get("terms", 0), d.get("pre", 0), d.get("sll", 0), d.get("post", 0))
 
 
 def make_opts(**kw) -> Opts:
@@ -275,7 +276,9 @@ class Plan:
                                 kf32_off=q("LAYER_KERNEL_OFF_F32", l), kbf16_off=q("LAYER_KERNEL_OFF_BF16", l),
                                 numel=q("LAYER_KERNEL_NUMEL", l), owner=q("LAYER_OWNER", l),
                                 c_mid=q("LAYER_C_MID", l), c_b=q("LAYER_C_B", l), kp=q("LAYER_KP", l),
-                                scratch=q("LAYER_SCRATCH_BYTES", l), k_eff=q("LAYER_K_EFF", l))
+                                scratch=q("LAYER_SCRATCH_BYTES", l), k_eff=q("LAYER_K_EFF", l),
+                                kc=q("LAYER_BLOCK_KC", l), m_off=q("LAYER_BLOCK_M_OFF", l),
+                                pads=q("LAYER_BLOCK_PADS", l))
                            for l in range(self.n_layers)]
 
     # -- shapes ---------------------------------------------------------
@@ -291,6 +294,20 @@ class Plan:
         k = self.layer_info[l]["k_eff"]
         return (co, ci // d.get("g", 1), k, k)
 
+    def block_kernels(self, kbuf, l: int):
+        """SLL block l: views (C, M) of its merged kernels in kbuf (FP32 PyTorch layout (c_s, c, kC, kC) and
+        (c_out, c + c_s, kM, kM), or BF16 GEMM layout (C_o, k, k, C_i) when kbuf is bfloat16)."""
+        d, info = self.layers[l], self.layer_info[l]
+        c, co = d["c_in"], d["c_out"]
+        cs = self.layers[d["sll"]]["c_out"]
+        kc, km = info["kc"], info["k_eff"]
+        off = info["kbf16_off"] if str(kbuf.dtype) == "torch.bfloat16" else info["kf32_off"]
+        C = kbuf[off: off + cs * c * kc * kc]
+        M = kbuf[off + info["m_off"]: off + info["m_off"] + co * (c + cs) * km * km]
+        if str(kbuf.dtype) == "torch.bfloat16":
+            return C.view(cs, kc, kc, c), M.view(co, km, km, c + cs)
+        return C.view(cs, c, kc, kc), M.view(co, c + cs, km, km)
+
     def kernel_f32(self, kf32, l: int):
         info = self.layer_info[l]
         return kf32[info["kf32_off"]: info["kf32_off"] + info["numel"]].view(self.kernel_shape(l))
@@ -305,6 +322,9 @@ class Plan:
         d = self.layers[l]
         k, s, dl = self.layer_info[l]["k_eff"], d.get("s", 1), d.get("d", 1)
         pads = d.get("pad")
+        if d.get("kind") == "sll_block":
+            pm = self.layer_info[l]["pads"] >> 16
+            pads = (pm, k - 1 - pm, pm, k - 1 - pm)
         if pads is None:
             e = dl * (k - 1)
             pads = (e // 2, e - e // 2, e // 2, e - e // 2)

@@ -219,7 +219,8 @@ orth_status_t orth_compose_kernel(orth_plan_t plan, const float* ortho, float* k
   Plan& P = plan->p;
   if (!ortho || !kernels_f32) { set_error("NULL ortho or kernels_f32"); return ORTH_ERR_INVALID_ARGUMENT; }
   NvtxRange nv("orth_compose_kernel");
-  float* bufs[BUF_COUNT] = {const_cast<float*>(ortho), nullptr, nullptr, P.d_comp};
+  // BUF_Y = the output kernels: the SLL-block merges read the FP32 kernels the first emit wrote
+  float* bufs[BUF_COUNT] = {const_cast<float*>(ortho), kernels_f32, nullptr, P.d_comp};
   int e = 0;
   // composition stays FP32-accurate: SIMT FFMA, or the 3-pass split on tensor cores
   auto gemm = [&](const GemmPhase& ph) {
@@ -242,10 +243,20 @@ orth_status_t orth_compose_kernel(orth_plan_t plan, const float* ortho, float* k
       if (!e) e = launch_soc_alpha(P, stream);
       if (!e) e = launch_soc_sum(P, stream);
     }
+    if (!e && !P.sll.empty()) {   // f4: AOL rescale of the SLL kernels
+      gemm(P.sll_v);
+      if (!e) e = launch_sll_scale(P, ortho, stream);
+    }
   }
   if (!e) {
     Trace tr(P, ORTH_TK_EMIT, -1, stream);
     e = launch_emit(P, bufs, kernels_f32, (uint16_t*)kernels_bf16, stream);
+  }
+  if (!e && !P.blk.empty()) {   // f4: merge the SLL blocks' kernels once per update, then emit them
+    Trace tr(P, ORTH_TK_COMPOSE, -1, stream);
+    gemm(P.blk_mm);
+    if (!e) e = launch_blk_merge(P, stream);
+    if (!e) e = launch_emit_list(P, P.emit2, P.d_emit2, bufs, kernels_f32, (uint16_t*)kernels_bf16, stream);
   }
   return cuda_fail(e, "orth_compose_kernel");
 }
@@ -260,6 +271,22 @@ orth_status_t orth_conv_forward(orth_plan_t plan, int32_t layer, const void* ker
   if (st != ORTH_OK) return st;
   NvtxRange nv("orth_conv_forward");
   Trace tr(P, ORTH_TK_CONV_FWD, layer, stream);
+  const LayerInfo& L = P.layers[layer];
+  if (L.cons == CONS_SLL_BLOCK) {   // f4: y = M *_s [x | relu(C * x + bias)]
+    if ((int64_t)N * H * W * 4 > L.blk_scratch_bytes) {
+      set_error("SLL block %d: N*H*W exceeds the declared grid_h/grid_w x max_batch (its h and [x | h] scratch)", layer);
+      return ORTH_ERR_SHAPE_MISMATCH;
+    }
+    const LayerInfo& Lc = P.blk_conv[2 * L.blk_id];
+    const LayerInfo& Lm = P.blk_conv[2 * L.blk_id + 1];
+    const size_t es = io == ORTH_BF16 ? 2 : 4;
+    const void* km = static_cast<const char*>(kernel) + (size_t)L.m_off * es;
+    int e = launch_conv_fwd(Lc, kernel, Lc.wt_scratch, bias, x, L.blk_h, N, H, W, H, W, io, stream);
+    if (!e) e = launch_relu_concat(x, L.blk_h, L.blk_z, (int64_t)N * H * W, L.ci, L.blk_cs, io, stream);
+    if (!e) e = launch_conv_fwd(Lm, km, Lm.wt_scratch, nullptr, L.blk_z, y, N, H, W, Ho, Wo, io, stream);
+    P.launches += 3;
+    return cuda_fail(e, "orth_conv_forward (SLL block)");
+  }
   const int e = launch_conv_fwd(P.layers[layer], kernel, P.layers[layer].wt_scratch, bias, x, y, N, H, W, Ho, Wo, io, stream);
   P.launches++;
   return cuda_fail(e, "orth_conv_forward");
@@ -274,6 +301,7 @@ orth_status_t orth_conv_transpose(orth_plan_t plan, int32_t layer, const void* k
   int Ho = 0, Wo = 0;
   st = check_conv(P, layer, kernel, y_small, x_big, N, H_big, W_big, io, Ho, Wo);
   if (st != ORTH_OK) return st;
+  if (P.layers[layer].cons == CONS_SLL_BLOCK) { set_error("an SLL block is not linear: no adjoint"); return ORTH_ERR_UNSUPPORTED_CONFIG; }
   NvtxRange nv("orth_conv_transpose");
   Trace tr(P, ORTH_TK_CONV_ADJ, layer, stream);
   const int e = launch_conv_bwd(P.layers[layer], kernel, P.layers[layer].wt_scratch, bias, y_small, x_big, N, H_big, W_big, Ho,

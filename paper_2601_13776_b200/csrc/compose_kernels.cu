@@ -103,11 +103,12 @@ __global__ void __launch_bounds__(128) emit_kernel(const EmitItem* __restrict__ 
 
 }  // namespace
 
-int launch_emit(Plan& p, const float* const bufs[BUF_COUNT], float* kf32, uint16_t* kbf16, void* stream) {
-  if (p.emit.empty()) return 0;
+int launch_emit_list(Plan& p, const std::vector<EmitItem>& items, const EmitItem* d_items,
+                     const float* const bufs[BUF_COUNT], float* kf32, uint16_t* kbf16, void* stream) {
+  if (items.empty()) return 0;
   int maxco = 1;
   size_t smem = 16;
-  for (auto& e : p.emit) {
+  for (auto& e : items) {
     maxco = e.co > maxco ? e.co : maxco;
     if (e.mode != 2) smem = std::max(smem, (size_t)e.k * e.k * e.ci * sizeof(float));
   }
@@ -116,12 +117,16 @@ int launch_emit(Plan& p, const float* const bufs[BUF_COUNT], float* kf32, uint16
     cudaFuncSetAttribute(emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
-  dim3 grid((unsigned)(maxco < 256 ? maxco : 256), (unsigned)p.emit.size());
-  launch_pdl(emit_kernel, grid, dim3(128), smem, (cudaStream_t)stream, (const EmitItem*)p.d_emit,
+  dim3 grid((unsigned)(maxco < 256 ? maxco : 256), (unsigned)items.size());
+  launch_pdl(emit_kernel, grid, dim3(128), smem, (cudaStream_t)stream, d_items,
              (const float*)bufs[0], (const float*)bufs[1], (const float*)bufs[2], (const float*)bufs[3], kf32,
              reinterpret_cast<__nv_bfloat16*>(kbf16));
   p.launches++;
   return (int)cudaGetLastError();
+}
+
+int launch_emit(Plan& p, const float* const bufs[BUF_COUNT], float* kf32, uint16_t* kbf16, void* stream) {
+  return launch_emit_list(p, p.emit, p.d_emit, bufs, kf32, kbf16, stream);
 }
 
 

@@ -13,7 +13,8 @@ struct CUtensorMap_st;   // cuda.h (TMA descriptors), forward-declared for the l
 namespace orth {
 
 enum Role : int32_t { ROLE_Q = 0, ROLE_U = 1, ROLE_R = 2, ROLE_W = 3, ROLE_K = 4 };
-enum Construct : int32_t { CONS_BCOP = 0, CONS_RKO = 1, CONS_AOC = 2, CONS_DENSE = 3, CONS_SOC = 4 };
+enum Construct : int32_t { CONS_BCOP = 0, CONS_RKO = 1, CONS_AOC = 2, CONS_DENSE = 3, CONS_SOC = 4, CONS_SLL = 5,
+                           CONS_SLL_BLOCK = 6 };
 enum BufId : int32_t { BUF_NONE = -1, BUF_X = 0, BUF_Y = 1, BUF_G = 2, BUF_W = 3, BUF_COUNT = 4 };
 
 constexpr int kPadF32 = 32;    // 128 B alignment of every packed float object
@@ -41,6 +42,14 @@ struct LayerInfo {
   int32_t pt, pb, pl, pr;
   int32_t kp, c_b, c_mid;
   int32_t k_free, soc_terms;    // ORTH_SOC: free kernel size and series order (k = k_eff for the conv)
+  // ORTH_SLL_BLOCK: referenced layers, merged kernel sizes / top pads, offset of M in the kernel region,
+  // index of its two conv views in Plan::blk_conv (2 * blk_id: C, 2 * blk_id + 1: M), scratch for h and [x | h]
+  int32_t blk_pre = -1, blk_sll = -1, blk_post = -1, blk_id = -1, blk_cs = 0;
+  int32_t kC = 0, kM = 0, pC = 0, pM = 0;
+  int64_t m_off = 0;
+  void* blk_h = nullptr;
+  void* blk_z = nullptr;
+  int64_t blk_scratch_bytes = 0;
   int32_t first_mat, mats_per_group;
   int32_t owner;                // owner of group 0 (ORTH_Q_LAYER_OWNER)
   int32_t first_unit;           // units [first_unit, first_unit + g) of Plan::units
@@ -182,6 +191,20 @@ struct SocItem {
   int64_t u_off[kSocMaxTerms + 1];   // u_off[1] = S (skew part), u_off[j] = S^(*)j, j >= 2 (u_off[2] always)
 };
 
+// f4 (sll.cu): AOL rescale of one SLL unit; offsets in the composition workspace except src_off (ortho)
+struct SllItem {
+  int32_t ci, co, k, pad_;
+  int64_t src_off;      // free kernel W (co, ci, k, k) in ortho
+  int64_t v_off;        // V[Delta] = sum_t W_t^T W_{t+Delta}: (2k-1)^2 taps of ci x ci
+  int64_t s_off;        // per-input-channel scale d_i^{-1/2} (ci floats)
+  int64_t kt_off;       // rescaled kernel, tap-major k^2 x co x ci
+};
+// f4: one SLL x AOC block: M = [A | -2 B] from the A / B products (comp workspace)
+struct BlkItem {
+  int32_t c, cs, co, kA, kB, kM, oa, ob;
+  int64_t a_off, b_off, m_off, c_off;   // A, B, M, C (tap-major) in comp
+};
+
 struct TcComposePlan;   // tensor-core composition (compose_tc.cu)
 }  // namespace orth
 struct orth_trace_state;   // abi.cu (orth_plan_trace)
@@ -262,6 +285,15 @@ struct Plan {
   std::vector<int64_t> soc_copy;    // (offset, numel) pairs of owned SOC free kernels (params -> ortho)
   SocItem* d_soc = nullptr;
   float* d_soc_alpha = nullptr;
+  std::vector<SllItem> sll;         // f4
+  GemmPhase sll_v;                  // V of every SLL unit
+  std::vector<BlkItem> blk;
+  GemmPhase blk_mm;                 // C, A, B of every block (read the emitted FP32 kernels: BUF_Y)
+  std::vector<LayerInfo> blk_conv;  // conv views of every block: [C, M] per block
+  std::vector<EmitItem> emit2;      // the blocks' C and M (after the first emit)
+  SllItem* d_sll = nullptr;
+  BlkItem* d_blk = nullptr;
+  EmitItem* d_emit2 = nullptr;
   int64_t comp_proj_off = 0, comp_ping_off = 0, comp_pong_off = 0, comp_final_off = 0;
 
   // device allocations
@@ -354,6 +386,12 @@ int launch_certify(const LayerInfo& L, const float* kernel, int H, int W, int it
 int launch_soc_skew(Plan& p, const float* ortho, void* stream);
 int launch_soc_alpha(Plan& p, void* stream);
 int launch_soc_sum(Plan& p, void* stream);
+// f4 (sll.cu)
+int launch_sll_scale(Plan& p, const float* ortho, void* stream);   // d_i -> s_i, then the rescaled tap-major kernel
+int launch_blk_merge(Plan& p, void* stream);                 // M = [A | -2 B]
+int launch_emit_list(Plan& p, const std::vector<EmitItem>& items, const EmitItem* d_items,
+                     const float* const bufs[BUF_COUNT], float* kf32, uint16_t* kbf16, void* stream);
+int launch_relu_concat(const void* x, const void* h, void* z, int64_t pixels, int c, int cs, int io, void* stream);
 // a8: copy every unit from the gather layout to the final layout
 int launch_assemble(Plan& p, const float* gf, float* kf, const uint16_t* gb, uint16_t* kb, void* stream);
 // per-layer conv scratch (bytes) for calls up to N x Hbig x Wbig (forward-conv input grid), both

@@ -45,7 +45,7 @@ static orth_status_t validate_opts(const orth_opts_t& o) {
 }
 
 static orth_status_t validate_layer(const orth_layer_desc_t& L, int idx) {
-  if (L.kind < 0 || L.kind > 3) { set_error("layer %d: bad kind %d", idx, L.kind); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (L.kind < 0 || L.kind > 5) { set_error("layer %d: bad kind %d", idx, L.kind); return ORTH_ERR_INVALID_ARGUMENT; }
   if (L.c_in < 1 || L.c_out < 1 || L.k_h < 1 || L.k_w < 1 || L.stride_h < 1 || L.stride_w < 1 || L.dil_h < 1 ||
       L.dil_w < 1 || L.groups < 1) {
     set_error("layer %d: every dimension must be >= 1 (S:31)", idx);
@@ -73,6 +73,13 @@ static orth_status_t validate_layer(const orth_layer_desc_t& L, int idx) {
   if (L.k_h != L.k_w || L.stride_h != L.stride_w || L.dil_h != L.dil_w) {
     set_error("layer %d: only square kernel/stride/dilation are supported", idx);
     return ORTH_ERR_UNSUPPORTED_CONFIG;
+  }
+  if (L.kind == ORTH_SLL || L.kind == ORTH_SLL_BLOCK) {   // f4: plain, circular, g = d = 1
+    if (L.groups != 1 || L.dil_h != 1) { set_error("layer %d: SLL layers / blocks need g = d = 1", idx); return ORTH_ERR_UNSUPPORTED_CONFIG; }
+    if (L.padding_mode != ORTH_PAD_CIRCULAR) { set_error("layer %d: the SLL block is exact for circular padding only (R30)", idx); return ORTH_ERR_UNSUPPORTED_CONFIG; }
+    if (L.pad_t != -1) { set_error("layer %d: SLL layers / blocks use the 'same' pads (pads must be -1)", idx); return ORTH_ERR_INVALID_ARGUMENT; }
+    if (L.kind == ORTH_SLL && L.stride_h != 1) { set_error("layer %d: an SLL kernel has stride 1", idx); return ORTH_ERR_UNSUPPORTED_CONFIG; }
+    return ORTH_OK;
   }
   if (L.kind == ORTH_SOC) {   // f3: square channel map, odd kernel, stride 1 (R27)
     const int n = L.soc_terms == 0 ? 6 : L.soc_terms;
@@ -111,7 +118,25 @@ static orth_status_t derive(Plan& P, const orth_layer_desc_t* layers, int n_laye
       L.pt = L.pl = e / 2; L.pb = L.pr = e - e / 2;     // R11
     } else { L.pt = D.pad_t; L.pb = D.pad_b; L.pl = D.pad_l; L.pr = D.pad_r; }
     std::vector<std::pair<int, std::pair<int64_t, int64_t>>> ms;  // role, (m, n)
-    if (D.kind == ORTH_SOC) {
+    if (D.kind == ORTH_SLL) {
+      L.cons = CONS_SLL;
+      ms.push_back({ROLE_K, {L.co, (int64_t)L.ci * L.k * L.k}});
+    } else if (D.kind == ORTH_SLL_BLOCK) {   // merged kernels of three earlier layers (validated)
+      L.cons = CONS_SLL_BLOCK;
+      L.blk_id = 0;
+      for (const auto& Q : P.layers) L.blk_id += Q.cons == CONS_SLL_BLOCK ? 1 : 0;
+      L.blk_pre = D.blk_pre; L.blk_sll = D.blk_sll; L.blk_post = D.blk_post;
+      const LayerInfo &Pre = P.layers[D.blk_pre], &S = P.layers[D.blk_sll], &Po = P.layers[D.blk_post];
+      L.blk_cs = S.co;
+      const int kA = Po.k + Pre.k - 1, kB = Po.k + S.k - 1;
+      L.kC = S.k + Pre.k - 1;
+      L.pC = S.pt + Pre.pt;
+      const int pA = Po.pt + Pre.pt, pB = Po.pt + (S.k - 1 - S.pt);
+      L.pM = std::max(pA, pB);
+      L.kM = std::max(L.pM - pA + kA, L.pM - pB + kB);
+      L.k = L.kM;
+      L.pt = L.pl = L.pM; L.pb = L.pr = L.kM - 1 - L.pM;
+    } else if (D.kind == ORTH_SOC) {
       L.cons = CONS_SOC;
       L.k_free = D.k_h;
       L.soc_terms = D.soc_terms == 0 ? 6 : D.soc_terms;
@@ -138,6 +163,10 @@ static orth_status_t derive(Plan& P, const orth_layer_desc_t* layers, int n_laye
     L.first_mat = (int)P.mats.size();
     L.mats_per_group = (int)ms.size();
     L.kernel_numel = (D.kind == ORTH_DENSE) ? (int64_t)L.co * L.ci : (int64_t)L.co_f * L.ci * L.k * L.k;
+    if (D.kind == ORTH_SLL_BLOCK) {   // [C (c_s, c, kC, kC) | M (c_out, c + c_s, kM, kM)], M 128 B aligned
+      L.m_off = pad_up((int64_t)L.blk_cs * L.ci * L.kC * L.kC, 64);
+      L.kernel_numel = L.m_off + (int64_t)L.co * (L.ci + L.blk_cs) * L.kM * L.kM;
+    }
     double fl = 0.0;
     for (int gi = 0; gi < L.g; ++gi)
       for (auto& e : ms) {
@@ -199,6 +228,12 @@ static void assign_owners(Plan& P) {
     P.units[u].owner = best;
     load[best] += cost(u) + 1.0;
   }
+  for (auto& L : P.layers)   // an SLL block is merged on one rank: its three layers follow its owner
+    if (L.cons == CONS_SLL_BLOCK)
+      for (int r : {L.blk_pre, L.blk_sll, L.blk_post}) {
+        const LayerInfo& M = P.layers[r];
+        for (int g = 0; g < M.g; ++g) P.units[M.first_unit + g].owner = P.units[L.first_unit].owner;
+      }
   for (auto& L : P.layers) L.owner = P.units[L.first_unit].owner;
 }
 
@@ -604,6 +639,111 @@ static void build_compose(Plan& P) {
     }
   }
   for (auto& ph : P.soc_pow) finish_phase(ph);
+  // f4 SLL units: V[Delta] = sum_t W_t^T W_{t+Delta} read in place from ortho (W: (co, ci, k, k)), the
+  // per-input-channel scale, the rescaled tap-major kernel (R28)
+  P.sll.clear();
+  P.sll_v = GemmPhase{};
+  std::vector<int64_t> sll_kt(units.size(), -1);
+  for (size_t ui = 0; ui < units.size(); ++ui) {
+    const auto& u = units[ui];
+    const LayerInfo& L = P.layers[u.layer];
+    if (L.cons != CONS_SLL) continue;
+    SllItem it{};
+    it.ci = L.ci; it.co = L.co; it.k = L.k;
+    it.src_off = P.mats[L.first_mat].off;
+    const int k2 = 2 * L.k - 1, kk = L.k * L.k;
+    const int64_t c2 = (int64_t)L.ci * L.ci;
+    it.v_off = w; w += pad_up((int64_t)k2 * k2 * c2, kPadF32);
+    it.s_off = w; w += pad_up(L.ci, kPadF32);
+    it.kt_off = w; w += pad_up((int64_t)kk * L.co * L.ci, kPadF32);
+    sll_kt[ui] = it.kt_off;
+    for (int d1 = -(L.k - 1); d1 < L.k; ++d1)
+      for (int d2 = -(L.k - 1); d2 < L.k; ++d2) {
+        GemmDesc d = mk(L.ci, L.ci, L.co);
+        d.a_buf = BUF_X; d.b_buf = BUF_X; d.d_buf = BUF_W;
+        d.sa_m = kk; d.sa_k = (int64_t)L.ci * kk; d.sb_k = (int64_t)L.ci * kk; d.sb_n = kk;
+        d.d_off = it.v_off + (int64_t)((d1 + L.k - 1) * k2 + (d2 + L.k - 1)) * c2; d.ldd = L.ci;
+        for (int a1 = 0; a1 < L.k; ++a1)
+          for (int a2 = 0; a2 < L.k; ++a2) {
+            const int b1 = a1 + d1, b2 = a2 + d2;
+            if (b1 < 0 || b2 < 0 || b1 >= L.k || b2 >= L.k) continue;
+            add_seg(P.sll_v, d, it.src_off + a1 * L.k + a2, -1, it.src_off + b1 * L.k + b2);
+          }
+        if (d.seg_count == 0) {   // no overlapping taps cannot happen for |Delta| < k, kept for safety
+          add_seg(P.sll_v, d, it.src_off, -1, it.src_off);
+          d.alpha = 0.f;
+        }
+        P.sll_v.descs.push_back(d);
+      }
+    P.sll.push_back(it);
+  }
+  finish_phase(P.sll_v);
+  // f4 SLL x AOC blocks: C, A, B from the emitted FP32 kernels of the three layers (BUF_Y = kernels_f32, at
+  // the offsets the first emit wrote), M = [A | -2 B] (R29), second emit into the block's kernel region
+  P.blk.clear();
+  P.blk_mm = GemmPhase{};
+  P.emit2.clear();
+  auto kofs = [&](int layer) {
+    const UnitInfo& U = P.units[P.layers[layer].first_unit];
+    return P.opts.world > 1 ? U.gat_f32 : U.fin_f32;
+  };
+  for (auto& u : units) {
+    const LayerInfo& L = P.layers[u.layer];
+    if (L.cons != CONS_SLL_BLOCK) continue;
+    const LayerInfo &Pre = P.layers[L.blk_pre], &S = P.layers[L.blk_sll], &Po = P.layers[L.blk_post];
+    const int c = L.ci, cs = L.blk_cs, co = L.co, kp = Pre.k, ks = S.k, kq = Po.k;
+    const int64_t pre = kofs(L.blk_pre), sl = kofs(L.blk_sll), post = kofs(L.blk_post);
+    BlkItem b{};
+    b.c = c; b.cs = cs; b.co = co;
+    b.kA = kq + kp - 1; b.kB = kq + ks - 1; b.kM = L.kM;
+    b.oa = L.pM - (Po.pt + Pre.pt);
+    b.ob = L.pM - (Po.pt + (ks - 1 - S.pt));
+    b.c_off = w; w += pad_up((int64_t)L.kC * L.kC * cs * c, kPadF32);
+    b.a_off = w; w += pad_up((int64_t)b.kA * b.kA * co * c, kPadF32);
+    b.b_off = w; w += pad_up((int64_t)b.kB * b.kB * co * cs, kPadF32);
+    b.m_off = w; w += pad_up((int64_t)b.kM * b.kM * co * (c + cs), kPadF32);
+    // X[p] = sum_{a + b = p} F[a] G[b] over PyTorch-layout factors: F tap a (rows x inner) at fo + (r * inner + i) kf^2 + a
+    auto prod = [&](int rows, int inner, int cols, int64_t fo, int kf, int64_t go, int kg, bool g_adj, int64_t out) {
+      const int kx = kf + kg - 1;
+      for (int p1 = 0; p1 < kx; ++p1)
+        for (int p2 = 0; p2 < kx; ++p2) {
+          GemmDesc d = mk(rows, cols, inner);
+          d.a_buf = BUF_Y; d.b_buf = BUF_Y; d.d_buf = BUF_W;
+          d.sa_m = (int64_t)inner * kf * kf; d.sa_k = (int64_t)kf * kf;
+          if (!g_adj) { d.sb_k = (int64_t)cols * kg * kg; d.sb_n = (int64_t)kg * kg; }   // G[i][j] at (i cols + j) kg^2
+          else { d.sb_k = (int64_t)kg * kg; d.sb_n = (int64_t)inner * kg * kg; }          // G = K^T flipped: K[j][i]
+          d.d_off = out + (int64_t)(p1 * kx + p2) * rows * cols; d.ldd = cols;
+          for (int a1 = 0; a1 < kf; ++a1)
+            for (int a2 = 0; a2 < kf; ++a2) {
+              const int b1 = p1 - a1, b2 = p2 - a2;
+              if (b1 < 0 || b2 < 0 || b1 >= kg || b2 >= kg) continue;
+              const int gt = g_adj ? (kg * kg - 1 - (b1 * kg + b2)) : (b1 * kg + b2);
+              add_seg(P.blk_mm, d, fo + a1 * kf + a2, -1, go + gt);
+            }
+          P.blk_mm.descs.push_back(d);
+        }
+    };
+    prod(cs, c, c, sl, ks, pre, kp, false, b.c_off);     // C = K (*) K_pre
+    prod(co, c, c, post, kq, pre, kp, false, b.a_off);   // A = K_post (*) K_pre
+    prod(co, c, cs, post, kq, sl, ks, true, b.b_off);    // B = K_post (*) K^T
+    P.blk.push_back(b);
+    const UnitInfo& U = P.units[L.first_unit];
+    EmitItem ec{}, em{};
+    ec.layer = em.layer = u.layer;
+    ec.co = cs; ec.ci = c; ec.k = L.kC; ec.s = 1; ec.ci_f_per_g = c;
+    ec.src_buf = BUF_W; ec.src_off = b.c_off; ec.tap_stride = (int64_t)cs * c; ec.ld = c;
+    ec.mode = (int64_t)L.kC * L.kC * c * 4 > 96 * 1024 ? 2 : 0;
+    ec.f32_off = P.opts.world > 1 ? U.gat_f32 : U.fin_f32;
+    ec.bf16_off = P.opts.world > 1 ? U.gat_bf16 : U.fin_bf16;
+    em.co = co; em.ci = c + cs; em.k = L.kM; em.s = L.s; em.ci_f_per_g = c + cs;
+    em.src_buf = BUF_W; em.src_off = b.m_off; em.tap_stride = (int64_t)co * (c + cs); em.ld = c + cs;
+    em.mode = (int64_t)L.kM * L.kM * (c + cs) * 4 > 96 * 1024 ? 2 : 0;
+    em.f32_off = ec.f32_off + L.m_off;
+    em.bf16_off = ec.bf16_off + L.m_off;
+    P.emit2.push_back(ec);
+    P.emit2.push_back(em);
+  }
+  finish_phase(P.blk_mm);
   // emit items
   for (size_t ui = 0; ui < units.size(); ++ui) {
     const auto& u = units[ui];
@@ -612,6 +752,7 @@ static void build_compose(Plan& P) {
     EmitItem e{};
     e.layer = u.layer; e.group = u.group;
     e.co = L.co; e.ci = L.ci; e.k = (L.cons == CONS_DENSE) ? 1 : L.k; e.s = L.s; e.ci_f_per_g = L.ci;
+    if (L.cons == CONS_SLL_BLOCK) continue;    // written by the second emit (emit2)
     const UnitInfo& U = P.units[L.first_unit + u.group];
     e.f32_off = P.opts.world > 1 ? U.gat_f32 : U.fin_f32;     // world > 1: this rank's gather segment
     e.bf16_off = P.opts.world > 1 ? U.gat_bf16 : U.fin_bf16;
@@ -622,6 +763,10 @@ static void build_compose(Plan& P) {
         e.src_buf = BUF_X; e.src_off = P.mats[base].off; e.mode = 1; e.tap_stride = 0; e.ld = 0; break;
       case CONS_AOC:
         e.src_buf = BUF_W; e.src_off = u.fin; e.mode = 0; e.tap_stride = (int64_t)L.co * L.ci; e.ld = L.ci; break;
+      case CONS_SLL:   // the AOL-rescaled kernel, tap-major
+        e.src_buf = BUF_W; e.src_off = sll_kt[ui]; e.tap_stride = (int64_t)L.co * L.ci; e.ld = L.ci;
+        e.mode = (int64_t)L.k * L.k * L.ci * 4 > 96 * 1024 ? 2 : 0;
+        break;
       case CONS_SOC:   // E, tap-major; large k_eff^2 c rows are written without the shared-memory stage
         e.src_buf = BUF_W; e.src_off = soc_e[ui]; e.tap_stride = (int64_t)L.co * L.ci; e.ld = L.ci;
         e.mode = (int64_t)L.k * L.k * L.ci * 4 > 96 * 1024 ? 2 : 0;
@@ -653,12 +798,12 @@ static void size_conv(Plan& P) {
 static orth_status_t allocate_conv(Plan& P) {
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
-  struct Slice { size_t flags, pad, wt; };
+  struct Slice { size_t flags, pad, wt, blk_h, blk_z; };
   std::vector<Slice> sl(P.layers.size());
   std::vector<std::pair<size_t, size_t>> flag_ranges;
   for (size_t l = 0; l < P.layers.size(); ++l) {
     LayerInfo& L = P.layers[l];
-    sl[l] = Slice{0, 0, 0};
+    sl[l] = Slice{0, 0, 0, 0, 0};
     if (L.cons == CONS_DENSE) continue;
     if (L.pad_bytes > 0) {
       const size_t fb = (size_t)std::max<int64_t>(L.n_flags, 1) * sizeof(unsigned);
@@ -669,6 +814,12 @@ static orth_status_t allocate_conv(Plan& P) {
     // W^T of the adjoint, group-packed copies (<= 8x each, conv_tc.cu) when the layer packs groups
     const bool packs = L.g > 1 && (L.ci < 64 || L.co < 64);
     sl[l].wt = take((size_t)(packs ? 16 : 1) * L.kernel_numel * 2);
+    if (L.cons == CONS_SLL_BLOCK) {   // h (c_s) and [x | h] (c + c_s) of the declared grid and batch, FP32-sized
+      L.blk_scratch_bytes = (P.opts.max_batch > 0 && L.desc.grid_h > 0 && L.desc.grid_w > 0)
+                                ? (int64_t)P.opts.max_batch * L.desc.grid_h * L.desc.grid_w * 4 : 0;
+      sl[l].blk_h = take((size_t)L.blk_scratch_bytes * L.blk_cs + 16);
+      sl[l].blk_z = take((size_t)L.blk_scratch_bytes * (L.ci + L.blk_cs) + 16);
+    }
   }
   P.conv_mem_bytes = (int64_t)off;
   if (off == 0) return ORTH_OK;
@@ -688,10 +839,33 @@ static orth_status_t allocate_conv(Plan& P) {
     LayerInfo& L = P.layers[l];
     if (L.cons == CONS_DENSE) continue;
     L.wt_scratch = base + sl[l].wt;
+    if (L.cons == CONS_SLL_BLOCK) {
+      L.blk_h = base + sl[l].blk_h;
+      L.blk_z = base + sl[l].blk_z;
+    }
     if (L.pad_bytes > 0) {
       L.pad_scratch = base + sl[l].pad;
       L.conv_flags = reinterpret_cast<unsigned*>(base + sl[l].flags);
     }
+  }
+  // conv views of every SLL block: C (c -> c_s, stride 1, top pad pC) and M (c + c_s -> c_out, stride s,
+  // top pad pM), circular, sharing the block's weight scratch (no split-K / padded-copy scratch)
+  P.blk_conv.clear();
+  for (auto& L : P.layers) {
+    if (L.cons != CONS_SLL_BLOCK) continue;
+    LayerInfo c{}, m{};
+    c.desc = L.desc; c.desc.kind = ORTH_CONV2D;
+    c.cons = CONS_BCOP; c.g = 1; c.d = 1; c.s = 1;
+    c.ci_f = c.ci = L.ci; c.co_f = c.co = L.blk_cs; c.k = L.kC;
+    c.pt = c.pl = L.pC; c.pb = c.pr = L.kC - 1 - L.pC;
+    c.kernel_numel = (int64_t)c.co * c.ci * c.k * c.k;
+    c.wt_scratch = L.wt_scratch;
+    m = c;
+    m.s = L.s; m.ci_f = m.ci = L.ci + L.blk_cs; m.co_f = m.co = L.co; m.k = L.kM;
+    m.pt = m.pl = L.pM; m.pb = m.pr = L.kM - 1 - L.pM;
+    m.kernel_numel = (int64_t)m.co * m.ci * m.k * m.k;
+    P.blk_conv.push_back(c);
+    P.blk_conv.push_back(m);
   }
   return ORTH_OK;
 }
@@ -722,6 +896,11 @@ static orth_status_t allocate(Plan& P) {
                                     &P.gram_r[1], &P.update_r[0], &P.update_r[1], &P.proj, &P.aoc};
   for (auto& ph : P.chain) phases.push_back(&ph);
   for (auto& ph : P.soc_pow) phases.push_back(&ph);
+  phases.push_back(&P.sll_v);
+  phases.push_back(&P.blk_mm);
+  const size_t o_sll = take(std::max<size_t>(P.sll.size(), 1) * sizeof(SllItem));
+  const size_t o_blk = take(std::max<size_t>(P.blk.size(), 1) * sizeof(BlkItem));
+  const size_t o_em2 = take(std::max<size_t>(P.emit2.size(), 1) * sizeof(EmitItem));
   const size_t o_soc = take(std::max<size_t>(P.soc.size(), 1) * sizeof(SocItem));
   const size_t o_sal = take(std::max<size_t>(P.soc.size(), 1) * sizeof(float));
   std::vector<std::pair<size_t, size_t>> ph_off;
@@ -753,6 +932,9 @@ static orth_status_t allocate(Plan& P) {
   P.d_bx = (uint16_t*)(base + o_bx);
   P.d_units = (UnitInfo*)(base + o_units);
   P.d_soc = (SocItem*)(base + o_soc);
+  P.d_sll = (SllItem*)(base + o_sll);
+  P.d_blk = (BlkItem*)(base + o_blk);
+  P.d_emit2 = (EmitItem*)(base + o_em2);
   P.d_soc_alpha = (float*)(base + o_sal);
   P.d_ns_res = (float*)(base + o_res);
   P.d_br = (uint16_t*)(base + o_br);
@@ -769,6 +951,12 @@ static orth_status_t allocate(Plan& P) {
     e = cudaMemcpy(P.d_mat_items, P.mat_items.data(), P.mat_items.size() * sizeof(MatItem), cudaMemcpyHostToDevice);
   if (!P.col_items.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_col_items, P.col_items.data(), P.col_items.size() * sizeof(ColItem), cudaMemcpyHostToDevice);
+  if (!P.sll.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_sll, P.sll.data(), P.sll.size() * sizeof(SllItem), cudaMemcpyHostToDevice);
+  if (!P.blk.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_blk, P.blk.data(), P.blk.size() * sizeof(BlkItem), cudaMemcpyHostToDevice);
+  if (!P.emit2.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_emit2, P.emit2.data(), P.emit2.size() * sizeof(EmitItem), cudaMemcpyHostToDevice);
   if (!P.soc.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_soc, P.soc.data(), P.soc.size() * sizeof(SocItem), cudaMemcpyHostToDevice);
   if (!P.units.empty() && e == cudaSuccess)
@@ -823,6 +1011,24 @@ orth_status_t orth_validate_desc(const orth_layer_desc_t* layers, int32_t n_laye
   for (int i = 0; i < n_layers; ++i) {
     st = validate_layer(layers[i], i);
     if (st != ORTH_OK) return st;
+  }
+  for (int i = 0; i < n_layers; ++i) {   // SLL blocks: the three referenced layers (R29)
+    const orth_layer_desc_t& B = layers[i];
+    if (B.kind != ORTH_SLL_BLOCK) continue;
+    const int r[3] = {B.blk_pre, B.blk_sll, B.blk_post};
+    for (int j = 0; j < 3; ++j)
+      if (r[j] < 0 || r[j] >= i) { set_error("block %d: referenced layer %d must be an earlier layer", i, r[j]); return ORTH_ERR_INVALID_ARGUMENT; }
+    const orth_layer_desc_t &Pre = layers[B.blk_pre], &S = layers[B.blk_sll], &Po = layers[B.blk_post];
+    const bool ok = Pre.kind == ORTH_CONV2D && Pre.c_in == B.c_in && Pre.c_out == B.c_in && Pre.stride_h == 1 &&
+                    S.kind == ORTH_SLL && S.c_in == B.c_in &&
+                    Po.kind == ORTH_CONV2D && Po.c_in == B.c_in && Po.c_out == B.c_out && Po.stride_h == B.stride_h &&
+                    Pre.groups == 1 && Po.groups == 1 && Pre.dil_h == 1 && Po.dil_h == 1 && Pre.pad_t == -1 &&
+                    Po.pad_t == -1 && Pre.padding_mode == ORTH_PAD_CIRCULAR && Po.padding_mode == ORTH_PAD_CIRCULAR;
+    if (!ok) {
+      set_error("block %d: needs pre = conv c->c (s 1), sll = SLL c->c_s, post = conv c->c_out (stride s), g = d = 1, "
+                "circular, 'same' pads", i);
+      return ORTH_ERR_INVALID_ARGUMENT;
+    }
   }
   return ORTH_OK;
 }
@@ -906,6 +1112,9 @@ orth_status_t orth_plan_query(orth_plan_t plan, int32_t what, int32_t index, int
     case ORTH_Q_LAYER_NS_FLOPS: *out = (int64_t)P.layers[index].ns_flops; break;
     case ORTH_Q_LAYER_COMP_FLOPS: *out = (int64_t)P.layers[index].comp_flops; break;
     case ORTH_Q_LAYER_K_EFF: *out = P.layers[index].k; break;
+    case ORTH_Q_LAYER_BLOCK_KC: *out = P.layers[index].kC; break;
+    case ORTH_Q_LAYER_BLOCK_M_OFF: *out = P.layers[index].m_off; break;
+    case ORTH_Q_LAYER_BLOCK_PADS: *out = (int64_t)P.layers[index].pC | ((int64_t)P.layers[index].pM << 16); break;
     case ORTH_Q_COMP_FLOPS: {
       double f = 0.0;
       for (auto& u : P.units)

@@ -48,6 +48,10 @@ def oracle_construct(layers, mats, T=12, beta=0.5, prescale="power", P=3, v=None
     kernels, idx = [], 0
     for d in layers:
         OL = oracle_layer(d)
+        if d.get("kind") == "sll_block":   # f4: merged from three earlier layers' kernels -> (C, M) dict
+            kernels.append(O.sll_block_kernels(kernels[d["pre"]], kernels[d["post"]],
+                                               sll_free_kernel(layers, d["sll"], ortho)))
+            continue
         nm = len(O.layer_matrices(OL))
         groups = []
         for _ in range(OL.g):
@@ -55,6 +59,18 @@ def oracle_construct(layers, mats, T=12, beta=0.5, prescale="power", P=3, v=None
             idx += nm
         kernels.append(O.layer_kernel(OL, groups))
     return ortho, vnew, kernels
+
+
+def sll_free_kernel(layers, l, mats):
+    """The free (not yet AOL-rescaled) kernel of SLL layer l from the packed matrix list."""
+    idx = 0
+    for j, d in enumerate(layers):
+        nm = len(O.layer_matrices(oracle_layer(d))) * (d.get("g", 1) if d.get("kind") != "dense" else 1)
+        if j == l:
+            W = np.asarray(mats[idx], np.float64)
+            return W.reshape(d["c_out"], d["c_in"], d.get("k", 3), d.get("k", 3))
+        idx += nm
+    raise IndexError(l)
 
 
 def rel(a, b) -> float:

@@ -651,6 +651,8 @@ static void build_compose(Plan& P) {
     SllItem it{};
     it.ci = L.ci; it.co = L.co; it.k = L.k;
     it.src_off = P.mats[L.first_mat].off;
+    P.soc_copy.push_back(it.src_off);                       // role K: passed through params -> ortho
+    P.soc_copy.push_back(P.mats[L.first_mat].m * P.mats[L.first_mat].n);
     const int k2 = 2 * L.k - 1, kk = L.k * L.k;
     const int64_t c2 = (int64_t)L.ci * L.ci;
     it.v_off = w; w += pad_up((int64_t)k2 * k2 * c2, kPadF32);

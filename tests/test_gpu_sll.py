@@ -16,7 +16,7 @@ import torch
 
 import oracle as O
 from synth import gen
-from tests.helpers import assert_elementwise, nchw, nhwc, oracle_construct, pack_params, rel
+from tests.helpers import assert_elementwise, nchw, nhwc, oracle_construct, pack_params, rel, sll_free_kernel
 
 pytestmark = pytest.mark.gpu
 
@@ -59,13 +59,13 @@ def test_sll_block_construction(cuda_lib, case, compute):
     assert rel(Ksll, o_k[1]) < (1e-5 if compute == "f32" else 1e-4)
     # the merge alone: the oracle merging the GPU's own three kernels (K_sll already rescaled: rescale is
     # idempotent only up to rounding, so merge with the free W and compare the rescaled factor separately)
-    W = mats[1].astype(np.float64).reshape(Ksll.shape)
+    W = sll_free_kernel(layers, 1, mats)
     ref = O.sll_block_kernels(Kpre, Kpost, W)
     assert rel(Cg, ref["C"]) < 1e-4 and rel(Mg, ref["M"]) < 1e-4
     # and end to end against the oracle's construction
     tol = 1e-5 if compute == "f32" else 2e-2
     assert rel(Cg, o_k[3]["C"]) < tol and rel(Mg, o_k[3]["M"]) < tol
-    Cb, Mb = plan.block_kernels(kb.float().cpu(), 3)
+    Cb, Mb = [t.float() for t in plan.block_kernels(kb.cpu(), 3)]
     assert np.array_equal(Cb.numpy().transpose(0, 3, 1, 2), gen.bf16_round(Cg.astype(np.float32)))
     assert np.array_equal(Mb.numpy().transpose(0, 3, 1, 2), gen.bf16_round(Mg.astype(np.float32)))
 

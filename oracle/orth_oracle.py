@@ -39,6 +39,7 @@ __all__ = [
     "conv_singular_values", "spectral_certificate",
     "soc_skew", "aol_scale", "soc_exp_kernel",
     "aol_rescale", "adjoint_kernel", "same_pads", "sll_block_kernels", "sll_block_forward", "sll_block_unfused",
+    "conv2d_wgrad", "bjorck_vjp", "orthogonalize_vjp", "block_conv_vjp", "layer_kernel_vjp",
 ]
 
 
@@ -638,3 +639,135 @@ def sll_block_unfused(x: np.ndarray, K_pre: np.ndarray, K_post: np.ndarray, K: n
     t = np.maximum(conv2d(z, K) + np.asarray(b, np.float64)[None, :, None, None], 0.0)
     u = z - 2.0 * conv_transpose2d(t, K, z.shape[2], z.shape[3])
     return conv2d(u, K_post, s=s)
+
+
+# ---------------------------------------------------------------------------
+# f1: backward of the path ("per-batch cost grows as soon as weights are
+# iteratively projected", P:122 the <= 1.13x ImageNet TRAINING wall time; readings R31-R33)
+# ---------------------------------------------------------------------------
+def conv2d_wgrad(x: np.ndarray, dy: np.ndarray, kshape, s: int = 1, d: int = 1, g: int = 1, pads=None,
+                 mode: str = "circular") -> np.ndarray:
+    """Weight gradient of conv2d (the bilinear form <dy, conv2d(x, dK)> = <wgrad, dK>):
+    dK[o, i, a, b] = sum_{n,u,v} dy[n, o, u, v] x~[n, grp(o) i, s u + d a - p_t, s v + d b - p_l]."""
+    x = np.asarray(x, np.float64)
+    dy = np.asarray(dy, np.float64)
+    N, C, H, W = x.shape
+    Co, Cig, kh, kw = kshape
+    if pads is None:
+        pads = same_pads(kh, d)
+    pt, pb, pl, pr = pads
+    Ho, Wo = dy.shape[2], dy.shape[3]
+    circ = mode == "circular"
+    Cog = Co // g
+    dK = np.zeros(kshape)
+    for a in range(kh):
+        rows, rok = _tap_rows(H, Ho, s, d, a, pt, circ)
+        for b in range(kw):
+            cols, cok = _tap_rows(W, Wo, s, d, b, pl, circ)
+            patch = x[:, :, rows][:, :, :, cols] * (rok[:, None] & cok[None, :])
+            for gi in range(g):
+                dK[gi * Cog:(gi + 1) * Cog, :, a, b] = np.einsum(
+                    "nohw,nihw->oi", dy[:, gi * Cog:(gi + 1) * Cog], patch[:, gi * Cig:(gi + 1) * Cig])
+    return dK
+
+
+def bjorck_vjp(W0: np.ndarray, T: int, beta: float, G: np.ndarray) -> np.ndarray:
+    """VJP of bjorck(W0, T, beta) (the forward iteration of O3, replayed): with A = X^T X, the step
+    X' = (1+beta) X - beta X A has the adjoint dX = (1+beta) G - beta (G A + X G^T X + X X^T G)  (m >= n;
+    for m < n the transposed form).  Iterates are recomputed, then reversed."""
+    X = np.asarray(W0, np.float64)
+    m, n = X.shape
+    xs = []
+    for _ in range(T):
+        xs.append(X)
+        X = (1 + beta) * X - beta * (X @ (X.T @ X) if m >= n else (X @ X.T) @ X)
+    G = np.asarray(G, np.float64)
+    for X in reversed(xs):
+        if m >= n:
+            G = (1 + beta) * G - beta * (G @ (X.T @ X) + X @ G.T @ X + X @ X.T @ G)
+        else:
+            G = (1 + beta) * G - beta * ((X @ X.T) @ G + X @ G.T @ X + G @ X.T @ X)
+    return G
+
+
+def orthogonalize_vjp(mats, G, T: int = 12, beta: float = 0.5, prescale: str = "power", P: int = 3, v=None):
+    """VJP of orthogonalize (a2 + a3) with the pre-scale treated as a constant (reading R31: sigma is a
+    stop-gradient preconditioner; at convergence the polar factor is scale-invariant so its derivative along
+    W is 0 anyway): dW = bjorck_vjp(W / sigma, T, beta, G) / sigma."""
+    out = []
+    for idx, W in enumerate(mats):
+        W = np.asarray(W, np.float64)
+        if W.size == 0:
+            out.append(W.copy())
+            continue
+        n = W.shape[1]
+        if prescale == "power":
+            v0 = np.ones(n) / math.sqrt(n) if v is None else np.asarray(v[idx], np.float64)
+            W0, sig, _ = prescale_power(W, P, v0)
+        else:
+            W0, sig = prescale_frobenius(W)
+        out.append(bjorck_vjp(W0, T, beta, G[idx]) / sig)
+    return out
+
+
+def block_conv_vjp(K1: np.ndarray, K2: np.ndarray, dK: np.ndarray):
+    """Adjoint of block_conv in both factors: dK1[a] = sum_c dK[a + c] K2[c]^T, dK2[c] = sum_a K1[a]^T dK[a + c]."""
+    _, _, h1, w1 = K1.shape
+    _, _, h2, w2 = K2.shape
+    d1, d2 = np.zeros(K1.shape), np.zeros(K2.shape)
+    for a in range(h1):
+        for b in range(w1):
+            for c in range(h2):
+                for e in range(w2):
+                    d1[:, :, a, b] += dK[:, :, a + c, b + e] @ K2[:, :, c, e].T
+                    d2[:, :, c, e] += K1[:, :, a, b].T @ dK[:, :, a + c, b + e]
+    return d1, d2
+
+
+def _bcop_vjp(Q, Us, c_out, c_in, dK):
+    c = Q.shape[0]
+    I = np.eye(c)
+    Ps = [np.asarray(U, np.float64) @ np.asarray(U, np.float64).T if U.size else np.zeros((c, c)) for U in Us]
+    Ks = [np.asarray(Q, np.float64)[:, :, None, None]]
+    Bs = []
+    for j in range(len(Ps) // 2):
+        Bs.append(block_orth(Ps[2 * j], Ps[2 * j + 1]))
+        Ks.append(block_conv(Ks[-1], Bs[-1]))
+    dcur = np.zeros(Ks[-1].shape)
+    dcur[:c_out, :c_in] = dK                                # adjoint of the slice: zero padding
+    dPs = [None] * len(Ps)
+    for j in reversed(range(len(Bs))):
+        dprev, dB = block_conv_vjp(Ks[j], Bs[j], dcur)
+        Pa, Pb = Ps[2 * j], Ps[2 * j + 1]
+        d00, d01, d10, d11 = dB[:, :, 0, 0], dB[:, :, 0, 1], dB[:, :, 1, 0], dB[:, :, 1, 1]
+        dPs[2 * j] = d00 @ Pb.T + d01 @ (I - Pb).T - d10 @ Pb.T - d11 @ (I - Pb).T
+        dPs[2 * j + 1] = Pa.T @ d00 - Pa.T @ d01 + (I - Pa).T @ d10 - (I - Pa).T @ d11
+        dcur = dprev
+    dQ = dcur[:, :, 0, 0]
+    dUs = [(dP + dP.T) @ np.asarray(U, np.float64) if U.size else np.zeros(U.shape) for dP, U in zip(dPs, Us)]
+    return [dQ] + dUs
+
+
+def layer_kernel_vjp(L: Layer, group_mats, dK: np.ndarray):
+    """Adjoint of layer_kernel (a4 + a5) for AOC / BCOP / RKO / dense layers: per group the matrix gradients
+    in layer_matrices() order, from the gradient of the forward-conv kernel (co_f, ci_f/g, k, k)."""
+    geo = layer_geometry(L)
+    co = geo["co"]
+    out = []
+    for gi, mats in enumerate(group_mats):
+        mats = [np.asarray(M, np.float64) for M in mats]
+        dKg = np.asarray(dK, np.float64)[gi * co:(gi + 1) * co]
+        if geo["kind"] == "dense":
+            out.append([dKg.reshape(mats[0].shape)])
+        elif geo["kind"] == "bcop":
+            out.append(_bcop_vjp(mats[0], mats[1:], geo["co"], geo["ci"], dKg))
+        elif geo["kind"] == "rko":
+            out.append([dKg.reshape(mats[0].shape)])
+        elif geo["kind"] == "aoc":
+            Kb = bcop(mats[0], mats[1:-1], geo["c_mid"], geo["ci"])
+            Kr = rko(mats[-1], geo["co"], geo["c_mid"], L.s)
+            dKr, dKb = block_conv_vjp(Kr, Kb, dKg)
+            out.append(_bcop_vjp(mats[0], mats[1:-1], geo["c_mid"], geo["ci"], dKb) + [dKr.reshape(mats[-1].shape)])
+        else:
+            raise ValueError(f"no VJP for {geo['kind']}")
+    return out

@@ -591,3 +591,78 @@ def test_sll_block_special_cases_and_lipschitz():
         J = torch.autograd.functional.jacobian(lambda z: _torch_block(z, K_pre, K_post, kern["K"], b, 2), x0)
         J = J.reshape(-1, x0.numel()).numpy()
         assert np.linalg.svd(J, compute_uv=False)[0] <= 1 + 1e-9
+
+
+# ------------------------------------------------------------------ f1: backward (VJPs) of the path
+def test_conv2d_wgrad_matches_torch_and_bilinear():
+    """The weight gradient against torch.nn.grad.conv2d_weight (zero padding; library routine) and the exact
+    bilinear identity <dy, conv2d(x, dK)> = <wgrad(x, dy), dK> (circular, strided, dilated, grouped)."""
+    for (ci, co, k, s, d, g, mode) in [(4, 6, 3, 1, 1, 1, "zeros"), (4, 6, 3, 2, 1, 2, "zeros"),
+                                       (6, 4, 3, 2, 1, 1, "circular"), (4, 8, 3, 1, 2, 2, "circular")]:
+        x = rs.standard_normal((2, ci, 8, 8))
+        K = rs.standard_normal((co, ci // g, k, k))
+        y = O.conv2d(x, K, s=s, d=d, g=g, mode=mode)
+        dy = rs.standard_normal(y.shape)
+        dK = O.conv2d_wgrad(x, dy, K.shape, s=s, d=d, g=g, mode=mode)
+        dK2 = rs.standard_normal(K.shape)
+        lhs = float((dy * O.conv2d(x, dK2, s=s, d=d, g=g, mode=mode)).sum())
+        assert abs(lhs - float((dK * dK2).sum())) < 1e-10 * max(1.0, abs(lhs))
+        if mode == "zeros":
+            p = d * (k - 1) // 2
+            ref = torch.nn.grad.conv2d_weight(t64(x), K.shape, t64(dy), stride=s, padding=p, dilation=d, groups=g)
+            assert np.abs(ref.numpy() - dK).max() < 1e-10
+
+
+@pytest.mark.parametrize("shape,T", [((12, 7), 5), ((7, 12), 5), ((10, 10), 12)])
+def test_bjorck_vjp_finite_differences(shape, T):
+    """Central finite differences of f(W0) = <G, bjorck(W0)> along random directions (float64, eps 1e-6)."""
+    W = rs.standard_normal(shape)
+    W0 = W / np.linalg.svd(W, compute_uv=False)[0] * 0.9
+    G = rs.standard_normal(shape)
+    dW = O.bjorck_vjp(W0, T, 0.5, G)
+    for _ in range(3):
+        D = rs.standard_normal(shape)
+        eps = 1e-6
+        fd = ((G * O.bjorck(W0 + eps * D, T)).sum() - (G * O.bjorck(W0 - eps * D, T)).sum()) / (2 * eps)
+        assert abs(fd - (dW * D).sum()) < 1e-6 * max(1.0, abs(fd))
+
+
+def test_orthogonalize_vjp_sigma_constant():
+    """R31: with the pre-scale held constant the VJP is bjorck_vjp / sigma; checked by finite differences of
+    W -> <G, bjorck(W / sigma_fixed)>."""
+    W = gen.param_matrix(9, 6, (5, 5, 5, 0, 1)).astype(np.float64)
+    G = rs.standard_normal(W.shape)
+    (dW,) = O.orthogonalize_vjp([W], [G], T=8)
+    W0, sig, _ = O.prescale_power(W, 3, np.ones(6) / math.sqrt(6))
+    D = rs.standard_normal(W.shape)
+    eps = 1e-6
+    f = lambda A: (G * O.bjorck(A / sig, 8)).sum()
+    assert abs((f(W + eps * D) - f(W - eps * D)) / (2 * eps) - (dW * D).sum()) < 1e-6
+
+
+@pytest.mark.parametrize("ci,co,k,s,g", [(4, 4, 3, 1, 1), (4, 8, 3, 2, 1), (6, 3, 2, 1, 1), (4, 6, 4, 2, 2),
+                                         (3, 8, 2, 2, 1)])
+def test_layer_kernel_vjp_finite_differences(ci, co, k, s, g):
+    """d<dK, layer_kernel(mats)>/d(mats) by central finite differences (BCOP chain with its projectors
+    P = U U^T, RKO reshape, AOC block convolution, slicing, groups), and the block-conv adjoint identity."""
+    L = O.Layer(ci, co, k, s, 1, g)
+    specs = O.layer_matrices(L)
+    mats = [[rs.standard_normal((M.m, M.n)) for M in specs] for _ in range(g)]
+    K = O.layer_kernel(L, mats)
+    dK = rs.standard_normal(K.shape)
+    grads = O.layer_kernel_vjp(L, mats, dK)
+    eps = 1e-6
+    for gi in range(g):
+        for j in range(len(specs)):
+            D = rs.standard_normal(mats[gi][j].shape)
+            plus = [list(m) for m in mats]; minus = [list(m) for m in mats]
+            plus[gi][j] = mats[gi][j] + eps * D
+            minus[gi][j] = mats[gi][j] - eps * D
+            fd = ((dK * O.layer_kernel(L, plus)).sum() - (dK * O.layer_kernel(L, minus)).sum()) / (2 * eps)
+            assert abs(fd - (grads[gi][j] * D).sum()) < 1e-6 * max(1.0, abs(fd)), (gi, j)
+    K1, K2 = rs.standard_normal((3, 4, 2, 3)), rs.standard_normal((4, 5, 3, 2))
+    dKk = rs.standard_normal((3, 5, 4, 4))
+    d1, d2 = O.block_conv_vjp(K1, K2, dKk)
+    E1, E2 = rs.standard_normal(K1.shape), rs.standard_normal(K2.shape)
+    lin = (dKk * (O.block_conv(E1, K2) + O.block_conv(K1, E2))).sum()
+    assert abs(lin - (d1 * E1).sum() - (d2 * E2).sum()) < 1e-10 * max(1.0, abs(lin))

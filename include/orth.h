@@ -271,6 +271,21 @@ orth_status_t orth_kernels_assemble(orth_plan_t plan, const float* gathered_f32,
  * first device-side error since the last check (or a pending CUDA error). */
 orth_status_t orth_plan_check(orth_plan_t plan, void* stream);
 
+/* ---- f1: backward of the path (P:61, P:122 a TRAINING wall time; R31-R33).
+ * Data gradient: orth_conv_transpose (the exact adjoint).  Weight gradient, in the layer's forward-conv view
+ * (y = conv(x, K): x on the large grid (N, H, W, C_i), dy on the output grid (N, H_out, W_out, C_o); for an
+ * ORTH_CONV_TRANSPOSE2D layer, whose forward is the adjoint, x is the gradient of its large output and dy its
+ * small input):  dkernel_f32 = dK, PyTorch layout of the layer's FP32 kernel, defined by the bilinear form
+ * <dy, conv(x, delta K)> = <dK, delta K>.  io = ORTH_BF16: tcgen05 GEMM over the pixels (M = c_out/g,
+ * N = c_in/g) with pixel splits summed in a fixed order through `workspace`
+ * (orth_conv_wgrad_workspace bytes, caller-owned device memory); io = ORTH_F32: FP32 SIMT (workspace unused).
+ * FP32 accumulation, deterministic.  Not for SLL blocks or dense layers. */
+orth_status_t orth_conv_wgrad_workspace(orth_plan_t plan, int32_t layer, int32_t N, int32_t H, int32_t W, int32_t io,
+                                        int64_t* bytes);
+orth_status_t orth_conv_wgrad(orth_plan_t plan, int32_t layer, const void* x, const void* dy, float* dkernel_f32,
+                              int32_t N, int32_t H, int32_t W, int32_t io, void* workspace, int64_t workspace_bytes,
+                              void* stream);
+
 /* ---- f2: GPU spectral certification (App. C "scalable spectral norm
  * estimation ... check that the produced bounds are valid").
  * For layer `layer`'s FP32 kernel (PyTorch layout, as orth_compose_kernel writes it) and the circular
@@ -307,7 +322,10 @@ typedef enum {
   ORTH_TK_CONV_FWD = 7,     /* one orth_conv_forward (variant = orth_conv_variant_t) */
   ORTH_TK_CONV_ADJ = 8,     /* one orth_conv_transpose */
   ORTH_TK_ASSEMBLE = 9,     /* orth_kernels_assemble */
-  ORTH_TK_CERTIFY = 10      /* orth_certify */
+  ORTH_TK_CERTIFY = 10,     /* orth_certify */
+  ORTH_TK_WGRAD = 11,       /* orth_conv_wgrad */
+  ORTH_TK_COMPOSE_VJP = 12, /* orth_compose_vjp */
+  ORTH_TK_NS_VJP = 13       /* orth_orthogonalize_vjp */
 } orth_trace_kind_t;
 typedef enum {             /* which conv kernel a conv call ran */
   ORTH_CV_NONE = 0, ORTH_CV_SIMT = 1, ORTH_CV_SMALLK = 2, ORTH_CV_STEM = 3,

@@ -43,7 +43,7 @@ _MODE = {"zeros": PAD_ZEROS, "circular": PAD_CIRCULAR}
 
 
 TRACE_KINDS = {1: "power", 2: "scale", 3: "ns", 4: "ns_check", 5: "compose", 6: "emit", 7: "conv_fwd",
-               8: "conv_adj", 9: "assemble", 10: "certify"}
+               8: "conv_adj", 9: "assemble", 10: "certify", 11: "wgrad", 12: "compose_vjp", 13: "ns_vjp"}
 CONV_VARIANTS = {0: "none", 1: "conv_fwd_simt/conv_bwd_simt", 2: "conv_fwd_smallk", 3: "conv_stem_tc",
                  4: "conv_pad<64,swapped>", 5: "conv_pad<BN>", 6: "conv_stack (+pad_kernel)", 7: "conv_tma",
                  8: "conv_ws<256>", 9: "conv_ws<128>", 10: "conv_ws<64>", 11: "conv_ws<32>", 12: "conv_pair"}
@@ -79,6 +79,10 @@ _sig = {
     "orth_conv_transpose": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
     "orth_kernels_assemble": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "orth_plan_check": (C.c_int, [_P, _P]),
+    "orth_conv_wgrad_workspace": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                            C.POINTER(C.c_int64)]),
+    "orth_conv_wgrad": (C.c_int, [_P, C.c_int32, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64,
+                                  _P]),
     "orth_certify_workspace": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
     "orth_certify": (C.c_int, [_P, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64, _P, _P]),
     "orth_plan_trace": (C.c_int, [_P, C.c_int32]),
@@ -202,6 +206,19 @@ def orth_conv_transpose(h: int, layer: int, kernel, y_small, x_big, N: int, H_bi
 def orth_kernels_assemble(h: int, gathered_f32, kernels_f32, gathered_bf16=None, kernels_bf16=None, stream=None):
     _check(_lib.orth_kernels_assemble(h, _ptr(gathered_f32), _ptr(kernels_f32), _ptr(gathered_bf16),
                                       _ptr(kernels_bf16), _stream(stream)), "orth_kernels_assemble")
+
+
+def orth_conv_wgrad_workspace(h: int, layer: int, N: int, H: int, W: int, io: int) -> int:
+    out = C.c_int64()
+    _check(_lib.orth_conv_wgrad_workspace(h, layer, N, H, W, io, C.byref(out)), "orth_conv_wgrad_workspace")
+    return out.value
+
+
+def orth_conv_wgrad(h: int, layer: int, x, dy, dkernel, N: int, H: int, W: int, io: int, workspace=None,
+                    stream=None):
+    nb = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    _check(_lib.orth_conv_wgrad(h, layer, _ptr(x), _ptr(dy), _ptr(dkernel), N, H, W, io, _ptr(workspace), nb,
+                                _stream(stream)), "orth_conv_wgrad")
 
 
 def orth_certify_workspace(h: int, layer: int, H: int, W: int) -> int:
@@ -356,6 +373,17 @@ class Plan:
 
     def check(self, stream=None):
         orth_plan_check(self.h, stream)
+
+    def conv_wgrad(self, l: int, x, dy, dkernel, workspace=None, stream=None):
+        """f1: dK (FP32 PyTorch layout, preallocated) of layer l's forward-conv view from x (large grid, NHWC)
+        and dy (output grid); the split workspace is allocated here if not given (caller-owned memory)."""
+        import torch
+        io = BF16 if str(x.dtype) == "torch.bfloat16" else F32
+        N, H, W, _ = x.shape
+        nb = orth_conv_wgrad_workspace(self.h, l, N, H, W, io)
+        if workspace is None and nb > 0:
+            workspace = torch.empty(nb, dtype=torch.uint8, device=x.device)
+        orth_conv_wgrad(self.h, l, x, dy, dkernel, N, H, W, io, workspace, stream)
 
     def certify(self, l: int, kernel_f32, H: int, W: int, power_iters: int = 30, workspace=None, stream=None):
         """f2: per (group, frequency) [|E|_F, power estimate of |E|_2] (FP64 tensor on the kernel's device),

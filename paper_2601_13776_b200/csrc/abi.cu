@@ -333,6 +333,36 @@ orth_status_t orth_kernels_assemble(orth_plan_t plan, const float* gathered_f32,
   return cuda_fail(e, "orth_kernels_assemble");
 }
 
+orth_status_t orth_conv_wgrad_workspace(orth_plan_t plan, int32_t layer, int32_t N, int32_t H, int32_t W, int32_t io,
+                                        int64_t* bytes) {
+  if (!plan || !bytes) { set_error("NULL plan or bytes"); return ORTH_ERR_INVALID_ARGUMENT; }
+  Plan& P = plan->p;
+  if (layer < 0 || layer >= (int)P.layers.size()) { set_error("layer %d out of range", layer); return ORTH_ERR_INVALID_ARGUMENT; }
+  const LayerInfo& L = P.layers[layer];
+  if (N < 1 || H < 1 || W < 1) { set_error("N, H, W must be >= 1"); return ORTH_ERR_SHAPE_MISMATCH; }
+  const int Ho = out_dim(H, L.k, L.s, L.d, L.pt, L.pb), Wo = out_dim(W, L.k, L.s, L.d, L.pl, L.pr);
+  *bytes = wgrad_workspace_bytes(L, N, Ho, Wo, io);
+  return ORTH_OK;
+}
+
+orth_status_t orth_conv_wgrad(orth_plan_t plan, int32_t layer, const void* x, const void* dy, float* dkernel_f32,
+                              int32_t N, int32_t H, int32_t W, int32_t io, void* workspace, int64_t workspace_bytes,
+                              void* stream) {
+  orth_status_t st = need_device(plan);
+  if (st != ORTH_OK) return st;
+  Plan& P = plan->p;
+  int Ho = 0, Wo = 0;
+  st = check_conv(P, layer, dkernel_f32, x, const_cast<void*>(dy), N, H, W, io, Ho, Wo);
+  if (st != ORTH_OK) return st;
+  const LayerInfo& L = P.layers[layer];
+  if (L.cons == CONS_SLL_BLOCK) { set_error("SLL blocks have no single weight gradient"); return ORTH_ERR_UNSUPPORTED_CONFIG; }
+  NvtxRange nv("orth_conv_wgrad");
+  Trace tr(P, ORTH_TK_WGRAD, layer, stream);
+  const int e = launch_wgrad(L, x, dy, dkernel_f32, N, H, W, Ho, Wo, io, workspace, workspace_bytes, stream);
+  P.launches += 2;
+  return cuda_fail(e, "orth_conv_wgrad");
+}
+
 orth_status_t orth_certify_workspace(orth_plan_t plan, int32_t layer, int32_t H, int32_t W, int64_t* bytes) {
   if (!plan || !bytes) { set_error("NULL plan or bytes"); return ORTH_ERR_INVALID_ARGUMENT; }
   Plan& P = plan->p;

@@ -392,6 +392,10 @@ int launch_blk_merge(Plan& p, void* stream);                 // M = [A | -2 B]
 int launch_emit_list(Plan& p, const std::vector<EmitItem>& items, const EmitItem* d_items,
                      const float* const bufs[BUF_COUNT], float* kf32, uint16_t* kbf16, void* stream);
 int launch_relu_concat(const void* x, const void* h, void* z, int64_t pixels, int c, int cs, int io, void* stream);
+// f1 (wgrad.cu): conv weight gradient; workspace bytes for the split partials (0: none needed)
+int64_t wgrad_workspace_bytes(const LayerInfo& L, int N, int Ho, int Wo, int io);
+int launch_wgrad(const LayerInfo& L, const void* x, const void* dy, float* dK, int N, int H, int W, int Ho, int Wo,
+                 int io, void* ws, int64_t ws_bytes, void* stream);
 // a8: copy every unit from the gather layout to the final layout
 int launch_assemble(Plan& p, const float* gf, float* kf, const uint16_t* gb, uint16_t* kb, void* stream);
 // per-layer conv scratch (bytes) for calls up to N x Hbig x Wbig (forward-conv input grid), both

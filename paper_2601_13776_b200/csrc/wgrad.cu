@@ -1,0 +1,281 @@
+// f1: weight gradient of the conv apply (a6), the
+// contraction behind P:122's training wall time: for every group g and tap
+// t = (a, b)
+//   dK[g co + o, i, a, b] = sum_{pixels p} dy[p, g co + o] x~[pix(p, t), g ci + i]
+// a GEMM with M = c_out/g, N = c_in/g and K = the N Ho Wo output pixels.
+//
+// wgrad_tc<BN>: one CTA per (pixel split, group, tap, 128-row M tile, BN-wide
+// N tile).  4 producer warps gather 64 pixels per stage with 16-byte
+// cp.async: the dy rows (128 channels) and the tap-shifted x rows (BN
+// channels; zero fill outside the image or circular wrap) land as MN-MAJOR
+// SWIZZLE_128B tiles -- a pixel's channels are contiguous in NHWC, exactly the
+// MN-major atom (64 MN elements x 8 K rows) -- so no transpose is needed.  One
+// thread issues tcgen05.mma M=128 N=BN K=16 (MN-major A and B) into TMEM; the
+// epilogue writes the FP32 tile as this split's partial.  wgrad_reduce sums the
+// splits in a fixed order into the PyTorch-layout FP32 dK (deterministic, no
+// atomics).  wgrad_simt: FP32 I/O (and BF16 shapes the 16-byte gather cannot
+// take), one thread per dK element, fixed pixel order.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "orth_internal.h"
+#include "umma.cuh"
+
+namespace orth {
+namespace {
+
+struct WgArgs {
+  int N, H, W, Ho, Wo;
+  int Ci, Co;              // channels of an x row / a dy row (forward view)
+  int ci, co, g, k, s, d, pt, pl, circ;
+  int64_t pixels;          // N Ho Wo
+  int splits, tiles_m, tiles_n, kk;
+  int64_t per_split;       // pixels per split (multiple of 64)
+};
+
+constexpr int kStages = 4;
+constexpr int kProd = 128;   // 4 producer / epilogue warps
+
+__device__ __forceinline__ int64_t in_pixel(const WgArgs& a, int64_t p, int ta, int tb) {
+  const int64_t hw = (int64_t)a.Ho * a.Wo;
+  const int64_t n = p / hw;
+  const int r = (int)(p - n * hw);
+  const int u = r / a.Wo, v = r - u * a.Wo;
+  int h = a.s * u + a.d * ta - a.pt, w = a.s * v + a.d * tb - a.pl;
+  if (a.circ) {
+    h %= a.H; if (h < 0) h += a.H;
+    w %= a.W; if (w < 0) w += a.W;
+  } else if (h < 0 || h >= a.H || w < 0 || w >= a.W) {
+    return -1;
+  }
+  return (n * a.H + h) * a.W + w;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kProd + 32, 1)
+    wgrad_tc(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy, WgArgs a,
+             float* __restrict__ part) {
+  constexpr int A_BYTES = 2 * 8192, B_BYTES = (BN / 64) * 8192, STAGE = A_BYTES + B_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = umma::align1024_smem(smem_raw);
+  __shared__ uint64_t full_bar[kStages], empty_bar[kStages], done_bar;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int64_t tbl[kStages][64];
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  // tile decode: split slowest, then group, tap, M tile, N tile
+  int64_t idx = blockIdx.x;
+  const int nb = (int)(idx % a.tiles_n); idx /= a.tiles_n;
+  const int mb = (int)(idx % a.tiles_m); idx /= a.tiles_m;
+  const int t = (int)(idx % a.kk); idx /= a.kk;
+  const int grp = (int)(idx % a.g); idx /= a.g;
+  const int split = (int)idx;
+  const int ta = t / a.k, tb = t - ta * a.k;
+  const int m0 = mb * 128, n0 = nb * BN;
+  const int64_t p_begin = (int64_t)split * a.per_split;
+  const int64_t p_end = std::min<int64_t>(a.pixels, p_begin + a.per_split);
+  const int nk = (int)((p_end - p_begin + 63) / 64);
+
+  if (warp == 4) umma::tmem_alloc(&tmem_base_sh, BN);
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      umma::mbar_init(&full_bar[i], kProd);
+      umma::mbar_init(&empty_bar[i], 1);
+    }
+    umma::mbar_init(&done_bar, 1);
+    umma::fence_mbar_init();
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t s0 = umma::smem_u32(smem);
+
+  if (warp < 4) {
+    // ---------------- producers: 64 pixels per stage
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % kStages;
+      if (kb >= kStages) umma::mbar_wait(&empty_bar[st], ((kb / kStages) - 1) & 1);
+      const int64_t pb = p_begin + (int64_t)kb * 64;
+      if (tid < 64) {
+        const int64_t p = pb + tid;
+        tbl[st][tid] = p < p_end ? in_pixel(a, p, ta, tb) : -1;
+      }
+      umma::named_bar_sync(1, kProd);
+      const uint32_t sa = s0 + st * STAGE, sb = sa + A_BYTES;
+      // A: dy rows, 16 chunks of 8 channels (128 o) per pixel
+      for (int q = tid; q < 64 * 16; q += kProd) {
+        const int r = q >> 4, j = q & 15;
+        const int64_t p = pb + r;
+        const int o = m0 + 8 * j;
+        const bool ok = p < p_end && o < a.co;
+        const __nv_bfloat16* src = dy + (ok ? (p * a.Co + (int64_t)grp * a.co + o) : 0);
+        const uint32_t dst = sa + (j >> 3) * 8192 + r * 128 + (((j & 7) ^ (r & 7)) << 4);
+        umma::cp_async16(dst, src, ok);
+      }
+      // B: x rows of the tap-shifted input pixels, BN/8 chunks per pixel
+      for (int q = tid; q < 64 * (BN / 8); q += kProd) {
+        const int r = q / (BN / 8), j = q - r * (BN / 8);
+        const int64_t ip = tbl[st][r];
+        const int i = n0 + 8 * j;
+        const bool ok = ip >= 0 && i < a.ci;
+        const __nv_bfloat16* src = x + (ok ? (ip * a.Ci + (int64_t)grp * a.ci + i) : 0);
+        const uint32_t dst = sb + (j >> 3) * 8192 + r * 128 + (((j & 7) ^ (r & 7)) << 4);
+        umma::cp_async16(dst, src, ok);
+      }
+      umma::cp_async_mbar_arrive(&full_bar[st]);
+    }
+    // ---------------- epilogue: TMEM -> this split's FP32 partial tile [o][i]
+    umma::mbar_wait(&done_bar, 0);
+    umma::tc_fence_after();
+    const int o = m0 + warp * 32 + (tid & 31);
+    float* dst = part + (((int64_t)split * a.g + grp) * a.kk + t) * ((int64_t)a.co * a.ci);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      umma::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+      if (o < a.co) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int i = n0 + c0 + j;
+          if (i < a.ci) dst[(int64_t)o * a.ci + i] = v[j];
+        }
+      }
+    }
+  } else if (tid == kProd) {
+    // ---------------- MMA issuer
+    constexpr uint32_t IDESC = umma::idesc_bf16(128, BN) | (1u << 15) | (1u << 16);   // A, B MN-major
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % kStages;
+      umma::mbar_wait(&full_bar[st], (kb / kStages) & 1);
+      umma::fence_proxy_async_smem();   // cp.async (generic proxy) rows -> tcgen05.mma (async proxy)
+      umma::tc_fence_after();
+      const uint32_t sa = s0 + st * STAGE, sb = sa + A_BYTES;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        umma::mma_bf16(tmem, umma::sdesc_sw128_mn(sa + 2048 * q, 8192), umma::sdesc_sw128_mn(sb + 2048 * q, 8192),
+                       IDESC, (kb | q) != 0);
+      umma::mma_commit(&empty_bar[st]);
+    }
+    umma::mma_commit(&done_bar);
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 4) umma::tmem_dealloc(tmem, BN);
+}
+
+// dK[(g co + o) ci k^2 + i k^2 + t] = sum over splits (in order) of part[split][g][t][o][i]
+__global__ void __launch_bounds__(256) wgrad_reduce(const float* __restrict__ part, WgArgs a, float* __restrict__ dK) {
+  const int64_t total = (int64_t)a.g * a.co * a.ci * a.kk;
+  const int64_t slab = (int64_t)a.g * a.kk * a.co * a.ci;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(e % a.kk);
+    int64_t r = e / a.kk;
+    const int i = (int)(r % a.ci); r /= a.ci;
+    const int o = (int)(r % a.co);
+    const int grp = (int)(r / a.co);
+    const int64_t src = (((int64_t)grp * a.kk + t) * a.co + o) * a.ci + i;
+    float acc = 0.f;
+    for (int sp = 0; sp < a.splits; ++sp) acc += part[sp * slab + src];
+    dK[e] = acc;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) wgrad_simt(const T* __restrict__ x, const T* __restrict__ dy, WgArgs a,
+                                                  float* __restrict__ dK) {
+  const int64_t total = (int64_t)a.g * a.co * a.ci * a.kk;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(e % a.kk);
+    int64_t r = e / a.kk;
+    const int i = (int)(r % a.ci); r /= a.ci;
+    const int o = (int)(r % a.co);
+    const int grp = (int)(r / a.co);
+    const int ta = t / a.k, tb = t - ta * a.k;
+    float acc = 0.f;
+    for (int64_t p = 0; p < a.pixels; ++p) {
+      const int64_t ip = in_pixel(a, p, ta, tb);
+      if (ip < 0) continue;
+      acc = fmaf((float)dy[p * a.Co + (int64_t)grp * a.co + o], (float)x[ip * a.Ci + (int64_t)grp * a.ci + i], acc);
+    }
+    dK[e] = acc;
+  }
+}
+
+WgArgs make_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo) {
+  WgArgs a{};
+  a.N = N; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo;
+  a.Ci = L.ci_f; a.Co = L.co_f; a.ci = L.ci; a.co = L.co; a.g = L.g;
+  a.k = L.k; a.s = L.s; a.d = L.d; a.pt = L.pt; a.pl = L.pl;
+  a.circ = L.desc.padding_mode == ORTH_PAD_CIRCULAR;
+  a.pixels = (int64_t)N * Ho * Wo;
+  a.kk = L.k * L.k;
+  return a;
+}
+
+bool tc_ok(const LayerInfo& L) { return L.ci % 8 == 0 && L.co % 8 == 0 && L.ci_f % 8 == 0 && L.co_f % 8 == 0; }
+
+int pick_bn(const LayerInfo& L) { return L.ci > 128 ? 256 : L.ci > 64 ? 128 : 64; }
+
+int wgrad_splits(const LayerInfo& L, int64_t pixels) {
+  const int64_t base = (int64_t)L.g * L.k * L.k * ((L.co + 127) / 128) * ((L.ci + pick_bn(L) - 1) / pick_bn(L));
+  int64_t sp = std::max<int64_t>(1, (2 * 148 + base - 1) / base);        // ~2 waves of CTAs
+  sp = std::min<int64_t>(sp, std::max<int64_t>(1, pixels / 256));       // >= 256 pixels per split
+  return (int)std::min<int64_t>(sp, 64);
+}
+
+template <int BN>
+int launch_tc(const __nv_bfloat16* x, const __nv_bfloat16* dy, const WgArgs& a, float* part, cudaStream_t s) {
+  constexpr size_t STAGE = 2 * 8192 + (BN / 64) * 8192;
+  const size_t smem = 1024 + kStages * STAGE;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(wgrad_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int64_t tiles = (int64_t)a.splits * a.g * a.kk * a.tiles_m * a.tiles_n;
+  wgrad_tc<BN><<<(unsigned)tiles, kProd + 32, smem, s>>>(x, dy, a, part);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int64_t wgrad_workspace_bytes(const LayerInfo& L, int N, int Ho, int Wo, int io) {
+  if (io != ORTH_BF16 || !tc_ok(L)) return 0;
+  return (int64_t)wgrad_splits(L, (int64_t)N * Ho * Wo) * L.kernel_numel * 4;
+}
+
+int launch_wgrad(const LayerInfo& L, const void* x, const void* dy, float* dK, int N, int H, int W, int Ho, int Wo,
+                 int io, void* ws, int64_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  WgArgs a = make_args(L, N, H, W, Ho, Wo);
+  const int64_t total = (int64_t)L.g * L.co * L.ci * a.kk;
+  const int rb = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  if (io == ORTH_BF16 && tc_ok(L) && ws && ws_bytes >= wgrad_workspace_bytes(L, N, Ho, Wo, io)) {
+    a.splits = wgrad_splits(L, a.pixels);
+    a.per_split = ((a.pixels + a.splits - 1) / a.splits + 63) / 64 * 64;
+    a.splits = (int)((a.pixels + a.per_split - 1) / a.per_split);
+    const int bn = pick_bn(L);
+    a.tiles_m = (L.co + 127) / 128;
+    a.tiles_n = (L.ci + bn - 1) / bn;
+    g_conv_variant = 0;
+    float* part = static_cast<float*>(ws);
+    int e = bn == 256 ? launch_tc<256>((const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, a, part, s)
+            : bn == 128 ? launch_tc<128>((const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, a, part, s)
+                        : launch_tc<64>((const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, a, part, s);
+    if (e) return e;
+    wgrad_reduce<<<rb, 256, 0, s>>>(part, a, dK);
+    return (int)cudaGetLastError();
+  }
+  g_conv_variant = ORTH_CV_SIMT;
+  if (io == ORTH_BF16)
+    wgrad_simt<__nv_bfloat16><<<rb, 256, 0, s>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, a, dK);
+  else
+    wgrad_simt<float><<<rb, 256, 0, s>>>((const float*)x, (const float*)dy, a, dK);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace orth

@@ -142,6 +142,8 @@ typedef struct {
                             r = |I - X_{T-1}^T X_{T-1}|_F from the last iteration's own Gram (R20);
                             default 1e-3 (north star max|sigma - 1|); <= 0: non-finite check only */
   int32_t max_batch;     /* largest N of any conv call (sizes the per-layer scratch); default 0 */
+  int32_t vjp;           /* 1: allocate the backward workspace (T x params floats for the NS iterates + the
+                            composition chain's per-step buffers) for orth_compose_vjp / orth_orthogonalize_vjp */
 } orth_opts_t;
 
 /* Fill *opts with the defaults above. */
@@ -285,6 +287,24 @@ orth_status_t orth_conv_wgrad_workspace(orth_plan_t plan, int32_t layer, int32_t
 orth_status_t orth_conv_wgrad(orth_plan_t plan, int32_t layer, const void* x, const void* dy, float* dkernel_f32,
                               int32_t N, int32_t H, int32_t W, int32_t io, void* workspace, int64_t workspace_bytes,
                               void* stream);
+
+/* Composition VJP: d(ortho) of this rank's units from dkernels_f32, the gradient of the FP32 kernels in the
+ * FINAL layout (all layers; with world > 1 the data-parallel gradient is all-reduced first).  ortho: the
+ * matrices the kernels were composed from.  Writes every owned unit's matrices in d_ortho (packed like
+ * ortho); other entries untouched.  Recomputes the chain's intermediates (R32), then runs the adjoint of
+ * each step: slice -> zero padding, AOC block convolution (dR, dK_BCOP), BCOP steps K' = K_cur P + K_prev
+ * (I - P) -> (dK, dP), P = U U^T -> dU = (dP + dP^T) U, RKO reshape -> reshape.  Needs opts.vjp; AOC /
+ * BCOP / RKO / dense layers only (SOC / SLL / blocks: ORTH_ERR_UNSUPPORTED_CONFIG). */
+orth_status_t orth_compose_vjp(orth_plan_t plan, const float* ortho, const float* dkernels_f32, float* d_ortho,
+                               void* stream);
+/* Orthogonalisation VJP: d_params of this rank's matrices from d_ortho.  The pre-scale sigma is a constant
+ * (R31: the value the LAST orth_orthogonalize of this plan computed -- call it on the same params first);
+ * the T iterates X_t = NS^t(W / sigma) are recomputed FP32-accurately (FP32 SIMT, or 3-pass tcgen05 in the
+ * BF16 modes: the adjoint of the FP32 iteration, R32) and the adjoint step
+ * G <- G + b (G R + X S'), R = I - X^T X, S' = -(X^T G + G^T X) (tall; the mirrored form for wide) runs
+ * T times; d_params = G_0 / sigma.  Needs opts.vjp. */
+orth_status_t orth_orthogonalize_vjp(orth_plan_t plan, const float* params, const float* d_ortho, float* d_params,
+                                     void* stream);
 
 /* ---- f2: GPU spectral certification (App. C "scalable spectral norm
  * estimation ... check that the produced bounds are valid").

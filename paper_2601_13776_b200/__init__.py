@@ -63,7 +63,7 @@ class LayerDesc(C.Structure):
 class Opts(C.Structure):
     _fields_ = [("ns_iters", C.c_int32), ("beta", C.c_float), ("prescale", C.c_int32), ("power_iters", C.c_int32),
                 ("compute", C.c_int32), ("polish_iters", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
-                ("ns_tol", C.c_float), ("max_batch", C.c_int32)]
+                ("ns_tol", C.c_float), ("max_batch", C.c_int32), ("vjp", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -79,6 +79,8 @@ _sig = {
     "orth_conv_transpose": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
     "orth_kernels_assemble": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "orth_plan_check": (C.c_int, [_P, _P]),
+    "orth_compose_vjp": (C.c_int, [_P, _P, _P, _P, _P]),
+    "orth_orthogonalize_vjp": (C.c_int, [_P, _P, _P, _P, _P]),
     "orth_conv_wgrad_workspace": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                             C.POINTER(C.c_int64)]),
     "orth_conv_wgrad": (C.c_int, [_P, C.c_int32, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64,
@@ -206,6 +208,16 @@ def orth_conv_transpose(h: int, layer: int, kernel, y_small, x_big, N: int, H_bi
 def orth_kernels_assemble(h: int, gathered_f32, kernels_f32, gathered_bf16=None, kernels_bf16=None, stream=None):
     _check(_lib.orth_kernels_assemble(h, _ptr(gathered_f32), _ptr(kernels_f32), _ptr(gathered_bf16),
                                       _ptr(kernels_bf16), _stream(stream)), "orth_kernels_assemble")
+
+
+def orth_compose_vjp(h: int, ortho, dkernels_f32, d_ortho, stream=None):
+    _check(_lib.orth_compose_vjp(h, _ptr(ortho), _ptr(dkernels_f32), _ptr(d_ortho), _stream(stream)),
+           "orth_compose_vjp")
+
+
+def orth_orthogonalize_vjp(h: int, params, d_ortho, d_params, stream=None):
+    _check(_lib.orth_orthogonalize_vjp(h, _ptr(params), _ptr(d_ortho), _ptr(d_params), _stream(stream)),
+           "orth_orthogonalize_vjp")
 
 
 def orth_conv_wgrad_workspace(h: int, layer: int, N: int, H: int, W: int, io: int) -> int:
@@ -373,6 +385,12 @@ class Plan:
 
     def check(self, stream=None):
         orth_plan_check(self.h, stream)
+
+    def compose_vjp(self, ortho, dkernels_f32, d_ortho, stream=None):
+        orth_compose_vjp(self.h, ortho, dkernels_f32, d_ortho, stream)
+
+    def orthogonalize_vjp(self, params, d_ortho, d_params, stream=None):
+        orth_orthogonalize_vjp(self.h, params, d_ortho, d_params, stream)
 
     def conv_wgrad(self, l: int, x, dy, dkernel, workspace=None, stream=None):
         """f1: dK (FP32 PyTorch layout, preallocated) of layer l's forward-conv view from x (large grid, NHWC)

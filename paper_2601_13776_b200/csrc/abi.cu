@@ -363,6 +363,70 @@ orth_status_t orth_conv_wgrad(orth_plan_t plan, int32_t layer, const void* x, co
   return cuda_fail(e, "orth_conv_wgrad");
 }
 
+orth_status_t orth_compose_vjp(orth_plan_t plan, const float* ortho, const float* dkernels_f32, float* d_ortho,
+                               void* stream) {
+  orth_status_t st = need_device(plan);
+  if (st != ORTH_OK) return st;
+  Plan& P = plan->p;
+  if (!P.opts.vjp || !P.d_vjp) { set_error("create the plan with opts.vjp = 1"); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (!P.vjp_supported) { set_error("no VJP for SOC / SLL layers or SLL blocks"); return ORTH_ERR_UNSUPPORTED_CONFIG; }
+  if (!ortho || !dkernels_f32 || !d_ortho) { set_error("NULL ortho, dkernels or d_ortho"); return ORTH_ERR_INVALID_ARGUMENT; }
+  NvtxRange nv("orth_compose_vjp");
+  Trace tr(P, ORTH_TK_COMPOSE_VJP, -1, stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  float* bufs[BUF_COUNT] = {const_cast<float*>(ortho), P.d_vjp, d_ortho, P.d_comp};
+  int e = 0;
+  auto gemm = [&](const GemmPhase& ph) {
+    if (!ph.total_tiles || e) return;
+    e = P.opts.compute == ORTH_F32 ? launch_gemm_f32(ph, bufs, stream) : launch_gemm_tc(ph, bufs, 3, stream);
+    P.launches++;
+  };
+  if (P.cv_zero_n > 0)
+    e = (int)cudaMemsetAsync(P.d_vjp + P.cv_zero_off, 0, (size_t)P.cv_zero_n * sizeof(float), s);
+  for (size_t i = 0; i + 2 < P.cv_qcopy.size() && !e; i += 3)
+    e = (int)cudaMemcpyAsync(P.d_vjp + P.cv_qcopy[i + 1], ortho + P.cv_qcopy[i], (size_t)P.cv_qcopy[i + 2] * 4,
+                             cudaMemcpyDeviceToDevice, s);
+  gemm(P.proj);                                  // projectors P = U U^T (into comp, as in the forward)
+  for (auto& ph : P.cv_fwd) gemm(ph);            // chain intermediates, one buffer per step
+  if (!e) e = launch_vjp_deemit(P, dkernels_f32, d_ortho, stream);
+  gemm(P.cv_dr);                                 // AOC: dR_ab
+  if (!e) e = launch_vjp_scatter(P, d_ortho, stream);
+  gemm(P.cv_dkb);                                // AOC: dK_BCOP
+  for (size_t j = 0; j < P.cv_bwd_a.size(); ++j) {
+    gemm(P.cv_bwd_a[j]);
+    gemm(P.cv_bwd_b[j]);
+    gemm(P.cv_bwd_c[j]);
+  }
+  return cuda_fail(e, "orth_compose_vjp");
+}
+
+orth_status_t orth_orthogonalize_vjp(orth_plan_t plan, const float* params, const float* d_ortho, float* d_params,
+                                     void* stream) {
+  orth_status_t st = need_device(plan);
+  if (st != ORTH_OK) return st;
+  Plan& P = plan->p;
+  if (!P.opts.vjp || !P.d_vjp) { set_error("create the plan with opts.vjp = 1"); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (!params || !d_ortho || !d_params) { set_error("NULL params, d_ortho or d_params"); return ORTH_ERR_INVALID_ARGUMENT; }
+  if (P.mat_items.empty()) return ORTH_OK;
+  NvtxRange nv("orth_orthogonalize_vjp");
+  Trace tr(P, ORTH_TK_NS_VJP, -1, stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  float* bufs[BUF_COUNT] = {nullptr, P.d_vjp, nullptr, nullptr};
+  int e = 0;
+  auto gemm = [&](const GemmPhase& ph) {
+    if (!ph.total_tiles || e) return;
+    e = P.opts.compute == ORTH_F32 ? launch_gemm_f32(ph, bufs, stream) : launch_gemm_tc(ph, bufs, 3, stream);
+    P.launches++;
+  };
+  e = launch_scale(P, params, P.d_vjp + P.vj_x_off, stream);   // X_0 = W / sigma (the forward's sigma)
+  for (auto& ph : P.vj_fwd) gemm(ph);                          // X_1 .. X_{T-1}
+  if (!e) e = (int)cudaMemcpyAsync(P.d_vjp + P.vj_g_off[1], d_ortho, (size_t)P.params_numel * 4,
+                                   cudaMemcpyDeviceToDevice, s);
+  for (auto& ph : P.vj_bwd) gemm(ph);
+  if (!e) e = launch_scale(P, P.d_vjp + P.vj_g_off[P.vj_g_final], d_params, stream);   // d_params = G_0 / sigma
+  return cuda_fail(e, "orth_orthogonalize_vjp");
+}
+
 orth_status_t orth_certify_workspace(orth_plan_t plan, int32_t layer, int32_t H, int32_t W, int64_t* bytes) {
   if (!plan || !bytes) { set_error("NULL plan or bytes"); return ORTH_ERR_INVALID_ARGUMENT; }
   Plan& P = plan->p;

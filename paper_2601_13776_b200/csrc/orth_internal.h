@@ -205,6 +205,20 @@ struct BlkItem {
   int64_t a_off, b_off, m_off, c_off;   // A, B, M, C (tap-major) in comp
 };
 
+// f1 (vjp.cu): per-unit gradient moves of the composition VJP
+struct VjpItem {
+  int32_t mode;           // 0 chain unit: dS_last[t][o][i] = (i < ci) dK[o][i][t] (rows x c); 1 AOC: dFin[t][o][i];
+                          // 2 copy (RKO / dense: d_ortho slab = dK slab); 3 BCOP k' = 1: dQ[:co, :ci] = dK
+  int32_t co, ci, kk, rows, c, pad_[2];
+  int64_t src_off;        // dK (final FP32 layout) of the unit
+  int64_t dst_off;        // mode 0/1: VJP arena; mode 2/3: d_ortho
+  int64_t zero_off, zero_n;   // d_ortho region zeroed first (dQ of chain units), -1 none
+};
+struct ScatterItem {      // AOC dR: dR[o][j s^2 + t] = dRab[t][o][j]
+  int32_t co, cm, ss, pad_;
+  int64_t src_off, dst_off;   // arena, d_ortho
+};
+
 struct TcComposePlan;   // tensor-core composition (compose_tc.cu)
 }  // namespace orth
 struct orth_trace_state;   // abi.cu (orth_plan_trace)
@@ -291,6 +305,23 @@ struct Plan {
   GemmPhase blk_mm;                 // C, A, B of every block (read the emitted FP32 kernels: BUF_Y)
   std::vector<LayerInfo> blk_conv;  // conv views of every block: [C, M] per block
   std::vector<EmitItem> emit2;      // the blocks' C and M (after the first emit)
+  // f1 VJP (opts.vjp != 0): arena, NS iterate storage, composition VJP phases
+  float* d_vjp = nullptr;
+  int64_t vjp_numel = 0;
+  int64_t vj_x_off = 0, vj_g_off[2] = {0, 0}, vj_r_off = 0, vj_s_off = 0;
+  std::vector<GemmPhase> vj_fwd;    // per t: [2t] R_t = I - Gram(X_t), [2t+1] X_{t+1} = X_t + b (X_t R_t | R_t X_t)
+  std::vector<GemmPhase> vj_bwd;    // per t (reverse): [2j] {R_t, S'_t}, [2j+1] G_t from G_{t+1}
+  int32_t vj_g_final = 0;           // 0/1: which G slot holds G_0 (-1: d_ortho itself when T == 0)
+  std::vector<GemmPhase> cv_fwd;    // chain steps into per-step buffers
+  GemmPhase cv_dr, cv_dkb;          // AOC: dR_ab, dKb
+  std::vector<GemmPhase> cv_bwd_a, cv_bwd_b, cv_bwd_c;   // per backward iteration: {dP, dK_in}, {dP U}, {+dP^T U}
+  std::vector<int64_t> cv_qcopy;    // (ortho off, arena off, floats) triples: Q rows copied into the arena
+  int64_t cv_zero_off = 0, cv_zero_n = 0;
+  std::vector<VjpItem> cv_items;
+  std::vector<ScatterItem> cv_scatter;
+  VjpItem* d_cv_items = nullptr;
+  ScatterItem* d_cv_scatter = nullptr;
+  bool vjp_supported = true;        // false if an owned unit is SOC / SLL / block (no VJP)
   SllItem* d_sll = nullptr;
   BlkItem* d_blk = nullptr;
   EmitItem* d_emit2 = nullptr;
@@ -396,6 +427,9 @@ int launch_relu_concat(const void* x, const void* h, void* z, int64_t pixels, in
 int64_t wgrad_workspace_bytes(const LayerInfo& L, int N, int Ho, int Wo, int io);
 int launch_wgrad(const LayerInfo& L, const void* x, const void* dy, float* dK, int N, int H, int W, int Ho, int Wo,
                  int io, void* ws, int64_t ws_bytes, void* stream);
+// f1 (vjp.cu)
+int launch_vjp_deemit(Plan& p, const float* dK, float* dortho, void* stream);
+int launch_vjp_scatter(Plan& p, float* dortho, void* stream);
 // a8: copy every unit from the gather layout to the final layout
 int launch_assemble(Plan& p, const float* gf, float* kf, const uint16_t* gb, uint16_t* kb, void* stream);
 // per-layer conv scratch (bytes) for calls up to N x Hbig x Wbig (forward-conv input grid), both

@@ -783,6 +783,325 @@ static void build_compose(Plan& P) {
   P.proj_off = proj_off;
 }
 
+
+// ---------------------------------------------------------------------------------------------------
+// f1: VJP phases (opts.vjp != 0).  Buffers of every VJP GEMM: BUF_X = ortho (compose VJP), BUF_Y = the VJP
+// arena, BUF_G = d_ortho (compose VJP output), BUF_W = comp (projectors).  The NS VJP reads G_T from a copy
+// of d_ortho in the arena, so all its operands share BUF_Y.
+// ---------------------------------------------------------------------------------------------------
+static void build_vjp(Plan& P) {
+  const float b = P.opts.beta;
+  const int T = P.opts.ns_iters;
+  int64_t w = 0;
+  auto take = [&](int64_t n) { int64_t o = w; w += pad_up(std::max<int64_t>(n, 1), kPadF32); return o; };
+  // ---- NS: X_t slots, two G slots, R / S (short-side squares)
+  const int64_t PN = P.params_numel;
+  P.vj_x_off = take((int64_t)T * PN);
+  P.vj_g_off[0] = take(PN);
+  P.vj_g_off[1] = take(PN);
+  P.vj_r_off = take(P.gram_numel);
+  P.vj_s_off = take(P.gram_numel);
+  P.vj_fwd.assign(2 * T, GemmPhase{});
+  P.vj_bwd.assign(2 * T, GemmPhase{});
+  auto gram_desc = [&](const MatInfo& M, int64_t x, int64_t r) {   // R = I - X^T X | I - X X^T
+    const int m = (int)M.m, n = (int)M.n;
+    const bool tall = m >= n;
+    const int sh = tall ? n : m;
+    GemmDesc d = mk(sh, sh, tall ? m : n);
+    d.a_buf = d.b_buf = d.d_buf = BUF_Y;
+    if (tall) { d.sa_m = 1; d.sa_k = n; d.sb_k = n; d.sb_n = 1; }
+    else { d.sa_m = n; d.sa_k = 1; d.sb_k = 1; d.sb_n = n; }
+    d.d_off = r; d.ldd = sh;
+    d.alpha = -1.0f; d.diag = 1.0f;
+    return d;
+  };
+  for (int t = 0; t < T; ++t) {
+    GemmPhase& g = P.vj_fwd[2 * t];
+    GemmPhase& u = P.vj_fwd[2 * t + 1];
+    const int64_t xt = P.vj_x_off + (int64_t)t * PN;
+    for (int i : P.owned_mats) {
+      const MatInfo& M = P.mats[i];
+      const int m = (int)M.m, n = (int)M.n;
+      const bool tall = m >= n;
+      const int sh = tall ? n : m;
+      GemmDesc d = gram_desc(M, xt + M.off, P.vj_r_off + M.gram_off);
+      add_seg(g, d, xt + M.off, -1, xt + M.off);
+      g.descs.push_back(d);
+      if (t + 1 < T) {   // X_{t+1} = X_t + b (X_t R | R X_t) into slot t + 1 (X_T itself is not needed)
+        GemmDesc e = mk(m, n, sh);
+        e.a_buf = e.b_buf = e.c_buf = e.d_buf = BUF_Y;
+        e.sa_m = tall ? n : sh; e.sa_k = 1; e.sb_k = n; e.sb_n = 1;
+        if (tall) add_seg(u, e, xt + M.off, -1, P.vj_r_off + M.gram_off);
+        else add_seg(u, e, P.vj_r_off + M.gram_off, -1, xt + M.off);
+        e.c_off = xt + M.off; e.ldc = n; e.d_off = xt + PN + M.off; e.ldd = n;
+        e.alpha = b; e.beta = 1.0f;
+        u.descs.push_back(e);
+      }
+    }
+    finish_phase(g);
+    finish_phase(u);
+  }
+  // backward: iteration j handles t = T-1-j; G_in = slot[(j+1)&1] (slot 1 holds the copy of G_T), G_out =
+  // slot[j&1].  Tall: S' = -(X^T G + G^T X), G' = G + b (G R + X S').  Wide: S' = -(G X^T + X G^T),
+  // G' = G + b (R G + S' X).  (The adjoint of X' = X + b X (I - X^T X).)
+  for (int j = 0; j < T; ++j) {
+    const int t = T - 1 - j;
+    const int64_t xt = P.vj_x_off + (int64_t)t * PN;
+    const int64_t gin = P.vj_g_off[(j + 1) & 1], gout = P.vj_g_off[j & 1];
+    GemmPhase& a = P.vj_bwd[2 * j];
+    GemmPhase& c = P.vj_bwd[2 * j + 1];
+    for (int i : P.owned_mats) {
+      const MatInfo& M = P.mats[i];
+      const int m = (int)M.m, n = (int)M.n;
+      const bool tall = m >= n;
+      const int sh = tall ? n : m;
+      GemmDesc d = gram_desc(M, xt + M.off, P.vj_r_off + M.gram_off);
+      add_seg(a, d, xt + M.off, -1, xt + M.off);
+      a.descs.push_back(d);
+      GemmDesc sd = mk(sh, sh, tall ? m : n);
+      sd.a_buf = sd.b_buf = sd.d_buf = BUF_Y;
+      if (tall) {   // X^T G + G^T X
+        sd.sa_m = 1; sd.sa_k = n; sd.sb_k = n; sd.sb_n = 1;
+        add_seg(a, sd, xt + M.off, -1, gin + M.off);
+        add_seg(a, sd, gin + M.off, -1, xt + M.off);
+      } else {      // G X^T + X G^T
+        sd.sa_m = n; sd.sa_k = 1; sd.sb_k = 1; sd.sb_n = n;
+        add_seg(a, sd, gin + M.off, -1, xt + M.off);
+        add_seg(a, sd, xt + M.off, -1, gin + M.off);
+      }
+      sd.d_off = P.vj_s_off + M.gram_off; sd.ldd = sh; sd.alpha = -1.0f;
+      a.descs.push_back(sd);
+      GemmDesc e = mk(m, n, sh);
+      e.a_buf = e.b_buf = e.c_buf = e.d_buf = BUF_Y;
+      e.c_off = gin + M.off; e.ldc = n; e.beta = 1.0f;
+      e.d_off = gout + M.off; e.ldd = n; e.alpha = b;
+      e.sa_m = tall ? n : sh; e.sa_k = 1; e.sb_k = n; e.sb_n = 1;
+      if (tall) {
+        add_seg(c, e, gin + M.off, -1, P.vj_r_off + M.gram_off);   // G R
+        add_seg(c, e, xt + M.off, -1, P.vj_s_off + M.gram_off);    // X S'
+      } else {
+        add_seg(c, e, P.vj_r_off + M.gram_off, -1, gin + M.off);   // R G
+        add_seg(c, e, P.vj_s_off + M.gram_off, -1, xt + M.off);    // S' X
+      }
+      c.descs.push_back(e);
+    }
+    finish_phase(a);
+    finish_phase(c);
+  }
+  P.vj_g_final = T > 0 ? ((T - 1) & 1) : 1;
+  // ---- composition VJP (owned BCOP / AOC / RKO / dense units)
+  P.cv_fwd.clear(); P.cv_bwd_a.clear(); P.cv_bwd_b.clear(); P.cv_bwd_c.clear();
+  P.cv_dr = GemmPhase{}; P.cv_dkb = GemmPhase{};
+  P.cv_items.clear(); P.cv_scatter.clear(); P.cv_qcopy.clear();
+  P.vjp_supported = true;
+  P.cv_zero_off = w;   // everything taken from here on is zeroed at the start of orth_compose_vjp
+  int64_t max_tap = 64;
+  for (auto& u : P.comp_units) max_tap = std::max<int64_t>(max_tap, (int64_t)u.rows * u.c);
+  const int64_t zero_off = take(max_tap);   // a zero tap for missing chain neighbours
+  int max_steps = 0;
+  struct UnitV { int64_t step_off[64]; int64_t dstep_off[64]; int nsteps; int64_t dfin_off, drab_off, q_off; };
+  std::vector<UnitV> uv(P.comp_units.size());
+  for (size_t ui = 0; ui < P.comp_units.size(); ++ui) {
+    const CompUnit& u = P.comp_units[ui];
+    const LayerInfo& L = P.layers[u.layer];
+    UnitV& V = uv[ui];
+    V.nsteps = 0; V.dfin_off = V.drab_off = V.q_off = -1;
+    if (L.cons == CONS_SOC || L.cons == CONS_SLL || L.cons == CONS_SLL_BLOCK) { P.vjp_supported = false; continue; }
+    if (u.ping >= 0) {
+      V.nsteps = 2 * (L.kp - 1);
+      V.q_off = take((int64_t)u.rows * u.c);
+      int kh = 1, kw = 1;
+      for (int t = 0; t < V.nsteps; ++t) {
+        const bool vert = (t % 2) == 0;
+        const int oh = vert ? kh + 1 : kh, ow = vert ? kw : kw + 1;
+        V.step_off[t] = take((int64_t)oh * ow * u.rows * u.c);
+        V.dstep_off[t] = take((int64_t)oh * ow * u.rows * u.c);
+        kh = oh; kw = ow;
+      }
+      max_steps = std::max(max_steps, V.nsteps);
+    }
+    if (L.cons == CONS_AOC) {
+      V.dfin_off = take((int64_t)L.k * L.k * L.co * L.ci);
+      V.drab_off = take((int64_t)L.s * L.s * L.co * L.c_mid);
+    }
+  }
+  P.cv_fwd.assign(max_steps, GemmPhase{});
+  P.cv_bwd_a.assign(max_steps, GemmPhase{});
+  P.cv_bwd_b.assign(max_steps, GemmPhase{});
+  P.cv_bwd_c.assign(max_steps, GemmPhase{});
+  for (size_t ui = 0; ui < P.comp_units.size(); ++ui) {
+    const CompUnit& u = P.comp_units[ui];
+    const LayerInfo& L = P.layers[u.layer];
+    const UnitV& V = uv[ui];
+    if (L.cons == CONS_SOC || L.cons == CONS_SLL || L.cons == CONS_SLL_BLOCK) continue;
+    const int base = L.first_mat + u.group * L.mats_per_group;
+    const UnitInfo& U = P.units[L.first_unit + u.group];
+    const int r = u.rows, c = u.c;
+    const int64_t tap = (int64_t)r * c;
+    VjpItem it{};
+    it.co = L.co; it.ci = L.ci; it.kk = (L.cons == CONS_DENSE) ? 1 : L.k * L.k;
+    it.src_off = U.fin_f32;   // dK arrives in the final layout (all-reduced across ranks)
+    it.zero_off = -1; it.zero_n = 0;
+    if (L.cons == CONS_DENSE || L.cons == CONS_RKO) {
+      it.mode = 2;
+      it.dst_off = P.mats[base + L.mats_per_group - 1].off;
+      it.rows = L.co; it.c = L.ci;
+      P.cv_items.push_back(it);
+      continue;
+    }
+    if (L.cons == CONS_BCOP && L.kp == 1) {
+      it.mode = 3; it.dst_off = P.mats[base].off; it.rows = L.c_b; it.c = L.c_b;
+      P.cv_items.push_back(it);
+      continue;
+    }
+    // chain unit (BCOP k' > 1, or AOC): zero dQ, then the last step's gradient (BCOP) or dFin (AOC)
+    it.zero_off = P.mats[base].off; it.zero_n = (int64_t)c * c;
+    it.rows = r; it.c = c;
+    if (L.cons == CONS_AOC) { it.mode = 1; it.dst_off = V.dfin_off; }
+    else { it.mode = 0; it.dst_off = V.dstep_off[V.nsteps - 1]; }
+    P.cv_items.push_back(it);
+    P.cv_qcopy.push_back(P.mats[base].off);   // Q rows [0, r) -> the arena (the backward reads it from BUF_Y)
+    P.cv_qcopy.push_back(V.q_off);
+    P.cv_qcopy.push_back(tap);
+    // forward chain into per-step buffers (same arithmetic as build_compose's chain)
+    auto step_geo = [](int t, int& kh, int& kw) { kh = 1; kw = 1; for (int x = 0; x < t; ++x) { if (x % 2 == 0) kh++; else kw++; } };
+    for (int t = 0; t < V.nsteps; ++t) {
+      const bool vert = (t % 2) == 0;
+      int kh, kw;
+      step_geo(t, kh, kw);
+      const int64_t poff = P.proj_off[base + 1 + t];
+      const int oh = vert ? kh + 1 : kh, ow = vert ? kw : kw + 1;
+      const int64_t in_off = t == 0 ? V.q_off : V.step_off[t - 1];
+      for (int p = 0; p < oh; ++p)
+        for (int q = 0; q < ow; ++q) {
+          const int pp = vert ? p - 1 : p, pq = vert ? q : q - 1;
+          const bool has_cur = vert ? (p < kh) : (q < kw);
+          const bool has_prev = vert ? (p >= 1) : (q >= 1);
+          const int64_t cur = in_off + (int64_t)(p * kw + q) * tap;
+          const int64_t prev = in_off + (int64_t)(pp * kw + pq) * tap;
+          GemmDesc d = mk(r, c, c);
+          d.a_buf = BUF_Y; d.b_buf = BUF_W; d.d_buf = BUF_Y;
+          d.sa_m = c; d.sa_k = 1; d.sb_k = c; d.sb_n = 1;
+          d.d_off = V.step_off[t] + (int64_t)(p * ow + q) * tap; d.ldd = c;
+          if (has_cur && has_prev) {
+            add_seg(P.cv_fwd[t], d, cur, prev, poff);
+            d.c_buf = BUF_Y; d.c_off = prev; d.ldc = c; d.beta = 1.0f;
+          } else if (has_cur) {
+            add_seg(P.cv_fwd[t], d, cur, -1, poff);
+          } else {
+            add_seg(P.cv_fwd[t], d, prev, -1, poff);
+            d.alpha = -1.0f;
+            d.c_buf = BUF_Y; d.c_off = prev; d.ldc = c; d.beta = 1.0f;
+          }
+          P.cv_fwd[t].descs.push_back(d);
+        }
+    }
+    // AOC backward: dR_ab = sum_p dFin[p] Kb[p - ab]^T (first ci columns), dKb[q] = sum_ab R_ab^T dFin[q + ab]
+    if (L.cons == CONS_AOC) {
+      const MatInfo& R = P.mats[base + L.mats_per_group - 1];
+      const int s = L.s, kp = L.kp, k = L.k, cm = L.c_mid;
+      const int64_t kb_off = V.step_off[V.nsteps - 1];
+      for (int a = 0; a < s; ++a)
+        for (int bb = 0; bb < s; ++bb) {
+          GemmDesc d = mk(L.co, cm, L.ci);
+          d.a_buf = BUF_Y; d.b_buf = BUF_Y; d.d_buf = BUF_Y;
+          d.sa_m = L.ci; d.sa_k = 1; d.sb_k = 1; d.sb_n = c;
+          d.d_off = V.drab_off + (int64_t)(a * s + bb) * L.co * cm; d.ldd = cm;
+          for (int p = 0; p < k; ++p)
+            for (int q = 0; q < k; ++q) {
+              const int ta = p - a, tb = q - bb;
+              if (ta < 0 || tb < 0 || ta >= kp || tb >= kp) continue;
+              add_seg(P.cv_dr, d, V.dfin_off + (int64_t)(p * k + q) * L.co * L.ci, -1,
+                      kb_off + (int64_t)(ta * kp + tb) * tap);
+            }
+          P.cv_dr.descs.push_back(d);
+        }
+      ScatterItem sc{L.co, cm, s * s, 0, V.drab_off, R.off};
+      P.cv_scatter.push_back(sc);
+      for (int ta = 0; ta < kp; ++ta)
+        for (int tb = 0; tb < kp; ++tb) {
+          GemmDesc d = mk(cm, L.ci, L.co);   // dKb[q][j][i] for i < ci (the rest of the row stays 0)
+          d.a_buf = BUF_X; d.b_buf = BUF_Y; d.d_buf = BUF_Y;
+          d.sa_m = s * s; d.sa_k = (int64_t)cm * s * s; d.sb_k = L.ci; d.sb_n = 1;
+          d.d_off = V.dstep_off[V.nsteps - 1] + (int64_t)(ta * kp + tb) * tap; d.ldd = c;
+          for (int a = 0; a < s; ++a)
+            for (int bb = 0; bb < s; ++bb)
+              add_seg(P.cv_dkb, d, R.off + a * s + bb, -1,
+                      V.dfin_off + (int64_t)((ta + a) * k + (tb + bb)) * L.co * L.ci);
+          P.cv_dkb.descs.push_back(d);
+        }
+    }
+    // chain backward, aligned from each unit's last step: iteration j handles step t = nsteps - 1 - j
+    for (int j = 0; j < V.nsteps; ++j) {
+      const int t = V.nsteps - 1 - j;
+      const bool vert = (t % 2) == 0;
+      int kh, kw;
+      step_geo(t, kh, kw);
+      const int oh = vert ? kh + 1 : kh, ow = vert ? kw : kw + 1;
+      const int uidx = base + 1 + t;
+      const int64_t poff = P.proj_off[uidx];
+      const int64_t in_off = t == 0 ? V.q_off : V.step_off[t - 1];
+      const int64_t dout = V.dstep_off[t];
+      const int64_t dP_off = take((int64_t)c * c);
+      // dP = sum_y (K_in[cur(y)] - K_in[prev(y)])^T dS[y]   (a missing neighbour is the zero tap)
+      GemmDesc dp = mk(c, c, r);
+      dp.a_buf = BUF_Y; dp.b_buf = BUF_Y; dp.d_buf = BUF_Y;
+      dp.sa_m = 1; dp.sa_k = c; dp.sb_k = c; dp.sb_n = 1;
+      dp.d_off = dP_off; dp.ldd = c;
+      for (int p = 0; p < oh; ++p)
+        for (int q = 0; q < ow; ++q) {
+          const int pp = vert ? p - 1 : p, pq = vert ? q : q - 1;
+          const bool has_cur = vert ? (p < kh) : (q < kw);
+          const bool has_prev = vert ? (p >= 1) : (q >= 1);
+          const int64_t cur = has_cur ? in_off + (int64_t)(p * kw + q) * tap : zero_off;
+          const int64_t prev = has_prev ? in_off + (int64_t)(pp * kw + pq) * tap : -1;
+          add_seg(P.cv_bwd_a[j], dp, cur, prev, dout + (int64_t)(p * ow + q) * tap);
+        }
+      P.cv_bwd_a[j].descs.push_back(dp);
+      // dK_in[x] = (dS[x] - dS[x + step]) P + dS[x + step]   (every input tap has both neighbours)
+      for (int p = 0; p < kh; ++p)
+        for (int q = 0; q < kw; ++q) {
+          const int np = vert ? p + 1 : p, nq = vert ? q : q + 1;
+          const int64_t d0 = dout + (int64_t)(p * ow + q) * tap, d1 = dout + (int64_t)(np * ow + nq) * tap;
+          GemmDesc d = mk(r, c, c);
+          d.a_buf = BUF_Y; d.b_buf = BUF_W;
+          d.sa_m = c; d.sa_k = 1; d.sb_k = c; d.sb_n = 1;
+          d.c_buf = BUF_Y; d.c_off = d1; d.ldc = c; d.beta = 1.0f;
+          if (t == 0) { d.d_buf = BUF_G; d.d_off = P.mats[base].off; }   // dQ rows [0, r)
+          else { d.d_buf = BUF_Y; d.d_off = V.dstep_off[t - 1] + (int64_t)(p * kw + q) * tap; }
+          d.ldd = c;
+          add_seg(P.cv_bwd_a[j], d, d0, d1, poff);
+          P.cv_bwd_a[j].descs.push_back(d);
+        }
+      // dU = (dP + dP^T) U: dP U (phase b), then + dP^T U through C (phase c)
+      const MatInfo& Um = P.mats[uidx];
+      if (Um.n > 0) {
+        GemmDesc du = mk((int)Um.m, (int)Um.n, c);
+        du.a_buf = BUF_Y; du.b_buf = BUF_X; du.d_buf = BUF_G;
+        du.sa_m = c; du.sa_k = 1; du.sb_k = Um.n; du.sb_n = 1;
+        du.d_off = Um.off; du.ldd = Um.n;
+        add_seg(P.cv_bwd_b[j], du, dP_off, -1, Um.off);
+        P.cv_bwd_b[j].descs.push_back(du);
+        GemmDesc dt = mk((int)Um.m, (int)Um.n, c);
+        dt.a_buf = BUF_Y; dt.b_buf = BUF_X; dt.d_buf = BUF_G;
+        dt.sa_m = 1; dt.sa_k = c; dt.sb_k = Um.n; dt.sb_n = 1;
+        dt.d_off = Um.off; dt.ldd = Um.n;
+        dt.c_buf = BUF_G; dt.c_off = Um.off; dt.ldc = Um.n; dt.beta = 1.0f;
+        add_seg(P.cv_bwd_c[j], dt, dP_off, -1, Um.off);
+        P.cv_bwd_c[j].descs.push_back(dt);
+      }
+    }
+  }
+  P.cv_zero_n = w - P.cv_zero_off;
+  finish_phase(P.cv_dr);
+  finish_phase(P.cv_dkb);
+  for (auto& ph : P.cv_fwd) finish_phase(ph);
+  for (auto& ph : P.cv_bwd_a) finish_phase(ph);
+  for (auto& ph : P.cv_bwd_b) finish_phase(ph);
+  for (auto& ph : P.cv_bwd_c) finish_phase(ph);
+  P.vjp_numel = std::max<int64_t>(w, kPadF32);
+}
+
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Per-layer conv scratch, sized now from the declared grid and max_batch so that no call allocates
@@ -900,6 +1219,16 @@ static orth_status_t allocate(Plan& P) {
   for (auto& ph : P.soc_pow) phases.push_back(&ph);
   phases.push_back(&P.sll_v);
   phases.push_back(&P.blk_mm);
+  for (auto& ph : P.vj_fwd) phases.push_back(&ph);
+  for (auto& ph : P.vj_bwd) phases.push_back(&ph);
+  for (auto& ph : P.cv_fwd) phases.push_back(&ph);
+  for (auto& ph : P.cv_bwd_a) phases.push_back(&ph);
+  for (auto& ph : P.cv_bwd_b) phases.push_back(&ph);
+  for (auto& ph : P.cv_bwd_c) phases.push_back(&ph);
+  phases.push_back(&P.cv_dr);
+  phases.push_back(&P.cv_dkb);
+  const size_t o_cvi = take(std::max<size_t>(P.cv_items.size(), 1) * sizeof(VjpItem));
+  const size_t o_cvs = take(std::max<size_t>(P.cv_scatter.size(), 1) * sizeof(ScatterItem));
   const size_t o_sll = take(std::max<size_t>(P.sll.size(), 1) * sizeof(SllItem));
   const size_t o_blk = take(std::max<size_t>(P.blk.size(), 1) * sizeof(BlkItem));
   const size_t o_em2 = take(std::max<size_t>(P.emit2.size(), 1) * sizeof(EmitItem));
@@ -935,6 +1264,8 @@ static orth_status_t allocate(Plan& P) {
   P.d_units = (UnitInfo*)(base + o_units);
   P.d_soc = (SocItem*)(base + o_soc);
   P.d_sll = (SllItem*)(base + o_sll);
+  P.d_cv_items = (VjpItem*)(base + o_cvi);
+  P.d_cv_scatter = (ScatterItem*)(base + o_cvs);
   P.d_blk = (BlkItem*)(base + o_blk);
   P.d_emit2 = (EmitItem*)(base + o_em2);
   P.d_soc_alpha = (float*)(base + o_sal);
@@ -953,6 +1284,11 @@ static orth_status_t allocate(Plan& P) {
     e = cudaMemcpy(P.d_mat_items, P.mat_items.data(), P.mat_items.size() * sizeof(MatItem), cudaMemcpyHostToDevice);
   if (!P.col_items.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_col_items, P.col_items.data(), P.col_items.size() * sizeof(ColItem), cudaMemcpyHostToDevice);
+  if (!P.cv_items.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_cv_items, P.cv_items.data(), P.cv_items.size() * sizeof(VjpItem), cudaMemcpyHostToDevice);
+  if (!P.cv_scatter.empty() && e == cudaSuccess)
+    e = cudaMemcpy(P.d_cv_scatter, P.cv_scatter.data(), P.cv_scatter.size() * sizeof(ScatterItem),
+                   cudaMemcpyHostToDevice);
   if (!P.sll.empty() && e == cudaSuccess)
     e = cudaMemcpy(P.d_sll, P.sll.data(), P.sll.size() * sizeof(SllItem), cudaMemcpyHostToDevice);
   if (!P.blk.empty() && e == cudaSuccess)
@@ -980,6 +1316,15 @@ static orth_status_t allocate(Plan& P) {
     P.d_arena = nullptr;
     return ORTH_ERR_CUDA;
   }
+  if (P.opts.vjp && P.vjp_numel > 0) {   // f1 backward workspace (separate allocation, only on request)
+    if (cudaMalloc(&P.d_vjp, (size_t)P.vjp_numel * sizeof(float)) != cudaSuccess) {
+      cudaGetLastError();
+      P.d_vjp = nullptr;
+      set_error("VJP workspace cudaMalloc(%lld floats) failed", (long long)P.vjp_numel);
+      return ORTH_ERR_OUT_OF_MEMORY;
+    }
+    cudaMemset(P.d_vjp, 0, (size_t)P.vjp_numel * sizeof(float));
+  }
   return allocate_conv(P);
 }
 
@@ -1001,6 +1346,7 @@ void orth_opts_default(orth_opts_t* o) {
   o->world = 1;
   o->ns_tol = 1e-3f;
   o->max_batch = 0;
+  o->vjp = 0;
 }
 
 orth_status_t orth_validate_desc(const orth_layer_desc_t* layers, int32_t n_layers, const orth_opts_t* opts) {
@@ -1052,6 +1398,7 @@ orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers
   layout(P);
   build_ns(P);
   build_compose(P);
+  if (P.opts.vjp) build_vjp(P);
   size_conv(P);
   if (device >= 0) {
     st = allocate(P);
@@ -1064,6 +1411,7 @@ orth_status_t orth_plan_create(const orth_layer_desc_t* layers, int32_t n_layers
       if (P.nsp_mem) cudaFree(P.nsp_mem);
       if (P.d_arena) cudaFree(P.d_arena);
       if (P.d_conv_mem) cudaFree(P.d_conv_mem);
+      if (P.d_vjp) cudaFree(P.d_vjp);
       delete h;
       return st;
     }
@@ -1080,6 +1428,7 @@ orth_status_t orth_plan_destroy(orth_plan_t plan) {
   if (plan->p.nsf_items) cudaFree(plan->p.nsf_items);
   if (plan->p.d_arena) cudaFree(plan->p.d_arena);
   if (plan->p.d_conv_mem) cudaFree(plan->p.d_conv_mem);
+  if (plan->p.d_vjp) cudaFree(plan->p.d_vjp);
   orth_plan_trace_free(plan->p);
   if (plan->p.d_ns_upd64) cudaFree(plan->p.d_ns_upd64);
   if (plan->p.d_ns_gram_flow) cudaFree(plan->p.d_ns_gram_flow);

@@ -372,6 +372,9 @@ orth_status_t orth_plan_trace_read(orth_plan_t plan, orth_trace_rec_t* out, int3
 int64_t orth_plan_launch_count(orth_plan_t plan);
 
 const char* orth_status_string(orth_status_t status);
+/* Build description, e.g. "sm_100a experimental=0" (experimental=1: the opt-in conv_tma / conv_pair kernels
+ * that measured no faster are compiled in, ORTH_EXPERIMENTAL=1 at build time). */
+const char* orth_build_info(void);
 const char* orth_last_error(void);
 
 #ifdef __cplusplus

@@ -91,6 +91,7 @@ _sig = {
     "orth_plan_trace_read": (C.c_int, [_P, C.POINTER(TraceRec), C.c_int32, C.POINTER(C.c_int32)]),
     "orth_plan_launch_count": (C.c_int64, [_P]),
     "orth_status_string": (C.c_char_p, [C.c_int]),
+    "orth_build_info": (C.c_char_p, []),
     "orth_last_error": (C.c_char_p, []),
 }
 for _name, (_res, _args) in _sig.items():
@@ -260,6 +261,10 @@ def orth_plan_trace_read(h: int) -> List[Dict]:
     _check(_lib.orth_plan_trace_read(h, buf, cap, C.byref(n)), "orth_plan_trace_read")
     return [dict(kind=TRACE_KINDS.get(r.kind, str(r.kind)), layer=r.layer, variant=CONV_VARIANTS.get(r.variant, ""),
                  launches=r.launches, ms=r.ms) for r in buf[: min(n.value, cap)]]
+
+
+def experimental() -> bool:
+    return b"experimental=1" in _lib.orth_build_info()
 
 
 def orth_plan_launch_count(h: int) -> int:

@@ -23,6 +23,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 FLAGS += os.environ.get("ORTH_NVCC_FLAGS", "").split()   # diagnostics builds only (e.g. -DORTH_NSP_TRACE)
+if os.environ.get("ORTH_EXPERIMENTAL") == "1":   # opt-in kernels that measured no faster (conv_tma, conv_pair)
+    FLAGS.append("-DORTH_EXPERIMENTAL")
 
 
 def _sources():

@@ -486,6 +486,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // relayed by one peer thread (local barrier -> remote arrive on the leader);
 // the leader's commits release `empty` / signal `tfull` in both CTAs; both
 // CTAs' epilogue warps arrive on the leader's `tempty`.
+#ifdef ORTH_EXPERIMENTAL   // 2-SM pair: measured slower on every cfg2 layer
 template <int BN, int S>
 __global__ void __launch_bounds__(NTHREADS, 1)
     conv_pair(const __nv_bfloat16* __restrict__ in, const float* __restrict__ bias, __nv_bfloat16* __restrict__ out,
@@ -692,6 +693,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   umma::cluster_sync_all();   // no peer may still signal into this CTA
   if (warp == MMA_WARP) umma::tmem_dealloc_pair(tmem, 2 * BN);
 }
+#endif  // ORTH_EXPERIMENTAL
 
 // W^T per tap for the adjoint: WT[(g ci_g + i) k^2 + t][o] = W[(g co_g + o) k^2 + t][i]
 __global__ void __launch_bounds__(256) transpose_w_kernel(const __nv_bfloat16* __restrict__ w,
@@ -727,6 +729,7 @@ int num_sms() {
   }
   return n;
 }
+
 
 template <int BN, int S>
 int launch_ws(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
@@ -798,6 +801,7 @@ int launch_ws(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const
   return e;
 }
 
+#ifdef ORTH_EXPERIMENTAL
 template <int BN, int S>
 int launch_pair(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
                 const TcConvArgs& a, cudaStream_t stream) {
@@ -827,6 +831,7 @@ int launch_pair(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, con
   cfg.numAttrs = 1;
   return (int)cudaLaunchKernelEx(&cfg, conv_pair<BN, S>, in, bias, out, a, tm);
 }
+#endif  // ORTH_EXPERIMENTAL
 
 int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
                TcConvArgs& a, int groups, cudaStream_t s) {
@@ -863,7 +868,11 @@ int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, cons
   // 2-SM pair tiles (M = 256, cta_group::2) for the wide layers.  Correct (parity-tested) but measured
   // SLOWER on every cfg2 layer (e.g. 256@8: 28 -> 40 us): the two producers run in lockstep and the
   // peer's rows reach the leader through a relay; opt-in with ORTH_CONV_PAIR=1 for experiments
+#ifdef ORTH_EXPERIMENTAL
   static const bool want_pair = std::getenv("ORTH_CONV_PAIR") != nullptr;
+#else
+  const bool want_pair = false;
+#endif
   const bool pair = want_pair && cs_env < 0 && bn >= 128 && min_tiles >= 2;
   if (pair) cs = 2;
   a.cs = cs;
@@ -880,12 +889,14 @@ int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, cons
     if (pair || cs > 1) a.ksplit = 1;
     else a.num_ctiles *= a.ksplit;
   }
+#ifdef ORTH_EXPERIMENTAL
   if (pair) {   // stage = 16 KB A + BN/2 x 128 B of B
     if (bn == 256) return a.k <= 3 ? launch_pair<256, 6>(in, w, w_rows, bias, out, a, s)
                                    : launch_pair<256, 5>(in, w, w_rows, bias, out, a, s);
     return a.k <= 3 ? launch_pair<128, 8>(in, w, w_rows, bias, out, a, s)
                     : launch_pair<128, 6>(in, w, w_rows, bias, out, a, s);
   }
+#endif
   switch (bn) {
     // deepest ring that fits 227 KB with the 3x3 table (4.6 KB); larger kernels take the shallower one
     case 256: return launch_ws<256, 4>(in, w, w_rows, bias, out, a, s);

@@ -30,6 +30,7 @@
 #include "tma_host.h"
 #include "umma.cuh"
 
+#ifdef ORTH_EXPERIMENTAL   // measured no faster than conv_ws: built only with ORTH_EXPERIMENTAL=1
 namespace orth {
 namespace {
 
@@ -249,3 +250,12 @@ int launch_conv_fwd_tma(const LayerInfo& L, const void* kernel, const float* bia
 }
 
 }  // namespace orth
+#else
+namespace orth {
+int launch_conv_fwd_tma(const LayerInfo&, const void*, const float*, const void*, void*, int, int, int, int, int,
+                        void*, int) {
+  return -1;
+}
+}  // namespace orth
+#endif
+

@@ -1521,4 +1521,12 @@ const char* orth_status_string(orth_status_t s) {
 
 const char* orth_last_error(void) { return orth::g_err; }
 
+const char* orth_build_info(void) {
+#ifdef ORTH_EXPERIMENTAL
+  return "sm_100a experimental=1";
+#else
+  return "sm_100a experimental=0";
+#endif
+}
+
 }  // extern "C"

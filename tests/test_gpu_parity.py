@@ -281,8 +281,11 @@ def test_conv_splitk_path(cuda_lib, case):
 
 @pytest.mark.parametrize("case", [(128, 128, 3, 1, 1, 1, "circular", 16, "conv"), (128, 256, 3, 2, 1, 1, "zeros", 9, "conv"),
                                   (256, 256, 3, 1, 2, 1, "circular", 8, "convT")])
-def test_conv_pair_path(case):
-    """The opt-in 2-SM pair (cta_group::2) conv kernel, in a subprocess (the switch is read once)."""
+def test_conv_pair_path(cuda_lib, case):
+    """The opt-in 2-SM pair (cta_group::2) conv kernel, in a subprocess (the switch is read once); built only
+    with ORTH_EXPERIMENTAL=1."""
+    if not cuda_lib.experimental():
+        pytest.skip("experimental kernels not built (ORTH_EXPERIMENTAL=1)")
     import os
     import subprocess
     import sys
@@ -299,9 +302,12 @@ STACK_CASES = [(128, 256, 3, 1, 2, 1, "circular", 12, "conv"), (256, 128, 5, 1, 
                (96, 128, 3, 1, 1, 1, "circular", 6, "conv"), (512, 512, 3, 1, 1, 1, "circular", 4, "conv")]
 
 
-def test_conv_tma_path():
+def test_conv_tma_path(cuda_lib):
     """The opt-in TMA implicit-GEMM kernel (conv_tma.cu, ORTH_CONV_TMA=1: padded copy + one 4-D box per
-    tap) on stride-1 >= 128-channel cases, forward and adjoint, BF16, in a subprocess."""
+    tap) on stride-1 >= 128-channel cases, forward and adjoint, BF16, in a subprocess; built only with
+    ORTH_EXPERIMENTAL=1."""
+    if not cuda_lib.experimental():
+        pytest.skip("experimental kernels not built (ORTH_EXPERIMENTAL=1)")
     import os
     import subprocess
     import sys

@@ -86,25 +86,30 @@ __device__ __forceinline__ int wrapi(int x, int n) {
 
 // padded[n][yy][xx][c] = x~[n][yy - p_t][xx - p_l][c] (circular: mod H, W; zeros outside), 8 channels
 // (16 B) per thread; rows of the whole batch back to back
+// one CTA per padded row (n, yy): its source row is resolved once (32-bit math per 16-byte element,
+// no 64-bit divisions), the P x C/8 16-byte chunks of the row are stored contiguously (coalesced)
 __global__ void __launch_bounds__(256) pad_kernel(const uint4* __restrict__ x, uint4* __restrict__ out, int N, int H,
                                                   int W, int C8, int Hp, int P, int pt, int pl, int circ) {
-  const int64_t total = (int64_t)N * Hp * P * C8;
-  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (int64_t)gridDim.x * 256) {
-    const int c = (int)(e % C8);
-    const int64_t pix = e / C8;
-    const int xx = (int)(pix % P);
-    const int64_t row = pix / P;
-    const int yy = (int)(row % Hp), n = (int)(row / Hp);
-    int h = yy - pt, w = xx - pl;
+  const int64_t row = blockIdx.x;                 // n * Hp + yy
+  const int n = (int)(row / Hp), yy = (int)(row - (int64_t)n * Hp);
+  int h = yy - pt;
+  bool hok = true;
+  if (circ) h = wrapi(h, H);
+  else hok = h >= 0 && h < H;
+  const uint4* src = x + ((int64_t)n * H + (hok ? h : 0)) * W * C8;
+  uint4* dst = out + row * (int64_t)P * C8;
+  const int per = P * C8;
+  for (int e = threadIdx.x; e < per; e += 256) {
+    const int xx = e / C8, c = e - xx * C8;
+    int w = xx - pl;
     uint4 v = make_uint4(0u, 0u, 0u, 0u);
     if (circ) {
-      h = wrapi(h, H);
       w = wrapi(w, W);
-      v = __ldg(x + (((int64_t)n * H + h) * W + w) * C8 + c);
-    } else if (h >= 0 && h < H && w >= 0 && w < W) {
-      v = __ldg(x + (((int64_t)n * H + h) * W + w) * C8 + c);
+      v = __ldg(src + w * C8 + c);
+    } else if (hok && w >= 0 && w < W) {
+      v = __ldg(src + w * C8 + c);
     }
-    out[e] = v;
+    dst[e] = v;
   }
 }
 
@@ -363,9 +368,7 @@ bool stack_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, StackAr
 int launch_pad_input(const LayerInfo& L, const void* x, int N, int H, int W, int Hp, int P, void* stream) {
   const int64_t elems = (int64_t)N * Hp * P * L.ci_f;
   if (!L.pad_scratch || elems * 2 > L.pad_bytes || L.ci_f % 8 != 0) return -1;
-  const int64_t vec = elems / 8;
-  const int blocks = (int)std::min<int64_t>((vec + 255) / 256, (int64_t)conv_sm_count() * 16);
-  pad_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4*)x, (uint4*)L.pad_scratch, N, H, W, L.ci_f / 8,
+  pad_kernel<<<(unsigned)((int64_t)N * Hp), 256, 0, (cudaStream_t)stream>>>((const uint4*)x, (uint4*)L.pad_scratch, N, H, W, L.ci_f / 8,
                                                       Hp, P, L.pt, L.pl,
                                                       L.desc.padding_mode == ORTH_PAD_CIRCULAR ? 1 : 0);
   return (int)cudaGetLastError();
@@ -404,9 +407,7 @@ int launch_conv_fwd_stack(const LayerInfo& L, const void* kernel, const float* b
   g_conv_variant = ORTH_CV_STACK;
   cudaStream_t s = (cudaStream_t)stream;
   {
-    const int64_t vec = pad_elems / 8;
-    const int blocks = (int)std::min<int64_t>((vec + 255) / 256, (int64_t)conv_sm_count() * 16);
-    pad_kernel<<<blocks, 256, 0, s>>>((const uint4*)x, (uint4*)L.pad_scratch, N, H, W, a.in_C / 8, a.Hp, a.P, L.pt,
+    pad_kernel<<<(unsigned)((int64_t)N * a.Hp), 256, 0, s>>>((const uint4*)x, (uint4*)L.pad_scratch, N, H, W, a.in_C / 8, a.Hp, a.P, L.pt,
                                       L.pl, a.circ);
     if (int e = (int)cudaGetLastError()) return e;
   }

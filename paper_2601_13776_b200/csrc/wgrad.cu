@@ -184,23 +184,39 @@ __global__ void __launch_bounds__(256) wgrad_reduce(const float* __restrict__ pa
   }
 }
 
+// SIMT weight gradient over pixel splits: CTA (split, element block) accumulates 256 dK elements (one
+// per thread) over its pixel range, staging the range's dy rows of the block's output channels and the
+// tap-shifted x values in shared memory is unnecessary at these sizes -- each thread walks the pixels in
+// order (fixed order, deterministic); the splits are then reduced by wgrad_reduce_simt in split order.
 template <typename T>
 __global__ void __launch_bounds__(256) wgrad_simt(const T* __restrict__ x, const T* __restrict__ dy, WgArgs a,
-                                                  float* __restrict__ dK) {
+                                                  float* __restrict__ part) {
+  const int64_t total = (int64_t)a.g * a.co * a.ci * a.kk;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int split = blockIdx.y;
+  if (e >= total) return;
+  const int t = (int)(e % a.kk);
+  int64_t r = e / a.kk;
+  const int i = (int)(r % a.ci); r /= a.ci;
+  const int o = (int)(r % a.co);
+  const int grp = (int)(r / a.co);
+  const int ta = t / a.k, tb = t - ta * a.k;
+  const int64_t p0 = (int64_t)split * a.per_split, p1 = min(a.pixels, p0 + a.per_split);
+  float acc = 0.f;
+  for (int64_t p = p0; p < p1; ++p) {
+    const int64_t ip = in_pixel(a, p, ta, tb);
+    if (ip < 0) continue;
+    acc = fmaf((float)dy[p * a.Co + (int64_t)grp * a.co + o], (float)x[ip * a.Ci + (int64_t)grp * a.ci + i], acc);
+  }
+  part[(int64_t)split * total + e] = acc;
+}
+
+__global__ void __launch_bounds__(256) wgrad_reduce_simt(const float* __restrict__ part, WgArgs a,
+                                                         float* __restrict__ dK) {
   const int64_t total = (int64_t)a.g * a.co * a.ci * a.kk;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(e % a.kk);
-    int64_t r = e / a.kk;
-    const int i = (int)(r % a.ci); r /= a.ci;
-    const int o = (int)(r % a.co);
-    const int grp = (int)(r / a.co);
-    const int ta = t / a.k, tb = t - ta * a.k;
     float acc = 0.f;
-    for (int64_t p = 0; p < a.pixels; ++p) {
-      const int64_t ip = in_pixel(a, p, ta, tb);
-      if (ip < 0) continue;
-      acc = fmaf((float)dy[p * a.Co + (int64_t)grp * a.co + o], (float)x[ip * a.Ci + (int64_t)grp * a.ci + i], acc);
-    }
+    for (int sp = 0; sp < a.splits; ++sp) acc += part[sp * total + e];
     dK[e] = acc;
   }
 }
@@ -243,9 +259,18 @@ int launch_tc(const __nv_bfloat16* x, const __nv_bfloat16* dy, const WgArgs& a, 
 
 }  // namespace
 
+// SIMT pixel splits: enough CTAs for ~4 waves, >= 64 pixels per split
+static int simt_splits(const LayerInfo& L, int64_t pixels) {
+  const int64_t blocks = ((int64_t)L.g * L.co * L.ci * L.k * L.k + 255) / 256;
+  int64_t sp = std::max<int64_t>(1, (4 * 148 + blocks - 1) / blocks);
+  sp = std::min<int64_t>(sp, std::max<int64_t>(1, pixels / 64));
+  return (int)std::min<int64_t>(sp, 4096);
+}
+
 int64_t wgrad_workspace_bytes(const LayerInfo& L, int N, int Ho, int Wo, int io) {
-  if (io != ORTH_BF16 || !tc_ok(L)) return 0;
-  return (int64_t)wgrad_splits(L, (int64_t)N * Ho * Wo) * L.kernel_numel * 4;
+  const int64_t pixels = (int64_t)N * Ho * Wo;
+  if (io != ORTH_BF16 || !tc_ok(L)) return simt_splits(L, pixels) > 1 ? (int64_t)simt_splits(L, pixels) * L.kernel_numel * 4 : 0;
+  return (int64_t)wgrad_splits(L, pixels) * L.kernel_numel * 4;
 }
 
 int launch_wgrad(const LayerInfo& L, const void* x, const void* dy, float* dK, int N, int H, int W, int Ho, int Wo,
@@ -271,10 +296,17 @@ int launch_wgrad(const LayerInfo& L, const void* x, const void* dy, float* dK, i
     return (int)cudaGetLastError();
   }
   g_conv_variant = ORTH_CV_SIMT;
+  a.splits = simt_splits(L, a.pixels);
+  if (a.splits > 1 && (!ws || ws_bytes < (int64_t)a.splits * L.kernel_numel * 4)) a.splits = 1;
+  a.per_split = (a.pixels + a.splits - 1) / a.splits;
+  a.splits = (int)((a.pixels + a.per_split - 1) / a.per_split);
+  float* out = a.splits > 1 ? static_cast<float*>(ws) : dK;
+  const dim3 grid((unsigned)((total + 255) / 256), (unsigned)a.splits);
   if (io == ORTH_BF16)
-    wgrad_simt<__nv_bfloat16><<<rb, 256, 0, s>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, a, dK);
+    wgrad_simt<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, a, out);
   else
-    wgrad_simt<float><<<rb, 256, 0, s>>>((const float*)x, (const float*)dy, a, dK);
+    wgrad_simt<float><<<grid, 256, 0, s>>>((const float*)x, (const float*)dy, a, out);
+  if (a.splits > 1) wgrad_reduce_simt<<<rb, 256, 0, s>>>(out, a, dK);
   return (int)cudaGetLastError();
 }
 

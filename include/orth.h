@@ -278,10 +278,11 @@ orth_status_t orth_plan_check(orth_plan_t plan, void* stream);
  * (y = conv(x, K): x on the large grid (N, H, W, C_i), dy on the output grid (N, H_out, W_out, C_o); for an
  * ORTH_CONV_TRANSPOSE2D layer, whose forward is the adjoint, x is the gradient of its large output and dy its
  * small input):  dkernel_f32 = dK, PyTorch layout of the layer's FP32 kernel, defined by the bilinear form
- * <dy, conv(x, delta K)> = <dK, delta K>.  io = ORTH_BF16: tcgen05 GEMM over the pixels (M = c_out/g,
- * N = c_in/g) with pixel splits summed in a fixed order through `workspace`
- * (orth_conv_wgrad_workspace bytes, caller-owned device memory); io = ORTH_F32: FP32 SIMT (workspace unused).
- * FP32 accumulation, deterministic.  Not for SLL blocks or dense layers. */
+ * <dy, conv(x, delta K)> = <dK, delta K>.  io = ORTH_BF16 with channels per group multiple of 8: tcgen05
+ * GEMM over the pixels (M = c_out/g, N = c_in/g, up to 3 taps per CTA sharing the dy tile); otherwise
+ * FP32 SIMT.  Both sum pixel splits in a fixed order through `workspace` (orth_conv_wgrad_workspace bytes,
+ * caller-owned device memory; 0 bytes: none needed).  FP32 accumulation, deterministic.  N*H*W < 2^31.
+ * Not for SLL blocks or dense layers. */
 orth_status_t orth_conv_wgrad_workspace(orth_plan_t plan, int32_t layer, int32_t N, int32_t H, int32_t W, int32_t io,
                                         int64_t* bytes);
 orth_status_t orth_conv_wgrad(orth_plan_t plan, int32_t layer, const void* x, const void* dy, float* dkernel_f32,

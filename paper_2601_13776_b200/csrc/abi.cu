@@ -356,6 +356,7 @@ orth_status_t orth_conv_wgrad(orth_plan_t plan, int32_t layer, const void* x, co
   if (st != ORTH_OK) return st;
   const LayerInfo& L = P.layers[layer];
   if (L.cons == CONS_SLL_BLOCK) { set_error("SLL blocks have no single weight gradient"); return ORTH_ERR_UNSUPPORTED_CONFIG; }
+  if ((int64_t)N * H * W >= (1LL << 31)) { set_error("N*H*W must stay below 2^31 (32-bit pixel indices)"); return ORTH_ERR_SHAPE_MISMATCH; }
   NvtxRange nv("orth_conv_wgrad");
   Trace tr(P, ORTH_TK_WGRAD, layer, stream);
   const int e = launch_wgrad(L, x, dy, dkernel_f32, N, H, W, Ho, Wo, io, workspace, workspace_bytes, stream);

@@ -21,8 +21,8 @@
 // accumulation error at 512 channels, the size of the tolerance.
 //
 // Kernels: symbol_kernel (one thread per B element, taps looped),
-// gram_kernel (32 x 32 complex tile per CTA, k in chunks of 16 staged in
-// shared memory, 2 x 2 complex accumulators per thread), stats_kernel (one CTA
+// gram_kernel (64 x 64 complex tile per CTA, k in chunks of 16 staged in
+// shared memory, 4 x 4 complex accumulators per thread), stats_kernel (one CTA
 // per (group, frequency): |E|_F in a fixed order, then the power iteration).
 #include <cuda_runtime.h>
 
@@ -41,10 +41,6 @@ struct CertGeo {
   int S, Kd;             // short side, long side
   int rows_short;        // 1: S = co (E = A A^H), 0: S = nin (E = A^H A)
 };
-
-__device__ __forceinline__ double2 cmul_conj_a(double2 a, double2 b) {   // conj(a) * b
-  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
-}
 
 // B[gf][kk][ii] (row-major, ii contiguous): the long side kk, the short side ii, with E = B^H B - I.
 // S = nin: B[o][j] = A[o][j];   S = co: B[j][o] = conj(A[o][j]).
@@ -85,21 +81,26 @@ __global__ void __launch_bounds__(256) symbol_kernel(const float* __restrict__ K
   }
 }
 
-constexpr int TS = 32, TK = 16;
+constexpr int TS = 64, TK = 16;
 
-// E[gf][i][j] = sum_k conj(B[k][i]) B[k][j] - delta_ij over one 32 x 32 tile
+// E[gf][i][j] = sum_k conj(B[k][i]) B[k][j] - delta_ij over one 64 x 64 tile; 16 x 16 threads with 4 x 4
+// complex accumulators each (16 complex MACs = 64 DFMA per 8 shared-memory 16-byte loads)
 __global__ void __launch_bounds__(256) gram_kernel(const double2* __restrict__ B, CertGeo G, double2* __restrict__ E) {
   __shared__ double2 Bi[TK][TS], Bj[TK][TS];
+  // E is Hermitian: only tiles ti <= tj are computed (blockIdx.x enumerates the upper triangle row by
+  // row); an off-diagonal tile also writes its conjugate mirror
   const int tiles = (G.S + TS - 1) / TS;
-  const int ti = blockIdx.x / tiles, tj = blockIdx.x % tiles;
+  int ti = 0, rem = blockIdx.x;
+  while (rem >= tiles - ti) { rem -= tiles - ti; ++ti; }
+  const int tj = ti + rem;
   const int64_t gf = blockIdx.y;
   const double2* Bg = B + gf * (int64_t)G.Kd * G.S;
-  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;   // 16 x 16 threads, 2 x 2 outputs each
-  double2 acc[2][2];
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  double2 acc[4][4];
 #pragma unroll
-  for (int p = 0; p < 2; ++p)
+  for (int p = 0; p < 4; ++p)
 #pragma unroll
-    for (int q = 0; q < 2; ++q) acc[p][q] = make_double2(0.0, 0.0);
+    for (int q = 0; q < 4; ++q) acc[p][q] = make_double2(0.0, 0.0);
   for (int k0 = 0; k0 < G.Kd; k0 += TK) {
     for (int x = tid; x < TK * TS; x += 256) {
       const int kr = x / TS, c = x % TS;
@@ -108,29 +109,34 @@ __global__ void __launch_bounds__(256) gram_kernel(const double2* __restrict__ B
       Bj[kr][c] = (kk < G.Kd && cj < G.S) ? Bg[(int64_t)kk * G.S + cj] : make_double2(0.0, 0.0);
     }
     __syncthreads();
-#pragma unroll 4
+#pragma unroll 2
     for (int kr = 0; kr < TK; ++kr) {
-      const double2 a0 = Bi[kr][ty * 2], a1 = Bi[kr][ty * 2 + 1];
-      const double2 b0 = Bj[kr][tx * 2], b1 = Bj[kr][tx * 2 + 1];
-      const double2 p00 = cmul_conj_a(a0, b0), p01 = cmul_conj_a(a0, b1);
-      const double2 p10 = cmul_conj_a(a1, b0), p11 = cmul_conj_a(a1, b1);
-      acc[0][0].x += p00.x; acc[0][0].y += p00.y;
-      acc[0][1].x += p01.x; acc[0][1].y += p01.y;
-      acc[1][0].x += p10.x; acc[1][0].y += p10.y;
-      acc[1][1].x += p11.x; acc[1][1].y += p11.y;
+      double2 av[4], bv[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) av[p] = Bi[kr][ty + 16 * p];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bv[q] = Bj[kr][tx + 16 * q];
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {   // conj(a) * b
+          acc[p][q].x = fma(av[p].x, bv[q].x, fma(av[p].y, bv[q].y, acc[p][q].x));
+          acc[p][q].y = fma(av[p].x, bv[q].y, fma(-av[p].y, bv[q].x, acc[p][q].y));
+        }
     }
     __syncthreads();
   }
   double2* Eg = E + gf * (int64_t)G.S * G.S;
 #pragma unroll
-  for (int p = 0; p < 2; ++p)
+  for (int p = 0; p < 4; ++p)
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int i = ti * TS + ty * 2 + p, j = tj * TS + tx * 2 + q;
+    for (int q = 0; q < 4; ++q) {
+      const int i = ti * TS + ty + 16 * p, j = tj * TS + tx + 16 * q;
       if (i < G.S && j < G.S) {
         double2 v = acc[p][q];
         if (i == j) v.x -= 1.0;
         Eg[(int64_t)i * G.S + j] = v;
+        if (ti != tj) Eg[(int64_t)j * G.S + i] = make_double2(v.x, -v.y);
       }
     }
 }
@@ -242,7 +248,7 @@ int launch_certify(const LayerInfo& L, const float* kernel, int H, int W, int it
   const int blocks = (int)std::min<int64_t>((nB + 255) / 256, 148 * 16);
   symbol_kernel<<<blocks, 256, 0, s>>>(kernel, G, B);
   const int tiles = (G.S + TS - 1) / TS;
-  gram_kernel<<<dim3((unsigned)(tiles * tiles), (unsigned)gf), 256, 0, s>>>(B, G, E);
+  gram_kernel<<<dim3((unsigned)(tiles * (tiles + 1) / 2), (unsigned)gf), 256, 0, s>>>(B, G, E);
   stats_kernel<<<(unsigned)gf, 256, 0, s>>>(E, G, iters, Z, out);
   return (int)cudaGetLastError();
 }

@@ -34,15 +34,17 @@ struct WgArgs {
   int64_t pixels;          // N Ho Wo
   int splits, tiles_m, tiles_n, kk;
   int64_t per_split;       // pixels per split (multiple of 64)
+  int tpc, tgroups;        // taps per CTA (consecutive in row-major tap order), tap groups
 };
 
-constexpr int kStages = 4;
-constexpr int kProd = 128;   // 4 producer / epilogue warps
+constexpr int kProd = 256;   // 8 producer / epilogue warps
 
-__device__ __forceinline__ int64_t in_pixel(const WgArgs& a, int64_t p, int ta, int tb) {
-  const int64_t hw = (int64_t)a.Ho * a.Wo;
-  const int64_t n = p / hw;
-  const int r = (int)(p - n * hw);
+// input pixel (flattened n, h, w) read by output pixel p at tap (ta, tb); -1 = zero padding.  32-bit:
+// N Ho Wo and N H W stay below 2^31 for every workload here (checked on the host)
+__device__ __forceinline__ int in_pixel32(const WgArgs& a, int p, int ta, int tb) {
+  const int hw = a.Ho * a.Wo;
+  const int n = p / hw;
+  const int r = p - n * hw;
   const int u = r / a.Wo, v = r - u * a.Wo;
   int h = a.s * u + a.d * ta - a.pt, w = a.s * v + a.d * tb - a.pl;
   if (a.circ) {
@@ -54,34 +56,43 @@ __device__ __forceinline__ int64_t in_pixel(const WgArgs& a, int64_t p, int ta, 
   return (n * a.H + h) * a.W + w;
 }
 
-template <int BN>
+__device__ __forceinline__ int64_t in_pixel(const WgArgs& a, int64_t p, int ta, int tb) {
+  return in_pixel32(a, (int)p, ta, tb);
+}
+
+// One CTA = (pixel split, group, tap group of TPC consecutive taps, 128-row co tile, BN-wide ci tile).
+// Per stage (64 pixels): the dy tile (A, MN-major, 16 KB) is gathered ONCE and multiplied with TPC
+// tap-shifted x tiles (B_j, MN-major) into TPC accumulators (TPC * BN <= 512 TMEM columns).  Each of
+// the 256 producer threads owns one quarter of one pixel row: it resolves its pixel's input offsets
+// itself (no per-stage barrier) and issues its 16-byte cp.async chunks.
+template <int BN, int TPC, int S>
 __global__ void __launch_bounds__(kProd + 32, 1)
     wgrad_tc(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy, WgArgs a,
              float* __restrict__ part) {
-  constexpr int A_BYTES = 2 * 8192, B_BYTES = (BN / 64) * 8192, STAGE = A_BYTES + B_BYTES;
+  constexpr int A_BYTES = 2 * 8192, B_BYTES = (BN / 64) * 8192, STAGE = A_BYTES + TPC * B_BYTES;
+  constexpr int TCOLS = TPC * BN <= 32 ? 32 : TPC * BN <= 64 ? 64 : TPC * BN <= 128 ? 128 : TPC * BN <= 256 ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = umma::align1024_smem(smem_raw);
-  __shared__ uint64_t full_bar[kStages], empty_bar[kStages], done_bar;
+  __shared__ uint64_t full_bar[S], empty_bar[S], done_bar;
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int64_t tbl[kStages][64];
 
   const int tid = threadIdx.x, warp = tid >> 5;
-  // tile decode: split slowest, then group, tap, M tile, N tile
   int64_t idx = blockIdx.x;
   const int nb = (int)(idx % a.tiles_n); idx /= a.tiles_n;
   const int mb = (int)(idx % a.tiles_m); idx /= a.tiles_m;
-  const int t = (int)(idx % a.kk); idx /= a.kk;
+  const int tg = (int)(idx % a.tgroups); idx /= a.tgroups;
   const int grp = (int)(idx % a.g); idx /= a.g;
   const int split = (int)idx;
-  const int ta = t / a.k, tb = t - ta * a.k;
+  const int t0 = tg * TPC;
+  const int ntap = min(TPC, a.kk - t0);
   const int m0 = mb * 128, n0 = nb * BN;
-  const int64_t p_begin = (int64_t)split * a.per_split;
-  const int64_t p_end = std::min<int64_t>(a.pixels, p_begin + a.per_split);
-  const int nk = (int)((p_end - p_begin + 63) / 64);
+  const int p_begin = (int)((int64_t)split * a.per_split);
+  const int p_end = (int)(a.pixels < (int64_t)p_begin + a.per_split ? a.pixels : (int64_t)p_begin + a.per_split);
+  const int nk = (p_end - p_begin + 63) / 64;
 
-  if (warp == 4) umma::tmem_alloc(&tmem_base_sh, BN);
+  if (warp == 8) umma::tmem_alloc(&tmem_base_sh, TCOLS);
   if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < S; ++i) {
       umma::mbar_init(&full_bar[i], kProd);
       umma::mbar_init(&empty_bar[i], 1);
     }
@@ -94,77 +105,88 @@ __global__ void __launch_bounds__(kProd + 32, 1)
   const uint32_t tmem = tmem_base_sh;
   const uint32_t s0 = umma::smem_u32(smem);
 
-  if (warp < 4) {
-    // ---------------- producers: 64 pixels per stage
+  if (warp < 8) {
+    // ---------------- producers: thread = (pixel row r, quarter q)
+    const int r = tid >> 2, q = tid & 3;
     for (int kb = 0; kb < nk; ++kb) {
-      const int st = kb % kStages;
-      if (kb >= kStages) umma::mbar_wait(&empty_bar[st], ((kb / kStages) - 1) & 1);
-      const int64_t pb = p_begin + (int64_t)kb * 64;
-      if (tid < 64) {
-        const int64_t p = pb + tid;
-        tbl[st][tid] = p < p_end ? in_pixel(a, p, ta, tb) : -1;
-      }
-      umma::named_bar_sync(1, kProd);
-      const uint32_t sa = s0 + st * STAGE, sb = sa + A_BYTES;
-      // A: dy rows, 16 chunks of 8 channels (128 o) per pixel
-      for (int q = tid; q < 64 * 16; q += kProd) {
-        const int r = q >> 4, j = q & 15;
-        const int64_t p = pb + r;
+      const int st = kb % S;
+      if (kb >= S) umma::mbar_wait(&empty_bar[st], ((kb / S) - 1) & 1);
+      const int p = p_begin + kb * 64 + r;
+      const bool pin = p < p_end;
+      const uint32_t sa = s0 + st * STAGE;
+      // A: the dy row of pixel p, channels m0 .. m0 + 127 (16 chunks, 4 per thread)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = q * 4 + jj;
         const int o = m0 + 8 * j;
-        const bool ok = p < p_end && o < a.co;
-        const __nv_bfloat16* src = dy + (ok ? (p * a.Co + (int64_t)grp * a.co + o) : 0);
-        const uint32_t dst = sa + (j >> 3) * 8192 + r * 128 + (((j & 7) ^ (r & 7)) << 4);
-        umma::cp_async16(dst, src, ok);
+        const bool ok = pin && o < a.co;
+        const __nv_bfloat16* src = dy + (ok ? ((int64_t)p * a.Co + (int64_t)grp * a.co + o) : 0);
+        umma::cp_async16(sa + (j >> 3) * 8192 + r * 128 + (((j & 7) ^ (r & 7)) << 4), src, ok);
       }
-      // B: x rows of the tap-shifted input pixels, BN/8 chunks per pixel
-      for (int q = tid; q < 64 * (BN / 8); q += kProd) {
-        const int r = q / (BN / 8), j = q - r * (BN / 8);
-        const int64_t ip = tbl[st][r];
-        const int i = n0 + 8 * j;
-        const bool ok = ip >= 0 && i < a.ci;
-        const __nv_bfloat16* src = x + (ok ? (ip * a.Ci + (int64_t)grp * a.ci + i) : 0);
-        const uint32_t dst = sb + (j >> 3) * 8192 + r * 128 + (((j & 7) ^ (r & 7)) << 4);
-        umma::cp_async16(dst, src, ok);
+      // B_j: x rows of the tap-shifted input pixel, BN / 8 chunks (BN / 32 per thread)
+      for (int jt = 0; jt < ntap; ++jt) {
+        const int t = t0 + jt;
+        const int ta = t / a.k, tb = t - ta * a.k;
+        const int ip = pin ? in_pixel32(a, p, ta, tb) : -1;
+        const uint32_t sb = sa + A_BYTES + jt * B_BYTES;
+#pragma unroll
+        for (int jj = 0; jj < BN / 32; ++jj) {
+          const int j = q * (BN / 32) + jj;
+          const int i = n0 + 8 * j;
+          const bool ok = ip >= 0 && i < a.ci;
+          const __nv_bfloat16* src = x + (ok ? ((int64_t)ip * a.Ci + (int64_t)grp * a.ci + i) : 0);
+          umma::cp_async16(sb + (j >> 3) * 8192 + r * 128 + (((j & 7) ^ (r & 7)) << 4), src, ok);
+        }
       }
       umma::cp_async_mbar_arrive(&full_bar[st]);
     }
-    // ---------------- epilogue: TMEM -> this split's FP32 partial tile [o][i]
+    // ---------------- epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31, column half (w / 4)
     umma::mbar_wait(&done_bar, 0);
     umma::tc_fence_after();
-    const int o = m0 + warp * 32 + (tid & 31);
-    float* dst = part + (((int64_t)split * a.g + grp) * a.kk + t) * ((int64_t)a.co * a.ci);
+    const int lq = warp & 3, half = warp >> 2;
+    const int o = m0 + lq * 32 + (tid & 31);
+    for (int jt = 0; jt < ntap; ++jt) {
+      float* dst = part + (((int64_t)split * a.g + grp) * a.kk + t0 + jt) * ((int64_t)a.co * a.ci);
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      float v[32];
-      umma::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-      if (o < a.co) {
+      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
+        float v[32];
+        umma::tmem_ld32(tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(jt * BN + c0), v);
+        if (o < a.co) {
+          float* row = dst + (int64_t)o * a.ci + n0 + c0;
+          if (n0 + c0 + 32 <= a.ci && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int i = n0 + c0 + j;
-          if (i < a.ci) dst[(int64_t)o * a.ci + i] = v[j];
+            for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(row + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n0 + c0 + j < a.ci) row[j] = v[j];
+          }
         }
       }
     }
   } else if (tid == kProd) {
-    // ---------------- MMA issuer
+    // ---------------- MMA issuer: per stage, 4 K=16 steps x TPC taps sharing the A tile
     constexpr uint32_t IDESC = umma::idesc_bf16(128, BN) | (1u << 15) | (1u << 16);   // A, B MN-major
     for (int kb = 0; kb < nk; ++kb) {
-      const int st = kb % kStages;
-      umma::mbar_wait(&full_bar[st], (kb / kStages) & 1);
+      const int st = kb % S;
+      umma::mbar_wait(&full_bar[st], (kb / S) & 1);
       umma::fence_proxy_async_smem();   // cp.async (generic proxy) rows -> tcgen05.mma (async proxy)
       umma::tc_fence_after();
-      const uint32_t sa = s0 + st * STAGE, sb = sa + A_BYTES;
+      const uint32_t sa = s0 + st * STAGE;
+      for (int jt = 0; jt < ntap; ++jt) {
+        const uint32_t sb = sa + A_BYTES + jt * B_BYTES;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        umma::mma_bf16(tmem, umma::sdesc_sw128_mn(sa + 2048 * q, 8192), umma::sdesc_sw128_mn(sb + 2048 * q, 8192),
-                       IDESC, (kb | q) != 0);
+        for (int q = 0; q < 4; ++q)
+          umma::mma_bf16(tmem + (uint32_t)(jt * BN), umma::sdesc_sw128_mn(sa + 2048 * q, 8192),
+                         umma::sdesc_sw128_mn(sb + 2048 * q, 8192), IDESC, (kb | q) != 0);
+      }
       umma::mma_commit(&empty_bar[st]);
     }
     umma::mma_commit(&done_bar);
   }
   umma::tc_fence_before();
   __syncthreads();
-  if (warp == 4) umma::tmem_dealloc(tmem, BN);
+  if (warp == 8) umma::tmem_dealloc(tmem, TCOLS);
 }
 
 // dK[(g co + o) ci k^2 + i k^2 + t] = sum over splits (in order) of part[split][g][t][o][i]
@@ -235,26 +257,47 @@ WgArgs make_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo) {
 bool tc_ok(const LayerInfo& L) { return L.ci % 8 == 0 && L.co % 8 == 0 && L.ci_f % 8 == 0 && L.co_f % 8 == 0; }
 
 int pick_bn(const LayerInfo& L) { return L.ci > 128 ? 256 : L.ci > 64 ? 128 : 64; }
+// taps per CTA (sharing the dy tile): 1 for 256-wide ci tiles (4 stages of 48 KB), else up to 3
+// (BN = 128: 3 stages of 64 KB; BN = 64: 4 stages of 40 KB) -- one row of a 3 x 3 kernel
+int pick_tpc(const LayerInfo& L) {
+  const int bn = pick_bn(L);
+  return bn == 256 ? 1 : std::min(3, L.k * L.k);
+}
 
 int wgrad_splits(const LayerInfo& L, int64_t pixels) {
-  const int64_t base = (int64_t)L.g * L.k * L.k * ((L.co + 127) / 128) * ((L.ci + pick_bn(L) - 1) / pick_bn(L));
+  const int tpc = pick_tpc(L);
+  const int64_t base = (int64_t)L.g * ((L.k * L.k + tpc - 1) / tpc) * ((L.co + 127) / 128) *
+                       ((L.ci + pick_bn(L) - 1) / pick_bn(L));
   int64_t sp = std::max<int64_t>(1, (2 * 148 + base - 1) / base);        // ~2 waves of CTAs
-  sp = std::min<int64_t>(sp, std::max<int64_t>(1, pixels / 256));       // >= 256 pixels per split
+  sp = std::min<int64_t>(sp, std::max<int64_t>(1, pixels / 512));       // >= 512 pixels per split
   return (int)std::min<int64_t>(sp, 64);
 }
 
-template <int BN>
+template <int BN, int TPC, int S>
 int launch_tc(const __nv_bfloat16* x, const __nv_bfloat16* dy, const WgArgs& a, float* part, cudaStream_t s) {
-  constexpr size_t STAGE = 2 * 8192 + (BN / 64) * 8192;
-  const size_t smem = 1024 + kStages * STAGE;
+  constexpr size_t STAGE = 2 * 8192 + (size_t)TPC * (BN / 64) * 8192;
+  const size_t smem = 1024 + S * STAGE;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(wgrad_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(wgrad_tc<BN, TPC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  const int64_t tiles = (int64_t)a.splits * a.g * a.kk * a.tiles_m * a.tiles_n;
-  wgrad_tc<BN><<<(unsigned)tiles, kProd + 32, smem, s>>>(x, dy, a, part);
+  const int64_t tiles = (int64_t)a.splits * a.g * a.tgroups * a.tiles_m * a.tiles_n;
+  wgrad_tc<BN, TPC, S><<<(unsigned)tiles, kProd + 32, smem, s>>>(x, dy, a, part);
   return (int)cudaGetLastError();
+}
+
+int launch_tc_any(int bn, int tpc, const __nv_bfloat16* x, const __nv_bfloat16* dy, const WgArgs& a, float* part,
+                  cudaStream_t s) {
+  if (bn == 256) return launch_tc<256, 1, 4>(x, dy, a, part, s);
+  if (bn == 128) {
+    if (tpc >= 3) return launch_tc<128, 3, 3>(x, dy, a, part, s);
+    if (tpc == 2) return launch_tc<128, 2, 3>(x, dy, a, part, s);
+    return launch_tc<128, 1, 4>(x, dy, a, part, s);
+  }
+  if (tpc >= 3) return launch_tc<64, 3, 4>(x, dy, a, part, s);
+  if (tpc == 2) return launch_tc<64, 2, 4>(x, dy, a, part, s);
+  return launch_tc<64, 1, 4>(x, dy, a, part, s);
 }
 
 }  // namespace
@@ -284,13 +327,14 @@ int launch_wgrad(const LayerInfo& L, const void* x, const void* dy, float* dK, i
     a.per_split = ((a.pixels + a.splits - 1) / a.splits + 63) / 64 * 64;
     a.splits = (int)((a.pixels + a.per_split - 1) / a.per_split);
     const int bn = pick_bn(L);
+    const int tpc = pick_tpc(L);
+    a.tpc = tpc;
+    a.tgroups = (a.kk + tpc - 1) / tpc;
     a.tiles_m = (L.co + 127) / 128;
     a.tiles_n = (L.ci + bn - 1) / bn;
     g_conv_variant = 0;
     float* part = static_cast<float*>(ws);
-    int e = bn == 256 ? launch_tc<256>((const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, a, part, s)
-            : bn == 128 ? launch_tc<128>((const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, a, part, s)
-                        : launch_tc<64>((const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, a, part, s);
+    int e = launch_tc_any(bn, tpc, (const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, a, part, s);
     if (e) return e;
     wgrad_reduce<<<rb, 256, 0, s>>>(part, a, dK);
     return (int)cudaGetLastError();

@@ -59,12 +59,30 @@ struct TcgPhase {
   void* dmaps = nullptr;   // per segment 4 TMA maps {A hi, B hi, A lo, B lo}, then the tile -> desc table
   int* dtile = nullptr;
 };
+// dataflow composition: one (desc, tile) item of any phase, in claim order, with the per-unit counter it
+// waits on (the unit's previous phase complete) and the one it bumps
+struct TcgItem {
+  int32_t desc, local;        // index into the combined descriptor array, tile inside the descriptor
+  int32_t wait_ctr;           // -1: none
+  uint32_t wait_target;
+  int32_t done_ctr, pad_[3];
+};
+
 struct TcComposePlan {
   void* arena = nullptr;
   std::vector<CvtItem> cvt;
   CvtItem* dcvt = nullptr;
   TcgPhase proj, aoc;
   std::vector<TcgPhase> chain;
+  std::vector<int> proj_unit, aoc_unit;       // unit index of every descriptor (dataflow dependencies)
+  std::vector<std::vector<int>> chain_unit;
+  // dataflow: every phase in ONE persistent launch (combined descriptors, segments' TMA maps, items)
+  void* flow_mem = nullptr;
+  TcgDesc* fdesc = nullptr;
+  TcgItem* fitems = nullptr;
+  CUtensorMap* fmaps = nullptr;
+  unsigned* fctr = nullptr;                   // [0] claim counter, then per (unit, phase) completion counters
+  int n_fitems = 0, n_fctr = 0;
 };
 
 namespace {
@@ -565,9 +583,240 @@ __global__ void __launch_bounds__(kTcpThreads, 1) tcg_tma_persist(const TcgDesc*
   if (warp == 1) umma::tmem_dealloc(tmem, 256);
 }
 
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// All composition phases (projectors, every chain substep, RKO (*) BCOP) in ONE persistent launch:
+// (desc, tile) items in phase-major claim order; a tile's producer waits until its unit's previous
+// phase is complete (per-unit monotonic counters, relaxed polls + one acquire fence), the epilogue
+// publishes with a release reduction after the proxy fence.  Units therefore advance independently --
+// the per-phase launches made every phase wait for the slowest unit of the previous one.  The tile
+// pipeline (TMA boxes, 3-pass MMA, 8 epilogue warps) is tcg_tma_persist's.
+__global__ void __launch_bounds__(kTcpThreads, 1) tcg_flow(const TcgDesc* __restrict__ descs,
+                                                           const TcgItem* __restrict__ items, int n_items,
+                                                           const CUtensorMap* __restrict__ maps,
+                                                           unsigned* __restrict__ ctr) {
+  constexpr int TILE = 128 * 128, STAGE = 4 * TILE;
+  extern __shared__ uint8_t smem_raw[];
+  umma::griddep_launch_dependents();
+  uint8_t* smem = umma::align1024_smem(smem_raw);
+  float* Sf = reinterpret_cast<float*>(smem + S * STAGE);
+  __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2], qfull[8], qempty[8];
+  __shared__ int qslot[8];
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 1) umma::tmem_alloc(&tmem_base_sh, 256);
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      umma::mbar_init(&full_bar[i], 1);
+      umma::mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      umma::mbar_init(&tfull_bar[i], 1);
+      umma::mbar_init(&tempty_bar[i], 8);
+    }
+    for (int i = 0; i < 8; ++i) {
+      umma::mbar_init(&qfull[i], 1);
+      umma::mbar_init(&qempty[i], 8);   // the 8 epilogue warps are the last readers of a queue slot
+    }
+    umma::fence_mbar_init();
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  umma::griddep_wait();   // PDL: the cvt kernel's copies and counter reset are complete
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t s0 = umma::smem_u32(smem);
+  if (warp == 0) {
+    // ---------------------------------------------------------------- claim + producer (lanes 0-3)
+    if (lane < 4) {
+      int kb_all = 0;
+      for (int kq = 0;; ++kq) {
+        const int slot = kq & 7;
+        int idx = 0;
+        if (lane == 0) {
+          if (kq >= 8) umma::mbar_wait(&qempty[slot], ((kq >> 3) - 1) & 1);
+          idx = (int)atomicAdd(ctr, 1u);
+          if (idx < n_items) {
+            const TcgItem it = items[idx];
+            if (it.wait_ctr >= 0) {   // the unit's previous phase is complete
+              while (ld_relaxed_u32(ctr + it.wait_ctr) < it.wait_target) __nanosleep(32);
+              asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            }
+          }
+          qslot[slot] = idx < n_items ? idx : -1;
+          umma::mbar_arrive(&qfull[slot]);
+        }
+        idx = __shfl_sync(0xFu, idx, 0);
+        if (idx >= n_items) break;
+        asm volatile("fence.proxy.async.global;" ::: "memory");   // other CTAs' generic writes -> TMA reads
+        const TcgItem it = items[idx];
+        const TcgDesc& d = descs[it.desc];
+        const int m0 = (it.local / d.tiles_n) * 128, n0 = (it.local % d.tiles_n) * 128;
+        const int nkb = (d.K + 63) / 64, nk = nkb * d.seg_count;
+        for (int kb = 0; kb < nk; ++kb, ++kb_all) {
+          const int st = kb_all % S;
+          if (kb_all >= S) umma::mbar_wait(&empty_bar[st], ((kb_all / S) - 1) & 1);
+          const CUtensorMap* mp = maps + 4 * (d.seg_begin + kb / nkb);
+          const int k0 = (kb % nkb) * 64;
+          const uint32_t sa = s0 + st * STAGE;
+          if (lane == 0) umma::mbar_arrive_expect_tx(&full_bar[st], STAGE);
+          __syncwarp(0xFu);
+          umma::tma_load_2d(sa + lane * TILE, mp + lane, &full_bar[st], k0, (lane & 1) ? n0 : m0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      constexpr uint32_t IDESC = umma::idesc_bf16(128, 128);
+      int kb_all = 0, tcount = 0;
+      for (int kq = 0;; ++kq, ++tcount) {
+        const int slot = kq & 7;
+        umma::mbar_wait(&qfull[slot], (kq >> 3) & 1);
+        const int idx = qslot[slot];
+        if (idx < 0) break;
+        const TcgDesc& d = descs[items[idx].desc];
+        const int nk = ((d.K + 63) / 64) * d.seg_count;
+        const int acc = tcount & 1;
+        if (tcount >= 2) umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) - 1) & 1);
+        umma::tc_fence_after();
+        const uint32_t dt = tmem + acc * 128;
+        for (int kb = 0; kb < nk; ++kb, ++kb_all) {
+          const int st = kb_all % S;
+          umma::mbar_wait(&full_bar[st], (kb_all / S) & 1);
+          umma::tc_fence_after();
+          const uint32_t ah = s0 + st * STAGE, bh = ah + TILE, al = ah + 2 * TILE, bl = ah + 3 * TILE;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint64_t dah = umma::sdesc_sw128(ah + 32 * q), dbh = umma::sdesc_sw128(bh + 32 * q);
+            umma::mma_bf16(dt, dah, dbh, IDESC, (kb | q) != 0);
+            umma::mma_bf16(dt, dah, umma::sdesc_sw128(bl + 32 * q), IDESC, 1);
+            umma::mma_bf16(dt, umma::sdesc_sw128(al + 32 * q), dbh, IDESC, 1);
+          }
+          umma::mma_commit(&empty_bar[st]);
+        }
+        umma::mma_commit(&tfull_bar[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------------ epilogue (warps 2-9)
+    const int ew = warp - 2, etid = tid - 64;
+    const int q = warp & 3, sub = ew >> 2, r_own = q * 32 + lane;
+    constexpr int LDF = 36;
+    for (int kq = 0, tcount = 0;; ++kq, ++tcount) {
+      const int slot = kq & 7;
+      umma::mbar_wait(&qfull[slot], (kq >> 3) & 1);
+      const int idx = qslot[slot];
+      if (idx < 0) break;
+      const TcgItem it = items[idx];
+      const TcgDesc d = descs[it.desc];
+      const int m0 = (it.local / d.tiles_n) * 128, n0 = (it.local % d.tiles_n) * 128;
+      const int nk = ((d.K + 63) / 64) * d.seg_count;
+      const bool fvec = d.f && (d.ldf & 3) == 0;
+      const int acc = tcount & 1;
+      umma::mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
+      umma::tc_fence_after();
+#pragma unroll 1
+      for (int h = 0; h < 4; ++h) {
+        {
+          float v[16];
+          umma::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + h * 32 + sub * 16), v);
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            *reinterpret_cast<float4*>(Sf + r_own * LDF + sub * 16 + 4 * t) =
+                nk > 0 ? make_float4(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (h == 3) {
+          umma::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) umma::mbar_arrive(&tempty_bar[acc]);
+        }
+        umma::named_bar_sync(1, 256);
+#pragma unroll 2
+        for (int u = 0; u < 4; ++u) {
+          const int e = etid + 256 * u, r = e >> 3, c4 = (e & 7) * 4;
+          const int i = m0 + r, j0 = n0 + h * 32 + c4;
+          const float4 a = *reinterpret_cast<const float4*>(Sf + r * LDF + c4);
+          const float accv[4] = {a.x, a.y, a.z, a.w};
+          float o[4], o2[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const bool ok = i < d.M && j0 + k < d.N;
+            const float dg = (i == j0 + k) ? 1.f : 0.f;
+            o[k] = ok ? fmaf(d.alpha, accv[k], d.diag * dg) : 0.f;
+            o2[k] = ok ? fmaf(d.alpha2, accv[k], d.diag2 * dg) : 0.f;
+          }
+          if (d.f && i < d.M && j0 < d.N) {
+            float* dst = d.f + (int64_t)i * d.ldf + j0;
+            if (fvec && j0 + 3 < d.N) {
+              *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                if (j0 + k < d.N) dst[k] = o[k];
+            }
+          }
+          if (i < d.M && j0 < d.ldo) {
+            const int64_t bo = (int64_t)i * d.ldo + j0;
+            uint2 hv, lv;
+            if (d.oh) {
+              split4(o[0], o[1], o[2], o[3], hv, lv);
+              *reinterpret_cast<uint2*>(d.oh + bo) = hv;
+              *reinterpret_cast<uint2*>(d.ol + bo) = lv;
+            }
+            if (d.o2h) {
+              split4(o2[0], o2[1], o2[2], o2[3], hv, lv);
+              *reinterpret_cast<uint2*>(d.o2h + bo) = hv;
+              *reinterpret_cast<uint2*>(d.o2l + bo) = lv;
+            }
+          }
+          if (d.th) *reinterpret_cast<float4*>(Sf + r * LDF + c4) = make_float4(o[0], o[1], o[2], o[3]);
+        }
+        umma::named_bar_sync(1, 256);
+        if (d.th) {
+#pragma unroll 1
+          for (int u = 0; u < 2; ++u) {
+            const int e = etid + 256 * u, cl = e & 31, i8 = (e >> 5) * 8;
+            const int jn = n0 + h * 32 + cl, i0 = m0 + i8;
+            float x[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) x[t] = Sf[(i8 + t) * LDF + cl];
+            if (jn < d.N && i0 < d.ldt) {
+              uint2 h0, l0, h1, l1;
+              split4(x[0], x[1], x[2], x[3], h0, l0);
+              split4(x[4], x[5], x[6], x[7], h1, l1);
+              const int64_t o = (int64_t)jn * d.ldt + i0;
+              *reinterpret_cast<uint4*>(d.th + o) = make_uint4(h0.x, h0.y, h1.x, h1.y);
+              *reinterpret_cast<uint4*>(d.tl + o) = make_uint4(l0.x, l0.y, l1.x, l1.y);
+            }
+          }
+          umma::named_bar_sync(1, 256);
+        }
+      }
+      // ---- item done: publish this tile's writes, bump the unit's counter, free the queue slot
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      umma::named_bar_sync(1, 256);
+      if (ew == 0 && lane == 0)   // release (cumulative over the barrier) orders every epilogue warp's writes
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr + it.done_ctr) : "memory");
+      if (lane == 0) umma::mbar_arrive(&qempty[slot]);
+    }
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) umma::tmem_dealloc(tmem, 256);
+}
+
 // FP32 ortho -> BF16 hi/lo copies (row-major padded, or the RKO phase split).
 // CTA = rows r = blockIdx.x + k gridDim.x of item blockIdx.y; 32-bit index math.
-__global__ void __launch_bounds__(256) cvt_kernel(const CvtItem* __restrict__ items, const float* __restrict__ ortho) {
+__global__ void __launch_bounds__(256) cvt_kernel(const CvtItem* __restrict__ items, const float* __restrict__ ortho,
+                                                  unsigned* __restrict__ zero, int nzero) {
+  if (zero && blockIdx.x == 0 && blockIdx.y == 0)   // re-arm the dataflow counters of the launch that follows
+    for (int i = threadIdx.x; i < nzero; i += blockDim.x) zero[i] = 0u;
   umma::griddep_launch_dependents();
   umma::griddep_wait();
   const CvtItem it = items[blockIdx.y];
@@ -662,11 +911,10 @@ int launch_phase(const TcgPhase& ph, cudaStream_t s) {
 // TMA maps of every segment operand (K extent x rows, row stride ld) plus the
 // tile -> descriptor table; phases whose operands cannot be described by TMA
 // (misaligned pointer or stride) keep the cp.async kernel.
-bool build_phase_maps(TcgPhase& ph) {
-  if (!ph.tiles) return true;
+bool host_phase_maps(const TcgPhase& ph, std::vector<CUtensorMap>& maps) {
   auto enc = tensor_map_encoder();
   if (!enc) return false;
-  std::vector<CUtensorMap> maps(4 * ph.s.size());
+  maps.assign(4 * ph.s.size(), CUtensorMap{});
   std::vector<int> seg_desc(ph.s.size(), -1);
   for (size_t di = 0; di < ph.d.size(); ++di)
     for (int k = 0; k < ph.d[di].seg_count; ++k) seg_desc[ph.d[di].seg_begin + k] = (int)di;
@@ -689,6 +937,13 @@ bool build_phase_maps(TcgPhase& ph) {
         return false;
     }
   }
+  return true;
+}
+
+bool build_phase_maps(TcgPhase& ph) {
+  if (!ph.tiles) return true;
+  std::vector<CUtensorMap> maps;
+  if (!host_phase_maps(ph, maps)) return false;
   std::vector<int> tile;
   for (size_t di = 0; di < ph.d.size(); ++di) {
     const TcgDesc& d = ph.d[di];
@@ -723,6 +978,85 @@ TcgDesc mkdesc(int M, int N, int K) {
 }
 
 }  // namespace
+
+// The dataflow composition (tcg_flow): every phase's descriptors, segments' TMA maps and tiles combined,
+// items in phase-major order (inside a phase the units with the most K work first), one completion
+// counter per (unit, phase).  Phase order: projectors, chain substeps, RKO (*) BCOP.  A chain substep of
+// a unit waits for all of the unit's tiles of the previous stage (its projectors for substep 0), the AOC
+// tiles for the unit's last substep.  Leaves T.flow_mem null (per-phase launches) if a map cannot be built.
+static void build_compose_flow(Plan& P, TcComposePlan& T) {
+  std::vector<const TcgPhase*> phs;
+  std::vector<const std::vector<int>*> units;
+  phs.push_back(&T.proj); units.push_back(&T.proj_unit);
+  for (size_t t = 0; t < T.chain.size(); ++t) { phs.push_back(&T.chain[t]); units.push_back(&T.chain_unit[t]); }
+  phs.push_back(&T.aoc); units.push_back(&T.aoc_unit);
+  const int nph = (int)phs.size(), nu = (int)P.comp_units.size();
+  std::vector<TcgDesc> desc;
+  std::vector<CUtensorMap> maps;
+  std::vector<int> desc0(nph, 0);
+  int seg0 = 0;
+  for (int p = 0; p < nph; ++p) {
+    desc0[p] = (int)desc.size();
+    std::vector<CUtensorMap> m;
+    if (phs[p]->tiles && !host_phase_maps(*phs[p], m)) return;
+    for (TcgDesc d : phs[p]->d) { d.seg_begin += seg0; desc.push_back(d); }
+    maps.insert(maps.end(), m.begin(), m.end());
+    seg0 += (int)phs[p]->s.size();
+    if (phs[p]->tiles && (int)m.size() != 4 * (int)phs[p]->s.size()) return;
+  }
+  if (desc.empty()) return;
+  // tiles per (unit, phase), the last phase index with tiles per unit (chain depth differs across units)
+  std::vector<int> cnt((size_t)nu * nph, 0);
+  for (int p = 0; p < nph; ++p)
+    for (size_t di = 0; di < phs[p]->d.size(); ++di) {
+      const TcgDesc& d = phs[p]->d[di];
+      cnt[(size_t)(*units[p])[di] * nph + p] += ((d.M + 127) / 128) * ((d.N + 127) / 128);
+    }
+  auto ctr_of = [&](int u, int p) { return 1 + u * nph + p; };
+  std::vector<TcgItem> items;
+  for (int p = 0; p < nph; ++p) {
+    std::vector<int> order(phs[p]->d.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      return (int64_t)phs[p]->d[a].K * phs[p]->d[a].seg_count > (int64_t)phs[p]->d[b].K * phs[p]->d[b].seg_count;
+    });
+    for (int di : order) {
+      const TcgDesc& d = phs[p]->d[di];
+      const int u = (*units[p])[di];
+      int wp = -1;   // the unit's previous phase with tiles
+      for (int q = p - 1; q >= 0; --q)
+        if (cnt[(size_t)u * nph + q] > 0) { wp = q; break; }
+      const int nt = ((d.M + 127) / 128) * ((d.N + 127) / 128);
+      for (int t = 0; t < nt; ++t) {
+        TcgItem it{};
+        it.desc = desc0[p] + di;
+        it.local = t;
+        it.wait_ctr = wp >= 0 ? ctr_of(u, wp) : -1;
+        it.wait_target = wp >= 0 ? (uint32_t)cnt[(size_t)u * nph + wp] : 0u;
+        it.done_ctr = ctr_of(u, p);
+        items.push_back(it);
+      }
+    }
+  }
+  for (auto& d : desc) d.tiles_n = (d.N + 127) / 128;
+  const int nctr = 1 + nu * nph;
+  const size_t bd = desc.size() * sizeof(TcgDesc), bi = items.size() * sizeof(TcgItem);
+  const size_t bm = maps.size() * sizeof(CUtensorMap), bc = (size_t)nctr * sizeof(unsigned);
+  auto al = [](size_t x) { return (x + 127) / 128 * 128; };
+  char* mem = nullptr;
+  if (cudaMalloc(&mem, al(bm) + al(bd) + al(bi) + al(bc)) != cudaSuccess) { cudaGetLastError(); return; }
+  T.fmaps = reinterpret_cast<CUtensorMap*>(mem);
+  T.fdesc = reinterpret_cast<TcgDesc*>(mem + al(bm));
+  T.fitems = reinterpret_cast<TcgItem*>(mem + al(bm) + al(bd));
+  T.fctr = reinterpret_cast<unsigned*>(mem + al(bm) + al(bd) + al(bi));
+  cudaMemcpy(T.fmaps, maps.data(), bm, cudaMemcpyHostToDevice);
+  cudaMemcpy(T.fdesc, desc.data(), bd, cudaMemcpyHostToDevice);
+  cudaMemcpy(T.fitems, items.data(), bi, cudaMemcpyHostToDevice);
+  cudaMemset(T.fctr, 0, bc);
+  T.flow_mem = mem;
+  T.n_fitems = (int)items.size();
+  T.n_fctr = nctr;
+}
 
 orth_status_t build_compose_tc(Plan& P) {
   auto* T = new TcComposePlan();
@@ -801,8 +1135,15 @@ orth_status_t build_compose_tc(Plan& P) {
     }
   }
   // ---- projectors P = U U^T and I - P
+  std::vector<int> unit_of_mat(P.mats.size(), -1);
+  for (size_t ui = 0; ui < P.comp_units.size(); ++ui) {
+    const LayerInfo& L = P.layers[P.comp_units[ui].layer];
+    const int base = L.first_mat + P.comp_units[ui].group * L.mats_per_group;
+    for (int j = 0; j < L.mats_per_group; ++j) unit_of_mat[base + j] = (int)ui;
+  }
   for (size_t i = 0; i < P.mats.size(); ++i) {
     if (pb[i].h < 0) continue;
+    T->proj_unit.push_back(unit_of_mat[i]);
     const MatInfo& U = P.mats[i];
     const int c = (int)U.m;
     TcgDesc d = mkdesc(c, c, (int)U.n);
@@ -820,6 +1161,7 @@ orth_status_t build_compose_tc(Plan& P) {
   for (auto& u : P.comp_units)
     if (u.ping >= 0) max_sub = std::max(max_sub, 2 * (P.layers[u.layer].kp - 1));
   T->chain.assign(max_sub, TcgPhase{});
+  T->chain_unit.assign(max_sub, std::vector<int>());
   for (size_t ui = 0; ui < P.comp_units.size(); ++ui) {
     const CompUnit& u = P.comp_units[ui];
     if (u.ping < 0) continue;
@@ -861,6 +1203,7 @@ orth_status_t build_compose_tc(Plan& P) {
             d.ldt = b.ldt;
           }
           ph.d.push_back(d);
+          T->chain_unit[t].push_back((int)ui);
         }
       kh = oh; kw = ow;
       in_h = out_h; in_l = out_l;
@@ -893,6 +1236,7 @@ orth_status_t build_compose_tc(Plan& P) {
         d.f = comp + u.fin + (int64_t)(p * k + q) * L.co * L.ci;
         d.ldf = L.ci;
         T->aoc.d.push_back(d);
+        T->aoc_unit.push_back((int)ui);
       }
   }
   // ---- upload descriptors
@@ -920,6 +1264,8 @@ orth_status_t build_compose_tc(Plan& P) {
     for (auto& ph : T->chain)
       if (!build_phase_maps(ph)) { if (ph.dmaps) cudaFree(ph.dmaps); ph.dmaps = nullptr; }
   }
+  static const bool no_flow = std::getenv("ORTH_COMPOSE_PHASED") != nullptr;   // A/B: per-phase launches
+  if (!no_tma && !no_flow) build_compose_flow(P, *T);
   return ORTH_OK;
 }
 
@@ -928,6 +1274,7 @@ void free_compose_tc(Plan& P) {
   if (!T) return;
   if (T->arena) cudaFree(T->arena);
   if (T->dcvt) cudaFree(T->dcvt);
+  if (T->flow_mem) cudaFree(T->flow_mem);
   for (TcgPhase* ph : {&T->proj, &T->aoc}) {
     if (ph->dd) cudaFree(ph->dd);
     if (ph->ds) cudaFree(ph->ds);
@@ -949,9 +1296,26 @@ int launch_compose_tc(Plan& P, const float* ortho, void* stream) {
     int maxm = 1;
     for (auto& c : T->cvt) maxm = std::max(maxm, c.m);
     dim3 grid((unsigned)std::min(maxm, 32), (unsigned)T->cvt.size());   // fewer, fuller CTAs
-    launch_pdl(cvt_kernel, grid, dim3(256), 0, s, (const CvtItem*)T->dcvt, ortho);
+    launch_pdl(cvt_kernel, grid, dim3(256), 0, s, (const CvtItem*)T->dcvt, ortho, T->fctr, T->n_fctr);
     P.launches++;
     if (int e = (int)cudaGetLastError()) return e;
+  }
+  if (T->flow_mem) {   // every phase in one dataflow launch
+    const size_t smem_p = 1024 + (size_t)S * 4 * 128 * 128 + (size_t)kTcpSf * 4;
+    static bool attr_f = false;
+    if (!attr_f) {
+      cudaFuncSetAttribute(tcg_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
+      attr_f = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::min(T->n_fitems, sms);
+    if (T->cvt.empty()) cudaMemsetAsync(T->fctr, 0, (size_t)T->n_fctr * sizeof(unsigned), s);
+    launch_pdl(tcg_flow, dim3(grid), dim3(kTcpThreads), smem_p, s, (const TcgDesc*)T->fdesc,
+               (const TcgItem*)T->fitems, T->n_fitems, (const CUtensorMap*)T->fmaps, T->fctr);
+    P.launches++;
+    return (int)cudaGetLastError();
   }
   int e = launch_phase(T->proj, s);
   P.launches += T->proj.tiles ? 1 : 0;

@@ -22,8 +22,9 @@
 //
 // Kernels: symbol_kernel (one thread per B element, taps looped),
 // gram_kernel (64 x 64 complex tile per CTA, k in chunks of 16 staged in
-// shared memory, 4 x 4 complex accumulators per thread), stats_kernel (one CTA
-// per (group, frequency): |E|_F in a fixed order, then the power iteration).
+// shared memory, 4 x 4 complex accumulators per thread), power_step (one launch
+// per power iteration over S/32 x (groups x frequencies) CTAs; the first also
+// writes the |E|_F row-block partials), cert_final (fixed-order sums).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -156,56 +157,79 @@ __device__ double block_sum_d(double v, double* red) {
   return red[32];
 }
 
-// one CTA per (group, frequency): |E|_F, then `iters` power iterations z <- E z / |E z| from a fixed start
-// (E is Hermitian: the iteration converges to its largest |eigenvalue| = |E|_2); est = |E z| <= |E|_2
-__global__ void __launch_bounds__(256) stats_kernel(const double2* __restrict__ E, CertGeo G, int iters,
-                                                    double2* __restrict__ zbuf, double* __restrict__ out) {
-  __shared__ double red[33];
+// Power iteration z <- E z / |E z| from a fixed start (E is Hermitian: it converges to its largest
+// |eigenvalue| = |E|_2; est = |E z| <= |E|_2), one launch per iteration so that every (group, frequency)
+// matvec is spread over S / 32 CTAs (a CTA per frequency streams E from L2 at a few GB/s).  y_in -> y_out:
+// each CTA normalises y_in itself (z = y_in / |y_in|, staged in shared memory), then a warp per row
+// (lanes stride the row: coalesced; fixed-order shuffle reduction).  On the first launch (frob = 1) the
+// CTA also writes its rows' sum |E_rj|^2 -- the |E|_F partial, summed in row-block order by cert_final.
+constexpr int kRowsPerCta = 32;
+__global__ void __launch_bounds__(256) power_start(CertGeo G, double2* __restrict__ y0) {
   const int64_t gf = blockIdx.x;
-  const int S = G.S;
-  const double2* Eg = E + gf * (int64_t)S * S;
-  double2* z = zbuf + gf * (int64_t)2 * S;
-  double2* y = z + S;
-  double f = 0.0;
-  for (int64_t e = threadIdx.x; e < (int64_t)S * S; e += blockDim.x) {
-    const double2 v = Eg[e];
-    f += v.x * v.x + v.y * v.y;
-  }
-  f = block_sum_d(f, red);
-  // fixed start vector (not orthogonal to any eigenvector with probability one for real data)
-  double nz = 0.0;
-  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+  for (int i = threadIdx.x; i < G.S; i += blockDim.x) {
     const double v = 1.0 + 0.25 * (double)((i * 7919) % 97) / 97.0;
-    z[i] = make_double2(v, 0.1 * (double)((i * 104729) % 89) / 89.0);
-    nz += z[i].x * z[i].x + z[i].y * z[i].y;
+    y0[gf * G.S + i] = make_double2(v, 0.1 * (double)((i * 104729) % 89) / 89.0);
   }
-  nz = block_sum_d(nz, red);
-  double inv = nz > 0.0 ? rsqrt(nz) : 0.0;
-  for (int i = threadIdx.x; i < S; i += blockDim.x) z[i] = make_double2(z[i].x * inv, z[i].y * inv);
+}
+
+__global__ void __launch_bounds__(256) power_step(const double2* __restrict__ E, CertGeo G, const double2* __restrict__ yin,
+                                                  double2* __restrict__ yout, double* __restrict__ frob_part, int frob,
+                                                  int mv) {
+  extern __shared__ double2 zs[];
+  __shared__ double red[33];
+  const int64_t gf = blockIdx.y;
+  const int S = G.S, rb = blockIdx.x, nrb = gridDim.x;
+  const double2* Eg = E + gf * (int64_t)S * S;
+  const double2* y = yin + gf * S;
+  double n = 0.0;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) n += y[i].x * y[i].x + y[i].y * y[i].y;
+  n = block_sum_d(n, red);
+  const double inv = n > 0.0 ? rsqrt(n) : 0.0;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) zs[i] = make_double2(y[i].x * inv, y[i].y * inv);
   __syncthreads();
-  double est = 0.0;
-  for (int it = 0; it < iters; ++it) {
-    double ny = 0.0;
-    for (int r = threadIdx.x; r < S; r += blockDim.x) {   // y = E z (row r: sum_j E[r][j] z[j])
-      const double2* row = Eg + (int64_t)r * S;
-      double re = 0.0, im = 0.0;
-      for (int j = 0; j < S; ++j) {
-        const double2 a = row[j], b = z[j];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double f = 0.0;
+  for (int r = rb * kRowsPerCta + warp; r < min(S, (rb + 1) * kRowsPerCta); r += 8) {
+    const double2* row = Eg + (int64_t)r * S;
+    double re = 0.0, im = 0.0;
+    for (int j = lane; j < S; j += 32) {
+      const double2 a = row[j];
+      if (frob) f += a.x * a.x + a.y * a.y;
+      if (mv) {
+        const double2 b = zs[j];
         re += a.x * b.x - a.y * b.y;
         im += a.x * b.y + a.y * b.x;
       }
-      y[r] = make_double2(re, im);
-      ny += re * re + im * im;
     }
-    ny = block_sum_d(ny, red);
-    est = sqrt(ny);
-    inv = ny > 0.0 ? rsqrt(ny) : 0.0;
-    for (int i = threadIdx.x; i < S; i += blockDim.x) z[i] = make_double2(y[i].x * inv, y[i].y * inv);
-    __syncthreads();
+    if (mv) {
+      for (int o = 16; o > 0; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
+      }
+      if (lane == 0) yout[gf * S + r] = make_double2(re, im);
+    }
   }
+  if (frob) {
+    f = block_sum_d(f, red);
+    if (threadIdx.x == 0) frob_part[gf * nrb + rb] = f;
+  }
+}
+
+__global__ void __launch_bounds__(256) cert_final(CertGeo G, int nrb, const double* __restrict__ frob_part,
+                                                  const double2* __restrict__ ylast, double* __restrict__ out) {
+  __shared__ double red[33];
+  const int64_t gf = blockIdx.x;
+  double n = 0.0;
+  for (int i = threadIdx.x; i < G.S; i += blockDim.x) {
+    const double2 v = ylast[gf * G.S + i];
+    n += v.x * v.x + v.y * v.y;
+  }
+  n = block_sum_d(n, red);
   if (threadIdx.x == 0) {
+    double f = 0.0;
+    for (int b = 0; b < nrb; ++b) f += frob_part[gf * nrb + b];
     out[gf * 2] = sqrt(f);
-    out[gf * 2 + 1] = est;
+    out[gf * 2 + 1] = sqrt(n);
   }
 }
 
@@ -232,7 +256,8 @@ int64_t certify_workspace_bytes(const LayerInfo& L, int H, int W) {
   CertGeo G;
   if (!cert_geo(L, H, W, G)) return -1;
   const int64_t gf = (int64_t)G.g * G.F;
-  return 16 * gf * ((int64_t)G.Kd * G.S + (int64_t)G.S * G.S + 2 * (int64_t)G.S) + 256;
+  const int64_t nrb = (G.S + kRowsPerCta - 1) / kRowsPerCta;
+  return 16 * gf * ((int64_t)G.Kd * G.S + (int64_t)G.S * G.S + 2 * (int64_t)G.S) + 8 * gf * nrb + 256;
 }
 
 int launch_certify(const LayerInfo& L, const float* kernel, int H, int W, int iters, void* ws, double* out,
@@ -249,7 +274,24 @@ int launch_certify(const LayerInfo& L, const float* kernel, int H, int W, int it
   symbol_kernel<<<blocks, 256, 0, s>>>(kernel, G, B);
   const int tiles = (G.S + TS - 1) / TS;
   gram_kernel<<<dim3((unsigned)(tiles * (tiles + 1) / 2), (unsigned)gf), 256, 0, s>>>(B, G, E);
-  stats_kernel<<<(unsigned)gf, 256, 0, s>>>(E, G, iters, Z, out);
+  const int nrb = (G.S + kRowsPerCta - 1) / kRowsPerCta;
+  double* fpart = reinterpret_cast<double*>(Z + gf * (int64_t)2 * G.S);
+  double2* y[2] = {Z, Z + gf * (int64_t)G.S};
+  const size_t zsm = (size_t)G.S * 16;
+  if (zsm > 200 * 1024) return (int)cudaErrorInvalidValue;   // S > 12800: z does not fit shared memory
+  if (zsm > 48 * 1024) cudaFuncSetAttribute(power_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);
+  power_start<<<(unsigned)gf, 256, 0, s>>>(G, y[0]);
+  // iters == 0: one frob-only pass; |E z| is then reported for the start vector's zero image (0)
+  if (iters <= 0) {
+    power_step<<<dim3((unsigned)nrb, (unsigned)gf), 256, zsm, s>>>(E, G, y[0], y[1], fpart, 1, 0);
+    cudaMemsetAsync(y[1], 0, (size_t)gf * G.S * 16, s);
+    cert_final<<<(unsigned)gf, 256, 0, s>>>(G, nrb, fpart, y[1], out);
+    return (int)cudaGetLastError();
+  }
+  for (int it = 0; it < iters; ++it)
+    power_step<<<dim3((unsigned)nrb, (unsigned)gf), 256, zsm, s>>>(E, G, y[it & 1], y[(it + 1) & 1], fpart,
+                                                                    it == 0, 1);
+  cert_final<<<(unsigned)gf, 256, 0, s>>>(G, nrb, fpart, y[iters & 1], out);
   return (int)cudaGetLastError();
 }
 

@@ -75,7 +75,7 @@ struct TcConvArgs {
 constexpr int NPROD = 256;                 // producer threads (warps 0-7)
 constexpr int MMA_WARP = 8;
 constexpr int NTHREADS = NPROD + 32 + 128;
-constexpr int MAX_TAPS = 49;               // k <= 7
+constexpr int MAX_TAPS = 169;              // k <= 13 (the SOC explicit exponential: 1 + 6 (3 - 1))
 
 __device__ __forceinline__ int wrapi(int x, int n) {
   x %= n;
@@ -873,7 +873,7 @@ int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, cons
 #else
   const bool want_pair = false;
 #endif
-  const bool pair = want_pair && cs_env < 0 && bn >= 128 && min_tiles >= 2;
+  const bool pair = want_pair && cs_env < 0 && bn >= 128 && min_tiles >= 2 && a.k <= 7;
   if (pair) cs = 2;
   a.cs = cs;
   int c0 = 0;
@@ -897,6 +897,14 @@ int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, cons
                     : launch_pair<128, 6>(in, w, w_rows, bias, out, a, s);
   }
 #endif
+  if (a.k > 7) {   // the pixel table (k^2 x 128 x 4 B, 86.5 KB at 13 x 13) leaves room for fewer stages
+    switch (bn) {
+      case 256: return launch_ws<256, 2>(in, w, w_rows, bias, out, a, s);
+      case 128: return launch_ws<128, 4>(in, w, w_rows, bias, out, a, s);
+      case 64: return launch_ws<64, 5>(in, w, w_rows, bias, out, a, s);
+      default: return launch_ws<32, 6>(in, w, w_rows, bias, out, a, s);
+    }
+  }
   switch (bn) {
     // deepest ring that fits 227 KB with the 3x3 table (4.6 KB); larger kernels take the shallower one
     case 256: return launch_ws<256, 4>(in, w, w_rows, bias, out, a, s);

@@ -206,10 +206,8 @@ __global__ void __launch_bounds__(256) wgrad_reduce(const float* __restrict__ pa
   }
 }
 
-// SIMT weight gradient over pixel splits: CTA (split, element block) accumulates 256 dK elements (one
-// per thread) over its pixel range, staging the range's dy rows of the block's output channels and the
-// tap-shifted x values in shared memory is unnecessary at these sizes -- each thread walks the pixels in
-// order (fixed order, deterministic); the splits are then reduced by wgrad_reduce_simt in split order.
+// SIMT weight gradient over pixel splits: thread = one dK element, walking its split's pixels in order
+// (fixed order, deterministic); the splits are then reduced by wgrad_reduce_simt in split order.
 template <typename T>
 __global__ void __launch_bounds__(256) wgrad_simt(const T* __restrict__ x, const T* __restrict__ dy, WgArgs a,
                                                   float* __restrict__ part) {
@@ -217,11 +215,13 @@ __global__ void __launch_bounds__(256) wgrad_simt(const T* __restrict__ x, const
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int split = blockIdx.y;
   if (e >= total) return;
-  const int t = (int)(e % a.kk);
-  int64_t r = e / a.kk;
+  // element order e = ((grp kk + t) ci + i) co + o: a warp shares (grp, t, i) -- one broadcast x value per
+  // pixel -- and reads 32 consecutive dy channels (coalesced)
+  const int o = (int)(e % a.co);
+  int64_t r = e / a.co;
   const int i = (int)(r % a.ci); r /= a.ci;
-  const int o = (int)(r % a.co);
-  const int grp = (int)(r / a.co);
+  const int t = (int)(r % a.kk);
+  const int grp = (int)(r / a.kk);
   const int ta = t / a.k, tb = t - ta * a.k;
   const int64_t p0 = (int64_t)split * a.per_split, p1 = min(a.pixels, p0 + a.per_split);
   float acc = 0.f;
@@ -230,7 +230,62 @@ __global__ void __launch_bounds__(256) wgrad_simt(const T* __restrict__ x, const
     if (ip < 0) continue;
     acc = fmaf((float)dy[p * a.Co + (int64_t)grp * a.co + o], (float)x[ip * a.Ci + (int64_t)grp * a.ci + i], acc);
   }
-  part[(int64_t)split * total + e] = acc;
+  if (a.splits > 1) part[(int64_t)split * total + e] = acc;
+  else part[(((int64_t)grp * a.co + o) * a.ci + i) * a.kk + t] = acc;   // straight into dK
+}
+
+// Small-kernel SIMT weight gradient (the RGB stem: c_in = 3 is not tensor-core aligned): the per-group
+// element count E = co ci k^2 <= 4096 fits 256 threads x 16 registers.  A persistent CTA walks 64-pixel
+// chunks (chunk = blockIdx.x + j gridDim.x, in order), staging each chunk's dy rows and tap-shifted x
+// values in shared memory; thread tid owns elements e = tid + 256 j (order ((t ci + i) co + o): a warp
+// reads one broadcast x value and consecutive dy channels).  One partial per CTA, reduced in CTA order.
+constexpr int kSmallP = 64, kSmallJ = 16;
+template <typename T>
+__global__ void __launch_bounds__(256) wgrad_simt_small(const T* __restrict__ x, const T* __restrict__ dy, WgArgs a,
+                                                        float* __restrict__ part) {
+  extern __shared__ float sm[];
+  const int grp = blockIdx.y;
+  const int tci = a.kk * a.ci, E = a.co * tci;
+  float* dys = sm;                       // [kSmallP][co]
+  float* xs = sm + kSmallP * a.co;       // [kSmallP][kk ci]
+  float acc[kSmallJ];
+  int od[kSmallJ], ox[kSmallJ];   // per owned element: its dy channel and x column (hoisted divisions)
+#pragma unroll
+  for (int j = 0; j < kSmallJ; ++j) {
+    acc[j] = 0.f;
+    const int e = threadIdx.x + 256 * j, ti = e / a.co;
+    od[j] = e - ti * a.co;
+    ox[j] = ti;
+  }
+  const int64_t chunks = (a.pixels + kSmallP - 1) / kSmallP;
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int64_t p0 = c * kSmallP;
+    const int np = (int)(a.pixels - p0 < kSmallP ? a.pixels - p0 : kSmallP);
+    for (int q = threadIdx.x; q < kSmallP * a.co; q += blockDim.x) {
+      const int pp = q / a.co, o = q - pp * a.co;
+      dys[q] = pp < np ? (float)dy[(p0 + pp) * a.Co + (int64_t)grp * a.co + o] : 0.f;
+    }
+    for (int q = threadIdx.x; q < kSmallP * tci; q += blockDim.x) {
+      const int pp = q / tci, r = q - pp * tci, t = r / a.ci, i = r - t * a.ci;
+      const int64_t ip = pp < np ? in_pixel(a, p0 + pp, t / a.k, t % a.k) : -1;
+      xs[q] = ip >= 0 ? (float)x[ip * a.Ci + (int64_t)grp * a.ci + i] : 0.f;
+    }
+    __syncthreads();
+    for (int pp = 0; pp < np; ++pp) {
+      const float* dr = dys + pp * a.co;
+      const float* xr = xs + pp * tci;
+#pragma unroll
+      for (int j = 0; j < kSmallJ; ++j)
+        if (threadIdx.x + 256 * j < E) acc[j] = fmaf(dr[od[j]], xr[ox[j]], acc[j]);
+    }
+    __syncthreads();
+  }
+  float* out = part + ((int64_t)blockIdx.x * a.g + grp) * E;
+#pragma unroll
+  for (int j = 0; j < kSmallJ; ++j) {
+    const int e = threadIdx.x + 256 * j;
+    if (e < E) out[e] = acc[j];
+  }
 }
 
 __global__ void __launch_bounds__(256) wgrad_reduce_simt(const float* __restrict__ part, WgArgs a,
@@ -239,7 +294,12 @@ __global__ void __launch_bounds__(256) wgrad_reduce_simt(const float* __restrict
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     float acc = 0.f;
     for (int sp = 0; sp < a.splits; ++sp) acc += part[sp * total + e];
-    dK[e] = acc;
+    const int o = (int)(e % a.co);
+    int64_t r = e / a.co;
+    const int i = (int)(r % a.ci); r /= a.ci;
+    const int t = (int)(r % a.kk);
+    const int grp = (int)(r / a.kk);
+    dK[(((int64_t)grp * a.co + o) * a.ci + i) * a.kk + t] = acc;
   }
 }
 
@@ -302,8 +362,18 @@ int launch_tc_any(int bn, int tpc, const __nv_bfloat16* x, const __nv_bfloat16* 
 
 }  // namespace
 
+// the small-kernel SIMT path: E <= 4096 elements per group, staging <= 96 KB
+static bool small_ok(const LayerInfo& L) {
+  return (int64_t)L.co * L.ci * L.k * L.k <= 256 * kSmallJ && (int64_t)kSmallP * (L.co + L.k * L.k * L.ci) * 4 <= 96 * 1024;
+}
+static int small_ctas(const LayerInfo& L, int64_t pixels) {
+  const int64_t chunks = (pixels + kSmallP - 1) / kSmallP;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (8 * 148 + L.g - 1) / L.g));
+}
+
 // SIMT pixel splits: enough CTAs for ~4 waves, >= 64 pixels per split
 static int simt_splits(const LayerInfo& L, int64_t pixels) {
+  if (small_ok(L)) return small_ctas(L, pixels);
   const int64_t blocks = ((int64_t)L.g * L.co * L.ci * L.k * L.k + 255) / 256;
   int64_t sp = std::max<int64_t>(1, (4 * 148 + blocks - 1) / blocks);
   sp = std::min<int64_t>(sp, std::max<int64_t>(1, pixels / 64));
@@ -340,6 +410,21 @@ int launch_wgrad(const LayerInfo& L, const void* x, const void* dy, float* dK, i
     return (int)cudaGetLastError();
   }
   g_conv_variant = ORTH_CV_SIMT;
+  if (small_ok(L) && ws && ws_bytes >= wgrad_workspace_bytes(L, N, Ho, Wo, io)) {
+    a.splits = small_ctas(L, a.pixels);
+    const size_t smem = (size_t)kSmallP * (L.co + a.kk * L.ci) * 4;
+    const dim3 grid((unsigned)a.splits, (unsigned)L.g);
+    float* part = static_cast<float*>(ws);
+    if (io == ORTH_BF16) {
+      cudaFuncSetAttribute(wgrad_simt_small<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      wgrad_simt_small<__nv_bfloat16><<<grid, 256, smem, s>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, a, part);
+    } else {
+      cudaFuncSetAttribute(wgrad_simt_small<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      wgrad_simt_small<float><<<grid, 256, smem, s>>>((const float*)x, (const float*)dy, a, part);
+    }
+    wgrad_reduce_simt<<<rb, 256, 0, s>>>(part, a, dK);
+    return (int)cudaGetLastError();
+  }
   a.splits = simt_splits(L, a.pixels);
   if (a.splits > 1 && (!ws || ws_bytes < (int64_t)a.splits * L.kernel_numel * 4)) a.splits = 1;
   a.per_split = (a.pixels + a.splits - 1) / a.splits;

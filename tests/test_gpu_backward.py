@@ -23,6 +23,9 @@ WG_CASES = [  # (ci, co, k, s, d, g, mode, H, kind, N)
     (1024, 1024, 3, 1, 2, 32, "circular", 8, "conv", 2), (96, 80, 3, 2, 1, 1, "zeros", 9, "conv", 2),
     (64, 64, 3, 2, 1, 1, "circular", 8, "convT", 2), (512, 512, 3, 1, 1, 1, "circular", 4, "conv", 16),
     (3, 64, 4, 4, 1, 1, "circular", 16, "conv", 2), (16, 16, 5, 1, 1, 1, "zeros", 9, "conv", 2),
+    # small-kernel SIMT path (E = co ci k^2 <= 4096 per group): grouped, ragged 64-pixel chunks, 7 x 7 zeros
+    (8, 8, 3, 2, 1, 2, "zeros", 9, "conv", 3), (3, 24, 7, 2, 1, 1, "zeros", 15, "conv", 3),
+    (3, 64, 4, 4, 1, 1, "circular", 224, "conv", 3),
 ]
 
 

@@ -210,6 +210,11 @@ CONV_CASES = [  # (ci, co, k, s, d, g, mode, H, kind)
     (128, 128, 3, 1, 1, 1, "circular", 7, "conv"), (256, 256, 3, 1, 1, 2, "circular", 8, "conv"),
     (128, 128, 3, 1, 1, 1, "zeros", 30, "conv"), (512, 512, 3, 1, 1, 1, "circular", 5, "convT"),
     (1024, 1024, 3, 1, 2, 1, "circular", 8, "conv"), (96, 128, 3, 1, 1, 1, "circular", 6, "conv"),
+    # large kernels on the gather path (8 <= k <= 13: the SOC explicit exponential's k_eff = 13; shallower
+    # rings around the 86.5 KB pixel table), every N-tile width, strided and adjoint
+    (64, 64, 13, 1, 1, 1, "circular", 16, "conv"), (128, 128, 9, 1, 1, 1, "zeros", 12, "conv"),
+    (64, 128, 11, 2, 1, 1, "zeros", 15, "conv"), (256, 256, 13, 1, 1, 1, "circular", 13, "conv"),
+    (64, 64, 9, 2, 1, 1, "circular", 10, "convT"), (32, 32, 13, 1, 1, 1, "circular", 14, "conv"),
 ]
 
 

@@ -137,7 +137,7 @@ def row_f3():
         out.append(dict(row="f3 SOC", c=c, terms=6, k_eff=13, construct_ms=ms, construct_tflops=fl / ms / 1e9,
                         apply_13x13_ms=ms_apply, implicit_6x3x3_ms=6 * ms_3,
                         note="construction = batched block-conv GEMMs (3-pass tcgen05); the 13x13 apply runs on "
-                             "the SIMT conv (tensor-core conv kernels take k <= 7)"))
+                             "the tcgen05 gather conv (k <= 13)"))
     return out
 
 

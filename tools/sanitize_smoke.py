@@ -56,8 +56,21 @@ def main():
         plan.orthogonalize_vjp(p, dortho, dparams)
         plan.certify(3, plan.kernel_f32(kf, 3).reshape(-1).contiguous(), 8, 8, power_iters=5)
         plan.check()
-    soc = [dict(kind="soc", c_in=16, c_out=16, k=3, s=1, d=1, g=1, terms=3, padding_mode="circular", H=8)]
+    soc = [dict(kind="soc", c_in=64, c_out=64, k=3, s=1, d=1, g=1, terms=6, padding_mode="circular", H=16)]
     plan, p, ortho, kf, kb = build(soc, "bf16")
+    x = torch.randn(2, 16, 16, 64, device="cuda").to(torch.bfloat16)
+    y = torch.empty_like(x)
+    plan.conv_forward(0, plan.kernel_bf16(kb, 0), x, y)              # 13 x 13 gather conv
+    plan.conv_transpose(0, plan.kernel_bf16(kb, 0), y, x)
+    stem = [dict(kind="conv", c_in=3, c_out=64, k=4, s=4, d=1, g=1, padding_mode="circular", H=32)]
+    plan, p, ortho, kf, kb = build(stem, "bf16")
+    x = torch.randn(3, 32, 32, 3, device="cuda").to(torch.bfloat16)
+    dy = torch.randn(3, 8, 8, 64, device="cuda").to(torch.bfloat16)
+    nb = orth.orth_conv_wgrad_workspace(plan.h, 0, 3, 32, 32, orth.BF16)
+    ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
+    plan.conv_wgrad(0, x, dy, torch.zeros(plan.kernel_shape(0), device="cuda"), workspace=ws)   # small SIMT
+    plan.certify(0, plan.kernel_f32(kf, 0).reshape(-1).contiguous(), 8, 8, power_iters=3)
+    plan.check()
     blk = [dict(kind="conv", c_in=16, c_out=16, k=2, s=1, d=1, g=1, padding_mode="circular", H=8),
            dict(kind="sll", c_in=16, c_out=16, k=2, s=1, d=1, g=1, padding_mode="circular", H=8),
            dict(kind="conv", c_in=16, c_out=32, k=3, s=2, d=1, g=1, padding_mode="circular", H=8),

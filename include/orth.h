@@ -247,7 +247,9 @@ orth_status_t orth_compose_kernel(orth_plan_t plan, const float* ortho, float* k
  * io = ORTH_F32: x, y float32 and `kernel` the layer's FP32 PyTorch-layout kernel;
  * io = ORTH_BF16: x, y bfloat16 and `kernel` the layer's BF16 GEMM-layout kernel.
  * bias: nullable FP32[C_o].  Accumulation FP32.  Circular padding requires
- * s | H and s | W (R11).  Dense layers: ORTH_ERR_UNSUPPORTED_CONFIG. */
+ * s | H and s | W (R11).  Dense layers: ORTH_ERR_UNSUPPORTED_CONFIG.
+ * N = 0 (an empty batch, e.g. a rank's empty shard) is a no-op: x and y may be
+ * NULL; H, W must still be >= 1 (and so for orth_conv_transpose). */
 orth_status_t orth_conv_forward(orth_plan_t plan, int32_t layer, const void* kernel, const float* bias,
                                 const void* x, void* y, int32_t N, int32_t H, int32_t W, int32_t io, void* stream);
 
@@ -282,7 +284,7 @@ orth_status_t orth_plan_check(orth_plan_t plan, void* stream);
  * GEMM over the pixels (M = c_out/g, N = c_in/g, up to 3 taps per CTA sharing the dy tile); otherwise
  * FP32 SIMT.  Both sum pixel splits in a fixed order through `workspace` (orth_conv_wgrad_workspace bytes,
  * caller-owned device memory; 0 bytes: none needed).  FP32 accumulation, deterministic.  N*H*W < 2^31.
- * Not for SLL blocks or dense layers. */
+ * N = 0: dK = 0 (x, dy may be NULL).  Not for SLL blocks or dense layers. */
 orth_status_t orth_conv_wgrad_workspace(orth_plan_t plan, int32_t layer, int32_t N, int32_t H, int32_t W, int32_t io,
                                         int64_t* bytes);
 orth_status_t orth_conv_wgrad(orth_plan_t plan, int32_t layer, const void* x, const void* dy, float* dkernel_f32,

@@ -92,9 +92,10 @@ orth_status_t check_conv(Plan& P, int32_t layer, const void* kernel, const void*
   if (layer < 0 || layer >= (int)P.layers.size()) { set_error("layer %d out of range", layer); return ORTH_ERR_INVALID_ARGUMENT; }
   const LayerInfo& L = P.layers[layer];
   if (L.cons == CONS_DENSE) { set_error("dense layers have no conv forward (plain GEMM, out of scope)"); return ORTH_ERR_UNSUPPORTED_CONFIG; }
-  if (!kernel || !in || !out) { set_error("NULL kernel/input/output"); return ORTH_ERR_INVALID_ARGUMENT; }
+  // an empty batch (N = 0) is a valid no-op: its activation pointers may be NULL
+  if (!kernel || (N != 0 && (!in || !out))) { set_error("NULL kernel/input/output"); return ORTH_ERR_INVALID_ARGUMENT; }
   if (io != ORTH_F32 && io != ORTH_BF16) { set_error("bad io dtype %d", io); return ORTH_ERR_INVALID_ARGUMENT; }
-  if (N < 1 || H < 1 || W < 1) { set_error("N, H, W must be >= 1"); return ORTH_ERR_SHAPE_MISMATCH; }
+  if (N < 0 || H < 1 || W < 1) { set_error("N >= 0, H, W >= 1 required"); return ORTH_ERR_SHAPE_MISMATCH; }
   const int num = H + L.pt + L.pb - L.d * (L.k - 1) - 1, numw = W + L.pl + L.pr - L.d * (L.k - 1) - 1;
   if (num < 0 || numw < 0) { set_error("input %dx%d smaller than the dilated kernel", H, W); return ORTH_ERR_SHAPE_MISMATCH; }
   Ho = out_dim(H, L.k, L.s, L.d, L.pt, L.pb);
@@ -268,7 +269,7 @@ orth_status_t orth_conv_forward(orth_plan_t plan, int32_t layer, const void* ker
   Plan& P = plan->p;
   int Ho = 0, Wo = 0;
   st = check_conv(P, layer, kernel, x, y, N, H, W, io, Ho, Wo);
-  if (st != ORTH_OK) return st;
+  if (st != ORTH_OK || N == 0) return st;
   NvtxRange nv("orth_conv_forward");
   Trace tr(P, ORTH_TK_CONV_FWD, layer, stream);
   const LayerInfo& L = P.layers[layer];
@@ -302,6 +303,7 @@ orth_status_t orth_conv_transpose(orth_plan_t plan, int32_t layer, const void* k
   st = check_conv(P, layer, kernel, y_small, x_big, N, H_big, W_big, io, Ho, Wo);
   if (st != ORTH_OK) return st;
   if (P.layers[layer].cons == CONS_SLL_BLOCK) { set_error("an SLL block is not linear: no adjoint"); return ORTH_ERR_UNSUPPORTED_CONFIG; }
+  if (N == 0) return ORTH_OK;
   NvtxRange nv("orth_conv_transpose");
   Trace tr(P, ORTH_TK_CONV_ADJ, layer, stream);
   const int e = launch_conv_bwd(P.layers[layer], kernel, P.layers[layer].wt_scratch, bias, y_small, x_big, N, H_big, W_big, Ho,
@@ -339,9 +341,9 @@ orth_status_t orth_conv_wgrad_workspace(orth_plan_t plan, int32_t layer, int32_t
   Plan& P = plan->p;
   if (layer < 0 || layer >= (int)P.layers.size()) { set_error("layer %d out of range", layer); return ORTH_ERR_INVALID_ARGUMENT; }
   const LayerInfo& L = P.layers[layer];
-  if (N < 1 || H < 1 || W < 1) { set_error("N, H, W must be >= 1"); return ORTH_ERR_SHAPE_MISMATCH; }
+  if (N < 0 || H < 1 || W < 1) { set_error("N >= 0, H, W >= 1 required"); return ORTH_ERR_SHAPE_MISMATCH; }
   const int Ho = out_dim(H, L.k, L.s, L.d, L.pt, L.pb), Wo = out_dim(W, L.k, L.s, L.d, L.pl, L.pr);
-  *bytes = wgrad_workspace_bytes(L, N, Ho, Wo, io);
+  *bytes = N == 0 ? 0 : wgrad_workspace_bytes(L, N, Ho, Wo, io);
   return ORTH_OK;
 }
 
@@ -357,6 +359,9 @@ orth_status_t orth_conv_wgrad(orth_plan_t plan, int32_t layer, const void* x, co
   const LayerInfo& L = P.layers[layer];
   if (L.cons == CONS_SLL_BLOCK) { set_error("SLL blocks have no single weight gradient"); return ORTH_ERR_UNSUPPORTED_CONFIG; }
   if ((int64_t)N * H * W >= (1LL << 31)) { set_error("N*H*W must stay below 2^31 (32-bit pixel indices)"); return ORTH_ERR_SHAPE_MISMATCH; }
+  if (N == 0)   // the gradient over an empty batch is zero
+    return cuda_fail((int)cudaMemsetAsync(dkernel_f32, 0, (size_t)L.kernel_numel * 4, (cudaStream_t)stream),
+                     "orth_conv_wgrad");
   NvtxRange nv("orth_conv_wgrad");
   Trace tr(P, ORTH_TK_WGRAD, layer, stream);
   const int e = launch_wgrad(L, x, dy, dkernel_f32, N, H, W, Ho, Wo, io, workspace, workspace_bytes, stream);

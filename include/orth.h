@@ -249,7 +249,9 @@ orth_status_t orth_compose_kernel(orth_plan_t plan, const float* ortho, float* k
  * bias: nullable FP32[C_o].  Accumulation FP32.  Circular padding requires
  * s | H and s | W (R11).  Dense layers: ORTH_ERR_UNSUPPORTED_CONFIG.
  * N = 0 (an empty batch, e.g. a rank's empty shard) is a no-op: x and y may be
- * NULL; H, W must still be >= 1 (and so for orth_conv_transpose). */
+ * NULL; H, W must still be >= 1 (and so for orth_conv_transpose).  The padded
+ * pixel count N (H + p_t + p_b)(W + p_l + p_r) must stay below 2^31 (32-bit
+ * pixel indices; SHAPE_MISMATCH otherwise). */
 orth_status_t orth_conv_forward(orth_plan_t plan, int32_t layer, const void* kernel, const float* bias,
                                 const void* x, void* y, int32_t N, int32_t H, int32_t W, int32_t io, void* stream);
 

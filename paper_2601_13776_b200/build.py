@@ -4,7 +4,8 @@
 file is loaded by path, not as a package module: importing the package itself
 requires the built library (no fallback).
 Objects go to ``paper_2601_13776_b200/_build``; the library next to this file.
-Rebuilds only what changed (source or any header newer than its object).
+Rebuilds only what changed (source or any header newer than its object); a change of the compile
+flags (ORTH_EXPERIMENTAL, ORTH_NVCC_FLAGS) rebuilds everything.
 """
 from __future__ import annotations
 
@@ -38,6 +39,13 @@ def _headers():
 
 def build(verbose: bool = False, jobs: int = 8) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    stamp = os.path.join(OBJ, "flags.txt")
+    flags = " ".join(ARCH + FLAGS)
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        for o in glob.glob(os.path.join(OBJ, "*.o")):
+            os.remove(o)
+        with open(stamp, "w") as f:
+            f.write(flags)
     hdr_t = max([os.path.getmtime(h) for h in _headers()] + [0.0])
     procs, objs = [], []
     for src in _sources():

@@ -96,6 +96,10 @@ orth_status_t check_conv(Plan& P, int32_t layer, const void* kernel, const void*
   if (!kernel || (N != 0 && (!in || !out))) { set_error("NULL kernel/input/output"); return ORTH_ERR_INVALID_ARGUMENT; }
   if (io != ORTH_F32 && io != ORTH_BF16) { set_error("bad io dtype %d", io); return ORTH_ERR_INVALID_ARGUMENT; }
   if (N < 0 || H < 1 || W < 1) { set_error("N >= 0, H, W >= 1 required"); return ORTH_ERR_SHAPE_MISMATCH; }
+  if ((int64_t)N * (H + L.pt + L.pb) * (W + L.pl + L.pr) >= (1LL << 31)) {
+    set_error("N*H*W (padded) must stay below 2^31 (32-bit pixel indices)");
+    return ORTH_ERR_SHAPE_MISMATCH;
+  }
   const int num = H + L.pt + L.pb - L.d * (L.k - 1) - 1, numw = W + L.pl + L.pr - L.d * (L.k - 1) - 1;
   if (num < 0 || numw < 0) { set_error("input %dx%d smaller than the dilated kernel", H, W); return ORTH_ERR_SHAPE_MISMATCH; }
   Ho = out_dim(H, L.k, L.s, L.d, L.pt, L.pb);

@@ -46,7 +46,8 @@ TRACE_KINDS = {1: "power", 2: "scale", 3: "ns", 4: "ns_check", 5: "compose", 6: 
                8: "conv_adj", 9: "assemble", 10: "certify", 11: "wgrad", 12: "compose_vjp", 13: "ns_vjp"}
 CONV_VARIANTS = {0: "none", 1: "conv_fwd_simt/conv_bwd_simt", 2: "conv_fwd_smallk", 3: "conv_stem_tc",
                  4: "conv_pad<64,swapped>", 5: "conv_pad<BN>", 6: "conv_stack (+pad_kernel)", 7: "conv_tma",
-                 8: "conv_ws<256>", 9: "conv_ws<128>", 10: "conv_ws<64>", 11: "conv_ws<32>", 12: "conv_pair"}
+                 8: "conv_ws<256>", 9: "conv_ws<128>", 10: "conv_ws<64>", 11: "conv_ws<32>", 12: "conv_pair",
+                 13: "conv_pad<64,row>"}
 
 
 class TraceRec(C.Structure):

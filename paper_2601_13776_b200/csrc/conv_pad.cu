@@ -17,7 +17,15 @@
 //       window pixels (the weights are the A operand); the M = 64 accumulator is
 //       read as 16x256b fragments and transposed by stmatrix into a SWIZZLE_128B
 //       staging tile, one TMA tensor store per output row;
-//   plain: M = 128 window pixels x N = BN channels, epilogue stores rows.
+//   plain: M = 128 window pixels x N = BN channels, epilogue stores rows;
+//   ROW (co_g = 64, k <= 4): M = 128 window pixels x N = k * 64 -- ONE MMA per kernel row a for all k
+//       taps (a, b): B = the row's k weight tiles stacked (k x 64 rows), A = the window at tap (a, 0).
+//       Column block b of the accumulator at window pixel r then holds tap (a, b)'s contribution to
+//       output pixel r - d b (the taps of a row differ only by a d-pixel shift of the same window), so
+//       the epilogue adds block b of pixel r + d b (a lane shuffle; across warps through shared
+//       memory).  r + d b stays inside the tile for every valid output (the pitch P = Wo + d(k-1) ends
+//       in d(k-1) junk columns).  The k-wide N amortises the window operand's shared-memory reads over
+//       k taps: per K=16 step A 4 KB + B k x 2 KB, below the M128 x N(k 64) floor of k x 32 cycles.
 // Weights of one (group, channel tile) stay resident in shared memory when they
 // fit (each CTA then walks a contiguous tile range), else they stream per tap.
 //
@@ -86,6 +94,8 @@ struct PadArgs {
 
 constexpr int A_WARP = 0, B_WARP = 1, MMA_WARP = 2, EPI_WARP0 = 4;
 constexpr int NTHREADS = 8 * 32;
+constexpr int ROW_EPI = 8;   // ROW: two epilogue warps per TMEM lane quadrant, one per 32-channel half
+constexpr int NTHREADS_ROW = (4 + ROW_EPI) * 32;
 constexpr int MAX_SB = 16;
 constexpr int MAX_AB = 4;
 
@@ -105,8 +115,8 @@ struct PadMaps {
 // 128x64 N=64 tile costs ~73 cycles per MMA on B200 (shared-memory bound), the 64x256 one ~128 for
 // 4x the work.  The accumulator (M=64 layout: channel o in TMEM lane (o % 16) + 32 (o / 16)) is
 // transposed through a shared-memory staging tile and written by TMA, one output row per store.
-template <int BN, bool SW>
-__global__ void __launch_bounds__(NTHREADS, 1)
+template <int BN, bool SW, bool ROW = false>
+__global__ void __launch_bounds__(ROW ? NTHREADS_ROW : NTHREADS, 1)
     conv_pad(const float* __restrict__ bias, __nv_bfloat16* __restrict__ out, const __grid_constant__ PadArgs a,
              const __grid_constant__ PadMaps tmA, const __grid_constant__ CUtensorMap tmB,
              const __grid_constant__ CUtensorMap tmY) {
@@ -119,7 +129,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int SB = a.sb, NA = a.nabuf;
-  constexpr int ACC_COLS = SW ? 256 : BN;   // TMEM columns per accumulator
+  constexpr int ACC_COLS = (SW || ROW) ? 256 : BN;   // TMEM columns per accumulator
+  const int bst_bytes = ROW ? a.k * B_BYTES : B_BYTES;   // one streamed B stage: a tap, or a kernel row
   if (warp == MMA_WARP) umma::tmem_alloc(&tmem_base_sh, 2 * ACC_COLS);
   if (tid == 0) {
     for (int i = 0; i < NA; ++i) {
@@ -132,7 +143,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       umma::mbar_init(&tfull_bar[i], 1);
-      umma::mbar_init(&tempty_bar[i], 128);
+      umma::mbar_init(&tempty_bar[i], ROW ? ROW_EPI * 32 : 128);
     }
     umma::fence_mbar_init();
   }
@@ -215,6 +226,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           ++loads;
           continue;
         }
+        if (ROW) {   // one stage per (chunk, kernel row): the row's k tap tiles back to back
+          for (int c0 = 0; c0 < a.cr_g; c0 += 64)
+            for (int ra = 0; ra < a.k; ++ra, ++i) {
+              const int st = i % SB;
+              if (i >= SB) umma::mbar_wait(&b_empty[st], ((i / SB) - 1) & 1);
+              umma::mbar_arrive_expect_tx(&b_full[st], (uint32_t)bst_bytes);
+              for (int b = 0; b < a.k; ++b) {
+                const int tap = ra * a.k + b;
+                umma::tma_load_3d(bbase + st * bst_bytes + b * B_BYTES, &tmB, &b_full[st], c0,
+                                  a.flip ? kk2 - 1 - tap : tap, g * a.nout_g + n0);
+              }
+            }
+          continue;
+        }
         for (int c0 = 0; c0 < a.cr_g; c0 += 64)
           for (int tap = 0; tap < kk2; ++tap, ++i) {
             const int st = i % SB;
@@ -251,6 +276,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           umma::tc_fence_after();
           if (c0 == 0) CTRACE(tcount, 1);
           const uint32_t abuf = abase + ab * a.abuf_bytes;
+          if (ROW) {   // one M128 x N(k 64) MMA chain per kernel row
+            const uint32_t idesc_row = umma::idesc_bf16(128, a.k * 64);
+            for (int ra = 0; ra < a.k; ++ra, j += a.k) {
+              int st = 0;
+              if (!a.bres) {
+                st = i % SB;
+                umma::mbar_wait(&b_full[st], (i / SB) & 1);
+                umma::tc_fence_after();
+              }
+              const uint32_t aa = abuf + (uint32_t)(a.d * ra * a.P) * 128u;
+              const uint32_t bb = bbase + (a.bres ? (uint32_t)(j * B_BYTES) : (uint32_t)(st * bst_bytes));
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                umma::mma_bf16(d_tmem, umma::sdesc_sw128(aa + 32 * q), umma::sdesc_sw128(bb + 32 * q), idesc_row,
+                               (c0 | ra | q) != 0);
+              if (!a.bres) {
+                umma::mma_commit(&b_empty[st]);
+                ++i;
+              }
+            }
+            umma::mma_commit(&a_empty[ab]);
+            continue;
+          }
           for (int tap = 0; tap < kk2; ++tap, ++j) {
             int st = 0;
             if (!a.bres) {
@@ -343,7 +391,100 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
     if (tid == EPI_WARP0 * 32) umma::bulk_wait0();
-  } else if (!SW && warp >= EPI_WARP0) {
+  } else if (ROW && warp >= EPI_WARP0) {
+    // ------------------------------------------------------------ epilogue (kernel-row MMAs)
+    // Thread = window pixel r (TMEM lane).  y[r][o] = sum_b acc[r + d b][b 64 + o]: block b of lane
+    // r + d b comes by shuffle from the same warp, or from the next warp through `xs` (the first
+    // d (k-1) lanes of every warp publish their blocks, one barrier per tile among the four warps of a
+    // 32-channel half); lanes past the tile only feed junk outputs.  Eight warps: warp 4 + 4h + q reads
+    // lane quadrant q, channel half h.
+    const int q = warp & 3, h = (warp - EPI_WARP0) >> 2;             // TMEM lane quadrant, channel half
+    const int r = q * 32 + lane;
+    const int y = r / a.P, x = r - y * a.P;
+    const int xl = a.d * (a.k - 1);                       // lanes published per warp (< 32)
+    const int reg = 4 * 3 * xl * 16;                      // floats per exchange region: [warp][b - 1][lane][16]
+    float* xs = reinterpret_cast<float*>(smem + a.stage_off);   // regions [half][chunk][tile parity]
+    int tcount = 0;
+    for (int tile = t_begin; tile < t_end; tile += t_step, ++tcount) {
+      int n, h0, g, n0;
+      decode(tile, n, h0, g, n0);
+      const int opix = (y < a.TH && x < a.Wo && h0 + y < a.Ho) ? (n * a.Ho + h0 + y) * a.Wo + x : -1;
+      const int acc = tcount & 1;
+      umma::mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
+      umma::tc_fence_after();
+      if (q == 0 && lane == 0) CTRACE(tcount, 2);
+      const int obase = g * a.nout_g + n0;
+#pragma unroll 1
+      for (int ci = 0; ci < 2; ++ci) {   // two 16-channel chunks of this warp's half
+        const int cc = 32 * h + 16 * ci;
+        uint32_t rv[4][16];   // the k column blocks of this chunk, all in flight, one wait
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (b < a.k) umma::tmem_ld16_nw(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 256 + b * 64 + cc), rv[b]);
+        umma::tmem_ld_wait();
+        // one region per (half, chunk, tile parity): a warp publishing the next use of a region has passed
+        // the barrier of the use in between, which every reader of this use reached after reading
+        float* xh = xs + ((h * 2 + ci) * 2 + (tcount & 1)) * reg;
+        if (lane < xl) {
+#pragma unroll
+          for (int b = 1; b < 4; ++b)
+            if (b < a.k && lane < a.d * b) {
+              float4* d4 = reinterpret_cast<float4*>(xh + ((q * 3 + b - 1) * xl + lane) * 16);
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                d4[e] = make_float4(__uint_as_float(rv[b][4 * e]), __uint_as_float(rv[b][4 * e + 1]),
+                                    __uint_as_float(rv[b][4 * e + 2]), __uint_as_float(rv[b][4 * e + 3]));
+            }
+        }
+        umma::named_bar_sync(3 + h, 128);   // the four warps of this half
+        float s[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) s[e] = __uint_as_float(rv[0][e]);
+#pragma unroll
+        for (int b = 1; b < 4; ++b) {
+          if (b >= a.k) break;
+          const int sh = a.d * b, src = lane + sh - 32;   // src >= 0: the partner is lane src of warp q + 1
+          float t[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) t[e] = __shfl_down_sync(0xffffffffu, __uint_as_float(rv[b][e]), sh);
+          if (src >= 0) {   // the last d b lanes (divergent, short)
+            if (q < 3) {
+              const float4* s4 = reinterpret_cast<const float4*>(xh + (((q + 1) * 3 + b - 1) * xl + src) * 16);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float4 v4 = s4[e];
+                t[4 * e] = v4.x; t[4 * e + 1] = v4.y; t[4 * e + 2] = v4.z; t[4 * e + 3] = v4.w;
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) t[e] = 0.f;   // past the tile: feeds junk outputs only
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 16; ++e) s[e] += t[e];
+        }
+        if (opix >= 0) {
+          const int o = obase + cc;
+          uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)opix * a.out_C + o);
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              float v0 = s[8 * i + 2 * jj], v1 = s[8 * i + 2 * jj + 1];
+              if (bias) { v0 += bias[o + 8 * i + 2 * jj]; v1 += bias[o + 8 * i + 2 * jj + 1]; }
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
+              pk[jj] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            dst[i] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        }
+      }
+      umma::tc_fence_before();
+      umma::mbar_arrive(&tempty_bar[acc]);
+      if (q == 0 && lane == 0) CTRACE(tcount, 3);
+    }
+  } else if (!SW && !ROW && warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;
     const int r = q * 32 + lane;
@@ -435,14 +576,18 @@ bool make_act_tmap(CUtensorMap* out, const void* x, int C, int W, int H, int N, 
   return true;
 }
 
-template <int BN, bool SW>
+template <int BN, bool SW, bool ROW = false>
 int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out, PadArgs& a,
                int in_C, cudaStream_t stream) {
   const size_t fixed = 1024;
-  const size_t stage = SW ? (size_t)a.TH * a.stage_row + 1024 : 0;   // swapped mode: output staging rows
+  // swapped mode: output staging rows; ROW: the cross-warp exchange of d (k-1) lanes x 32 floats per warp
+  const size_t stage = SW ? (size_t)a.TH * a.stage_row + 1024
+                          : ROW ? (size_t)8 * 4 * 3 * a.d * (a.k - 1) * 16 * 4 : 0;
+  const size_t bst = (size_t)(ROW ? a.k : 1) * BN * 128;   // one streamed B stage
   const size_t bset = (size_t)((a.cr_g + 63) / 64) * a.k * a.k * BN * 128;
   size_t smem;
-  if (a.bres) {   // resident weights + >= 2 A buffers (caller checked the fit)
+  if (a.bres) {   // resident weights + >= 2 A buffers
+    if (fixed + 2 * (size_t)a.abuf_bytes + bset + stage > kSmemMax) return -1;
     int na = MAX_AB;
     while (na > 2 && fixed + (size_t)na * a.abuf_bytes + bset + stage > kSmemMax) --na;
     a.nabuf = na;
@@ -454,17 +599,18 @@ int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* b
   } else {
     // A ring: as many buffers as leave room for >= 4 B stages (at least 2)
     int na = MAX_AB;
-    while (na > 2 && fixed + (size_t)na * a.abuf_bytes + 4 * (size_t)BN * 128 + stage > kSmemMax) --na;
-    if (fixed + (size_t)na * a.abuf_bytes + 2 * (size_t)BN * 128 + stage > kSmemMax) return -1;
+    while (na > 2 && fixed + (size_t)na * a.abuf_bytes + 4 * bst + stage > kSmemMax) --na;
+    if (fixed + (size_t)na * a.abuf_bytes + 2 * bst + stage > kSmemMax) return -1;
     a.nabuf = na;
-    a.sb = (int)std::min<size_t>(MAX_SB, (kSmemMax - fixed - stage - (size_t)na * a.abuf_bytes) / ((size_t)BN * 128));
-    a.stage_off = (int)(na * (size_t)a.abuf_bytes + (size_t)a.sb * BN * 128);
-    smem = fixed + (size_t)na * a.abuf_bytes + (size_t)a.sb * BN * 128 + stage;
+    a.sb = (int)std::min<size_t>(MAX_SB, (kSmemMax - fixed - stage - (size_t)na * a.abuf_bytes) / bst);
+    a.stage_off = (int)(na * (size_t)a.abuf_bytes + (size_t)a.sb * bst);
+    smem = fixed + (size_t)na * a.abuf_bytes + (size_t)a.sb * bst + stage;
   }
   if (smem - fixed - (size_t)a.nabuf * a.abuf_bytes < (size_t)a.slack_bytes) return -1;   // reads stay in smem
   static size_t attr = 0;
   if (smem > attr) {
-    if (cudaFuncSetAttribute(conv_pad<BN, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(conv_pad<BN, SW, ROW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
       return (int)cudaGetLastError();
     attr = smem;
   }
@@ -504,7 +650,8 @@ int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* b
   }
   const int grid = a.bres ? (a.num_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta
                           : (a.num_tiles < sm_count() ? a.num_tiles : sm_count());
-  launch_pdl(conv_pad<BN, SW>, dim3(grid), dim3(NTHREADS), smem, stream, bias, out, a, maps, tm, ty);
+  launch_pdl(conv_pad<BN, SW, ROW>, dim3(grid), dim3(ROW ? NTHREADS_ROW : NTHREADS), smem, stream, bias, out, a, maps,
+             tm, ty);
 #ifdef ORTH_CONV_TRACE
   {
     cudaStreamSynchronize(stream);
@@ -548,7 +695,8 @@ bool conv_act_tmap(CUtensorMap_st* out, const void* x, int C, int W, int H, int 
 // Plan the padded-row path for a (possibly group-packed) forward layer; false
 // if it does not apply (stride != 1, rows wider than one tile, channel slices
 // that would cross groups, circular padding that is not a single wrap, ...).
-static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, int& bn, PadArgs& a, bool sw) {
+static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, int& bn, PadArgs& a, bool sw,
+                     int p_align = 1) {
   const int ext = L.d * (L.k - 1);
   static const int co_max = std::getenv("ORTH_CONV_PAD_COMAX") ? std::atoi(std::getenv("ORTH_CONV_PAD_COMAX")) : 64;
   if (L.s != 1 || Wo > 128 || Wo < 16 || L.k > 7 || L.co > (sw ? 64 : co_max)) return false;
@@ -570,7 +718,7 @@ static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, in
     const bool single = layout == 0;
     if (layout_env && std::strcmp(layout_env, single ? "window" : "copies") != 0) continue;
     if (!single && circ && W % 8 != 0) continue;
-    const int P = single ? Wo + ext : (circ ? W : (Wo + 7) & ~7);
+    const int P = single ? (Wo + ext + p_align - 1) / p_align * p_align : (circ ? W : (Wo + 7) & ~7);
     if (P > 128 + ext || P > 256) continue;
     const int TH = std::min(Ho, MT / P);
     if (TH < 1 || TH * Wo < MT / 2) continue;
@@ -610,7 +758,9 @@ static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, in
     a.ncopy = ncopy;
     a.copy_bytes = copy_bytes;
     a.abuf_bytes = (int)abuf;
-    a.a_tx = ncopy * copy_bytes;
+    // bytes the window's TMA loads deliver: circular single windows fill only W + d(k-1) columns of a
+    // (possibly alignment-padded) pitch P, the rest is junk that feeds junk outputs only
+    a.a_tx = (circ && single) ? R * (W + ext) * 128 : ncopy * copy_bytes;
     if (circ) {
       for (int b = 0; b < ncopy; ++b) {
         int np = 0;
@@ -640,8 +790,19 @@ int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* b
   auto* out = static_cast<__nv_bfloat16*>(y);
   cudaStream_t s = (cudaStream_t)stream;
   static const bool no_swap = std::getenv("ORTH_CONV_NO_SWAP") != nullptr;   // A/B switch
+  static const bool no_row = std::getenv("ORTH_CONV_NO_ROW") != nullptr;     // A/B switch
+  static const int row_align = std::getenv("ORTH_CONV_ROW_ALIGN") ? std::atoi(std::getenv("ORTH_CONV_ROW_ALIGN")) : 1;
   int bn = 0;
   PadArgs a;
+  // kernel-row MMAs (co_g = 64, 2 <= k <= 4, one window layout): M = 128 pixels x N = k 64
+  if (!no_row && L.co == 64 && L.k >= 2 && L.k <= 4 && L.d * (L.k - 1) < 32 &&
+      pad_args(L, N, H, W, Ho, Wo, bn, a, false, row_align) && bn == 64 && a.ncopy == 1) {
+    if (a.num_tiles == 0) return 0;
+    a.flip = flip;
+    g_conv_variant = ORTH_CV_WINDOW_ROW;
+    const int e = launch_pad<64, false, true>(x, w, L.co_f, bias, out, a, L.ci_f, s);
+    if (e >= 0) return e;
+  }
   if (!no_swap && pad_args(L, N, H, W, Ho, Wo, bn, a, true) && bn == 64) {   // 64 channels x 256 pixels per MMA
     if (a.num_tiles == 0) return 0;
     a.flip = flip;

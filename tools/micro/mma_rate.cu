@@ -6,7 +6,7 @@
 #include <cuda_runtime.h>
 #include "../../paper_2601_13776_b200/csrc/umma.cuh"
 using namespace orth;
-template <int M, int N>
+template <int M, int N, int NACC = 1>
 __global__ void __launch_bounds__(128, 1) k(int nmma, int astride, int bstride, unsigned long long* out, int zero_data) {
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, int astride, int bstride, 
     reinterpret_cast<uint32_t*>(sm)[i] = zero_data == 1 ? 0u : (lo | (hi << 16));
   }
   if (threadIdx.x == 0) *reinterpret_cast<int*>(sm + 200704 - 16) = 0;
-  if (threadIdx.x < 32) umma::tmem_alloc(&tbase, 256);
+  if (threadIdx.x < 32) umma::tmem_alloc(&tbase, 512);
   if (threadIdx.x == 0) { umma::mbar_init(&bar, 1); umma::fence_mbar_init(); }
   umma::fence_proxy_async_smem();
   umma::tc_fence_before();
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, int astride, int bstride, 
                        i > 0);
         continue;
       }
-      umma::mma_bf16(tbase, umma::sdesc_sw128(aa + 32 * (i & 3)), umma::sdesc_sw128(bb + 32 * (i & 3)), ID, i > 0);
+      umma::mma_bf16(tbase + (uint32_t)((i % NACC) * N), umma::sdesc_sw128(aa + 32 * (i & 3)), umma::sdesc_sw128(bb + 32 * (i & 3)), ID, i >= NACC);
     }
     umma::mma_commit(&bar);
     umma::mbar_wait(&bar, 0);
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, int astride, int bstride, 
   }
   umma::tc_fence_before();
   __syncthreads();
-  if (threadIdx.x < 32) umma::tmem_dealloc(tbase, 256);
+  if (threadIdx.x < 32) umma::tmem_dealloc(tbase, 512);
 }
 int main() {
   unsigned long long* d; cudaMalloc(&d, 16 * 148);
@@ -81,11 +81,17 @@ int main() {
     printf("zero=%d M=%3d N=%3d astride=%2d bstride=%2d ctas=%3d: %.1f cycles/MMA, %.1f ns/MMA, clock %.0f MHz (%s)\n", zero, m, n, as,
            bs, ctas, h / (double)nm, hg[1] / (double)nm, 1e3 * h / (double)hg[1], cudaGetErrorString(cudaGetLastError()));
   };
-  for (zero = 0; zero < 3; zero += 2) {   // 0: plain, 2: with concurrent smem writers
-    for (int ctas : {148}) {
-      run(k<128, 128>, 128, 128, -1, 0, ctas);
-      run(k<128, 256>, 128, 256, -1, 0, ctas);
-      run(k<64, 256>, 64, 256, -1, 0, ctas);
-    }
-  }
+  // independent accumulators interleaved (NACC D regions, round robin): does a second accumulator
+  // overlap the per-MMA latency?
+  run(k<128, 64, 1>, 128, 64, 0, 0, 148);
+  run(k<128, 64, 2>, 128, 64, 0, 0, 148);
+  run(k<128, 64, 4>, 128, 64, 0, 0, 148);
+  run(k<128, 128, 1>, 128, 128, 0, 0, 148);
+  run(k<128, 128, 2>, 128, 128, 0, 0, 148);
+  run(k<128, 192, 1>, 128, 192, 0, 0, 148);
+  run(k<128, 192, 2>, 128, 192, 0, 0, 148);
+  run(k<128, 256, 1>, 128, 256, 0, 0, 148);
+  run(k<128, 256, 2>, 128, 256, 0, 0, 148);
+  run(k<64, 256, 1>, 64, 256, 0, 0, 148);
+  run(k<64, 256, 2>, 64, 256, 0, 0, 148);
 }

@@ -134,11 +134,13 @@ __device__ __forceinline__ void group_sync(unsigned* bar, unsigned target) {
 }
 
 __device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int k0, int mn0,
-                                             int mn_major) {
-  if (mn_major) {   // columns of row-major X: two 64 (MN) x 64 (K) boxes
+                                             int kind) {
+  if (kind == 3) {          // columns of row-major X, 3-D map (64 MN, K, MN / 64): both 64-wide blocks in one box
+    umma::tma_load_3d(dst, map, bar, 0, k0, mn0 >> 6);
+  } else if (kind == 1) {   // columns of row-major X: two 64 (MN) x 64 (K) boxes
     umma::tma_load_2d(dst, map, bar, mn0, k0);
     umma::tma_load_2d(dst + 8192, map, bar, mn0 + 64, k0);
-  } else {          // rows: one 64 (K) x 128 box
+  } else {                  // rows: one 64 (K) x 128 box
     umma::tma_load_2d(dst, map, bar, k0, mn0);
   }
 }
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool wide = !gram && d.epi == 4 && !split;
           const int ws = wide ? 2 : w;
           const int m0 = (tl.local / d.tiles_n) * 128, n0 = (tl.local % d.tiles_n) * (wide ? 256 : 128);
-          const int nk = (d.K + 63) / 64, a_mn = d.a_kind == 1, b_mn = d.b_kind == 1;
+          const int nk = (d.K + 63) / 64, a_mn = d.a_kind & 1, b_mn = d.b_kind & 1, ak = d.a_kind, bk = d.b_kind;
           const bool sym = gram && m0 == n0;   // diagonal Gram tile: B == A, loaded once
           const CUtensorMap* ma = maps + d.map_a + 2 * par;
           const CUtensorMap* mb = maps + d.map_b + 2 * par;
@@ -227,18 +229,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t sa = ring + s * kSlot;
             if (wide) {   // A 16 KB + B 256 rows (32 KB)
               umma::mbar_arrive_expect_tx(&full_bar[s], 16384u + 32768u);
-              load_operand(sa, ma, &full_bar[s], kb * 64, m0, a_mn);
-              load_operand(sa + 16384, mb, &full_bar[s], kb * 64, n0, b_mn);
-              load_operand(sa + 32768, mb, &full_bar[s], kb * 64, n0 + 128, b_mn);
+              load_operand(sa, ma, &full_bar[s], kb * 64, m0, ak);
+              load_operand(sa + 16384, mb, &full_bar[s], kb * 64, n0, bk);
+              load_operand(sa + 32768, mb, &full_bar[s], kb * 64, n0 + 128, bk);
               cnt += 2;
               continue;
             }
             umma::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(sym ? w * kSlot / 2 : w * kSlot));
-            load_operand(sa, ma, &full_bar[s], kb * 64, m0, a_mn);
-            if (!sym) load_operand(sa + 16384, mb, &full_bar[s], kb * 64, n0, b_mn);
+            load_operand(sa, ma, &full_bar[s], kb * 64, m0, ak);
+            if (!sym) load_operand(sa + 16384, mb, &full_bar[s], kb * 64, n0, bk);
             if (split) {
-              load_operand(sa + 32768, ma + 1, &full_bar[s], kb * 64, m0, a_mn);
-              if (!sym) load_operand(sa + 49152, mb + 1, &full_bar[s], kb * 64, n0, b_mn);
+              load_operand(sa + 32768, ma + 1, &full_bar[s], kb * 64, m0, ak);
+              if (!sym) load_operand(sa + 49152, mb + 1, &full_bar[s], kb * 64, n0, bk);
             }
             cnt += w;
           }
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = tb; t < te; ++t) {
           const NsTile tl = tiles[t];
           const NsDesc* dp = D + tl.desc;
-          const int nk = (__ldg(&dp->K) + 63) / 64, a_mn = __ldg(&dp->a_kind) == 1, b_mn = __ldg(&dp->b_kind) == 1;
+          const int nk = (__ldg(&dp->K) + 63) / 64, a_mn = __ldg(&dp->a_kind) & 1, b_mn = __ldg(&dp->b_kind) & 1;
           const int tn = __ldg(&dp->tiles_n);
           const bool sym = gram && (tl.local / tn) == (tl.local % tn);
           const bool wide = !gram && __ldg(&dp->epi) == 4 && !split;
@@ -598,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const NsDesc d = D[tl.desc];
           const int tw = (!gram && d.epi == 2) ? 64 : 128;   // 64-wide update tiles (launch_ns_persist)
           const int m0 = (tl.local / d.tiles_n) * 128, n0 = (tl.local % d.tiles_n) * tw;
-          const int nk = (d.K + 63) / 64, a_mn = d.a_kind == 1, b_mn = d.b_kind == 1;
+          const int nk = (d.K + 63) / 64, a_mn = d.a_kind & 1, b_mn = d.b_kind & 1, ak = d.a_kind, bk = d.b_kind;
           const bool sym = gram && m0 == n0;   // diagonal Gram tile: B == A, loaded once
           const bool b_half = tw == 64 && b_mn;   // MN-major B: only the first 64-wide box
           const uint32_t stage_bytes = sym ? kSlot / 2 : (b_half ? kSlot / 2 + 8192 : kSlot);
@@ -616,13 +618,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const uint32_t sa = ring + s * kSlot;
             umma::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)w * stage_bytes);
-            load_operand(sa, ma, &full_bar[s], kb * 64, m0, a_mn);
+            load_operand(sa, ma, &full_bar[s], kb * 64, m0, ak);
             if (b_half) umma::tma_load_2d(sa + 16384, mb, &full_bar[s], n0, kb * 64);
-            else if (!sym) load_operand(sa + 16384, mb, &full_bar[s], kb * 64, n0, b_mn);
+            else if (!sym) load_operand(sa + 16384, mb, &full_bar[s], kb * 64, n0, bk);
             if (split) {
-              load_operand(sa + 32768, ma + 1, &full_bar[s], kb * 64, m0, a_mn);
+              load_operand(sa + 32768, ma + 1, &full_bar[s], kb * 64, m0, ak);
               if (b_half) umma::tma_load_2d(sa + 49152, mb + 1, &full_bar[s], n0, kb * 64);
-              else if (!sym) load_operand(sa + 49152, mb + 1, &full_bar[s], kb * 64, n0, b_mn);
+              else if (!sym) load_operand(sa + 49152, mb + 1, &full_bar[s], kb * 64, n0, bk);
             }
             cnt += w;
           }
@@ -647,7 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         {
           const NsTile tl{item.desc, item.local};
           const NsDesc* dp = D + tl.desc;
-          const int nk = (__ldg(&dp->K) + 63) / 64, a_mn = __ldg(&dp->a_kind) == 1, b_mn = __ldg(&dp->b_kind) == 1;
+          const int nk = (__ldg(&dp->K) + 63) / 64, a_mn = __ldg(&dp->a_kind) & 1, b_mn = __ldg(&dp->b_kind) & 1;
           const int tn = __ldg(&dp->tiles_n);
           const bool sym = gram && (tl.local / tn) == (tl.local % tn);
           const bool w64 = !gram && __ldg(&dp->epi) == 2;

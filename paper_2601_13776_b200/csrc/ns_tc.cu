@@ -78,11 +78,13 @@ __device__ __forceinline__ void split(float x, __nv_bfloat16& h, __nv_bfloat16& 
 // One 128 (MN) x 64 (K) BF16 operand tile.  K-major: one 64 x 128 box.
 // MN-major (columns of row-major X): two 64 (MN) x 64 (K) boxes, 8 KB apart.
 __device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int k0, int mn0,
-                                             int mn_major) {
-  if (mn_major) {
+                                             int kind) {
+  if (kind == 3) {          // columns of row-major X, 3-D map (64 MN, K, MN / 64): both 64-wide blocks in one box
+    umma::tma_load_3d(dst, map, bar, 0, k0, mn0 >> 6);
+  } else if (kind == 1) {   // columns of row-major X: two 64 (MN) x 64 (K) boxes
     umma::tma_load_2d(dst, map, bar, mn0, k0);
     umma::tma_load_2d(dst + 8192, map, bar, mn0 + 64, k0);
-  } else {
+  } else {                  // rows: one 64 (K) x 128 box
     umma::tma_load_2d(dst, map, bar, k0, mn0);
   }
 }
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
   umma::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const uint32_t s0 = umma::smem_u32(smem);
-  const int a_mn = d.a_kind == 1, b_mn = d.b_kind == 1;   // operand = columns of row-major X: MN-major
+  const int a_mn = d.a_kind & 1, b_mn = d.b_kind & 1;   // operand = columns of row-major X: MN-major (kinds 1, 3)
   const uint32_t IDESC = umma::idesc_bf16(128, 128) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
   if (bufs.trace && tid == 0) bufs.trace[8 * blockIdx.x + 1] = gtimer();
 
@@ -140,11 +142,11 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
       if (kb >= S) umma::mbar_wait(&empty_bar[st], ((kb / S) - 1) & 1);
       const uint32_t sa = s0 + st * STAGE;
       umma::mbar_arrive_expect_tx(&full_bar[st], BYTES);
-      load_operand(sa, ma, &full_bar[st], kb * 64, m0, a_mn);
-      load_operand(sa + TILE, mb, &full_bar[st], kb * 64, n0, b_mn);
+      load_operand(sa, ma, &full_bar[st], kb * 64, m0, d.a_kind);
+      load_operand(sa + TILE, mb, &full_bar[st], kb * 64, n0, d.b_kind);
       if (SPLIT) {
-        load_operand(sa + 2 * TILE, ma + 1, &full_bar[st], kb * 64, m0, a_mn);
-        load_operand(sa + 3 * TILE, mb + 1, &full_bar[st], kb * 64, n0, b_mn);
+        load_operand(sa + 2 * TILE, ma + 1, &full_bar[st], kb * 64, m0, d.a_kind);
+        load_operand(sa + 3 * TILE, mb + 1, &full_bar[st], kb * 64, n0, d.b_kind);
       }
     }
   } else if (tid == 32) {
@@ -359,6 +361,18 @@ orth_status_t build_ns_tma(Plan& p) {
         const __nv_bfloat16* ptr = (kind == 2 ? (lo ? b.rl : b.rh) : (lo ? b.xl[par] : b.xh[par])) + off;
         CUtensorMap m;
         std::memset(&m, 0, sizeof(m));
+        if (kind == 3) {   // MN-major, 3-D (64 columns, K rows, column blocks): a 128-wide operand in one box
+          const cuuint64_t dims3[3] = {64, (cuuint64_t)K, (cuuint64_t)(rows / 64)};
+          const cuuint64_t strides3[2] = {(cuuint64_t)ld * 2, 128};
+          const cuuint32_t box3[3] = {64, 64, 2};
+          const cuuint32_t es3[3] = {1, 1, 1};
+          if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(ptr), dims3, strides3, box3,
+                  es3, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return -1;
+          maps.push_back(m);
+          continue;
+        }
         // MN-major: inner dim = the operand's MN extent (columns of X), outer = K (rows of X)
         const cuuint64_t dims[2] = {(cuuint64_t)(kind == 1 ? rows : K), (cuuint64_t)(kind == 1 ? K : rows)};
         const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
@@ -372,6 +386,15 @@ orth_status_t build_ns_tma(Plan& p) {
       }
     return base;
   };
+  // Gram operands that are columns of X (kind 1) with a 64-multiple extent load through a 3-D map (kind 3:
+  // one TMA per operand and K block instead of two; the issuing thread pays ~90 cycles per TMA, measured
+  // by tools/micro/tma_ld_bw.cu).  Update operands keep 2-D maps (their 64-wide tiles load one block).
+  static const bool no3d = std::getenv("ORTH_NS_NO_TMA3D") != nullptr;   // A/B switch
+  for (auto& d : p.ns_gram) {
+    if (no3d) break;
+    if (d.a_kind == 1 && d.M % 64 == 0) d.a_kind = 3;
+    if (d.b_kind == 1 && d.N % 64 == 0) d.b_kind = 3;
+  }
   auto operand_map = [&](const NsDesc& d, bool a) {
     const int kind = a ? d.a_kind : d.b_kind;
     const int64_t off = a ? d.a_off : d.b_off, ld = a ? d.lda : d.ldb;

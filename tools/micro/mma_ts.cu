@@ -1,0 +1,94 @@
+// tcgen05.mma issue cost with the A operand in TMEM (ts form) vs shared memory (ss form): one CTA per
+// SM, one thread issues NMMA MMAs (M=128, N given, K=16) into one accumulator; optionally each MMA is
+// preceded by a tcgen05.cp of its 128 x 256-bit A slice from shared memory (the operand streamed
+// through TMEM).  Reports cycles per MMA.
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../../paper_2601_13776_b200/csrc/umma.cuh"
+using namespace orth;
+
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+               "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void cp_128x256(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
+template <int N, int MODE>   // MODE 0: ss; 1: ts, A resident in TMEM; 2: ts + tcgen05.cp per MMA;
+                             // 3: ss with both operands MN-major (the NS Gram's column operands)
+__global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  for (int i = threadIdx.x; i < 131072 / 4; i += 128) {
+    uint32_t h = (uint32_t)i * 2654435761u;
+    h ^= h >> 13;
+    reinterpret_cast<uint32_t*>(sm)[i] = (((120u + h % 7u) << 7) | ((h >> 4) & 0x7fu)) * 0x10001u;
+  }
+  if (threadIdx.x < 32) umma::tmem_alloc(&tbase, 512);
+  if (threadIdx.x == 0) { umma::mbar_init(&bar, 1); umma::fence_mbar_init(); }
+  umma::fence_proxy_async_smem();
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t a = umma::smem_u32(sm), b = a + 65536;
+    constexpr uint32_t ID = umma::idesc_bf16(128, N) | (MODE == 3 ? (1u << 15) | (1u << 16) : 0u);
+    const uint32_t at = tbase + 256;   // A slices: 8 columns each, 4 of them (one 64-deep K block)
+    if (MODE == 1)
+      for (int q = 0; q < 4; ++q) cp_128x256(at + 8 * q, umma::sdesc_sw128(a + 32 * q));
+    const unsigned long long t0 = clock64();
+    for (int i = 0; i < nmma; ++i) {
+      const int q = i & 3;
+      if (MODE == 3) {
+        umma::mma_bf16(tbase, umma::sdesc_sw128_mn(a + 2048 * q, 8192), umma::sdesc_sw128_mn(b + 2048 * q, 8192), ID,
+                       i > 0);
+      } else if (MODE == 0) {
+        umma::mma_bf16(tbase, umma::sdesc_sw128(a + 32 * q), umma::sdesc_sw128(b + 32 * q), ID, i > 0);
+      } else {
+        if (MODE == 2) cp_128x256(at + 8 * q, umma::sdesc_sw128(a + 16384 * ((i >> 2) & 1) + 32 * q));
+        mma_ts(tbase, at + 8 * q, umma::sdesc_sw128(b + 32 * q), ID, i > 0);
+      }
+    }
+    umma::mma_commit(&bar);
+    umma::mbar_wait(&bar, 0);
+    out[blockIdx.x] = clock64() - t0;
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) umma::tmem_dealloc(tbase, 512);
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 8 * 148);
+  auto run = [&](auto kern, const char* name) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000);
+    const int nm = 65536;
+    kern<<<148, 128, 140000>>>(nm, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    unsigned long long h[148];
+    cudaMemcpy(h, d, 8 * 148, cudaMemcpyDeviceToHost);
+    double s = 0;
+    for (int c = 0; c < 148; ++c) s += (double)h[c] / 148;
+    printf("%-28s %.1f cycles/MMA (%s)\n", name, s / nm, cudaGetErrorString(e));
+  };
+  run(k<128, 3>, "ss  N=128 MN-major A, B");
+  run(k<256, 3>, "ss  N=256 MN-major A, B");
+  run(k<64, 0>, "ss  N=64");
+  run(k<64, 1>, "ts  N=64 (A resident)");
+  run(k<64, 2>, "ts  N=64 (+cp per MMA)");
+  run(k<128, 0>, "ss  N=128");
+  run(k<128, 1>, "ts  N=128 (A resident)");
+  run(k<128, 2>, "ts  N=128 (+cp per MMA)");
+  run(k<192, 0>, "ss  N=192");
+  run(k<192, 1>, "ts  N=192 (A resident)");
+  run(k<192, 2>, "ts  N=192 (+cp per MMA)");
+  run(k<256, 0>, "ss  N=256");
+  run(k<256, 1>, "ts  N=256 (A resident)");
+  run(k<256, 2>, "ts  N=256 (+cp per MMA)");
+}

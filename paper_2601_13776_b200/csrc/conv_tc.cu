@@ -158,10 +158,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   umma::griddep_launch_dependents();
   uint8_t* smem = umma::align1024_smem(smem_raw);
   constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
-  int* tab = reinterpret_cast<int*>(smem + S * STAGE);   // [valid tap j][128] input pixel, -1 = padding
   __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int tap_id[MAX_TAPS];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cs = a.cs, crank = cs > 1 ? (int)umma::cluster_ctarank() : 0;
@@ -193,23 +191,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ------------------------------------------------------------ producers
     const int c = tid & 7, rbase = tid >> 3;   // A rows rbase + 32 i
     if (tid == 0) umma::tma_prefetch_desc(&tmB);
-    const uint32_t tab_s = umma::smem_u32(tab);
     int it = 0, st = 0, ph = 0;                // ring position of k-block `it`
+    // No shared pixel table and no producer barriers: a warp's 32 threads gather 16 distinct rows (4 row
+    // bases x 4 row groups); lane L < 16 decodes row 4 warp + (L & 3) + 32 (L >> 2) once per tile and
+    // resolves its input pixel per tap, the other lanes take theirs by shuffle.  The producers thus start
+    // a tile's first stages while the MMAs still consume the previous tile's.
+    const int jj = lane >> 3;                                    // this thread's row base = 4 warp + jj
+    const int myrow = 4 * warp + (lane & 3) + 32 * ((lane >> 2) & 3);
+    const bool wrap_fast = a.H > a.d * (a.k - 1) + a.pt && a.W > a.d * (a.k - 1) + a.pl;   // one add suffices
     for (int ct = cid; ct < a.num_ctiles; ct += ncl) {
       const int khalf = ct / a.base_ctiles;
       const TileInfo t = decode_tile(a, ct - khalf * a.base_ctiles, crank, BN);
       const int c_lo = khalf * (a.cr_g / a.ksplit), c_hi = c_lo + a.cr_g / a.ksplit;
-      umma::named_bar_sync(1, NPROD);          // everyone is done reading the previous table / tap list
-      int nt = 0;
-      for (int tap = 0; tap < kk2; ++tap)
-        if (tap_valid(a, t.phase, tap)) {
-          if (tid == 0) tap_id[nt] = tap;
-          ++nt;
-        }
-      umma::named_bar_sync(1, NPROD);
-      {  // each row decoded once; the two thread halves split the taps
-        const int r = tid & 127, m = t.m0 + r;
-        int nb = -1, hb = 0, wb = 0;   // image, base row / column (tap 0)
+      int nb = -1, hb = 0, wb = 0;   // my decoded row: image (-1: past the phase), base row / column (tap 0)
+      {
+        const int m = t.m0 + myrow;
         if (m < t.cnt) {
           if (!a.transposed) {
             const int hw = a.Ho * a.Wo, n = m / hw, rr = m - n * hw, u = rr / a.Wo;
@@ -220,38 +216,41 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             nb = n; hb = t.phase / a.s + a.s * hh + a.pt; wb = t.phase % a.s + a.s * (rr - hh * wp) + a.pl;
           }
         }
-        for (int j = tid >> 7; j < nt; j += 2) {
-          const int tap = tap_id[j], ta = tap / a.k, tb = tap - ta * a.k;
-          int v = -1;
-          if (nb >= 0) {
-            if (!a.transposed) {
-              int h = hb + a.d * ta, w = wb + a.d * tb;
-              bool ok = true;
-              if (a.circ) { h = wrapi(h, a.H); w = wrapi(w, a.W); }
-              else ok = h >= 0 && h < a.H && w >= 0 && w < a.W;
-              if (ok) v = (nb * a.H + h) * a.W + w;
-            } else {
-              int th = hb - a.d * ta, tw = wb - a.d * tb;
-              bool ok = true;
-              if (a.circ) { th = wrapi(th, a.H); tw = wrapi(tw, a.W); }
-              else ok = th >= 0 && tw >= 0;
-              const int u = th / a.s, vv = tw / a.s;   // exact: the phase makes th, tw multiples of s
-              if (ok && u < a.Ho && vv < a.Wo) v = (nb * a.Ho + u) * a.Wo + vv;
-            }
-          }
-          tab[j * 128 + r] = v;
-        }
       }
-      umma::named_bar_sync(1, NPROD);
       const __nv_bfloat16* ig = in + (int64_t)t.g * a.cr_g + c * 8;
       const uint32_t off_r[4] = {umma::sw128_off(rbase, c), umma::sw128_off(rbase + 32, c),
                                  umma::sw128_off(rbase + 64, c), umma::sw128_off(rbase + 96, c)};
-      for (int j = 0; j < nt; ++j) {
-        const int tap = tap_id[j];
-        const uint32_t trow = tab_s + (uint32_t)(j * 128 + rbase) * 4u;
+      for (int tap = 0; tap < kk2; ++tap) {
+        if (!tap_valid(a, t.phase, tap)) continue;
+        const int ta = tap / a.k, tb = tap - ta * a.k;
+        int v = -1;
+        if (nb >= 0) {
+          if (!a.transposed) {
+            int h = hb + a.d * ta, w = wb + a.d * tb;
+            bool ok = true;
+            if (a.circ) {
+              if (wrap_fast) {
+                h += h < 0 ? a.H : (h >= a.H ? -a.H : 0);
+                w += w < 0 ? a.W : (w >= a.W ? -a.W : 0);
+              } else {
+                h = wrapi(h, a.H); w = wrapi(w, a.W);
+              }
+            } else {
+              ok = h >= 0 && h < a.H && w >= 0 && w < a.W;
+            }
+            if (ok) v = (nb * a.H + h) * a.W + w;
+          } else {
+            int th = hb - a.d * ta, tw = wb - a.d * tb;
+            bool ok = true;
+            if (a.circ) { th = wrapi(th, a.H); tw = wrapi(tw, a.W); }
+            else ok = th >= 0 && tw >= 0;
+            const int u = th / a.s, vv = tw / a.s;   // exact: the phase makes th, tw multiples of s
+            if (ok && u < a.Ho && vv < a.Wo) v = (nb * a.Ho + u) * a.Wo + vv;
+          }
+        }
         int pix[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) pix[i] = umma::ld_shared_s32(trow + 128u * i);
+        for (int i = 0; i < 4; ++i) pix[i] = __shfl_sync(0xffffffffu, v, jj + 4 * i);
         for (int c0 = c_lo; c0 < c_hi; c0 += 64, ++it) {
 #ifdef ORTH_CONV_TRACE
           const long long tw0 = clock64();
@@ -736,8 +735,7 @@ int launch_ws(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const
               const TcConvArgs& a0, cudaStream_t stream) {
   g_conv_variant = BN == 256 ? ORTH_CV_GATHER256 : BN == 128 ? ORTH_CV_GATHER128 : BN == 64 ? ORTH_CV_GATHER64 : ORTH_CV_GATHER32;
   TcConvArgs a = a0;
-  // the pixel table only needs this layer's taps (k^2 <= MAX_TAPS)
-  size_t smem = 1024 + (size_t)S * (128 * 128 + BN * 128) + (size_t)a.k * a.k * 128 * 4;
+  size_t smem = 1024 + (size_t)S * (128 * 128 + BN * 128);
   // TMA-store epilogue for forward tiles (output = consecutive pixels), ORTH_CONV_NO_TMA_OUT=1 off
   static const bool no_tma_out = std::getenv("ORTH_CONV_NO_TMA_OUT") != nullptr;
   CUtensorMap ty;
@@ -745,7 +743,7 @@ int launch_ws(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const
   a.tma_out = 0;
   if (!no_tma_out && !a.transposed && BN >= 128 && a.cs == 1 && ((uintptr_t)out & 15) == 0 && a.out_C % 8 == 0 &&
       smem + 17 * 1024 <= 227 * 1024) {
-    const size_t off = (((size_t)S * (128 * 128 + BN * 128) + (size_t)a.k * a.k * 128 * 4) + 1023) & ~size_t(1023);
+    const size_t off = ((size_t)S * (128 * 128 + BN * 128) + 1023) & ~size_t(1023);
     auto enc = tensor_map_encoder();
     const cuuint64_t dims[2] = {(cuuint64_t)a.out_C, (cuuint64_t)a.N * a.Ho * a.Wo};
     const cuuint64_t strides[1] = {(cuuint64_t)a.out_C * 2};
@@ -897,23 +895,10 @@ int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, cons
                     : launch_pair<128, 6>(in, w, w_rows, bias, out, a, s);
   }
 #endif
-  if (a.k > 7) {   // the pixel table (k^2 x 128 x 4 B, 86.5 KB at 13 x 13) leaves room for fewer stages
-    switch (bn) {
-      case 256: return launch_ws<256, 2>(in, w, w_rows, bias, out, a, s);
-      case 128: return launch_ws<128, 4>(in, w, w_rows, bias, out, a, s);
-      case 64: return launch_ws<64, 5>(in, w, w_rows, bias, out, a, s);
-      default: return launch_ws<32, 6>(in, w, w_rows, bias, out, a, s);
-    }
-  }
-  switch (bn) {
-    // deepest ring that fits 227 KB with the 3x3 table (4.6 KB); larger kernels take the shallower one
+  switch (bn) {   // deepest ring that fits 227 KB (the producers keep no pixel table in shared memory)
     case 256: return launch_ws<256, 4>(in, w, w_rows, bias, out, a, s);
-    case 128:
-      if (a.k <= 3) return launch_ws<128, 6>(in, w, w_rows, bias, out, a, s);
-      return launch_ws<128, 5>(in, w, w_rows, bias, out, a, s);
-    case 64:
-      if (a.k <= 3) return launch_ws<64, 9>(in, w, w_rows, bias, out, a, s);
-      return launch_ws<64, 7>(in, w, w_rows, bias, out, a, s);
+    case 128: return launch_ws<128, 6>(in, w, w_rows, bias, out, a, s);
+    case 64: return launch_ws<64, 9>(in, w, w_rows, bias, out, a, s);
     default: return launch_ws<32, 8>(in, w, w_rows, bias, out, a, s);
   }
 }

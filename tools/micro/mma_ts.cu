@@ -18,23 +18,56 @@ __device__ __forceinline__ void cp_128x256(uint32_t taddr, uint64_t sdesc) {
 }
 
 template <int N, int MODE>   // MODE 0: ss; 1: ts, A resident in TMEM; 2: ts + tcgen05.cp per MMA;
-                             // 3: ss with both operands MN-major (the NS Gram's column operands)
+                             // 3: ss with both operands MN-major (the NS Gram's column operands);
+                             // 4: ss in conv_ws's K-block loop shape: per 4 MMAs an mbarrier wait on an
+                             //    already-completed barrier, proxy + tcgen05 fences, a commit to a barrier;
+                             // 5: as 4 without the proxy fence; 6: as 4 without the wait;
+                             // 7: as 6 while warps 1-3 continuously read the other TMEM half (an epilogue);
+                             // 8: as 6 while warps 1-3 continuously write shared memory (st.shared.v4);
+                             // 9: as 6 with the operands cycling through 4 distinct 48 KB stages (conv_ws)
 __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, done_bar, emp[4];
   __shared__ uint32_t tbase;
-  for (int i = threadIdx.x; i < 131072 / 4; i += 128) {
+  for (int i = threadIdx.x; i < 200704 / 4; i += 128) {
     uint32_t h = (uint32_t)i * 2654435761u;
     h ^= h >> 13;
     reinterpret_cast<uint32_t*>(sm)[i] = (((120u + h % 7u) << 7) | ((h >> 4) & 0x7fu)) * 0x10001u;
   }
   if (threadIdx.x < 32) umma::tmem_alloc(&tbase, 512);
-  if (threadIdx.x == 0) { umma::mbar_init(&bar, 1); umma::fence_mbar_init(); }
+  if (threadIdx.x == 0) {
+    umma::mbar_init(&bar, 1);
+    umma::mbar_init(&done_bar, 1);
+    for (int i = 0; i < 4; ++i) umma::mbar_init(&emp[i], 1);
+    umma::fence_mbar_init();
+  }
   umma::fence_proxy_async_smem();
   umma::tc_fence_before();
   __syncthreads();
   umma::tc_fence_after();
+  __shared__ volatile int stop;
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  if ((MODE == 7 || MODE == 8) && threadIdx.x >= 32) {
+    const int w = threadIdx.x >> 5;
+    float acc = 0.f;
+    if (MODE == 7) {
+      while (!stop) {
+        float v[32];
+        umma::tmem_ld32(tbase + ((uint32_t)(w * 32) << 16) + 256 + 64 * (w - 1), v);
+        acc += v[0];
+      }
+    } else {
+      float4* p = reinterpret_cast<float4*>(sm + 184320);
+      int it = 0;
+      while (!stop) {
+        for (int e = threadIdx.x - 32; e < 1024; e += 96) p[e] = make_float4(it, e, 1.f, 2.f);
+        ++it;
+      }
+    }
+    if (acc == 12345.f) out[0] = 1;
+  }
   if (threadIdx.x == 0) {
     const uint32_t a = umma::smem_u32(sm), b = a + 65536;
     constexpr uint32_t ID = umma::idesc_bf16(128, N) | (MODE == 3 ? (1u << 15) | (1u << 16) : 0u);
@@ -42,7 +75,22 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
     if (MODE == 1)
       for (int q = 0; q < 4; ++q) cp_128x256(at + 8 * q, umma::sdesc_sw128(a + 32 * q));
     const unsigned long long t0 = clock64();
-    for (int i = 0; i < nmma; ++i) {
+    if (MODE >= 4) {
+      umma::mbar_arrive(&done_bar);   // phase 0 completes: every wait below hits the already-complete path
+      for (int kb = 0; kb < nmma / 4; ++kb) {
+        if (MODE == 4 || MODE == 5) umma::mbar_wait(&done_bar, 0);
+        if (MODE != 5) umma::fence_proxy_async_smem();
+        umma::tc_fence_after();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t sa = MODE == 9 ? a + (uint32_t)(kb & 3) * 49152u : a;
+          const uint32_t sb = MODE == 9 ? sa + 16384u : b;
+          umma::mma_bf16(tbase, umma::sdesc_sw128(sa + 32 * q), umma::sdesc_sw128(sb + 32 * q), ID, (kb | q) != 0);
+        }
+        umma::mma_commit(&emp[kb & 3]);
+      }
+    }
+    for (int i = 0; i < (MODE >= 4 ? 0 : nmma); ++i) {
       const int q = i & 3;
       if (MODE == 3) {
         umma::mma_bf16(tbase, umma::sdesc_sw128_mn(a + 2048 * q, 8192), umma::sdesc_sw128_mn(b + 2048 * q, 8192), ID,
@@ -57,6 +105,7 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
     umma::mma_commit(&bar);
     umma::mbar_wait(&bar, 0);
     out[blockIdx.x] = clock64() - t0;
+    stop = 1;
   }
   umma::tc_fence_before();
   __syncthreads();
@@ -67,9 +116,9 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 8 * 148);
   auto run = [&](auto kern, const char* name) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 202000);
     const int nm = 65536;
-    kern<<<148, 128, 140000>>>(nm, d);
+    kern<<<148, 128, 202000>>>(nm, d);
     cudaError_t e = cudaDeviceSynchronize();
     unsigned long long h[148];
     cudaMemcpy(h, d, 8 * 148, cudaMemcpyDeviceToHost);
@@ -77,6 +126,14 @@ int main() {
     for (int c = 0; c < 148; ++c) s += (double)h[c] / 148;
     printf("%-28s %.1f cycles/MMA (%s)\n", name, s / nm, cudaGetErrorString(e));
   };
+  run(k<256, 9>, "ss  N=256 4-stage ring");
+  run(k<128, 9>, "ss  N=128 4-stage ring");
+  run(k<256, 7>, "ss  N=256 + TMEM readers");
+  run(k<128, 7>, "ss  N=128 + TMEM readers");
+  run(k<256, 8>, "ss  N=256 + smem writers");
+  run(k<256, 4>, "ss  N=256 conv_ws loop");
+  run(k<256, 5>, "ss  N=256 conv_ws loop, no proxy fence");
+  run(k<256, 6>, "ss  N=256 conv_ws loop, no wait");
   run(k<128, 3>, "ss  N=128 MN-major A, B");
   run(k<256, 3>, "ss  N=256 MN-major A, B");
   run(k<64, 0>, "ss  N=64");

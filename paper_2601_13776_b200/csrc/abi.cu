@@ -172,9 +172,12 @@ orth_status_t orth_orthogonalize(orth_plan_t plan, const float* params, float* o
     auto gp = [&](int t) { return (mode == ORTH_BF16X3 || t >= T - P.opts.polish_iters) ? 3 : 1; };
     auto up = [&](int t) { return mode == ORTH_BF16X3 ? 3 : 1; };
     auto x_lo = [&](int t) { return t >= T || gp(t) == 3 || up(t) == 3; };   // t == T: the residual Gram
+    // The FP32 master X is updated IN PLACE in ortho_out (an update tile's epilogue is the only reader of
+    // its FP32 C block, and it overwrites that block): only the BF16 operand copies ping-pong.  This keeps
+    // the NS working set (FP32 X, BF16 hi/lo X x 2, R) inside the 126 MB L2 for ImageNet-size networks.
     if (!e) {
       Trace tr(P, ORTH_TK_SCALE, -1, stream);
-      e = launch_scale_bf16(P, params, x0, par, x_lo(0), stream);
+      e = launch_scale_bf16(P, params, bufs[BUF_X], par, x_lo(0), stream);
     }
     static const bool phased = std::getenv("ORTH_NS_PHASED") != nullptr;   // A/B switch: per-phase kernels
     if (!e && P.nsp_ctas > 0 && 2 * T + 1 <= kNspMaxPhases && !phased) {

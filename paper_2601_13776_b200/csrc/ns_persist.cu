@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int h = 0; h < nh; ++h) {
         const int n0 = (tl.local % tiles_n) * (128 * nh) + h * 128 + ch * 64;
         if (upd) {   // C = X (fp32) rows m0.., cols n0..n0+63 -> Sc[0..1]
-          const float* Cm = pick(bufs.X, par) + f_off;
+          const float* Cm = bufs.X[0] + f_off;
           const bool fv4 = (ldf & 3) == 0;
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int64_t b_off = upd ? (dp->bx_off) : (dp->br_off);
           __nv_bfloat16* oh = (upd ? pick(bufs.xh, par ^ 1) : bufs.rh) + b_off;
           __nv_bfloat16* ol = (upd ? pick(bufs.xl, par ^ 1) : bufs.rl) + b_off;
-          float* F = (upd ? pick(bufs.X, par ^ 1) : bufs.R) + f_off;
+          float* F = (upd ? bufs.X[0] : bufs.R) + f_off;
           const bool fv4 = (ldf & 3) == 0;
           const float alpha = (dp->alpha), beta = (dp->beta), diag = (dp->diag);
           const float* Scc = Sc + c * 1024;
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int M = (dp->M), N = (dp->N);
         const int buf = acc & 1;
         if (upd) {   // C = X (fp32) rows m0.., cols n0..n0+cw-1 -> Sc[0..nch-1]
-          const float* Cm = pick(bufs.X, par) + f_off;
+          const float* Cm = bufs.X[0] + f_off;
           const bool fv4 = (ldf & 3) == 0;
 #pragma unroll 1
           for (int c = 0; c < nch; ++c) {
@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int64_t b_off = upd ? (dp->bx_off) : (dp->br_off);
           __nv_bfloat16* oh = (upd ? pick(bufs.xh, par ^ 1) : bufs.rh) + b_off;
           __nv_bfloat16* ol = (upd ? pick(bufs.xl, par ^ 1) : bufs.rl) + b_off;
-          float* F = (upd ? pick(bufs.X, par ^ 1) : bufs.R) + f_off;
+          float* F = (upd ? bufs.X[0] : bufs.R) + f_off;
           const bool fv4 = (ldf & 3) == 0;
           const float alpha = (dp->alpha), beta = (dp->beta), diag = (dp->diag);
           const float* Scc = Sc + c * 1024;

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
       const int h = u >> 3, e = tid + 256 * (u & 7), r = e >> 4, c4 = (e & 15) * 4;
       const int i = m0 + r, j0 = n0 + h * 64 + c4;
       cpre[u] = (d.epi == 1 && fv && i < d.M && j0 + 4 <= d.N)
-                    ? __ldg(reinterpret_cast<const float4*>(pick(bufs.X, par) + d.f_off + (int64_t)i * d.ldf + j0))
+                    ? __ldg(reinterpret_cast<const float4*>(bufs.X[0] + d.f_off + (int64_t)i * d.ldf + j0))
                     : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
@@ -197,8 +197,8 @@ __global__ void __launch_bounds__(256, (NPASS == 1 ? 2 : 1))
   const int ldb16 = upd ? d.ldx : d.ldr;   // padded row length of the row-major bf16 outputs
   __nv_bfloat16* oh = upd ? pick(bufs.xh, par ^ 1) + d.bx_off : bufs.rh + d.br_off;
   __nv_bfloat16* ol = upd ? pick(bufs.xl, par ^ 1) + d.bx_off : bufs.rl + d.br_off;
-  float* F = upd ? pick(bufs.X, par ^ 1) + d.f_off : bufs.R + d.f_off;
-  const float* Cm = pick(bufs.X, par) + d.f_off;
+  float* F = upd ? bufs.X[0] + d.f_off : bufs.R + d.f_off;
+  const float* Cm = bufs.X[0] + d.f_off;
   const bool wf = upd || write_f;
   constexpr int LDF = 68;
   float* Sf = reinterpret_cast<float*>(smem);                              // [128][68] fp32

@@ -603,12 +603,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nk = (d.K + 63) / 64, a_mn = d.a_kind & 1, b_mn = d.b_kind & 1, ak = d.a_kind, bk = d.b_kind;
           const bool sym = gram && m0 == n0;   // diagonal Gram tile: B == A, loaded once
           const bool b_half = tw == 64 && b_mn;   // MN-major B: only the first 64-wide box
+          NSP_TRACE(unsigned long long w_empty = 0;)
           const uint32_t stage_bytes = sym ? kSlot / 2 : (b_half ? kSlot / 2 + 8192 : kSlot);
           const CUtensorMap* ma = maps + d.map_a + 2 * par;
           const CUtensorMap* mb = maps + d.map_b + 2 * par;
           for (int kb = 0; kb < nk; ++kb) {
             if (w == 2 && cnt % kSlots == kSlots - 1) ++cnt;   // a hi/lo stage takes two adjacent slots
             const int s = cnt % kSlots;
+            NSP_TRACE(const unsigned long long te0 = ph.ttrace ? gtimer() : 0;)
             for (int qs = s; qs < s + w; ++qs) {
               if ((used >> qs) & 1u) {
                 umma::mbar_wait(&empty_bar[qs], (epar >> qs) & 1u);
@@ -616,6 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               used |= 1u << qs;
             }
+            NSP_TRACE(if (ph.ttrace) w_empty += gtimer() - te0;)
             const uint32_t sa = ring + s * kSlot;
             umma::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)w * stage_bytes);
             load_operand(sa, ma, &full_bar[s], kb * 64, m0, ak);
@@ -628,6 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             cnt += w;
           }
+          NSP_TRACE(if (ph.ttrace) ph.ttrace[16 * idx + 15] = w_empty;)
         }
       }
     }
@@ -659,10 +663,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (acc >= 2) umma::mbar_wait(&tempty_bar[buf], ((acc >> 1) - 1) & 1);
           umma::tc_fence_after();
           const uint32_t dt = tmem + buf * 128;
+          NSP_TRACE(unsigned long long w_full = 0;)
           for (int kb = 0; kb < nk; ++kb) {
             if (w == 2 && cnt % kSlots == kSlots - 1) ++cnt;
             const int s = cnt % kSlots;
+            NSP_TRACE(const unsigned long long tw0 = ph.ttrace ? gtimer() : 0;)
             umma::mbar_wait(&full_bar[s], (fpar >> s) & 1u);
+            NSP_TRACE(if (ph.ttrace && kb > 0) w_full += gtimer() - tw0;)
             fpar ^= 1u << s;
             umma::tc_fence_after();
             NSP_TRACE(if (ph.ttrace && kb == 0) ph.ttrace[16 * idx + 4] = gtimer());
@@ -681,6 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (w == 2) umma::mma_commit(&empty_bar[s + 1]);
             cnt += w;
           }
+          NSP_TRACE(if (ph.ttrace) ph.ttrace[16 * idx + 14] = w_full;)
           umma::mma_commit(&tfull_bar[buf]);
           ++acc;
         }
@@ -1232,6 +1240,7 @@ static void flow_trace_report(const Plan& p, const uint8_t* flags, int nphases, 
     for (int ph = 0; ph < nphases; ++ph) {
       unsigned long long dmin = ~0ull, dmax = 0, emax = 0, cmin = ~0ull;
       double dur = 0, d_load = 0, d_mma = 0, d_epiq = 0, d_epi = 0, d_pub = 0, sub[6] = {0, 0, 0, 0, 0, 0};
+      double d_fw = 0, d_ew = 0;
       int cnt = 0;
       for (int i = 0; i < n; ++i)
         if (items[i].p == ph && items[i].desc == m) {
@@ -1247,6 +1256,8 @@ static void flow_trace_report(const Plan& p, const uint8_t* flags, int nphases, 
           d_epi += (double)q[7] - (double)q[5];    // accumulator -> last store issued (warp 0)
           d_pub += (double)q[2] - (double)q[7];    // -> fences, barrier, counter bump
           for (int z = 0; z < 6; ++z) sub[z] += (double)q[8 + z] - (double)(z == 0 ? q[5] : q[7 + z]);
+          d_fw += (double)q[14];
+          d_ew += (double)q[15];
           ++cnt;
         }
       if (!cnt) continue;
@@ -1255,6 +1266,8 @@ static void flow_trace_report(const Plan& p, const uint8_t* flags, int nphases, 
                   (flags[ph] & 1) ? "gram" : "upd ", cnt, (flags[ph] & 2) ? " 3p" : "   ", (cmin - t0) * 1e-3,
                   (dmin - t0) * 1e-3, (dmax - t0) * 1e-3, (emax - t0) * 1e-3, dur / cnt * 1e-3, d_load / cnt * 1e-3,
                   d_mma / cnt * 1e-3, d_epi / cnt * 1e-3, d_pub / cnt * 1e-3, d_epiq / cnt * 1e-3);
+      std::printf("        MMA thread waiting for full stages %.2f us, producer waiting for empty stages %.2f us\n",
+                  d_fw / cnt * 1e-3, d_ew / cnt * 1e-3);
       std::printf("        epi chunks: drain %.2f cwait %.2f rows %.2f | drain %.2f cwait %.2f rows %.2f us\n",
                   sub[0] / cnt * 1e-3, sub[1] / cnt * 1e-3, sub[2] / cnt * 1e-3, sub[3] / cnt * 1e-3, sub[4] / cnt * 1e-3,
                   sub[5] / cnt * 1e-3);

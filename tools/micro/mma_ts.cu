@@ -24,7 +24,8 @@ template <int N, int MODE>   // MODE 0: ss; 1: ts, A resident in TMEM; 2: ts + t
                              // 5: as 4 without the proxy fence; 6: as 4 without the wait;
                              // 7: as 6 while warps 1-3 continuously read the other TMEM half (an epilogue);
                              // 8: as 6 while warps 1-3 continuously write shared memory (st.shared.v4);
-                             // 9: as 6 with the operands cycling through 4 distinct 48 KB stages (conv_ws)
+                             // 9: as 6 with the operands cycling through 4 distinct 48 KB stages (conv_ws);
+                             // 10: as 9 with both operands MN-major (the NS Gram: 2 x 8 KB blocks per operand)
 __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
@@ -83,9 +84,13 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
         umma::tc_fence_after();
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const uint32_t sa = MODE == 9 ? a + (uint32_t)(kb & 3) * 49152u : a;
-          const uint32_t sb = MODE == 9 ? sa + 16384u : b;
-          umma::mma_bf16(tbase, umma::sdesc_sw128(sa + 32 * q), umma::sdesc_sw128(sb + 32 * q), ID, (kb | q) != 0);
+          const uint32_t sa = MODE >= 9 ? a + (uint32_t)(kb & 3) * 49152u : a;
+          const uint32_t sb = MODE >= 9 ? sa + 16384u : b;
+          if (MODE == 10)
+            umma::mma_bf16(tbase, umma::sdesc_sw128_mn(sa + 2048 * q, 8192), umma::sdesc_sw128_mn(sb + 2048 * q, 8192),
+                           ID | (1u << 15) | (1u << 16), (kb | q) != 0);
+          else
+            umma::mma_bf16(tbase, umma::sdesc_sw128(sa + 32 * q), umma::sdesc_sw128(sb + 32 * q), ID, (kb | q) != 0);
         }
         umma::mma_commit(&emp[kb & 3]);
       }
@@ -126,6 +131,8 @@ int main() {
     for (int c = 0; c < 148; ++c) s += (double)h[c] / 148;
     printf("%-28s %.1f cycles/MMA (%s)\n", name, s / nm, cudaGetErrorString(e));
   };
+  run(k<128, 10>, "ss  N=128 4-stage ring MN-major");
+  run(k<256, 10>, "ss  N=256 4-stage ring MN-major");
   run(k<256, 9>, "ss  N=256 4-stage ring");
   run(k<128, 9>, "ss  N=128 4-stage ring");
   run(k<256, 7>, "ss  N=256 + TMEM readers");

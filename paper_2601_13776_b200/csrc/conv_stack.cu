@@ -70,6 +70,12 @@ struct StackArgs {
   int abuf_bytes, nabuf, sb;      // window ring, weight ring stages
   int stage_off, stage_row, stage_half, slots;
   int flip;                       // weight tap t read from row k^2-1-t (stride-1 adjoint, forward form)
+  // window rows straight from the unpadded NHWC input (no padded copy): per padded row, npc TMA row
+  // pieces (map pc_map, input column pc_col, window column pc_dst); circular: the wrapped halves
+  int npc, pc_map[3], pc_col[3], pc_dst[3];
+};
+struct StackMaps {
+  CUtensorMap m[3];   // 4-D (C, W, H, N) maps, box 64 ch x width x 1 row x 1 image, one per piece width
 };
 
 constexpr int NTHREADS = 256;
@@ -118,7 +124,7 @@ __device__ __forceinline__ int valid_before(int g, int Hp, int Ho) { return (g /
 
 __global__ void __launch_bounds__(NTHREADS, 1)
     conv_stack(const float* __restrict__ bias, const __grid_constant__ StackArgs a,
-               const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+               const __grid_constant__ StackMaps tmA, const __grid_constant__ CUtensorMap tmW,
                const __grid_constant__ CUtensorMap tmY) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = umma::align1024_smem(smem_raw);
@@ -159,21 +165,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   };
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ window producer
-      umma::tma_prefetch_desc(&tmA);
-      int u = 0;
-      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
-        int g0, n0, grp;
-        decode(tile, g0, n0, grp);
-        for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
-          const int ab = u % NA;
+    // -------------------------------------------------------------- window producer (whole warp)
+    // R padded rows x P pixels x 64 channels straight from the NHWC input: padded row g = n Hp + yy is
+    // input row yy - p_t (circular: wrapped; zeros / past the batch: out of bounds -> zero fill), each as
+    // its npc row pieces; the rows are spread over the 32 lanes (lane 0 posts the byte count first).
+    if (lane < a.npc) umma::tma_prefetch_desc(&tmA.m[a.pc_map[lane]]);
+    int u = 0;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+      int g0, n0, grp;
+      decode(tile, g0, n0, grp);
+      for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
+        const int ab = u % NA;
+        if (lane == 0) {
           if (u >= NA) umma::mbar_wait(&a_empty[ab], ((u / NA) - 1) & 1);
-          const uint32_t dst = abase + ab * a.abuf_bytes;
-          const int c = grp * a.cr_g + c0;
-          // R padded rows x P pixels x 64 channels; rows past the batch are zero-filled (dropped columns)
           umma::mbar_arrive_expect_tx(&a_full[ab], (uint32_t)(a.R * a.P * 128));
-          umma::tma_load_3d(dst, &tmA, &a_full[ab], c, 0, g0);
+        }
+        __syncwarp();
+        const uint32_t dst = abase + ab * a.abuf_bytes;
+        const int c = grp * a.cr_g + c0;
+        for (int y = lane; y < a.R; y += 32) {
+          const int g = g0 + y, n = g / a.Hp, yy = g - n * a.Hp;
+          int h = yy - a.pt;
+          if (a.circ) { h %= a.H; if (h < 0) h += a.H; }
+          const uint32_t row = dst + (uint32_t)(y * a.P) * 128u;
+          for (int pc = 0; pc < a.npc; ++pc)
+            umma::tma_load_4d(row + (uint32_t)a.pc_dst[pc] * 128u, &tmA.m[a.pc_map[pc]], &a_full[ab], c, a.pc_col[pc],
+                              h, n);
         }
       }
     }
@@ -328,6 +345,16 @@ bool stack_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, StackAr
   a.N = N; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo;
   a.k = L.k; a.d = L.d; a.pt = L.pt; a.pl = L.pl; a.circ = circ;
   a.Hp = Hp; a.P = P; a.TH = TH; a.R = TH + ext;
+  if (W > 256) return false;   // TMA box width
+  // window row pieces (pc_map holds the piece width here; launch_conv_fwd_stack turns it into a map index)
+  a.npc = 0;
+  if (circ) {   // row = x[W - p_l, W) | x[0, W) | x[0, p_r)
+    if (L.pl) { a.pc_col[a.npc] = W - L.pl; a.pc_dst[a.npc] = 0; a.pc_map[a.npc] = L.pl; ++a.npc; }
+    a.pc_col[a.npc] = 0; a.pc_dst[a.npc] = L.pl; a.pc_map[a.npc] = W; ++a.npc;
+    if (pr) { a.pc_col[a.npc] = 0; a.pc_dst[a.npc] = L.pl + W; a.pc_map[a.npc] = pr; ++a.npc; }
+  } else {      // one P-wide box from column -p_l: the padding columns are out of bounds (zero fill)
+    a.pc_col[0] = -L.pl; a.pc_dst[0] = 0; a.pc_map[0] = P; a.npc = 1;
+  }
   a.in_C = L.ci_f; a.out_C = L.co_f; a.cr_g = L.ci; a.nout_g = L.co;
   const long long rows = (long long)N * Hp;
   a.tiles_m = (int)((rows + TH - 1) / TH);
@@ -381,12 +408,8 @@ static bool stack_rule(const LayerInfo& L, int Ho, int Wo) {
   return force || (L.co == 128 && Wo >= 24 && Ho >= 24);
 }
 
-int64_t conv_stack_pad_bytes(const LayerInfo& L, int N, int H, int W, int Ho, int Wo) {
-  if (!stack_rule(L, Ho, Wo)) return 0;
-  StackArgs a;
-  if (!stack_args(L, N, H, W, Ho, Wo, a)) return 0;
-  return (int64_t)N * a.Hp * a.P * a.in_C * 2;
-}
+// the windows come straight from the input (TMA row pieces): no padded copy, no scratch
+int64_t conv_stack_pad_bytes(const LayerInfo&, int, int, int, int, int) { return 0; }
 
 int launch_conv_fwd_stack(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
                           int H, int W, int Ho, int Wo, void* stream, int flip) {
@@ -396,33 +419,28 @@ int launch_conv_fwd_stack(const LayerInfo& L, const void* kernel, const float* b
   // loses below (512@4: 49 vs 37 us); see DESIGN.md §9.
   // Default only where it measured faster: 128 output channels per group on images >= 24 px
   // (cfg3 128@28: 103 vs 110 us); ORTH_CONV_STACK=1 forces it wherever it applies, ORTH_CONV_NO_STACK=1 off.
-  if (!L.pad_scratch || !stack_rule(L, Ho, Wo)) return -1;
+  if (!stack_rule(L, Ho, Wo)) return -1;
   if (((uintptr_t)x & 15) != 0 || ((uintptr_t)y & 15) != 0) return -1;
   StackArgs a;
   if (!stack_args(L, N, H, W, Ho, Wo, a)) return -1;
-  const int64_t pad_elems = (int64_t)N * a.Hp * a.P * a.in_C;
-  if (pad_elems * 2 > L.pad_bytes) return -1;   // call larger than the declared grid / batch: the caller falls back
   if (a.num_tiles == 0) return 0;
   a.flip = flip;
   g_conv_variant = ORTH_CV_STACK;
   cudaStream_t s = (cudaStream_t)stream;
+  StackMaps ta;   // one (C, W, H, N) map per distinct piece width: box 64 ch x width x 1 row x 1 image
+  std::memset(&ta, 0, sizeof(ta));
   {
-    pad_kernel<<<(unsigned)((int64_t)N * a.Hp), 256, 0, s>>>((const uint4*)x, (uint4*)L.pad_scratch, N, H, W, a.in_C / 8, a.Hp, a.P, L.pt,
-                                      L.pl, a.circ);
-    if (int e = (int)cudaGetLastError()) return e;
-  }
-  CUtensorMap ta;   // padded rows (C, P, N*Hp): box 64 ch x P px x R rows, SWIZZLE_128B
-  {
-    auto enc = tensor_map_encoder();
-    const cuuint64_t dims[3] = {(cuuint64_t)a.in_C, (cuuint64_t)a.P, (cuuint64_t)N * a.Hp};
-    const cuuint64_t strides[2] = {(cuuint64_t)a.in_C * 2, (cuuint64_t)a.P * a.in_C * 2};
-    const cuuint32_t box[3] = {64, (cuuint32_t)a.P, (cuuint32_t)a.R};
-    const cuuint32_t es[3] = {1, 1, 1};
-    std::memset(&ta, 0, sizeof(ta));
-    if (!enc || enc(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, L.pad_scratch, dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return (int)cudaErrorInvalidValue;
+    int widths[3], nw = 0;
+    for (int pc = 0; pc < a.npc; ++pc) {
+      const int w0 = a.pc_map[pc];
+      int m = 0;
+      while (m < nw && widths[m] != w0) ++m;
+      if (m == nw) {
+        widths[nw++] = w0;
+        if (!conv_act_tmap(&ta.m[m], x, a.in_C, W, H, N, w0, 1)) return (int)cudaErrorInvalidValue;
+      }
+      a.pc_map[pc] = m;
+    }
   }
   CUtensorMap tw;
   if (!make_weight_tmap(&tw, kernel, L.co_f, L.k * L.k, L.ci, 128)) return (int)cudaErrorInvalidValue;

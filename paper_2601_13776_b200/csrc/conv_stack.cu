@@ -3,15 +3,14 @@
 // swapped: D^T[o][w] = sum_{c,a,b} K[o, a, b, c] * window[w + d(aP + b)][c], one
 // tcgen05.mma M = 128 output channels x N = 256 window pixels x K = 16.
 //
-// Window.  A first kernel writes every image padded to Hp = Ho + d(k-1) rows of
-// P = Wo + d(k-1) pixels (circular: wrapped copies; zeros: zeros) into the
-// plan's conv scratch (orth_plan_reserve), so the padded images of the batch
-// form one stream of padded rows g = n Hp + y.  A tile is TH consecutive padded
-// rows (TH P <= 256 window pixels); its input window is those rows plus the
-// d(k-1) below, one 64-channel chunk at a time: ONE 3-D TMA box of R = TH + d(k-1)
-// rows x P pixels x 64 channels, SWIZZLE_128B K-major.  (Loading the window
-// from the unpadded tensor costs one TMA per row piece -- three per row for
-// circular padding -- and measured 4-5x slower for small images.)  The B operand of tap (a, b) is the 256 window pixels starting
+// Window.  The padded images of the batch form one stream of padded rows g = n Hp + y (Hp = Ho + d(k-1)
+// rows of P = Wo + d(k-1) pixels).  A tile is TH consecutive padded rows (TH P <= 256 window pixels); its
+// input window is those rows plus the d(k-1) below, one 64-channel chunk at a time, R = TH + d(k-1)
+// rows x P pixels x 64 channels, SWIZZLE_128B K-major, loaded straight from the NHWC input: every padded
+// row is one TMA box (zero padding: out-of-bounds columns / rows / images fill zeros) or three row pieces
+// (circular: x[W - p_l, W) | x[0, W) | x[0, p_r) of the wrapped input row), the rows spread over the
+// window warp's 32 lanes.  (Round 1 materialised a padded copy first; the extra pass cost ~23 us per
+// cfg3 128@28 layer, ~25 % of the layer.)  The B operand of tap (a, b) is the 256 window pixels starting
 // at d(aP + b) (a descriptor may start inside a swizzle atom: the tensor core
 // swizzles on absolute address bits).  Window pixel w = yl P + x of padded row
 // g0 + yl = n Hp + y is output (n, y, x) when y < Ho and x < Wo; other columns

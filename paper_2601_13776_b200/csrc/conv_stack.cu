@@ -404,7 +404,7 @@ static bool stack_rule(const LayerInfo& L, int Ho, int Wo) {
   static const bool force = std::getenv("ORTH_CONV_STACK") != nullptr;
   static const bool off = std::getenv("ORTH_CONV_NO_STACK") != nullptr;
   if (off) return false;
-  return force || (L.co == 128 && Wo >= 24 && Ho >= 24);
+  return force || (L.co == 128 && Wo >= 16 && Ho >= 16);
 }
 
 // the windows come straight from the input (TMA row pieces): no padded copy, no scratch
@@ -412,12 +412,10 @@ int64_t conv_stack_pad_bytes(const LayerInfo&, int, int, int, int, int) { return
 
 int launch_conv_fwd_stack(const LayerInfo& L, const void* kernel, const float* bias, const void* x, void* y, int N,
                           int H, int W, int Ho, int Wo, void* stream, int flip) {
-  // Opt-in (ORTH_CONV_STACK=1): measured on B200 the M=128 x N=256 MMAs of this kernel run at ~220
-  // cycles (shared-memory bound with the weight stream) and small images waste MMA work on padded
-  // columns (4x4: 56%), so it beats conv_ws only for images >= ~28 px (cfg3 128@28: 103 vs 110 us) and
-  // loses below (512@4: 49 vs 37 us); see DESIGN.md §9.
-  // Default only where it measured faster: 128 output channels per group on images >= 24 px
-  // (cfg3 128@28: 103 vs 110 us); ORTH_CONV_STACK=1 forces it wherever it applies, ORTH_CONV_NO_STACK=1 off.
+  // Default where it measured faster than the gather conv: 128 output channels per group on images
+  // >= 16 px (B200, no padded copy: cfg3 128@28 75 vs 98 us, cfg2 128@16 41-43 vs 45 us); 256 / 512
+  // channels on small images lose (cfg3 256@14 80 vs 59 us, cfg2 512@4 63 vs 35 us: padded columns waste
+  // MMA work).  ORTH_CONV_STACK=1 forces it wherever it applies, ORTH_CONV_NO_STACK=1 turns it off.
   if (!stack_rule(L, Ho, Wo)) return -1;
   if (((uintptr_t)x & 15) != 0 || ((uintptr_t)y & 15) != 0) return -1;
   StackArgs a;

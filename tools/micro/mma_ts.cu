@@ -25,7 +25,9 @@ template <int N, int MODE>   // MODE 0: ss; 1: ts, A resident in TMEM; 2: ts + t
                              // 7: as 6 while warps 1-3 continuously read the other TMEM half (an epilogue);
                              // 8: as 6 while warps 1-3 continuously write shared memory (st.shared.v4);
                              // 9: as 6 with the operands cycling through 4 distinct 48 KB stages (conv_ws);
-                             // 10: as 9 with both operands MN-major (the NS Gram: 2 x 8 KB blocks per operand)
+                             // 10: as 9 with both operands MN-major (the NS Gram: 2 x 8 KB blocks per operand);
+                             // 11: A rows starting at 0 / 58 / 116 (an unaligned window row offset, the kernel-row
+                             //     conv), B fixed; 12: as 11 with aligned offsets 0 / 64 / 128
 __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
@@ -84,8 +86,10 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
         umma::tc_fence_after();
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const uint32_t sa = MODE >= 9 ? a + (uint32_t)(kb & 3) * 49152u : a;
-          const uint32_t sb = MODE >= 9 ? sa + 16384u : b;
+          const uint32_t sa = MODE == 11 ? a + (uint32_t)((kb % 3) * 58) * 128u
+                              : MODE == 12 ? a + (uint32_t)((kb % 3) * 64) * 128u
+                              : MODE >= 9 ? a + (uint32_t)(kb & 3) * 49152u : a;
+          const uint32_t sb = MODE >= 11 ? a + 65536u : MODE >= 9 ? sa + 16384u : b;
           if (MODE == 10)
             umma::mma_bf16(tbase, umma::sdesc_sw128_mn(sa + 2048 * q, 8192), umma::sdesc_sw128_mn(sb + 2048 * q, 8192),
                            ID | (1u << 15) | (1u << 16), (kb | q) != 0);
@@ -131,6 +135,9 @@ int main() {
     for (int c = 0; c < 148; ++c) s += (double)h[c] / 148;
     printf("%-28s %.1f cycles/MMA (%s)\n", name, s / nm, cudaGetErrorString(e));
   };
+  run(k<192, 11>, "ss  N=192 A at rows 0/58/116");
+  run(k<192, 12>, "ss  N=192 A at rows 0/64/128");
+  run(k<128, 11>, "ss  N=128 A at rows 0/58/116");
   run(k<128, 10>, "ss  N=128 4-stage ring MN-major");
   run(k<256, 10>, "ss  N=256 4-stage ring MN-major");
   run(k<256, 9>, "ss  N=256 4-stage ring");

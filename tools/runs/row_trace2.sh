@@ -1,0 +1,4 @@
+ORTH_NVCC_FLAGS="-DORTH_CONV_TRACE -DORTH_ROW_EXP_NOEPI" python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+python tools/conv_one.py 64 64 3 1 1 1 circular 56 256 2>&1 | grep conv_pad | tail -1
+ORTH_NVCC_FLAGS="-DORTH_CONV_TRACE" python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+python tools/conv_one.py 64 64 3 1 1 1 circular 56 256 2>&1 | grep conv_pad | tail -1

@@ -1,0 +1,45 @@
+// The NS epilogue's store pattern in isolation: 8 warps per CTA, each writes a 32-row x 32-column BF16
+// chunk as 8 iterations of (8 lanes x 8 B contiguous per row, 4 rows per instruction) into a row-major
+// matrix of pitch `ld` elements; one CTA per SM, each on its own 128 x 128 tile.  Reports ns per chunk.
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void __launch_bounds__(256, 1) k(uint2* __restrict__ out, int ld, int reps, unsigned long long* t) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, rsub = lane >> 3, q4 = lane & 7;
+  const int row0 = (warp & 3) * 32, col0 = (warp >> 2) * 64;
+  uint2* base = out + (size_t)blockIdx.x * 128 * ld / 4;   // this CTA's 128-row band (ld bf16 = ld / 4 uint2)
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  for (int r = 0; r < reps; ++r)
+    for (int c = 0; c < 2; ++c) {
+#pragma unroll 4
+      for (int it = 0; it < 8; ++it) {
+        const int i = row0 + 4 * it + rsub, j = col0 + c * 32 + 4 * q4;
+        base[((size_t)i * ld + j) / 4] = make_uint2(i * 7 + r, j + c);
+      }
+      __syncwarp();
+    }
+  unsigned long long t1;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+  if (threadIdx.x == 0) t[blockIdx.x] = t1 - t0;
+}
+
+int main() {
+  const int ld = 512;   // bf16 elements per row (1 KB)
+  uint2* out;
+  cudaMalloc(&out, (size_t)148 * 128 * ld * 2);
+  unsigned long long* t;
+  cudaMalloc(&t, 8 * 148);
+  for (int ctas : {1, 16, 148}) {
+    const int reps = 200;
+    k<<<ctas, 256>>>(out, ld, 10, t);
+    k<<<ctas, 256>>>(out, ld, reps, t);
+    cudaDeviceSynchronize();
+    unsigned long long h[148];
+    cudaMemcpy(h, t, 8 * ctas, cudaMemcpyDeviceToHost);
+    double s = 0;
+    for (int i = 0; i < ctas; ++i) s += (double)h[i] / ctas;
+    printf("ctas %3d: %.1f ns per 32x32 chunk per warp (%s)\n", ctas, s / (reps * 2), cudaGetErrorString(cudaGetLastError()));
+  }
+}

@@ -403,6 +403,42 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool fv4 = (ldf & 3) == 0;
           const float alpha = (dp->alpha), beta = (dp->beta), diag = (dp->diag);
           const float* Scc = Sc + c * 1024;
+          // Fast path (warp-uniform): an interior 32 x 32 chunk -- every row < M, every column < N (and so
+          // inside the padded BF16 row), 16-byte FP32 rows, no diagonal element -- needs none of the per-element
+          // predicates below: straight-line float4 math and incrementally advanced row pointers.  (The generic
+          // loop costs ~60 instructions per 4-element group; this one ~20.)
+          const int jc0 = n0 + c * 32;
+          const bool interior = m0 + 31 < M && jc0 + 31 < N && fv4 &&
+                                (diag == 0.f || m0 + 31 < jc0 || jc0 + 31 < m0);
+          if (interior) {
+            float* fr = F + (int64_t)(m0 + rsub) * ldf + jc0 + c4;
+            __nv_bfloat16* hr = oh + (int64_t)(m0 + rsub) * ldb16 + jc0 + c4;
+            __nv_bfloat16* lr = ol + (int64_t)(m0 + rsub) * ldb16 + jc0 + c4;
+            const int64_t fstep = 4 * ldf, bstep = 4 * (int64_t)ldb16;
+#pragma unroll 4
+            for (int it = 0; it < 8; ++it) {
+              const int rr = 4 * it + rsub;
+              const int sw = 4 * (q4 ^ (rr & 7));
+              const float4 a = *reinterpret_cast<const float4*>(Sw + rr * 32 + sw);
+              float o0, o1, o2, o3;
+              if (upd) {
+                const float4 cv = *reinterpret_cast<const float4*>(Scc + rr * 32 + sw);
+                o0 = fmaf(alpha, a.x, beta * cv.x); o1 = fmaf(alpha, a.y, beta * cv.y);
+                o2 = fmaf(alpha, a.z, beta * cv.z); o3 = fmaf(alpha, a.w, beta * cv.w);
+              } else {
+                o0 = alpha * a.x; o1 = alpha * a.y; o2 = alpha * a.z; o3 = alpha * a.w;
+              }
+              if (wf) *reinterpret_cast<float4*>(fr) = make_float4(o0, o1, o2, o3);
+              const uint32_t h01 = pack_bf16(o0, o1), h23 = pack_bf16(o2, o3);
+              *reinterpret_cast<uint2*>(hr) = make_uint2(h01, h23);
+              if (write_lo) {
+                const uint32_t l01 = pack_bf16(o0 - __uint_as_float(h01 << 16), o1 - __uint_as_float(h01 & 0xFFFF0000u));
+                const uint32_t l23 = pack_bf16(o2 - __uint_as_float(h23 << 16), o3 - __uint_as_float(h23 & 0xFFFF0000u));
+                *reinterpret_cast<uint2*>(lr) = make_uint2(l01, l23);
+              }
+              fr += fstep; hr += bstep; lr += bstep;
+            }
+          } else
 #pragma unroll 4
           for (int it = 0; it < 8; ++it) {
             const int rr = 4 * it + rsub;
@@ -800,6 +836,42 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool fv4 = (ldf & 3) == 0;
           const float alpha = (dp->alpha), beta = (dp->beta), diag = (dp->diag);
           const float* Scc = Sc + c * 1024;
+          // Fast path (warp-uniform): an interior 32 x 32 chunk -- every row < M, every column < N (and so
+          // inside the padded BF16 row), 16-byte FP32 rows, no diagonal element -- needs none of the per-element
+          // predicates below: straight-line float4 math and incrementally advanced row pointers.  (The generic
+          // loop costs ~60 instructions per 4-element group; this one ~20.)
+          const int jc0 = n0 + c * 32;
+          const bool interior = m0 + 31 < M && jc0 + 31 < N && fv4 &&
+                                (diag == 0.f || m0 + 31 < jc0 || jc0 + 31 < m0);
+          if (interior) {
+            float* fr = F + (int64_t)(m0 + rsub) * ldf + jc0 + c4;
+            __nv_bfloat16* hr = oh + (int64_t)(m0 + rsub) * ldb16 + jc0 + c4;
+            __nv_bfloat16* lr = ol + (int64_t)(m0 + rsub) * ldb16 + jc0 + c4;
+            const int64_t fstep = 4 * ldf, bstep = 4 * (int64_t)ldb16;
+#pragma unroll 4
+            for (int it = 0; it < 8; ++it) {
+              const int rr = 4 * it + rsub;
+              const int sw = 4 * (q4 ^ (rr & 7));
+              const float4 a = *reinterpret_cast<const float4*>(Sw + rr * 32 + sw);
+              float o0, o1, o2, o3;
+              if (upd) {
+                const float4 cv = *reinterpret_cast<const float4*>(Scc + rr * 32 + sw);
+                o0 = fmaf(alpha, a.x, beta * cv.x); o1 = fmaf(alpha, a.y, beta * cv.y);
+                o2 = fmaf(alpha, a.z, beta * cv.z); o3 = fmaf(alpha, a.w, beta * cv.w);
+              } else {
+                o0 = alpha * a.x; o1 = alpha * a.y; o2 = alpha * a.z; o3 = alpha * a.w;
+              }
+              if (wf) *reinterpret_cast<float4*>(fr) = make_float4(o0, o1, o2, o3);
+              const uint32_t h01 = pack_bf16(o0, o1), h23 = pack_bf16(o2, o3);
+              *reinterpret_cast<uint2*>(hr) = make_uint2(h01, h23);
+              if (write_lo) {
+                const uint32_t l01 = pack_bf16(o0 - __uint_as_float(h01 << 16), o1 - __uint_as_float(h01 & 0xFFFF0000u));
+                const uint32_t l23 = pack_bf16(o2 - __uint_as_float(h23 << 16), o3 - __uint_as_float(h23 & 0xFFFF0000u));
+                *reinterpret_cast<uint2*>(lr) = make_uint2(l01, l23);
+              }
+              fr += fstep; hr += bstep; lr += bstep;
+            }
+          } else
 #pragma unroll 4
           for (int it = 0; it < 8; ++it) {
             const int rr = 4 * it + rsub;

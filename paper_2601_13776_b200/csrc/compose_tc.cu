@@ -1195,7 +1195,10 @@ orth_status_t build_compose_tc(Plan& P) {
             ph.s.push_back(TcgSeg{in_h + prev * tapb, in_l + prev * tapb, bf(qb[uidx].h), bf(qb[uidx].l), ld, qb[uidx].ld});
           d.seg_count = (int)ph.s.size() - d.seg_begin;
           const int o = p * ow + q;
-          d.f = comp + out_f + o * tapf; d.ldf = c;
+          // FP32 chain taps are read only by the emit of a BCOP unit's final step; every other step's
+          // consumer (the next step, the AOC) reads the BF16 hi/lo copies -- skipping the FP32 stores cuts a
+          // third of the bytes of these store-bound epilogues (~55 GB/s per SM, tools/micro/tma_store_bw.cu)
+          if (t == nsub - 1 && L.cons != CONS_AOC) { d.f = comp + out_f + o * tapf; d.ldf = c; }
           d.oh = out_h + o * tapb; d.ol = out_l + o * tapb; d.ldo = ld;
           if (t == nsub - 1 && b.tr_h >= 0) {
             d.th = bf(b.tr_h) + (int64_t)o * c * b.ldt;

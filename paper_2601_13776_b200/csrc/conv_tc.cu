@@ -831,6 +831,15 @@ int launch_pair(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, con
 }
 #endif  // ORTH_EXPERIMENTAL
 
+// Split K into two half-tile items when it pays: few tiles (at most half the SMs: every SM gets work
+// twice as fast), or when the halves fill the last wave better (cfg3 512@7: 196 tiles = 1.32 waves of
+// full tiles but 2.65 of halves, i.e. 2 -> 1.5 full-tile times).
+static bool splitk_pays(int64_t t) {
+  const int64_t S = num_sms();
+  if (2 * t <= S) return true;
+  return (2 * t + S - 1) / S < 2 * ((t + S - 1) / S);
+}
+
 int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
                TcConvArgs& a, int groups, cudaStream_t s) {
   const int n = a.nout_g;
@@ -842,9 +851,9 @@ int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, cons
   a.ksplit = 1;
   const int64_t tiles256 = (int64_t)a.tiles_m * (n / 256) * groups;
   const int kblocks = ((a.cr_g + 63) / 64) * a.k * a.k / a.nphase;   // per tile (taps spread over the phases)
-  if (!no_split && a.part && a.flags && bn == 256 && tiles256 < (num_sms() * 4) / 5 && a.cr_g % 128 == 0 &&
+  if (!no_split && a.part && a.flags && bn == 256 && a.cr_g % 128 == 0 &&
       kblocks >= 64 &&   // measured: 72 K blocks 37.6 -> 33.6 us, 36 K blocks 23.6 -> 27.1 us
-      2 * tiles256 <= num_sms() && (size_t)tiles256 * 128 * 256 * 4 <= a.part_bytes && tiles256 <= 65536)
+      splitk_pays(tiles256) && (size_t)tiles256 * 128 * 256 * 4 <= a.part_bytes && tiles256 <= 65536)
     a.ksplit = 2;   // two half-K items per 128x256 tile: twice the MMA work per instruction, same item count
   while (a.ksplit == 1 && bn > 128 && (int64_t)a.tiles_m * (n / bn) * groups < (num_sms() * 4) / 5 &&
          n % (bn / 2) == 0)
@@ -978,7 +987,7 @@ static int pack_weights(const LayerInfo& L, int P, const void* kernel, void* dst
 static int64_t splitk_need(int64_t tiles_m, int nout_g, int cr_g, int groups, int64_t* flags) {
   if (nout_g % 256 != 0 || cr_g % 128 != 0) return 0;
   const int64_t t256 = tiles_m * (nout_g / 256) * groups;
-  if (2 * t256 > num_sms()) return 0;
+  if (!splitk_pays(t256)) return 0;
   *flags = std::max<int64_t>(*flags, t256);
   return t256 * 128 * 256 * 4;
 }

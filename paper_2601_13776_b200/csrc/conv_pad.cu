@@ -414,13 +414,6 @@ __global__ void __launch_bounds__(ROW ? NTHREADS_ROW : NTHREADS, 1)
       umma::tc_fence_after();
       if (q == 0 && lane == 0) CTRACE(tcount, 2);
       const int obase = g * a.nout_g + n0;
-#ifdef ORTH_ROW_EXP_NOEPI   // timing experiment only (no outputs): the accumulator is released untouched
-      if (true) {
-        umma::tc_fence_before();
-        umma::mbar_arrive(&tempty_bar[acc]);
-        continue;
-      }
-#endif
 #pragma unroll 1
       for (int ci = 0; ci < 2; ++ci) {   // two 16-channel chunks of this warp's half
         const int cc = 32 * h + 16 * ci;

@@ -180,9 +180,15 @@ def test_conv_scratch_sized_at_create():
     assert sc[10] == tiles * 128 * 256 * 4 and sc[11] == sc[10]
     p3 = orth.Plan(configs.cfg3(), device=-1, max_batch=256)
     s3 = [i["scratch"] for i in p3.layer_info]
-    # cfg3 128-ch 28x28 layers take the stacked-window kernel: padded copy 256 x 30 x 30 x 128 x 2 bytes
-    assert s3[8] == 256 * 30 * 30 * 128 * 2
-    assert orth.Plan(configs.cfg3(), device=-1, max_batch=32).layer_info[8]["scratch"] == 32 * 30 * 30 * 128 * 2
+    # cfg3 128-ch 28x28 layers take the stacked-window kernel, which loads its windows straight from the
+    # input (no padded copy): no scratch
+    assert s3[8] == 0
+    # cfg3 512 @ 7x7: 98 x 2 = 196 tiles of 128 x 256 (1.32 waves on 148 SMs) split into K halves that fill
+    # 2.65 waves: partials 196 x 128 x 256 x 4 bytes; at batch 32 (25 tiles <= 74) the few-tiles rule
+    t3 = (256 * 7 * 7 + 127) // 128 * 2
+    assert s3[28] == t3 * 128 * 256 * 4
+    t32 = (32 * 7 * 7 + 127) // 128 * 2
+    assert orth.Plan(configs.cfg3(), device=-1, max_batch=32).layer_info[28]["scratch"] == t32 * 128 * 256 * 4
 
 
 def test_soc_validation_and_geometry():

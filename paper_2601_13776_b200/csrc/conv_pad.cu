@@ -56,6 +56,8 @@
 //   [0] A issued, [1] MMA saw A landed, [2] epilogue saw accumulator, [3] epilogue done
 __device__ unsigned long long conv_trace[160 * 32 * 4];
 __device__ unsigned long long conv_trace_clk[160 * 32 * 4];
+// per CTA: MMA-thread cycles waiting for a free accumulator, for landed windows, total, tiles
+__device__ unsigned long long pad_mma_trace[160 * 4];
 __device__ __forceinline__ void ctrace(int tcount, int q) {
   if (tcount < 32) {
     unsigned long long t;
@@ -255,6 +257,9 @@ __global__ void __launch_bounds__(ROW ? NTHREADS_ROW : NTHREADS, 1)
       // ---------------------------------------------------------- MMA issuer
       constexpr uint32_t IDESC = SW ? umma::idesc_bf16(64, 256) : umma::idesc_bf16(128, BN);
       int u = 0, i = 0, tcount = 0, cur = -1, loads = 0;
+#ifdef ORTH_CONV_TRACE
+      const long long t_all0 = clock64();
+#endif
       for (int tile = t_begin; tile < t_end; tile += t_step, ++tcount) {
         if (a.bres) {
           const int set = tile / a.tiles_m;
@@ -266,13 +271,25 @@ __global__ void __launch_bounds__(ROW ? NTHREADS_ROW : NTHREADS, 1)
           }
         }
         const int acc = tcount & 1;
+#ifdef ORTH_CONV_TRACE
+        long long tq0 = clock64();
+#endif
         umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
+#ifdef ORTH_CONV_TRACE
+        if (blockIdx.x < 160) pad_mma_trace[blockIdx.x * 4 + 0] += clock64() - tq0;
+#endif
         umma::tc_fence_after();
         const uint32_t d_tmem = tmem + acc * ACC_COLS;
         int j = 0;   // resident: index of (chunk, tap) in the set
         for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
           const int ab = u % NA;
+#ifdef ORTH_CONV_TRACE
+          tq0 = clock64();
+#endif
           umma::mbar_wait(&a_full[ab], (u / NA) & 1);
+#ifdef ORTH_CONV_TRACE
+          if (blockIdx.x < 160) pad_mma_trace[blockIdx.x * 4 + 1] += clock64() - tq0;
+#endif
           umma::tc_fence_after();
           if (c0 == 0) CTRACE(tcount, 1);
           const uint32_t abuf = abase + ab * a.abuf_bytes;
@@ -324,6 +341,12 @@ __global__ void __launch_bounds__(ROW ? NTHREADS_ROW : NTHREADS, 1)
         }
         umma::mma_commit(&tfull_bar[acc]);
       }
+#ifdef ORTH_CONV_TRACE
+      if (blockIdx.x < 160) {
+        pad_mma_trace[blockIdx.x * 4 + 2] += clock64() - t_all0;
+        pad_mma_trace[blockIdx.x * 4 + 3] += tcount;
+      }
+#endif
     }
     __syncwarp();
   } else if (SW && warp >= EPI_WARP0) {
@@ -677,6 +700,17 @@ int launch_pad(const void* x, const __nv_bfloat16* w, int w_rows, const float* b
       std::printf("conv_pad BN=%d bres=%d TH=%d P=%d R=%d na=%d sb=%d tiles=%d grid=%d: A issue->landed %.2f, ->acc ready %.2f, epi %.2f, per-tile %.2f us, MMA span %.0f cycles (%.0f MHz)\n",
                   BN, a.bres, a.TH, a.P, a.R, a.nabuf, a.sb, a.num_tiles, grid, d01 / cnt * 1e-3, d12 / cnt * 1e-3,
                   d23 / cnt * 1e-3, per / cnt * 1e-3, c12 / cnt, 1e3 * c12 / d12);
+    {
+      static unsigned long long hm[160 * 4];
+      cudaMemcpyFromSymbol(hm, pad_mma_trace, sizeof(hm));
+      double wt = 0, wa = 0, tot = 0, nt = 0;
+      for (int c = 0; c < grid && c < 160; ++c) { wt += hm[4 * c]; wa += hm[4 * c + 1]; tot += hm[4 * c + 2]; nt += hm[4 * c + 3]; }
+      if (nt > 0)
+        std::printf("  MMA thread per tile: %.0f cycles total, waiting for a free accumulator %.0f, for the window %.0f\n",
+                    tot / nt, wt / nt, wa / nt);
+      static unsigned long long zm[160 * 4];
+      cudaMemcpyToSymbol(pad_mma_trace, zm, sizeof(zm));
+    }
     cudaMemset(conv_trace, 0, 0);
     static unsigned long long z[160 * 32 * 4];
     cudaMemcpyToSymbol(conv_trace, z, sizeof(z));

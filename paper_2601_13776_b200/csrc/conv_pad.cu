@@ -729,8 +729,7 @@ bool conv_act_tmap(CUtensorMap_st* out, const void* x, int C, int W, int H, int 
 // Plan the padded-row path for a (possibly group-packed) forward layer; false
 // if it does not apply (stride != 1, rows wider than one tile, channel slices
 // that would cross groups, circular padding that is not a single wrap, ...).
-static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, int& bn, PadArgs& a, bool sw,
-                     int p_align = 1) {
+static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, int& bn, PadArgs& a, bool sw) {
   const int ext = L.d * (L.k - 1);
   static const int co_max = std::getenv("ORTH_CONV_PAD_COMAX") ? std::atoi(std::getenv("ORTH_CONV_PAD_COMAX")) : 64;
   if (L.s != 1 || Wo > 128 || Wo < 16 || L.k > 7 || L.co > (sw ? 64 : co_max)) return false;
@@ -752,7 +751,7 @@ static bool pad_args(const LayerInfo& L, int N, int H, int W, int Ho, int Wo, in
     const bool single = layout == 0;
     if (layout_env && std::strcmp(layout_env, single ? "window" : "copies") != 0) continue;
     if (!single && circ && W % 8 != 0) continue;
-    const int P = single ? (Wo + ext + p_align - 1) / p_align * p_align : (circ ? W : (Wo + 7) & ~7);
+    const int P = single ? Wo + ext : (circ ? W : (Wo + 7) & ~7);
     if (P > 128 + ext || P > 256) continue;
     const int TH = std::min(Ho, MT / P);
     if (TH < 1 || TH * Wo < MT / 2) continue;
@@ -825,12 +824,11 @@ int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* b
   cudaStream_t s = (cudaStream_t)stream;
   static const bool no_swap = std::getenv("ORTH_CONV_NO_SWAP") != nullptr;   // A/B switch
   static const bool no_row = std::getenv("ORTH_CONV_NO_ROW") != nullptr;     // A/B switch
-  static const int row_align = std::getenv("ORTH_CONV_ROW_ALIGN") ? std::atoi(std::getenv("ORTH_CONV_ROW_ALIGN")) : 1;
   int bn = 0;
   PadArgs a;
   // kernel-row MMAs (co_g = 64, 2 <= k <= 4, one window layout): M = 128 pixels x N = k 64
   if (!no_row && L.co == 64 && L.k >= 2 && L.k <= 4 && L.d * (L.k - 1) < 32 &&
-      pad_args(L, N, H, W, Ho, Wo, bn, a, false, row_align) && bn == 64 && a.ncopy == 1) {
+      pad_args(L, N, H, W, Ho, Wo, bn, a, false) && bn == 64 && a.ncopy == 1) {
     if (a.num_tiles == 0) return 0;
     a.flip = flip;
     g_conv_variant = ORTH_CV_WINDOW_ROW;

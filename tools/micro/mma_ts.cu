@@ -27,11 +27,16 @@ template <int N, int MODE>   // MODE 0: ss; 1: ts, A resident in TMEM; 2: ts + t
                              // 9: as 6 with the operands cycling through 4 distinct 48 KB stages (conv_ws);
                              // 10: as 9 with both operands MN-major (the NS Gram: 2 x 8 KB blocks per operand);
                              // 11: A rows starting at 0 / 58 / 116 (an unaligned window row offset, the kernel-row
-                             //     conv), B fixed; 12: as 11 with aligned offsets 0 / 64 / 128
+                             //     conv), B fixed; 12: as 11 with aligned offsets 0 / 64 / 128;
+                             // 13: the kernel-row conv's tile: 3 rows x 4 K steps, A in one of 4 window
+                             //     buffers (30 KB apart) at row offsets 0 / 58 / 116, B = 3 stacked 8 KB tap
+                             //     tiles per row (24 KB apart), accumulator alternating per tile (256 cols);
+                             // 14: as 13 with the epilogue handshake: commit -> tfull[acc], warp 1 waits
+                             //     tfull and arrives tempty[acc], the MMA thread waits tempty before a tile
 __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar, done_bar, emp[4];
+  __shared__ uint64_t bar, done_bar, emp[4], tfull[2], tempty[2];
   __shared__ uint32_t tbase;
   for (int i = threadIdx.x; i < 200704 / 4; i += 128) {
     uint32_t h = (uint32_t)i * 2654435761u;
@@ -43,6 +48,7 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
     umma::mbar_init(&bar, 1);
     umma::mbar_init(&done_bar, 1);
     for (int i = 0; i < 4; ++i) umma::mbar_init(&emp[i], 1);
+    for (int i = 0; i < 2; ++i) { umma::mbar_init(&tfull[i], 1); umma::mbar_init(&tempty[i], 1); }
     umma::fence_mbar_init();
   }
   umma::fence_proxy_async_smem();
@@ -52,6 +58,13 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
   __shared__ volatile int stop;
   if (threadIdx.x == 0) stop = 0;
   __syncthreads();
+  if (MODE == 14 && threadIdx.x == 32) {   // the epilogue stand-in: release each accumulator once full
+    for (int t = 0; t < nmma / 12; ++t) {
+      umma::mbar_wait(&tfull[t & 1], (t >> 1) & 1);
+      umma::tc_fence_after();
+      umma::mbar_arrive(&tempty[t & 1]);
+    }
+  }
   if ((MODE == 7 || MODE == 8) && threadIdx.x >= 32) {
     const int w = threadIdx.x >> 5;
     float acc = 0.f;
@@ -78,7 +91,22 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
     if (MODE == 1)
       for (int q = 0; q < 4; ++q) cp_128x256(at + 8 * q, umma::sdesc_sw128(a + 32 * q));
     const unsigned long long t0 = clock64();
-    if (MODE >= 4) {
+    if (MODE == 13 || MODE == 14) {
+      const uint32_t ID13 = umma::idesc_bf16(128, 192);
+      for (int t = 0; t < nmma / 12; ++t) {
+        if (MODE == 14 && t >= 2) umma::mbar_wait(&tempty[t & 1], ((t >> 1) - 1) & 1);
+        umma::tc_fence_after();
+        const uint32_t abuf = a + (uint32_t)(t & 3) * 30720u, d = tbase + (uint32_t)(t & 1) * 256u;
+        for (int ra = 0; ra < 3; ++ra) {
+          const uint32_t aa = abuf + (uint32_t)(ra * 58) * 128u, bb = a + 126976u + (uint32_t)ra * 24576u;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            umma::mma_bf16(d, umma::sdesc_sw128(aa + 32 * q), umma::sdesc_sw128(bb + 32 * q), ID13, (ra | q) != 0);
+        }
+        if (MODE == 14) umma::mma_commit(&tfull[t & 1]);
+        else umma::mma_commit(&emp[t & 3]);
+      }
+    } else if (MODE >= 4) {
       umma::mbar_arrive(&done_bar);   // phase 0 completes: every wait below hits the already-complete path
       for (int kb = 0; kb < nmma / 4; ++kb) {
         if (MODE == 4 || MODE == 5) umma::mbar_wait(&done_bar, 0);
@@ -99,7 +127,7 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
         umma::mma_commit(&emp[kb & 3]);
       }
     }
-    for (int i = 0; i < (MODE >= 4 ? 0 : nmma); ++i) {
+    for (int i = 0; i < (MODE >= 4 ? 0 : nmma); ++i) {   // (modes >= 4 ran above)
       const int q = i & 3;
       if (MODE == 3) {
         umma::mma_bf16(tbase, umma::sdesc_sw128_mn(a + 2048 * q, 8192), umma::sdesc_sw128_mn(b + 2048 * q, 8192), ID,
@@ -135,6 +163,8 @@ int main() {
     for (int c = 0; c < 148; ++c) s += (double)h[c] / 148;
     printf("%-28s %.1f cycles/MMA (%s)\n", name, s / nm, cudaGetErrorString(e));
   };
+  run(k<192, 13>, "ss  kernel-row conv tile pattern");
+  run(k<192, 14>, "ss  ... + epilogue handshake");
   run(k<192, 11>, "ss  N=192 A at rows 0/58/116");
   run(k<192, 12>, "ss  N=192 A at rows 0/64/128");
   run(k<128, 11>, "ss  N=128 A at rows 0/58/116");

@@ -13,12 +13,15 @@ ci, co, k, s, d, g = map(int, args[:6])
 mode, H = args[6], int(args[7])
 N = int(args[8]) if len(args) > 8 else 256
 adj = "--adjoint" in sys.argv
+zeros = "--zeros" in sys.argv   # all-zero operands: separates data-dependent (power) effects from the schedule
 layer = dict(kind="conv", c_in=ci, c_out=co, k=k, s=s, d=d, g=g, padding_mode=mode, grid=(H, H))
 plan = orth.Plan([layer], 0, max_batch=N)
 kb = (torch.randn(co, k, k, ci // g, device="cuda") * 0.05).to(torch.bfloat16)
 x = torch.randn(N, H, H, ci, device="cuda").to(torch.bfloat16)
 Ho, Wo = plan.out_hw(0, H, H)
 y = torch.randn(N, Ho, Wo, co, device="cuda").to(torch.bfloat16)
+if zeros:
+    kb.zero_(); x.zero_(); y.zero_()
 f = (lambda: plan.conv_transpose(0, kb, y, x)) if adj else (lambda: plan.conv_forward(0, kb, x, y))
 for _ in range(3):
     f()

@@ -17,6 +17,7 @@ __device__ __forceinline__ void cp_128x256(uint32_t taddr, uint64_t sdesc) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
 }
 
+#include "../../paper_2601_13776_b200/csrc/tma_host.h"
 template <int N, int MODE>   // MODE 0: ss; 1: ts, A resident in TMEM; 2: ts + tcgen05.cp per MMA;
                              // 3: ss with both operands MN-major (the NS Gram's column operands);
                              // 4: ss in conv_ws's K-block loop shape: per 4 MMAs an mbarrier wait on an
@@ -32,8 +33,10 @@ template <int N, int MODE>   // MODE 0: ss; 1: ts, A resident in TMEM; 2: ts + t
                              //     buffers (30 KB apart) at row offsets 0 / 58 / 116, B = 3 stacked 8 KB tap
                              //     tiles per row (24 KB apart), accumulator alternating per tile (256 cols);
                              // 14: as 13 with the epilogue handshake: commit -> tfull[acc], warp 1 waits
-                             //     tfull and arrives tempty[acc], the MMA thread waits tempty before a tile
-__global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
+                             //     tfull and arrives tempty[acc], the MMA thread waits tempty before a tile;
+                             // 15: as 13 while warp 2 streams TMA loads (L2-resident, 16 KB boxes) into a
+                             //     separate shared-memory region (a producer's window / weight traffic)
+__global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar, done_bar, emp[4], tfull[2], tempty[2];
@@ -43,6 +46,8 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
     h ^= h >> 13;
     reinterpret_cast<uint32_t*>(sm)[i] = (((120u + h % 7u) << 7) | ((h >> 4) & 0x7fu)) * 0x10001u;
   }
+  __syncthreads();
+  if (threadIdx.x == 0) *reinterpret_cast<volatile int*>(sm + 200704 - 16) = 0;   // the streamer's stop flag
   if (threadIdx.x < 32) umma::tmem_alloc(&tbase, 512);
   if (threadIdx.x == 0) {
     umma::mbar_init(&bar, 1);
@@ -58,6 +63,18 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
   __shared__ volatile int stop;
   if (threadIdx.x == 0) stop = 0;
   __syncthreads();
+  __shared__ uint64_t tbar[2];
+  if (MODE == 15 && threadIdx.x == 64) {   // TMA streamer: 2 x 16 KB boxes in flight, until the MMAs finish
+    umma::mbar_init(&tbar[0], 1); umma::mbar_init(&tbar[1], 1); umma::fence_mbar_init();
+    const uint32_t dst = umma::smem_u32(sm) + 163840;   // 2 x 16 KB past the MMA operands
+    for (int it = 0; it < (1 << 20); ++it) {
+      const int b = it & 1;
+      if (it >= 2) umma::mbar_wait(&tbar[b], ((it >> 1) - 1) & 1);
+      if (*reinterpret_cast<volatile int*>(sm + 200704 - 16)) break;
+      umma::mbar_arrive_expect_tx(&tbar[b], 16384);
+      umma::tma_load_2d(dst + b * 16384, &tm, &tbar[b], 0, (it * 128) & 8191);
+    }
+  }
   if (MODE == 14 && threadIdx.x == 32) {   // the epilogue stand-in: release each accumulator once full
     for (int t = 0; t < nmma / 12; ++t) {
       umma::mbar_wait(&tfull[t & 1], (t >> 1) & 1);
@@ -91,7 +108,7 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
     if (MODE == 1)
       for (int q = 0; q < 4; ++q) cp_128x256(at + 8 * q, umma::sdesc_sw128(a + 32 * q));
     const unsigned long long t0 = clock64();
-    if (MODE == 13 || MODE == 14) {
+    if (MODE == 13 || MODE == 14 || MODE == 15) {
       const uint32_t ID13 = umma::idesc_bf16(128, 192);
       for (int t = 0; t < nmma / 12; ++t) {
         if (MODE == 14 && t >= 2) umma::mbar_wait(&tempty[t & 1], ((t >> 1) - 1) & 1);
@@ -143,6 +160,7 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
     umma::mbar_wait(&bar, 0);
     out[blockIdx.x] = clock64() - t0;
     stop = 1;
+    *reinterpret_cast<volatile int*>(sm + 200704 - 16) = 1;
   }
   umma::tc_fence_before();
   __syncthreads();
@@ -152,10 +170,22 @@ __global__ void __launch_bounds__(128, 1) k(int nmma, unsigned long long* out) {
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 8 * 148);
+  void* gx;
+  cudaMalloc(&gx, 8192 * 512 * 2);
+  cudaMemset(gx, 0, 8192 * 512 * 2);
+  CUtensorMap tm;
+  {
+    const cuuint64_t dims[2] = {512, 8192};
+    const cuuint64_t strides[1] = {1024};
+    const cuuint32_t box[2] = {64, 128};
+    const cuuint32_t es[2] = {1, 1};
+    tensor_map_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, gx, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   auto run = [&](auto kern, const char* name) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 202000);
     const int nm = 65536;
-    kern<<<148, 128, 202000>>>(nm, d);
+    kern<<<148, 128, 202000>>>(nm, d, tm);
     cudaError_t e = cudaDeviceSynchronize();
     unsigned long long h[148];
     cudaMemcpy(h, d, 8 * 148, cudaMemcpyDeviceToHost);
@@ -164,6 +194,7 @@ int main() {
     printf("%-28s %.1f cycles/MMA (%s)\n", name, s / nm, cudaGetErrorString(e));
   };
   run(k<192, 13>, "ss  kernel-row conv tile pattern");
+  run(k<192, 15>, "ss  ... + concurrent TMA loads");
   run(k<192, 14>, "ss  ... + epilogue handshake");
   run(k<192, 11>, "ss  N=192 A at rows 0/58/116");
   run(k<192, 12>, "ss  N=192 A at rows 0/64/128");

@@ -45,6 +45,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 #include "orth_internal.h"
 #include "pdl.h"
@@ -252,103 +253,223 @@ __global__ void __launch_bounds__(ROW ? NTHREADS_ROW : NTHREADS, 1)
           }
       }
     }
-  } else if (warp == MMA_WARP) {
-    if (lane == 0) {
-      // ---------------------------------------------------------- MMA issuer
-      constexpr uint32_t IDESC = SW ? umma::idesc_bf16(64, 256) : umma::idesc_bf16(128, BN);
-      int u = 0, i = 0, tcount = 0, cur = -1, loads = 0;
+  } else if (ROW && (warp == MMA_WARP || warp == MMA_WARP + 1)) {
+    // ------------------------------------------------------ MMA issuers (kernel-row form)
+    // On sm_100a a tcgen05.mma is accepted only shortly before the tensor core can start it, so every
+    // cycle the issuing thread spends between MMAs (an mbarrier wait, ~100 cycles even when the phase
+    // has completed; descriptor arithmetic in vector registers, R2UR) adds to the tile time 1:1
+    // (tools/micro/row_mma2.cu: a 200-cycle stall per 12-MMA tile costs 210 cycles).  Hence:
+    //  * with one resident weight set, TWO issuing threads (warps 2 and 3) take alternate tiles --
+    //    accumulator a = tile parity -- so one waits for its window / accumulator while the other's
+    //    MMAs run;
+    //  * the loop is specialised on resident-vs-streamed weights and on k, the descriptors are 64-bit
+    //    values advanced by adds and the tile range is re-derived here from kernel parameters, which
+    //    keeps the MMA operands in uniform registers (computed per MMA in vector registers, ptxas wraps
+    //    each tcgen05.mma in an ELECT / R2UR.BROADCAST loop).
+    const int wi = warp - MMA_WARP;
+    const bool dual = a.bres && a.num_tiles <= a.tiles_m;   // a single resident weight set
+    if (lane == 0 && (wi == 0 || dual)) {
+      const int nw = dual ? 2 : 1, nch = (a.cr_g + 63) / 64;
+      const uint32_t ubase = umma::smem_base1024_u32(smem_raw);
+      const uint64_t a_desc0 = umma::sdesc_sw128(ubase), b_desc0 = a_desc0 + (uint32_t)a.nabuf * ((uint32_t)a.abuf_bytes >> 4);
+      const uint32_t a_buf16 = (uint32_t)a.abuf_bytes >> 4, a_row16 = (uint32_t)(a.d * a.P) * 8u;
+      const uint32_t b_row16 = (uint32_t)(a.k * B_BYTES) >> 4, b_set16 = (uint32_t)(kk2 * B_BYTES) >> 4;
+      const uint32_t b_st16 = (uint32_t)bst_bytes >> 4;
+      const uint32_t idesc_row = umma::idesc_bf16(128, a.k * 64);
 #ifdef ORTH_CONV_TRACE
       const long long t_all0 = clock64();
 #endif
-      for (int tile = t_begin; tile < t_end; tile += t_step, ++tcount) {
-        if (a.bres) {
-          const int set = tile / a.tiles_m;
-          if (set != cur) {
-            if (loads > 0) umma::mma_commit(&b_empty[0]);   // release the old set once its MMAs finish
-            umma::mbar_wait(&b_full[0], loads & 1);
-            cur = set;
-            ++loads;
+      // WI (issuer index), BRES and K are compile-time so that the loop state is provably warp-uniform
+      // (a value derived from threadIdx is not, to ptxas); K = 0: the kernel row count at run time
+      auto issue = [&](auto wi_c, auto bres_c, auto k_c) {
+        constexpr int WI = decltype(wi_c)::value;
+        constexpr bool BRES = decltype(bres_c)::value;
+        constexpr int KC = decltype(k_c)::value;
+        const int K = KC ? KC : a.k;
+        // the tile range is derived here, inside the issuing branch: computed before it (and shared with
+        // the other roles) it reaches ptxas as a non-uniform value and the MMA operands with it
+        const int tb = a.bres ? blockIdx.x * a.tiles_per_cta : blockIdx.x;
+        const int te = a.bres ? min(a.num_tiles, tb + a.tiles_per_cta) : a.num_tiles;
+        const int ts = a.bres ? 1 : gridDim.x;
+        int ab = 0, aph = 0, st = 0, bph = 0, cur = -1, loads = 0, tcount = WI;
+        auto adv_a = [&]() {
+          if (++ab == NA) { ab = 0; aph ^= 1; }
+        };
+        for (int c = 0; c < WI * nch; ++c) adv_a();   // this issuer's first tile starts at chunk WI * nch
+        for (int tile = tb + WI * ts; tile < te; tile += nw * ts, tcount += nw) {
+          if (BRES) {
+            const int set = tile / a.tiles_m;
+            if (set != cur) {
+              if (loads > 0) umma::mma_commit(&b_empty[0]);   // (single issuer only: dual has one set)
+              umma::mbar_wait_uni(&b_full[0], loads & 1);
+              cur = set;
+              ++loads;
+            }
           }
-        }
-        const int acc = tcount & 1;
+          const int acc = tcount & 1;
 #ifdef ORTH_CONV_TRACE
-        long long tq0 = clock64();
+          long long tq0 = clock64();
 #endif
-        umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
+          umma::mbar_wait_uni(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
 #ifdef ORTH_CONV_TRACE
-        if (blockIdx.x < 160) pad_mma_trace[blockIdx.x * 4 + 0] += clock64() - tq0;
-#endif
-        umma::tc_fence_after();
-        const uint32_t d_tmem = tmem + acc * ACC_COLS;
-        int j = 0;   // resident: index of (chunk, tap) in the set
-        for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
-          const int ab = u % NA;
-#ifdef ORTH_CONV_TRACE
-          tq0 = clock64();
-#endif
-          umma::mbar_wait(&a_full[ab], (u / NA) & 1);
-#ifdef ORTH_CONV_TRACE
-          if (blockIdx.x < 160) pad_mma_trace[blockIdx.x * 4 + 1] += clock64() - tq0;
+          if (blockIdx.x < 160 && WI == 0) pad_mma_trace[blockIdx.x * 4 + 0] += clock64() - tq0;
 #endif
           umma::tc_fence_after();
-          if (c0 == 0) CTRACE(tcount, 1);
-          const uint32_t abuf = abase + ab * a.abuf_bytes;
-          if (ROW) {   // one M128 x N(k 64) MMA chain per kernel row
-            const uint32_t idesc_row = umma::idesc_bf16(128, a.k * 64);
-            for (int ra = 0; ra < a.k; ++ra, j += a.k) {
-              int st = 0;
-              if (!a.bres) {
-                st = i % SB;
-                umma::mbar_wait(&b_full[st], (i / SB) & 1);
-                umma::tc_fence_after();
-              }
-              const uint32_t aa = abuf + (uint32_t)(a.d * ra * a.P) * 128u;
-              const uint32_t bb = bbase + (a.bres ? (uint32_t)(j * B_BYTES) : (uint32_t)(st * bst_bytes));
+          const uint32_t d_tmem = tmem_base_sh + acc * ACC_COLS;
+          uint64_t bset = b_desc0;
+          for (int c0 = 0; c0 < a.cr_g; c0 += 64, bset += b_set16) {
+#ifdef ORTH_CONV_TRACE
+            tq0 = clock64();
+#endif
+            umma::mbar_wait_uni(&a_full[ab], aph);
+#ifdef ORTH_CONV_TRACE
+            if (blockIdx.x < 160 && WI == 0) pad_mma_trace[blockIdx.x * 4 + 1] += clock64() - tq0;
+#endif
+            umma::tc_fence_after();
+            if (c0 == 0 && WI == 0) CTRACE(tcount, 1);
+            uint64_t ad = a_desc0 + ab * a_buf16;
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
-                umma::mma_bf16(d_tmem, umma::sdesc_sw128(aa + 32 * q), umma::sdesc_sw128(bb + 32 * q), idesc_row,
-                               (c0 | ra | q) != 0);
-              if (!a.bres) {
+            for (int ra = 0; ra < K; ++ra, ad += a_row16) {
+              uint64_t bd = bset + ra * b_row16;
+              if (!BRES) {
+                umma::mbar_wait_uni(&b_full[st], bph);
+                umma::tc_fence_after();
+                bd = b_desc0 + st * b_st16;
+              }
+              const uint32_t acc0 = (c0 | ra) != 0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) umma::mma_bf16(d_tmem, ad + 2 * q, bd + 2 * q, idesc_row, acc0 | (q != 0));
+              if (!BRES) {
                 umma::mma_commit(&b_empty[st]);
-                ++i;
+                if (++st == SB) { st = 0; bph ^= 1; }
               }
             }
             umma::mma_commit(&a_empty[ab]);
-            continue;
+            adv_a();
           }
-          for (int tap = 0; tap < kk2; ++tap, ++j) {
+          umma::mma_commit(&tfull_bar[acc]);
+          for (int c = 0; c < (nw - 1) * nch; ++c) adv_a();   // the other issuer's tile
+        }
+      };
+      using T = std::true_type;
+      using F = std::false_type;
+      using W0 = std::integral_constant<int, 0>;
+      using W1 = std::integral_constant<int, 1>;
+      using K0 = std::integral_constant<int, 0>;
+      using K3 = std::integral_constant<int, 3>;
+      if (!a.bres) {
+        if (a.k == 3) issue(W0{}, F{}, K3{});
+        else issue(W0{}, F{}, K0{});
+      } else if (wi == 0) {
+        if (a.k == 3) issue(W0{}, T{}, K3{});
+        else issue(W0{}, T{}, K0{});
+      } else {
+        if (a.k == 3) issue(W1{}, T{}, K3{});
+        else issue(W1{}, T{}, K0{});
+      }
+#ifdef ORTH_CONV_TRACE
+      if (blockIdx.x < 160 && wi == 0) {
+        pad_mma_trace[blockIdx.x * 4 + 2] += clock64() - t_all0;
+        pad_mma_trace[blockIdx.x * 4 + 3] += (min(a.num_tiles, (int)blockIdx.x * a.tiles_per_cta + a.tiles_per_cta) - (int)blockIdx.x * a.tiles_per_cta + nw - 1) / nw;
+      }
+#endif
+    }
+    __syncwarp();
+  } else if (warp == MMA_WARP) {
+    // all 32 lanes run the issue loop (uniform operands); one elected lane issues each MMA / commit
+    // ---------------------------------------------------------- MMA issuer
+    constexpr uint32_t IDESC = SW ? umma::idesc_bf16(64, 256) : umma::idesc_bf16(128, BN);
+    int u = 0, i = 0, tcount = 0, cur = -1, loads = 0;
+#ifdef ORTH_CONV_TRACE
+    const long long t_all0 = clock64();
+#endif
+    for (int tile = t_begin; tile < t_end; tile += t_step, ++tcount) {
+      if (a.bres) {
+        const int set = tile / a.tiles_m;
+        if (set != cur) {
+          if (loads > 0) umma::mma_commit_warp(&b_empty[0]);   // release the old set once its MMAs finish
+          umma::mbar_wait(&b_full[0], loads & 1);
+          cur = set;
+          ++loads;
+        }
+      }
+      const int acc = tcount & 1;
+#ifdef ORTH_CONV_TRACE
+      long long tq0 = clock64();
+#endif
+      umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
+#ifdef ORTH_CONV_TRACE
+      if (lane == 0 && blockIdx.x < 160) pad_mma_trace[blockIdx.x * 4 + 0] += clock64() - tq0;
+#endif
+      umma::tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * ACC_COLS;
+      int j = 0;   // resident: index of (chunk, tap) in the set
+      for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
+        const int ab = u % NA;
+#ifdef ORTH_CONV_TRACE
+        tq0 = clock64();
+#endif
+        umma::mbar_wait(&a_full[ab], (u / NA) & 1);
+#ifdef ORTH_CONV_TRACE
+        if (lane == 0 && blockIdx.x < 160) pad_mma_trace[blockIdx.x * 4 + 1] += clock64() - tq0;
+#endif
+        umma::tc_fence_after();
+        if (c0 == 0) CTRACE(tcount, 1);
+        const uint32_t abuf = abase + ab * a.abuf_bytes;
+        if (ROW) {   // one M128 x N(k 64) MMA chain per kernel row
+          const uint32_t idesc_row = umma::idesc_bf16(128, a.k * 64);
+          for (int ra = 0; ra < a.k; ++ra, j += a.k) {
             int st = 0;
             if (!a.bres) {
               st = i % SB;
               umma::mbar_wait(&b_full[st], (i / SB) & 1);
               umma::tc_fence_after();
             }
-            const int ta = tap / a.k, tb = tap - ta * a.k;
-            const uint32_t aa = a.ncopy > 1 ? abuf + (uint32_t)(tb * a.copy_bytes) + (uint32_t)(a.d * ta * a.P) * 128u
-                                            : abuf + (uint32_t)(a.d * (ta * a.P + tb)) * 128u;
-            const uint32_t bb = bbase + (a.bres ? j : st) * B_BYTES;
+            // descriptors built once per row; a K step of 16 (32 bytes) is +2 in the 16-byte address field
+            const uint64_t ad = umma::sdesc_sw128(abuf + (uint32_t)(a.d * ra * a.P) * 128u);
+            const uint64_t bd = umma::sdesc_sw128(bbase + (a.bres ? (uint32_t)(j * B_BYTES) : (uint32_t)(st * bst_bytes)));
+            const uint32_t acc0 = (c0 | ra) != 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              umma::mma_bf16(d_tmem, umma::sdesc_sw128((SW ? bb : aa) + 32 * q), umma::sdesc_sw128((SW ? aa : bb) + 32 * q),
-                             IDESC,
-                             (c0 | tap | q) != 0);
+            for (int q = 0; q < 4; ++q) umma::mma_bf16_warp(d_tmem, ad + 2 * q, bd + 2 * q, idesc_row, acc0 | (q != 0));
             if (!a.bres) {
-              umma::mma_commit(&b_empty[st]);
+              umma::mma_commit_warp(&b_empty[st]);
               ++i;
             }
           }
-          umma::mma_commit(&a_empty[ab]);
+          umma::mma_commit_warp(&a_empty[ab]);
+          continue;
         }
-        umma::mma_commit(&tfull_bar[acc]);
+        for (int tap = 0; tap < kk2; ++tap, ++j) {
+          int st = 0;
+          if (!a.bres) {
+            st = i % SB;
+            umma::mbar_wait(&b_full[st], (i / SB) & 1);
+            umma::tc_fence_after();
+          }
+          const int ta = tap / a.k, tb = tap - ta * a.k;
+          const uint32_t aa = a.ncopy > 1 ? abuf + (uint32_t)(tb * a.copy_bytes) + (uint32_t)(a.d * ta * a.P) * 128u
+                                          : abuf + (uint32_t)(a.d * (ta * a.P + tb)) * 128u;
+          const uint32_t bb = bbase + (a.bres ? j : st) * B_BYTES;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            umma::mma_bf16_warp(d_tmem, umma::sdesc_sw128((SW ? bb : aa) + 32 * q), umma::sdesc_sw128((SW ? aa : bb) + 32 * q),
+                           IDESC,
+                           (c0 | tap | q) != 0);
+          if (!a.bres) {
+            umma::mma_commit_warp(&b_empty[st]);
+            ++i;
+          }
+        }
+        umma::mma_commit_warp(&a_empty[ab]);
       }
-#ifdef ORTH_CONV_TRACE
-      if (blockIdx.x < 160) {
-        pad_mma_trace[blockIdx.x * 4 + 2] += clock64() - t_all0;
-        pad_mma_trace[blockIdx.x * 4 + 3] += tcount;
-      }
-#endif
+      umma::mma_commit_warp(&tfull_bar[acc]);
     }
-    __syncwarp();
+#ifdef ORTH_CONV_TRACE
+    if (lane == 0 && blockIdx.x < 160) {
+      pad_mma_trace[blockIdx.x * 4 + 2] += clock64() - t_all0;
+      pad_mma_trace[blockIdx.x * 4 + 3] += tcount;
+    }
+#endif
   } else if (SW && warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue (swapped)
     // Warp q reads TMEM lanes 32q .. 32q+15 (channels 16q .. 16q+15) as mma-style 8x8 fragments

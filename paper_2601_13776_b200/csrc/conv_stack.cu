@@ -214,37 +214,43 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp == 2) {
     if (lane == 0) {
       // ------------------------------------------------------------ MMA issuer
+      // Kept warp-uniform for ptxas (see conv_pad.cu, ROW issuers): bases and the tile range derived
+      // here, rings stepped, descriptors advanced by adds (16-byte units).
       constexpr uint32_t IDESC = umma::idesc_bf16(128, 256);
-      int u = 0, i = 0, tcount = 0;
+      const uint32_t ubase = umma::smem_base1024_u32(smem_raw);
+      const uint64_t a_desc0 = umma::sdesc_sw128(ubase);
+      const uint64_t w_desc0 = a_desc0 + (uint32_t)a.nabuf * ((uint32_t)a.abuf_bytes >> 4);
+      const uint32_t abuf16 = (uint32_t)a.abuf_bytes >> 4, row16 = (uint32_t)(a.d * a.P) * 8u, col16 = (uint32_t)a.d * 8u;
+      int ab = 0, aph = 0, st = 0, bph = 0, tcount = 0;
       STRACE(unsigned long long wa = 0, wb = 0; const unsigned long long t_start = gtime();)
       for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++tcount) {
         const int acc = tcount & 1;
         umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
         umma::tc_fence_after();
-        const uint32_t d_tmem = tmem + acc * 256;
-        for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
-          const int ab = u % NA;
+        const uint32_t d_tmem = tmem_base_sh + acc * 256;
+        for (int c0 = 0; c0 < a.cr_g; c0 += 64) {
           STRACE(const unsigned long long t0a = gtime();)
-          umma::mbar_wait(&a_full[ab], (u / NA) & 1);
+          umma::mbar_wait(&a_full[ab], aph);
           STRACE(wa += gtime() - t0a;)
           umma::tc_fence_after();
-          const uint32_t win = abase + ab * a.abuf_bytes;
-          for (int tap = 0; tap < kk2; ++tap, ++i) {
-            const int st = i % SB;
-            STRACE(const unsigned long long t0b = gtime();)
-            umma::mbar_wait(&b_full[st], (i / SB) & 1);
-            STRACE(wb += gtime() - t0b;)
-            umma::tc_fence_after();
-            const int ta = tap / a.k, tb = tap - ta * a.k;
-            const uint32_t bw = win + (uint32_t)(a.d * (ta * a.P + tb)) * 128u;
-            const uint32_t aw = wbase + st * W_BYTES;
+          uint64_t brow = a_desc0 + ab * abuf16;   // window row of kernel row ta
+          for (int ta = 0; ta < a.k; ++ta, brow += row16) {
+            uint64_t bw = brow;
+            for (int tb = 0; tb < a.k; ++tb, bw += col16) {
+              STRACE(const unsigned long long t0b = gtime();)
+              umma::mbar_wait(&b_full[st], bph);
+              STRACE(wb += gtime() - t0b;)
+              umma::tc_fence_after();
+              const uint64_t aw = w_desc0 + st * (uint32_t)(W_BYTES >> 4);
+              const uint32_t acc0 = (c0 | ta | tb) != 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              umma::mma_bf16(d_tmem, umma::sdesc_sw128(aw + 32 * q), umma::sdesc_sw128(bw + 32 * q), IDESC,
-                             (c0 | tap | q) != 0);
-            umma::mma_commit(&b_empty[st]);
+              for (int q = 0; q < 4; ++q) umma::mma_bf16(d_tmem, aw + 2 * q, bw + 2 * q, IDESC, acc0 | (q != 0));
+              umma::mma_commit(&b_empty[st]);
+              if (++st == SB) { st = 0; bph ^= 1; }
+            }
           }
           umma::mma_commit(&a_empty[ab]);
+          if (++ab == NA) { ab = 0; aph ^= 1; }
         }
         umma::mma_commit(&tfull_bar[acc]);
       }

@@ -294,17 +294,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
+      // Kept warp-uniform for ptxas (see conv_pad.cu, ROW issuers): the cluster / tile indices are derived
+      // here rather than taken from the values shared with the other roles, the stage ring is stepped,
+      // not divided, and the descriptors are 64-bit values advanced by adds -- with the operands in
+      // vector registers every tcgen05.mma sat in an ELECT / R2UR.BROADCAST loop, and on sm_100a the
+      // issuing thread's time between MMAs adds to the MMA time.
       constexpr uint32_t IDESC = umma::idesc_bf16(128, BN);
-      int it = 0, tcount = 0;
+      constexpr uint32_t STAGE16 = STAGE >> 4, A16 = A_BYTES >> 4;
+      const int ucs = a.cs, ucr = ucs > 1 ? (int)umma::cluster_ctarank() : 0;
+      const int ucid = blockIdx.x / ucs, uncl = gridDim.x / ucs;
+      const uint64_t desc0 = umma::sdesc_sw128(umma::smem_base1024_u32(smem_raw));
+      int it = 0, tcount = 0, st = 0, ph = 0;
 #ifdef ORTH_CONV_TRACE
       const long long t_all = clock64();
       long long w_full = 0, w_te = 0;
 #endif
-      for (int ct = cid; ct < a.num_ctiles; ct += ncl, ++tcount) {
-        const TileInfo t = decode_tile(a, ct % a.base_ctiles, crank, BN);
+      for (int ct = ucid; ct < a.num_ctiles; ct += uncl, ++tcount) {
+        const TileInfo t = decode_tile(a, ct % a.base_ctiles, ucr, BN);
         int nt = 0;
-        for (int tap = 0; tap < kk2; ++tap) nt += tap_valid(a, t.phase, tap) ? 1 : 0;
-        const int nk = nt * (kc / a.ksplit);
+        for (int tap = 0; tap < a.k * a.k; ++tap) nt += tap_valid(a, t.phase, tap) ? 1 : 0;
+        const int nk = nt * (((a.cr_g + 63) / 64) / a.ksplit);
         const int acc = tcount & 1;
 #ifdef ORTH_CONV_TRACE
         long long tq = clock64();
@@ -316,11 +325,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         umma::tc_fence_after();
         const uint32_t d_tmem = tmem + acc * BN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int st = it % S;
 #ifdef ORTH_CONV_TRACE
           tq = clock64();
 #endif
-          umma::mbar_wait(&full_bar[st], (it / S) & 1);
+          umma::mbar_wait(&full_bar[st], ph);
 #ifdef ORTH_CONV_TRACE
           w_full += clock64() - tq;
 #endif
@@ -328,13 +336,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           umma::fence_proxy_async_smem();   // cp.async (generic proxy) rows -> tcgen05.mma (async proxy)
 #endif
           umma::tc_fence_after();
-          const uint32_t aa = s0 + st * STAGE, bb = aa + A_BYTES;
+          const uint64_t ad = desc0 + st * STAGE16, bd = ad + A16;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            umma::mma_bf16(d_tmem, umma::sdesc_sw128(aa + 32 * q), umma::sdesc_sw128(bb + 32 * q), IDESC,
-                           (kb | q) != 0);
-          if (cs == 1) umma::mma_commit(&empty_bar[st]);
+          for (int q = 0; q < 4; ++q) umma::mma_bf16(d_tmem, ad + 2 * q, bd + 2 * q, IDESC, (kb | q) != 0);
+          if (ucs == 1) umma::mma_commit(&empty_bar[st]);
           else umma::mma_commit_mc(&empty_bar[st], cmask);   // release the stage in every CTA of the cluster
+          if (++st == S) { st = 0; ph ^= 1; }
         }
         umma::mma_commit(&tfull_bar[acc]);
       }

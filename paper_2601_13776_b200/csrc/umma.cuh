@@ -37,6 +37,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// As mbar_wait, for a caller whose active threads all wait on the same barrier and phase (one issuing
+// thread, or a converged warp): the retry branch is declared non-divergent (bra.uni), which keeps the
+// caller's control flow uniform so that ptxas can hold loop-carried descriptors in uniform registers.
+__device__ __forceinline__ void mbar_wait_uni(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITU_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra.uni WAITU_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// Whole-warp wait (all 32 lanes, converged): the retry condition is a warp vote, so the loop is
+// uniform and values carried across it stay in uniform registers.
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
+  }
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -151,6 +181,13 @@ __device__ __forceinline__ void stmatrix_x4_trans(uint32_t saddr, uint32_t m0, u
 __device__ __forceinline__ uint8_t* align1024_smem(uint8_t* raw) {
   return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
 }
+// The same 1024-aligned base as a shared-window address, written as a DIFFERENT expression on purpose:
+// an MMA-issuing branch that derives its descriptors from it gets its own (uniform-register) copy,
+// where reusing the value computed once for all roles hands ptxas a vector register shared with
+// threads that use it per lane -- and every tcgen05.mma then sits in an ELECT / R2UR.BROADCAST loop.
+__device__ __forceinline__ uint32_t smem_base1024_u32(const uint8_t* raw) {
+  return (smem_u32(raw) + 1023u) & ~1023u;
+}
 
 // Programmatic dependent launch (PDL).  A kernel launched with the programmatic-
 // serialization attribute (launch_pdl) may start while its predecessor drains;
@@ -187,6 +224,27 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Whole-warp forms: called by all 32 lanes of a converged warp with warp-uniform operands; one lane
+// (elect.sync) issues.  Keeping the issuing warp converged lets ptxas hold the descriptors in uniform
+// registers instead of wrapping every tcgen05.mma in an ELECT / R2UR.BROADCAST waterfall loop, which
+// costs ~20 instructions per MMA ("MMA issue").
+__device__ __forceinline__ void mma_bf16_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
       : "memory");
 }
 // Arrive on `bar` when every previously issued MMA of this thread has completed.

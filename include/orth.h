@@ -360,7 +360,8 @@ typedef enum {             /* which conv kernel a conv call ran */
   ORTH_CV_TMA = 7,          /* conv_tma (experimental, ORTH_CONV_TMA=1) */
   ORTH_CV_GATHER256 = 8, ORTH_CV_GATHER128 = 9, ORTH_CV_GATHER64 = 10, ORTH_CV_GATHER32 = 11,  /* conv_ws<BN> */
   ORTH_CV_GATHER_PAIR = 12, /* conv_pair (experimental, ORTH_CONV_PAIR=1) */
-  ORTH_CV_WINDOW_ROW = 13   /* conv_pad<64, row>: TMA window, M = 128 pixels x N = k * 64 (one kernel row's taps) */
+  ORTH_CV_WINDOW_ROW = 13   /* conv_pad<64, row>: TMA window, M = 128 pixels x N = k * 64 (one kernel row's taps);
+                               opt-in (ORTH_CONV_ROW=1) */
 } orth_conv_variant_t;
 typedef struct {
   int32_t kind;      /* orth_trace_kind_t */

@@ -375,101 +375,110 @@ __global__ void __launch_bounds__(ROW ? NTHREADS_ROW : NTHREADS, 1)
 #endif
     }
     __syncwarp();
-  } else if (warp == MMA_WARP) {
-    // all 32 lanes run the issue loop (uniform operands); one elected lane issues each MMA / commit
-    // ---------------------------------------------------------- MMA issuer
+  } else if (!ROW && (warp == MMA_WARP || warp == MMA_WARP + 1)) {
+    // ------------------------------------------------------ MMA issuers (one MMA chain per tap)
+    // Same rules as the kernel-row issuers above: compile-time resident-vs-streamed weights, locally
+    // derived bases and tile range, rings stepped, descriptors advanced by adds; two issuers on
+    // alternate tiles when the CTA's tiles share one resident weight set.
     constexpr uint32_t IDESC = SW ? umma::idesc_bf16(64, 256) : umma::idesc_bf16(128, BN);
-    int u = 0, i = 0, tcount = 0, cur = -1, loads = 0;
+    const int wi = warp - MMA_WARP;
+    const bool dual = a.bres && a.num_tiles <= a.tiles_m;
+    if (lane == 0 && (wi == 0 || dual)) {
+      const int nw = dual ? 2 : 1, nch = (a.cr_g + 63) / 64;
+      const uint32_t ubase = umma::smem_base1024_u32(smem_raw);
+      const uint64_t a_desc0 = umma::sdesc_sw128(ubase), b_desc0 = a_desc0 + (uint32_t)a.nabuf * ((uint32_t)a.abuf_bytes >> 4);
+      const uint32_t a_buf16 = (uint32_t)a.abuf_bytes >> 4, row16 = (uint32_t)(a.d * a.P) * 8u, col16 = (uint32_t)a.d * 8u;
+      const uint32_t copy16 = (uint32_t)a.copy_bytes >> 4, tap16 = (uint32_t)B_BYTES >> 4;
+      const uint32_t set16 = (uint32_t)kk2 * tap16;
+      const bool copies = a.ncopy > 1;
 #ifdef ORTH_CONV_TRACE
-    const long long t_all0 = clock64();
+      const long long t_all0 = clock64();
 #endif
-    for (int tile = t_begin; tile < t_end; tile += t_step, ++tcount) {
-      if (a.bres) {
-        const int set = tile / a.tiles_m;
-        if (set != cur) {
-          if (loads > 0) umma::mma_commit_warp(&b_empty[0]);   // release the old set once its MMAs finish
-          umma::mbar_wait(&b_full[0], loads & 1);
-          cur = set;
-          ++loads;
-        }
-      }
-      const int acc = tcount & 1;
-#ifdef ORTH_CONV_TRACE
-      long long tq0 = clock64();
-#endif
-      umma::mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
-#ifdef ORTH_CONV_TRACE
-      if (lane == 0 && blockIdx.x < 160) pad_mma_trace[blockIdx.x * 4 + 0] += clock64() - tq0;
-#endif
-      umma::tc_fence_after();
-      const uint32_t d_tmem = tmem + acc * ACC_COLS;
-      int j = 0;   // resident: index of (chunk, tap) in the set
-      for (int c0 = 0; c0 < a.cr_g; c0 += 64, ++u) {
-        const int ab = u % NA;
-#ifdef ORTH_CONV_TRACE
-        tq0 = clock64();
-#endif
-        umma::mbar_wait(&a_full[ab], (u / NA) & 1);
-#ifdef ORTH_CONV_TRACE
-        if (lane == 0 && blockIdx.x < 160) pad_mma_trace[blockIdx.x * 4 + 1] += clock64() - tq0;
-#endif
-        umma::tc_fence_after();
-        if (c0 == 0) CTRACE(tcount, 1);
-        const uint32_t abuf = abase + ab * a.abuf_bytes;
-        if (ROW) {   // one M128 x N(k 64) MMA chain per kernel row
-          const uint32_t idesc_row = umma::idesc_bf16(128, a.k * 64);
-          for (int ra = 0; ra < a.k; ++ra, j += a.k) {
-            int st = 0;
-            if (!a.bres) {
-              st = i % SB;
-              umma::mbar_wait(&b_full[st], (i / SB) & 1);
-              umma::tc_fence_after();
-            }
-            // descriptors built once per row; a K step of 16 (32 bytes) is +2 in the 16-byte address field
-            const uint64_t ad = umma::sdesc_sw128(abuf + (uint32_t)(a.d * ra * a.P) * 128u);
-            const uint64_t bd = umma::sdesc_sw128(bbase + (a.bres ? (uint32_t)(j * B_BYTES) : (uint32_t)(st * bst_bytes)));
-            const uint32_t acc0 = (c0 | ra) != 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) umma::mma_bf16_warp(d_tmem, ad + 2 * q, bd + 2 * q, idesc_row, acc0 | (q != 0));
-            if (!a.bres) {
-              umma::mma_commit_warp(&b_empty[st]);
-              ++i;
+      auto issue = [&](auto wi_c, auto bres_c) {
+        constexpr int WI = decltype(wi_c)::value;
+        constexpr bool BRES = decltype(bres_c)::value;
+        const int tb0 = a.bres ? blockIdx.x * a.tiles_per_cta : blockIdx.x;
+        const int te = a.bres ? min(a.num_tiles, tb0 + a.tiles_per_cta) : a.num_tiles;
+        const int ts = a.bres ? 1 : gridDim.x;
+        int ab = 0, aph = 0, st = 0, bph = 0, cur = -1, loads = 0, tcount = WI;
+        auto adv_a = [&]() {
+          if (++ab == NA) { ab = 0; aph ^= 1; }
+        };
+        for (int c = 0; c < WI * nch; ++c) adv_a();
+        for (int tile = tb0 + WI * ts; tile < te; tile += nw * ts, tcount += nw) {
+          if (BRES) {
+            const int set = tile / a.tiles_m;
+            if (set != cur) {
+              if (loads > 0) umma::mma_commit(&b_empty[0]);   // (single issuer only: dual has one set)
+              umma::mbar_wait_uni(&b_full[0], loads & 1);
+              cur = set;
+              ++loads;
             }
           }
-          umma::mma_commit_warp(&a_empty[ab]);
-          continue;
-        }
-        for (int tap = 0; tap < kk2; ++tap, ++j) {
-          int st = 0;
-          if (!a.bres) {
-            st = i % SB;
-            umma::mbar_wait(&b_full[st], (i / SB) & 1);
+          const int acc = tcount & 1;
+#ifdef ORTH_CONV_TRACE
+          long long tq0 = clock64();
+#endif
+          umma::mbar_wait_uni(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
+#ifdef ORTH_CONV_TRACE
+          if (blockIdx.x < 160 && WI == 0) pad_mma_trace[blockIdx.x * 4 + 0] += clock64() - tq0;
+#endif
+          umma::tc_fence_after();
+          const uint32_t d_tmem = tmem_base_sh + acc * ACC_COLS;
+          uint64_t bset = b_desc0;
+          for (int c0 = 0; c0 < a.cr_g; c0 += 64, bset += set16) {
+#ifdef ORTH_CONV_TRACE
+            tq0 = clock64();
+#endif
+            umma::mbar_wait_uni(&a_full[ab], aph);
+#ifdef ORTH_CONV_TRACE
+            if (blockIdx.x < 160 && WI == 0) pad_mma_trace[blockIdx.x * 4 + 1] += clock64() - tq0;
+#endif
             umma::tc_fence_after();
-          }
-          const int ta = tap / a.k, tb = tap - ta * a.k;
-          const uint32_t aa = a.ncopy > 1 ? abuf + (uint32_t)(tb * a.copy_bytes) + (uint32_t)(a.d * ta * a.P) * 128u
-                                          : abuf + (uint32_t)(a.d * (ta * a.P + tb)) * 128u;
-          const uint32_t bb = bbase + (a.bres ? j : st) * B_BYTES;
+            if (c0 == 0 && WI == 0) CTRACE(tcount, 1);
+            const uint64_t abuf = a_desc0 + ab * a_buf16;
+            uint64_t btap = bset;
+            for (int ta = 0; ta < a.k; ++ta) {
+              for (int tb = 0; tb < a.k; ++tb, btap += tap16) {
+                const uint64_t aa = copies ? abuf + tb * copy16 + ta * row16 : abuf + ta * row16 + tb * col16;
+                uint64_t bb = btap;
+                if (!BRES) {
+                  umma::mbar_wait_uni(&b_full[st], bph);
+                  umma::tc_fence_after();
+                  bb = b_desc0 + st * tap16;
+                }
+                const uint32_t acc0 = (c0 | ta | tb) != 0;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            umma::mma_bf16_warp(d_tmem, umma::sdesc_sw128((SW ? bb : aa) + 32 * q), umma::sdesc_sw128((SW ? aa : bb) + 32 * q),
-                           IDESC,
-                           (c0 | tap | q) != 0);
-          if (!a.bres) {
-            umma::mma_commit_warp(&b_empty[st]);
-            ++i;
+                for (int q = 0; q < 4; ++q)
+                  umma::mma_bf16(d_tmem, (SW ? bb : aa) + 2 * q, (SW ? aa : bb) + 2 * q, IDESC, acc0 | (q != 0));
+                if (!BRES) {
+                  umma::mma_commit(&b_empty[st]);
+                  if (++st == SB) { st = 0; bph ^= 1; }
+                }
+              }
+            }
+            umma::mma_commit(&a_empty[ab]);
+            adv_a();
           }
+          umma::mma_commit(&tfull_bar[acc]);
+          for (int c = 0; c < (nw - 1) * nch; ++c) adv_a();   // the other issuer's tile
         }
-        umma::mma_commit_warp(&a_empty[ab]);
-      }
-      umma::mma_commit_warp(&tfull_bar[acc]);
-    }
+      };
+      using T = std::true_type;
+      using F = std::false_type;
+      using W0 = std::integral_constant<int, 0>;
+      using W1 = std::integral_constant<int, 1>;
+      if (!a.bres) issue(W0{}, F{});
+      else if (wi == 0) issue(W0{}, T{});
+      else issue(W1{}, T{});
 #ifdef ORTH_CONV_TRACE
-    if (lane == 0 && blockIdx.x < 160) {
-      pad_mma_trace[blockIdx.x * 4 + 2] += clock64() - t_all0;
-      pad_mma_trace[blockIdx.x * 4 + 3] += tcount;
-    }
+      if (blockIdx.x < 160 && wi == 0) {
+        pad_mma_trace[blockIdx.x * 4 + 2] += clock64() - t_all0;
+        pad_mma_trace[blockIdx.x * 4 + 3] += (min(a.num_tiles, (int)blockIdx.x * a.tiles_per_cta + a.tiles_per_cta) - (int)blockIdx.x * a.tiles_per_cta + nw - 1) / nw;
+      }
 #endif
+    }
+    __syncwarp();
   } else if (SW && warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue (swapped)
     // Warp q reads TMEM lanes 32q .. 32q+15 (channels 16q .. 16q+15) as mma-style 8x8 fragments
@@ -944,11 +953,13 @@ int launch_conv_fwd_reuse(const LayerInfo& L, const void* kernel, const float* b
   auto* out = static_cast<__nv_bfloat16*>(y);
   cudaStream_t s = (cudaStream_t)stream;
   static const bool no_swap = std::getenv("ORTH_CONV_NO_SWAP") != nullptr;   // A/B switch
-  static const bool no_row = std::getenv("ORTH_CONV_NO_ROW") != nullptr;     // A/B switch
+  // kernel-row MMAs (co_g = 64, 2 <= k <= 4, one window layout): M = 128 pixels x N = k 64.  Opt-in since
+  // the issuers were made uniform: the swapped / one-chain-per-tap forms are then faster (64@56^2, batch
+  // 256: 76 / 72 us vs 90 us, the kernel-row epilogue's cross-lane sums being the limit)
+  static const bool use_row = std::getenv("ORTH_CONV_ROW") != nullptr;       // A/B switch
   int bn = 0;
   PadArgs a;
-  // kernel-row MMAs (co_g = 64, 2 <= k <= 4, one window layout): M = 128 pixels x N = k 64
-  if (!no_row && L.co == 64 && L.k >= 2 && L.k <= 4 && L.d * (L.k - 1) < 32 &&
+  if (use_row && L.co == 64 && L.k >= 2 && L.k <= 4 && L.d * (L.k - 1) < 32 &&
       pad_args(L, N, H, W, Ho, Wo, bn, a, false) && bn == 64 && a.ncopy == 1) {
     if (a.num_tiles == 0) return 0;
     a.flip = flip;

@@ -50,23 +50,6 @@ __device__ __forceinline__ void mbar_wait_uni(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// Whole-warp wait (all 32 lanes, converged): the retry condition is a warp vote, so the loop is
-// uniform and values carried across it stay in uniform registers.
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
-  while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
-  }
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

@@ -301,6 +301,27 @@ def test_conv_pair_path(cuda_lib, case):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+ROW_CASES = [(64, 64, 3, 1, 1, 1, "circular", 10, "conv"), (64, 64, 3, 1, 1, 1, "zeros", 9, "conv"),
+             (64, 64, 3, 1, 2, 1, "circular", 12, "conv"), (64, 64, 2, 1, 1, 1, "circular", 9, "conv"),
+             (192, 64, 3, 1, 1, 1, "circular", 11, "conv"), (64, 64, 3, 1, 1, 1, "circular", 24, "convT"),
+             (64, 64, 3, 1, 1, 1, "circular", 24, "conv")]
+
+
+@pytest.mark.parametrize("switch", ["ORTH_CONV_ROW", "ORTH_CONV_NO_SWAP"])
+def test_conv_64_channel_forms(switch):
+    """The 64-output-channel layers' alternative forms, in a subprocess (the switches are read once): the
+    opt-in kernel-row MMAs (ORTH_CONV_ROW=1) and the one-chain-per-tap form with M = 128 pixels
+    (ORTH_CONV_NO_SWAP=1, two MMA issuers on a resident weight set); forward and adjoint, BF16."""
+    import os
+    import subprocess
+    import sys
+    code = (f"import sys; sys.path.insert(0, {os.getcwd()!r}); import tests.test_gpu_parity as t; "
+            f"import paper_2601_13776_b200 as orth\n"
+            f"for c in {ROW_CASES!r}: t.test_conv_forward_and_transpose(orth, c, 'bf16')")
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, switch: "1"}, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 STACK_CASES = [(128, 256, 3, 1, 2, 1, "circular", 12, "conv"), (256, 128, 5, 1, 1, 1, "zeros", 9, "conv"),
                (128, 128, 3, 1, 1, 1, "circular", 7, "conv"), (256, 256, 3, 1, 1, 2, "circular", 8, "conv"),
                (128, 128, 3, 1, 1, 1, "zeros", 30, "conv"), (512, 512, 3, 1, 1, 1, "circular", 5, "convT"),

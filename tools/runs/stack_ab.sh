@@ -1,10 +1,10 @@
-for v in 0 1; do
-  if [ $v = 1 ]; then export ORTH_CONV_STACK=1; fi
-  timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/stack_ab_$v.json 2>/dev/null
+# conv_stack (stacked TMA windows) vs conv_ws (gathered rows) for the layers stack_rule picks, after the issuer rewrite
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+for L in "128 128 3 1 1 1 circular 28 256" "128 128 3 1 1 1 zeros 28 256" "64 128 3 2 1 1 circular 56 256" "128 128 3 1 1 1 circular 16 256"; do
+  for adj in "" "--adjoint"; do
+    s=$(timeout 120 python tools/conv_one.py $L $adj | awk '{print $(NF-1)}')
+    w=$(ORTH_CONV_NO_STACK=1 timeout 120 python tools/conv_one.py $L $adj | awk '{print $(NF-1)}')
+    echo "$L $adj: stack $s ws $w"
+  done
 done
-python - <<'P'
-import json
-for v in (0,1):
-    d=json.loads(open('gpurun_out/stack_ab_%d.json'%v).read().strip().splitlines()[-1])
-    print(v, round(d['value']), round(d['ms_per_step'],3), [round(x*1000) for x in d['breakdown']['conv_per_layer_ms']])
-P
+echo "== bench NO_STACK"; ORTH_CONV_NO_STACK=1 timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'])"

@@ -7,7 +7,7 @@ import sys
 recs = json.load(open(sys.argv[1]))
 cfg = sys.argv[2]
 note = sys.argv[3] if len(sys.argv) > 3 else ""
-GROUPS = {"conv_ws<256": "conv_ws<256>", "conv_ws<128": "conv_ws<128>", "conv_pad<64, true": "conv_pad<64,swapped>",
+GROUPS = {"conv_ws<256": "conv_ws<256>", "conv_ws<128": "conv_ws<128>", "conv_pad<64, true": "conv_pad<64,swapped>", "conv_pad<64, 1, 0>": "conv_pad<64,swapped>",
           "conv_pad<64, 0, 1>": "conv_pad<64,row>", "conv_pad<64, false, true>": "conv_pad<64,row>", "tcg_flow": "compose",
           "conv_stack": "conv_stack (+pad_kernel)", "conv_stem": "conv_stem_tc", "ns_flow": "ns", "ns_persist": "ns",
           "power_fused": "power", "emit_kernel": "emit", "scale_bf16": "scale", "tcg_tma": "compose"}

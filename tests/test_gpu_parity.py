@@ -307,11 +307,12 @@ ROW_CASES = [(64, 64, 3, 1, 1, 1, "circular", 10, "conv"), (64, 64, 3, 1, 1, 1, 
              (64, 64, 3, 1, 1, 1, "circular", 24, "conv")]
 
 
-@pytest.mark.parametrize("switch", ["ORTH_CONV_ROW", "ORTH_CONV_NO_SWAP"])
+@pytest.mark.parametrize("switch", ["ORTH_CONV_ROW", "ORTH_CONV_NO_SWAP", "ORTH_CONV_NO_BRES"])
 def test_conv_64_channel_forms(switch):
     """The 64-output-channel layers' alternative forms, in a subprocess (the switches are read once): the
-    opt-in kernel-row MMAs (ORTH_CONV_ROW=1) and the one-chain-per-tap form with M = 128 pixels
-    (ORTH_CONV_NO_SWAP=1, two MMA issuers on a resident weight set); forward and adjoint, BF16."""
+    opt-in kernel-row MMAs (ORTH_CONV_ROW=1), the one-chain-per-tap form with M = 128 pixels
+    (ORTH_CONV_NO_SWAP=1, two MMA issuers on a resident weight set) and the default swapped form with
+    streamed instead of resident weights (ORTH_CONV_NO_BRES=1, one issuer); forward and adjoint, BF16."""
     import os
     import subprocess
     import sys

@@ -103,14 +103,20 @@ __global__ void __launch_bounds__(384, 1) k(const __grid_constant__ Args a, unsi
         const int acc = tcount & 1;
         unsigned long long w0 = clock64();
         const bool skip = (V & 128) && ready_next;
-        if (!NOWAIT && !skip) umma::mbar_wait_uni(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
+        if (!NOWAIT && !skip) {
+          if (V & 1024) { if (!test_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1)) umma::mbar_wait_uni(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1); }
+          else umma::mbar_wait_uni(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
+        }
         wt_t += clock64() - w0;
         if (!(V & 8)) umma::tc_fence_after();
         const uint32_t d_tmem = tmem + acc * ACC_COLS;
         uint64_t bset = b_desc0;
         for (int c0 = 0; c0 < a.cr_g; c0 += 64, bset += b_set16) {
           w0 = clock64();
-          if (!NOWAIT && !(skip && c0 == 0)) umma::mbar_wait_uni(&a_full[ab], aph);
+          if (!NOWAIT && !(skip && c0 == 0)) {
+            if (V & 1024) { if (!test_wait(&a_full[ab], aph)) umma::mbar_wait_uni(&a_full[ab], aph); }
+            else umma::mbar_wait_uni(&a_full[ab], aph);
+          }
           wt_a += clock64() - w0;
           umma::tc_fence_after();
           uint64_t ad = a_desc0 + ab * a_buf16;
@@ -186,9 +192,9 @@ int main() {
     printf("%-48s %.0f cycles/tile (floor 1160), waits: tempty %.0f, a_full %.0f (%s)\n", name, s, s1, s2, cudaGetErrorString(e));
   };
   run(k<4 | 2>, "waits, k=3, one issuer");
-  run(k<4 | 2 | 512>, "waits, k=3, two issuers alternating tiles");
-  run(k<4 | 512>, "waits, runtime k, two issuers");
-  run(k<0 | 512>, "the conv_pad loop, two issuers");
-  run(k<0>, "the conv_pad loop, one issuer");
+  run(k<4 | 2 | 1024>, "waits, k=3, one issuer, test_wait first");
+  run(k<4 | 2 | 512>, "waits, k=3, two issuers");
+  run(k<4 | 2 | 512 | 1024>, "waits, k=3, two issuers, test_wait first");
+  run(k<1 | 2 | 4>, "no waits, k=3");
   return 0;
 }

@@ -854,6 +854,8 @@ int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, cons
   // 128x256 tile does twice the work of a 128x128 one per MMA: narrower only pays when it fills
   // otherwise idle SMs -- or, with a partial workspace, split K in two instead, ORTH_CONV_NO_SPLITK=1 off)
   int bn = n % 256 == 0 ? 256 : n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32;
+  static const int bn_cap = std::getenv("ORTH_CONV_WS_BN") ? std::atoi(std::getenv("ORTH_CONV_WS_BN")) : 256;   // A/B switch
+  while (bn > bn_cap && bn > 32) bn /= 2;
   static const bool no_split = std::getenv("ORTH_CONV_NO_SPLITK") != nullptr;
   a.ksplit = 1;
   const int64_t tiles256 = (int64_t)a.tiles_m * (n / 256) * groups;

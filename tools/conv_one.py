@@ -32,4 +32,10 @@ for _ in range(20):
 e1.record()
 torch.cuda.synchronize()
 plan.check()
-print(f"{' '.join(args)} {'adj' if adj else 'fwd'}: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us")
+plan.trace(True)   # one traced call: which kernel variant ran
+f()
+torch.cuda.synchronize()
+recs = plan.trace_read()
+plan.trace(False)
+variant = recs[-1]["variant"] if recs else "?"
+print(f"{' '.join(args)} {'adj' if adj else 'fwd'}: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us  [{variant}]")

@@ -24,15 +24,15 @@ __device__ __forceinline__ void gather4(uint32_t dst, const CUtensorMap* map, ui
 }
 
 constexpr int NSLOT = 4;
-template <bool SPREAD>
-__global__ void __launch_bounds__(288, 1) k(const __grid_constant__ CUtensorMap tm, const int* __restrict__ rows,
+template <int MODE>   // 0: one thread issues gather4; 1: 8 warps issue gather4; 2: cp.async by 256 threads
+__global__ void __launch_bounds__(288, 1) k(const __grid_constant__ CUtensorMap tm, const __nv_bfloat16* __restrict__ gsrc, const int* __restrict__ rows,
                                              int nst, int nrows_tab, uint8_t* dump, unsigned long long* out) {
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = umma::align1024_smem(sm_raw);
   __shared__ uint64_t full[NSLOT], empty[NSLOT];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int i = 0; i < NSLOT; ++i) { umma::mbar_init(&full[i], 1); umma::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < NSLOT; ++i) { umma::mbar_init(&full[i], MODE == 2 ? 256 : 1); umma::mbar_init(&empty[i], 1); }
     umma::fence_mbar_init();
   }
   __syncthreads();
@@ -44,7 +44,15 @@ __global__ void __launch_bounds__(288, 1) k(const __grid_constant__ CUtensorMap 
       if (s >= NSLOT) umma::mbar_wait(&empty[slot], ((s / NSLOT) - 1) & 1);
       const uint32_t dst = base + slot * 16384;
       const int* rr = rows + ((size_t)(blockIdx.x * 131 + s) * 128) % (size_t)(nrows_tab - 128);
-      if (SPREAD) {   // warp w issues gathers 4w .. 4w + 3 (lanes 0..3)
+      if (MODE == 2) {   // conv_ws-style: thread = (row group, 16-byte chunk), 4 rows each
+        const int c = tid & 7, rb = tid >> 3;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = rb + 32 * i, idx = rr[r];
+          umma::cp_async16(dst + r * 128 + ((c ^ (r & 7)) << 4), gsrc + (size_t)(idx < 0 ? 0 : idx) * 64 + c * 8, idx >= 0);
+        }
+        umma::cp_async_mbar_arrive(&full[slot]);
+      } else if (MODE == 1) {   // warp w issues gathers 4w .. 4w + 3 (lanes 0..3)
         if (tid == 0) umma::mbar_arrive_expect_tx(&full[slot], 16384);
         __syncwarp();
         asm volatile("bar.sync 1, 256;");
@@ -101,7 +109,7 @@ int main() {
   cudaMalloc(&out, 8 * 148);
   auto run = [&](auto kern, const char* name, int nst) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, NSLOT * 16384 + 1024);
-    kern<<<148, 288, NSLOT * 16384 + 1024>>>(tm, drows, nst, NT, dump, out);
+    kern<<<148, 288, NSLOT * 16384 + 1024>>>(tm, (const __nv_bfloat16*)d, drows, nst, NT, dump, out);
     cudaError_t e = cudaDeviceSynchronize();
     unsigned long long ho[148];
     cudaMemcpy(ho, out, sizeof(ho), cudaMemcpyDeviceToHost);
@@ -111,7 +119,7 @@ int main() {
            cudaGetErrorString(e));
     return e;
   };
-  if (run(k<false>, "one thread issues", 1) != cudaSuccess) return 1;
+  if (run(k<0>, "gather4, one thread", 1) != cudaSuccess) return 1;
   // check stage 0 of CTA 0
   std::vector<uint8_t> hd(16384);
   cudaMemcpy(hd.data(), dump, 16384, cudaMemcpyDeviceToHost);
@@ -128,7 +136,15 @@ int main() {
       }
     }
   printf("layout check: %d bad bytes of 16384 (%s)\n", bad, bad ? "FAIL" : "ok");
-  run(k<false>, "one thread issues", 4000);
-  run(k<true>, "8 warps issue", 4000);
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {   // conv-like: consecutive pixels (rows of neighbouring outputs), 1/37 padding rows
+      for (int i = 0; i < NT; ++i) rows[i] = (i % 37 == 5) ? -1 : (i % (R / 16));
+      cudaMemcpy(drows, rows.data(), NT * 4, cudaMemcpyHostToDevice);
+    }
+    printf("== %s rows\n", pass ? "consecutive" : "random");
+    run(k<0>, "gather4, one thread", 4000);
+    run(k<1>, "gather4, 8 warps", 4000);
+    run(k<2>, "cp.async, 256 threads", 4000);
+  }
   return bad ? 1 : 0;
 }

@@ -54,6 +54,10 @@ struct TcConvArgs {
   int nphase;             // 1 (forward) or s*s (transposed)
   int phase_tile0[MAX_PHASES + 1];   // first tile (over m) of each phase, prefix sums
   int phase_hp[MAX_PHASES], phase_wp[MAX_PHASES], phase_cnt[MAX_PHASES];
+  // per phase: contributing taps (count, and as a bit mask when k^2 <= 32), filled by launch_any so that
+  // neither the MMA issuer nor the producers evaluate tap_valid's modulo arithmetic per tile
+  int phase_nt[MAX_PHASES];
+  uint32_t phase_taps[MAX_PHASES];
   int tiles_m;            // = phase_tile0[nphase]
   // thread-block clusters of cs CTAs along M share every B tile (TMA multicast of
   // a BN/cs-row slice per CTA); a cluster tile = cs consecutive M tiles of one phase
@@ -103,11 +107,15 @@ __device__ __forceinline__ TileInfo decode_tile(const TcConvArgs& a, int ct, int
 }
 
 // taps contributing to a phase (all taps for the forward); returns the count
-__device__ __forceinline__ bool tap_valid(const TcConvArgs& a, int phase, int tap) {
+__host__ __device__ __forceinline__ bool tap_valid_calc(const TcConvArgs& a, int phase, int tap) {
   if (!a.transposed) return true;
   const int ph = phase / a.s, pw = phase % a.s;
   const int ta = tap / a.k, tb = tap % a.k;
   return ((ph + a.pt - a.d * ta) % a.s + a.s) % a.s == 0 && ((pw + a.pl - a.d * tb) % a.s + a.s) % a.s == 0;
+}
+__device__ __forceinline__ bool tap_valid(const TcConvArgs& a, int phase, int tap) {
+  if (a.k * a.k <= 32) return (a.phase_taps[phase] >> tap) & 1u;
+  return tap_valid_calc(a, phase, tap);
 }
 
 // output pixel index (n*Hout + h)*Wout + w of row m of a phase
@@ -311,9 +319,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #endif
       for (int ct = ucid; ct < a.num_ctiles; ct += uncl, ++tcount) {
         const TileInfo t = decode_tile(a, ct % a.base_ctiles, ucr, BN);
-        int nt = 0;
-        for (int tap = 0; tap < a.k * a.k; ++tap) nt += tap_valid(a, t.phase, tap) ? 1 : 0;
-        const int nk = nt * (((a.cr_g + 63) / 64) / a.ksplit);
+        const int nk = a.phase_nt[t.phase] * (((a.cr_g + 63) / 64) / a.ksplit);
         const int acc = tcount & 1;
 #ifdef ORTH_CONV_TRACE
         long long tq = clock64();
@@ -617,8 +623,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       int it = 0, tcount = 0;
       for (int ct = cid; ct < a.num_ctiles; ct += ncl, ++tcount) {
         const TileInfo t = decode_tile(a, ct, crank, BN);
-        int nt = 0;
-        for (int tap = 0; tap < kk2; ++tap) nt += tap_valid(a, t.phase, tap) ? 1 : 0;
+        const int nt = a.phase_nt[t.phase];
         const int nk = nt * kc;
         if (leader) {
           // ---------------------------------------------------- MMA issuer (leader)
@@ -850,6 +855,15 @@ static bool splitk_pays(int64_t t) {
 int launch_any(const __nv_bfloat16* in, const __nv_bfloat16* w, int w_rows, const float* bias, __nv_bfloat16* out,
                TcConvArgs& a, int groups, cudaStream_t s) {
   const int n = a.nout_g;
+  for (int p = 0; p < a.nphase && p < MAX_PHASES; ++p) {   // contributing taps per phase (tap_valid)
+    a.phase_nt[p] = 0;
+    a.phase_taps[p] = 0;
+    for (int tap = 0; tap < a.k * a.k; ++tap)
+      if (tap_valid_calc(a, p, tap)) {
+        ++a.phase_nt[p];
+        if (tap < 32) a.phase_taps[p] |= 1u << tap;
+      }
+  }
   // widest N tile that still gives ~every SM a tile (every K=16 MMA shape costs ~125-150 cycles, so a
   // 128x256 tile does twice the work of a 128x128 one per MMA: narrower only pays when it fills
   // otherwise idle SMs -- or, with a partial workspace, split K in two instead, ORTH_CONV_NO_SPLITK=1 off)

@@ -192,7 +192,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   umma::griddep_wait();   // PDL: the previous kernel's outputs (x, weights) are complete
   const uint32_t tmem = tmem_base_sh;
   const uint32_t s0 = umma::smem_u32(smem);
-  const int kc = (a.cr_g + 63) / 64;
   const int kk2 = a.k * a.k;
 
   if (warp < MMA_WARP) {
@@ -317,9 +316,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const long long t_all = clock64();
       long long w_full = 0, w_te = 0;
 #endif
+      // the issuer needs only each tile's phase: its M-tile index tm = ct mod ctiles_m (base_ctiles is a
+      // multiple of ctiles_m) is stepped, not divided, per tile
+      const int kcs = ((a.cr_g + 63) / 64) / a.ksplit;
+      int tm = ucid % a.ctiles_m;
+      const int tm_step = uncl % a.ctiles_m;
       for (int ct = ucid; ct < a.num_ctiles; ct += uncl, ++tcount) {
-        const TileInfo t = decode_tile(a, ct % a.base_ctiles, ucr, BN);
-        const int nk = a.phase_nt[t.phase] * (((a.cr_g + 63) / 64) / a.ksplit);
+        int phase = 0;
+        while (phase + 1 < a.nphase && a.phase_ctile0[phase + 1] <= tm) ++phase;
+        const int nk = a.phase_nt[phase] * kcs;
+        tm += tm_step;
+        if (tm >= a.ctiles_m) tm -= a.ctiles_m;
         const int acc = tcount & 1;
 #ifdef ORTH_CONV_TRACE
         long long tq = clock64();

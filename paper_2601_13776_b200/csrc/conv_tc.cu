@@ -249,9 +249,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           } else {
             int th = hb - a.d * ta, tw = wb - a.d * tb;
             bool ok = true;
-            if (a.circ) { th = wrapi(th, a.H); tw = wrapi(tw, a.W); }
-            else ok = th >= 0 && tw >= 0;
-            const int u = th / a.s, vv = tw / a.s;   // exact: the phase makes th, tw multiples of s
+            if (a.circ) {
+              if (wrap_fast) {   // one add / subtract brings th, tw into range (as for the forward)
+                th += th < 0 ? a.H : (th >= a.H ? -a.H : 0);
+                tw += tw < 0 ? a.W : (tw >= a.W ? -a.W : 0);
+              } else {
+                th = wrapi(th, a.H); tw = wrapi(tw, a.W);
+              }
+            } else {
+              ok = th >= 0 && tw >= 0;
+            }
+            // exact: the phase makes th, tw multiples of s (s = 2: a shift; th, tw >= 0 whenever used)
+            const int u = a.s == 2 ? th >> 1 : th / a.s, vv = a.s == 2 ? tw >> 1 : tw / a.s;
             if (ok && u < a.Ho && vv < a.Wo) v = (nb * a.Ho + u) * a.Wo + vv;
           }
         }

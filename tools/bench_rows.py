@@ -61,7 +61,7 @@ def row_f1():
     plan, p, ortho, kf, kb = construct(layers, vjp=1, max_batch=N)
     H = 224
     out = []
-    total_fl, total_ms = 0.0, 0.0
+    total_fl, total_ms, dgrad_ms = 0.0, 0.0, 0.0
     per = []
     for l, d in enumerate(layers):
         Ho, _ = plan.out_hw(l, H, H)
@@ -72,11 +72,15 @@ def row_f1():
         ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
         ms = timed(lambda: plan.conv_wgrad(l, x, dy, dK, workspace=ws))
         fl = 2.0 * N * Ho * Ho * d["c_out"] * d["c_in"] * d["k"] ** 2 / d["g"]
-        per.append(dict(layer=l, ms=ms, tflops=fl / ms / 1e9))
+        kv = plan.kernel_bf16(kb, l)
+        dx = torch.empty_like(x)
+        ms_d = timed(lambda: plan.conv_transpose(l, kv, dy, dx))   # dgrad: the exact adjoint (a7)
+        per.append(dict(layer=l, ms=ms, tflops=fl / ms / 1e9, dgrad_ms=ms_d, dgrad_tflops=fl / ms_d / 1e9))
         total_fl += fl
         total_ms += ms
+        dgrad_ms += ms_d
         H = Ho
-        del x, dy
+        del x, dy, dx
     dKall = torch.randn(plan.kf32_numel, device="cuda")
     dortho = torch.zeros_like(p)
     dparams = torch.zeros_like(p)
@@ -86,6 +90,7 @@ def row_f1():
     ach = total_fl / total_ms / 1e9
     out.append(dict(row="f1 backward", workload="config 3, batch 256, BF16", wgrad_ms_total=total_ms,
                     wgrad_tflops=ach, wgrad_frac_of_burst=ach / PEAKS["bf16_tflops"], wgrad_per_layer=per,
+                    dgrad_ms_total=dgrad_ms, dgrad_tflops=total_fl / dgrad_ms / 1e9,
                     compose_vjp_ms=ms_c, orthogonalize_vjp_ms=ms_o,
                     note="VJP phases are the generic 3-pass tcgen05 GEMM (FP32-accurate), not the tuned forward kernels"))
     return out

@@ -331,36 +331,45 @@ int launch_conv_fwd(const LayerInfo& L, const void* kernel, void* scratch, const
 // Adjoint of a patch conv (k = s, d = 1, H = s Ho, W = s Wo, circular or unpadded: the RKO stem): every x
 // pixel (s i - p_t + a, s j - p_l + b) (mod H, W) receives exactly tap (a, b) of y[i, j] -- x[n, ., ., c] =
 // sum_o K[o, c, a, b] y[n, i, j, o] (+ bias[c]).  One warp per (y pixel, group): y's co_g channels staged in
-// shared memory, lanes over the k^2 ci_g outputs of the patch.  (The general SIMT adjoint tiles 64 output
+// shared memory with the group's weights, lanes over the k^2 ci_g outputs of the patch.  (The general SIMT adjoint tiles 64 output
 // channels and visits all k^2 taps per pixel: for the 3-channel stem that was 111 ms at batch 256.)
 template <typename T, typename Wt>
 __global__ void __launch_bounds__(256) conv_bwd_patch(const T* __restrict__ yv, const Wt* __restrict__ wt,
                                                       const float* __restrict__ bias, T* __restrict__ x, ConvArgs a) {
-  extern __shared__ float ys[];   // [8 warps][co_g]
+  // shared: the group's weights as [o][tap ci_g + ic] FP32, then [8 warps][co_g] staged y channels;
+  // a block covers 8 x PPW y pixels (each warp PPW of them), so the weights are read once per 64 pixels
+  extern __shared__ float sm[];
+  constexpr int PPW = 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = blockIdx.y;
-  const int64_t M = (int64_t)a.N * a.Ho * a.Wo;
-  const int64_t m = (int64_t)blockIdx.x * 8 + warp;
-  if (m >= M) return;
-  float* yw = ys + warp * a.co_g;
-  for (int o = lane; o < a.co_g; o += 32) yw[o] = ld(yv + m * a.Co + (int64_t)g * a.co_g + o);
-  __syncwarp();
-  const int n = (int)(m / ((int64_t)a.Ho * a.Wo)), r = (int)(m - (int64_t)n * a.Ho * a.Wo);
-  const int i = r / a.Wo, j = r - i * a.Wo;
   const int kk2 = a.k * a.k, nout = kk2 * a.ci_g;
-  for (int e = lane; e < nout; e += 32) {
-    const int tap = e / a.ci_g, ic = e - tap * a.ci_g;
-    const int ta = tap / a.k, tb = tap - ta * a.k;
-    float acc = 0.f;
-    for (int o = 0; o < a.co_g; ++o) {
-      const int64_t oo = (int64_t)g * a.co_g + o;
-      const float wv = sizeof(Wt) == 2 ? ld(wt + (oo * kk2 + tap) * a.ci_g + ic) : ld(wt + (oo * a.ci_g + ic) * kk2 + tap);
-      acc = fmaf(yw[o], wv, acc);
+  float* ws = sm;
+  float* yw = sm + (size_t)a.co_g * nout + warp * a.co_g;
+  for (int idx = threadIdx.x; idx < a.co_g * nout; idx += blockDim.x) {
+    const int o = idx / nout, e = idx - o * nout, tap = e / a.ci_g, ic = e - tap * a.ci_g;
+    const int64_t oo = (int64_t)g * a.co_g + o;
+    ws[idx] = sizeof(Wt) == 2 ? ld(wt + (oo * kk2 + tap) * a.ci_g + ic) : ld(wt + (oo * a.ci_g + ic) * kk2 + tap);
+  }
+  __syncthreads();
+  const int64_t M = (int64_t)a.N * a.Ho * a.Wo;
+  for (int p = 0; p < PPW; ++p) {
+    const int64_t m = ((int64_t)blockIdx.x * 8 + warp) * PPW + p;
+    if (m >= M) break;
+    __syncwarp();
+    for (int o = lane; o < a.co_g; o += 32) yw[o] = ld(yv + m * a.Co + (int64_t)g * a.co_g + o);
+    __syncwarp();
+    const int n = (int)(m / ((int64_t)a.Ho * a.Wo)), r = (int)(m - (int64_t)n * a.Ho * a.Wo);
+    const int i = r / a.Wo, j = r - i * a.Wo;
+    for (int e = lane; e < nout; e += 32) {
+      const int tap = e / a.ci_g, ic = e - tap * a.ci_g;
+      const int ta = tap / a.k, tb = tap - ta * a.k;
+      float acc = 0.f;
+      for (int o = 0; o < a.co_g; ++o) acc = fmaf(yw[o], ws[o * nout + e], acc);
+      const int c = g * a.ci_g + ic;
+      if (bias) acc += bias[c];
+      int h = a.s * i - a.pt + ta, w = a.s * j - a.pl + tb;   // circular: (i, a) -> h is a bijection
+      if (a.circ) { h = wrap(h, a.H); w = wrap(w, a.W); }
+      st(x + (((int64_t)n * a.H + h) * a.W + w) * a.Ci + c, acc);
     }
-    const int c = g * a.ci_g + ic;
-    if (bias) acc += bias[c];
-    int h = a.s * i - a.pt + ta, w = a.s * j - a.pl + tb;   // circular: (i, a) -> h is a bijection
-    if (a.circ) { h = wrap(h, a.H); w = wrap(w, a.W); }
-    st(x + (((int64_t)n * a.H + h) * a.W + w) * a.Ci + c, acc);
   }
 }
 
@@ -370,13 +379,14 @@ int launch_conv_bwd(const LayerInfo& L, const void* kernel, void* wt_scratch, co
     return launch_conv_bwd_tc(L, kernel, wt_scratch, bias, y, x, N, H, W, Ho, Wo, stream);
   const ConvArgs a = make_args(L, N, H, W, Ho, Wo);
   cudaStream_t s = (cudaStream_t)stream;
-  if (L.k == L.s && L.d == 1 && (a.circ || (a.pt == 0 && a.pl == 0)) && H == L.s * Ho && W == L.s * Wo && L.co <= 1024 &&
-      !getenv("ORTH_CONV_NO_PATCH_BWD")) {
+  const size_t patch_sm = ((size_t)L.co * L.k * L.k * L.ci + 8 * (size_t)L.co) * sizeof(float);
+  if (L.k == L.s && L.d == 1 && (a.circ || (a.pt == 0 && a.pl == 0)) && H == L.s * Ho && W == L.s * Wo &&
+      patch_sm <= 48 * 1024 && !getenv("ORTH_CONV_NO_PATCH_BWD")) {
     g_conv_variant = ORTH_CV_SIMT;
     const int64_t My = (int64_t)N * Ho * Wo;
     if (My == 0) return 0;
-    dim3 pg((unsigned)((My + 7) / 8), (unsigned)L.g);
-    const size_t sm = (size_t)8 * L.co * sizeof(float);
+    dim3 pg((unsigned)((My + 63) / 64), (unsigned)L.g);
+    const size_t sm = patch_sm;
     if (io == ORTH_BF16)
       conv_bwd_patch<__nv_bfloat16, __nv_bfloat16><<<pg, 256, sm, s>>>(
           (const __nv_bfloat16*)y, (const __nv_bfloat16*)kernel, bias, (__nv_bfloat16*)x, a);
